@@ -1,0 +1,368 @@
+"""Pins of the float64 oracle against things other than itself.
+
+Each test names what fixes the expected value: a hand-worked example, a closed form,
+an invariant implied by the paper's construction, finite differences, brute force,
+or an independent second differentiation (torch autograd).  CPU only.
+"""
+import json
+import struct
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+GOLD = Path(__file__).resolve().parent / "golden"
+DELTA = 0.10
+
+
+def _write(tmp_path, name, act, dims, layers):
+    p = tmp_path / name
+    synth.write_mlpw(p, act, dims, layers)
+    return p
+
+
+def _rand_inputs(rng, M, W, dyadic=False):
+    pts = np.stack([rng.uniform(-7, 7, M), rng.uniform(-7, 7, M), rng.uniform(0, 2, M)], 1)
+    q = np.concatenate([rng.uniform(-5, 5, (W, 2)), rng.uniform(-np.pi, np.pi, (W, 7))], 1)
+    if dyadic:
+        pts = np.round(pts * 1024) / 1024
+        q = np.round(q * 1024) / 1024
+    return pts, q
+
+
+@pytest.fixture(scope="module")
+def mlp32(tmp_path_factory):
+    act, dims, layers = synth.make_weights(32, seed=11)
+    p = tmp_path_factory.mktemp("w") / "h32.mlpw"
+    synth.write_mlpw(p, act, dims, layers)
+    return oracle.MLP(p), (act, dims, layers)
+
+
+# ------------------------------------------------------------------ O1: weights file
+def test_mlpw_errors(tmp_path):
+    act, dims, layers = synth.make_weights(32, seed=1)
+    good = _write(tmp_path, "g.mlpw", act, dims, layers)
+    m = oracle.MLP(good)
+    assert m.dims == [12] + [32] * 6 + [1] and m.L == 7 and m.act == 1
+    raw = good.read_bytes()
+    cases = {
+        "bad_magic": (b"MLPX" + raw[4:], "BAD_MAGIC"),
+        "version": (raw[:4] + struct.pack("<I", 2) + raw[8:], "VERSION"),
+        "truncated": (raw[:-8], "IO"),
+        "trailing": (raw + b"\0" * 8, "DIM_MISMATCH"),
+    }
+    for name, (blob, err) in cases.items():
+        p = tmp_path / (name + ".mlpw")
+        p.write_bytes(blob)
+        with pytest.raises(oracle.OracleError) as ei:
+            oracle.MLP(p)
+        assert ei.value.name == err, name
+    # input width must be 3 + n = 12
+    bad_dims = [13] + [32] * 6 + [1]
+    rng = np.random.default_rng(0)
+    bl = [(rng.normal(size=(bad_dims[i + 1], bad_dims[i])), np.zeros(bad_dims[i + 1])) for i in range(7)]
+    with pytest.raises(oracle.OracleError) as ei:
+        oracle.MLP(_write(tmp_path, "d.mlpw", 1, bad_dims, bl))
+    assert ei.value.name == "DIM_MISMATCH"
+
+
+# ------------------------------------------------------------------ hand-worked golden example
+def test_hand_worked_example(tmp_path):
+    g = json.loads((GOLD / "hand_example.json").read_text())
+    for ni, net in enumerate(g["networks"]):
+        layers = [(np.array(l["W"], float), np.array(l["b"], float)) for l in net["layers"]]
+        dims = [12] + [1] * 6 + [1]
+        m = oracle.MLP(_write(tmp_path, "hand%d.mlpw" % ni, 1, dims, layers))
+        for case in net["cases"]:
+            out = m.eval(np.array([case["p"]]), np.array([case["q"]]))
+            assert abs(out["f"][0, 0] - case["f"]) <= 1e-12
+            np.testing.assert_allclose(out["g"][0, 0], case["grad"], rtol=0, atol=1e-12)
+
+
+# ------------------------------------------------------------------ closed forms
+def test_identity_activation_closed_form(tmp_path):
+    """Identity activation: f = (W7...W1) x_in + b_eff; grad = mapped rows of the product."""
+    rng = np.random.default_rng(5)
+    dims = [12, 9, 7, 8, 6, 5, 4, 1]
+    layers = [(rng.normal(size=(dims[i + 1], dims[i])), rng.normal(size=dims[i + 1])) for i in range(7)]
+    m = oracle.MLP(_write(tmp_path, "id.mlpw", 0, dims, layers))
+    A = np.eye(12)
+    c = np.zeros(12)
+    for W, b in layers:  # affine composition x -> W (A x + c) + b
+        A, c = W @ A, W @ c + b
+    pts, q = _rand_inputs(rng, 13, 5)
+    out = m.eval(pts, q)
+    out_qc = m.eval(pts, q, flags=oracle.TGRAD_QCHANNEL)
+    for w in range(q.shape[0]):
+        for j in range(pts.shape[0]):
+            x = np.concatenate([[pts[j, 0] - q[w, 0], pts[j, 1] - q[w, 1], pts[j, 2], 0, 0], q[w, 2:]])
+            f = (A @ x + c)[0]
+            assert abs(out["f"][w, j] - f) <= 1e-10 * max(1, abs(f))
+            row = A[0]
+            want = np.concatenate([[-row[0], -row[1]], row[5:]])
+            np.testing.assert_allclose(out["g"][w, j], want, rtol=1e-11, atol=1e-11)
+            want_qc = np.concatenate([[row[3], row[4]], row[5:]])
+            np.testing.assert_allclose(out_qc["g"][w, j], want_qc, rtol=1e-11, atol=1e-11)
+
+
+def test_zero_head_constant(tmp_path):
+    """Zero output layer -> f == b7 and grad == 0 for every input."""
+    act, dims, layers = synth.make_weights(32, seed=2)
+    layers[-1] = (np.zeros_like(layers[-1][0]), np.array([0.731]))
+    m = oracle.MLP(_write(tmp_path, "z.mlpw", act, dims, layers))
+    pts, q = _rand_inputs(np.random.default_rng(1), 20, 4)
+    out = m.eval(pts, q)
+    assert np.all(out["f"] == 0.731)
+    assert np.all(out["g"] == 0.0)
+
+
+# ------------------------------------------------------------------ second implementation
+def test_torch_autograd_float64(mlp32):
+    """Independent differentiation: torch float64 autograd of the same network."""
+    torch = pytest.importorskip("torch")
+    m, (act, dims, layers) = mlp32
+    rng = np.random.default_rng(9)
+    pts, q = _rand_inputs(rng, 64, 6)
+    out = m.eval(pts, q, want_kappa=True)
+    Ws = [(torch.tensor(W), torch.tensor(b)) for W, b in layers]
+    P = torch.tensor(pts)
+    for w in range(q.shape[0]):
+        qt = torch.tensor(q[w]).repeat(P.shape[0], 1).requires_grad_(True)
+        pq = torch.cat([P[:, :2] - qt[:, :2], P[:, 2:3], torch.zeros(P.shape[0], 2, dtype=torch.float64),
+                        qt[:, 2:]], 1)
+        h = pq
+        for li, (W, b) in enumerate(Ws):
+            h = h @ W.T + b
+            if li < len(Ws) - 1:
+                h = torch.relu(h)
+        f = h[:, 0]
+        (gq,) = torch.autograd.grad(f.sum(), qt)
+        np.testing.assert_allclose(out["f"][w], f.detach().numpy(), rtol=1e-12, atol=1e-12)
+        ok = out["kappa"][w] > 1e-9
+        np.testing.assert_allclose(out["g"][w][ok], gq.numpy()[ok], rtol=1e-10, atol=1e-12)
+
+
+# ------------------------------------------------------------------ finite differences
+def test_central_fd_all_components(mlp32):
+    """P3: central FD of the oracle's own forward, all 9 q components, rel <= 1e-6."""
+    m, _ = mlp32
+    rng = np.random.default_rng(3)
+    pts, q = _rand_inputs(rng, 40, 5)
+    base = m.eval(pts, q, want_hash=True)
+    checked = skipped = 0
+    for k in range(9):
+        h = 1e-6 * np.maximum(1.0, np.abs(q[:, k]))
+        qp, qm = q.copy(), q.copy()
+        qp[:, k] += h
+        qm[:, k] -= h
+        op = m.eval(pts, qp, want_grad=False, want_hash=True)
+        om = m.eval(pts, qm, want_grad=False, want_hash=True)
+        fd = (op["f"] - om["f"]) / (2 * h[:, None])
+        same = (op["mask_hash"] == base["mask_hash"]) & (om["mask_hash"] == base["mask_hash"])
+        g = base["g"][:, :, k]
+        err = np.abs(fd - g) / np.maximum(1.0, np.abs(g))
+        assert np.all(err[same] <= 1e-6), (k, err[same].max())
+        checked += same.sum()
+        skipped += (~same).sum()
+    assert skipped <= 0.01 * (checked + skipped)
+
+
+def test_chain_rule_translation_equals_minus_point_gradient(mlp32):
+    """dF/dq_x = -dF/dp_x (FD on p)."""
+    m, _ = mlp32
+    rng = np.random.default_rng(4)
+    pts, q = _rand_inputs(rng, 30, 3)
+    base = m.eval(pts, q, want_hash=True)
+    for ax in (0, 1):
+        h = 1e-6 * np.maximum(1.0, np.abs(pts[:, ax]))
+        pp, pm = pts.copy(), pts.copy()
+        pp[:, ax] += h
+        pm[:, ax] -= h
+        op = m.eval(pp, q, want_grad=False, want_hash=True)
+        om = m.eval(pm, q, want_grad=False, want_hash=True)
+        fd_p = (op["f"] - om["f"]) / (2 * h[None, :])
+        same = (op["mask_hash"] == base["mask_hash"]) & (om["mask_hash"] == base["mask_hash"])
+        g = base["g"][:, :, ax]
+        assert np.all(np.abs(-fd_p - g)[same] <= 1e-6 * np.maximum(1, np.abs(g[same])))
+
+
+# ------------------------------------------------------------------ invariants
+def test_base_translation_invariance_bitexact(mlp32):
+    """P1: moving the base and the point rigidly together leaves value and gradient
+    unchanged (BASELINE north_star).  Dyadic inputs make the f64
+    subtraction exact, so the result is bit-identical."""
+    m, _ = mlp32
+    rng = np.random.default_rng(6)
+    pts, q = _rand_inputs(rng, 50, 4, dyadic=True)
+    a = m.eval(pts, q)
+    for t in ([3.5, -2.25], [-6.0009765625, 0.5]):
+        p2, q2 = pts.copy(), q.copy()
+        p2[:, :2] += t
+        q2[:, :2] += t
+        b = m.eval(p2, q2)
+        assert np.array_equal(a["f"], b["f"]) and np.array_equal(a["g"], b["g"])
+    # general inputs: <= 1e-12 relative
+    pts, q = _rand_inputs(rng, 50, 4)
+    a = m.eval(pts, q)
+    t = np.array([1.2345, -0.987])
+    p2, q2 = pts.copy(), q.copy()
+    p2[:, :2] += t
+    q2[:, :2] += t
+    b = m.eval(p2, q2, want_kappa=True)
+    np.testing.assert_allclose(a["f"], b["f"], rtol=1e-12, atol=1e-12)
+    ok = b["kappa"] > 1e-9
+    np.testing.assert_allclose(a["g"][ok], b["g"][ok], rtol=1e-9, atol=1e-12)
+
+
+def test_point_above_base_and_batch_consistency(mlp32):
+    """P1b: p_xy = q_xy gives the same value as the point at the origin with the base at
+    the origin.  P2(iv): a batch row equals the single-pair evaluation bit for bit."""
+    m, _ = mlp32
+    rng = np.random.default_rng(7)
+    pts, q = _rand_inputs(rng, 17, 3)
+    for w in range(3):
+        p = np.array([[q[w, 0], q[w, 1], 0.7]])
+        q0 = q[w].copy()
+        q0[:2] = 0.0
+        a = m.eval(p, q[w:w + 1])
+        b = m.eval(np.array([[0.0, 0.0, 0.7]]), q0[None])
+        assert a["f"][0, 0] == b["f"][0, 0]
+        np.testing.assert_array_equal(a["g"], b["g"])
+    full = m.eval(pts, q)
+    for w in range(3):
+        for j in (0, 5, 16):
+            one = m.eval(pts[j:j + 1], q[w:w + 1])
+            assert one["f"][0, 0] == full["f"][w, j]
+            np.testing.assert_array_equal(one["g"][0, 0], full["g"][w, j])
+    multi = m.eval(pts, q, nthreads=3)
+    np.testing.assert_array_equal(multi["f"], full["f"])
+    np.testing.assert_array_equal(multi["g"], full["g"])
+
+
+# ------------------------------------------------------------------ brute-force active set
+def test_detect_bruteforce_C1(tmp_path):
+    """P4: enumerate all pairs, filter, sort by (wp, pt), min per waypoint (smallest id on
+    ties), compare with the oracle's loop-order output exactly."""
+    cfg = synth.get_config("C1")
+    pts, _ = synth.make_scene_points(cfg)
+    q = synth.make_waypoints(cfg).reshape(-1, 9)
+    m = oracle.MLP(synth.weights_path(cfg.H))
+    # a scene with holes: ids are not 0..M-1
+    ids = np.arange(pts.shape[0], dtype=np.int64) * 3 + 1
+    # exact ties: duplicate each waypoint's nearest point under the next id, so the
+    # argmin must pick the smaller id and both copies appear in order
+    pre = m.eval(pts, q, want_grad=False)["f"]
+    dup = np.unique(np.argmin(pre, axis=1))
+    order = np.argsort(np.concatenate([ids, ids[dup] + 1]), kind="stable")
+    pts = np.concatenate([pts, pts[dup]])[order]
+    ids = np.concatenate([ids, ids[dup] + 1])[order]
+    tau = synth.load_tau("C1")
+    d = m.detect(pts, ids, q, DELTA, tau)
+    full = m.eval(pts, q)
+    F = full["f"]
+    pairs = sorted((w, int(ids[j])) for w in range(q.shape[0]) for j in range(len(ids))
+                   if F[w, j] - DELTA <= tau)
+    assert d["count"] == len(pairs)
+    assert [(int(a), int(b)) for a, b in zip(d["wp"], d["pt"])] == pairs
+    pos = {int(i): j for j, i in enumerate(ids)}
+    for k, (w, pt) in enumerate(pairs):
+        assert d["value"][k] == F[w, pos[pt]]
+        np.testing.assert_array_equal(d["grad"][k], full["g"][w, pos[pt]])
+    for w in range(q.shape[0]):
+        best = min(range(len(ids)), key=lambda j: (F[w, j], ids[j]))
+        assert d["wp_min"][w] == F[w, best] and d["wp_argmin"][w] == ids[best]
+        assert d["wp_offsets"][w] == sum(1 for a, _ in pairs if a < w)
+    assert d["wp_offsets"][-1] == len(pairs)
+    # sparsity sits near the calibrated 5% target
+    assert 0.02 <= len(pairs) / F.size <= 0.10
+    # every record satisfies the predicate, every non-record violates it
+    assert np.all(d["value"] - DELTA <= tau)
+    # empty scene: +inf / -1 / zero records
+    e = m.detect(np.zeros((0, 3)), np.zeros(0, np.int64), q, DELTA, tau)
+    assert e["count"] == 0 and np.all(np.isinf(e["wp_min"])) and np.all(e["wp_argmin"] == -1)
+
+
+# ------------------------------------------------------------------ EMU_BF16 self-consistency
+def test_emu_bf16_consistency(tmp_path):
+    """P6(i): bf16-representable weights + weight rounding only == exact, bit for bit.
+    P6(ii): full emulation stays within the bf16 error scale of the exact result."""
+    act, dims, layers = synth.make_weights(32, seed=3)
+
+    def to_bf16(a):
+        u = np.asarray(a, np.float32).view(np.uint32).astype(np.uint64)
+        u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+        return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+    rl = [(to_bf16(W), b) for W, b in layers]
+    m = oracle.MLP(_write(tmp_path, "bf.mlpw", act, dims, rl))
+    pts, q = _rand_inputs(np.random.default_rng(8), 64, 4)
+    a = m.eval(pts, q)
+    b = m.eval(pts, q, flags=oracle.EMU_W)
+    assert np.array_equal(a["f"], b["f"]) and np.array_equal(a["g"], b["g"])
+    c = m.eval(pts, q, flags=oracle.EMU_BF16, want_hash=True)
+    d = m.eval(pts, q, want_hash=True)
+    assert np.max(np.abs(c["f"] - d["f"])) <= 2e-2 * max(1.0, np.abs(d["f"]).max())
+    same = c["mask_hash"] == d["mask_hash"]
+    gn = np.linalg.norm(d["g"], axis=-1)
+    dg = np.linalg.norm(c["g"] - d["g"], axis=-1)
+    assert np.all(dg[same] <= 2e-2 * np.maximum(1.0, gn[same]))
+
+
+# ------------------------------------------------------------------ scene replay (O2)
+def test_scene_id_rule():
+    s = oracle.Scene(10)
+    ids = s.update(np.arange(18, dtype=np.float32).reshape(6, 3))
+    assert list(ids) == [0, 1, 2, 3, 4, 5]
+    ids2 = s.update(np.ones((3, 3), np.float32), remove_ids=[1, 4])
+    assert list(ids2) == [6, 7, 8]          # freed ids are not reused in the same call
+    ids3 = s.update(np.ones((2, 3), np.float32))
+    assert list(ids3) == [1, 4]             # ... but are in the next one
+    live, xyz = s.export()
+    assert list(live) == [0, 1, 2, 3, 4, 5, 6, 7, 8]
+    with pytest.raises(oracle.OracleError):
+        s.update(remove_ids=[9])            # unknown id: atomic failure
+    assert list(s.export()[0]) == list(live)
+    with pytest.raises(oracle.OracleError):
+        s.update(np.ones((2, 3), np.float32))   # capacity
+
+
+def test_emu_rounding_points_hand_example(tmp_path):
+    """O8 pinned by hand: which quantities are rounded to bf16 (golden emu_network)."""
+    g = json.loads((GOLD / "hand_example.json").read_text())["emu_network"]
+    layers = [(np.array(l["W"], float), np.array(l["b"], float)) for l in g["layers"]]
+    m = oracle.MLP(_write(tmp_path, "emu.mlpw", 1, [12] + [1] * 6 + [1], layers))
+    P, Q = np.array([g["p"]]), np.array([g["q"]])
+    for flags, key in ((0, "exact"), (oracle.EMU_W, "exact"), (oracle.EMU_A, "emu_a"),
+                       (oracle.EMU_BF16, "emu_a")):
+        out = m.eval(P, Q, flags=flags)
+        assert out["f"][0, 0] == g[key]["f"], (flags, out["f"][0, 0])
+        np.testing.assert_array_equal(out["g"][0, 0], g[key]["grad"])
+
+
+def test_threshold_inclusive_hand_example(tmp_path):
+    g = json.loads((GOLD / "hand_example.json").read_text())["networks"][1]
+    layers = [(np.array(l["W"], float), np.array(l["b"], float)) for l in g["layers"]]
+    m = oracle.MLP(_write(tmp_path, "thr.mlpw", 1, [12] + [1] * 6 + [1], layers))
+    # both cases share q_xy = (1, 0) after re-basing their points: p = (1, 0) -> f = 21, p = (2, 0) -> f = 25
+    pts = np.array([[1.0, 0.0, 0.3], [2.0, 0.0, 0.0]])
+    q = np.array([[1.0, 0.0, 0, 0, 0, 0, 0, 0, 0]])
+    tau = 25.0 - 0.1
+    d = m.detect(pts, np.array([4, 9]), q, 0.1, tau)
+    assert list(d["pt"]) == [4, 9] and list(d["value"]) == [21.0, 25.0]
+    d = m.detect(pts, np.array([4, 9]), q, 0.1, np.nextafter(tau, -np.inf))
+    assert list(d["pt"]) == [4]
+    assert d["wp_min"][0] == 21.0 and d["wp_argmin"][0] == 4
+
+
+def test_emu_weight_rounding_hand_example(tmp_path):
+    g = json.loads((GOLD / "hand_example.json").read_text())["emu_w_network"]
+    layers = [(np.array(l["W"], float), np.array(l["b"], float)) for l in g["layers"]]
+    m = oracle.MLP(_write(tmp_path, "emuw.mlpw", 1, [12] + [1] * 6 + [1], layers))
+    P, Q = np.array([g["p"]]), np.array([g["q"]])
+    for flags, key in ((0, "exact"), (oracle.EMU_W, "emu_w"), (oracle.EMU_BF16, "emu_bf16")):
+        out = m.eval(P, Q, flags=flags)
+        assert out["f"][0, 0] == g[key]["f"], flags
+        np.testing.assert_array_equal(out["g"][0, 0], g[key]["grad"])
