@@ -1,0 +1,324 @@
+"""bench.py -- GCDF value+grad queries/s with active-set detection on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--precision bf16|fp32]
+    python bench.py --impl reference ...      # the float64 CPU oracle on host cores
+
+One step = one SCO iteration of the hot path (all SURVEY §8(a) rows): an incremental
+scene update (A9: 200 removes + 200 adds on a moved box) followed by the fused
+detect over every (waypoint, live point) pair (A2-A8) with the count read back on the
+host; at N > 1 the points are sharded by rank and the active sets are gathered with
+NCCL + the merge kernel.  `value` counts every (waypoint, live point) pair of the whole
+job per second.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import synth  # noqa: E402
+
+METRIC = "GCDF value+grad queries/sec (with active-set detection)"
+FLOPS_PAIR_TOTAL = {128: 333_312, 32: 21_888}      # fwd 167,168 + bwd 166,144 (H=128)
+FLOPS_PAIR_TENSOR = {128: 327_680, 32: 20_480}     # the ten H x H GEMMs (tensor-eligible)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--precision", default="auto", choices=["auto", "bf16", "fp32"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w_max": max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()), default=None)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ----------------------------------------------------------------------------- oracle timing
+def cpu_oracle_rate(cfg, pts, q, sample_wp=4, sample_pts=32768, nthreads=None):
+    """The oracle as it stands on the host cores: detect over a bounded sample."""
+    import oracle
+    nthreads = nthreads or os.cpu_count() or 1
+    m = oracle.MLP(synth.weights_path(cfg.H))
+    rng = np.random.default_rng(12345)
+    qs = q.reshape(-1, 9)
+    wsel = np.sort(rng.choice(qs.shape[0], size=min(sample_wp, qs.shape[0]), replace=False))
+    psel = np.sort(rng.choice(pts.shape[0], size=min(sample_pts, pts.shape[0]), replace=False))
+    t0 = time.perf_counter()
+    m.detect(pts[psel], psel.astype(np.int64), qs[wsel], synth.inputs.DELTA, synth.load_tau(cfg.name),
+             nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    n = len(wsel) * len(psel)
+    return {"value": n / dt, "unit": "queries/s", "cores": int(nthreads), "kind": "oracle",
+            "sample": f"{len(wsel)} waypoints x {len(psel)} points of {cfg.name} ({n} pairs, "
+                      f"float64 detect incl. gradients), {dt:.1f} s"}
+
+
+def run_reference(a):
+    """--impl reference: the float64 oracle (this tier's reference arm) on host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = synth.get_config(a.config)
+    pts, _ = synth.make_scene_points(cfg)
+    q = synth.make_waypoints(cfg)
+    import oracle  # noqa: F401
+    times, n_pairs = [], 0
+    nthreads = os.cpu_count() or 1
+    for i in range(a.warmup + a.steps):
+        r = cpu_oracle_rate(cfg, pts, q, sample_wp=2, sample_pts=8192, nthreads=nthreads)
+        if i >= a.warmup:
+            times.append(2 * 8192 / r["value"])
+            n_pairs += 2 * 8192
+    total = sum(times)
+    v = n_pairs / total
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * total / a.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.desc}; each step a bounded sample of 2 waypoints x 8192 points",
+                       "pairs_per_step_sampled": 2 * 8192},
+            "cpu_baseline": {"value": v, "unit": "queries/s", "cores": nthreads, "kind": "oracle",
+                             "sample": "2 waypoints x 8192 points per step"},
+            "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2601_18548_b200 import BF16, FP32, Context
+    from paper_2601_18548_b200.dist import gather_active_sets
+    from paper_2601_18548_b200.gcdf import load_library
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    lib = load_library()
+    prec = a.precision
+    if prec == "auto":
+        prec = "bf16" if lib.gcdf_has_tcgen05() else "fp32"
+    cfg = synth.get_config(a.config)
+    tau = synth.load_tau(cfg.name)
+    delta = synth.inputs.DELTA
+    pts, boxes = synth.make_scene_points(cfg)
+    q_np = synth.make_waypoints(cfg)
+    n_wp = cfg.B * cfg.N
+    slack = 4096
+    max_active = int(min(cfg.pairs // world + 1024, max(4 * cfg.pairs // 100 // world, 1 << 16)))
+    ctx = Context(local, precision=BF16 if prec == "bf16" else FP32, scene_capacity=cfg.M + slack,
+                  max_waypoints=n_wp, max_active=max_active, rank=rank, world=world)
+    ctx.load_weights(synth.weights_path(cfg.H))
+    ctx.update_scene(pts)
+    q = torch.from_numpy(q_np).to(dev)
+    outs = ctx.alloc_detect_outputs(n_wp, max_active)
+    upd_rng = np.random.default_rng([cfg.seed, 7])
+    live_ids = np.arange(cfg.M, dtype=np.int64)
+
+    def scene_step():
+        nonlocal live_ids
+        add, rem = synth.scene_update_batch(upd_rng, boxes, live_ids)
+        ids = ctx.update_scene(add, rem)
+        live_ids = np.union1d(np.setdiff1d(live_ids, rem, assume_unique=True), ids)
+        return add, rem
+
+    def step():
+        scene_step()
+        o = ctx.detect_active_set(q, delta, tau, outputs=outs, sync_count=True)
+        if world > 1:
+            o = gather_active_sets(ctx, o, n_wp, group=None)
+        return o
+
+    # L2 flush buffer (> 126 MB L2) written between timed steps
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ctx.profile_enable(True)
+    ctx.profile_read(reset=True)
+    l0 = ctx.launches
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    n_live_total = 0
+    last = None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(a.steps):
+        flush.zero_()
+        ev[i][0].record()
+        last = step()
+        ev[i][1].record()
+        n_live_total += ctx.scene_info()["n_live"]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = ctx.launches - l0
+    mlp_ms, mlp_n = ctx.profile_read(reset=True)
+    ctx.profile_enable(False)
+    clk = clocks.stop()
+    t_ms = sum(s.elapsed_time(e) for s, e in ev)
+    t_max = t_ms
+    if world > 1:
+        t = torch.tensor([t_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+    pairs_total = n_live_total * n_wp           # every (waypoint, live point) pair of the job
+    value = pairs_total / (t_max / 1e3)
+    n_active = int(last["n"])
+
+    # roofline of the dominant kernel (fused MLP): algorithmic flops per launch / live duration
+    peaks, peak_src = measured_peaks()
+    local_pairs = n_wp * (n_live_total / a.steps) / world
+    if prec == "bf16":
+        flops = FLOPS_PAIR_TENSOR[cfg.H] * local_pairs
+        achieved = flops / (mlp_ms / mlp_n / 1e3) / 1e12
+        peak = float(peaks.get("bf16_tflops_sustained" if a.steps * t_max / a.steps > 1000 else "bf16_tflops"))
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": None, "peak_source": f"{peak_src} bf16 dense (MEASURED_PEAKS.json)",
+                "kernel": "k_mlp_tc (fused transform + MLP fwd/bwd + threshold/min/compaction)",
+                "kernel_ms_avg": mlp_ms / mlp_n, "flops_per_pair": FLOPS_PAIR_TENSOR[cfg.H]}
+    else:
+        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12   # FP32 FFMA: 148 SMs x 128 lanes x 2 flops x clock
+        flops = FLOPS_PAIR_TOTAL[cfg.H] * local_pairs
+        achieved = flops / (mlp_ms / mlp_n / 1e3) / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": None, "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz",
+                "kernel": "k_mlp_simt (fused transform + MLP fwd/bwd + threshold/min/compaction)",
+                "kernel_ms_avg": mlp_ms / mlp_n, "flops_per_pair": FLOPS_PAIR_TOTAL[cfg.H]}
+    kshare = mlp_ms / t_ms if t_ms > 0 else None
+
+    # e2e through the public API with host buffers: pinned q H2D + update + detect + D2H of results
+    e2e_steps = a.e2e_steps or max(1, min(a.steps, 5))
+    q_pin = torch.from_numpy(q_np).pin_memory()
+    q_dev = torch.empty_like(q_pin, device=dev)
+    h2d = d2h = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_pairs = 0
+    for i in range(e2e_steps):
+        add, rem = scene_step()
+        q_dev.copy_(q_pin, non_blocking=True)
+        o = ctx.detect_active_set(q_dev, delta, tau, outputs=outs, sync_count=True)
+        if world > 1:
+            o = gather_active_sets(ctx, o, n_wp)
+        n = int(o["n"])
+        rec_h = o["records"][:n].cpu()
+        wmin_h, warg_h, offs_h = o["wp_min"].cpu(), o["wp_argmin"].cpu(), o["wp_offsets"].cpu()
+        h2d += q_pin.numel() * 4 + add.nbytes + rem.nbytes
+        d2h += rec_h.numel() + wmin_h.numel() * 4 + warg_h.numel() * 8 + offs_h.numel() * 8 + 8
+        e2e_pairs += ctx.scene_info()["n_live"] * n_wp
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_oracle_rate(cfg, pts, q_np)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": t_max / a.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": prec, "data": "synthetic (seeded clutter clouds + random-init weights)",
+            "config": {"workload": f"{cfg.name}: {cfg.desc}", "B": cfg.B, "N": cfg.N, "points": cfg.M,
+                       "hidden": cfg.H, "pairs_per_step": int(pairs_total / a.steps), "delta": delta, "tau": tau,
+                       "active_per_step": n_active, "scene_update_per_step": "200 removes + 200 adds",
+                       "parallelism": f"points sharded over {world} GPU(s)",
+                       "l2": "256 MiB buffer written between timed steps (L2 flush)"},
+            "roofline": roof, "mlp_kernel_share_of_step": kshare,
+            "detect_latency_ms": t_max / a.steps,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_pairs / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": h2d // e2e_steps,
+                    "d2h_bytes_per_step": d2h // e2e_steps, "steps": e2e_steps},
+            "gpu_launches": launches, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

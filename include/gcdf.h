@@ -1,0 +1,196 @@
+/* gcdf.h -- C ABI of libgcdf: the batched neural GCDF query and sparsity-aware
+ * active-set detection of arXiv 2601.18548, on NVIDIA B200 (sm_100a).
+ *
+ * Citations are /root/reference/PAPER.md line numbers (the paper's LaTeX source);
+ * "R<k>" refers to the readings listed in DESIGN.md §3.
+ *
+ * What is computed (the hot path):
+ *   For every pair (waypoint configuration q_i of trajectory b, obstacle point p_j):
+ *     x_in = [p_x - q_x, p_y - q_y, p_z, 0, 0, theta, j1..j6]
+ *       base-frame bias of the obstacle point, PAPER.md:388 ("treat the robot base
+ *       pose as the origin and bias all obstacle points"); R1, R2.
+ *     f = MLP(x_in): the paper's "7-layer MLP" on the concatenation [p, q]
+ *       (PAPER.md:284), ReLU hidden layers, signed scalar output; R7-R10.
+ *     grad_q f in R^9 by the chain rule through the bias; R3.
+ *   Constraint f - delta >= 0 over all i, j (Eq. 11d).
+ *   Active set: f - delta <= tau (R12); per-waypoint min (union = min);
+ *   records in step-major (waypoint, point id) order = c_gcdf of Eq. 14.
+ *   Online point injection/removal without rebuilding.
+ *
+ * Conventions for every entry point:
+ *   - Returns a gcdf_status (0 = OK, < 0 = error).  No C++ exception crosses the ABI.
+ *   - Validation errors are atomic: the call changes nothing.  gcdf_last_error(ctx)
+ *     returns the message of the last failing call (storage owned by ctx).
+ *   - "_dev" pointers are CUDA device pointers (e.g. torch tensor data_ptr()),
+ *     "_host" pointers are host memory.  The caller owns every argument buffer.
+ *   - All device work is enqueued on the given stream (cudaStream_t passed as
+ *     void*; NULL = legacy default stream).  Only calls that return host results
+ *     (update_scene's ids are computed on the host; detect with count_host_or_null
+ *     != NULL) synchronize that stream.
+ *   - A context is bound to one CUDA device and is NOT thread-safe.
+ *   - After gcdf_bind_workspace no call allocates device memory.
+ */
+#ifndef GCDF_H
+#define GCDF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gcdf_ctx gcdf_ctx;
+
+enum gcdf_status {
+  GCDF_OK = 0,
+  GCDF_ERR_INVALID_ARG = -1,
+  GCDF_ERR_IO = -2,
+  GCDF_ERR_BAD_MAGIC = -3,     /* weights file does not start with "MLPW" */
+  GCDF_ERR_VERSION = -4,       /* MLPW version != 1 */
+  GCDF_ERR_DIM_MISMATCH = -5,  /* dims not [12, H x 6, 1] with H in {32, 128}, or activation != ReLU */
+  GCDF_ERR_NOT_LOADED = -6,    /* no weights loaded / no workspace bound */
+  GCDF_ERR_CAPACITY = -7,      /* scene, waypoint, staging or output capacity exceeded */
+  GCDF_ERR_UNKNOWN_ID = -8,    /* remove of an id that is not live (or duplicated in the call) */
+  GCDF_ERR_NONFINITE = -9,     /* NaN / Inf in points or weights */
+  GCDF_ERR_CUDA = -10,         /* CUDA runtime error (message has the CUDA string); sticky */
+  GCDF_ERR_UNSUPPORTED = -11   /* e.g. no sm_100 device */
+};
+
+enum gcdf_precision {
+  GCDF_FP32 = 0, /* fp32 SIMT path: parity path, tolerance 1e-4 rel / 1e-5 abs */
+  GCDF_BF16 = 1  /* tcgen05 tensor-core path: bf16 operands, fp32 accumulate */
+};
+
+enum gcdf_tgrad {
+  GCDF_TGRAD_CHAINRULE = 0, /* d f/d q_xy = -d F/d p'_xy; default, R3 */
+  GCDF_TGRAD_QCHANNEL = 1   /* d f/d q_xy = d F/d x_in[3..4] (the network's q^t channels) */
+};
+
+typedef struct {
+  int32_t precision;       /* gcdf_precision (default GCDF_BF16 if the device supports it) */
+  int32_t tgrad_mode;      /* gcdf_tgrad */
+  int64_t scene_capacity;  /* global id space [0, scene_capacity) of obstacle points */
+  int32_t max_waypoints;   /* largest B*N accepted by query/detect */
+  int64_t max_active;      /* staging capacity (records) of detect on this rank */
+  int32_t rank;            /* point sharding: this rank owns ids whose 128-id block */
+  int32_t world;           /*   (id / 128) satisfies block % world == rank; world >= 1 */
+} gcdf_options;
+
+/* One active constraint (48 B): f, grad_q f (9), wp = b*N + i, pt = global point id. */
+typedef struct {
+  float value;
+  float grad[9];
+  uint32_t wp;
+  uint32_t pt;
+} gcdf_active_t;
+
+/* ------------------------------------------------------------------ lifecycle */
+/* Fills *opt with defaults (precision BF16, chain rule, capacity 1<<20, 256 waypoints,
+   max_active 1<<22, rank 0, world 1). */
+void gcdf_default_options(gcdf_options *opt);
+
+/* Creates a context on CUDA device cuda_device.  Fails with UNSUPPORTED unless the
+   device is compute capability 10.0 (B200).  opt may be NULL (defaults). */
+int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out);
+int gcdf_destroy(gcdf_ctx *ctx);
+const char *gcdf_last_error(const gcdf_ctx *ctx);
+/* Returns 1 if the library was built with the tcgen05 kernels for sm_100a. */
+int gcdf_has_tcgen05(void);
+
+/* Device workspace: the caller allocates `bytes` (256-B aligned) and binds it.  It
+   holds the scene slots, packed weights and detect scratch.  Rebinding resets the
+   scene and requires reloading weights. */
+int gcdf_workspace_bytes(const gcdf_ctx *ctx, int64_t *bytes);
+int gcdf_bind_workspace(gcdf_ctx *ctx, void *dev_ptr, int64_t bytes);
+
+/* ------------------------------------------------------------------ weights */
+/* Loads an MLPW v1 file: "MLPW", u32 version = 1, u32 activation
+   (1 = ReLU), u32 L = 7, u32 dims[8] = [12, H, H, H, H, H, H, 1] with H in {32, 128},
+   then per layer f64 W[out][in] row-major and f64 b[out].  Packs fp32 and bf16
+   (UMMA SWIZZLE_128B) copies into the workspace (enqueued on `stream`, host staging
+   synchronized before return).  Errors: IO (missing/truncated), BAD_MAGIC, VERSION,
+   DIM_MISMATCH, NONFINITE.  Atomic: a failed load keeps the previous weights. */
+int gcdf_load_weights(gcdf_ctx *ctx, const char *mlpw_path, void *stream);
+
+/* ------------------------------------------------------------------ scene (A0, A9) */
+/* Incremental point injection / removal without problem reconstruction
+   (PAPER.md:75 (c), :401 "both components can be modified online").
+   add_xyz_host [n_add][3] fp32 metres; out_ids_host [n_add] receives the ids;
+   remove_ids_host [n_remove].  Id rule (identical on every rank, so SPMD ranks
+   agree without communication): removals are validated (live, not duplicated);
+   each add takes the lowest id that is free at the start of the call (ids removed by
+   this call become free for the NEXT call).  Each rank stores only the points whose
+   128-id block it owns.  O(n_add + n_remove) device work: one scatter kernel.
+   Errors: UNKNOWN_ID, NONFINITE, CAPACITY (atomic).  Synchronizes `stream` only to
+   recycle its pinned staging buffer. */
+int gcdf_update_scene(gcdf_ctx *ctx, const float *add_xyz_host, int64_t n_add, int64_t *out_ids_host,
+                      const int64_t *remove_ids_host, int64_t n_remove, void *stream);
+
+/* n_live: live points (global); id_bound: 1 + highest id ever assigned (ids < id_bound);
+   local_bound: number of this rank's local slots covering ids < id_bound (a multiple of
+   128; the stride of query outputs).  Local slot s holds global id
+   ((s / 128) * world + rank) * 128 + s % 128. */
+int gcdf_scene_info(const gcdf_ctx *ctx, int64_t *n_live, int64_t *id_bound, int64_t *local_bound);
+
+/* ------------------------------------------------------------------ hot path */
+/* A2 standalone: pair generation + base-frame transform.  out_dev [B*N][local_bound]
+   float4 (p_x - q_x, p_y - q_y, p_z, live) for this rank's local slots. */
+int gcdf_pairgen_transform(gcdf_ctx *ctx, const float *q_dev, int32_t B, int32_t N, void *out_dev,
+                           void *stream);
+
+/* A2-A5 dense: values_dev [B*N][local_bound] fp32 and grads_dev [B*N][local_bound][9]
+   fp32 for every pair of this rank's local slots; dead slots give +INF and a zero
+   gradient.  q_dev [B][N][9] fp32 = [x, y, theta, j1..j6].
+   grads_dev may be NULL (values only). */
+int gcdf_query_values_grads(gcdf_ctx *ctx, const float *q_dev, int32_t B, int32_t N, float *values_dev,
+                            float *grads_dev, void *stream);
+
+/* A2-A8 fused: query + threshold + per-waypoint min + stream compaction.
+   out_dev [out_capacity] records in (wp, pt) order; wp_offsets_dev [B*N+1] (Eq. 14
+   block structure); wp_min_dev [B*N] (+INF if no live point);
+   wp_argmin_dev [B*N] (smallest id on ties, -1 if none); wp_key_dev [B*N] (may be
+   NULL): int64 signed-order key (ordered(f) << 32 | pt) ^ INT64_MIN, INT64_MAX if
+   none, for a cross-rank MIN reduction; count_dev [1] (total active).
+   count_host_or_null: if non-NULL the stream is synchronized and the count written.
+   CAPACITY is returned (count still exact, out content unspecified) when the count
+   exceeds out_capacity or the staging capacity max_active; grow and retry.  On a
+   sharded scene (world > 1) the result covers this rank's points only; see
+   gcdf_merge_active_sets. */
+int gcdf_detect_active_set(gcdf_ctx *ctx, const float *q_dev, int32_t B, int32_t N, float delta,
+                           float tau, gcdf_active_t *out_dev, int64_t out_capacity, int64_t *wp_offsets_dev,
+                           float *wp_min_dev, int64_t *wp_argmin_dev, int64_t *wp_key_dev,
+                           int64_t *count_dev, int64_t *count_host_or_null, void *stream);
+
+/* A6-A8 standalone over a dense value/gradient array (e.g. from
+   gcdf_query_values_grads): same outputs as detect.  values_dev [n_wp][stride],
+   grads_dev [n_wp][stride][9], column s = local slot s of this context's scene. */
+int gcdf_compact_dense(gcdf_ctx *ctx, const float *values_dev, const float *grads_dev, int32_t n_wp,
+                       int64_t stride, float delta, float tau, gcdf_active_t *out_dev, int64_t out_capacity,
+                       int64_t *wp_offsets_dev, float *wp_min_dev, int64_t *wp_argmin_dev,
+                       int64_t *wp_key_dev, int64_t *count_dev, int64_t *count_host_or_null, void *stream);
+
+/* Multi-GPU gather step: merge the per-rank active sets gathered from
+   `world` ranks into one canonical (wp, pt) ordered set.
+   recs_dev [world][rec_stride] (rank r's records at r*rec_stride, in its own order);
+   offsets_dev [world][n_wp+1] (each rank's wp_offsets); wp_key_dev [n_wp] the MIN over
+   ranks of wp_key.  Outputs as in detect.  Pure device work; no collective inside
+   (the collectives run through torch.distributed / NCCL around it). */
+int gcdf_merge_active_sets(gcdf_ctx *ctx, int32_t world, int32_t n_wp, const gcdf_active_t *recs_dev,
+                           int64_t rec_stride, const int64_t *offsets_dev, const int64_t *wp_key_dev,
+                           gcdf_active_t *out_dev, int64_t out_capacity, int64_t *wp_offsets_dev,
+                           float *wp_min_dev, int64_t *wp_argmin_dev, int64_t *count_dev, void *stream);
+
+/* Number of kernels this context launched since creation (for bench accounting). */
+int64_t gcdf_launch_count(const gcdf_ctx *ctx);
+
+/* Optional live timing of the fused MLP kernel (the dominant kernel): when enabled,
+   query/detect record a CUDA event pair around that launch on the call's stream.
+   gcdf_profile_read synchronizes on the last pair and returns the accumulated kernel
+   milliseconds and launch count since the last reset. */
+int gcdf_profile_enable(gcdf_ctx *ctx, int enable);
+int gcdf_profile_read(gcdf_ctx *ctx, double *mlp_ms, int64_t *mlp_launches, int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GCDF_H */

@@ -1,0 +1,634 @@
+// gcdf_host.cpp -- the C-ABI host layer of libgcdf (include/gcdf.h).
+//
+// Owns: argument validation (atomic failures), the MLPW v1 parser (its own
+// implementation -- the oracle has a separate one), weight packing (fp32 SIMT layout and
+// bf16 UMMA SWIZZLE_128B layout), the replicated scene-id allocator ("both
+// components can be modified online"), the workspace carve-up, and kernel dispatch.
+// No device memory is allocated after gcdf_bind_workspace; no CPU compute path exists
+// for any hot-path step (every step runs in the kernels of this directory).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <string>
+#include <vector>
+
+#include "gcdf_internal.h"
+
+using namespace gcdf;
+
+namespace {
+
+constexpr int64_t kUpdChunk = 65536;  // points per scene-update scatter chunk
+constexpr int kMaxH = 128;
+constexpr int kEvPool = 64;
+
+inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
+
+struct Layout {
+  int64_t pts, wf32, wbf16, meta, staging, wp_key, wp_count, counter, upd_payload, upd_slots, total;
+  int64_t wf32_bytes, wbf16_bytes;
+};
+
+// fp32 block sizes (floats) for H = kMaxH
+constexpr int64_t kF32W1p = kMaxH * 4, kF32W1q = kMaxH * 8, kF32W1full = kMaxH * 12;
+constexpr int64_t kF32Mat = (int64_t)kMaxH * kMaxH;
+constexpr int64_t kF32Total = kF32W1p + kF32W1q + kF32W1full + 10 * kF32Mat + 5 * kMaxH + kMaxH;
+// bf16 block sizes (bytes)
+constexpr int64_t kBfMat = (int64_t)kMaxH * kMaxH * 2;
+constexpr int64_t kBfW1t = 16LL * kMaxH * 2;
+constexpr int64_t kBfTotal = 5 * kBfMat + kBfW1t;
+
+}  // namespace
+
+struct gcdf_ctx {
+  int device = 0;
+  int num_sms = 148;
+  gcdf_options opt{};
+  std::string err;
+  bool cuda_failed = false;
+  int64_t launches = 0;
+  // workspace
+  char *ws = nullptr;
+  int64_t ws_bytes = 0;
+  Layout L{};
+  int64_t local_cap = 0;   // local slots (multiple of 128)
+  int64_t tiles_cap = 0;   // local_cap / 128
+  // weights
+  bool loaded = false;
+  int H = 0;
+  float b7 = 0.f;
+  // scene (replicated on every rank)
+  std::vector<uint64_t> live;  // global id bitmap
+  int64_t n_live = 0, id_bound = 0, cursor = 0;
+  // pinned staging for scene updates
+  float4 *h_payload = nullptr;
+  int64_t *h_slots = nullptr;
+  cudaEvent_t upd_done = nullptr;
+  // optional MLP-kernel timing
+  bool prof = false;
+  std::vector<cudaEvent_t> ev;  // 2 * kEvPool
+  int ev_used = 0;
+  double prof_ms = 0.0;
+  int64_t prof_n = 0;
+};
+
+namespace {
+
+int fail(gcdf_ctx *c, int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+int cuda_fail(gcdf_ctx *c, cudaError_t e, const char *what) {
+  if (c) c->cuda_failed = true;
+  return fail(c, GCDF_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define CK(c, expr, what)                               \
+  do {                                                  \
+    cudaError_t _e = (expr);                            \
+    if (_e != cudaSuccess) return cuda_fail(c, _e, what); \
+  } while (0)
+
+int precheck(gcdf_ctx *c, bool need_weights = true) {
+  if (!c) return GCDF_ERR_INVALID_ARG;
+  if (c->cuda_failed) return fail(c, GCDF_ERR_CUDA, "context is in a failed CUDA state: %s", c->err.c_str());
+  if (!c->ws) return fail(c, GCDF_ERR_NOT_LOADED, "no workspace bound");
+  if (need_weights && !c->loaded) return fail(c, GCDF_ERR_NOT_LOADED, "no weights loaded");
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaSetDevice");
+  return GCDF_OK;
+}
+
+inline bool owned(const gcdf_ctx *c, int64_t id) {
+  return ((id / kTile) % c->opt.world) == c->opt.rank;
+}
+inline int64_t local_slot(const gcdf_ctx *c, int64_t id) {
+  return ((id / kTile) / c->opt.world) * kTile + id % kTile;
+}
+int64_t local_bound_of(const gcdf_ctx *c) {
+  const int64_t nblk = (c->id_bound + kTile - 1) / kTile;
+  const int64_t r = c->opt.rank, W = c->opt.world;
+  const int64_t owned_blocks = nblk > r ? (nblk - r + W - 1) / W : 0;
+  return owned_blocks * kTile;
+}
+inline bool is_live(const gcdf_ctx *c, int64_t id) { return (c->live[id >> 6] >> (id & 63)) & 1ull; }
+
+WeightsF32 f32_view(const gcdf_ctx *c) {
+  const int H = c->H;
+  float *base = reinterpret_cast<float *>(c->ws + c->L.wf32);
+  WeightsF32 w{};
+  float *p = base;
+  w.w1p = reinterpret_cast<const float4 *>(p); p += kF32W1p;
+  w.w1q = p; p += kF32W1q;
+  w.w1full = p; p += kF32W1full;
+  for (int li = 0; li < 5; ++li) { w.wt[li] = p; p += (int64_t)H * H; }
+  for (int li = 0; li < 5; ++li) { w.wb[li] = p; p += (int64_t)H * H; }
+  for (int li = 0; li < 5; ++li) { w.bias[li] = p; p += H; }
+  w.w7 = p;
+  w.b7 = c->b7;
+  return w;
+}
+
+WeightsBF16 bf16_view(const gcdf_ctx *c) {
+  WeightsF32 f = f32_view(c);
+  WeightsBF16 w{};
+  w.w_sw128 = c->ws + c->L.wbf16;
+  w.w1t_sw128 = c->ws + c->L.wbf16 + 5 * kBfMat;
+  w.w1p = f.w1p;
+  w.w1q = f.w1q;
+  w.bias = f.bias[0];  // the five bias vectors are contiguous [5][H]
+  w.w7 = f.w7;
+  w.b7 = f.b7;
+  return w;
+}
+
+DetectScratch scratch_view(const gcdf_ctx *c) {
+  DetectScratch d{};
+  d.tile_meta = reinterpret_cast<int2 *>(c->ws + c->L.meta);
+  d.staging = reinterpret_cast<gcdf_active_t *>(c->ws + c->L.staging);
+  d.max_active = c->opt.max_active;
+  d.counter = reinterpret_cast<unsigned long long *>(c->ws + c->L.counter);
+  d.wp_key = reinterpret_cast<unsigned long long *>(c->ws + c->L.wp_key);
+  return d;
+}
+
+SceneView scene_view(const gcdf_ctx *c) {
+  SceneView s{};
+  s.pts = reinterpret_cast<const float4 *>(c->ws + c->L.pts);
+  s.local_bound = local_bound_of(c);
+  s.rank = c->opt.rank;
+  s.world = c->opt.world;
+  return s;
+}
+
+uint16_t to_bf16_rne(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+// UMMA canonical SWIZZLE_128B (K-major view): matrix [rows][cols] bf16, cols % 64 == 0.
+// chunk = col / 64 -> [rows][128 B] block; 16-B granule g of row r at g ^ (r % 8).
+void pack_sw128(const std::vector<float> &m, int rows, int cols, uint16_t *dst) {
+  for (int r = 0; r < rows; ++r)
+    for (int c = 0; c < cols; ++c) {
+      const int chunk = c / 64, cb = (c % 64) * 2, g = cb / 16;
+      const int64_t byte = (int64_t)chunk * rows * 128 + (int64_t)r * 128 + ((g ^ (r % 8)) * 16) + (cb % 16);
+      dst[byte / 2] = to_bf16_rne(m[(size_t)r * cols + c]);
+    }
+}
+
+int count_launch(gcdf_ctx *c, cudaError_t e, const char *what, int n = 1) {
+  c->launches += n;
+  if (e != cudaSuccess) return cuda_fail(c, e, what);
+  return GCDF_OK;
+}
+
+int prof_drain(gcdf_ctx *c) {
+  for (int i = 0; i < c->ev_used; ++i) {
+    CK(c, cudaEventSynchronize(c->ev[2 * i + 1]), "profile sync");
+    float ms = 0.f;
+    CK(c, cudaEventElapsedTime(&ms, c->ev[2 * i], c->ev[2 * i + 1]), "profile elapsed");
+    c->prof_ms += ms;
+    ++c->prof_n;
+  }
+  c->ev_used = 0;
+  return GCDF_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+void gcdf_default_options(gcdf_options *o) {
+  if (!o) return;
+  o->precision = GCDF_BF16;
+  o->tgrad_mode = GCDF_TGRAD_CHAINRULE;
+  o->scene_capacity = 1 << 20;
+  o->max_waypoints = 256;
+  o->max_active = 1 << 22;
+  o->rank = 0;
+  o->world = 1;
+}
+
+int gcdf_has_tcgen05(void) { return tc_compiled() ? 1 : 0; }
+
+int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out) {
+  if (!out) return GCDF_ERR_INVALID_ARG;
+  *out = nullptr;
+  gcdf_options o;
+  gcdf_default_options(&o);
+  if (opt) o = *opt;
+  if (o.scene_capacity <= 0 || o.scene_capacity >= (1LL << 32) || o.max_waypoints <= 0 || o.max_active <= 0 ||
+      o.max_active >= (1LL << 31) || o.world < 1 || o.rank < 0 || o.rank >= o.world ||
+      (o.precision != GCDF_FP32 && o.precision != GCDF_BF16) ||
+      (o.tgrad_mode != GCDF_TGRAD_CHAINRULE && o.tgrad_mode != GCDF_TGRAD_QCHANNEL))
+    return GCDF_ERR_INVALID_ARG;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev) return GCDF_ERR_UNSUPPORTED;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, cuda_device) != cudaSuccess) return GCDF_ERR_CUDA;
+  if (prop.major != 10 || prop.minor != 0) return GCDF_ERR_UNSUPPORTED;  // sm_100a kernels only
+  if (o.precision == GCDF_BF16 && !tc_compiled()) return GCDF_ERR_UNSUPPORTED;
+  gcdf_ctx *c = new gcdf_ctx();
+  c->device = cuda_device;
+  c->num_sms = prop.multiProcessorCount;
+  c->opt = o;
+  const int64_t gblocks = (o.scene_capacity + kTile - 1) / kTile;
+  const int64_t lblocks = (gblocks + o.world - 1) / o.world;
+  c->local_cap = lblocks * kTile;
+  c->tiles_cap = lblocks;
+  c->live.assign((size_t)((o.scene_capacity + 63) / 64), 0ull);
+  // workspace layout
+  Layout &L = c->L;
+  int64_t off = 0;
+  L.pts = off; off = align256(off + c->local_cap * 16);
+  L.wf32 = off; L.wf32_bytes = kF32Total * 4; off = align256(off + L.wf32_bytes);
+  L.wbf16 = off; L.wbf16_bytes = kBfTotal; off = align256(off + kBfTotal);
+  L.meta = off; off = align256(off + (int64_t)o.max_waypoints * c->tiles_cap * 8);
+  L.staging = off; off = align256(off + o.max_active * (int64_t)sizeof(gcdf_active_t));
+  L.wp_key = off; off = align256(off + (int64_t)o.max_waypoints * 8);
+  L.wp_count = off; off = align256(off + (int64_t)o.max_waypoints * 8);
+  L.counter = off; off = align256(off + 16);
+  L.upd_payload = off; off = align256(off + kUpdChunk * 16);
+  L.upd_slots = off; off = align256(off + kUpdChunk * 8);
+  L.total = off;
+  cudaSetDevice(cuda_device);
+  if (cudaHostAlloc(&c->h_payload, kUpdChunk * 16, cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc(&c->h_slots, kUpdChunk * 8, cudaHostAllocDefault) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->upd_done, cudaEventDisableTiming) != cudaSuccess) {
+    gcdf_destroy(c);
+    return GCDF_ERR_CUDA;
+  }
+  *out = c;
+  return GCDF_OK;
+}
+
+int gcdf_destroy(gcdf_ctx *c) {
+  if (!c) return GCDF_OK;
+  cudaSetDevice(c->device);
+  if (c->upd_done) { cudaEventSynchronize(c->upd_done); cudaEventDestroy(c->upd_done); }
+  if (c->h_payload) cudaFreeHost(c->h_payload);
+  if (c->h_slots) cudaFreeHost(c->h_slots);
+  for (auto &e : c->ev) cudaEventDestroy(e);
+  delete c;
+  return GCDF_OK;
+}
+
+const char *gcdf_last_error(const gcdf_ctx *c) { return c ? c->err.c_str() : "null context"; }
+
+int64_t gcdf_launch_count(const gcdf_ctx *c) { return c ? c->launches : 0; }
+
+int gcdf_workspace_bytes(const gcdf_ctx *c, int64_t *bytes) {
+  if (!c || !bytes) return GCDF_ERR_INVALID_ARG;
+  *bytes = c->L.total;
+  return GCDF_OK;
+}
+
+int gcdf_bind_workspace(gcdf_ctx *c, void *dev_ptr, int64_t bytes) {
+  if (!c) return GCDF_ERR_INVALID_ARG;
+  if (!dev_ptr || bytes < c->L.total || ((uintptr_t)dev_ptr & 255))
+    return fail(c, GCDF_ERR_INVALID_ARG, "workspace must be >= %lld bytes and 256-B aligned", (long long)c->L.total);
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, dev_ptr) != cudaSuccess || at.type != cudaMemoryTypeDevice || at.device != c->device)
+    return fail(c, GCDF_ERR_INVALID_ARG, "workspace is not device memory of device %d", c->device);
+  c->ws = static_cast<char *>(dev_ptr);
+  c->ws_bytes = bytes;
+  c->loaded = false;
+  std::fill(c->live.begin(), c->live.end(), 0ull);
+  c->n_live = c->id_bound = c->cursor = 0;
+  cudaSetDevice(c->device);
+  cudaError_t e = launch_fill(reinterpret_cast<float4 *>(c->ws + c->L.pts), c->local_cap, nullptr);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  return count_launch(c, e, "workspace init");
+}
+
+int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
+  int rc = precheck(c, false);
+  if (rc) return rc;
+  if (!path) return fail(c, GCDF_ERR_INVALID_ARG, "null path");
+  std::ifstream fh(path, std::ios::binary);
+  if (!fh) return fail(c, GCDF_ERR_IO, "cannot open %s", path);
+  std::vector<char> buf((std::istreambuf_iterator<char>(fh)), std::istreambuf_iterator<char>());
+  size_t pos = 0;
+  auto rd = [&](void *d, size_t n) -> bool {
+    if (pos + n > buf.size()) return false;
+    std::memcpy(d, buf.data() + pos, n);
+    pos += n;
+    return true;
+  };
+  char magic[4];
+  if (!rd(magic, 4)) return fail(c, GCDF_ERR_IO, "%s: truncated header", path);
+  if (std::memcmp(magic, "MLPW", 4) != 0) return fail(c, GCDF_ERR_BAD_MAGIC, "%s: bad magic", path);
+  uint32_t hdr[3];
+  if (!rd(hdr, 12)) return fail(c, GCDF_ERR_IO, "%s: truncated header", path);
+  if (hdr[0] != 1) return fail(c, GCDF_ERR_VERSION, "%s: version %u != 1", path, hdr[0]);
+  const uint32_t act = hdr[1], L = hdr[2];
+  if (L != 7) return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: %u layers, expected 7 (R7)", path, L);
+  uint32_t dims[8];
+  if (!rd(dims, 32)) return fail(c, GCDF_ERR_IO, "%s: truncated dims", path);
+  const int H = (int)dims[1];
+  bool ok = dims[0] == (uint32_t)kNin && dims[7] == 1 && (H == 32 || H == 128);
+  for (int l = 1; l <= 6; ++l) ok = ok && dims[l] == (uint32_t)H;
+  if (!ok) return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: dims must be [12, H x 6, 1], H in {32, 128}", path);
+  if (act != 1) return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: activation %u (only ReLU = 1 is supported, R9)", path, act);
+  if (c->opt.precision == GCDF_BF16 && H != 128)
+    return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: the bf16 tensor-core path needs H = 128 (use GCDF_FP32 for H = %d)", path, H);
+  std::vector<std::vector<double>> Wd(7), bd(7);
+  for (int l = 0; l < 7; ++l) {
+    Wd[l].resize((size_t)dims[l + 1] * dims[l]);
+    bd[l].resize(dims[l + 1]);
+    if (!rd(Wd[l].data(), Wd[l].size() * 8) || !rd(bd[l].data(), bd[l].size() * 8))
+      return fail(c, GCDF_ERR_IO, "%s: truncated body (layer %d)", path, l + 1);
+    for (double v : Wd[l]) if (!std::isfinite(v)) return fail(c, GCDF_ERR_NONFINITE, "%s: non-finite weight", path);
+    for (double v : bd[l]) if (!std::isfinite(v)) return fail(c, GCDF_ERR_NONFINITE, "%s: non-finite bias", path);
+  }
+  if (pos != buf.size()) return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: %zu trailing bytes", path, buf.size() - pos);
+
+  // ---- pack fp32 (SIMT layout) ----
+  std::vector<float> f32((size_t)kF32Total, 0.f);
+  float *p = f32.data();
+  auto W = [&](int l, int r, int col) { return (float)Wd[l][(size_t)r * dims[l] + col]; };
+  for (int u = 0; u < H; ++u) {
+    p[u * 4 + 0] = W(0, u, 0); p[u * 4 + 1] = W(0, u, 1); p[u * 4 + 2] = W(0, u, 2); p[u * 4 + 3] = (float)bd[0][u];
+  }
+  p += kF32W1p;
+  for (int u = 0; u < H; ++u)
+    for (int i = 0; i < 7; ++i) p[u * 8 + i] = W(0, u, 5 + i);
+  p += kF32W1q;
+  for (int u = 0; u < H; ++u)
+    for (int i = 0; i < kNin; ++i) p[u * kNin + i] = W(0, u, i);
+  p += kF32W1full;
+  const int UPT = H / 16;
+  for (int li = 0; li < 5; ++li, p += (int64_t)H * H)  // wt[k][tu][i] = W[tu + 16 i][k]
+    for (int k = 0; k < H; ++k)
+      for (int tu = 0; tu < 16; ++tu)
+        for (int i = 0; i < UPT; ++i) p[(int64_t)k * H + tu * UPT + i] = W(li + 1, tu + 16 * i, k);
+  for (int li = 0; li < 5; ++li, p += (int64_t)H * H)  // wb[k][tu][i] = W[k][tu + 16 i]
+    for (int k = 0; k < H; ++k)
+      for (int tu = 0; tu < 16; ++tu)
+        for (int i = 0; i < UPT; ++i) p[(int64_t)k * H + tu * UPT + i] = W(li + 1, k, tu + 16 * i);
+  for (int li = 0; li < 5; ++li, p += H)
+    for (int u = 0; u < H; ++u) p[u] = (float)bd[li + 1][u];
+  for (int u = 0; u < H; ++u) p[u] = W(6, 0, u);
+  // ---- pack bf16 (UMMA SW128) ----
+  std::vector<uint16_t> bf((size_t)kBfTotal / 2, 0);
+  if (H == 128) {
+    std::vector<float> m((size_t)H * H);
+    for (int li = 0; li < 5; ++li) {
+      for (int r = 0; r < H; ++r)
+        for (int col = 0; col < H; ++col) m[(size_t)r * H + col] = W(li + 1, r, col);
+      pack_sw128(m, H, H, bf.data() + (size_t)li * kBfMat / 2);
+    }
+    std::vector<float> w1t((size_t)16 * H, 0.f);  // [n = input 0..15][k = unit]
+    for (int n = 0; n < kNin; ++n)
+      for (int k = 0; k < H; ++k) w1t[(size_t)n * H + k] = W(0, k, n);
+    pack_sw128(w1t, 16, H, bf.data() + (size_t)5 * kBfMat / 2);
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CK(c, cudaMemcpyAsync(c->ws + c->L.wf32, f32.data(), f32.size() * 4, cudaMemcpyHostToDevice, s), "weights H2D");
+  CK(c, cudaMemcpyAsync(c->ws + c->L.wbf16, bf.data(), bf.size() * 2, cudaMemcpyHostToDevice, s), "weights H2D");
+  CK(c, cudaStreamSynchronize(s), "weights sync");
+  c->H = H;
+  c->b7 = (float)bd[6][0];
+  c->loaded = true;
+  return GCDF_OK;
+}
+
+int gcdf_update_scene(gcdf_ctx *c, const float *add_xyz, int64_t n_add, int64_t *out_ids, const int64_t *rem,
+                      int64_t n_rem, void *stream) {
+  int rc = precheck(c, false);
+  if (rc) return rc;
+  if (n_add < 0 || n_rem < 0 || (n_add > 0 && (!add_xyz || !out_ids)) || (n_rem > 0 && !rem))
+    return fail(c, GCDF_ERR_INVALID_ARG, "bad update arguments");
+  // validate (atomic): removes live and unique, adds finite, capacity
+  std::vector<int64_t> rs(rem, rem + n_rem);
+  std::sort(rs.begin(), rs.end());
+  for (int64_t i = 0; i < n_rem; ++i) {
+    if (rs[i] < 0 || rs[i] >= c->opt.scene_capacity || !is_live(c, rs[i]))
+      return fail(c, GCDF_ERR_UNKNOWN_ID, "remove id %lld is not live", (long long)rs[i]);
+    if (i > 0 && rs[i] == rs[i - 1]) return fail(c, GCDF_ERR_UNKNOWN_ID, "remove id %lld repeated", (long long)rs[i]);
+  }
+  for (int64_t i = 0; i < 3 * n_add; ++i)
+    if (!std::isfinite(add_xyz[i])) return fail(c, GCDF_ERR_NONFINITE, "non-finite point coordinate at %lld", (long long)i);
+  if (c->opt.scene_capacity - c->n_live < n_add)
+    return fail(c, GCDF_ERR_CAPACITY, "scene capacity %lld exceeded", (long long)c->opt.scene_capacity);
+  // allocate: lowest ids free at the start of the call (removed ids stay live until after)
+  int64_t cur = c->cursor;
+  for (int64_t a = 0; a < n_add; ++a) {
+    while (is_live(c, cur)) {
+      // skip full words quickly
+      if ((cur & 63) == 0 && c->live[cur >> 6] == ~0ull) cur += 64;
+      else ++cur;
+    }
+    out_ids[a] = cur;
+    c->live[cur >> 6] |= 1ull << (cur & 63);
+    ++cur;
+  }
+  c->cursor = cur;
+  for (int64_t i = 0; i < n_rem; ++i) c->live[rs[i] >> 6] &= ~(1ull << (rs[i] & 63));
+  if (n_rem > 0) c->cursor = std::min(c->cursor, rs[0]);
+  c->n_live += n_add - n_rem;
+  for (int64_t a = 0; a < n_add; ++a) c->id_bound = std::max(c->id_bound, out_ids[a] + 1);
+  // device scatter of this rank's share, in pinned chunks
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  float4 *d_pay = reinterpret_cast<float4 *>(c->ws + c->L.upd_payload);
+  int64_t *d_slot = reinterpret_cast<int64_t *>(c->ws + c->L.upd_slots);
+  float4 *pts = reinterpret_cast<float4 *>(c->ws + c->L.pts);
+  int64_t n = 0;
+  auto flush = [&]() -> int {
+    if (n == 0) return GCDF_OK;
+    CK(c, cudaMemcpyAsync(d_pay, c->h_payload, n * 16, cudaMemcpyHostToDevice, s), "scene H2D");
+    CK(c, cudaMemcpyAsync(d_slot, c->h_slots, n * 8, cudaMemcpyHostToDevice, s), "scene H2D");
+    int r = count_launch(c, launch_scene_scatter(d_pay, d_slot, n, pts, s), "scene scatter");
+    if (r) return r;
+    CK(c, cudaEventRecord(c->upd_done, s), "event");
+    CK(c, cudaEventSynchronize(c->upd_done), "scene sync");  // pinned buffer reusable
+    n = 0;
+    return GCDF_OK;
+  };
+  for (int64_t i = 0; i < n_rem; ++i)
+    if (owned(c, rs[i])) {
+      c->h_payload[n] = make_float4(0.f, 0.f, 0.f, 0.f);
+      c->h_slots[n] = local_slot(c, rs[i]);
+      if (++n == kUpdChunk && (rc = flush())) return rc;
+    }
+  for (int64_t a = 0; a < n_add; ++a)
+    if (owned(c, out_ids[a])) {
+      c->h_payload[n] = make_float4(add_xyz[3 * a], add_xyz[3 * a + 1], add_xyz[3 * a + 2], 1.f);
+      c->h_slots[n] = local_slot(c, out_ids[a]);
+      if (++n == kUpdChunk && (rc = flush())) return rc;
+    }
+  return flush();
+}
+
+int gcdf_scene_info(const gcdf_ctx *c, int64_t *n_live, int64_t *id_bound, int64_t *local_bound) {
+  if (!c) return GCDF_ERR_INVALID_ARG;
+  if (n_live) *n_live = c->n_live;
+  if (id_bound) *id_bound = c->id_bound;
+  if (local_bound) *local_bound = local_bound_of(c);
+  return GCDF_OK;
+}
+
+static int check_wp(gcdf_ctx *c, const float *q, int32_t B, int32_t N) {
+  if (!q || B <= 0 || N <= 0) return fail(c, GCDF_ERR_INVALID_ARG, "q must be non-null with B, N > 0");
+  if ((int64_t)B * N > c->opt.max_waypoints)
+    return fail(c, GCDF_ERR_CAPACITY, "B*N = %lld exceeds max_waypoints %d", (long long)B * N, c->opt.max_waypoints);
+  return GCDF_OK;
+}
+
+static QueryArgs make_args(gcdf_ctx *c, const float *q, int32_t nwp) {
+  QueryArgs a{};
+  a.scene = scene_view(c);
+  a.q = q;
+  a.n_wp = nwp;
+  a.tiles_per_wp = (int32_t)(a.scene.local_bound / kTile);
+  a.tgrad = c->opt.tgrad_mode;
+  return a;
+}
+
+static cudaError_t run_mlp(gcdf_ctx *c, const QueryArgs &a, cudaStream_t s) {
+  if ((int64_t)a.n_wp * a.tiles_per_wp == 0) return cudaSuccess;
+  int slot = -1;
+  if (c->prof) {
+    if (c->ev_used == kEvPool && prof_drain(c)) return cudaErrorUnknown;
+    slot = c->ev_used++;
+    cudaEventRecord(c->ev[2 * slot], s);
+  }
+  cudaError_t e = c->opt.precision == GCDF_BF16 ? launch_mlp_tc(c->H, bf16_view(c), a, c->num_sms, s)
+                                                : launch_mlp_simt(c->H, f32_view(c), a, c->num_sms, s);
+  if (slot >= 0) cudaEventRecord(c->ev[2 * slot + 1], s);
+  return e;
+}
+
+int gcdf_profile_enable(gcdf_ctx *c, int enable) {
+  if (!c) return GCDF_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  if (enable && c->ev.empty()) {
+    c->ev.resize(2 * kEvPool);
+    for (auto &e : c->ev) CK(c, cudaEventCreate(&e), "event create");
+  }
+  c->prof = enable != 0;
+  return GCDF_OK;
+}
+
+int gcdf_profile_read(gcdf_ctx *c, double *ms, int64_t *n, int reset) {
+  if (!c) return GCDF_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  int rc = prof_drain(c);
+  if (rc) return rc;
+  if (ms) *ms = c->prof_ms;
+  if (n) *n = c->prof_n;
+  if (reset) { c->prof_ms = 0.0; c->prof_n = 0; }
+  return GCDF_OK;
+}
+
+int gcdf_pairgen_transform(gcdf_ctx *c, const float *q, int32_t B, int32_t N, void *out, void *stream) {
+  int rc = precheck(c, false);
+  if (rc) return rc;
+  if ((rc = check_wp(c, q, B, N))) return rc;
+  if (!out) return fail(c, GCDF_ERR_INVALID_ARG, "null output");
+  SceneView sv = scene_view(c);
+  return count_launch(c, launch_pairgen(sv.pts, sv.local_bound, q, B * N, static_cast<float4 *>(out),
+                                        static_cast<cudaStream_t>(stream)), "pairgen");
+}
+
+int gcdf_query_values_grads(gcdf_ctx *c, const float *q, int32_t B, int32_t N, float *values, float *grads,
+                            void *stream) {
+  int rc = precheck(c);
+  if (rc) return rc;
+  if ((rc = check_wp(c, q, B, N))) return rc;
+  if (!values) return fail(c, GCDF_ERR_INVALID_ARG, "null values output");
+  QueryArgs a = make_args(c, q, B * N);
+  a.values = values;
+  a.grads = grads;
+  a.detect = 0;
+  return count_launch(c, run_mlp(c, a, static_cast<cudaStream_t>(stream)), "query kernel");
+}
+
+static int finish_detect(gcdf_ctx *c, int32_t nwp, int32_t tpw, gcdf_active_t *out, int64_t cap, int64_t *offs,
+                         float *wmin, int64_t *warg, int64_t *wkey, int64_t *count_dev, int64_t *count_host,
+                         cudaStream_t s) {
+  DetectScratch ds = scratch_view(c);
+  int nl = 0;
+  cudaError_t e = launch_finalize(ds, nwp, tpw, out, cap, offs, wmin, warg, wkey, count_dev,
+                                  reinterpret_cast<int64_t *>(c->ws + c->L.wp_count), s, &nl);
+  int rc = count_launch(c, e, "detect finalize", nl);
+  if (rc) return rc;
+  if (count_host) {
+    unsigned long long hc[2];
+    CK(c, cudaMemcpyAsync(hc, ds.counter, 16, cudaMemcpyDeviceToHost, s), "count D2H");
+    CK(c, cudaStreamSynchronize(s), "detect sync");
+    *count_host = (int64_t)hc[0];
+    if (hc[1] || (int64_t)hc[0] > cap)
+      return fail(c, GCDF_ERR_CAPACITY, "active count %lld exceeds output capacity %lld or staging %lld",
+                  (long long)hc[0], (long long)cap, (long long)c->opt.max_active);
+  }
+  return GCDF_OK;
+}
+
+int gcdf_detect_active_set(gcdf_ctx *c, const float *q, int32_t B, int32_t N, float delta, float tau,
+                           gcdf_active_t *out, int64_t cap, int64_t *offs, float *wmin, int64_t *warg,
+                           int64_t *wkey, int64_t *count_dev, int64_t *count_host, void *stream) {
+  int rc = precheck(c);
+  if (rc) return rc;
+  if ((rc = check_wp(c, q, B, N))) return rc;
+  if (!out || cap < 0 || !offs || !count_dev || !std::isfinite(delta) || !std::isfinite(tau))
+    return fail(c, GCDF_ERR_INVALID_ARG, "detect: null output or non-finite delta/tau");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  QueryArgs a = make_args(c, q, B * N);
+  a.detect = 1;
+  a.delta = delta;
+  a.tau = tau;
+  a.ds = scratch_view(c);
+  if ((rc = count_launch(c, launch_detect_init(a.ds, a.n_wp, s), "detect init"))) return rc;
+  if ((rc = count_launch(c, run_mlp(c, a, s), "detect kernel"))) return rc;
+  return finish_detect(c, a.n_wp, a.tiles_per_wp, out, cap, offs, wmin, warg, wkey, count_dev, count_host, s);
+}
+
+int gcdf_compact_dense(gcdf_ctx *c, const float *values, const float *grads, int32_t n_wp, int64_t stride,
+                       float delta, float tau, gcdf_active_t *out, int64_t cap, int64_t *offs, float *wmin,
+                       int64_t *warg, int64_t *wkey, int64_t *count_dev, int64_t *count_host, void *stream) {
+  int rc = precheck(c, false);
+  if (rc) return rc;
+  SceneView sv = scene_view(c);
+  if (!values || !grads || n_wp <= 0 || n_wp > c->opt.max_waypoints || stride < sv.local_bound || !out || !offs ||
+      !count_dev || !std::isfinite(delta) || !std::isfinite(tau))
+    return fail(c, GCDF_ERR_INVALID_ARG, "compact_dense: bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DetectScratch ds = scratch_view(c);
+  const int32_t tpw = (int32_t)(sv.local_bound / kTile);
+  if ((rc = count_launch(c, launch_detect_init(ds, n_wp, s), "compact init"))) return rc;
+  if ((rc = count_launch(c, launch_compact_dense(values, grads, stride, n_wp, tpw, sv, delta, tau, ds, s),
+                         "compact kernel")))
+    return rc;
+  return finish_detect(c, n_wp, tpw, out, cap, offs, wmin, warg, wkey, count_dev, count_host, s);
+}
+
+int gcdf_merge_active_sets(gcdf_ctx *c, int32_t world, int32_t n_wp, const gcdf_active_t *recs, int64_t rec_stride,
+                           const int64_t *offsets, const int64_t *wp_key, gcdf_active_t *out, int64_t cap,
+                           int64_t *offs, float *wmin, int64_t *warg, int64_t *count, void *stream) {
+  int rc = precheck(c, false);
+  if (rc) return rc;
+  if (world < 1 || n_wp <= 0 || !recs || rec_stride < 0 || !offsets || !wp_key || !out || !offs || !count)
+    return fail(c, GCDF_ERR_INVALID_ARG, "merge: bad arguments");
+  int nl = 0;
+  cudaError_t e = launch_merge(world, n_wp, recs, rec_stride, offsets, wp_key, out, cap, offs, wmin, warg, count,
+                               static_cast<cudaStream_t>(stream), &nl);
+  return count_launch(c, e, "merge", nl);
+}
+
+}  // extern "C"

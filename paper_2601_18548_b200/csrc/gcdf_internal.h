@@ -1,0 +1,106 @@
+// gcdf_internal.h -- private types shared by the host layer and the sm_100a kernels.
+// Nothing here is visible through the C ABI (include/gcdf.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gcdf.h"
+
+namespace gcdf {
+
+constexpr int kNdof = 9;      // q = [x, y, theta, j1..j6]
+constexpr int kNin = 12;      // MLP input 3 + n
+constexpr int kTile = 128;    // pairs per tile = 1 waypoint x 128 consecutive local slots
+constexpr int kHidden = 6;    // hidden (ReLU) layers of the 7-layer MLP (R7)
+
+// fp32 weight block (SIMT path).  Hidden layer li = 0..4 is the paper's layer l = li + 2.
+//   w1p[u]        = {W1[u][0], W1[u][1], W1[u][2], b1[u]}          (layer 1, point columns)
+//   w1q[u][8]     = W1[u][5..11], 0                                 (layer 1, q^r columns)
+//   w1full[u][12] = W1[u][0..11]                                    (layer-1 backward)
+//   wt[li][k][tu][i] = W[tu + 16 i][k]   (forward  B operand, units interleaved by 16)
+//   wb[li][k][tu][i] = W[k][tu + 16 i]   (backward B operand)
+//   bias[li][u], w7[u], b7
+struct WeightsF32 {
+  const float4 *w1p;
+  const float *w1q;
+  const float *w1full;
+  const float *wt[5];
+  const float *wb[5];
+  const float *bias[5];
+  const float *w7;
+  float b7;
+};
+
+// bf16 weight block (tcgen05 path): hidden W_l (l = 2..6) as [out][in] bf16 in the UMMA
+// canonical SWIZZLE_128B layout: two 64-column chunks of [H rows][128 B], 16-B granule g
+// of row r stored at granule g ^ (r % 8).  The same bytes serve as a K-major B operand
+// (forward, N = out, K = in) and an MN-major B operand (backward, N = in, K = out).
+// w1t: W1^T restricted to the 12 input columns, padded to N = 16 rows, K-major SW128.
+struct WeightsBF16 {
+  const void *w_sw128;   // 5 * H * H * 2 bytes
+  const void *w1t_sw128; // 16 * H * 2 bytes
+  const float4 *w1p;     // fp32, as WeightsF32
+  const float *w1q;
+  const float *bias;     // [5][H] fp32
+  const float *w7;       // [H] fp32
+  float b7;
+};
+
+struct SceneView {
+  const float4 *pts;     // [local_cap] (x, y, z, live)
+  int64_t local_bound;   // multiple of 128
+  int32_t rank, world;
+};
+
+// Detect scratch (in the bound workspace).
+struct DetectScratch {
+  int2 *tile_meta;                 // [n_wp * tiles_per_wp] (staging base, count)
+  gcdf_active_t *staging;          // [max_active]
+  int64_t max_active;
+  unsigned long long *counter;     // [2]: staging allocation counter, overflow flag
+  unsigned long long *wp_key;      // [max_waypoints] unsigned order key, ~0 = none
+};
+
+struct QueryArgs {
+  SceneView scene;
+  const float *q;                  // [n_wp][9]
+  int32_t n_wp;
+  int32_t tiles_per_wp;
+  int32_t tgrad;                   // gcdf_tgrad
+  // dense outputs (query) -- NULL in detect mode
+  float *values;
+  float *grads;
+  // detect mode
+  int32_t detect;
+  float delta, tau;
+  DetectScratch ds;
+};
+
+__host__ __device__ inline int64_t local_to_global(int64_t slot, int rank, int world) {
+  return ((slot / kTile) * world + rank) * kTile + slot % kTile;
+}
+
+// ---- launchers (return cudaError_t of the launch) ----
+cudaError_t launch_scene_scatter(const float4 *payload, const int64_t *slots, int64_t n, float4 *pts,
+                                 cudaStream_t s);
+cudaError_t launch_fill(float4 *pts, int64_t n, cudaStream_t s);
+cudaError_t launch_pairgen(const float4 *pts, int64_t local_bound, const float *q, int32_t n_wp,
+                           float4 *out, cudaStream_t s);
+cudaError_t launch_detect_init(DetectScratch ds, int32_t n_wp, cudaStream_t s);
+cudaError_t launch_mlp_simt(int H, const WeightsF32 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
+cudaError_t launch_mlp_tc(int H, const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
+bool tc_compiled();
+cudaError_t launch_compact_dense(const float *values, const float *grads, int64_t stride, int32_t n_wp,
+                                 int32_t tiles_per_wp, SceneView scene, float delta, float tau,
+                                 DetectScratch ds, cudaStream_t s);
+// finalize: tile counts -> wp_offsets, ordered copy staging -> out, wp_min/argmin/key, count
+cudaError_t launch_finalize(DetectScratch ds, int32_t n_wp, int32_t tiles_per_wp, gcdf_active_t *out,
+                            int64_t out_capacity, int64_t *wp_offsets, float *wp_min, int64_t *wp_argmin,
+                            int64_t *wp_key, int64_t *count, int64_t *wp_count_scratch, cudaStream_t s,
+                            int *n_launches);
+cudaError_t launch_merge(int32_t world, int32_t n_wp, const gcdf_active_t *recs, int64_t rec_stride,
+                         const int64_t *offsets, const int64_t *wp_key, gcdf_active_t *out,
+                         int64_t out_capacity, int64_t *wp_offsets, float *wp_min, int64_t *wp_argmin,
+                         int64_t *count, cudaStream_t s, int *n_launches);
+
+}  // namespace gcdf

@@ -1,0 +1,283 @@
+// k_compact.cu -- K3: threshold + per-waypoint min + stream compaction (A6-A8), the
+// finalize pass that turns per-tile staging into the canonical (wp, pt) order, and the
+// multi-rank merge of gathered active sets.
+//
+// Paper: constraint f - delta >= 0, active test R12; union = min
+// (PAPER.md:164); c_gcdf "indexed by time step" (Eq. 14).
+//
+// Min keys: key = ord(f) << 32 | pt, ord() order-preserving float -> uint32, so the
+// unsigned minimum is (min f, smallest id on ties) -- one atomicMin per tile.
+#include "gcdf_internal.h"
+
+namespace gcdf {
+namespace {
+
+__device__ __forceinline__ unsigned ord_f32(float f) {
+  unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float unord_f32(unsigned o) {
+  return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+}
+
+__global__ void k_detect_init(unsigned long long *wp_key, unsigned long long *counter, int32_t n_wp) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_wp; i += gridDim.x * blockDim.x) wp_key[i] = ~0ull;
+  if (blockIdx.x == 0 && threadIdx.x < 2) counter[threadIdx.x] = 0ull;
+}
+
+// exclusive scan of v over the block (blockDim.x multiple of 32, <= 1024)
+__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t *total, int64_t *sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t s = lane < nw ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < nw) sh[lane] = s;  // inclusive prefix of warp totals
+  }
+  __syncthreads();
+  const int64_t res = x - v + (warp > 0 ? sh[warp - 1] : 0);
+  *total = sh[nw - 1];
+  __syncthreads();
+  return res;
+}
+
+// K3 standalone over dense values: one CTA (128 threads) per tile of 128 slots.
+__global__ void __launch_bounds__(128) k_compact_dense(const float *__restrict__ values,
+                                                      const float *__restrict__ grads, int64_t stride,
+                                                      int32_t n_wp, int32_t tpw, SceneView scene, float delta,
+                                                      float tau, DetectScratch ds) {
+  __shared__ unsigned actw[4];
+  __shared__ unsigned long long kmin[4];
+  __shared__ int sbase;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n_tiles = (int64_t)n_wp * tpw;
+  for (int64_t T = blockIdx.x; T < n_tiles; T += gridDim.x) {
+    const int w = (int)(T / tpw);
+    const int64_t slot = (T % tpw) * kTile + tid;
+    const bool inb = slot < scene.local_bound;
+    const bool live = inb && __ldg(&scene.pts[slot].w) > 0.f;
+    const float f = inb ? __ldcs(values + (int64_t)w * stride + slot) : 0.f;
+    const bool act = live && (f - delta <= tau);
+    const unsigned bal = __ballot_sync(0xffffffffu, act);
+    unsigned long long key = ~0ull;
+    if (live) key = ((unsigned long long)ord_f32(f) << 32) | (unsigned long long)local_to_global(slot, scene.rank, scene.world);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+      key = other < key ? other : key;
+    }
+    if (lane == 0) { actw[warp] = bal; kmin[warp] = key; }
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long km = kmin[0];
+      int cnt = 0;
+      for (int i = 0; i < 4; ++i) { km = kmin[i] < km ? kmin[i] : km; cnt += __popc(actw[i]); }
+      if (km != ~0ull) atomicMin(ds.wp_key + w, km);
+      int base = 0;
+      if (cnt > 0) {
+        unsigned long long b = atomicAdd(ds.counter, (unsigned long long)cnt);
+        if (b + cnt > (unsigned long long)ds.max_active) { atomicOr(ds.counter + 1, 1ull); base = -1; }
+        else base = (int)b;
+      }
+      sbase = base;
+      ds.tile_meta[T] = make_int2(base, cnt);
+    }
+    __syncthreads();
+    if (act && sbase >= 0) {
+      int r = __popc(bal & ((1u << lane) - 1u));
+      for (int i = 0; i < warp; ++i) r += __popc(actw[i]);
+      const float *g = grads + ((int64_t)w * stride + slot) * kNdof;
+      float4 *dst = reinterpret_cast<float4 *>(ds.staging + sbase + r);
+      dst[0] = make_float4(f, g[0], g[1], g[2]);
+      dst[1] = make_float4(g[3], g[4], g[5], g[6]);
+      dst[2] = make_float4(g[7], g[8], __uint_as_float((unsigned)w),
+                           __uint_as_float((unsigned)local_to_global(slot, scene.rank, scene.world)));
+    }
+    __syncthreads();
+  }
+}
+
+// per-waypoint active counts from the tile meta
+__global__ void __launch_bounds__(256) k_wp_count(const int2 *__restrict__ meta, int32_t tpw,
+                                                  int64_t *__restrict__ wp_count) {
+  __shared__ int64_t sh[32];
+  const int w = blockIdx.x;
+  int64_t s = 0;
+  for (int t = threadIdx.x; t < tpw; t += blockDim.x) s += meta[(int64_t)w * tpw + t].y;
+  int64_t tot;
+  block_excl_scan(s, &tot, sh);
+  if (threadIdx.x == 0) wp_count[w] = tot;
+}
+
+// exclusive scan over waypoints + min/argmin/key export (single CTA)
+__global__ void __launch_bounds__(1024) k_wp_scan(const int64_t *__restrict__ wp_count, int32_t n_wp,
+                                                  int64_t *__restrict__ wp_offsets, int64_t *__restrict__ count,
+                                                  const unsigned long long *__restrict__ keys, float *wp_min,
+                                                  int64_t *wp_argmin, int64_t *wp_key_out) {
+  __shared__ int64_t sh[32];
+  int64_t carry = 0;
+  for (int base = 0; base < n_wp; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int64_t v = i < n_wp ? wp_count[i] : 0;
+    int64_t tot;
+    const int64_t ex = block_excl_scan(v, &tot, sh);
+    if (i < n_wp) wp_offsets[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    wp_offsets[n_wp] = carry;
+    *count = carry;
+  }
+  if (keys) {
+    for (int i = threadIdx.x; i < n_wp; i += blockDim.x) {
+      const unsigned long long k = keys[i];
+      if (wp_min) wp_min[i] = k == ~0ull ? __int_as_float(0x7f800000) : unord_f32((unsigned)(k >> 32));
+      if (wp_argmin) wp_argmin[i] = k == ~0ull ? -1 : (int64_t)(k & 0xffffffffull);
+      if (wp_key_out) wp_key_out[i] = (int64_t)(k ^ 0x8000000000000000ull);
+    }
+  }
+}
+
+// ordered copy staging -> out: one CTA per waypoint, tiles scanned in order
+__global__ void __launch_bounds__(256) k_wp_scatter(const int2 *__restrict__ meta, int32_t tpw,
+                                                    const gcdf_active_t *__restrict__ staging,
+                                                    const int64_t *__restrict__ wp_offsets,
+                                                    gcdf_active_t *__restrict__ out, int64_t cap) {
+  __shared__ int64_t sh[32];
+  const int w = blockIdx.x;
+  int64_t carry = wp_offsets[w];
+  for (int t0 = 0; t0 < tpw; t0 += blockDim.x) {
+    const int t = t0 + threadIdx.x;
+    int2 m = make_int2(0, 0);
+    if (t < tpw) m = meta[(int64_t)w * tpw + t];
+    int64_t tot;
+    const int64_t ex = block_excl_scan(m.y, &tot, sh);
+    if (m.y > 0 && m.x >= 0) {
+      const float4 *src = reinterpret_cast<const float4 *>(staging + m.x);
+      for (int k = 0; k < m.y; ++k) {
+        const int64_t o = carry + ex + k;
+        if (o < cap) {
+          float4 *dst = reinterpret_cast<float4 *>(out + o);
+          dst[0] = src[3 * k];
+          dst[1] = src[3 * k + 1];
+          dst[2] = src[3 * k + 2];
+        }
+      }
+    }
+    carry += tot;
+  }
+}
+
+// ---- multi-rank merge ----
+__global__ void k_merge_offsets(int32_t world, int32_t n_wp, const int64_t *__restrict__ offsets,
+                                int64_t *__restrict__ wp_offsets, int64_t *__restrict__ count) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w <= n_wp; w += gridDim.x * blockDim.x) {
+    int64_t s = 0;
+    for (int r = 0; r < world; ++r) s += offsets[(int64_t)r * (n_wp + 1) + w];
+    wp_offsets[w] = s;
+    if (w == n_wp) *count = s;
+  }
+}
+
+__global__ void k_merge_records(int32_t world, int32_t n_wp, const gcdf_active_t *__restrict__ recs,
+                                int64_t rec_stride, const int64_t *__restrict__ offsets,
+                                const int64_t *__restrict__ wp_offsets, gcdf_active_t *__restrict__ out,
+                                int64_t cap) {
+  const int r = blockIdx.y;
+  const int64_t *off = offsets + (int64_t)r * (n_wp + 1);
+  const int64_t n = off[n_wp];
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    // waypoint of record k: last w with off[w] <= k
+    int lo = 0, hi = n_wp - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (off[mid] <= k) lo = mid; else hi = mid - 1;
+    }
+    const int w = lo;
+    const gcdf_active_t rec = recs[(int64_t)r * rec_stride + k];
+    int64_t pos = wp_offsets[w] + (k - off[w]);
+    for (int s = 0; s < world; ++s) {
+      if (s == r) continue;
+      const int64_t *os = offsets + (int64_t)s * (n_wp + 1);
+      int64_t a = os[w], b = os[w + 1];  // count records of rank s in wp w with pt < rec.pt
+      const gcdf_active_t *rs = recs + (int64_t)s * rec_stride;
+      while (a < b) {
+        const int64_t mid = (a + b) >> 1;
+        if (rs[mid].pt < rec.pt) a = mid + 1; else b = mid;
+      }
+      pos += a - os[w];
+    }
+    if (pos < cap) out[pos] = rec;
+  }
+}
+
+__global__ void k_keys_export(const int64_t *__restrict__ skeys, int32_t n_wp, float *wp_min, int64_t *wp_argmin) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_wp; i += gridDim.x * blockDim.x) {
+    const unsigned long long k = (unsigned long long)skeys[i] ^ 0x8000000000000000ull;
+    if (wp_min) wp_min[i] = k == ~0ull ? __int_as_float(0x7f800000) : unord_f32((unsigned)(k >> 32));
+    if (wp_argmin) wp_argmin[i] = k == ~0ull ? -1 : (int64_t)(k & 0xffffffffull);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_detect_init(DetectScratch ds, int32_t n_wp, cudaStream_t s) {
+  int grid = (n_wp + 255) / 256;
+  if (grid < 1) grid = 1;
+  k_detect_init<<<grid, 256, 0, s>>>(ds.wp_key, ds.counter, n_wp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact_dense(const float *values, const float *grads, int64_t stride, int32_t n_wp,
+                                 int32_t tiles_per_wp, SceneView scene, float delta, float tau,
+                                 DetectScratch ds, cudaStream_t s) {
+  const int64_t n_tiles = (int64_t)n_wp * tiles_per_wp;
+  if (n_tiles <= 0) return cudaSuccess;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t grid = n_tiles < (int64_t)sms * 16 ? n_tiles : (int64_t)sms * 16;
+  k_compact_dense<<<(unsigned)grid, 128, 0, s>>>(values, grads, stride, n_wp, tiles_per_wp, scene, delta, tau, ds);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(DetectScratch ds, int32_t n_wp, int32_t tiles_per_wp, gcdf_active_t *out,
+                            int64_t out_capacity, int64_t *wp_offsets, float *wp_min, int64_t *wp_argmin,
+                            int64_t *wp_key, int64_t *count, int64_t *wp_count_scratch, cudaStream_t s,
+                            int *n_launches) {
+  if (n_wp <= 0) return cudaSuccess;
+  k_wp_count<<<n_wp, 256, 0, s>>>(ds.tile_meta, tiles_per_wp, wp_count_scratch);
+  k_wp_scan<<<1, 1024, 0, s>>>(wp_count_scratch, n_wp, wp_offsets, count, ds.wp_key, wp_min, wp_argmin, wp_key);
+  k_wp_scatter<<<n_wp, 256, 0, s>>>(ds.tile_meta, tiles_per_wp, ds.staging, wp_offsets, out, out_capacity);
+  *n_launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge(int32_t world, int32_t n_wp, const gcdf_active_t *recs, int64_t rec_stride,
+                         const int64_t *offsets, const int64_t *wp_key, gcdf_active_t *out, int64_t out_capacity,
+                         int64_t *wp_offsets, float *wp_min, int64_t *wp_argmin, int64_t *count, cudaStream_t s,
+                         int *n_launches) {
+  int g = (n_wp + 1 + 255) / 256;
+  k_merge_offsets<<<g, 256, 0, s>>>(world, n_wp, offsets, wp_offsets, count);
+  int gx = (int)((rec_stride + 255) / 256);
+  if (gx > 2048) gx = 2048;
+  if (gx < 1) gx = 1;
+  k_merge_records<<<dim3(gx, world), 256, 0, s>>>(world, n_wp, recs, rec_stride, offsets, wp_offsets, out,
+                                                   out_capacity);
+  k_keys_export<<<(n_wp + 255) / 256 > 0 ? (n_wp + 255) / 256 : 1, 256, 0, s>>>(wp_key, n_wp, wp_min, wp_argmin);
+  *n_launches += 3;
+  return cudaGetLastError();
+}
+
+}  // namespace gcdf

@@ -1,0 +1,243 @@
+"""Thin ctypes binding of libgcdf (include/gcdf.h).  Argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels; torch supplies device
+memory (output tensors, the workspace) and the current CUDA stream.  There is no CPU
+path: if libgcdf.so is missing or no B200 is present, construction raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+import torch
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libgcdf.so"
+
+FP32, BF16 = 0, 1
+TGRAD_CHAINRULE, TGRAD_QCHANNEL = 0, 1
+STATUS = {0: "OK", -1: "INVALID_ARG", -2: "IO", -3: "BAD_MAGIC", -4: "VERSION", -5: "DIM_MISMATCH",
+          -6: "NOT_LOADED", -7: "CAPACITY", -8: "UNKNOWN_ID", -9: "NONFINITE", -10: "CUDA",
+          -11: "UNSUPPORTED"}
+REC_BYTES = 48  # sizeof(gcdf_active_t)
+
+EXPORTED = ["gcdf_default_options", "gcdf_create", "gcdf_destroy", "gcdf_last_error", "gcdf_has_tcgen05",
+            "gcdf_workspace_bytes", "gcdf_bind_workspace", "gcdf_load_weights", "gcdf_update_scene",
+            "gcdf_scene_info", "gcdf_pairgen_transform", "gcdf_query_values_grads", "gcdf_detect_active_set",
+            "gcdf_compact_dense", "gcdf_merge_active_sets", "gcdf_launch_count", "gcdf_profile_enable",
+            "gcdf_profile_read"]
+
+
+class GcdfError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        self.code = code
+        self.name = STATUS.get(code, str(code))
+        super().__init__(f"gcdf {self.name}: {msg}")
+
+
+class Options(C.Structure):
+    _fields_ = [("precision", C.c_int32), ("tgrad_mode", C.c_int32), ("scene_capacity", C.c_int64),
+                ("max_waypoints", C.c_int32), ("max_active", C.c_int64), ("rank", C.c_int32),
+                ("world", C.c_int32)]
+
+
+_lib = None
+
+
+def load_library(path: str | Path = LIB_PATH):
+    """Load libgcdf.so (raises if it has not been built: no fallback exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not Path(path).exists():
+        raise ImportError(f"{path} not built: run `python -m paper_2601_18548_b200.build` (nvcc, sm_100a)")
+    lib = C.CDLL(str(path))
+    P, I32, I64, F = C.c_void_p, C.c_int32, C.c_int64, C.c_float
+    PI64 = C.POINTER(C.c_int64)
+    lib.gcdf_default_options.argtypes = [C.POINTER(Options)]
+    lib.gcdf_default_options.restype = None
+    lib.gcdf_create.argtypes = [C.c_int, C.POINTER(Options), C.POINTER(P)]
+    lib.gcdf_destroy.argtypes = [P]
+    lib.gcdf_last_error.argtypes = [P]
+    lib.gcdf_last_error.restype = C.c_char_p
+    lib.gcdf_has_tcgen05.argtypes = []
+    lib.gcdf_workspace_bytes.argtypes = [P, PI64]
+    lib.gcdf_bind_workspace.argtypes = [P, P, I64]
+    lib.gcdf_load_weights.argtypes = [P, C.c_char_p, P]
+    lib.gcdf_update_scene.argtypes = [P, P, I64, P, P, I64, P]
+    lib.gcdf_scene_info.argtypes = [P, PI64, PI64, PI64]
+    lib.gcdf_pairgen_transform.argtypes = [P, P, I32, I32, P, P]
+    lib.gcdf_query_values_grads.argtypes = [P, P, I32, I32, P, P, P]
+    lib.gcdf_detect_active_set.argtypes = [P, P, I32, I32, F, F, P, I64, P, P, P, P, P, P, P]
+    lib.gcdf_compact_dense.argtypes = [P, P, P, I32, I64, F, F, P, I64, P, P, P, P, P, P, P]
+    lib.gcdf_merge_active_sets.argtypes = [P, I32, I32, P, I64, P, P, P, I64, P, P, P, P, P]
+    lib.gcdf_launch_count.argtypes = [P]
+    lib.gcdf_launch_count.restype = I64
+    lib.gcdf_profile_enable.argtypes = [P, C.c_int]
+    lib.gcdf_profile_read.argtypes = [P, C.POINTER(C.c_double), PI64, C.c_int]
+    _lib = lib
+    return lib
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(device):
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def records_to_dict(rec: torch.Tensor, n: int) -> dict:
+    """View [n] gcdf_active_t records (uint8 [cap, 48]) as value / grad / wp / pt tensors."""
+    r = rec[:n].view(torch.int32).view(n, 12) if n > 0 else rec.new_zeros((0, 12), dtype=torch.int32)
+    f = r.view(torch.float32)
+    return {"value": f[:, 0], "grad": f[:, 1:10], "wp": r[:, 10].to(torch.int64) & 0xFFFFFFFF,
+            "pt": r[:, 11].to(torch.int64) & 0xFFFFFFFF}
+
+
+class Context:
+    """One libgcdf context on one CUDA device (one rank)."""
+
+    def __init__(self, device: int = 0, precision: int = BF16, tgrad_mode: int = TGRAD_CHAINRULE,
+                 scene_capacity: int = 1 << 20, max_waypoints: int = 256, max_active: int = 1 << 22,
+                 rank: int = 0, world: int = 1):
+        self.lib = load_library()
+        if not torch.cuda.is_available():
+            raise RuntimeError("libgcdf needs a CUDA device (B200); no CPU path exists")
+        self.device = torch.device("cuda", device)
+        o = Options()
+        self.lib.gcdf_default_options(C.byref(o))
+        o.precision, o.tgrad_mode, o.scene_capacity = precision, tgrad_mode, scene_capacity
+        o.max_waypoints, o.max_active, o.rank, o.world = max_waypoints, max_active, rank, world
+        self.opts = o
+        h = C.c_void_p()
+        rc = self.lib.gcdf_create(device, C.byref(o), C.byref(h))
+        if rc:
+            raise GcdfError(rc, "gcdf_create failed (needs an sm_100 device; bf16 needs the tcgen05 build)")
+        self._h = h
+        nb = C.c_int64()
+        self._check(self.lib.gcdf_workspace_bytes(h, C.byref(nb)))
+        self.workspace = torch.empty(int(nb.value), dtype=torch.uint8, device=self.device)
+        self._check(self.lib.gcdf_bind_workspace(h, _ptr(self.workspace), int(nb.value)))
+        self.max_active = max_active
+        self.rank, self.world = rank, world
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.gcdf_destroy(h)
+            self._h = None
+
+    def _check(self, rc):
+        if rc:
+            raise GcdfError(rc, self.lib.gcdf_last_error(self._h).decode(errors="replace"))
+        return rc
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.gcdf_launch_count(self._h))
+
+    def profile_enable(self, on: bool = True) -> None:
+        self._check(self.lib.gcdf_profile_enable(self._h, int(on)))
+
+    def profile_read(self, reset: bool = True):
+        ms, n = C.c_double(), C.c_int64()
+        self._check(self.lib.gcdf_profile_read(self._h, C.byref(ms), C.byref(n), int(reset)))
+        return ms.value, n.value
+
+    # -------------------------------------------------------------- weights / scene
+    def load_weights(self, path) -> None:
+        self._check(self.lib.gcdf_load_weights(self._h, str(path).encode(), _stream(self.device)))
+
+    def update_scene(self, add_xyz=None, remove_ids=None) -> np.ndarray:
+        add = np.ascontiguousarray(np.zeros((0, 3)) if add_xyz is None else add_xyz, dtype=np.float32).reshape(-1, 3)
+        rem = np.ascontiguousarray(np.zeros(0) if remove_ids is None else remove_ids, dtype=np.int64).ravel()
+        ids = np.empty(add.shape[0], dtype=np.int64)
+        self._check(self.lib.gcdf_update_scene(self._h, add.ctypes.data_as(C.c_void_p), add.shape[0],
+                                               ids.ctypes.data_as(C.c_void_p), rem.ctypes.data_as(C.c_void_p),
+                                               rem.shape[0], _stream(self.device)))
+        return ids
+
+    def scene_info(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(self.lib.gcdf_scene_info(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return {"n_live": a.value, "id_bound": b.value, "local_bound": c.value}
+
+    def local_to_global(self, slots: torch.Tensor) -> torch.Tensor:
+        return ((slots // 128) * self.world + self.rank) * 128 + slots % 128
+
+    # -------------------------------------------------------------- hot path
+    def _q(self, q: torch.Tensor):
+        if q.dim() != 3 or q.shape[2] != 9:
+            raise ValueError("q must be [B, N, 9]")
+        q = q.to(device=self.device, dtype=torch.float32).contiguous()
+        return q, int(q.shape[0]), int(q.shape[1])
+
+    def pairgen_transform(self, q: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        q, B, N = self._q(q)
+        lb = self.scene_info()["local_bound"]
+        if out is None:
+            out = torch.empty((B * N, lb, 4), dtype=torch.float32, device=self.device)
+        self._check(self.lib.gcdf_pairgen_transform(self._h, _ptr(q), B, N, _ptr(out), _stream(self.device)))
+        return out
+
+    def query_values_grads(self, q: torch.Tensor, want_grads: bool = True, values=None, grads=None):
+        q, B, N = self._q(q)
+        lb = self.scene_info()["local_bound"]
+        if values is None:
+            values = torch.empty((B * N, lb), dtype=torch.float32, device=self.device)
+        if want_grads and grads is None:
+            grads = torch.empty((B * N, lb, 9), dtype=torch.float32, device=self.device)
+        self._check(self.lib.gcdf_query_values_grads(self._h, _ptr(q), B, N, _ptr(values),
+                                                     _ptr(grads) if want_grads else None, _stream(self.device)))
+        return values, (grads if want_grads else None)
+
+    def alloc_detect_outputs(self, n_wp: int, capacity: int):
+        d = self.device
+        return {"records": torch.empty((max(capacity, 1), REC_BYTES), dtype=torch.uint8, device=d),
+                "wp_offsets": torch.empty(n_wp + 1, dtype=torch.int64, device=d),
+                "wp_min": torch.empty(n_wp, dtype=torch.float32, device=d),
+                "wp_argmin": torch.empty(n_wp, dtype=torch.int64, device=d),
+                "wp_key": torch.empty(n_wp, dtype=torch.int64, device=d),
+                "count": torch.empty(1, dtype=torch.int64, device=d), "capacity": capacity}
+
+    def detect_active_set(self, q: torch.Tensor, delta: float, tau: float, capacity: int | None = None,
+                          outputs: dict | None = None, sync_count: bool = True):
+        """Fused detect.  Returns the output dict (+ 'n' = host count when sync_count)."""
+        q, B, N = self._q(q)
+        if outputs is None:
+            outputs = self.alloc_detect_outputs(B * N, capacity if capacity is not None else self.max_active)
+        o = outputs
+        nh = C.c_int64(-1)
+        self._check(self.lib.gcdf_detect_active_set(
+            self._h, _ptr(q), B, N, float(delta), float(tau), _ptr(o["records"]), int(o["capacity"]),
+            _ptr(o["wp_offsets"]), _ptr(o["wp_min"]), _ptr(o["wp_argmin"]), _ptr(o["wp_key"]), _ptr(o["count"]),
+            C.byref(nh) if sync_count else None, _stream(self.device)))
+        if sync_count:
+            o["n"] = nh.value
+        return o
+
+    def compact_dense(self, values: torch.Tensor, grads: torch.Tensor, delta: float, tau: float,
+                      capacity: int | None = None, outputs: dict | None = None):
+        n_wp, stride = int(values.shape[0]), int(values.shape[1])
+        if outputs is None:
+            outputs = self.alloc_detect_outputs(n_wp, capacity if capacity is not None else self.max_active)
+        o = outputs
+        nh = C.c_int64(-1)
+        self._check(self.lib.gcdf_compact_dense(
+            self._h, _ptr(values), _ptr(grads), n_wp, stride, float(delta), float(tau), _ptr(o["records"]),
+            int(o["capacity"]), _ptr(o["wp_offsets"]), _ptr(o["wp_min"]), _ptr(o["wp_argmin"]), _ptr(o["wp_key"]),
+            _ptr(o["count"]), C.byref(nh), _stream(self.device)))
+        o["n"] = nh.value
+        return o
+
+    def merge_active_sets(self, world: int, n_wp: int, recs: torch.Tensor, rec_stride: int,
+                          offsets: torch.Tensor, wp_key: torch.Tensor, capacity: int):
+        o = self.alloc_detect_outputs(n_wp, capacity)
+        self._check(self.lib.gcdf_merge_active_sets(
+            self._h, world, n_wp, _ptr(recs), rec_stride, _ptr(offsets), _ptr(wp_key), _ptr(o["records"]),
+            capacity, _ptr(o["wp_offsets"]), _ptr(o["wp_min"]), _ptr(o["wp_argmin"]), _ptr(o["count"]),
+            _stream(self.device)))
+        o["wp_key"] = wp_key
+        return o
