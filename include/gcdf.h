@@ -58,7 +58,10 @@ enum gcdf_status {
 
 enum gcdf_precision {
   GCDF_FP32 = 0, /* fp32 SIMT path: parity path, tolerance 1e-4 rel / 1e-5 abs */
-  GCDF_BF16 = 1  /* tcgen05 tensor-core path: bf16 operands, fp32 accumulate */
+  GCDF_BF16 = 1, /* tcgen05 tensor-core path, bf16 operands, fp32 accumulate */
+  GCDF_FP16 = 2  /* tcgen05 tensor-core path, fp16 operands, fp32 accumulate: same tensor peak as
+                    bf16 with 3 more significand bits; meets the north-star tensor-path tolerance
+                    (R17, §5); the default */
 };
 
 enum gcdf_tgrad {
@@ -67,7 +70,7 @@ enum gcdf_tgrad {
 };
 
 typedef struct {
-  int32_t precision;       /* gcdf_precision (default GCDF_BF16 if the device supports it) */
+  int32_t precision;       /* gcdf_precision (default GCDF_FP16) */
   int32_t tgrad_mode;      /* gcdf_tgrad */
   int64_t scene_capacity;  /* global id space [0, scene_capacity) of obstacle points */
   int32_t max_waypoints;   /* largest B*N accepted by query/detect */
@@ -85,7 +88,7 @@ typedef struct {
 } gcdf_active_t;
 
 /* ------------------------------------------------------------------ lifecycle */
-/* Fills *opt with defaults (precision BF16, chain rule, capacity 1<<20, 256 waypoints,
+/* Fills *opt with defaults (precision FP16, chain rule, capacity 1<<20, 256 waypoints,
    max_active 1<<22, rank 0, world 1). */
 void gcdf_default_options(gcdf_options *opt);
 
@@ -189,6 +192,17 @@ int64_t gcdf_launch_count(const gcdf_ctx *ctx);
    milliseconds and launch count since the last reset. */
 int gcdf_profile_enable(gcdf_ctx *ctx, int enable);
 int gcdf_profile_read(gcdf_ctx *ctx, double *mlp_ms, int64_t *mlp_launches, int reset);
+
+/* ------------------------------------------------------------------ diagnostics */
+/* Runs one tcgen05 UMMA building block of the bf16 kernel on device `cuda_device`
+   (unit test of descriptors and TMEM layout).  A_dev fp32 [128][128] (rounded to bf16,
+   staged in TMEM), B_dev fp32 row-major (rounded to bf16, staged in smem, SWIZZLE_128B),
+   D_dev fp32 [128][128] output.  mode 0: D = A B^T, B [128][128] (K-major B);
+   mode 1: D = A B, B [128][128] (MN-major B); mode 2: D[:, 0:16] = A B^T, B [16][128];
+   mode | 4: the same with fp16 operands instead of bf16.
+   Synchronizes the stream.  UNSUPPORTED without the tcgen05 build. */
+int gcdf_selftest_umma(int cuda_device, int mode, const float *A_dev, const float *B_dev, float *D_dev,
+                       void *stream);
 
 #ifdef __cplusplus
 }

@@ -23,6 +23,8 @@ EMU_W = 1
 EMU_A = 2
 EMU_BF16 = EMU_W | EMU_A
 TGRAD_QCHANNEL = 4
+EMU_FP16_FLAG = 8
+EMU_FP16 = EMU_W | EMU_A | EMU_FP16_FLAG
 
 ERRORS = {0: "OK", -1: "INVALID", -2: "IO", -3: "BAD_MAGIC", -4: "VERSION", -5: "DIM_MISMATCH",
           -7: "CAPACITY", -12: "NOMEM"}

@@ -49,6 +49,7 @@
 #define OR_EMU_W 1           /* round hidden W_2..W_{L-1} and W_1 (as used by the gradient) to bf16 */
 #define OR_EMU_A 2           /* round MMA A-operands h_1..h_{L-2}, e_{L-1}..e_1 to bf16 */
 #define OR_TGRAD_QCHANNEL 4  /* translational gradient from the q^t input channels */
+#define OR_EMU_FP16 8        /* with OR_EMU_W / OR_EMU_A: round to fp16 instead of bf16 */
 
 #define OR_MAXL 16
 #define OR_NDOF 9
@@ -61,6 +62,7 @@ typedef struct {
   double *W[OR_MAXL]; /* [dims[l+1]][dims[l]] row-major */
   double *b[OR_MAXL];
   double *Wr[OR_MAXL]; /* bf16-rounded copies (O8) */
+  double *Wh[OR_MAXL]; /* fp16-rounded copies (O8, OR_EMU_FP16) */
   int maxw;
 } omlp_t;
 
@@ -78,12 +80,20 @@ static double bf16r(double v) {
   return (double)f;
 }
 
+static double f16r(double v) {
+  /* f64 -> fp32 (RN) -> fp16 (RN-even, with subnormals), as cvt.rn.f16x2.f32 does */
+  float f = (float)v;
+  _Float16 h = (_Float16)f;
+  return (double)(float)h;
+}
+
 void or_free(omlp_t *m) {
   if (!m) return;
   for (int l = 0; l < m->L; ++l) {
     free(m->W[l]);
     free(m->b[l]);
     free(m->Wr[l]);
+    free(m->Wh[l]);
   }
   free(m);
 }
@@ -121,11 +131,15 @@ int or_load(const char *path, omlp_t **out) {
     m->W[l] = (double *)malloc(nw * sizeof(double));
     m->b[l] = (double *)malloc(nb * sizeof(double));
     m->Wr[l] = (double *)malloc(nw * sizeof(double));
-    if (!m->W[l] || !m->b[l] || !m->Wr[l]) { fclose(fh); or_free(m); return OR_ERR_NOMEM; }
+    m->Wh[l] = (double *)malloc(nw * sizeof(double));
+    if (!m->W[l] || !m->b[l] || !m->Wr[l] || !m->Wh[l]) { fclose(fh); or_free(m); return OR_ERR_NOMEM; }
     if (fread(m->W[l], 8, nw, fh) != nw || fread(m->b[l], 8, nb, fh) != nb) {
       fclose(fh); or_free(m); return OR_ERR_IO;
     }
-    for (size_t i = 0; i < nw; ++i) m->Wr[l][i] = bf16r(m->W[l][i]);
+    for (size_t i = 0; i < nw; ++i) {
+      m->Wr[l][i] = bf16r(m->W[l][i]);
+      m->Wh[l][i] = f16r(m->W[l][i]);
+    }
   }
   /* trailing bytes mean the header does not describe the body */
   char extra;
@@ -155,6 +169,9 @@ static void eval_pair(const omlp_t *m, const double p[3], const double q[OR_NDOF
                       uint64_t *mhash) {
   const int L = m->L, MW = m->maxw;
   const int emu_w = flags & OR_EMU_W, emu_a = flags & OR_EMU_A;
+  const int fp16 = flags & OR_EMU_FP16;
+  double (*rnd)(double) = fp16 ? f16r : bf16r;
+  double *const *Wround = fp16 ? m->Wh : m->Wr;
   double *h0 = s->h;
   /* O3: base-frame bias (translation only; q^t channels fed zero) */
   h0[0] = p[0] - q[0];
@@ -168,7 +185,7 @@ static void eval_pair(const omlp_t *m, const double p[3], const double q[OR_NDOF
   for (int l = 0; l < L - 1; ++l) {
     const int din = m->dims[l], dout = m->dims[l + 1];
     /* layer 1 (l == 0) runs in fp32/f64 on CUDA cores in every GPU path: never rounded */
-    const double *Wl = (emu_w && l > 0) ? m->Wr[l] : m->W[l];
+    const double *Wl = (emu_w && l > 0) ? Wround[l] : m->W[l];
     const double *hin = s->h + (size_t)l * MW;
     double *zl = s->z + (size_t)l * MW;
     double *hout = s->h + (size_t)(l + 1) * MW;
@@ -176,7 +193,7 @@ static void eval_pair(const omlp_t *m, const double p[3], const double q[OR_NDOF
       double acc = 0.0;
       for (int j = 0; j < din; ++j) {
         double a = hin[j];
-        if (emu_a && l > 0) a = bf16r(a); /* A operand h_{l} of layer l+1 rounded (O8) */
+        if (emu_a && l > 0) a = rnd(a); /* A operand h_{l} of layer l+1 rounded (O8) */
         acc += Wl[(size_t)k * din + j] * a;
       }
       zl[k] = acc + m->b[l][k];
@@ -214,10 +231,10 @@ static void eval_pair(const omlp_t *m, const double p[3], const double q[OR_NDOF
     for (int k = 0; k < dout; ++k) {
       double d = (m->act == 1) ? (zl[k] > 0.0 ? 1.0 : 0.0) : 1.0;
       double e = s->g[k] * d;
-      if (emu_a) e = bf16r(e); /* A operand of the backward GEMM (O8) */
+      if (emu_a) e = rnd(e); /* A operand of the backward GEMM (O8) */
       s->e[k] = e;
     }
-    const double *Wl = emu_w ? m->Wr[l] : m->W[l];
+    const double *Wl = emu_w ? Wround[l] : m->W[l];
     for (int j = 0; j < din; ++j) {
       double acc = 0.0;
       for (int k = 0; k < dout; ++k) acc += Wl[(size_t)k * din + j] * s->e[k];

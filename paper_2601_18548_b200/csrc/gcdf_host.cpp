@@ -6,6 +6,7 @@
 // components can be modified online"), the workspace carve-up, and kernel dispatch.
 // No device memory is allocated after gcdf_bind_workspace; no CPU compute path exists
 // for any hot-path step (every step runs in the kernels of this directory).
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -30,7 +31,7 @@ constexpr int kEvPool = 64;
 inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
 struct Layout {
-  int64_t pts, wf32, wbf16, meta, staging, wp_key, wp_count, counter, upd_payload, upd_slots, total;
+  int64_t pts, wf32, wbf16, wf16, meta, staging, wp_key, wp_count, counter, upd_payload, upd_slots, total;
   int64_t wf32_bytes, wbf16_bytes;
 };
 
@@ -143,8 +144,9 @@ WeightsF32 f32_view(const gcdf_ctx *c) {
 WeightsBF16 bf16_view(const gcdf_ctx *c) {
   WeightsF32 f = f32_view(c);
   WeightsBF16 w{};
-  w.w_sw128 = c->ws + c->L.wbf16;
-  w.w1t_sw128 = c->ws + c->L.wbf16 + 5 * kBfMat;
+  const int64_t wo = c->opt.precision == GCDF_FP16 ? c->L.wf16 : c->L.wbf16;
+  w.w_sw128 = c->ws + wo;
+  w.w1t_sw128 = c->ws + wo + 5 * kBfMat;
   w.w1p = f.w1p;
   w.w1q = f.w1q;
   w.bias = f.bias[0];  // the five bias vectors are contiguous [5][H]
@@ -179,14 +181,22 @@ uint16_t to_bf16_rne(float f) {
   return (uint16_t)(u >> 16);
 }
 
-// UMMA canonical SWIZZLE_128B (K-major view): matrix [rows][cols] bf16, cols % 64 == 0.
+uint16_t to_f16_rne(float f) {
+  const __half h = __float2half_rn(f);
+  uint16_t b;
+  std::memcpy(&b, &h, 2);
+  return b;
+}
+
+// UMMA canonical SWIZZLE_128B (K-major view): matrix [rows][cols] 16-bit, cols % 64 == 0.
 // chunk = col / 64 -> [rows][128 B] block; 16-B granule g of row r at g ^ (r % 8).
-void pack_sw128(const std::vector<float> &m, int rows, int cols, uint16_t *dst) {
+void pack_sw128(const std::vector<float> &m, int rows, int cols, uint16_t *dst, bool f16) {
   for (int r = 0; r < rows; ++r)
     for (int c = 0; c < cols; ++c) {
       const int chunk = c / 64, cb = (c % 64) * 2, g = cb / 16;
       const int64_t byte = (int64_t)chunk * rows * 128 + (int64_t)r * 128 + ((g ^ (r % 8)) * 16) + (cb % 16);
-      dst[byte / 2] = to_bf16_rne(m[(size_t)r * cols + c]);
+      const float v = m[(size_t)r * cols + c];
+      dst[byte / 2] = f16 ? to_f16_rne(v) : to_bf16_rne(v);
     }
 }
 
@@ -215,7 +225,7 @@ extern "C" {
 
 void gcdf_default_options(gcdf_options *o) {
   if (!o) return;
-  o->precision = GCDF_BF16;
+  o->precision = GCDF_FP16;
   o->tgrad_mode = GCDF_TGRAD_CHAINRULE;
   o->scene_capacity = 1 << 20;
   o->max_waypoints = 256;
@@ -234,7 +244,7 @@ int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out) {
   if (opt) o = *opt;
   if (o.scene_capacity <= 0 || o.scene_capacity >= (1LL << 32) || o.max_waypoints <= 0 || o.max_active <= 0 ||
       o.max_active >= (1LL << 31) || o.world < 1 || o.rank < 0 || o.rank >= o.world ||
-      (o.precision != GCDF_FP32 && o.precision != GCDF_BF16) ||
+      (o.precision != GCDF_FP32 && o.precision != GCDF_BF16 && o.precision != GCDF_FP16) ||
       (o.tgrad_mode != GCDF_TGRAD_CHAINRULE && o.tgrad_mode != GCDF_TGRAD_QCHANNEL))
     return GCDF_ERR_INVALID_ARG;
   int ndev = 0;
@@ -242,7 +252,7 @@ int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out) {
   cudaDeviceProp prop;
   if (cudaGetDeviceProperties(&prop, cuda_device) != cudaSuccess) return GCDF_ERR_CUDA;
   if (prop.major != 10 || prop.minor != 0) return GCDF_ERR_UNSUPPORTED;  // sm_100a kernels only
-  if (o.precision == GCDF_BF16 && !tc_compiled()) return GCDF_ERR_UNSUPPORTED;
+  if (o.precision != GCDF_FP32 && !tc_compiled()) return GCDF_ERR_UNSUPPORTED;
   gcdf_ctx *c = new gcdf_ctx();
   c->device = cuda_device;
   c->num_sms = prop.multiProcessorCount;
@@ -258,6 +268,7 @@ int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out) {
   L.pts = off; off = align256(off + c->local_cap * 16);
   L.wf32 = off; L.wf32_bytes = kF32Total * 4; off = align256(off + L.wf32_bytes);
   L.wbf16 = off; L.wbf16_bytes = kBfTotal; off = align256(off + kBfTotal);
+  L.wf16 = off; off = align256(off + kBfTotal);
   L.meta = off; off = align256(off + (int64_t)o.max_waypoints * c->tiles_cap * 8);
   L.staging = off; off = align256(off + o.max_active * (int64_t)sizeof(gcdf_active_t));
   L.wp_key = off; off = align256(off + (int64_t)o.max_waypoints * 8);
@@ -345,8 +356,8 @@ int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
   for (int l = 1; l <= 6; ++l) ok = ok && dims[l] == (uint32_t)H;
   if (!ok) return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: dims must be [12, H x 6, 1], H in {32, 128}", path);
   if (act != 1) return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: activation %u (only ReLU = 1 is supported, R9)", path, act);
-  if (c->opt.precision == GCDF_BF16 && H != 128)
-    return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: the bf16 tensor-core path needs H = 128 (use GCDF_FP32 for H = %d)", path, H);
+  if (c->opt.precision != GCDF_FP32 && H != 128)
+    return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: the tensor-core path needs H = 128 (use GCDF_FP32 for H = %d)", path, H);
   std::vector<std::vector<double>> Wd(7), bd(7);
   for (int l = 0; l < 7; ++l) {
     Wd[l].resize((size_t)dims[l + 1] * dims[l]);
@@ -384,23 +395,26 @@ int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
   for (int li = 0; li < 5; ++li, p += H)
     for (int u = 0; u < H; ++u) p[u] = (float)bd[li + 1][u];
   for (int u = 0; u < H; ++u) p[u] = W(6, 0, u);
-  // ---- pack bf16 (UMMA SW128) ----
-  std::vector<uint16_t> bf((size_t)kBfTotal / 2, 0);
+  // ---- pack bf16 and fp16 (UMMA SW128); the weights are rounded f64 -> fp32 -> 16 bit ----
+  std::vector<uint16_t> bf((size_t)kBfTotal / 2, 0), hf((size_t)kBfTotal / 2, 0);
   if (H == 128) {
     std::vector<float> m((size_t)H * H);
     for (int li = 0; li < 5; ++li) {
       for (int r = 0; r < H; ++r)
         for (int col = 0; col < H; ++col) m[(size_t)r * H + col] = W(li + 1, r, col);
-      pack_sw128(m, H, H, bf.data() + (size_t)li * kBfMat / 2);
+      pack_sw128(m, H, H, bf.data() + (size_t)li * kBfMat / 2, false);
+      pack_sw128(m, H, H, hf.data() + (size_t)li * kBfMat / 2, true);
     }
     std::vector<float> w1t((size_t)16 * H, 0.f);  // [n = input 0..15][k = unit]
     for (int n = 0; n < kNin; ++n)
       for (int k = 0; k < H; ++k) w1t[(size_t)n * H + k] = W(0, k, n);
-    pack_sw128(w1t, 16, H, bf.data() + (size_t)5 * kBfMat / 2);
+    pack_sw128(w1t, 16, H, bf.data() + (size_t)5 * kBfMat / 2, false);
+    pack_sw128(w1t, 16, H, hf.data() + (size_t)5 * kBfMat / 2, true);
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   CK(c, cudaMemcpyAsync(c->ws + c->L.wf32, f32.data(), f32.size() * 4, cudaMemcpyHostToDevice, s), "weights H2D");
   CK(c, cudaMemcpyAsync(c->ws + c->L.wbf16, bf.data(), bf.size() * 2, cudaMemcpyHostToDevice, s), "weights H2D");
+  CK(c, cudaMemcpyAsync(c->ws + c->L.wf16, hf.data(), hf.size() * 2, cudaMemcpyHostToDevice, s), "weights H2D");
   CK(c, cudaStreamSynchronize(s), "weights sync");
   c->H = H;
   c->b7 = (float)bd[6][0];
@@ -508,8 +522,9 @@ static cudaError_t run_mlp(gcdf_ctx *c, const QueryArgs &a, cudaStream_t s) {
     slot = c->ev_used++;
     cudaEventRecord(c->ev[2 * slot], s);
   }
-  cudaError_t e = c->opt.precision == GCDF_BF16 ? launch_mlp_tc(c->H, bf16_view(c), a, c->num_sms, s)
-                                                : launch_mlp_simt(c->H, f32_view(c), a, c->num_sms, s);
+  cudaError_t e = c->opt.precision == GCDF_FP32
+                      ? launch_mlp_simt(c->H, f32_view(c), a, c->num_sms, s)
+                      : launch_mlp_tc(c->H, c->opt.precision == GCDF_FP16, bf16_view(c), a, c->num_sms, s);
   if (slot >= 0) cudaEventRecord(c->ev[2 * slot + 1], s);
   return e;
 }
@@ -629,6 +644,15 @@ int gcdf_merge_active_sets(gcdf_ctx *c, int32_t world, int32_t n_wp, const gcdf_
   cudaError_t e = launch_merge(world, n_wp, recs, rec_stride, offsets, wp_key, out, cap, offs, wmin, warg, count,
                                static_cast<cudaStream_t>(stream), &nl);
   return count_launch(c, e, "merge", nl);
+}
+
+int gcdf_selftest_umma(int dev, int mode, const float *A, const float *B, float *D, void *stream) {
+  if (!tc_compiled()) return GCDF_ERR_UNSUPPORTED;
+  if (mode < 0 || mode > 6 || (mode & 3) > 2 || !A || !B || !D) return GCDF_ERR_INVALID_ARG;
+  if (cudaSetDevice(dev) != cudaSuccess) return GCDF_ERR_CUDA;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (launch_selftest_umma(mode, A, B, D, s) != cudaSuccess) return GCDF_ERR_CUDA;
+  return cudaStreamSynchronize(s) == cudaSuccess ? GCDF_OK : GCDF_ERR_CUDA;
 }
 
 }  // extern "C"

@@ -88,8 +88,9 @@ cudaError_t launch_pairgen(const float4 *pts, int64_t local_bound, const float *
                            float4 *out, cudaStream_t s);
 cudaError_t launch_detect_init(DetectScratch ds, int32_t n_wp, cudaStream_t s);
 cudaError_t launch_mlp_simt(int H, const WeightsF32 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
-cudaError_t launch_mlp_tc(int H, const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
+cudaError_t launch_mlp_tc(int H, bool f16, const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
 bool tc_compiled();
+cudaError_t launch_selftest_umma(int mode, const float *A, const float *B, float *D, cudaStream_t s);
 cudaError_t launch_compact_dense(const float *values, const float *grads, int64_t stride, int32_t n_wp,
                                  int32_t tiles_per_wp, SceneView scene, float delta, float tau,
                                  DetectScratch ds, cudaStream_t s);

@@ -15,7 +15,7 @@ import torch
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "libgcdf.so"
 
-FP32, BF16 = 0, 1
+FP32, BF16, FP16 = 0, 1, 2
 TGRAD_CHAINRULE, TGRAD_QCHANNEL = 0, 1
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "IO", -3: "BAD_MAGIC", -4: "VERSION", -5: "DIM_MISMATCH",
           -6: "NOT_LOADED", -7: "CAPACITY", -8: "UNKNOWN_ID", -9: "NONFINITE", -10: "CUDA",
@@ -26,7 +26,7 @@ EXPORTED = ["gcdf_default_options", "gcdf_create", "gcdf_destroy", "gcdf_last_er
             "gcdf_workspace_bytes", "gcdf_bind_workspace", "gcdf_load_weights", "gcdf_update_scene",
             "gcdf_scene_info", "gcdf_pairgen_transform", "gcdf_query_values_grads", "gcdf_detect_active_set",
             "gcdf_compact_dense", "gcdf_merge_active_sets", "gcdf_launch_count", "gcdf_profile_enable",
-            "gcdf_profile_read"]
+            "gcdf_profile_read", "gcdf_selftest_umma"]
 
 
 class GcdfError(RuntimeError):
@@ -76,6 +76,7 @@ def load_library(path: str | Path = LIB_PATH):
     lib.gcdf_launch_count.restype = I64
     lib.gcdf_profile_enable.argtypes = [P, C.c_int]
     lib.gcdf_profile_read.argtypes = [P, C.POINTER(C.c_double), PI64, C.c_int]
+    lib.gcdf_selftest_umma.argtypes = [C.c_int, C.c_int, P, P, P, P]
     _lib = lib
     return lib
 
@@ -96,10 +97,22 @@ def records_to_dict(rec: torch.Tensor, n: int) -> dict:
             "pt": r[:, 11].to(torch.int64) & 0xFFFFFFFF}
 
 
+def selftest_umma(mode: int, A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
+    """Diagnostics: one tcgen05 UMMA block (see gcdf_selftest_umma)."""
+    lib = load_library()
+    A = A.to(torch.float32).contiguous()
+    B = B.to(device=A.device, dtype=torch.float32).contiguous()
+    D = torch.zeros((128, 128), dtype=torch.float32, device=A.device)
+    rc = lib.gcdf_selftest_umma(A.device.index or 0, mode, _ptr(A), _ptr(B), _ptr(D), _stream(A.device))
+    if rc:
+        raise GcdfError(rc, "selftest_umma")
+    return D
+
+
 class Context:
     """One libgcdf context on one CUDA device (one rank)."""
 
-    def __init__(self, device: int = 0, precision: int = BF16, tgrad_mode: int = TGRAD_CHAINRULE,
+    def __init__(self, device: int = 0, precision: int = FP16, tgrad_mode: int = TGRAD_CHAINRULE,
                  scene_capacity: int = 1 << 20, max_waypoints: int = 256, max_active: int = 1 << 22,
                  rank: int = 0, world: int = 1):
         self.lib = load_library()

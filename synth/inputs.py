@@ -159,10 +159,26 @@ def scene_update_batch(rng: np.random.Generator, boxes: np.ndarray, live_ids: np
     """C4 dynamics: remove n_remove random live ids; add n_add points on one box moved by
     U(-0.3, 0.3)^2 m.  Returns (add_xyz fp32 [n_add,3], remove_ids int64 [n_remove])."""
     rem = np.sort(rng.choice(live_ids, size=min(n_remove, live_ids.size), replace=False)).astype(np.int64)
+    return _moved_box_points(rng, boxes, n_add), rem
+
+
+def scene_update_batch_mask(rng: np.random.Generator, boxes: np.ndarray, alive: np.ndarray,
+                            n_remove: int = 200, n_add: int = 200):
+    """Same dynamics as scene_update_batch for a large scene given as a boolean alive[id]
+    mask (O(n_remove) rejection sampling instead of O(M) work per step)."""
+    picked = set()
+    while len(picked) < n_remove:
+        i = int(rng.integers(0, alive.size))
+        if alive[i]:
+            picked.add(i)
+    rem = np.array(sorted(picked), dtype=np.int64)
+    return _moved_box_points(rng, boxes, n_add), rem
+
+
+def _moved_box_points(rng, boxes, n_add):
     box = boxes[rng.integers(0, boxes.shape[0])].copy()
     box[0:2] += rng.uniform(-0.3, 0.3, 2)
-    add = _sample_on_boxes(rng, box[None, :], n_add).astype(np.float32)
-    return add, rem
+    return _sample_on_boxes(rng, box[None, :], n_add).astype(np.float32)
 
 
 # ----------------------------------------------------------------------------- weights

@@ -31,7 +31,7 @@ def test_default_options_and_struct_layout(lib):
     from paper_2601_18548_b200.gcdf import Options
     o = Options()
     lib.gcdf_default_options(C.byref(o))
-    assert (o.precision, o.tgrad_mode, o.world, o.rank) == (1, 0, 1, 0)
+    assert (o.precision, o.tgrad_mode, o.world, o.rank) == (2, 0, 1, 0)
     assert o.scene_capacity == 1 << 20 and o.max_waypoints == 256 and o.max_active == 1 << 22
     assert C.sizeof(Options) == 40
 

@@ -1,0 +1,198 @@
+"""GPU parity of the tcgen05 tensor-core path (GCDF_FP16 default, GCDF_BF16) vs the oracle.
+
+Gates (R17):
+  (1) same rounding points: vs the oracle's EMU mode for the operand type (fp16 / bf16
+      rounding of exactly the MMA operands) the median value error is fp32 noise (<= 1e-6)
+      and the p99 small (the tail differs only where fp32 accumulation order moves a value
+      across a 16-bit rounding boundary or a ReLU kink);
+  (2) vs the exact oracle, values on every pair: |df| <= 2e-2 (north star);
+  (3) vs the exact oracle, | ||g_gpu|| - ||g_exact|| | <= 5e-2 (north star) on >= 99% of pairs
+      and on every pair whose exact ReLU masks equal the emulated ones.
+fp16 meets (2) and (3) as stated; bf16 operand rounding alone (the EMU oracle, no GPU
+involved) exceeds them on this network, so for bf16 the measured bounds are asserted and
+the gap is reported.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import BF16_GNORM_ATOL, BF16_VAL_ATOL, DELTA, compare_active_sets, oracle_detect, oracle_mlp, records_np
+
+pytestmark = pytest.mark.gpu
+NT = max(1, min(os.cpu_count() or 1, 64))
+KINK_EMU = 1e-3
+PRECS = {"fp16": (2, oracle.EMU_FP16), "bf16": (1, oracle.EMU_BF16)}
+# bf16: bounds measured for this network by the EMU oracle alone (operand rounding), DESIGN.md §5
+BF16_MEASURED = {"val": 3e-2, "gnorm_frac": 0.95}
+
+
+def _ctx(cfg, prec, **kw):
+    from paper_2601_18548_b200 import Context
+    ctx = Context(0, precision=PRECS[prec][0], scene_capacity=cfg.M + 4096, max_waypoints=cfg.B * cfg.N,
+                  max_active=min(cfg.pairs, 1 << 22), **kw)
+    ctx.load_weights(synth.weights_path(cfg.H))
+    return ctx
+
+
+def _round(x, prec):
+    return x.to(torch.float16 if prec == "fp16" else torch.bfloat16).to(torch.float64)
+
+
+@pytest.mark.parametrize("prec", ["fp16", "bf16"])
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_selftest_umma(mode, prec):
+    """One UMMA block: K-major B (forward), MN-major B (backward), N = 16 (last GEMM)."""
+    from paper_2601_18548_b200.gcdf import selftest_umma
+    g = torch.Generator().manual_seed(mode)
+    A = torch.randn(128, 128, generator=g)
+    B = torch.randn(16 if mode == 2 else 128, 128, generator=g)
+    D = selftest_umma(mode | (4 if prec == "fp16" else 0), A.cuda(), B.cuda()).cpu().double()
+    ref = _round(A, prec) @ (_round(B, prec) if mode == 1 else _round(B, prec).T)
+    n = ref.shape[1]
+    err = (D[:, :n] - ref).abs().max().item()
+    assert err <= 1e-4 * max(1.0, ref.abs().max().item()), err
+
+
+def stats_and_gates(v, g, exact, emu, prec, what=""):
+    dv = np.abs(v - emu["f"])
+    de = np.abs(v - exact["f"])
+    gn_g = np.linalg.norm(g, axis=-1)
+    gd = np.abs(gn_g - np.linalg.norm(exact["g"], axis=-1))
+    dg_emu = np.linalg.norm(g - emu["g"], axis=-1) / np.maximum(1.0, np.linalg.norm(emu["g"], axis=-1))
+    kink_free = (exact["mask_hash"] == emu["mask_hash"]) & (emu["kappa"] > KINK_EMU)
+    st = {"emu_val_agree_1e-5": float(np.mean(dv <= 1e-5)), "emu_val_max": float(dv.max()),
+          "emu_val_p50": float(np.median(dv)), "emu_val_p99": float(np.percentile(dv, 99)),
+          "emu_grad_agree_1e-4": float(np.mean(dg_emu <= 1e-4)), "emu_grad_p99": float(np.percentile(dg_emu, 99)),
+          "exact_val_max": float(de.max()), "exact_val_p99": float(np.percentile(de, 99)),
+          "gnorm_within_5e-2": float(np.mean(gd <= BF16_GNORM_ATOL)), "gnorm_p99": float(np.percentile(gd, 99)),
+          "gnorm_max_kink_free": float(gd[kink_free].max()) if kink_free.any() else 0.0,
+          "kink_free_frac": float(kink_free.mean())}
+    print(f"\n[{prec}] {what}: {st}", flush=True)
+    # gate 1: the bulk agrees with the emulation to fp32-accumulation noise; the tail is
+    # 16-bit rounding-boundary / ReLU-kink flips (8x more frequent but 8x smaller for fp16)
+    assert st["emu_val_p50"] <= 1e-6, st
+    assert st["emu_val_p99"] <= (3e-4 if prec == "fp16" else 1e-4), st
+    assert st["emu_val_max"] <= 1e-2, st
+    assert st["emu_grad_p99"] <= 1e-2, st
+    if prec == "fp16":
+        assert st["exact_val_max"] <= BF16_VAL_ATOL, st    # gate 2
+        assert st["gnorm_within_5e-2"] >= 0.99, st         # gate 3
+        assert st["gnorm_max_kink_free"] <= BF16_GNORM_ATOL, st
+    else:
+        assert st["exact_val_max"] <= BF16_MEASURED["val"], st
+        assert st["gnorm_within_5e-2"] >= BF16_MEASURED["gnorm_frac"], st
+    return st
+
+
+@pytest.fixture(scope="module")
+def c2():
+    cfg = synth.get_config("C2")
+    pts, _ = synth.make_scene_points(cfg)
+    q = synth.make_waypoints(cfg)[:, :12]
+    m = oracle_mlp(cfg)
+    Q = q.reshape(-1, 9)
+    exact = m.eval(pts, Q, want_kappa=True, want_hash=True, nthreads=NT)
+    emu = {p: m.eval(pts, Q, flags=PRECS[p][1], want_kappa=True, want_hash=True, nthreads=NT) for p in PRECS}
+    return cfg, pts, q, m, exact, emu
+
+
+@pytest.mark.parametrize("prec", ["fp16", "bf16"])
+def test_query_dense(c2, prec):
+    cfg, pts, q, m, exact, emu = c2
+    ctx = _ctx(cfg, prec)
+    ctx.update_scene(pts)
+    v, g = ctx.query_values_grads(torch.from_numpy(q))
+    torch.cuda.synchronize()
+    M = len(pts)
+    vn, gnp = v.cpu().numpy(), g.cpu().numpy()
+    stats_and_gates(vn[:, :M], gnp[:, :M], exact, emu[prec], prec, "C2 dense (120k pairs)")
+    assert np.all(np.isinf(vn[:, M:])) and np.all(gnp[:, M:] == 0)
+
+
+@pytest.mark.parametrize("prec", ["fp16", "bf16"])
+def test_detect(c2, prec):
+    cfg, pts, q, m, exact, emu = c2
+    tau = synth.load_tau(cfg.name)
+    ctx = _ctx(cfg, prec)
+    ids = ctx.update_scene(pts)
+    out = ctx.detect_active_set(torch.from_numpy(q), DELTA, tau)
+    torch.cuda.synchronize()
+    gpu = records_np(out)
+    Q = q.reshape(-1, 9)
+    tol = BF16_VAL_ATOL if prec == "fp16" else BF16_MEASURED["val"]
+    orc = oracle_detect(m, pts, ids, Q, tau, nthreads=NT)
+    nd, nc = compare_active_sets(gpu, orc, exact["f"], ids, 1e-3 + tol, val_atol=tol, what="vs exact")
+    assert nc > 0
+    assert np.all(np.abs(out["wp_min"].cpu().numpy() - orc["wp_min"]) <= tol)
+    print(f"\n[{prec}] detect C2: {out['n']} active, oracle {orc['count']}, {nd} differ (all within the band)")
+
+
+@pytest.mark.parametrize("prec", ["fp16", "bf16"])
+def test_fused_equals_dense_plus_compact(c2, prec):
+    cfg, pts, q, m, exact, emu = c2
+    tau = synth.load_tau(cfg.name)
+    ctx = _ctx(cfg, prec)
+    ctx.update_scene(pts)
+    qt = torch.from_numpy(q)
+    v, g = ctx.query_values_grads(qt)
+    a = records_np(ctx.compact_dense(v, g, DELTA, tau))
+    b = records_np(ctx.detect_active_set(qt, DELTA, tau))
+    for k in ("wp", "pt", "value", "grad"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_qchannel_mode_fp16(c2):
+    """TGRAD_QCHANNEL: the translational gradient is the network's q^t input channel (R3)."""
+    from paper_2601_18548_b200 import TGRAD_QCHANNEL
+    cfg, pts, q, m, exact, emu = c2
+    ctx = _ctx(cfg, "fp16", tgrad_mode=TGRAD_QCHANNEL)
+    ctx.update_scene(pts[:2000])
+    v, g = ctx.query_values_grads(torch.from_numpy(q[:, :2]))
+    ex = m.eval(pts[:2000], q[:, :2].reshape(-1, 9), flags=oracle.TGRAD_QCHANNEL)
+    gn = g.cpu().numpy()[:, :2000]
+    d = np.abs(np.linalg.norm(gn, axis=-1) - np.linalg.norm(ex["g"], axis=-1))
+    assert np.mean(d <= BF16_GNORM_ATOL) >= 0.99
+
+
+def test_c5_full_size_sampled():
+    """The bench configuration (C5: 256 waypoints x 1M points, fp16, full-size detect):
+    sampled pairs against the oracle one by one, plus the per-waypoint min property."""
+    cfg = synth.get_config("C5")
+    pts, _ = synth.make_scene_points(cfg)
+    q = synth.make_waypoints(cfg)
+    tau = synth.load_tau(cfg.name)
+    ctx = _ctx(cfg, "fp16")
+    ids = ctx.update_scene(pts)
+    out = ctx.detect_active_set(torch.from_numpy(q), DELTA, tau)
+    torch.cuda.synchronize()
+    gpu = records_np(out)
+    rng = np.random.default_rng(2024)
+    m = oracle_mlp(cfg)
+    Q = q.reshape(-1, 9)
+    wsel = np.sort(rng.choice(Q.shape[0], 3, replace=False))
+    psel = np.sort(rng.choice(len(pts), 4096, replace=False))
+    ex = m.eval(pts[psel], Q[wsel], want_kappa=True, want_hash=True, nthreads=NT)
+    em = m.eval(pts[psel], Q[wsel], flags=oracle.EMU_FP16, want_kappa=True, want_hash=True, nthreads=NT)
+    v, g = ctx.query_values_grads(torch.from_numpy(Q[wsel].reshape(1, -1, 9)))
+    stats_and_gates(v.cpu().numpy()[:, psel], g.cpu().numpy()[:, psel], ex, em, "fp16", "C5 sampled")
+    recset = set(zip(gpu["wp"].tolist(), gpu["pt"].tolist()))
+    thr = tau + DELTA
+    checked = 0
+    for wi, w in enumerate(wsel):
+        for pj, pid in enumerate(psel):
+            f = ex["f"][wi, pj]
+            if abs(f - thr) > 1e-3 + BF16_VAL_ATOL:
+                assert ((int(w), int(ids[pid])) in recset) == (f <= thr), (w, pid, f)
+                checked += 1
+    assert checked > 0.9 * len(wsel) * len(psel)
+    wmin = out["wp_min"].cpu().numpy()[wsel]
+    assert np.all(wmin <= ex["f"].min(axis=1) + BF16_VAL_ATOL)
+    offs = out["wp_offsets"].cpu().numpy()
+    assert offs[-1] == out["n"] and np.all(np.diff(offs) >= 0)
+    frac = out["n"] / (len(pts) * Q.shape[0])
+    assert 0.001 < frac < 0.05
+    print(f"\nC5: {out['n']} active ({frac:.4%}), {checked} sampled memberships checked")

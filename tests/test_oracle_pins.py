@@ -366,3 +366,27 @@ def test_emu_weight_rounding_hand_example(tmp_path):
         out = m.eval(P, Q, flags=flags)
         assert out["f"][0, 0] == g[key]["f"], flags
         np.testing.assert_array_equal(out["g"][0, 0], g[key]["grad"])
+
+
+def test_emu_fp16_vs_bf16_hand_example(tmp_path):
+    """O8 for the fp16 operand type: hand-derived fp16 vs bf16 rounding (with a tie)."""
+    g = json.loads((GOLD / "hand_example.json").read_text())["emu16_network"]
+    layers = [(np.array(l["W"], float), np.array(l["b"], float)) for l in g["layers"]]
+    m = oracle.MLP(_write(tmp_path, "emu16.mlpw", 1, [12] + [1] * 6 + [1], layers))
+    P, Q = np.array([g["p"]]), np.array([g["q"]])
+    for flags, key in ((0, "exact"), (oracle.EMU_FP16, "emu_fp16"), (oracle.EMU_BF16, "emu_bf16")):
+        out = m.eval(P, Q, flags=flags)
+        assert out["f"][0, 0] == g[key]["f"], (flags, out["f"][0, 0])
+        np.testing.assert_array_equal(out["g"][0, 0], g[key]["grad"])
+
+
+def test_emu_fp16_subnormal_and_range(tmp_path):
+    """fp16 rounding of tiny backward deltas keeps subnormals (cvt.rn.f16 semantics):
+    a zero-head-like network with w7 = 2^-20 must give a gradient of exactly 2^-20 * W1
+    under EMU_FP16 (2^-20 is an fp16 subnormal: 2^-24 * 16)."""
+    g = json.loads((GOLD / "hand_example.json").read_text())["networks"][1]
+    layers = [(np.array(l["W"], float), np.array(l["b"], float)) for l in g["layers"]]
+    layers[-1] = (np.array([[2.0 ** -20]]), np.array([1.0]))
+    m = oracle.MLP(_write(tmp_path, "sub.mlpw", 1, [12] + [1] * 6 + [1], layers))
+    out = m.eval(np.array([[2.0, 0.0, 0.0]]), np.array([[1.0, 0, 0, 0, 0, 0, 0, 0, 0]]), flags=oracle.EMU_FP16)
+    assert out["g"][0, 0, 0] == -(2.0 ** -20) and out["g"][0, 0, 2] == 0.5 * 2.0 ** -20
