@@ -1,29 +1,30 @@
 // k_mlp_tc.cu -- K2b: fused pair generation + base-frame transform + 7-layer MLP forward
 // + input-gradient backward (+ threshold / min / per-tile compaction in detect mode) on
-// the 5th-generation tensor cores (tcgen05, bf16 operands, fp32 accumulation in TMEM).
+// the 5th-generation tensor cores (tcgen05, fp16 or bf16 operands, fp32 accumulation in TMEM).
 //
 // Paper steps (PAPER.md lines): base-frame bias :388/:171; "7-layer MLP" on [p, q] :284;
 // value + gradient :394 (dense gradient R^{NM x n}); constraint f - delta >= 0 :362-363;
 // union = min :164; c_gcdf step-major order :414-435.  DESIGN.md §5 "K2b".
 //
-// Design (H = 128, one persistent CTA per SM, 384 threads):
+// Design (H = 128, one persistent CTA per SM, 640 threads = 20 warps):
 //   * The ten H x H hidden-layer GEMMs of a 128-pair tile run as UMMA 128x128x16 with
-//     A = activations (bf16) in TMEM and B = W_l (bf16) resident in shared memory for the
-//     whole kernel (5 x 32 KB, UMMA SWIZZLE_128B).  The same smem bytes are the K-major B
-//     of the forward GEMM (D = h W^T) and the MN-major B of the backward GEMM (D = e W).
-//     The last backward GEMM g0 = e1 W1 is a 128x16x128 UMMA against W1^T (4 KB).
+//     A = activations (16-bit) in TMEM and B = W_l (16-bit) resident in shared memory for
+//     the whole kernel (5 x 32 KB, UMMA SWIZZLE_128B).  The same smem bytes are the
+//     K-major B of the forward GEMM (D = h W^T) and the MN-major B of the backward GEMM
+//     (D = e W).  The last backward GEMM g0 = e1 W1 is a 128x16x128 UMMA against W1^T.
 //   * Activations never leave the chip: accumulator D (fp32, 128 TMEM columns) ->
-//     epilogue registers (bias, ReLU, 1-bit mask, bf16 pack) -> A (64 TMEM columns) ->
-//     next UMMA.  ReLU masks stay in registers (24 x 32 bit per pair) for the backward.
+//     epilogue registers (bias, ReLU, 1-bit mask, 16-bit pack) -> A (64 TMEM columns) ->
+//     next UMMA.  ReLU masks stay in registers (12 x 32 bit per thread) for the backward.
 //   * Two tiles in flight: TMEM columns [0,256) belong to slot 0 and [256,512) to slot
-//     1; warpgroup 1 (warps 4-7) is slot 0's epilogue, warpgroup 2 (warps 8-11) slot 1's.
-//     One elected thread of warp 0 issues all UMMAs, alternating slots, so one slot's
-//     epilogue overlaps the other slot's tensor-core work.
+//     1.  Each slot has 8 epilogue warps: warp (h, q) owns TMEM lanes 32q..32q+31 (the
+//     tile's pairs) and accumulator columns 64h..64h+63, so every SM sub-partition runs
+//     two warps per slot (latency hiding) and one slot's epilogue overlaps the other
+//     slot's tensor-core work.  One elected thread of warp 0 issues all UMMAs.
 //   * Layer 1 (12 -> H) runs in fp32 on the CUDA cores (3 FMA per unit per pair plus a
 //     per-waypoint constant), so the metre-scale point coordinates are never rounded
-//     to bf16 (R16).
+//     to 16 bits (R16).
 //   * Synchronisation: mma_done[s] (tcgen05.commit -> mbarrier, count 1) and epi_done[s]
-//     (128 epilogue arrivals); 11 phases per tile.
+//     (256 epilogue arrivals); 11 phases per tile.
 #include "gcdf_internal.h"
 #include "tc_ptx.h"
 
@@ -33,7 +34,9 @@ namespace {
 using namespace tc;
 
 constexpr int H = 128;
-constexpr int kThreads = 384;
+constexpr int kWarps = 20;
+constexpr int kThreads = kWarps * 32;
+constexpr int kEpiPerSlot = 256;
 constexpr int kWBytes = 5 * H * H * 2;  // 163,840
 constexpr int kW1tBytes = 16 * H * 2;   // 4,096
 template <bool F16> constexpr uint32_t kIdescFwd = idesc_f16kind(128, 128, false, F16);
@@ -47,6 +50,8 @@ struct __align__(1024) SmemTC {
   float w1q[H * 8];
   float bias[5 * H];
   float w7[H];
+  float fpart[2][2][H];      // [slot][half][row] partial output-layer sums
+  uint32_t mask[2][kHidden][2][kEpiPerSlot];  // ReLU masks: [slot][layer][32-unit word][thread]
   uint64_t mma_done[2];
   uint64_t epi_done[2];
   unsigned act[2][4];
@@ -60,10 +65,13 @@ DEVI unsigned ord_f32(float f) {
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
+
 template <bool F16>
 __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, const QueryArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  SmemTC &S = *reinterpret_cast<SmemTC *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned view (SWIZZLE_128B atoms); pointer arithmetic on the __shared__ array
+  // keeps the shared address space visible to the compiler (LDS/STS, not generic LD/ST)
+  SmemTC &S = *reinterpret_cast<SmemTC *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // ---- one-time setup: weights -> smem (already in UMMA layout in global memory) ----
@@ -85,8 +93,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   if (tid == 32) {
     mbar_init(&S.mma_done[0], 1);
     mbar_init(&S.mma_done[1], 1);
-    mbar_init(&S.epi_done[0], 128);
-    mbar_init(&S.epi_done[1], 128);
+    mbar_init(&S.epi_done[0], kEpiPerSlot);
+    mbar_init(&S.epi_done[1], kEpiPerSlot);
     fence_barrier_init();
   }
   fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
@@ -101,15 +109,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     // =========================== MMA issuer (one thread) ===========================
     if (lane == 0) {
       const uint32_t sw = smem_u32(S.w), sw1t = smem_u32(S.w1t);
-      uint32_t ph[2] = {0u, 0u};
+      uint32_t phbits = 0u;  // bit s = phase parity of epi_done[s]
       for (int64_t base = (int64_t)blockIdx.x * 2; base < n_tiles; base += 2 * (int64_t)gridDim.x) {
         const int nslots = (base + 1 < n_tiles) ? 2 : 1;
 #pragma unroll 1
         for (int p = 0; p < 11; ++p) {
 #pragma unroll 1
           for (int s = 0; s < nslots; ++s) {
-            mbar_wait(&S.epi_done[s], ph[s]);
-            ph[s] ^= 1u;
+            mbar_wait(&S.epi_done[s], (phbits >> s) & 1u);
+            phbits ^= 1u << s;
             fence_after();
             const uint32_t d = tbase + (uint32_t)s * 256u, av = d + 128u;
             if (p < 5) {  // forward, layer l = p + 2: D = A W_l^T, B = W_l K-major
@@ -136,50 +144,54 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     }
     __syncwarp();
   } else if (warp >= 4) {
-    // =========================== epilogue warpgroups ===========================
-    const int s = (warp - 4) >> 2;
-    const int qd = warp & 3;          // TMEM lane quarter of this warp
+    // =========================== epilogue warps ===========================
+    const int e = warp - 4;
+    const int s = e >> 3;             // tile slot
+    const int hh = (e >> 2) & 1;      // accumulator column half: units 64 hh .. 64 hh + 63
+    const int qd = warp & 3;          // TMEM lane quarter of this warp (warp % 4)
     const int row = qd * 32 + lane;   // pair within the tile = TMEM lane
-    const uint32_t tD = tbase + (uint32_t)s * 256u + ((uint32_t)(qd * 32) << 16);
-    const uint32_t tA = tD + 128u;
+    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+    const uint32_t tD = tbase + (uint32_t)s * 256u + lane_off + 64u * hh;
+    const uint32_t tA = tbase + (uint32_t)s * 256u + 128u + lane_off + 32u * hh;
+    const int u0 = 64 * hh;           // first unit of this thread's columns
     uint32_t ph = 0u;
     for (int64_t T = (int64_t)blockIdx.x * 2 + s; T < n_tiles; T += 2 * (int64_t)gridDim.x) {
       const int w = (int)(T / a.tiles_per_wp);
       const int64_t slot = (T % a.tiles_per_wp) * kTile + row;
       const float *qw = a.q + (int64_t)w * kNdof;
-      float qv[kNdof];
-#pragma unroll
-      for (int i = 0; i < kNdof; ++i) qv[i] = __ldg(qw + i);
       // A2: pair generation + base-frame bias p' = p - [q_x, q_y, 0]
       const float4 pt = slot < lb ? __ldg(a.scene.pts + slot) : make_float4(0.f, 0.f, 0.f, 0.f);
       const bool live = slot < lb && pt.w > 0.f;
-      const float px = pt.x - qv[0], py = pt.y - qv[1], pz = pt.z;
+      const float px = pt.x - __ldg(qw), py = pt.y - __ldg(qw + 1), pz = pt.z;
       // layer-1 constant of this waypoint for unit u = row: c = b1 + W1[u, 5:12] . [theta, j1..j6]
-      {
+      if (hh == 0) {
         const float4 wv = __ldg(W.w1p + row);
         float c = wv.w;
 #pragma unroll
-        for (int i = 0; i < 7; ++i) c = fmaf(S.w1q[row * 8 + i], qv[2 + i], c);
+        for (int i = 0; i < 7; ++i) c = fmaf(S.w1q[row * 8 + i], __ldg(qw + 2 + i), c);
         S.w1c[s][row] = make_float4(wv.x, wv.y, wv.z, c);
       }
-      named_bar_sync(1 + s, 128);
+      named_bar_sync(1 + s, kEpiPerSlot);
 
-      uint32_t mask[kHidden][4];
-      // ---- E0: layer 1 in fp32 on CUDA cores -> h1 (bf16) into TMEM A ----
+      uint32_t *mk = &S.mask[s][0][0][hh * 128 + row];  // + (layer * 2 + word) * kEpiPerSlot
+      // ---- E0: layer 1 in fp32 on CUDA cores -> h1 (16-bit) into TMEM A ----
 #pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {
+      for (int c2 = 0; c2 < 2; ++c2) {
         uint32_t pk[16], m = 0u;
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          const float4 a0 = S.w1c[s][c4 * 32 + j], a1 = S.w1c[s][c4 * 32 + j + 1];
-          const float z0 = fmaf(a0.x, px, fmaf(a0.y, py, fmaf(a0.z, pz, a0.w)));
-          const float z1 = fmaf(a1.x, px, fmaf(a1.y, py, fmaf(a1.z, pz, a1.w)));
-          m |= (z0 > 0.f ? 1u : 0u) << j;
-          m |= (z1 > 0.f ? 1u : 0u) << (j + 1);
-          pk[j >> 1] = pack2_relu<F16>(z0, z1);
+        for (int j = 0; j < 32; j += 4) {
+          float z[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 a0 = S.w1c[s][u0 + c2 * 32 + j + i];
+            z[i] = fmaf(a0.x, px, fmaf(a0.y, py, fmaf(a0.z, pz, a0.w)));
+          }
+          pk[j >> 1] = pack2_relu<F16>(z[0], z[1]);
+          pk[(j >> 1) + 1] = pack2_relu<F16>(z[2], z[3]);
+          m |= mask_group(pk[j >> 1], pk[(j >> 1) + 1], j >> 2);
         }
-        mask[0][c4] = m;
-        st16(tA + c4 * 16, pk);
+        mk[c2 * kEpiPerSlot] = m;
+        st16(tA + c2 * 16, pk);
       }
       wait_st();
       fence_before();
@@ -188,131 +200,136 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
       float f = 0.f;
       bool act = false;
       int my_base = -1, my_rank = 0;
-#pragma unroll
+#pragma unroll 1
       for (int p = 0; p < 11; ++p) {
         mbar_wait(&S.mma_done[s], ph);
         ph ^= 1u;
         fence_after();
-        if (p < 4) {
+        if (p < 5) {
           // ---- forward hidden layer l = p + 2: z = D + b, h = ReLU(z) -> A ----
+          //      (l = 6: f += w7 . h6 in fp32, e6 = w7 (.) 1[z6 > 0] -> A)
+          float fp = 0.f;
 #pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4) {
-            uint32_t r[32], pk[16], m = 0u;
-            ld32(tD + c4 * 32, r);
-            wait_ld();
-            const float *bp = S.bias + p * H + c4 * 32;
+          for (int c2 = 0; c2 < 2; ++c2) {
+            uint32_t m = 0u;
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float4 b = *reinterpret_cast<const float4 *>(bp + j);
-              const float z0 = __uint_as_float(r[j]) + b.x, z1 = __uint_as_float(r[j + 1]) + b.y;
-              const float z2 = __uint_as_float(r[j + 2]) + b.z, z3 = __uint_as_float(r[j + 3]) + b.w;
-              m |= ((z0 > 0.f ? 1u : 0u) << j) | ((z1 > 0.f ? 1u : 0u) << (j + 1)) |
-                   ((z2 > 0.f ? 1u : 0u) << (j + 2)) | ((z3 > 0.f ? 1u : 0u) << (j + 3));
-              pk[j >> 1] = pack2_relu<F16>(z0, z1);
-              pk[(j >> 1) + 1] = pack2_relu<F16>(z2, z3);
-            }
-            mask[p + 1][c4] = m;
-            st16(tA + c4 * 16, pk);
-          }
-          wait_st();
-          fence_before();
-          mbar_arrive(&S.epi_done[s]);
-        } else if (p == 4) {
-          // ---- layer 6: h6 = ReLU(z6); f = w7 . h6 + b7 (fp32); e6 = w7 (.) 1[z6 > 0] -> A ----
+            for (int hf = 0; hf < 2; ++hf) {  // 16 accumulator columns per TMEM load
+              uint32_t r[16], pk[8];
+              const int cb = c2 * 32 + hf * 16;
+              ld16(tD + cb, r);
+              wait_ld();
+              const float *bp = S.bias + p * H + u0 + cb;
 #pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4) {
-            uint32_t r[32], pk[16], m = 0u;
-            ld32(tD + c4 * 32, r);
-            wait_ld();
-            const float *bp = S.bias + 4 * H + c4 * 32;
-            const float *wp7 = S.w7 + c4 * 32;
-#pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-              const float z0 = __uint_as_float(r[j]) + bp[j], z1 = __uint_as_float(r[j + 1]) + bp[j + 1];
-              const float w0 = wp7[j], w1 = wp7[j + 1];
-              f = fmaf(w0, fmaxf(z0, 0.f), f);
-              f = fmaf(w1, fmaxf(z1, 0.f), f);
-              m |= ((z0 > 0.f ? 1u : 0u) << j) | ((z1 > 0.f ? 1u : 0u) << (j + 1));
-              pk[j >> 1] = pack2<F16>(z0 > 0.f ? w0 : 0.f, z1 > 0.f ? w1 : 0.f);
-            }
-            mask[5][c4] = m;
-            st16(tA + c4 * 16, pk);
-          }
-          wait_st();
-          fence_before();
-          mbar_arrive(&S.epi_done[s]);
-          f += W.b7;
-          // A6/A7 (overlaps the next UMMA): threshold, per-tile slots, per-waypoint min key
-          if (a.detect) {
-            act = live && (f - a.delta <= a.tau);
-            const unsigned bal = __ballot_sync(0xffffffffu, act);
-            unsigned long long key = ~0ull;
-            if (live)
-              key = ((unsigned long long)ord_f32(f) << 32) |
-                    (unsigned long long)local_to_global(slot, a.scene.rank, a.scene.world);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-              key = other < key ? other : key;
-            }
-            if (lane == 0) {
-              S.act[s][qd] = bal;
-              S.kmin[s][qd] = key;
-            }
-            named_bar_sync(1 + s, 128);
-            if (row == 0) {
-              unsigned long long km = S.kmin[s][0];
-              int cnt = 0;
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                km = S.kmin[s][i] < km ? S.kmin[s][i] : km;
-                cnt += __popc(S.act[s][i]);
-              }
-              if (km != ~0ull) atomicMin(a.ds.wp_key + w, km);
-              int base = 0;
-              if (cnt > 0) {
-                const unsigned long long b = atomicAdd(a.ds.counter, (unsigned long long)cnt);
-                if (b + cnt > (unsigned long long)a.ds.max_active) {
-                  atomicOr(a.ds.counter + 1, 1ull);
-                  base = -1;
-                } else {
-                  base = (int)b;
+              for (int j = 0; j < 16; j += 4) {
+                const float4 b = *reinterpret_cast<const float4 *>(bp + j);
+                const float z0 = __uint_as_float(r[j]) + b.x, z1 = __uint_as_float(r[j + 1]) + b.y;
+                const float z2 = __uint_as_float(r[j + 2]) + b.z, z3 = __uint_as_float(r[j + 3]) + b.w;
+                const int jb = hf * 16 + j;
+                if (p < 4) {
+                  pk[j >> 1] = pack2_relu<F16>(z0, z1);
+                  pk[(j >> 1) + 1] = pack2_relu<F16>(z2, z3);
+                  m |= mask_group(pk[j >> 1], pk[(j >> 1) + 1], jb >> 2);
+                } else {  // layer 6: its mask is applied right here (e6), never stored
+                  const float4 w7 = *reinterpret_cast<const float4 *>(S.w7 + u0 + cb + j);
+                  fp = fmaf(w7.x, fmaxf(z0, 0.f), fp);
+                  fp = fmaf(w7.y, fmaxf(z1, 0.f), fp);
+                  fp = fmaf(w7.z, fmaxf(z2, 0.f), fp);
+                  fp = fmaf(w7.w, fmaxf(z3, 0.f), fp);
+                  pk[j >> 1] = pack2<F16>(z0 > 0.f ? w7.x : 0.f, z1 > 0.f ? w7.y : 0.f);
+                  pk[(j >> 1) + 1] = pack2<F16>(z2 > 0.f ? w7.z : 0.f, z3 > 0.f ? w7.w : 0.f);
                 }
               }
-              S.sbase[s] = base;
-              a.ds.tile_meta[T] = make_int2(base, cnt);
+              st8(tA + cb / 2, pk);
             }
-            named_bar_sync(1 + s, 128);
-            my_base = S.sbase[s];
-            my_rank = __popc(bal & ((1u << lane) - 1u));
-            for (int i = 0; i < qd; ++i) my_rank += __popc(S.act[s][i]);
-          } else if (slot < lb) {
-            a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
+            if (p < 4) mk[((p + 1) * 2 + c2) * kEpiPerSlot] = m;
+          }
+          wait_st();
+          fence_before();
+          mbar_arrive(&S.epi_done[s]);
+          if (p == 4) {
+            // f = w7 . h6 + b7 (fp32, no output activation: signed value)
+            S.fpart[s][hh][row] = fp;
+            named_bar_sync(1 + s, kEpiPerSlot);
+            f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
+            // A6/A7 (overlaps the next UMMA): threshold, per-tile slots, per-waypoint min key
+            if (hh == 0) {
+              if (a.detect) {
+                act = live && (f - a.delta <= a.tau);
+                const unsigned bal = __ballot_sync(0xffffffffu, act);
+                unsigned long long key = ~0ull;
+                if (live)
+                  key = ((unsigned long long)ord_f32(f) << 32) |
+                        (unsigned long long)local_to_global(slot, a.scene.rank, a.scene.world);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                  const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+                  key = other < key ? other : key;
+                }
+                if (lane == 0) {
+                  S.act[s][qd] = bal;
+                  S.kmin[s][qd] = key;
+                }
+                named_bar_sync(3 + s, 128);
+                if (row == 0) {
+                  unsigned long long km = S.kmin[s][0];
+                  int cnt = 0;
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) {
+                    km = S.kmin[s][i] < km ? S.kmin[s][i] : km;
+                    cnt += __popc(S.act[s][i]);
+                  }
+                  if (km != ~0ull) atomicMin(a.ds.wp_key + w, km);
+                  int base = 0;
+                  if (cnt > 0) {
+                    const unsigned long long b = atomicAdd(a.ds.counter, (unsigned long long)cnt);
+                    if (b + cnt > (unsigned long long)a.ds.max_active) {
+                      atomicOr(a.ds.counter + 1, 1ull);
+                      base = -1;
+                    } else {
+                      base = (int)b;
+                    }
+                  }
+                  S.sbase[s] = base;
+                  a.ds.tile_meta[T] = make_int2(base, cnt);
+                }
+                named_bar_sync(3 + s, 128);
+                my_base = S.sbase[s];
+                my_rank = __popc(bal & ((1u << lane) - 1u));
+                for (int i = 0; i < qd; ++i) my_rank += __popc(S.act[s][i]);
+              } else if (slot < lb) {
+                a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
+              }
+            }
           }
         } else if (p < 10) {
           // ---- backward: g_{l-1} = D; e_{l-1} = g (.) 1[z_{l-1} > 0] -> A ----
           const int mi = 9 - p;
 #pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4) {
-            uint32_t r[32], pk[16];
-            ld32(tD + c4 * 32, r);
-            wait_ld();
-            const uint32_t m = mask[mi][c4];
+          for (int c2 = 0; c2 < 2; ++c2) {
+            const uint32_t m = mk[(mi * 2 + c2) * kEpiPerSlot];
 #pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-              const float g0 = ((m >> j) & 1u) ? __uint_as_float(r[j]) : 0.f;
-              const float g1 = ((m >> (j + 1)) & 1u) ? __uint_as_float(r[j + 1]) : 0.f;
-              pk[j >> 1] = pack2<F16>(g0, g1);
+            for (int hf = 0; hf < 2; ++hf) {
+              uint32_t r[16], pk[8];
+              const int cb = c2 * 32 + hf * 16;
+              ld16(tD + cb, r);
+              wait_ld();
+#pragma unroll
+              for (int j = 0; j < 16; j += 4) {
+                uint32_t lo, hi;
+                mask_expand(m, (hf * 16 + j) >> 2, lo, hi);
+                pk[j >> 1] = pack2<F16>(__uint_as_float(r[j]), __uint_as_float(r[j + 1])) & lo;
+                pk[(j >> 1) + 1] = pack2<F16>(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])) & hi;
+              }
+              st8(tA + cb / 2, pk);
             }
-            st16(tA + c4 * 16, pk);
           }
           wait_st();
           fence_before();
           mbar_arrive(&S.epi_done[s]);
-        } else {
+        } else if (hh == 0) {
           // ---- g0 = W1^T e1 (16 columns); d f / d q by the chain rule (R3) ----
           uint32_t r[16];
-          ld16(tD, r);
+          ld16(tbase + (uint32_t)s * 256u + lane_off, r);
           wait_ld();
           float gq[kNdof];
           gq[0] = a.tgrad ? __uint_as_float(r[3]) : -__uint_as_float(r[0]);
@@ -343,8 +360,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
 }
 
 // ------------------------------------------------------------------ self-test kernel
-// One UMMA building block, for unit tests: A fp32 [128][128] -> bf16 TMEM, B fp32
-// [nrows][128] -> bf16 SW128 smem; mode 0: D = A B^T (K-major B, N = 128); mode 1:
+// One UMMA building block, for unit tests: A fp32 [128][128] -> 16-bit TMEM, B fp32
+// [nrows][128] -> 16-bit SW128 smem; mode 0: D = A B^T (K-major B, N = 128); mode 1:
 // D = A B (B read MN-major, N = 128); mode 2: D = A B^T with nrows = 16 (N = 16).
 template <bool F16>
 __global__ void __launch_bounds__(128, 1) k_selftest_umma(const float *A, const float *B, int mode, float *D) {
@@ -404,14 +421,13 @@ __global__ void __launch_bounds__(128, 1) k_selftest_umma(const float *A, const 
   fence_after();
   {
     const int m = warp * 32 + lane;
-    const int ncol = mode == 2 ? 16 : 128;
-    for (int c4 = 0; c4 < ncol / 32 + (ncol < 32); ++c4) {
-      if (ncol == 16) {
-        uint32_t r[16];
-        ld16(t0, r);
-        wait_ld();
-        for (int j = 0; j < 16; ++j) D[m * 128 + j] = __uint_as_float(r[j]);
-      } else {
+    if (mode == 2) {
+      uint32_t r[16];
+      ld16(t0, r);
+      wait_ld();
+      for (int j = 0; j < 16; ++j) D[m * 128 + j] = __uint_as_float(r[j]);
+    } else {
+      for (int c4 = 0; c4 < 4; ++c4) {
         uint32_t r[32];
         ld32(t0 + c4 * 32, r);
         wait_ld();

@@ -20,18 +20,28 @@ DEVI void mbar_init(uint64_t *bar, uint32_t count) {
 DEVI void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-DEVI void mbar_wait(uint64_t *bar, uint32_t parity) {
+DEVI bool mbar_try_wait(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n\t"
       ".reg .pred P1;\n\t"
-      "LAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE;\n\t"
-      "bra LAB_WAIT;\n\t"
-      "DONE:\n\t"
-      "}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t"
+      "}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+// Bounded wait: a protocol bug traps (the launch fails with an error) instead of hanging
+// the GPU; the bound (~2^34 cycles, seconds) is far above any legitimate wait.
+DEVI void mbar_wait(uint64_t *bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try_wait(addr, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait(addr, parity)) {
+    if (clock64() - t0 > (1ll << 34)) __trap();
+  }
 }
 DEVI void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 DEVI void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -95,6 +105,11 @@ DEVI void st16(uint32_t taddr, const uint32_t (&r)[16]) {
       "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
+DEVI void st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
 DEVI void st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -139,6 +154,29 @@ template <bool F16>
 DEVI uint32_t pack2_relu(float lo, float hi) {
   if constexpr (F16) return pack_f16_relu(lo, hi);
   else return pack_bf16_relu(lo, hi);
+}
+
+DEVI uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {  // byte permute; selector bit 3 = sign-replicate
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+
+// ReLU masks in "byte-sign" form.  A 32-unit chunk is stored in one word: unit e (group
+// k = e / 4, t = e % 4) at bit 8 t + 7 - k.
+// Build (forward): from the two packed ReLU'd 16-bit pairs of units 4k..4k+3 -- a
+// non-negative 16-bit value v is nonzero iff bit 15 of v + 0x7fff is set (no carry out of
+// the low half: |v| <= 0x7f7f) -- gather those bits into bytes 0..3 (prmt), shift by k.
+DEVI uint32_t mask_group(uint32_t pk01, uint32_t pk23, int k) {
+  const uint32_t v0 = pk01 + 0x7fff7fffu, v1 = pk23 + 0x7fff7fffu;
+  const uint32_t x = prmt(v0, v1, 0x7531u);  // bytes: (v0.b1, v0.b3, v1.b1, v1.b3) -> bit 7 of each
+  return (x >> k) & (0x80808080u >> k);
+}
+// Use (backward): 0xffff half-word masks for units (4k, 4k+1) and (4k+2, 4k+3).
+DEVI void mask_expand(uint32_t m, int k, uint32_t &lo, uint32_t &hi) {
+  const uint32_t y = m << k;
+  lo = prmt(y, 0u, 0x9988u);
+  hi = prmt(y, 0u, 0xbbaau);
 }
 
 // ------------------------------------------------------------------ descriptors
