@@ -204,6 +204,11 @@ int gcdf_profile_read(gcdf_ctx *ctx, double *mlp_ms, int64_t *mlp_launches, int 
 int gcdf_selftest_umma(int cuda_device, int mode, const float *A_dev, const float *B_dev, float *D_dev,
                        void *stream);
 
+/* Pipeline trace of the tensor-core kernel: when trace_dev (device, 624 int64) is non-NULL,
+   CTA 0 of every later query/detect records clock64 stamps [role 3][tile 4][phase 13][4]
+   (role 0 = MMA issuer, 1/2 = the slot-0/1 epilogue).  NULL switches it off. */
+int gcdf_debug_trace(gcdf_ctx *ctx, long long *trace_dev);
+
 #ifdef __cplusplus
 }
 #endif

@@ -42,7 +42,9 @@ constexpr int64_t kF32Total = kF32W1p + kF32W1q + kF32W1full + 10 * kF32Mat + 5 
 // bf16 block sizes (bytes)
 constexpr int64_t kBfMat = (int64_t)kMaxH * kMaxH * 2;
 constexpr int64_t kBfW1t = 16LL * kMaxH * 2;
-constexpr int64_t kBfTotal = 5 * kBfMat + kBfW1t;
+constexpr int64_t kBfB1 = 32LL * kMaxH * 2;    // layer-1 split weights [128][K = 32], no swizzle
+constexpr int64_t kBfBext = 16LL * kMaxH * 2;  // per hidden layer bias block [128][K = 16], no swizzle
+constexpr int64_t kBfTotal = 5 * kBfMat + kBfW1t + kBfB1 + 5 * kBfBext;
 
 }  // namespace
 
@@ -76,6 +78,7 @@ struct gcdf_ctx {
   int ev_used = 0;
   double prof_ms = 0.0;
   int64_t prof_n = 0;
+  long long *trace = nullptr;  // diagnostics buffer (device), see gcdf_debug_trace
 };
 
 namespace {
@@ -147,9 +150,8 @@ WeightsBF16 bf16_view(const gcdf_ctx *c) {
   const int64_t wo = c->opt.precision == GCDF_FP16 ? c->L.wf16 : c->L.wbf16;
   w.w_sw128 = c->ws + wo;
   w.w1t_sw128 = c->ws + wo + 5 * kBfMat;
-  w.w1p = f.w1p;
-  w.w1q = f.w1q;
-  w.bias = f.bias[0];  // the five bias vectors are contiguous [5][H]
+  w.b1_nosw = c->ws + wo + 5 * kBfMat + kBfW1t;
+  w.bext_nosw = c->ws + wo + 5 * kBfMat + kBfW1t + kBfB1;
   w.w7 = f.w7;
   w.b7 = f.b7;
   return w;
@@ -186,6 +188,30 @@ uint16_t to_f16_rne(float f) {
   uint16_t b;
   std::memcpy(&b, &h, 2);
   return b;
+}
+
+// UMMA canonical SWIZZLE_NONE, K-major: matrix [rows][K] 16-bit, rows % 8 == 0, K % 8 == 0:
+// 8-row x 16-B core matrices; core (n / 8, k / 8) at (k / 8) * (rows * 16) + (n / 8) * 128,
+// so one MMA K-step of 16 spans two K-cores LBO = rows * 16 bytes apart and the 8-row
+// groups are SBO = 128 bytes apart.
+void pack_nosw(const std::vector<float> &m, int rows, int K, uint16_t *dst, bool f16) {
+  for (int r = 0; r < rows; ++r)
+    for (int k = 0; k < K; ++k) {
+      const int64_t byte = (int64_t)(k / 8) * rows * 16 + (r / 8) * 128 + (r % 8) * 16 + (k % 8) * 2;
+      const float v = m[(size_t)r * K + k];
+      dst[byte / 2] = f16 ? to_f16_rne(v) : to_bf16_rne(v);
+    }
+}
+
+// hi/lo split of a value into two 16-bit operands (x ~= hi + lo to ~2^-22 relative for fp16)
+void split16(double x, bool f16, float &hi, float &lo) {
+  auto rnd = [&](float v) {
+    uint16_t b = f16 ? to_f16_rne(v) : to_bf16_rne(v);
+    if (f16) { __half h; std::memcpy(&h, &b, 2); return __half2float(h); }
+    uint32_t u = (uint32_t)b << 16; float g; std::memcpy(&g, &u, 4); return g;
+  };
+  hi = rnd((float)x);
+  lo = rnd((float)(x - (double)hi));
 }
 
 // UMMA canonical SWIZZLE_128B (K-major view): matrix [rows][cols] 16-bit, cols % 64 == 0.
@@ -410,6 +436,38 @@ int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
       for (int k = 0; k < H; ++k) w1t[(size_t)n * H + k] = W(0, k, n);
     pack_sw128(w1t, 16, H, bf.data() + (size_t)5 * kBfMat / 2, false);
     pack_sw128(w1t, 16, H, hf.data() + (size_t)5 * kBfMat / 2, true);
+    // layer 1 on the tensor cores, split in hi/lo 16-bit parts: K column 3 i + {0, 1, 2}
+    // multiplies A = {x_hi, x_lo, x_hi} by B = {w_hi, w_hi, w_lo} for the ten inputs
+    // i = [p'_x, p'_y, p_z, theta, j1..j6] (x_in columns 0, 1, 2, 5..11); columns 30, 31
+    // multiply A = 1 by {b_hi, b_lo}.  Hidden-layer biases: K column 0, 1 = {b_hi, b_lo}.
+    const int xin[10] = {0, 1, 2, 5, 6, 7, 8, 9, 10, 11};
+    for (int f16 = 0; f16 < 2; ++f16) {
+      uint16_t *dst = (f16 ? hf : bf).data();
+      std::vector<float> b1((size_t)H * 32, 0.f);
+      for (int u = 0; u < H; ++u) {
+        float hi, lo;
+        for (int i = 0; i < 10; ++i) {
+          split16(Wd[0][(size_t)u * kNin + xin[i]], f16, hi, lo);
+          b1[(size_t)u * 32 + 3 * i + 0] = hi;
+          b1[(size_t)u * 32 + 3 * i + 1] = hi;
+          b1[(size_t)u * 32 + 3 * i + 2] = lo;
+        }
+        split16(bd[0][u], f16, hi, lo);
+        b1[(size_t)u * 32 + 30] = hi;
+        b1[(size_t)u * 32 + 31] = lo;
+      }
+      pack_nosw(b1, H, 32, dst + (5 * kBfMat + kBfW1t) / 2, f16);
+      for (int li = 0; li < 5; ++li) {
+        std::vector<float> be((size_t)H * 16, 0.f);
+        for (int u = 0; u < H; ++u) {
+          float hi, lo;
+          split16(bd[li + 1][u], f16, hi, lo);
+          be[(size_t)u * 16 + 0] = hi;
+          be[(size_t)u * 16 + 1] = lo;
+        }
+        pack_nosw(be, H, 16, dst + (5 * kBfMat + kBfW1t + kBfB1 + li * kBfBext) / 2, f16);
+      }
+    }
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   CK(c, cudaMemcpyAsync(c->ws + c->L.wf32, f32.data(), f32.size() * 4, cudaMemcpyHostToDevice, s), "weights H2D");
@@ -511,6 +569,7 @@ static QueryArgs make_args(gcdf_ctx *c, const float *q, int32_t nwp) {
   a.n_wp = nwp;
   a.tiles_per_wp = (int32_t)(a.scene.local_bound / kTile);
   a.tgrad = c->opt.tgrad_mode;
+  a.trace = c->trace;
   return a;
 }
 
@@ -644,6 +703,12 @@ int gcdf_merge_active_sets(gcdf_ctx *c, int32_t world, int32_t n_wp, const gcdf_
   cudaError_t e = launch_merge(world, n_wp, recs, rec_stride, offsets, wp_key, out, cap, offs, wmin, warg, count,
                                static_cast<cudaStream_t>(stream), &nl);
   return count_launch(c, e, "merge", nl);
+}
+
+int gcdf_debug_trace(gcdf_ctx *c, long long *trace_dev) {
+  if (!c) return GCDF_ERR_INVALID_ARG;
+  c->trace = trace_dev;
+  return GCDF_OK;
 }
 
 int gcdf_selftest_umma(int dev, int mode, const float *A, const float *B, float *D, void *stream) {

@@ -36,12 +36,14 @@ struct WeightsF32 {
 // of row r stored at granule g ^ (r % 8).  The same bytes serve as a K-major B operand
 // (forward, N = out, K = in) and an MN-major B operand (backward, N = in, K = out).
 // w1t: W1^T restricted to the 12 input columns, padded to N = 16 rows, K-major SW128.
+// b1: layer 1 as a K = 32 GEMM on split hi/lo 16-bit operands (exact to ~fp32), and
+// bext: per hidden layer a K = 16 block {b_hi, b_lo, 0...} multiplied by a constant
+// "ones" A block -- both in the UMMA SWIZZLE_NONE K-major layout (gcdf_host.cpp).
 struct WeightsBF16 {
   const void *w_sw128;   // 5 * H * H * 2 bytes
   const void *w1t_sw128; // 16 * H * 2 bytes
-  const float4 *w1p;     // fp32, as WeightsF32
-  const float *w1q;
-  const float *bias;     // [5][H] fp32
+  const void *b1_nosw;   // H * 32 * 2 bytes
+  const void *bext_nosw; // 5 * H * 16 * 2 bytes
   const float *w7;       // [H] fp32
   float b7;
 };
@@ -74,7 +76,12 @@ struct QueryArgs {
   int32_t detect;
   float delta, tau;
   DetectScratch ds;
+  // diagnostics (gcdf_debug_trace): CTA 0 records clock64 stamps, NULL in normal runs
+  long long *trace;
 };
+// trace layout: [role 0 = MMA thread, 1 = slot-0 epilogue, 2 = slot-1 epilogue][tile 0..3][phase 0..12][4]
+constexpr int kTraceTiles = 4, kTracePhases = 13;
+constexpr int kTraceLen = 3 * kTraceTiles * kTracePhases * 4;
 
 __host__ __device__ inline int64_t local_to_global(int64_t slot, int rank, int world) {
   return ((slot / kTile) * world + rank) * kTile + slot % kTile;

@@ -6,25 +6,30 @@
 // value + gradient :394 (dense gradient R^{NM x n}); constraint f - delta >= 0 :362-363;
 // union = min :164; c_gcdf step-major order :414-435.  DESIGN.md §5 "K2b".
 //
-// Design (H = 128, one persistent CTA per SM, 640 threads = 20 warps):
-//   * The ten H x H hidden-layer GEMMs of a 128-pair tile run as UMMA 128x128x16 with
-//     A = activations (16-bit) in TMEM and B = W_l (16-bit) resident in shared memory for
-//     the whole kernel (5 x 32 KB, UMMA SWIZZLE_128B).  The same smem bytes are the
-//     K-major B of the forward GEMM (D = h W^T) and the MN-major B of the backward GEMM
-//     (D = e W).  The last backward GEMM g0 = e1 W1 is a 128x16x128 UMMA against W1^T.
+// Design (H = 128, one persistent CTA per SM, 512 threads = 16 warps, 128 registers each):
+//   * Every affine layer of a 128-pair tile is a UMMA with M = 128 pairs, A in TMEM and B
+//     resident in shared memory for the whole kernel:
+//       - layer 1 (12 -> 128): K = 32 of split hi/lo 16-bit operands (A = {x_hi, x_lo,
+//         x_hi}, B = {w_hi, w_hi, w_lo} per input, plus {1, 1} x {b_hi, b_lo}), which
+//         keeps the metre-scale point coordinates at ~fp32 accuracy (R16);
+//       - layers 2..6 (128 -> 128): K = 128 from the activations + one K = 16 step
+//         against a constant "ones" A block that adds the bias {b_hi, b_lo};
+//       - backward layers 6..2: D = E W_l with the same smem bytes read MN-major;
+//       - g0 = e1 W1: N = 16 rows of W1^T.
+//     W_2..W_6 use the UMMA SWIZZLE_128B layout (5 x 32 KB); the small K = 16 / 32 blocks
+//     the SWIZZLE_NONE layout.
 //   * Activations never leave the chip: accumulator D (fp32, 128 TMEM columns) ->
-//     epilogue registers (bias, ReLU, 1-bit mask, 16-bit pack) -> A (64 TMEM columns) ->
-//     next UMMA.  ReLU masks stay in registers (12 x 32 bit per thread) for the backward.
+//     epilogue registers (ReLU + 16-bit pack + 1-bit mask) -> A (64 TMEM columns) -> next
+//     UMMA.  ReLU masks go to shared memory (1 bit per unit) for the backward pass.
 //   * Two tiles in flight: TMEM columns [0,256) belong to slot 0 and [256,512) to slot
-//     1.  Each slot has 8 epilogue warps: warp (h, q) owns TMEM lanes 32q..32q+31 (the
-//     tile's pairs) and accumulator columns 64h..64h+63, so every SM sub-partition runs
-//     two warps per slot (latency hiding) and one slot's epilogue overlaps the other
-//     slot's tensor-core work.  One elected thread of warp 0 issues all UMMAs.
-//   * Layer 1 (12 -> H) runs in fp32 on the CUDA cores (3 FMA per unit per pair plus a
-//     per-waypoint constant), so the metre-scale point coordinates are never rounded
-//     to 16 bits (R16).
-//   * Synchronisation: mma_done[s] (tcgen05.commit -> mbarrier, count 1) and epi_done[s]
-//     (256 epilogue arrivals); 11 phases per tile.
+//     1 (D [0,128), A [128,192), ones [192,200)).  Each slot has 8 warps: warp (h, q) owns
+//     TMEM lanes 32q..32q+31 (the tile's pairs) and accumulator columns 64h..64h+63, so
+//     every SM sub-partition runs two warps per slot, and one slot's epilogue overlaps the
+//     other slot's tensor-core work.  There is no dedicated MMA warp: after each epilogue
+//     phase the slot's 256 threads meet at a named barrier and one elected thread issues
+//     the slot's next UMMAs and commits them to the slot's mbarrier (tcgen05.commit tracks
+//     the issuing thread's own MMAs); the tensor core executes both slots' MMAs in issue
+//     order.  12 MMA phases per tile.
 #include "gcdf_internal.h"
 #include "tc_ptx.h"
 
@@ -34,24 +39,29 @@ namespace {
 using namespace tc;
 
 constexpr int H = 128;
-constexpr int kWarps = 20;
+constexpr int kEpiWarps = 16;             // warps 0..15: epilogue (8 per tile slot)
+constexpr int kWarps = kEpiWarps + 1;     // warp 16: MMA issuer
 constexpr int kThreads = kWarps * 32;
 constexpr int kEpiPerSlot = 256;
-constexpr int kWBytes = 5 * H * H * 2;  // 163,840
-constexpr int kW1tBytes = 16 * H * 2;   // 4,096
+constexpr int kPhases = 12;               // MMA phases per tile
+constexpr int kMasks = 5;                 // stored ReLU masks: layers 1..5
+constexpr int kWBytes = 5 * H * H * 2;    // 163,840
+constexpr int kW1tBytes = 16 * H * 2;     // 4,096
+constexpr int kB1Bytes = 32 * H * 2;      // 8,192
+constexpr int kBextBytes = 16 * H * 2;    // 4,096 per hidden layer
+constexpr uint32_t kColA = 128, kColOnes = 192;
 template <bool F16> constexpr uint32_t kIdescFwd = idesc_f16kind(128, 128, false, F16);
 template <bool F16> constexpr uint32_t kIdescBwd = idesc_f16kind(128, 128, true, F16);
 template <bool F16> constexpr uint32_t kIdescFin = idesc_f16kind(128, 16, false, F16);
 
 struct __align__(1024) SmemTC {
-  uint8_t w[kWBytes];        // W_2..W_6, SW128 [2 chunks][128 rows][128 B] each
-  uint8_t w1t[kW1tBytes];    // W1^T [16][128], SW128
-  float4 w1c[2][H];          // per slot: {W1[u][0], W1[u][1], W1[u][2], c_u(waypoint)}
-  float w1q[H * 8];
-  float bias[5 * H];
+  uint8_t w[kWBytes];          // W_2..W_6, SW128 [2 chunks][128 rows][128 B] each
+  uint8_t w1t[kW1tBytes];      // W1^T [16][128], SW128
+  uint8_t b1[kB1Bytes];        // layer-1 split weights [128][32], no swizzle
+  uint8_t bext[5][kBextBytes]; // hidden-layer bias blocks [128][16], no swizzle
   float w7[H];
-  float fpart[2][2][H];      // [slot][half][row] partial output-layer sums
-  uint32_t mask[2][kHidden][2][kEpiPerSlot];  // ReLU masks: [slot][layer][32-unit word][thread]
+  float fpart[2][2][H];        // [slot][half][row] partial output-layer sums
+  uint32_t mask[2][kMasks][2][kEpiPerSlot];  // ReLU masks [slot][layer][32-unit word][thread]
   uint64_t mma_done[2];
   uint64_t epi_done[2];
   unsigned act[2][4];
@@ -65,6 +75,51 @@ DEVI unsigned ord_f32(float f) {
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
+template <bool F16>
+DEVI float round16(float x) {
+  const uint32_t p = pack2<F16>(x, 0.f);
+  if constexpr (F16) {
+    float f;
+    asm("{\n\t.reg .b16 t;\n\tmov.b16 t, %1;\n\tcvt.f32.f16 %0, t;\n\t}" : "=f"(f) : "h"((unsigned short)(p & 0xffffu)));
+    return f;
+  } else {
+    return __uint_as_float(p << 16);
+  }
+}
+
+// A1 operand values of the split layer-1 GEMM for one input x: {x_hi, x_lo, x_hi}
+template <bool F16>
+DEVI void split3(float x, float *o) {
+  const float hi = round16<F16>(x);
+  o[0] = hi;
+  o[1] = x - hi;  // exact in fp32; rounded to 16 bits by the pack
+  o[2] = hi;
+}
+
+// UMMAs of MMA phase p of the tile in slot s (one thread); commit to mma_done[s]
+template <bool F16>
+DEVI void issue_phase(int p, uint32_t d, uint32_t sw, uint32_t sw1t, uint32_t sb1, uint32_t sbx, uint64_t *bar) {
+  const uint32_t av = d + kColA;
+  if (p == 0) {  // layer 1: K = 32 split operands (bias included)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) mma_ts(d, av + 8u * k, sdesc_nosw(sb1 + k * 2 * 2048, 2048, 128), kIdescFwd<F16>, k > 0);
+  } else if (p < 6) {  // layer l = p + 1: D = A W_l^T (B = W_l K-major) + ones x bias
+    const uint32_t wb = sw + (uint32_t)(p - 1) * (H * H * 2);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      mma_ts(d, av + 8u * k, sdesc_sw128(wb + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024), kIdescFwd<F16>, k > 0);
+    mma_ts(d, d + kColOnes, sdesc_nosw(sbx + (uint32_t)(p - 1) * kBextBytes, 2048, 128), kIdescFwd<F16>, 1u);
+  } else if (p < 11) {  // backward through layer l = 12 - p: D = E W_l, B = W_l MN-major
+    const uint32_t wb = sw + (uint32_t)(10 - p) * (H * H * 2);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) mma_ts(d, av + 8u * k, sdesc_sw128(wb + k * 2048, 16384, 1024), kIdescBwd<F16>, k > 0);
+  } else {  // g0 = e1 W1 (N = 16 rows of W1^T)
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      mma_ts(d, av + 8u * k, sdesc_sw128(sw1t + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin<F16>, k > 0);
+  }
+  commit(bar);
+}
 
 template <bool F16>
 __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, const QueryArgs a) {
@@ -74,16 +129,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   SmemTC &S = *reinterpret_cast<SmemTC *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // ---- one-time setup: weights -> smem (already in UMMA layout in global memory) ----
+  // ---- one-time setup: weights -> smem (already in UMMA layouts in global memory) ----
   {
-    const uint4 *src = reinterpret_cast<const uint4 *>(W.w_sw128);
-    uint4 *dst = reinterpret_cast<uint4 *>(S.w);
-    for (int i = tid; i < kWBytes / 16; i += kThreads) dst[i] = __ldg(src + i);
-    const uint4 *src1 = reinterpret_cast<const uint4 *>(W.w1t_sw128);
-    uint4 *dst1 = reinterpret_cast<uint4 *>(S.w1t);
-    for (int i = tid; i < kW1tBytes / 16; i += kThreads) dst1[i] = __ldg(src1 + i);
-    for (int i = tid; i < H * 8; i += kThreads) S.w1q[i] = __ldg(W.w1q + i);
-    for (int i = tid; i < 5 * H; i += kThreads) S.bias[i] = __ldg(W.bias + i);
+    auto copy16 = [&](void *dst, const void *src, int bytes) {
+      const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+      uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+      for (int i = tid; i < bytes / 16; i += kThreads) d4[i] = __ldg(s4 + i);
+    };
+    copy16(S.w, W.w_sw128, kWBytes);
+    copy16(S.w1t, W.w1t_sw128, kW1tBytes);
+    copy16(S.b1, W.b1_nosw, kB1Bytes);
+    copy16(S.bext, W.bext_nosw, 5 * kBextBytes);
     for (int i = tid; i < H; i += kThreads) S.w7[i] = __ldg(W.w7 + i);
   }
   if (warp == 0) {
@@ -104,251 +160,263 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   const uint32_t tbase = S.tmem_base;
   const int64_t n_tiles = (int64_t)a.n_wp * a.tiles_per_wp;
   const int64_t lb = a.scene.local_bound;
+  const uint32_t sw = smem_u32(S.w), sw1t = smem_u32(S.w1t), sb1 = smem_u32(S.b1), sbx = smem_u32(S.bext);
 
-  if (warp == 0) {
-    // =========================== MMA issuer (one thread) ===========================
+  if (warp == kEpiWarps) {
+    // ===================== dedicated MMA warp: one thread issues both slots' UMMAs ==========
     if (lane == 0) {
-      const uint32_t sw = smem_u32(S.w), sw1t = smem_u32(S.w1t);
       uint32_t phbits = 0u;  // bit s = phase parity of epi_done[s]
       for (int64_t base = (int64_t)blockIdx.x * 2; base < n_tiles; base += 2 * (int64_t)gridDim.x) {
         const int nslots = (base + 1 < n_tiles) ? 2 : 1;
 #pragma unroll 1
-        for (int p = 0; p < 11; ++p) {
+        for (int p = 0; p < kPhases; ++p) {
 #pragma unroll 1
-          for (int s = 0; s < nslots; ++s) {
-            mbar_wait(&S.epi_done[s], (phbits >> s) & 1u);
-            phbits ^= 1u << s;
+          for (int ss = 0; ss < nslots; ++ss) {
+            mbar_wait(&S.epi_done[ss], (phbits >> ss) & 1u);
+            phbits ^= 1u << ss;
             fence_after();
-            const uint32_t d = tbase + (uint32_t)s * 256u, av = d + 128u;
-            if (p < 5) {  // forward, layer l = p + 2: D = A W_l^T, B = W_l K-major
-              const uint32_t wb = sw + (uint32_t)p * (H * H * 2);
-#pragma unroll
-              for (int k = 0; k < 8; ++k)
-                mma_ts(d, av + 8u * k, sdesc_sw128(wb + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024), kIdescFwd<F16>,
-                       k > 0);
-            } else if (p < 10) {  // backward through layer l = 11 - p: D = E W_l, B = W_l MN-major
-              const uint32_t wb = sw + (uint32_t)(9 - p) * (H * H * 2);
-#pragma unroll
-              for (int k = 0; k < 8; ++k)
-                mma_ts(d, av + 8u * k, sdesc_sw128(wb + k * 2048, 16384, 1024), kIdescBwd<F16>, k > 0);
-            } else {  // g0 = e1 W1 (N = 16 rows of W1^T)
-#pragma unroll
-              for (int k = 0; k < 8; ++k)
-                mma_ts(d, av + 8u * k, sdesc_sw128(sw1t + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin<F16>,
-                       k > 0);
-            }
-            commit(&S.mma_done[s]);
+            issue_phase<F16>(p, tbase + (uint32_t)ss * 256u, sw, sw1t, sb1, sbx, &S.mma_done[ss]);
           }
         }
       }
     }
     __syncwarp();
-  } else if (warp >= 4) {
-    // =========================== epilogue warps ===========================
-    const int e = warp - 4;
-    const int s = e >> 3;             // tile slot
-    const int hh = (e >> 2) & 1;      // accumulator column half: units 64 hh .. 64 hh + 63
-    const int qd = warp & 3;          // TMEM lane quarter of this warp (warp % 4)
-    const int row = qd * 32 + lane;   // pair within the tile = TMEM lane
-    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-    const uint32_t tD = tbase + (uint32_t)s * 256u + lane_off + 64u * hh;
-    const uint32_t tA = tbase + (uint32_t)s * 256u + 128u + lane_off + 32u * hh;
-    const int u0 = 64 * hh;           // first unit of this thread's columns
-    uint32_t ph = 0u;
-    for (int64_t T = (int64_t)blockIdx.x * 2 + s; T < n_tiles; T += 2 * (int64_t)gridDim.x) {
-      const int w = (int)(T / a.tiles_per_wp);
-      const int64_t slot = (T % a.tiles_per_wp) * kTile + row;
-      const float *qw = a.q + (int64_t)w * kNdof;
-      // A2: pair generation + base-frame bias p' = p - [q_x, q_y, 0]
-      const float4 pt = slot < lb ? __ldg(a.scene.pts + slot) : make_float4(0.f, 0.f, 0.f, 0.f);
-      const bool live = slot < lb && pt.w > 0.f;
-      const float px = pt.x - __ldg(qw), py = pt.y - __ldg(qw + 1), pz = pt.z;
-      // layer-1 constant of this waypoint for unit u = row: c = b1 + W1[u, 5:12] . [theta, j1..j6]
+    fence_before();
+    __syncthreads();
+    return;  // (TMEM is freed by warp 0 after the final barrier)
+  }
+  const int s = warp >> 3;          // tile slot
+  const int hh = (warp >> 2) & 1;   // accumulator column half: units 64 hh .. 64 hh + 63
+  const int qd = warp & 3;          // TMEM lane quarter of this warp (warp % 4)
+  const int row = qd * 32 + lane;   // pair within the tile = TMEM lane
+  const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+  const uint32_t tSlot = tbase + (uint32_t)s * 256u;  // MMA-side column base of this slot
+  const uint32_t tS = tSlot + lane_off;                 // this slot, this lane quarter
+  const uint32_t tD = tS + 64u * hh;
+  const uint32_t tA = tS + kColA + 32u * hh;
+  const int u0 = 64 * hh;           // first unit of this thread's columns
+  uint32_t *mk = &S.mask[s][0][0][hh * 128 + row];  // + (layer * 2 + word) * kEpiPerSlot
+  if (hh == 0) {  // the constant "ones" A block of the bias GEMM step: {1, 1, 0, ...}
+    uint32_t ones[8] = {pack2<F16>(1.f, 1.f), 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    st8(tS + kColOnes, ones);
+  }
+  // epilogue phase done: TMEM stores complete and ordered before the MMA warp's UMMAs
+  auto hand_off = [&](int) {
+    wait_st();
+    fence_before();
+    mbar_arrive(&S.epi_done[s]);
+  };
+  (void)tSlot;
+  uint32_t ph = 0u;
+  int it = 0;
+  const bool tracer = a.trace && blockIdx.x == 0 && hh == 0 && qd == 0 && lane == 0;
+  int w_prev = -1;
+  uint32_t qwords[8];  // the per-waypoint part of this half's A1 words
+  float q0h = 0.f;
+  // point of this lane's pair in the next tile, prefetched during the current tile
+  auto load_pt = [&](int64_t TT) -> float4 {
+    if (TT >= n_tiles) return make_float4(0.f, 0.f, 0.f, 0.f);
+    const int64_t sl = (TT % a.tiles_per_wp) * kTile + row;
+    return sl < lb ? __ldg(a.scene.pts + sl) : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  float4 pt_next = load_pt((int64_t)blockIdx.x * 2 + s);
+  for (int64_t T = (int64_t)blockIdx.x * 2 + s; T < n_tiles; T += 2 * (int64_t)gridDim.x, ++it) {
+    long long *tr = (tracer && it < kTraceTiles) ? a.trace + (size_t)((1 + s) * kTraceTiles + it) * kTracePhases * 4 : nullptr;
+    if (tr) tr[0] = clock64();
+    const int w = (int)(T / a.tiles_per_wp);
+    const int64_t slot = (T % a.tiles_per_wp) * kTile + row;
+    const float *qw = a.q + (int64_t)w * kNdof;
+    if (w != w_prev) {  // split the waypoint's [theta, j1..j6] once per waypoint
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 7; ++i) split3<F16>(__ldg(qw + 2 + i), v + 9 + 3 * i);
+      v[30] = 1.f;
+      v[31] = 1.f;
+      q0h = v[9];
+      // half 0 owns A1 words 0..7 (K 0..15): words 5..7 are per-waypoint (K 10..15);
+      // half 1 owns words 8..15 (K 16..31): all per-waypoint
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int kk = hh == 0 ? 2 * i : 16 + 2 * i;
+        qwords[i] = (hh == 0 && i < 5) ? 0u : pack2<F16>(v[kk], v[kk + 1]);
+      }
+      w_prev = w;
+    }
+    // A2: pair generation + base-frame bias p' = p - [q_x, q_y, 0]
+    const float4 pt = pt_next;
+    const bool live = slot < lb && pt.w > 0.f;
+    // ---- A1: the split layer-1 operands of this pair -> TMEM A ----
+    {
+      uint32_t a1[8];
       if (hh == 0) {
-        const float4 wv = __ldg(W.w1p + row);
-        float c = wv.w;
+        float v[10];
+        split3<F16>(pt.x - __ldg(qw), v);
+        split3<F16>(pt.y - __ldg(qw + 1), v + 3);
+        split3<F16>(pt.z, v + 6);
+        v[9] = q0h;
 #pragma unroll
-        for (int i = 0; i < 7; ++i) c = fmaf(S.w1q[row * 8 + i], __ldg(qw + 2 + i), c);
-        S.w1c[s][row] = make_float4(wv.x, wv.y, wv.z, c);
+        for (int i = 0; i < 5; ++i) a1[i] = pack2<F16>(v[2 * i], v[2 * i + 1]);
+#pragma unroll
+        for (int i = 5; i < 8; ++i) a1[i] = qwords[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a1[i] = qwords[i];
       }
-      named_bar_sync(1 + s, kEpiPerSlot);
+      st8(tS + kColA + 8u * hh, a1);
+    }
+    if (tr) tr[2] = clock64();
+    hand_off(0);
+    if (tr) tr[3] = clock64();
 
-      uint32_t *mk = &S.mask[s][0][0][hh * 128 + row];  // + (layer * 2 + word) * kEpiPerSlot
-      // ---- E0: layer 1 in fp32 on CUDA cores -> h1 (16-bit) into TMEM A ----
-#pragma unroll
-      for (int c2 = 0; c2 < 2; ++c2) {
-        uint32_t pk[16], m = 0u;
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          float z[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float4 a0 = S.w1c[s][u0 + c2 * 32 + j + i];
-            z[i] = fmaf(a0.x, px, fmaf(a0.y, py, fmaf(a0.z, pz, a0.w)));
-          }
-          pk[j >> 1] = pack2_relu<F16>(z[0], z[1]);
-          pk[(j >> 1) + 1] = pack2_relu<F16>(z[2], z[3]);
-          m |= mask_group(pk[j >> 1], pk[(j >> 1) + 1], j >> 2);
-        }
-        mk[c2 * kEpiPerSlot] = m;
-        st16(tA + c2 * 16, pk);
-      }
-      wait_st();
-      fence_before();
-      mbar_arrive(&S.epi_done[s]);
-
-      float f = 0.f;
-      bool act = false;
-      int my_base = -1, my_rank = 0;
+    float f = 0.f;
+    bool act = false;
+    int my_base = -1, my_rank = 0;
 #pragma unroll 1
-      for (int p = 0; p < 11; ++p) {
-        mbar_wait(&S.mma_done[s], ph);
-        ph ^= 1u;
-        fence_after();
-        if (p < 5) {
-          // ---- forward hidden layer l = p + 2: z = D + b, h = ReLU(z) -> A ----
-          //      (l = 6: f += w7 . h6 in fp32, e6 = w7 (.) 1[z6 > 0] -> A)
-          float fp = 0.f;
+    for (int p = 0; p < kPhases; ++p) {
+      mbar_wait(&S.mma_done[s], ph);
+      if (tr) tr[(p + 1) * 4 + 1] = clock64();
+      ph ^= 1u;
+      fence_after();
+      if (p < 6) {
+        // ---- forward layer l = p + 1: z = D (bias folded in); h = ReLU(z) -> A ----
+        //      (l = 6: f += w7 . h6 in fp32, e6 = w7 (.) 1[z6 > 0] -> A)
+        float fp = 0.f;
 #pragma unroll
-          for (int c2 = 0; c2 < 2; ++c2) {
-            uint32_t m = 0u;
+        for (int c2 = 0; c2 < 2; ++c2) {
+          uint32_t m = 0u;
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {  // 16 accumulator columns per TMEM load
-              uint32_t r[16], pk[8];
-              const int cb = c2 * 32 + hf * 16;
-              ld16(tD + cb, r);
-              wait_ld();
-              const float *bp = S.bias + p * H + u0 + cb;
+          for (int hf = 0; hf < 2; ++hf) {
+            uint32_t pk[8], rr[16];
+            const int cb = c2 * 32 + hf * 16;
+            ld16(tD + cb, rr);
+            wait_ld();
+            if (tr && cb == 0) tr[(p + 1) * 4 + 0] = clock64();
 #pragma unroll
-              for (int j = 0; j < 16; j += 4) {
-                const float4 b = *reinterpret_cast<const float4 *>(bp + j);
-                const float z0 = __uint_as_float(r[j]) + b.x, z1 = __uint_as_float(r[j + 1]) + b.y;
-                const float z2 = __uint_as_float(r[j + 2]) + b.z, z3 = __uint_as_float(r[j + 3]) + b.w;
-                const int jb = hf * 16 + j;
-                if (p < 4) {
-                  pk[j >> 1] = pack2_relu<F16>(z0, z1);
-                  pk[(j >> 1) + 1] = pack2_relu<F16>(z2, z3);
-                  m |= mask_group(pk[j >> 1], pk[(j >> 1) + 1], jb >> 2);
-                } else {  // layer 6: its mask is applied right here (e6), never stored
-                  const float4 w7 = *reinterpret_cast<const float4 *>(S.w7 + u0 + cb + j);
-                  fp = fmaf(w7.x, fmaxf(z0, 0.f), fp);
-                  fp = fmaf(w7.y, fmaxf(z1, 0.f), fp);
-                  fp = fmaf(w7.z, fmaxf(z2, 0.f), fp);
-                  fp = fmaf(w7.w, fmaxf(z3, 0.f), fp);
-                  pk[j >> 1] = pack2<F16>(z0 > 0.f ? w7.x : 0.f, z1 > 0.f ? w7.y : 0.f);
-                  pk[(j >> 1) + 1] = pack2<F16>(z2 > 0.f ? w7.z : 0.f, z3 > 0.f ? w7.w : 0.f);
-                }
-              }
-              st8(tA + cb / 2, pk);
-            }
-            if (p < 4) mk[((p + 1) * 2 + c2) * kEpiPerSlot] = m;
-          }
-          wait_st();
-          fence_before();
-          mbar_arrive(&S.epi_done[s]);
-          if (p == 4) {
-            // f = w7 . h6 + b7 (fp32, no output activation: signed value)
-            S.fpart[s][hh][row] = fp;
-            named_bar_sync(1 + s, kEpiPerSlot);
-            f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
-            // A6/A7 (overlaps the next UMMA): threshold, per-tile slots, per-waypoint min key
-            if (hh == 0) {
-              if (a.detect) {
-                act = live && (f - a.delta <= a.tau);
-                const unsigned bal = __ballot_sync(0xffffffffu, act);
-                unsigned long long key = ~0ull;
-                if (live)
-                  key = ((unsigned long long)ord_f32(f) << 32) |
-                        (unsigned long long)local_to_global(slot, a.scene.rank, a.scene.world);
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                  const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-                  key = other < key ? other : key;
-                }
-                if (lane == 0) {
-                  S.act[s][qd] = bal;
-                  S.kmin[s][qd] = key;
-                }
-                named_bar_sync(3 + s, 128);
-                if (row == 0) {
-                  unsigned long long km = S.kmin[s][0];
-                  int cnt = 0;
-#pragma unroll
-                  for (int i = 0; i < 4; ++i) {
-                    km = S.kmin[s][i] < km ? S.kmin[s][i] : km;
-                    cnt += __popc(S.act[s][i]);
-                  }
-                  if (km != ~0ull) atomicMin(a.ds.wp_key + w, km);
-                  int base = 0;
-                  if (cnt > 0) {
-                    const unsigned long long b = atomicAdd(a.ds.counter, (unsigned long long)cnt);
-                    if (b + cnt > (unsigned long long)a.ds.max_active) {
-                      atomicOr(a.ds.counter + 1, 1ull);
-                      base = -1;
-                    } else {
-                      base = (int)b;
-                    }
-                  }
-                  S.sbase[s] = base;
-                  a.ds.tile_meta[T] = make_int2(base, cnt);
-                }
-                named_bar_sync(3 + s, 128);
-                my_base = S.sbase[s];
-                my_rank = __popc(bal & ((1u << lane) - 1u));
-                for (int i = 0; i < qd; ++i) my_rank += __popc(S.act[s][i]);
-              } else if (slot < lb) {
-                a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
+            for (int j = 0; j < 16; j += 4) {
+              const float z0 = __uint_as_float(rr[j]), z1 = __uint_as_float(rr[j + 1]);
+              const float z2 = __uint_as_float(rr[j + 2]), z3 = __uint_as_float(rr[j + 3]);
+              if (p < 5) {
+                pk[j >> 1] = pack2_relu<F16>(z0, z1);
+                pk[(j >> 1) + 1] = pack2_relu<F16>(z2, z3);
+                m |= mask_group(pk[j >> 1], pk[(j >> 1) + 1], (hf * 16 + j) >> 2);
+              } else {  // layer 6: its mask is applied right here (e6), never stored
+                const float4 w7 = *reinterpret_cast<const float4 *>(S.w7 + u0 + cb + j);
+                fp = fmaf(w7.x, fmaxf(z0, 0.f), fp);
+                fp = fmaf(w7.y, fmaxf(z1, 0.f), fp);
+                fp = fmaf(w7.z, fmaxf(z2, 0.f), fp);
+                fp = fmaf(w7.w, fmaxf(z3, 0.f), fp);
+                pk[j >> 1] = pack2<F16>(z0 > 0.f ? w7.x : 0.f, z1 > 0.f ? w7.y : 0.f);
+                pk[(j >> 1) + 1] = pack2<F16>(z2 > 0.f ? w7.z : 0.f, z3 > 0.f ? w7.w : 0.f);
               }
             }
+            st8(tA + cb / 2, pk);
           }
-        } else if (p < 10) {
-          // ---- backward: g_{l-1} = D; e_{l-1} = g (.) 1[z_{l-1} > 0] -> A ----
-          const int mi = 9 - p;
+          if (p < 5) mk[(p * 2 + c2) * kEpiPerSlot] = m;
+        }
+        if (tr) tr[(p + 1) * 4 + 2] = clock64();
+        hand_off(p + 1);
+        if (tr) tr[(p + 1) * 4 + 3] = clock64();
+        if (p == 5) {
+          // f = w7 . h6 + b7 (fp32, no output activation: signed value)
+          S.fpart[s][hh][row] = fp;
+          named_bar_sync(1 + s, kEpiPerSlot);
+          f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
+          if (hh == 0 && !a.detect && slot < lb)
+            a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
+        }
+      } else if (p < 11) {
+        // ---- backward: g_{l-1} = D; e_{l-1} = g (.) 1[z_{l-1} > 0] -> A ----
+        const int mi = 10 - p;
 #pragma unroll
-          for (int c2 = 0; c2 < 2; ++c2) {
-            const uint32_t m = mk[(mi * 2 + c2) * kEpiPerSlot];
+        for (int c2 = 0; c2 < 2; ++c2) {
+          const uint32_t m = mk[(mi * 2 + c2) * kEpiPerSlot];
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-              uint32_t r[16], pk[8];
-              const int cb = c2 * 32 + hf * 16;
-              ld16(tD + cb, r);
-              wait_ld();
+          for (int hf = 0; hf < 2; ++hf) {
+            uint32_t pk[8], rr[16];
+            ld16(tD + 32 * c2 + 16 * hf, rr);
+            wait_ld();
+            if (tr && c2 + hf == 0) tr[(p + 1) * 4 + 0] = clock64();
 #pragma unroll
-              for (int j = 0; j < 16; j += 4) {
-                uint32_t lo, hi;
-                mask_expand(m, (hf * 16 + j) >> 2, lo, hi);
-                pk[j >> 1] = pack2<F16>(__uint_as_float(r[j]), __uint_as_float(r[j + 1])) & lo;
-                pk[(j >> 1) + 1] = pack2<F16>(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])) & hi;
+            for (int j = 0; j < 16; j += 4) {
+              uint32_t lo, hi;
+              mask_expand(m, (hf * 16 + j) >> 2, lo, hi);
+              pk[j >> 1] = pack2<F16>(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1])) & lo;
+              pk[(j >> 1) + 1] = pack2<F16>(__uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3])) & hi;
+            }
+            st8(tA + 16 * c2 + 8 * hf, pk);
+          }
+        }
+        if (tr) tr[(p + 1) * 4 + 2] = clock64();
+        hand_off(p + 1);
+        if (tr) tr[(p + 1) * 4 + 3] = clock64();
+        if (p == 6 && hh == 0 && a.detect) {
+          // A6/A7 (overlaps the tensor core): threshold, per-tile slots, per-waypoint min key
+          act = live && (f - a.delta <= a.tau);
+          const unsigned bal = __ballot_sync(0xffffffffu, act);
+          unsigned long long key = ~0ull;
+          if (live)
+            key = ((unsigned long long)ord_f32(f) << 32) |
+                  (unsigned long long)local_to_global(slot, a.scene.rank, a.scene.world);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+            key = other < key ? other : key;
+          }
+          if (lane == 0) {
+            S.act[s][qd] = bal;
+            S.kmin[s][qd] = key;
+          }
+          named_bar_sync(3 + s, 128);
+          if (row == 0) {
+            unsigned long long km = S.kmin[s][0];
+            int cnt = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              km = S.kmin[s][i] < km ? S.kmin[s][i] : km;
+              cnt += __popc(S.act[s][i]);
+            }
+            if (km != ~0ull) atomicMin(a.ds.wp_key + w, km);
+            int base = 0;
+            if (cnt > 0) {
+              const unsigned long long b = atomicAdd(a.ds.counter, (unsigned long long)cnt);
+              if (b + cnt > (unsigned long long)a.ds.max_active) {
+                atomicOr(a.ds.counter + 1, 1ull);
+                base = -1;
+              } else {
+                base = (int)b;
               }
-              st8(tA + cb / 2, pk);
             }
+            S.sbase[s] = base;
+            a.ds.tile_meta[T] = make_int2(base, cnt);
           }
-          wait_st();
-          fence_before();
-          mbar_arrive(&S.epi_done[s]);
-        } else if (hh == 0) {
-          // ---- g0 = W1^T e1 (16 columns); d f / d q by the chain rule (R3) ----
-          uint32_t r[16];
-          ld16(tbase + (uint32_t)s * 256u + lane_off, r);
-          wait_ld();
-          float gq[kNdof];
-          gq[0] = a.tgrad ? __uint_as_float(r[3]) : -__uint_as_float(r[0]);
-          gq[1] = a.tgrad ? __uint_as_float(r[4]) : -__uint_as_float(r[1]);
+          named_bar_sync(3 + s, 128);
+          my_base = S.sbase[s];
+          my_rank = __popc(bal & ((1u << lane) - 1u));
+          for (int i = 0; i < qd; ++i) my_rank += __popc(S.act[s][i]);
+        }
+        if (p == 7) pt_next = load_pt(T + 2 * (int64_t)gridDim.x);  // latency hidden by 4 phases
+      } else if (hh == 0) {
+        // ---- g0 = W1^T e1 (16 columns); d f / d q by the chain rule (R3) ----
+        uint32_t r[16];
+        ld16(tS, r);
+        wait_ld();
+        float gq[kNdof];
+        gq[0] = a.tgrad ? __uint_as_float(r[3]) : -__uint_as_float(r[0]);
+        gq[1] = a.tgrad ? __uint_as_float(r[4]) : -__uint_as_float(r[1]);
 #pragma unroll
-          for (int i = 0; i < 7; ++i) gq[2 + i] = __uint_as_float(r[5 + i]);
-          if (a.detect) {
-            if (act && my_base >= 0) {
-              float4 *dst = reinterpret_cast<float4 *>(a.ds.staging + my_base + my_rank);
-              dst[0] = make_float4(f, gq[0], gq[1], gq[2]);
-              dst[1] = make_float4(gq[3], gq[4], gq[5], gq[6]);
-              dst[2] = make_float4(gq[7], gq[8], __uint_as_float((unsigned)w),
-                                   __uint_as_float((unsigned)local_to_global(slot, a.scene.rank, a.scene.world)));
-            }
-          } else if (a.grads && slot < lb) {
-            float *o = a.grads + ((int64_t)w * lb + slot) * kNdof;
-#pragma unroll
-            for (int i = 0; i < kNdof; ++i) o[i] = live ? gq[i] : 0.f;
+        for (int i = 0; i < 7; ++i) gq[2 + i] = __uint_as_float(r[5 + i]);
+        if (a.detect) {
+          if (act && my_base >= 0) {
+            float4 *dst = reinterpret_cast<float4 *>(a.ds.staging + my_base + my_rank);
+            dst[0] = make_float4(f, gq[0], gq[1], gq[2]);
+            dst[1] = make_float4(gq[3], gq[4], gq[5], gq[6]);
+            dst[2] = make_float4(gq[7], gq[8], __uint_as_float((unsigned)w),
+                                 __uint_as_float((unsigned)local_to_global(slot, a.scene.rank, a.scene.world)));
           }
+        } else if (a.grads && slot < lb) {
+          float *o = a.grads + ((int64_t)w * lb + slot) * kNdof;
+#pragma unroll
+          for (int i = 0; i < kNdof; ++i) o[i] = live ? gq[i] : 0.f;
         }
       }
     }

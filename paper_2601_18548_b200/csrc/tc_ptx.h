@@ -182,6 +182,12 @@ DEVI void mask_expand(uint32_t m, int k, uint32_t &lo, uint32_t &hi) {
 // ------------------------------------------------------------------ descriptors
 // Shared-memory matrix descriptor (tcgen05): start>>4 [0,14), LBO>>4 [16,30),
 // SBO>>4 [32,46), version 1 [46,48), base offset 0 [49,52), layout SWIZZLE_128B = 2 [61,64).
+// SWIZZLE_NONE (layout 0): 8-row x 16-B core matrices; K-major LBO = distance between the
+// two K cores of one K = 16 step, SBO = distance between 8-row groups.
+DEVI uint64_t sdesc_nosw(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
 DEVI uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16) |
          ((uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);

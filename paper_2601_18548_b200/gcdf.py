@@ -26,7 +26,7 @@ EXPORTED = ["gcdf_default_options", "gcdf_create", "gcdf_destroy", "gcdf_last_er
             "gcdf_workspace_bytes", "gcdf_bind_workspace", "gcdf_load_weights", "gcdf_update_scene",
             "gcdf_scene_info", "gcdf_pairgen_transform", "gcdf_query_values_grads", "gcdf_detect_active_set",
             "gcdf_compact_dense", "gcdf_merge_active_sets", "gcdf_launch_count", "gcdf_profile_enable",
-            "gcdf_profile_read", "gcdf_selftest_umma"]
+            "gcdf_profile_read", "gcdf_selftest_umma", "gcdf_debug_trace"]
 
 
 class GcdfError(RuntimeError):
@@ -77,6 +77,7 @@ def load_library(path: str | Path = LIB_PATH):
     lib.gcdf_profile_enable.argtypes = [P, C.c_int]
     lib.gcdf_profile_read.argtypes = [P, C.POINTER(C.c_double), PI64, C.c_int]
     lib.gcdf_selftest_umma.argtypes = [C.c_int, C.c_int, P, P, P, P]
+    lib.gcdf_debug_trace.argtypes = [P, P]
     _lib = lib
     return lib
 
@@ -150,6 +151,10 @@ class Context:
     @property
     def launches(self) -> int:
         return int(self.lib.gcdf_launch_count(self._h))
+
+    def debug_trace(self, buf: torch.Tensor | None) -> None:
+        """Diagnostics: pipeline clock64 trace of CTA 0 (int64 [624] on the device) or None."""
+        self._check(self.lib.gcdf_debug_trace(self._h, _ptr(buf)))
 
     def profile_enable(self, on: bool = True) -> None:
         self._check(self.lib.gcdf_profile_enable(self._h, int(on)))
