@@ -99,23 +99,26 @@ def measured_peaks():
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def cpu_oracle_rate(cfg, pts, q, sample_wp=4, sample_pts=32768, nthreads=None):
-    """The oracle as it stands on the host cores: detect over a bounded sample."""
+def cpu_oracle_rate(cfg, pts, q, sample_pts=8192, nthreads=None, seed=12345):
+    """The oracle as it stands on the host cores: detect over a bounded sample of the
+    workload -- one waypoint row per core (the oracle threads over waypoint rows) x
+    sample_pts points."""
     import oracle
     nthreads = nthreads or os.cpu_count() or 1
     m = oracle.MLP(synth.weights_path(cfg.H))
-    rng = np.random.default_rng(12345)
+    rng = np.random.default_rng(seed)
     qs = q.reshape(-1, 9)
-    wsel = np.sort(rng.choice(qs.shape[0], size=min(sample_wp, qs.shape[0]), replace=False))
+    wsel = np.sort(rng.choice(qs.shape[0], size=min(nthreads, qs.shape[0]), replace=False))
     psel = np.sort(rng.choice(pts.shape[0], size=min(sample_pts, pts.shape[0]), replace=False))
+    used = min(nthreads, len(wsel))
     t0 = time.perf_counter()
     m.detect(pts[psel], psel.astype(np.int64), qs[wsel], synth.inputs.DELTA, synth.load_tau(cfg.name),
-             nthreads=nthreads)
+             nthreads=used)
     dt = time.perf_counter() - t0
     n = len(wsel) * len(psel)
-    return {"value": n / dt, "unit": "queries/s", "cores": int(nthreads), "kind": "oracle",
+    return {"value": n / dt, "unit": "queries/s", "cores": int(used), "kind": "oracle", "pairs": n, "seconds": dt,
             "sample": f"{len(wsel)} waypoints x {len(psel)} points of {cfg.name} ({n} pairs, "
-                      f"float64 detect incl. gradients), {dt:.1f} s"}
+                      f"float64 detect incl. gradients, one waypoint row per thread), {dt:.1f} s"}
 
 
 def run_reference(a):
@@ -126,23 +129,20 @@ def run_reference(a):
     cfg = synth.get_config(a.config)
     pts, _ = synth.make_scene_points(cfg)
     q = synth.make_waypoints(cfg)
-    import oracle  # noqa: F401
-    times, n_pairs = [], 0
-    nthreads = os.cpu_count() or 1
+    times, n_pairs, r = [], 0, None
     for i in range(a.warmup + a.steps):
-        r = cpu_oracle_rate(cfg, pts, q, sample_wp=2, sample_pts=8192, nthreads=nthreads)
+        r = cpu_oracle_rate(cfg, pts, q, sample_pts=2048, seed=1000 + i)
         if i >= a.warmup:
-            times.append(2 * 8192 / r["value"])
-            n_pairs += 2 * 8192
+            times.append(r["seconds"])
+            n_pairs += r["pairs"]
     total = sum(times)
     v = n_pairs / total
+    sample = f"each step: one waypoint row per core x 2048 points of {cfg.name} ({r['pairs']} pairs)"
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * total / a.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: {cfg.desc}; each step a bounded sample of 2 waypoints x 8192 points",
-                       "pairs_per_step_sampled": 2 * 8192},
-            "cpu_baseline": {"value": v, "unit": "queries/s", "cores": nthreads, "kind": "oracle",
-                             "sample": "2 waypoints x 8192 points per step"},
+            "config": {"workload": f"{cfg.name}: {cfg.desc}; {sample}"},
+            "cpu_baseline": {"value": v, "unit": "queries/s", "cores": r["cores"], "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -268,6 +268,13 @@ def main():
                 "traffic": None, "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz",
                 "kernel": "k_mlp_simt (fused transform + MLP fwd/bwd + threshold/min/compaction)",
                 "kernel_ms_avg": mlp_ms / mlp_n, "flops_per_pair": FLOPS_PAIR_TOTAL[cfg.H]}
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists() and prec in ("bf16", "fp16"):
+        t = json.loads(tf.read_text()).get("k_mlp_tc")
+        if t:
+            roof["traffic"] = t["bytes"]
+            roof["traffic_source"] = t["source"]
+            roof["algorithmic_dram_bytes"] = int(16 * cfg.M + 48 * n_active + 8 * local_pairs / 128)
     kshare = mlp_ms / t_ms if t_ms > 0 else None
 
     # e2e through the public API with host buffers: pinned q H2D + update + detect + D2H of results
@@ -301,7 +308,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cpu = cpu_oracle_rate(cfg, pts, q_np)
+        cpu = cpu_oracle_rate(cfg, pts, q_np, sample_pts=8192)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": a.steps,

@@ -166,7 +166,9 @@ int gcdf_detect_active_set(gcdf_ctx *ctx, const float *q_dev, int32_t B, int32_t
 
 /* A6-A8 standalone over a dense value/gradient array (e.g. from
    gcdf_query_values_grads): same outputs as detect.  values_dev [n_wp][stride],
-   grads_dev [n_wp][stride][9], column s = local slot s of this context's scene. */
+   grads_dev [n_wp][stride][9], column s = local slot s of this context's scene; stride
+   >= local_bound and a multiple of 4 (16-B aligned rows); a value of +INF marks a dead
+   slot (the query writes +INF there) and is never active nor the minimum. */
 int gcdf_compact_dense(gcdf_ctx *ctx, const float *values_dev, const float *grads_dev, int32_t n_wp,
                        int64_t stride, float delta, float tau, gcdf_active_t *out_dev, int64_t out_capacity,
                        int64_t *wp_offsets_dev, float *wp_min_dev, int64_t *wp_argmin_dev,

@@ -207,7 +207,7 @@ void pack_nosw(const std::vector<float> &m, int rows, int K, uint16_t *dst, bool
 void split16(double x, bool f16, float &hi, float &lo) {
   auto rnd = [&](float v) {
     uint16_t b = f16 ? to_f16_rne(v) : to_bf16_rne(v);
-    if (f16) { __half h; std::memcpy(&h, &b, 2); return __half2float(h); }
+    if (f16) { __half_raw hr; hr.x = b; return __half2float(__half(hr)); }
     uint32_t u = (uint32_t)b << 16; float g; std::memcpy(&g, &u, 4); return g;
   };
   hi = rnd((float)x);
@@ -679,7 +679,8 @@ int gcdf_compact_dense(gcdf_ctx *c, const float *values, const float *grads, int
   int rc = precheck(c, false);
   if (rc) return rc;
   SceneView sv = scene_view(c);
-  if (!values || !grads || n_wp <= 0 || n_wp > c->opt.max_waypoints || stride < sv.local_bound || !out || !offs ||
+  if (!values || !grads || n_wp <= 0 || n_wp > c->opt.max_waypoints || stride < sv.local_bound || (stride & 3) ||
+      ((uintptr_t)values & 15) || !out || !offs ||
       !count_dev || !std::isfinite(delta) || !std::isfinite(tau))
     return fail(c, GCDF_ERR_INVALID_ARG, "compact_dense: bad arguments");
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -52,59 +52,86 @@ __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t *total, in
   return res;
 }
 
-// K3 standalone over dense values: one CTA (128 threads) per tile of 128 slots.
-__global__ void __launch_bounds__(128) k_compact_dense(const float *__restrict__ values,
+// K3 standalone over dense values: one WARP per tile of 128 slots, 4 slots per lane
+// (one 16-B streaming load), no block barrier.  The tile's actives are ranked in slot
+// order by a warp prefix scan of per-lane counts (the "warp-ballot and prefix-sum"
+// compaction); the per-waypoint min key is a warp-shuffle min + one atomicMin per tile.
+// A value of +INF marks a dead slot (gcdf_query_values_grads writes +INF there).
+__global__ void __launch_bounds__(256) k_compact_dense(const float *__restrict__ values,
                                                       const float *__restrict__ grads, int64_t stride,
                                                       int32_t n_wp, int32_t tpw, SceneView scene, float delta,
                                                       float tau, DetectScratch ds) {
-  __shared__ unsigned actw[4];
-  __shared__ unsigned long long kmin[4];
-  __shared__ int sbase;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lane = threadIdx.x & 31;
   const int64_t n_tiles = (int64_t)n_wp * tpw;
-  for (int64_t T = blockIdx.x; T < n_tiles; T += gridDim.x) {
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t lb = scene.local_bound;
+  for (int64_t T = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); T < n_tiles; T += wstride) {
     const int w = (int)(T / tpw);
-    const int64_t slot = (T % tpw) * kTile + tid;
-    const bool inb = slot < scene.local_bound;
-    const bool live = inb && __ldg(&scene.pts[slot].w) > 0.f;
-    const float f = inb ? __ldcs(values + (int64_t)w * stride + slot) : 0.f;
-    const bool act = live && (f - delta <= tau);
-    const unsigned bal = __ballot_sync(0xffffffffu, act);
+    const int64_t slot0 = (T - (int64_t)w * tpw) * kTile + 4 * lane;
+    const float *vrow = values + (int64_t)w * stride;
+    float v[4];
+    if (slot0 + 3 < lb) {
+      const float4 x = __ldcs(reinterpret_cast<const float4 *>(vrow + slot0));
+      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = slot0 + k < lb ? vrow[slot0 + k] : __int_as_float(0x7f800000);
+    }
+    unsigned bits = 0u;
     unsigned long long key = ~0ull;
-    if (live) key = ((unsigned long long)ord_f32(f) << 32) | (unsigned long long)local_to_global(slot, scene.rank, scene.world);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool live = v[k] != __int_as_float(0x7f800000);
+      if (live && v[k] - delta <= tau) bits |= 1u << k;
+      if (live) {
+        const unsigned long long kk = ((unsigned long long)ord_f32(v[k]) << 32) |
+                                      (unsigned long long)local_to_global(slot0 + k, scene.rank, scene.world);
+        key = kk < key ? kk : key;
+      }
+    }
+    const int cnt = __popc(bits);
+    int incl = cnt;  // warp inclusive scan of the per-lane counts (slot order)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
       key = other < key ? other : key;
     }
-    if (lane == 0) { actw[warp] = bal; kmin[warp] = key; }
-    __syncthreads();
-    if (tid == 0) {
-      unsigned long long km = kmin[0];
-      int cnt = 0;
-      for (int i = 0; i < 4; ++i) { km = kmin[i] < km ? kmin[i] : km; cnt += __popc(actw[i]); }
-      if (km != ~0ull) atomicMin(ds.wp_key + w, km);
-      int base = 0;
-      if (cnt > 0) {
-        unsigned long long b = atomicAdd(ds.counter, (unsigned long long)cnt);
-        if (b + cnt > (unsigned long long)ds.max_active) { atomicOr(ds.counter + 1, 1ull); base = -1; }
-        else base = (int)b;
+    int base = 0;
+    if (lane == 0) {
+      if (key != ~0ull) atomicMin(ds.wp_key + w, key);
+      if (total > 0) {
+        const unsigned long long b = atomicAdd(ds.counter, (unsigned long long)total);
+        if (b + total > (unsigned long long)ds.max_active) {
+          atomicOr(ds.counter + 1, 1ull);
+          base = -1;
+        } else {
+          base = (int)b;
+        }
       }
-      sbase = base;
-      ds.tile_meta[T] = make_int2(base, cnt);
+      ds.tile_meta[T] = make_int2(base, total);
     }
-    __syncthreads();
-    if (act && sbase >= 0) {
-      int r = __popc(bal & ((1u << lane) - 1u));
-      for (int i = 0; i < warp; ++i) r += __popc(actw[i]);
-      const float *g = grads + ((int64_t)w * stride + slot) * kNdof;
-      float4 *dst = reinterpret_cast<float4 *>(ds.staging + sbase + r);
-      dst[0] = make_float4(f, g[0], g[1], g[2]);
-      dst[1] = make_float4(g[3], g[4], g[5], g[6]);
-      dst[2] = make_float4(g[7], g[8], __uint_as_float((unsigned)w),
-                           __uint_as_float((unsigned)local_to_global(slot, scene.rank, scene.world)));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (bits && base >= 0) {
+      int r = base + incl - cnt;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (!((bits >> k) & 1u)) continue;
+        const int64_t slot = slot0 + k;
+        const float *g = grads + ((int64_t)w * stride + slot) * kNdof;
+        float4 *dst = reinterpret_cast<float4 *>(ds.staging + r);
+        dst[0] = make_float4(v[k], g[0], g[1], g[2]);
+        dst[1] = make_float4(g[3], g[4], g[5], g[6]);
+        dst[2] = make_float4(g[7], g[8], __uint_as_float((unsigned)w),
+                             __uint_as_float((unsigned)local_to_global(slot, scene.rank, scene.world)));
+        ++r;
+      }
     }
-    __syncthreads();
   }
 }
 
@@ -247,8 +274,9 @@ cudaError_t launch_compact_dense(const float *values, const float *grads, int64_
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t grid = n_tiles < (int64_t)sms * 16 ? n_tiles : (int64_t)sms * 16;
-  k_compact_dense<<<(unsigned)grid, 128, 0, s>>>(values, grads, stride, n_wp, tiles_per_wp, scene, delta, tau, ds);
+  const int64_t need = (n_tiles + 7) / 8;  // 8 warps (tiles) per CTA, 8 CTAs per SM
+  const int64_t grid = need < (int64_t)sms * 8 ? need : (int64_t)sms * 8;
+  k_compact_dense<<<(unsigned)grid, 256, 0, s>>>(values, grads, stride, n_wp, tiles_per_wp, scene, delta, tau, ds);
   return cudaGetLastError();
 }
 

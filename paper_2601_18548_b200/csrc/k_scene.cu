@@ -22,24 +22,22 @@ __global__ void k_fill_dead(float4 *__restrict__ pts, int64_t n) {
     pts[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
-// One CTA row-block: each thread writes 4 consecutive pairs (4 x 16 B = 64 B) of one
-// waypoint; consecutive threads write consecutive 64 B -> fully coalesced 128-bit stores.
+// grid (slot blocks of 1024, waypoints): each thread writes 4 pairs of one waypoint at
+// stride 256 (every store instruction of a warp covers 512 contiguous bytes), the 4
+// point loads are issued before the stores (4 x 16 B in flight per thread), and the
+// pair index needs no 64-bit division.
 __global__ void __launch_bounds__(256) k_pairgen(const float4 *__restrict__ pts, int64_t lb,
-                                                 const float *__restrict__ q, int32_t n_wp,
-                                                 float4 *__restrict__ out) {
-  const int64_t quads = lb / 4;  // lb is a multiple of 128
-  const int64_t total = quads * n_wp;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t w = i / quads;
-    const int64_t s = (i - w * quads) * 4;
-    const float qx = __ldg(q + w * kNdof), qy = __ldg(q + w * kNdof + 1);
-    float4 *o = out + w * lb + s;
+                                                 const float *__restrict__ q, float4 *__restrict__ out) {
+  const int64_t w = blockIdx.y;
+  const int64_t s0 = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  const float qx = __ldg(q + w * kNdof), qy = __ldg(q + w * kNdof + 1);
+  float4 p[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float4 p = __ldg(pts + s + k);
-      __stcs(o + k, make_float4(p.x - qx, p.y - qy, p.z, p.w));  // streaming store
-    }
-  }
+  for (int k = 0; k < 4; ++k) p[k] = s0 + 256 * k < lb ? __ldg(pts + s0 + 256 * k) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 *o = out + w * lb;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (s0 + 256 * k < lb) __stcs(o + s0 + 256 * k, make_float4(p[k].x - qx, p[k].y - qy, p[k].z, p[k].w));
 }
 
 }  // namespace
@@ -63,14 +61,9 @@ cudaError_t launch_fill(float4 *pts, int64_t n, cudaStream_t s) {
 
 cudaError_t launch_pairgen(const float4 *pts, int64_t local_bound, const float *q, int32_t n_wp, float4 *out,
                            cudaStream_t s) {
-  const int64_t total = (local_bound / 4) * n_wp;
-  if (total <= 0) return cudaSuccess;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t grid = (total + 255) / 256;
-  if (grid > (int64_t)sms * 8) grid = (int64_t)sms * 8;  // 8 resident CTAs per SM, grid-stride
-  k_pairgen<<<(unsigned)grid, 256, 0, s>>>(pts, local_bound, q, n_wp, out);
+  if (local_bound <= 0 || n_wp <= 0) return cudaSuccess;
+  const dim3 grid((unsigned)((local_bound + 1023) / 1024), (unsigned)n_wp);
+  k_pairgen<<<grid, 256, 0, s>>>(pts, local_bound, q, out);
   return cudaGetLastError();
 }
 

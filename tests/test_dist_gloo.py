@@ -1,0 +1,122 @@
+"""Multi-process (world_size 2, gloo, CPU) test of the multi-GPU gather protocol.
+
+The product's collective step (paper_2601_18548_b200/dist.py gather_parts) runs on CPU
+tensors under gloo with 2 ranks.  Each rank's local detect result is produced by the
+float64 oracle over the points whose 128-id block the rank owns (block % world == rank,
+the library's sharding rule); the gathered pieces must reassemble the single-rank
+oracle result: MIN of the per-waypoint keys = global min / argmin, gathered offsets =
+per-rank block structure, padded records = each rank's records.  The device merge kernel
+itself is checked bit-exactly on the GPU (test_gpu_fp32.py::test_virtual_ranks_merge_bitexact).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+
+DELTA = synth.inputs.DELTA
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _ord_key(f, pid):
+    """int64 signed-order key (ordered(f32(f)) << 32 | id) ^ INT64_MIN (include/gcdf.h)."""
+    u = np.float32(f).view(np.uint32).astype(np.uint64)
+    o = np.where(u & 0x80000000, ~u & 0xFFFFFFFF, u | 0x80000000).astype(np.uint64)
+    k = (o << np.uint64(32)) | np.uint64(pid)
+    return (k ^ np.uint64(1 << 63)).astype(np.int64)
+
+
+def _records(d, n_wp):
+    n = d["count"]
+    rec = np.zeros((max(n, 1), 12), dtype=np.int32)
+    rf = rec.view(np.float32)
+    rf[:n, 0] = d["value"]
+    rf[:n, 1:10] = d["grad"]
+    rec[:n, 10] = d["wp"]
+    rec[:n, 11] = d["pt"]
+    return torch.from_numpy(rec.view(np.uint8).reshape(-1, 48).copy())
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2601_18548_b200.dist import gather_parts
+        cfg = synth.get_config("C1")
+        pts, _ = synth.make_scene_points(cfg)
+        Q = synth.make_waypoints(cfg).reshape(-1, 9)
+        n_wp = Q.shape[0]
+        ids = np.arange(len(pts))
+        mine = ((ids // 128) % world) == rank
+        m = oracle.MLP(synth.weights_path(cfg.H))
+        tau = synth.load_tau("C1")
+        d = m.detect(pts[mine], ids[mine], Q, DELTA, tau)
+        key = np.full(n_wp, np.iinfo(np.int64).max, dtype=np.int64)
+        ok = d["wp_argmin"] >= 0
+        key[ok] = _ord_key(d["wp_min"][ok], d["wp_argmin"][ok])
+        local = {"records": _records(d, n_wp), "wp_offsets": torch.from_numpy(d["wp_offsets"]),
+                 "wp_key": torch.from_numpy(key)}
+        parts = gather_parts(local, n_wp)
+        if rank == 0:
+            q.put({k: (v.numpy() if torch.is_tensor(v) else v) for k, v in parts.items()})
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_gather_protocol_world2():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # single-rank oracle reference
+    cfg = synth.get_config("C1")
+    pts, _ = synth.make_scene_points(cfg)
+    Q = synth.make_waypoints(cfg).reshape(-1, 9)
+    ids = np.arange(len(pts))
+    m = oracle.MLP(synth.weights_path(cfg.H))
+    ref = m.detect(pts, ids, Q, DELTA, synth.load_tau("C1"))
+    n_wp = Q.shape[0]
+    assert parts["world"] == world and parts["count"] == ref["count"]
+    # MIN-reduced keys = global min / smallest-id argmin (the per-rank min is over owned ids)
+    key = parts["wp_key"].astype(np.int64).view(np.uint64) ^ np.uint64(1 << 63)
+    arg = (key & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    assert np.array_equal(arg, ref["wp_argmin"])
+    offs = parts["offsets"].reshape(world, n_wp + 1)
+    assert np.array_equal(offs.sum(0), ref["wp_offsets"])
+    # the padded gathered records of each rank, merged by (wp, pt), equal the reference
+    rec = parts["records"].reshape(world, parts["stride"], 48)
+    allrec = []
+    for r in range(world):
+        n = offs[r, -1]
+        rr = rec[r, :n].copy().view(np.int32).reshape(n, 12)
+        allrec.append(rr)
+    cat = np.concatenate(allrec)
+    order = np.lexsort((cat[:, 11], cat[:, 10]))
+    merged = cat[order]
+    assert np.array_equal(merged[:, 10], ref["wp"]) and np.array_equal(merged[:, 11], ref["pt"])
+    np.testing.assert_array_equal(merged.view(np.float32)[:, 0], ref["value"].astype(np.float32))
+    # each rank's segment per waypoint is already sorted by id (canonical order per rank)
+    for r in range(world):
+        rr = allrec[r]
+        assert np.all(np.lexsort((rr[:, 11], rr[:, 10])) == np.arange(len(rr)))
