@@ -198,3 +198,47 @@ def test_c5_full_size_sampled():
     frac = out["n"] / (len(pts) * Q.shape[0])
     assert 0.001 < frac < 0.05
     print(f"\nC5: {out['n']} active ({frac:.4%}), {checked} sampled memberships checked")
+
+
+def test_c4_batched_replanning_with_updates():
+    """C4 (128 trajectories x 64 waypoints x 20k points, fp16) after 3 rounds of the scene
+    dynamics (200 removes + 200 adds on a moved box): ids equal the oracle's replay of the id
+    rule; sampled pairs and the per-waypoint minimum match the oracle on the replayed scene."""
+    cfg = synth.get_config("C4")
+    pts, boxes = synth.make_scene_points(cfg)
+    q = synth.make_waypoints(cfg)
+    tau = synth.load_tau(cfg.name)
+    ctx = _ctx(cfg, "fp16")
+    osc = oracle.Scene(cfg.M + 4096)
+    assert np.array_equal(ctx.update_scene(pts), osc.update(pts))
+    rng = np.random.default_rng(404)
+    for _ in range(3):
+        live, _ = osc.export()
+        add, rem = synth.scene_update_batch(rng, boxes, live)
+        assert np.array_equal(ctx.update_scene(add, rem), osc.update(add, rem))
+    ids, xyz = osc.export()
+    out = ctx.detect_active_set(torch.from_numpy(q), DELTA, tau)
+    torch.cuda.synchronize()
+    gpu = records_np(out)
+    Q = q.reshape(-1, 9)
+    m = oracle_mlp(cfg)
+    wsel = np.sort(rng.choice(Q.shape[0], 4, replace=False))
+    psel = np.sort(rng.choice(len(ids), 2048, replace=False))
+    ex = m.eval(xyz[psel], Q[wsel], want_grad=False)
+    recset = set(zip(gpu["wp"].tolist(), gpu["pt"].tolist()))
+    thr = tau + DELTA
+    for wi, w in enumerate(wsel):
+        for pj, pi in enumerate(psel):
+            f = ex["f"][wi, pj]
+            if abs(f - thr) > 1e-3 + BF16_VAL_ATOL:
+                assert ((int(w), int(ids[pi])) in recset) == (f <= thr)
+    # exact per-waypoint minimum on the sampled waypoints, over the whole replayed scene
+    full = m.eval(xyz, Q[wsel], want_grad=False, nthreads=NT)["f"]
+    wmin = out["wp_min"].cpu().numpy()[wsel]
+    assert np.all(np.abs(wmin - full.min(axis=1)) <= BF16_VAL_ATOL)
+    # values of the records of the sampled waypoints vs the oracle
+    pos = {int(i): j for j, i in enumerate(ids)}
+    sel = np.isin(gpu["wp"], wsel)
+    wrow = {int(w): k for k, w in enumerate(wsel)}
+    fo = np.array([full[wrow[int(w)], pos[int(p)]] for w, p in zip(gpu["wp"][sel], gpu["pt"][sel])])
+    assert len(fo) > 0 and np.all(np.abs(gpu["value"][sel] - fo) <= BF16_VAL_ATOL)
