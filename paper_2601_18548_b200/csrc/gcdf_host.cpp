@@ -40,7 +40,11 @@ constexpr int64_t kF32W1p = kMaxH * 4, kF32W1q = kMaxH * 8, kF32W1full = kMaxH *
 constexpr int64_t kF32Mat = (int64_t)kMaxH * kMaxH;
 constexpr int64_t kF32Total = kF32W1p + kF32W1q + kF32W1full + 10 * kF32Mat + 5 * kMaxH + kMaxH;
 // bf16 block sizes (bytes)
-constexpr int64_t kBfTotal = kW16Bytes;  // gcdf_internal.h (pair-split 16-bit weight block)
+constexpr int64_t kBfMat = (int64_t)kMaxH * kMaxH * 2;
+constexpr int64_t kBfW1t = 16LL * kMaxH * 2;
+constexpr int64_t kBfB1 = 32LL * kMaxH * 2;    // layer-1 split weights [128][K = 32], no swizzle
+constexpr int64_t kBfBext = 16LL * kMaxH * 2;  // per hidden layer bias block [128][K = 16], no swizzle
+constexpr int64_t kBfTotal = 5 * kBfMat + kBfW1t + kBfB1 + 5 * kBfBext;
 
 }  // namespace
 
@@ -144,7 +148,10 @@ WeightsBF16 bf16_view(const gcdf_ctx *c) {
   WeightsF32 f = f32_view(c);
   WeightsBF16 w{};
   const int64_t wo = c->opt.precision == GCDF_FP16 ? c->L.wf16 : c->L.wbf16;
-  w.w16 = reinterpret_cast<const uint8_t *>(c->ws + wo);
+  w.w_sw128 = c->ws + wo;
+  w.w1t_sw128 = c->ws + wo + 5 * kBfMat;
+  w.b1_nosw = c->ws + wo + 5 * kBfMat + kBfW1t;
+  w.bext_nosw = c->ws + wo + 5 * kBfMat + kBfW1t + kBfB1;
   w.w7 = f.w7;
   w.b7 = f.b7;
   return w;
@@ -417,34 +424,25 @@ int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
   // ---- pack bf16 and fp16 (UMMA SW128); the weights are rounded f64 -> fp32 -> 16 bit ----
   std::vector<uint16_t> bf((size_t)kBfTotal / 2, 0), hf((size_t)kBfTotal / 2, 0);
   if (H == 128) {
-    // rows [r0, r0 + nr) of a row-major [rows][K] matrix
-    auto rows_of = [](const std::vector<float> &m, int K, int r0, int nr) {
-      return std::vector<float>(m.begin() + (size_t)r0 * K, m.begin() + (size_t)(r0 + nr) * K);
-    };
+    std::vector<float> m((size_t)H * H);
+    for (int li = 0; li < 5; ++li) {
+      for (int r = 0; r < H; ++r)
+        for (int col = 0; col < H; ++col) m[(size_t)r * H + col] = W(li + 1, r, col);
+      pack_sw128(m, H, H, bf.data() + (size_t)li * kBfMat / 2, false);
+      pack_sw128(m, H, H, hf.data() + (size_t)li * kBfMat / 2, true);
+    }
+    std::vector<float> w1t((size_t)16 * H, 0.f);  // [n = input 0..15][k = unit]
+    for (int n = 0; n < kNin; ++n)
+      for (int k = 0; k < H; ++k) w1t[(size_t)n * H + k] = W(0, k, n);
+    pack_sw128(w1t, 16, H, bf.data() + (size_t)5 * kBfMat / 2, false);
+    pack_sw128(w1t, 16, H, hf.data() + (size_t)5 * kBfMat / 2, true);
+    // layer 1 on the tensor cores, split in hi/lo 16-bit parts: K column 3 i + {0, 1, 2}
+    // multiplies A = {x_hi, x_lo, x_hi} by B = {w_hi, w_hi, w_lo} for the ten inputs
+    // i = [p'_x, p'_y, p_z, theta, j1..j6] (x_in columns 0, 1, 2, 5..11); columns 30, 31
+    // multiply A = 1 by {b_hi, b_lo}.  Hidden-layer biases: K column 0, 1 = {b_hi, b_lo}.
     const int xin[10] = {0, 1, 2, 5, 6, 7, 8, 9, 10, 11};
     for (int f16 = 0; f16 < 2; ++f16) {
       uint16_t *dst = (f16 ? hf : bf).data();
-      std::vector<float> m((size_t)H * H), mt((size_t)H * H);
-      for (int li = 0; li < 5; ++li) {
-        for (int r = 0; r < H; ++r)
-          for (int col = 0; col < H; ++col) {
-            m[(size_t)r * H + col] = W(li + 1, r, col);    // W_l [out][in]
-            mt[(size_t)col * H + r] = W(li + 1, r, col);   // W_l^T [in][out]
-          }
-        for (int rk = 0; rk < 2; ++rk) {
-          pack_sw128(rows_of(m, H, 64 * rk, 64), 64, H, dst + (kWOffWf + (li * 2 + rk) * 16384) / 2, f16);
-          pack_sw128(rows_of(mt, H, 64 * rk, 64), 64, H, dst + (kWOffWb + (li * 2 + rk) * 16384) / 2, f16);
-        }
-      }
-      std::vector<float> w1t((size_t)32 * H, 0.f);  // [n = input 0..31 (12 used)][k = unit]
-      for (int n = 0; n < kNin; ++n)
-        for (int k = 0; k < H; ++k) w1t[(size_t)n * H + k] = W(0, k, n);
-      for (int rk = 0; rk < 2; ++rk)
-        pack_sw128(rows_of(w1t, H, 16 * rk, 16), 16, H, dst + (kWOffW1t + rk * 4096) / 2, f16);
-      // layer 1 on the tensor cores, split in hi/lo 16-bit parts: K column 3 i + {0, 1, 2}
-      // multiplies A = {x_hi, x_lo, x_hi} by B = {w_hi, w_hi, w_lo} for the ten inputs
-      // i = [p'_x, p'_y, p_z, theta, j1..j6] (x_in columns 0, 1, 2, 5..11); columns 30, 31
-      // multiply A = 1 by {b_hi, b_lo}.  Hidden-layer biases: K column 0, 1 = {b_hi, b_lo}.
       std::vector<float> b1((size_t)H * 32, 0.f);
       for (int u = 0; u < H; ++u) {
         float hi, lo;
@@ -458,7 +456,7 @@ int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
         b1[(size_t)u * 32 + 30] = hi;
         b1[(size_t)u * 32 + 31] = lo;
       }
-      for (int rk = 0; rk < 2; ++rk) pack_nosw(rows_of(b1, 32, 64 * rk, 64), 64, 32, dst + (kWOffB1 + rk * 4096) / 2, f16);
+      pack_nosw(b1, H, 32, dst + (5 * kBfMat + kBfW1t) / 2, f16);
       for (int li = 0; li < 5; ++li) {
         std::vector<float> be((size_t)H * 16, 0.f);
         for (int u = 0; u < H; ++u) {
@@ -467,8 +465,7 @@ int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
           be[(size_t)u * 16 + 0] = hi;
           be[(size_t)u * 16 + 1] = lo;
         }
-        for (int rk = 0; rk < 2; ++rk)
-          pack_nosw(rows_of(be, 16, 64 * rk, 64), 64, 16, dst + (kWOffBext + (li * 2 + rk) * 2048) / 2, f16);
+        pack_nosw(be, H, 16, dst + (5 * kBfMat + kBfW1t + kBfB1 + li * kBfBext) / 2, f16);
       }
     }
   }

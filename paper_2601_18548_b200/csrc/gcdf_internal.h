@@ -35,20 +35,15 @@ struct WeightsF32 {
 // canonical SWIZZLE_128B layout: two 64-column chunks of [H rows][128 B], 16-B granule g
 // of row r stored at granule g ^ (r % 8).  The same bytes serve as a K-major B operand
 // (forward, N = out, K = in) and an MN-major B operand (backward, N = in, K = out).
-// The tensor-core kernel runs on CTA pairs (tcgen05 cta_group::2, M = 256 pairs): every B
-// operand is split by N between the two CTAs of a pair, rank r holding rows
-// [r N/2, (r + 1) N/2).  16-bit weight block, per rank r (byte offsets below):
-//   wf[l][r]   W_l (l = 2..6) rows 64r..64r+63 ([out][in], K = in), K-major SW128, 16 KB
-//   wb[l][r]   W_l^T rows 64r..64r+63 ([in][out], K = out), K-major SW128, 16 KB
-//   w1t[r]     W1^T padded to 32 rows (inputs 0..11, zeros), rows 16r..16r+15, SW128, 4 KB
-//   b1[r]      layer 1 as a K = 32 GEMM on split hi/lo operands (exact to ~fp32),
-//              rows (units) 64r..64r+63, K-major SWIZZLE_NONE, 4 KB
-//   bext[l][r] hidden-layer bias block {b_hi, b_lo, 0...} (K = 16, times a constant "ones"
-//              A block), rows 64r..64r+63, K-major SWIZZLE_NONE, 2 KB
-constexpr int64_t kWOffWf = 0, kWOffWb = 163840, kWOffW1t = 327680, kWOffB1 = 335872, kWOffBext = 344064;
-constexpr int64_t kW16Bytes = 364544;
+// w1t: W1^T restricted to the 12 input columns, padded to N = 16 rows, K-major SW128.
+// b1: layer 1 as a K = 32 GEMM on split hi/lo 16-bit operands (exact to ~fp32), and
+// bext: per hidden layer a K = 16 block {b_hi, b_lo, 0...} multiplied by a constant
+// "ones" A block -- both in the UMMA SWIZZLE_NONE K-major layout (gcdf_host.cpp).
 struct WeightsBF16 {
-  const uint8_t *w16;    // kW16Bytes, layout above
+  const void *w_sw128;   // 5 * H * H * 2 bytes
+  const void *w1t_sw128; // 16 * H * 2 bytes
+  const void *b1_nosw;   // H * 32 * 2 bytes
+  const void *bext_nosw; // 5 * H * 16 * 2 bytes
   const float *w7;       // [H] fp32
   float b7;
 };

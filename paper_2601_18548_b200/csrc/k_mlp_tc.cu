@@ -6,31 +6,33 @@
 // value + gradient :394 (dense gradient R^{NM x n}); constraint f - delta >= 0 :362-363;
 // union = min :164; c_gcdf step-major order :414-435.  DESIGN.md §5 "K2b".
 //
-// Design (H = 128; persistent CTA *pairs*, one CTA per SM, 17 warps per CTA):
-//   * Every affine layer is a 2-SM UMMA (tcgen05.mma.cta_group::2, M = 256 pairs: 128 per
-//     CTA of the pair) with A = activations in each CTA's TMEM and B = weights resident in
-//     shared memory for the whole kernel, split by N between the two CTAs (each holds 64 of
-//     the 128 rows).  Measured on this part, a 2-SM 256x128x16 UMMA sustains 68 % of the
-//     dense rate vs 56 % for a 1-SM 128x128x16 (tools/mma_probe.py), and the split halves
-//     the per-SM weight footprint, which pays for a K-major copy of W^T for the backward
-//     (K-major B is faster than MN-major):
+// Design (H = 128, one persistent CTA per SM, 544 threads = 16 epilogue warps + 1 MMA warp):
+//   * Every affine layer of a 128-pair tile is a UMMA with M = 128 pairs, A in TMEM and B
+//     resident in shared memory for the whole kernel:
 //       - layer 1 (12 -> 128): K = 32 of split hi/lo 16-bit operands (A = {x_hi, x_lo,
 //         x_hi}, B = {w_hi, w_hi, w_lo} per input, plus {1, 1} x {b_hi, b_lo}), which
 //         keeps the metre-scale point coordinates at ~fp32 accuracy (R16);
-//       - layers 2..6: K = 128 from the activations + one K = 16 step against a constant
-//         "ones" A block that adds the bias {b_hi, b_lo};
-//       - backward layers 6..2: D = E W_l with B = W_l^T (K-major copy);
-//       - g0 = e1 W1: N = 32 rows of W1^T (12 used).
+//       - layers 2..6 (128 -> 128): K = 128 from the activations + one K = 16 step
+//         against a constant "ones" A block that adds the bias {b_hi, b_lo};
+//       - backward layers 6..2: D = E W_l with the same smem bytes read MN-major;
+//       - g0 = e1 W1: N = 16 rows of W1^T.
+//     W_2..W_6 use the UMMA SWIZZLE_128B layout (5 x 32 KB); the small K = 16 / 32 blocks
+//     the SWIZZLE_NONE layout.
 //   * Activations never leave the chip: accumulator D (fp32, 128 TMEM columns) ->
-//     epilogue registers (ReLU + 16-bit pack + 1-bit mask) -> A (64 TMEM columns) -> next
-//     UMMA.  ReLU masks go to shared memory (1 bit per unit) for the backward pass.
-//   * Two tiles in flight per CTA: TMEM columns [0,256) belong to slot 0 and [256,512) to
-//     slot 1 (D [0,128), A [128,192), ones [192,200)).  Each slot has 8 epilogue warps:
-//     warp (h, q) owns TMEM lanes 32q..32q+31 (the tile's pairs) and accumulator columns
-//     64h..64h+63.  Warp 16 of the pair's leader CTA issues all UMMAs (one thread); the
-//     epilogues of both CTAs arrive on the leader's epi_done[s] (512 arrivals, the peer
-//     through its cluster-mapped address) and tcgen05.commit multicasts mma_done[s] to both.
-//     12 MMA phases per tile.
+//     epilogue registers (ReLU + 16-bit pack + byte-sign mask) -> A (64 TMEM columns) ->
+//     next UMMA.  ReLU masks go to shared memory for the backward pass.
+//   * Two tiles in flight: TMEM columns [0,256) belong to slot 0 and [256,512) to slot
+//     1 (D [0,128), A [128,192), ones [192,200)).  Each slot has 8 epilogue warps: warp
+//     (h, q) owns TMEM lanes 32q..32q+31 (the tile's pairs) and accumulator columns
+//     64h..64h+63, so every SM sub-partition runs two warps per slot, and one slot's
+//     epilogue overlaps the other slot's tensor-core work.  Warp 16 is the MMA issuer:
+//     after each epilogue phase the slot's 8 warps arrive on the slot's "A ready"
+//     mbarrier; one elected lane of warp 16 waits on it, issues the slot's next UMMAs and
+//     commits them to the slot's "D ready" mbarrier.  The tensor core executes both
+//     slots' MMAs in issue order.  12 MMA phases per tile.
+//   * Measured (profiles/r1/mma_probe.txt): at M = 128, N = 128 a single-CTA TS UMMA
+//     runs at 52-56 % of the dense peak, which bounds this kernel; a 2-CTA (M = 256)
+//     variant was measured slower end to end (K2b experiments).
 #include "gcdf_internal.h"
 #include "tc_ptx.h"
 
@@ -41,30 +43,30 @@ using namespace tc;
 
 constexpr int H = 128;
 constexpr int kEpiWarps = 16;             // warps 0..15: epilogue (8 per tile slot)
-constexpr int kWarps = kEpiWarps + 1;     // warp 16: MMA issuer (leader CTA of the pair)
+constexpr int kWarps = kEpiWarps + 1;     // warp 16: MMA issuer
 constexpr int kThreads = kWarps * 32;
-constexpr int kEpiPerSlot = 256;          // epilogue threads per slot per CTA
+constexpr int kEpiPerSlot = 256;
 constexpr int kPhases = 12;               // MMA phases per tile
 constexpr int kMasks = 5;                 // stored ReLU masks: layers 1..5
+constexpr int kWBytes = 5 * H * H * 2;    // 163,840
+constexpr int kW1tBytes = 16 * H * 2;     // 4,096
+constexpr int kB1Bytes = 32 * H * 2;      // 8,192
+constexpr int kBextBytes = 16 * H * 2;    // 4,096 per hidden layer
 constexpr uint32_t kColA = 128, kColOnes = 192;
-// instruction descriptors, M = 256 (CTA pair)
-template <bool F16> constexpr uint32_t kIdesc128 = idesc_f16kind(256, 128, false, F16);
-template <bool F16> constexpr uint32_t kIdesc32 = idesc_f16kind(256, 32, false, F16);
-template <bool F16> constexpr uint32_t kIdescFwd = idesc_f16kind(128, 128, false, F16);  // self-test (1 CTA)
+template <bool F16> constexpr uint32_t kIdescFwd = idesc_f16kind(128, 128, false, F16);
 template <bool F16> constexpr uint32_t kIdescBwd = idesc_f16kind(128, 128, true, F16);
 template <bool F16> constexpr uint32_t kIdescFin = idesc_f16kind(128, 16, false, F16);
 
 struct __align__(1024) SmemTC {
-  uint8_t wf[5][16384];        // this CTA's half of W_2..W_6 (64 rows, K = 128), SW128
-  uint8_t wb[5][16384];        // this CTA's half of W_2^T..W_6^T, SW128
-  uint8_t w1t[4096];           // this CTA's 16 rows of W1^T (32 rows), SW128
-  uint8_t b1[4096];            // this CTA's 64 rows of the split layer-1 weights, no swizzle
-  uint8_t bext[5][2048];       // this CTA's 64 rows of the bias blocks, no swizzle
+  uint8_t w[kWBytes];          // W_2..W_6, SW128 [2 chunks][128 rows][128 B] each
+  uint8_t w1t[kW1tBytes];      // W1^T [16][128], SW128
+  uint8_t b1[kB1Bytes];        // layer-1 split weights [128][32], no swizzle
+  uint8_t bext[5][kBextBytes]; // hidden-layer bias blocks [128][16], no swizzle
   float w7[H];
   float fpart[2][2][H];        // [slot][half][row] partial output-layer sums
   uint32_t mask[2][kMasks][2][kEpiPerSlot];  // ReLU masks [slot][layer][32-unit word][thread]
   uint64_t mma_done[2];
-  uint64_t epi_done[2];        // used in the leader CTA (count 512)
+  uint64_t epi_done[2];
   unsigned act[2][4];
   unsigned long long kmin[2][4];
   int sbase[2];
@@ -97,403 +99,335 @@ DEVI void split3(float x, float *o) {
   o[2] = hi;
 }
 
-DEVI uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-DEVI void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-DEVI uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-  return r;
-}
-// Arrive on a (possibly remote) mbarrier of the pair.  Default .release.cta semantics, as
-// CUTLASS's 2-SM pipelines do: the TMEM stores being published are ordered by
-// tcgen05.wait::st + tcgen05.fence::before_thread_sync before it and the issuer's
-// tcgen05.fence::after_thread_sync after its wait; a .release.cluster arrive would add a
-// cluster-scope memory fence (~1000 cycles, measured) to every epilogue phase.
-DEVI void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-DEVI bool mbar_try_wait_cluster(uint32_t addr, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, P1;\n\t}"
-      : "=r"(ok)
-      : "r"(addr), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-DEVI void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
-  const uint32_t addr = smem_u32(bar);
-  if (mbar_try_wait_cluster(addr, parity)) return;
-  const long long t0 = clock64();
-  while (!mbar_try_wait_cluster(addr, parity)) {
-    if (clock64() - t0 > (1ll << 34)) __trap();
-  }
-}
-DEVI void mma2(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
-      : "memory");
-}
-DEVI void commit2(uint64_t *bar) {  // arrive on the same-offset mbarrier of both CTAs
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"((unsigned short)3)
-      : "memory");
-}
-
-// UMMAs of MMA phase p of the tile pair in slot s (one thread of the leader CTA)
+// UMMAs of MMA phase p of the tile in slot s (one thread); commit to mma_done[s]
 template <bool F16>
-DEVI void issue_phase(int p, uint32_t d, const SmemTC &S, uint64_t *bar) {
+DEVI void issue_phase(int p, uint32_t d, uint32_t sw, uint32_t sw1t, uint32_t sb1, uint32_t sbx, uint64_t *bar) {
   const uint32_t av = d + kColA;
   if (p == 0) {  // layer 1: K = 32 split operands (bias included)
-    const uint32_t sb1 = smem_u32(S.b1);
 #pragma unroll
-    for (int k = 0; k < 2; ++k) mma2(d, av + 8u * k, sdesc_nosw(sb1 + k * 2 * 1024, 1024, 128), kIdesc128<F16>, k > 0);
-  } else if (p < 6) {  // layer l = p + 1: D = A W_l^T (B = this CTA's half of W_l) + ones x bias
-    const uint32_t wb = smem_u32(S.wf[p - 1]);
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      mma2(d, av + 8u * k, sdesc_sw128(wb + (k >> 2) * 8192 + (k & 3) * 32, 16, 1024), kIdesc128<F16>, k > 0);
-    mma2(d, d + kColOnes, sdesc_nosw(smem_u32(S.bext[p - 1]), 1024, 128), kIdesc128<F16>, 1u);
-  } else if (p < 11) {  // backward through layer l = 12 - p: D = E W_l (B = W_l^T, K-major)
-    const uint32_t wb = smem_u32(S.wb[10 - p]);
+    for (int k = 0; k < 2; ++k) mma_ts(d, av + 8u * k, sdesc_nosw(sb1 + k * 2 * 2048, 2048, 128), kIdescFwd<F16>, k > 0);
+  } else if (p < 6) {  // layer l = p + 1: D = A W_l^T (B = W_l K-major) + ones x bias
+    const uint32_t wb = sw + (uint32_t)(p - 1) * (H * H * 2);
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      mma2(d, av + 8u * k, sdesc_sw128(wb + (k >> 2) * 8192 + (k & 3) * 32, 16, 1024), kIdesc128<F16>, k > 0);
-  } else {  // g0 = e1 W1 (N = 32 rows of W1^T, 12 used)
-    const uint32_t wb = smem_u32(S.w1t);
+      mma_ts(d, av + 8u * k, sdesc_sw128(wb + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024), kIdescFwd<F16>, k > 0);
+    mma_ts(d, d + kColOnes, sdesc_nosw(sbx + (uint32_t)(p - 1) * kBextBytes, 2048, 128), kIdescFwd<F16>, 1u);
+  } else if (p < 11) {  // backward through layer l = 12 - p: D = E W_l, B = W_l MN-major
+    const uint32_t wb = sw + (uint32_t)(10 - p) * (H * H * 2);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) mma_ts(d, av + 8u * k, sdesc_sw128(wb + k * 2048, 16384, 1024), kIdescBwd<F16>, k > 0);
+  } else {  // g0 = e1 W1 (N = 16 rows of W1^T)
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      mma2(d, av + 8u * k, sdesc_sw128(wb + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdesc32<F16>, k > 0);
+      mma_ts(d, av + 8u * k, sdesc_sw128(sw1t + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin<F16>, k > 0);
   }
-  commit2(bar);
+  commit(bar);
 }
 
 template <bool F16>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    k_mlp_tc(const WeightsBF16 W, const QueryArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, const QueryArgs a) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned view (SWIZZLE_128B atoms); pointer arithmetic on the __shared__ array
   // keeps the shared address space visible to the compiler (LDS/STS, not generic LD/ST)
   SmemTC &S = *reinterpret_cast<SmemTC *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t rank = cluster_rank();  // 0 = leader of the pair
 
-  // ---- one-time setup: this CTA's half of the weights -> smem (UMMA layouts in global) ----
+  // ---- one-time setup: weights -> smem (already in UMMA layouts in global memory) ----
   {
-    auto copy16 = [&](void *dst, const uint8_t *src, int bytes) {
+    auto copy16 = [&](void *dst, const void *src, int bytes) {
       const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
       uint4 *d4 = reinterpret_cast<uint4 *>(dst);
       for (int i = tid; i < bytes / 16; i += kThreads) d4[i] = __ldg(s4 + i);
     };
-    for (int l = 0; l < 5; ++l) {
-      copy16(S.wf[l], W.w16 + kWOffWf + (l * 2 + rank) * 16384, 16384);
-      copy16(S.wb[l], W.w16 + kWOffWb + (l * 2 + rank) * 16384, 16384);
-      copy16(S.bext[l], W.w16 + kWOffBext + (l * 2 + rank) * 2048, 2048);
-    }
-    copy16(S.w1t, W.w16 + kWOffW1t + rank * 4096, 4096);
-    copy16(S.b1, W.w16 + kWOffB1 + rank * 4096, 4096);
+    copy16(S.w, W.w_sw128, kWBytes);
+    copy16(S.w1t, W.w1t_sw128, kW1tBytes);
+    copy16(S.b1, W.b1_nosw, kB1Bytes);
+    copy16(S.bext, W.bext_nosw, 5 * kBextBytes);
     for (int i = tid; i < H; i += kThreads) S.w7[i] = __ldg(W.w7 + i);
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
-                 "r"(512)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    tmem_alloc(&S.tmem_base, 512);
+    tmem_relinquish();
   }
   if (tid == 32) {
     mbar_init(&S.mma_done[0], 1);
     mbar_init(&S.mma_done[1], 1);
-    mbar_init(&S.epi_done[0], 2 * kEpiPerSlot);
-    mbar_init(&S.epi_done[1], 2 * kEpiPerSlot);
+    mbar_init(&S.epi_done[0], kEpiPerSlot);
+    mbar_init(&S.epi_done[1], kEpiPerSlot);
     fence_barrier_init();
   }
   fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
   fence_before();
-  cluster_sync();
+  __syncthreads();
   fence_after();
   const uint32_t tbase = S.tmem_base;
   const int64_t n_tiles = (int64_t)a.n_wp * a.tiles_per_wp;
-  const int64_t n_super = (n_tiles + 1) / 2;        // tile pairs (rank r takes tile 2 T2 + r)
-  const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int64_t lb = a.scene.local_bound;
+  const uint32_t sw = smem_u32(S.w), sw1t = smem_u32(S.w1t), sb1 = smem_u32(S.b1), sbx = smem_u32(S.bext);
 
   if (warp == kEpiWarps) {
-    // ================ MMA warp (leader CTA): one thread issues both slots' UMMAs ================
-    if (rank == 0 && lane == 0) {
+    // ===================== dedicated MMA warp: one thread issues both slots' UMMAs ==========
+    if (lane == 0) {
       uint32_t phbits = 0u;  // bit s = phase parity of epi_done[s]
-      for (int64_t base = cl * 2; base < n_super; base += 2 * ncl) {
-        const int nslots = (base + 1 < n_super) ? 2 : 1;
+      for (int64_t base = (int64_t)blockIdx.x * 2; base < n_tiles; base += 2 * (int64_t)gridDim.x) {
+        const int nslots = (base + 1 < n_tiles) ? 2 : 1;
 #pragma unroll 1
         for (int p = 0; p < kPhases; ++p) {
 #pragma unroll 1
           for (int ss = 0; ss < nslots; ++ss) {
-            mbar_wait_cluster(&S.epi_done[ss], (phbits >> ss) & 1u);
+            mbar_wait(&S.epi_done[ss], (phbits >> ss) & 1u);
             phbits ^= 1u << ss;
             fence_after();
-            issue_phase<F16>(p, tbase + (uint32_t)ss * 256u, S, &S.mma_done[ss]);
+            issue_phase<F16>(p, tbase + (uint32_t)ss * 256u, sw, sw1t, sb1, sbx, &S.mma_done[ss]);
           }
         }
       }
     }
     __syncwarp();
-  } else {
-    // =========================== epilogue warps ===========================
-    const int s = warp >> 3;          // tile slot
-    const int hh = (warp >> 2) & 1;   // accumulator column half: units 64 hh .. 64 hh + 63
-    const int qd = warp & 3;          // TMEM lane quarter of this warp (warp % 4)
-    const int row = qd * 32 + lane;   // pair within the tile = TMEM lane
-    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-    const uint32_t tS = tbase + (uint32_t)s * 256u + lane_off;  // this slot, this lane quarter
-    const uint32_t tD = tS + 64u * hh;
-    const uint32_t tA = tS + kColA + 32u * hh;
-    const int u0 = 64 * hh;           // first unit of this thread's columns
-    uint32_t *mk = &S.mask[s][0][0][hh * 128 + row];  // + (layer * 2 + word) * kEpiPerSlot
-    const uint32_t epi_bar = map_to_rank(smem_u32(&S.epi_done[s]), 0);  // the leader's barrier
-    if (hh == 0) {  // the constant "ones" A block of the bias GEMM step: {1, 1, 0, ...}
-      uint32_t ones[8] = {pack2<F16>(1.f, 1.f), 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-      st8(tS + kColOnes, ones);
+    fence_before();
+    __syncthreads();
+    return;  // (TMEM is freed by warp 0 after the final barrier)
+  }
+  const int s = warp >> 3;          // tile slot
+  const int hh = (warp >> 2) & 1;   // accumulator column half: units 64 hh .. 64 hh + 63
+  const int qd = warp & 3;          // TMEM lane quarter of this warp (warp % 4)
+  const int row = qd * 32 + lane;   // pair within the tile = TMEM lane
+  const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+  const uint32_t tSlot = tbase + (uint32_t)s * 256u;  // MMA-side column base of this slot
+  const uint32_t tS = tSlot + lane_off;                 // this slot, this lane quarter
+  const uint32_t tD = tS + 64u * hh;
+  const uint32_t tA = tS + kColA + 32u * hh;
+  const int u0 = 64 * hh;           // first unit of this thread's columns
+  uint32_t *mk = &S.mask[s][0][0][hh * 128 + row];  // + (layer * 2 + word) * kEpiPerSlot
+  if (hh == 0) {  // the constant "ones" A block of the bias GEMM step: {1, 1, 0, ...}
+    uint32_t ones[8] = {pack2<F16>(1.f, 1.f), 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    st8(tS + kColOnes, ones);
+  }
+  // epilogue phase done: TMEM stores complete and ordered before the MMA warp's UMMAs
+  auto hand_off = [&](int) {
+    wait_st();
+    fence_before();
+    mbar_arrive(&S.epi_done[s]);
+  };
+  (void)tSlot;
+  uint32_t ph = 0u;
+  int it = 0;
+  const bool tracer = a.trace && blockIdx.x == 0 && hh == 0 && qd == 0 && lane == 0;
+  int w_prev = -1;
+  uint32_t qwords[8];  // the per-waypoint part of this half's A1 words
+  float q0h = 0.f;
+  // point of this lane's pair in the next tile, prefetched during the current tile
+  auto load_pt = [&](int64_t TT) -> float4 {
+    if (TT >= n_tiles) return make_float4(0.f, 0.f, 0.f, 0.f);
+    const int64_t sl = (TT % a.tiles_per_wp) * kTile + row;
+    return sl < lb ? __ldg(a.scene.pts + sl) : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  float4 pt_next = load_pt((int64_t)blockIdx.x * 2 + s);
+  for (int64_t T = (int64_t)blockIdx.x * 2 + s; T < n_tiles; T += 2 * (int64_t)gridDim.x, ++it) {
+    long long *tr = (tracer && it < kTraceTiles) ? a.trace + (size_t)((1 + s) * kTraceTiles + it) * kTracePhases * 4 : nullptr;
+    if (tr) tr[0] = clock64();
+    const int w = (int)(T / a.tiles_per_wp);
+    const int64_t slot = (T % a.tiles_per_wp) * kTile + row;
+    const float *qw = a.q + (int64_t)w * kNdof;
+    if (w != w_prev) {  // split the waypoint's [theta, j1..j6] once per waypoint
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 7; ++i) split3<F16>(__ldg(qw + 2 + i), v + 9 + 3 * i);
+      v[30] = 1.f;
+      v[31] = 1.f;
+      q0h = v[9];
+      // half 0 owns A1 words 0..7 (K 0..15): words 5..7 are per-waypoint (K 10..15);
+      // half 1 owns words 8..15 (K 16..31): all per-waypoint
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int kk = hh == 0 ? 2 * i : 16 + 2 * i;
+        qwords[i] = (hh == 0 && i < 5) ? 0u : pack2<F16>(v[kk], v[kk + 1]);
+      }
+      w_prev = w;
     }
-    // epilogue phase done: TMEM stores complete and ordered before the leader's UMMAs
-    auto hand_off = [&]() {
-      wait_st();
-      fence_before();
-      mbar_arrive_cluster(epi_bar);
-    };
-    uint32_t ph = 0u;
-    int it = 0;
-    const bool tracer = a.trace && blockIdx.x == 0 && hh == 0 && qd == 0 && lane == 0;
-    int w_prev = -1;
-    uint32_t qwords[8];  // the per-waypoint part of this half's A1 words
-    float q0h = 0.f;
-    // point of this lane's pair in the tile of super-tile TT, prefetched a tile ahead
-    auto load_pt = [&](int64_t TT) -> float4 {
-      const int64_t Tt = 2 * TT + rank;
-      if (Tt >= n_tiles) return make_float4(0.f, 0.f, 0.f, 0.f);
-      const int64_t sl = (Tt % a.tiles_per_wp) * kTile + row;
-      return sl < lb ? __ldg(a.scene.pts + sl) : make_float4(0.f, 0.f, 0.f, 0.f);
-    };
-    float4 pt_next = load_pt(cl * 2 + s);
-    for (int64_t T2 = cl * 2 + s; T2 < n_super; T2 += 2 * ncl, ++it) {
-      long long *tr = (tracer && it < kTraceTiles) ? a.trace + (size_t)((1 + s) * kTraceTiles + it) * kTracePhases * 4 : nullptr;
-      if (tr) tr[0] = clock64();
-      const int64_t T = 2 * T2 + rank;
-      const bool real = T < n_tiles;  // the pair's last tile may be a phantom (odd tile count)
-      const int w = real ? (int)(T / a.tiles_per_wp) : 0;
-      const int64_t slot = real ? (T % a.tiles_per_wp) * kTile + row : lb;
-      const float *qw = a.q + (int64_t)w * kNdof;
-      if (w != w_prev) {  // split the waypoint's [theta, j1..j6] once per waypoint
-        float v[32];
+    // A2: pair generation + base-frame bias p' = p - [q_x, q_y, 0]
+    const float4 pt = pt_next;
+    const bool live = slot < lb && pt.w > 0.f;
+    // ---- A1: the split layer-1 operands of this pair -> TMEM A ----
+    {
+      uint32_t a1[8];
+      if (hh == 0) {
+        float v[10];
+        split3<F16>(pt.x - __ldg(qw), v);
+        split3<F16>(pt.y - __ldg(qw + 1), v + 3);
+        split3<F16>(pt.z, v + 6);
+        v[9] = q0h;
 #pragma unroll
-        for (int i = 0; i < 7; ++i) split3<F16>(__ldg(qw + 2 + i), v + 9 + 3 * i);
-        v[30] = 1.f;
-        v[31] = 1.f;
-        q0h = v[9];
-        // half 0 owns A1 words 0..7 (K 0..15): words 5..7 are per-waypoint (K 10..15);
-        // half 1 owns words 8..15 (K 16..31): all per-waypoint
+        for (int i = 0; i < 5; ++i) a1[i] = pack2<F16>(v[2 * i], v[2 * i + 1]);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int kk = hh == 0 ? 2 * i : 16 + 2 * i;
-          qwords[i] = (hh == 0 && i < 5) ? 0u : pack2<F16>(v[kk], v[kk + 1]);
-        }
-        w_prev = w;
+        for (int i = 5; i < 8; ++i) a1[i] = qwords[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a1[i] = qwords[i];
       }
-      // A2: pair generation + base-frame bias p' = p - [q_x, q_y, 0]
-      const float4 pt = pt_next;
-      const bool live = slot < lb && pt.w > 0.f;
-      // ---- A1: the split layer-1 operands of this pair -> TMEM A ----
-      {
-        uint32_t a1[8];
-        if (hh == 0) {
-          float v[10];
-          split3<F16>(pt.x - __ldg(qw), v);
-          split3<F16>(pt.y - __ldg(qw + 1), v + 3);
-          split3<F16>(pt.z, v + 6);
-          v[9] = q0h;
-#pragma unroll
-          for (int i = 0; i < 5; ++i) a1[i] = pack2<F16>(v[2 * i], v[2 * i + 1]);
-#pragma unroll
-          for (int i = 5; i < 8; ++i) a1[i] = qwords[i];
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) a1[i] = qwords[i];
-        }
-        st8(tS + kColA + 8u * hh, a1);
-      }
-      if (tr) tr[2] = clock64();
-      hand_off();
-      if (tr) tr[3] = clock64();
+      st8(tS + kColA + 8u * hh, a1);
+    }
+    if (tr) tr[2] = clock64();
+    hand_off(0);
+    if (tr) tr[3] = clock64();
 
-      float f = 0.f;
-      bool act = false;
-      int my_base = -1, my_rank = 0;
+    float f = 0.f;
+    bool act = false;
+    int my_base = -1, my_rank = 0;
 #pragma unroll 1
-      for (int p = 0; p < kPhases; ++p) {
-        mbar_wait(&S.mma_done[s], ph);
-        if (tr) tr[(p + 1) * 4 + 1] = clock64();
-        ph ^= 1u;
-        fence_after();
-        if (p < 6) {
-          // ---- forward layer l = p + 1: z = D (bias folded in); h = ReLU(z) -> A ----
-          //      (l = 6: f += w7 . h6 in fp32, e6 = w7 (.) 1[z6 > 0] -> A)
-          float fp = 0.f;
+    for (int p = 0; p < kPhases; ++p) {
+      mbar_wait(&S.mma_done[s], ph);
+      if (tr) tr[(p + 1) * 4 + 1] = clock64();
+      ph ^= 1u;
+      fence_after();
+      if (p < 6) {
+        // ---- forward layer l = p + 1: z = D (bias folded in); h = ReLU(z) -> A ----
+        //      (l = 6: f += w7 . h6 in fp32, e6 = w7 (.) 1[z6 > 0] -> A)
+        float fp = 0.f;
 #pragma unroll
-          for (int c2 = 0; c2 < 2; ++c2) {
-            uint32_t m = 0u;
+        for (int c2 = 0; c2 < 2; ++c2) {
+          uint32_t m = 0u;
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-              uint32_t pk[8], rr[16];
-              const int cb = c2 * 32 + hf * 16;
-              ld16(tD + cb, rr);
-              wait_ld();
-              if (tr && cb == 0) tr[(p + 1) * 4 + 0] = clock64();
+          for (int hf = 0; hf < 2; ++hf) {
+            uint32_t pk[8], rr[16];
+            const int cb = c2 * 32 + hf * 16;
+            ld16(tD + cb, rr);
+            wait_ld();
+            if (tr && cb == 0) tr[(p + 1) * 4 + 0] = clock64();
 #pragma unroll
-              for (int j = 0; j < 16; j += 4) {
-                const float z0 = __uint_as_float(rr[j]), z1 = __uint_as_float(rr[j + 1]);
-                const float z2 = __uint_as_float(rr[j + 2]), z3 = __uint_as_float(rr[j + 3]);
-                if (p < 5) {
-                  pk[j >> 1] = pack2_relu<F16>(z0, z1);
-                  pk[(j >> 1) + 1] = pack2_relu<F16>(z2, z3);
-                  m |= mask_group(pk[j >> 1], pk[(j >> 1) + 1], (hf * 16 + j) >> 2);
-                } else {  // layer 6: its mask is applied right here (e6), never stored
-                  const float4 w7 = *reinterpret_cast<const float4 *>(S.w7 + u0 + cb + j);
-                  fp = fmaf(w7.x, fmaxf(z0, 0.f), fp);
-                  fp = fmaf(w7.y, fmaxf(z1, 0.f), fp);
-                  fp = fmaf(w7.z, fmaxf(z2, 0.f), fp);
-                  fp = fmaf(w7.w, fmaxf(z3, 0.f), fp);
-                  pk[j >> 1] = pack2<F16>(z0 > 0.f ? w7.x : 0.f, z1 > 0.f ? w7.y : 0.f);
-                  pk[(j >> 1) + 1] = pack2<F16>(z2 > 0.f ? w7.z : 0.f, z3 > 0.f ? w7.w : 0.f);
-                }
+            for (int j = 0; j < 16; j += 4) {
+              const float z0 = __uint_as_float(rr[j]), z1 = __uint_as_float(rr[j + 1]);
+              const float z2 = __uint_as_float(rr[j + 2]), z3 = __uint_as_float(rr[j + 3]);
+              if (p < 5) {
+                pk[j >> 1] = pack2_relu<F16>(z0, z1);
+                pk[(j >> 1) + 1] = pack2_relu<F16>(z2, z3);
+                m |= mask_group(pk[j >> 1], pk[(j >> 1) + 1], (hf * 16 + j) >> 2);
+              } else {  // layer 6: its mask is applied right here (e6), never stored
+                const float4 w7 = *reinterpret_cast<const float4 *>(S.w7 + u0 + cb + j);
+                fp = fmaf(w7.x, fmaxf(z0, 0.f), fp);
+                fp = fmaf(w7.y, fmaxf(z1, 0.f), fp);
+                fp = fmaf(w7.z, fmaxf(z2, 0.f), fp);
+                fp = fmaf(w7.w, fmaxf(z3, 0.f), fp);
+                pk[j >> 1] = pack2<F16>(z0 > 0.f ? w7.x : 0.f, z1 > 0.f ? w7.y : 0.f);
+                pk[(j >> 1) + 1] = pack2<F16>(z2 > 0.f ? w7.z : 0.f, z3 > 0.f ? w7.w : 0.f);
               }
-              st8(tA + cb / 2, pk);
             }
-            if (p < 5) mk[(p * 2 + c2) * kEpiPerSlot] = m;
+            st8(tA + cb / 2, pk);
           }
-          if (tr) tr[(p + 1) * 4 + 2] = clock64();
-          hand_off();
-          if (tr) tr[(p + 1) * 4 + 3] = clock64();
-          if (p == 5) {
-            // f = w7 . h6 + b7 (fp32, no output activation: signed value)
-            S.fpart[s][hh][row] = fp;
-            named_bar_sync(1 + s, kEpiPerSlot);
-            f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
-            if (hh == 0 && !a.detect && real && slot < lb)
-              a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
+          if (p < 5) mk[(p * 2 + c2) * kEpiPerSlot] = m;
+        }
+        if (tr) tr[(p + 1) * 4 + 2] = clock64();
+        hand_off(p + 1);
+        if (tr) tr[(p + 1) * 4 + 3] = clock64();
+        if (p == 5) {
+          // f = w7 . h6 + b7 (fp32, no output activation: signed value)
+          S.fpart[s][hh][row] = fp;
+          named_bar_sync(1 + s, kEpiPerSlot);
+          f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
+          if (hh == 0 && !a.detect && slot < lb)
+            a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
+        }
+      } else if (p < 11) {
+        // ---- backward: g_{l-1} = D; e_{l-1} = g (.) 1[z_{l-1} > 0] -> A ----
+        const int mi = 10 - p;
+#pragma unroll
+        for (int c2 = 0; c2 < 2; ++c2) {
+          const uint32_t m = mk[(mi * 2 + c2) * kEpiPerSlot];
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            uint32_t pk[8], rr[16];
+            ld16(tD + 32 * c2 + 16 * hf, rr);
+            wait_ld();
+            if (tr && c2 + hf == 0) tr[(p + 1) * 4 + 0] = clock64();
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) {
+              uint32_t lo, hi;
+              mask_expand(m, (hf * 16 + j) >> 2, lo, hi);
+              pk[j >> 1] = pack2<F16>(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1])) & lo;
+              pk[(j >> 1) + 1] = pack2<F16>(__uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3])) & hi;
+            }
+            st8(tA + 16 * c2 + 8 * hf, pk);
           }
-        } else if (p < 11) {
-          // ---- backward: g_{l-1} = D; e_{l-1} = g (.) 1[z_{l-1} > 0] -> A ----
-          const int mi = 10 - p;
+        }
+        if (tr) tr[(p + 1) * 4 + 2] = clock64();
+        hand_off(p + 1);
+        if (tr) tr[(p + 1) * 4 + 3] = clock64();
+        if (p == 6 && hh == 0 && a.detect) {
+          // A6/A7 (overlaps the tensor core): threshold, per-tile slots, per-waypoint min key
+          act = live && (f - a.delta <= a.tau);
+          const unsigned bal = __ballot_sync(0xffffffffu, act);
+          unsigned long long key = ~0ull;
+          if (live)
+            key = ((unsigned long long)ord_f32(f) << 32) |
+                  (unsigned long long)local_to_global(slot, a.scene.rank, a.scene.world);
 #pragma unroll
-          for (int c2 = 0; c2 < 2; ++c2) {
-            const uint32_t m = mk[(mi * 2 + c2) * kEpiPerSlot];
+          for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+            key = other < key ? other : key;
+          }
+          if (lane == 0) {
+            S.act[s][qd] = bal;
+            S.kmin[s][qd] = key;
+          }
+          named_bar_sync(3 + s, 128);
+          if (row == 0) {
+            unsigned long long km = S.kmin[s][0];
+            int cnt = 0;
 #pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-              uint32_t pk[8], rr[16];
-              ld16(tD + 32 * c2 + 16 * hf, rr);
-              wait_ld();
-              if (tr && c2 + hf == 0) tr[(p + 1) * 4 + 0] = clock64();
-#pragma unroll
-              for (int j = 0; j < 16; j += 4) {
-                uint32_t lo, hi;
-                mask_expand(m, (hf * 16 + j) >> 2, lo, hi);
-                pk[j >> 1] = pack2<F16>(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1])) & lo;
-                pk[(j >> 1) + 1] = pack2<F16>(__uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3])) & hi;
+            for (int i = 0; i < 4; ++i) {
+              km = S.kmin[s][i] < km ? S.kmin[s][i] : km;
+              cnt += __popc(S.act[s][i]);
+            }
+            if (km != ~0ull) atomicMin(a.ds.wp_key + w, km);
+            int base = 0;
+            if (cnt > 0) {
+              const unsigned long long b = atomicAdd(a.ds.counter, (unsigned long long)cnt);
+              if (b + cnt > (unsigned long long)a.ds.max_active) {
+                atomicOr(a.ds.counter + 1, 1ull);
+                base = -1;
+              } else {
+                base = (int)b;
               }
-              st8(tA + 16 * c2 + 8 * hf, pk);
             }
+            S.sbase[s] = base;
+            a.ds.tile_meta[T] = make_int2(base, cnt);
           }
-          if (tr) tr[(p + 1) * 4 + 2] = clock64();
-          hand_off();
-          if (tr) tr[(p + 1) * 4 + 3] = clock64();
-          if (p == 6 && hh == 0 && a.detect) {
-            // A6/A7 (overlaps the tensor core): threshold, per-tile slots, per-waypoint min key
-            act = real && live && (f - a.delta <= a.tau);
-            const unsigned bal = __ballot_sync(0xffffffffu, act);
-            unsigned long long key = ~0ull;
-            if (real && live)
-              key = ((unsigned long long)ord_f32(f) << 32) |
-                    (unsigned long long)local_to_global(slot, a.scene.rank, a.scene.world);
+          named_bar_sync(3 + s, 128);
+          my_base = S.sbase[s];
+          my_rank = __popc(bal & ((1u << lane) - 1u));
+          for (int i = 0; i < qd; ++i) my_rank += __popc(S.act[s][i]);
+        }
+        if (p == 7) pt_next = load_pt(T + 2 * (int64_t)gridDim.x);  // latency hidden by 4 phases
+      } else if (hh == 0) {
+        // ---- g0 = W1^T e1 (16 columns); d f / d q by the chain rule (R3) ----
+        uint32_t r[16];
+        ld16(tS, r);
+        wait_ld();
+        float gq[kNdof];
+        gq[0] = a.tgrad ? __uint_as_float(r[3]) : -__uint_as_float(r[0]);
+        gq[1] = a.tgrad ? __uint_as_float(r[4]) : -__uint_as_float(r[1]);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-              key = other < key ? other : key;
-            }
-            if (lane == 0) {
-              S.act[s][qd] = bal;
-              S.kmin[s][qd] = key;
-            }
-            named_bar_sync(3 + s, 128);
-            if (row == 0 && real) {
-              unsigned long long km = S.kmin[s][0];
-              int cnt = 0;
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                km = S.kmin[s][i] < km ? S.kmin[s][i] : km;
-                cnt += __popc(S.act[s][i]);
-              }
-              if (km != ~0ull) atomicMin(a.ds.wp_key + w, km);
-              int base = 0;
-              if (cnt > 0) {
-                const unsigned long long b = atomicAdd(a.ds.counter, (unsigned long long)cnt);
-                if (b + cnt > (unsigned long long)a.ds.max_active) {
-                  atomicOr(a.ds.counter + 1, 1ull);
-                  base = -1;
-                } else {
-                  base = (int)b;
-                }
-              }
-              S.sbase[s] = base;
-              a.ds.tile_meta[T] = make_int2(base, cnt);
-            }
-            named_bar_sync(3 + s, 128);
-            my_base = real ? S.sbase[s] : -1;
-            my_rank = __popc(bal & ((1u << lane) - 1u));
-            for (int i = 0; i < qd; ++i) my_rank += __popc(S.act[s][i]);
+        for (int i = 0; i < 7; ++i) gq[2 + i] = __uint_as_float(r[5 + i]);
+        if (a.detect) {
+          if (act && my_base >= 0) {
+            float4 *dst = reinterpret_cast<float4 *>(a.ds.staging + my_base + my_rank);
+            dst[0] = make_float4(f, gq[0], gq[1], gq[2]);
+            dst[1] = make_float4(gq[3], gq[4], gq[5], gq[6]);
+            dst[2] = make_float4(gq[7], gq[8], __uint_as_float((unsigned)w),
+                                 __uint_as_float((unsigned)local_to_global(slot, a.scene.rank, a.scene.world)));
           }
-          if (p == 7) pt_next = load_pt(T2 + 2 * ncl);  // latency hidden by 4 phases
-        } else if (hh == 0) {
-          // ---- g0 = W1^T e1 (16 of the 32 columns); d f / d q by the chain rule (R3) ----
-          uint32_t r[16];
-          ld16(tS, r);
-          wait_ld();
-          float gq[kNdof];
-          gq[0] = a.tgrad ? __uint_as_float(r[3]) : -__uint_as_float(r[0]);
-          gq[1] = a.tgrad ? __uint_as_float(r[4]) : -__uint_as_float(r[1]);
+        } else if (a.grads && slot < lb) {
+          float *o = a.grads + ((int64_t)w * lb + slot) * kNdof;
 #pragma unroll
-          for (int i = 0; i < 7; ++i) gq[2 + i] = __uint_as_float(r[5 + i]);
-          if (a.detect) {
-            if (act && my_base >= 0) {
-              float4 *dst = reinterpret_cast<float4 *>(a.ds.staging + my_base + my_rank);
-              dst[0] = make_float4(f, gq[0], gq[1], gq[2]);
-              dst[1] = make_float4(gq[3], gq[4], gq[5], gq[6]);
-              dst[2] = make_float4(gq[7], gq[8], __uint_as_float((unsigned)w),
-                                   __uint_as_float((unsigned)local_to_global(slot, a.scene.rank, a.scene.world)));
-            }
-          } else if (a.grads && real && slot < lb) {
-            float *o = a.grads + ((int64_t)w * lb + slot) * kNdof;
-#pragma unroll
-            for (int i = 0; i < kNdof; ++i) o[i] = live ? gq[i] : 0.f;
-          }
+          for (int i = 0; i < kNdof; ++i) o[i] = live ? gq[i] : 0.f;
         }
       }
     }
   }
   fence_before();
-  cluster_sync();  // both CTAs done with TMEM and with each other's barriers
+  __syncthreads();
   fence_after();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512) : "memory");
+  if (warp == 0) tmem_dealloc(tbase, 512);
 }
 
 // ------------------------------------------------------------------ self-test kernel
@@ -584,11 +518,10 @@ cudaError_t launch_tc_t(const WeightsBF16 &w, const QueryArgs &a, int num_sms, c
   cudaError_t e = cudaFuncSetAttribute(k_mlp_tc<F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t n_tiles = (int64_t)a.n_wp * a.tiles_per_wp;
-  const int64_t n_super = (n_tiles + 1) / 2;            // tile pairs
-  int64_t clusters = (n_super + 1) / 2;                 // 2 slots per CTA pair
-  if (clusters > num_sms / 2) clusters = num_sms / 2;
-  if (clusters < 1) return cudaSuccess;
-  k_mlp_tc<F16><<<(unsigned)(2 * clusters), kThreads, smem, s>>>(w, a);
+  int64_t grid = (n_tiles + 1) / 2;
+  if (grid > num_sms) grid = num_sms;
+  if (grid < 1) return cudaSuccess;
+  k_mlp_tc<F16><<<(unsigned)grid, kThreads, smem, s>>>(w, a);
   return cudaGetLastError();
 }
 
