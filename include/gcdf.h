@@ -202,13 +202,16 @@ int gcdf_profile_read(gcdf_ctx *ctx, double *mlp_ms, int64_t *mlp_launches, int 
    D_dev fp32 [128][128] output.  mode 0: D = A B^T, B [128][128] (K-major B);
    mode 1: D = A B, B [128][128] (MN-major B); mode 2: D[:, 0:16] = A B^T, B [16][128];
    mode | 4: the same with fp16 operands instead of bf16.
+   mode 16 + 2 v + f16 (v = 0..4, 8..12; 5..7 = CTA-pair probes): UMMA throughput probe,
+   A and B ignored, D[0] = cycles and D[1] = number of UMMAs (tools/mma_probe.py).
    Synchronizes the stream.  UNSUPPORTED without the tcgen05 build. */
 int gcdf_selftest_umma(int cuda_device, int mode, const float *A_dev, const float *B_dev, float *D_dev,
                        void *stream);
 
-/* Pipeline trace of the tensor-core kernel: when trace_dev (device, 624 int64) is non-NULL,
-   CTA 0 of every later query/detect records clock64 stamps [role 3][tile 4][phase 13][4]
-   (role 0 = MMA issuer, 1/2 = the slot-0/1 epilogue).  NULL switches it off. */
+/* Pipeline trace of the tensor-core kernel: when trace_dev (device, 3744 int64) is non-NULL,
+   CTA 0 of every later query/detect records clock64 stamps [role 18][tile 4][phase 13][4]
+   (role 0 = MMA issuer, 1 + w = epilogue warp w = 0..15 (warps 0-7 serve tile slot 0,
+   8-15 slot 1), 17 = MMA issuer wait stamps).  NULL switches it off. */
 int gcdf_debug_trace(gcdf_ctx *ctx, long long *trace_dev);
 
 #ifdef __cplusplus

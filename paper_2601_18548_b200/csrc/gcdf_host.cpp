@@ -152,6 +152,7 @@ WeightsBF16 bf16_view(const gcdf_ctx *c) {
   w.w1t_sw128 = c->ws + wo + 5 * kBfMat;
   w.b1_nosw = c->ws + wo + 5 * kBfMat + kBfW1t;
   w.bext_nosw = c->ws + wo + 5 * kBfMat + kBfW1t + kBfB1;
+  w.bh = f.bias[0];  // the five fp32 bias rows are contiguous in the fp32 block
   w.w7 = f.w7;
   w.b7 = f.b7;
   return w;
@@ -714,7 +715,7 @@ int gcdf_debug_trace(gcdf_ctx *c, long long *trace_dev) {
 
 int gcdf_selftest_umma(int dev, int mode, const float *A, const float *B, float *D, void *stream) {
   if (!tc_compiled()) return GCDF_ERR_UNSUPPORTED;
-  if (mode < 0 || (mode < 16 && (mode > 6 || (mode & 3) > 2)) || mode > 31 || !A || !B || !D) return GCDF_ERR_INVALID_ARG;
+  if (mode < 0 || (mode < 16 && (mode > 6 || (mode & 3) > 2)) || mode > 45 || !A || !B || !D) return GCDF_ERR_INVALID_ARG;
   if (cudaSetDevice(dev) != cudaSuccess) return GCDF_ERR_CUDA;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (launch_selftest_umma(mode, A, B, D, s) != cudaSuccess) return GCDF_ERR_CUDA;

@@ -44,6 +44,7 @@ struct WeightsBF16 {
   const void *w1t_sw128; // 16 * H * 2 bytes
   const void *b1_nosw;   // H * 32 * 2 bytes
   const void *bext_nosw; // 5 * H * 16 * 2 bytes
+  const float *bh;       // [5][H] fp32 biases of layers 2..6 (epilogue-add variant)
   const float *w7;       // [H] fp32
   float b7;
 };
@@ -79,9 +80,10 @@ struct QueryArgs {
   // diagnostics (gcdf_debug_trace): CTA 0 records clock64 stamps, NULL in normal runs
   long long *trace;
 };
-// trace layout: [role 0 = MMA thread, 1 = slot-0 epilogue, 2 = slot-1 epilogue][tile 0..3][phase 0..12][4]
-constexpr int kTraceTiles = 4, kTracePhases = 13;
-constexpr int kTraceLen = 3 * kTraceTiles * kTracePhases * 4;
+// trace layout: [role 0 = MMA thread (issue start / end per slot), 1 + w = epilogue warp w
+// (lane 0), w = 0..15, 17 = MMA thread (wait start / wait done per slot)][tile 0..3][phase 0..12][4]
+constexpr int kTraceTiles = 4, kTracePhases = 13, kTraceRoles = 18;
+constexpr int kTraceLen = kTraceRoles * kTraceTiles * kTracePhases * 4;
 
 __host__ __device__ inline int64_t local_to_global(int64_t slot, int rank, int world) {
   return ((slot / kTile) * world + rank) * kTile + slot % kTile;

@@ -27,12 +27,14 @@
 //     64h..64h+63, so every SM sub-partition runs two warps per slot, and one slot's
 //     epilogue overlaps the other slot's tensor-core work.  Warp 16 is the MMA issuer:
 //     after each epilogue phase the slot's 8 warps arrive on the slot's "A ready"
-//     mbarrier; one elected lane of warp 16 waits on it, issues the slot's next UMMAs and
-//     commits them to the slot's "D ready" mbarrier.  The tensor core executes both
-//     slots' MMAs in issue order.  12 MMA phases per tile.
-//   * Measured (profiles/r1/mma_probe.txt): at M = 128, N = 128 a single-CTA TS UMMA
-//     runs at 52-56 % of the dense peak, which bounds this kernel; a 2-CTA (M = 256)
-//     variant was measured slower end to end (K2b experiments).
+//     mbarrier; the converged MMA warp waits on it and an elected lane issues the slot's
+//     next UMMAs (operands in uniform registers) and commits them to the slot's "D ready"
+//     mbarrier.  The tensor core executes both slots' MMAs in issue order.  12 MMA phases
+//     per tile; the next tile's layer-1 operands are staged at the end of the current tile
+//     (its point prefetched by cp.async four phases earlier).
+//   * Measured (profiles/r1/mma_probe.txt, trace_tc_*.txt): a 128x128x16 UMMA runs at the
+//     dense rate (64 cycles) when the issue stream is lean; the kernel is bound by the
+//     per-slot chain MMA -> epilogue -> hand-off with two slots.
 #include "gcdf_internal.h"
 #include "tc_ptx.h"
 
@@ -53,6 +55,8 @@ constexpr int kW1tBytes = 16 * H * 2;     // 4,096
 constexpr int kB1Bytes = 32 * H * 2;      // 8,192
 constexpr int kBextBytes = 16 * H * 2;    // 4,096 per hidden layer
 constexpr uint32_t kColA = 128, kColOnes = 192;
+// or an fp32 add in the epilogue (1).
+// mbarrier waits: bit 0 = MMA thread spins with test_wait, bit 1 = epilogue warps spin
 template <bool F16> constexpr uint32_t kIdescFwd = idesc_f16kind(128, 128, false, F16);
 template <bool F16> constexpr uint32_t kIdescBwd = idesc_f16kind(128, 128, true, F16);
 template <bool F16> constexpr uint32_t kIdescFin = idesc_f16kind(128, 16, false, F16);
@@ -62,8 +66,11 @@ struct __align__(1024) SmemTC {
   uint8_t w1t[kW1tBytes];      // W1^T [16][128], SW128
   uint8_t b1[kB1Bytes];        // layer-1 split weights [128][32], no swizzle
   uint8_t bext[5][kBextBytes]; // hidden-layer bias blocks [128][16], no swizzle
-  float w7[H];
+  float w7half[H];             // w7 / 2: f = sum w7half (z6 + |z6|) = w7 . ReLU(z6), all on the FMA pipe
+  uint32_t w7h[H / 2];         // w7 as packed 16-bit pairs: e6 = w7 (.) 1[z6 > 0]
+  uint32_t one;                // 1 (runtime constant, see add7fff)
   float fpart[2][2][H];        // [slot][half][row] partial output-layer sums
+  float4 ptn[2][H];            // [slot][row] prefetched point of the slot's next tile
   uint32_t mask[2][kMasks][2][kEpiPerSlot];  // ReLU masks [slot][layer][32-unit word][thread]
   uint64_t mma_done[2];
   uint64_t epi_done[2];
@@ -99,9 +106,30 @@ DEVI void split3(float x, float *o) {
   o[2] = hi;
 }
 
-// UMMAs of MMA phase p of the tile in slot s (one thread); commit to mma_done[s]
+// The epilogue is ALU-pipe bound (F2FP, PRMT, LOP3, SHF); the "+ 0x7fff7fff" of the
+// mask tests is written as pk * one + c with a runtime one (read from shared memory) so
+// that it compiles to IMAD on the otherwise idle FMA pipe instead of VIADD on the ALU.
+DEVI uint32_t add7fff(uint32_t pk, uint32_t one) { return pk * one + 0x7fff7fffu; }
+// mask_group (tc_ptx.h) with the adds on the FMA pipe
+DEVI uint32_t mask_group_f(uint32_t pk01, uint32_t pk23, int k, uint32_t one) {
+  const uint32_t x = prmt(add7fff(pk01, one), add7fff(pk23, one), 0x7531u);
+  return (x >> k) & (0x80808080u >> k);
+}
+// 0xffff half-word masks of the nonzero halves of a packed pair of non-negative 16-bit
+// values (bit 15 of v + 0x7fff is set iff v != 0; sign-replicate bytes 1 and 3)
+DEVI uint32_t nz_halves(uint32_t pk, uint32_t one) { return prmt(add7fff(pk, one), 0u, 0xbb99u); }
+
+// UMMAs of MMA phase p of the tile whose accumulator starts at TMEM column d, committed
+// to bar.  Executed by the whole (converged) MMA warp with warp-uniform operands; one
+// elected lane issues.  Uniform operands stay in uniform registers, which keeps the issue
+// stream to a few instructions per UMMA: a lane-0-only loop paid a register-to-uniform
+// move per operand and issued at ~75-90 cycles per UMMA, slower than the tensor pipe
+// (64 cycles per 128x128x16 UMMA, tools/mma_probe.py "lean issue").
 template <bool F16>
 DEVI void issue_phase(int p, uint32_t d, uint32_t sw, uint32_t sw1t, uint32_t sb1, uint32_t sbx, uint64_t *bar) {
+  auto mma_ts = [](uint32_t dt, uint32_t at, uint64_t bd, uint32_t id, uint32_t acc) {
+    tc::mma_ts_elect(dt, at, bd, id, acc);
+  };
   const uint32_t av = d + kColA;
   if (p == 0) {  // layer 1: K = 32 split operands (bias included)
 #pragma unroll
@@ -121,7 +149,7 @@ DEVI void issue_phase(int p, uint32_t d, uint32_t sw, uint32_t sw1t, uint32_t sb
     for (int k = 0; k < 8; ++k)
       mma_ts(d, av + 8u * k, sdesc_sw128(sw1t + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin<F16>, k > 0);
   }
-  commit(bar);
+  commit_elect(bar);
 }
 
 template <bool F16>
@@ -143,7 +171,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     copy16(S.w1t, W.w1t_sw128, kW1tBytes);
     copy16(S.b1, W.b1_nosw, kB1Bytes);
     copy16(S.bext, W.bext_nosw, 5 * kBextBytes);
-    for (int i = tid; i < H; i += kThreads) S.w7[i] = __ldg(W.w7 + i);
+    for (int i = tid; i < H; i += kThreads) S.w7half[i] = 0.5f * __ldg(W.w7 + i);
+    if (tid == 0) S.one = 1u;
+    for (int i = tid; i < H / 2; i += kThreads) S.w7h[i] = pack2<F16>(__ldg(W.w7 + 2 * i), __ldg(W.w7 + 2 * i + 1));
   }
   if (warp == 0) {
     tmem_alloc(&S.tmem_base, 512);
@@ -163,22 +193,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   const uint32_t tbase = S.tmem_base;
   const int64_t n_tiles = (int64_t)a.n_wp * a.tiles_per_wp;
   const int64_t lb = a.scene.local_bound;
-  const uint32_t sw = smem_u32(S.w), sw1t = smem_u32(S.w1t), sb1 = smem_u32(S.b1), sbx = smem_u32(S.bext);
+  const int64_t stride = 2 * (int64_t)gridDim.x;
 
   if (warp == kEpiWarps) {
-    // ===================== dedicated MMA warp: one thread issues both slots' UMMAs ==========
-    if (lane == 0) {
+    // ===================== dedicated MMA warp: issues both slots' UMMAs (elected lane) ======
+    {
+      const uint32_t sw = smem_u32(S.w), sw1t = smem_u32(S.w1t), sb1 = smem_u32(S.b1);
+      const uint32_t sbx = smem_u32(S.bext);
       uint32_t phbits = 0u;  // bit s = phase parity of epi_done[s]
-      for (int64_t base = (int64_t)blockIdx.x * 2; base < n_tiles; base += 2 * (int64_t)gridDim.x) {
+      long long *tr0 = (a.trace && blockIdx.x == 0 && lane == 0) ? a.trace : nullptr;
+      int itt = 0;
+      for (int64_t base = (int64_t)blockIdx.x * 2; base < n_tiles; base += stride, ++itt) {
         const int nslots = (base + 1 < n_tiles) ? 2 : 1;
 #pragma unroll 1
         for (int p = 0; p < kPhases; ++p) {
 #pragma unroll 1
           for (int ss = 0; ss < nslots; ++ss) {
+            long long *t = (tr0 && itt < kTraceTiles) ? tr0 + ((size_t)itt * kTracePhases + p) * 4 + 2 * ss : nullptr;
+            long long *t2 = t ? t + (size_t)(kTraceRoles - 1) * kTraceTiles * kTracePhases * 4 : nullptr;
+            if (t2) t2[0] = clock64();
             mbar_wait(&S.epi_done[ss], (phbits >> ss) & 1u);
+            if (t2) t2[1] = clock64();
             phbits ^= 1u << ss;
             fence_after();
+            if (t) t[0] = clock64();
             issue_phase<F16>(p, tbase + (uint32_t)ss * 256u, sw, sw1t, sb1, sbx, &S.mma_done[ss]);
+            if (t) t[1] = clock64();
           }
         }
       }
@@ -193,8 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   const int qd = warp & 3;          // TMEM lane quarter of this warp (warp % 4)
   const int row = qd * 32 + lane;   // pair within the tile = TMEM lane
   const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-  const uint32_t tSlot = tbase + (uint32_t)s * 256u;  // MMA-side column base of this slot
-  const uint32_t tS = tSlot + lane_off;                 // this slot, this lane quarter
+  const uint32_t tS = tbase + (uint32_t)s * 256u + lane_off;  // this slot, this lane quarter
   const uint32_t tD = tS + 64u * hh;
   const uint32_t tA = tS + kColA + 32u * hh;
   const int u0 = 64 * hh;           // first unit of this thread's columns
@@ -204,86 +243,80 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     st8(tS + kColOnes, ones);
   }
   // epilogue phase done: TMEM stores complete and ordered before the MMA warp's UMMAs
-  auto hand_off = [&](int) {
+  auto hand_off = [&]() {
     wait_st();
     fence_before();
     mbar_arrive(&S.epi_done[s]);
   };
-  (void)tSlot;
+  // cp.async prefetch of this lane's point of tile TT into S.ptn[s][row] (zero if none);
+  // issued by the column-half-0 threads, which alone read it
+  auto prefetch_pt = [&](int64_t TT) {
+    const int64_t sl = (TT % a.tiles_per_wp) * kTile + row;
+    const bool ok = TT < n_tiles && sl < lb;
+    cp_async16(&S.ptn[s][row], ok ? (const void *)(a.scene.pts + sl) : (const void *)a.scene.pts, ok ? 16u : 0u);
+    cp_async_commit();
+  };
+  // A2 + A1 of tile TT: pair generation, base-frame bias p' = p - [q_x, q_y, 0]
+  // and the split layer-1 operands -> TMEM A (K = 32: half 0 writes K 0..15,
+  // half 1 K 16..31), then hand off.  Returns the pair's liveness (meaningful in half 0).
+  auto stage_a1 = [&](int64_t TT) -> bool {
+    const int wn = (int)(TT / a.tiles_per_wp);
+    const int64_t sl = (TT % a.tiles_per_wp) * kTile + row;
+    const float *qw = a.q + (int64_t)wn * kNdof;
+    float v[16];
+    bool lv = false;
+    if (hh == 0) {  // K 0..15: p'_x, p'_y, p_z, theta, j1 (3 each), x_hi of j2
+      const float4 pt = S.ptn[s][row];
+      lv = sl < lb && pt.w > 0.f;
+      split3<F16>(pt.x - __ldg(qw), v);
+      split3<F16>(pt.y - __ldg(qw + 1), v + 3);
+      split3<F16>(pt.z, v + 6);
+      split3<F16>(__ldg(qw + 2), v + 9);
+      split3<F16>(__ldg(qw + 3), v + 12);
+      v[15] = round16<F16>(__ldg(qw + 4));
+    } else {        // K 16..31: x_lo, x_hi of j2, j3..j6 (3 each), {1, 1} for b1
+      const float j2 = __ldg(qw + 4);
+      const float j2h = round16<F16>(j2);
+      v[0] = j2 - j2h;
+      v[1] = j2h;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) split3<F16>(__ldg(qw + 5 + i), v + 2 + 3 * i);
+      v[14] = 1.f;
+      v[15] = 1.f;
+    }
+    uint32_t a1[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a1[i] = pack2<F16>(v[2 * i], v[2 * i + 1]);
+    st8(tS + kColA + 8u * hh, a1);
+    hand_off();
+    return lv;
+  };
+  const uint32_t one = S.one;
   uint32_t ph = 0u;
   int it = 0;
-  const bool tracer = a.trace && blockIdx.x == 0 && hh == 0 && qd == 0 && lane == 0;
-  int w_prev = -1;
-  uint32_t qwords[8];  // the per-waypoint part of this half's A1 words
-  float q0h = 0.f;
-  // point of this lane's pair in the next tile, prefetched during the current tile
-  auto load_pt = [&](int64_t TT) -> float4 {
-    if (TT >= n_tiles) return make_float4(0.f, 0.f, 0.f, 0.f);
-    const int64_t sl = (TT % a.tiles_per_wp) * kTile + row;
-    return sl < lb ? __ldg(a.scene.pts + sl) : make_float4(0.f, 0.f, 0.f, 0.f);
-  };
-  float4 pt_next = load_pt((int64_t)blockIdx.x * 2 + s);
-  for (int64_t T = (int64_t)blockIdx.x * 2 + s; T < n_tiles; T += 2 * (int64_t)gridDim.x, ++it) {
-    long long *tr = (tracer && it < kTraceTiles) ? a.trace + (size_t)((1 + s) * kTraceTiles + it) * kTracePhases * 4 : nullptr;
+  const bool tracer = a.trace && blockIdx.x == 0 && lane == 0;  // lane 0 of every epilogue warp of CTA 0
+  bool live_n = false;
+  if ((int64_t)blockIdx.x * 2 + s < n_tiles) {
+    if (hh == 0) {
+      prefetch_pt((int64_t)blockIdx.x * 2 + s);
+      cp_async_wait_all();
+    }
+    live_n = stage_a1((int64_t)blockIdx.x * 2 + s);
+  }
+  for (int64_t T = (int64_t)blockIdx.x * 2 + s; T < n_tiles; T += stride, ++it) {
+    long long *tr = (tracer && it < kTraceTiles) ? a.trace + (size_t)((1 + warp) * kTraceTiles + it) * kTracePhases * 4 : nullptr;
     if (tr) tr[0] = clock64();
-    const int w = (int)(T / a.tiles_per_wp);
-    const int64_t slot = (T % a.tiles_per_wp) * kTile + row;
-    const float *qw = a.q + (int64_t)w * kNdof;
-    if (w != w_prev) {  // split the waypoint's [theta, j1..j6] once per waypoint
-      float v[32];
-#pragma unroll
-      for (int i = 0; i < 7; ++i) split3<F16>(__ldg(qw + 2 + i), v + 9 + 3 * i);
-      v[30] = 1.f;
-      v[31] = 1.f;
-      q0h = v[9];
-      // half 0 owns A1 words 0..7 (K 0..15): words 5..7 are per-waypoint (K 10..15);
-      // half 1 owns words 8..15 (K 16..31): all per-waypoint
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int kk = hh == 0 ? 2 * i : 16 + 2 * i;
-        qwords[i] = (hh == 0 && i < 5) ? 0u : pack2<F16>(v[kk], v[kk + 1]);
-      }
-      w_prev = w;
-    }
-    // A2: pair generation + base-frame bias p' = p - [q_x, q_y, 0]
-    const float4 pt = pt_next;
-    const bool live = slot < lb && pt.w > 0.f;
-    // ---- A1: the split layer-1 operands of this pair -> TMEM A ----
-    {
-      uint32_t a1[8];
-      if (hh == 0) {
-        float v[10];
-        split3<F16>(pt.x - __ldg(qw), v);
-        split3<F16>(pt.y - __ldg(qw + 1), v + 3);
-        split3<F16>(pt.z, v + 6);
-        v[9] = q0h;
-#pragma unroll
-        for (int i = 0; i < 5; ++i) a1[i] = pack2<F16>(v[2 * i], v[2 * i + 1]);
-#pragma unroll
-        for (int i = 5; i < 8; ++i) a1[i] = qwords[i];
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) a1[i] = qwords[i];
-      }
-      st8(tS + kColA + 8u * hh, a1);
-    }
-    if (tr) tr[2] = clock64();
-    hand_off(0);
-    if (tr) tr[3] = clock64();
-
+    const bool live = live_n;
     float f = 0.f;
-    bool act = false;
-    int my_base = -1, my_rank = 0;
+    int ridx = -1;  // staging record index (detect), -1 = none
 #pragma unroll 1
     for (int p = 0; p < kPhases; ++p) {
       mbar_wait(&S.mma_done[s], ph);
       if (tr) tr[(p + 1) * 4 + 1] = clock64();
       ph ^= 1u;
       fence_after();
-      if (p < 6) {
+      if (p < 5) {
         // ---- forward layer l = p + 1: z = D (bias folded in); h = ReLU(z) -> A ----
-        //      (l = 6: f += w7 . h6 in fp32, e6 = w7 (.) 1[z6 > 0] -> A)
-        float fp = 0.f;
 #pragma unroll
         for (int c2 = 0; c2 < 2; ++c2) {
           uint32_t m = 0u;
@@ -296,36 +329,56 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
             if (tr && cb == 0) tr[(p + 1) * 4 + 0] = clock64();
 #pragma unroll
             for (int j = 0; j < 16; j += 4) {
-              const float z0 = __uint_as_float(rr[j]), z1 = __uint_as_float(rr[j + 1]);
-              const float z2 = __uint_as_float(rr[j + 2]), z3 = __uint_as_float(rr[j + 3]);
-              if (p < 5) {
-                pk[j >> 1] = pack2_relu<F16>(z0, z1);
-                pk[(j >> 1) + 1] = pack2_relu<F16>(z2, z3);
-                m |= mask_group(pk[j >> 1], pk[(j >> 1) + 1], (hf * 16 + j) >> 2);
-              } else {  // layer 6: its mask is applied right here (e6), never stored
-                const float4 w7 = *reinterpret_cast<const float4 *>(S.w7 + u0 + cb + j);
-                fp = fmaf(w7.x, fmaxf(z0, 0.f), fp);
-                fp = fmaf(w7.y, fmaxf(z1, 0.f), fp);
-                fp = fmaf(w7.z, fmaxf(z2, 0.f), fp);
-                fp = fmaf(w7.w, fmaxf(z3, 0.f), fp);
-                pk[j >> 1] = pack2<F16>(z0 > 0.f ? w7.x : 0.f, z1 > 0.f ? w7.y : 0.f);
-                pk[(j >> 1) + 1] = pack2<F16>(z2 > 0.f ? w7.z : 0.f, z3 > 0.f ? w7.w : 0.f);
-              }
+              pk[j >> 1] = pack2_relu<F16>(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1]));
+              pk[(j >> 1) + 1] = pack2_relu<F16>(__uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3]));
+              m |= mask_group_f(pk[j >> 1], pk[(j >> 1) + 1], (hf * 16 + j) >> 2, one);
             }
             st8(tA + cb / 2, pk);
           }
-          if (p < 5) mk[(p * 2 + c2) * kEpiPerSlot] = m;
+          mk[(p * 2 + c2) * kEpiPerSlot] = m;
         }
         if (tr) tr[(p + 1) * 4 + 2] = clock64();
-        hand_off(p + 1);
+        hand_off();
         if (tr) tr[(p + 1) * 4 + 3] = clock64();
-        if (p == 5) {
-          // f = w7 . h6 + b7 (fp32, no output activation: signed value)
-          S.fpart[s][hh][row] = fp;
-          named_bar_sync(1 + s, kEpiPerSlot);
+      } else if (p == 5) {
+        // ---- layer 6: e6 = w7 (.) 1[z6 > 0] -> A; f = w7 . ReLU(z6) + b7 (fp32) ----
+        float fa[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int cb = 0; cb < 64; cb += 16) {
+          uint32_t pk[8], rr[16];
+          ld16(tD + cb, rr);
+          wait_ld();
+          if (tr && cb == 0) tr[(p + 1) * 4 + 0] = clock64();
+#pragma unroll
+          for (int j = 0; j < 16; j += 4) {
+            const float4 w7 = *reinterpret_cast<const float4 *>(S.w7half + u0 + cb + j);
+            const uint2 w2 = *reinterpret_cast<const uint2 *>(S.w7h + (u0 + cb + j) / 2);
+            const float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            const float z0 = __uint_as_float(rr[j]) + b4.x, z1 = __uint_as_float(rr[j + 1]) + b4.y;
+            const float z2 = __uint_as_float(rr[j + 2]) + b4.z, z3 = __uint_as_float(rr[j + 3]) + b4.w;
+            pk[j >> 1] = w2.x & nz_halves(pack2_relu<F16>(z0, z1), one);
+            pk[(j >> 1) + 1] = w2.y & nz_halves(pack2_relu<F16>(z2, z3), one);
+            // (w7 / 2) (z + |z|) = w7 ReLU(z) exactly (z + |z| = 2 ReLU(z), halving is exact)
+            fa[0] = fmaf(w7.x, z0 + fabsf(z0), fa[0]);
+            fa[1] = fmaf(w7.y, z1 + fabsf(z1), fa[1]);
+            fa[2] = fmaf(w7.z, z2 + fabsf(z2), fa[2]);
+            fa[3] = fmaf(w7.w, z3 + fabsf(z3), fa[3]);
+          }
+          st8(tA + cb / 2, pk);
+        }
+        if (tr) tr[(p + 1) * 4 + 2] = clock64();
+        hand_off();
+        if (tr) tr[(p + 1) * 4 + 3] = clock64();
+        // f = w7 . h6 + b7 (fp32, no output activation: signed value)
+        S.fpart[s][hh][row] = (fa[0] + fa[1]) + (fa[2] + fa[3]);
+        named_bar_sync(1 + s, kEpiPerSlot);
+        if (hh == 0) {
           f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
-          if (hh == 0 && !a.detect && slot < lb)
-            a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
+          if (!a.detect) {
+            const int w = (int)(T / a.tiles_per_wp);
+            const int64_t slot = (T % a.tiles_per_wp) * kTile + row;
+            if (slot < lb) a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
+          }
         }
       } else if (p < 11) {
         // ---- backward: g_{l-1} = D; e_{l-1} = g (.) 1[z_{l-1} > 0] -> A ----
@@ -350,11 +403,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
           }
         }
         if (tr) tr[(p + 1) * 4 + 2] = clock64();
-        hand_off(p + 1);
+        hand_off();
         if (tr) tr[(p + 1) * 4 + 3] = clock64();
         if (p == 6 && hh == 0 && a.detect) {
           // A6/A7 (overlaps the tensor core): threshold, per-tile slots, per-waypoint min key
-          act = live && (f - a.delta <= a.tau);
+          const int w = (int)(T / a.tiles_per_wp);
+          const int64_t slot = (T % a.tiles_per_wp) * kTile + row;
+          const bool act = live && (f - a.delta <= a.tau);
           const unsigned bal = __ballot_sync(0xffffffffu, act);
           unsigned long long key = ~0ull;
           if (live)
@@ -393,34 +448,48 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
             a.ds.tile_meta[T] = make_int2(base, cnt);
           }
           named_bar_sync(3 + s, 128);
-          my_base = S.sbase[s];
-          my_rank = __popc(bal & ((1u << lane) - 1u));
-          for (int i = 0; i < qd; ++i) my_rank += __popc(S.act[s][i]);
+          const int base = S.sbase[s];
+          int rk = __popc(bal & ((1u << lane) - 1u));
+          for (int i = 0; i < qd; ++i) rk += __popc(S.act[s][i]);
+          ridx = (act && base >= 0) ? base + rk : -1;
         }
-        if (p == 7) pt_next = load_pt(T + 2 * (int64_t)gridDim.x);  // latency hidden by 4 phases
-      } else if (hh == 0) {
+        if (p == 7 && hh == 0) prefetch_pt(T + stride);  // lands during the next 4 phases
+      } else {
         // ---- g0 = W1^T e1 (16 columns); d f / d q by the chain rule (R3) ----
+        // D is read first; the next tile's layer-1 operands are handed off before the
+        // outputs of this tile are written (short tile-boundary critical path).
         uint32_t r[16];
-        ld16(tS, r);
-        wait_ld();
-        float gq[kNdof];
-        gq[0] = a.tgrad ? __uint_as_float(r[3]) : -__uint_as_float(r[0]);
-        gq[1] = a.tgrad ? __uint_as_float(r[4]) : -__uint_as_float(r[1]);
-#pragma unroll
-        for (int i = 0; i < 7; ++i) gq[2 + i] = __uint_as_float(r[5 + i]);
-        if (a.detect) {
-          if (act && my_base >= 0) {
-            float4 *dst = reinterpret_cast<float4 *>(a.ds.staging + my_base + my_rank);
-            dst[0] = make_float4(f, gq[0], gq[1], gq[2]);
-            dst[1] = make_float4(gq[3], gq[4], gq[5], gq[6]);
-            dst[2] = make_float4(gq[7], gq[8], __uint_as_float((unsigned)w),
-                                 __uint_as_float((unsigned)local_to_global(slot, a.scene.rank, a.scene.world)));
-          }
-        } else if (a.grads && slot < lb) {
-          float *o = a.grads + ((int64_t)w * lb + slot) * kNdof;
-#pragma unroll
-          for (int i = 0; i < kNdof; ++i) o[i] = live ? gq[i] : 0.f;
+        if (hh == 0) {
+          ld16(tS, r);
+          wait_ld();
+          cp_async_wait_all();  // this thread's prefetched point of the next tile
         }
+        if (tr) tr[(p + 1) * 4 + 0] = clock64();
+        if (T + stride < n_tiles) live_n = stage_a1(T + stride);
+        if (tr) tr[(p + 1) * 4 + 2] = clock64();
+        if (hh == 0) {
+          const int w = (int)(T / a.tiles_per_wp);
+          const int64_t slot = (T % a.tiles_per_wp) * kTile + row;
+          float gq[kNdof];
+          gq[0] = a.tgrad ? __uint_as_float(r[3]) : -__uint_as_float(r[0]);
+          gq[1] = a.tgrad ? __uint_as_float(r[4]) : -__uint_as_float(r[1]);
+#pragma unroll
+          for (int i = 0; i < 7; ++i) gq[2 + i] = __uint_as_float(r[5 + i]);
+          if (a.detect) {
+            if (ridx >= 0) {
+              float4 *dst = reinterpret_cast<float4 *>(a.ds.staging + ridx);
+              dst[0] = make_float4(f, gq[0], gq[1], gq[2]);
+              dst[1] = make_float4(gq[3], gq[4], gq[5], gq[6]);
+              dst[2] = make_float4(gq[7], gq[8], __uint_as_float((unsigned)w),
+                                   __uint_as_float((unsigned)local_to_global(slot, a.scene.rank, a.scene.world)));
+            }
+          } else if (a.grads && slot < lb) {
+            float *o = a.grads + ((int64_t)w * lb + slot) * kNdof;
+#pragma unroll
+            for (int i = 0; i < kNdof; ++i) o[i] = live ? gq[i] : 0.f;
+          }
+        }
+        if (tr) tr[(p + 1) * 4 + 3] = clock64();
       }
     }
   }
@@ -575,8 +644,23 @@ __global__ void __launch_bounds__(128, 1) k_mma_probe(int variant, int reps, flo
     const uint32_t d0 = tb, av = tb + 256;
     long long t0 = clock64();
     int n = 0;
-    for (int r = 0; r < reps; ++r) {
-      const uint32_t d = (variant == 2 && (r & 1)) ? tb + 128 : d0;
+    if (variant >= 13) {  // minimal issue overhead: descriptors precomputed, branch-free loop
+      uint64_t bd[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        bd[k] = variant == 13 ? sdesc_sw128(sB + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024)
+                              : sdesc_sw128(sB + k * 2048, 16384, 1024);
+      const uint32_t idesc = variant == 13 ? kIdescFwd<F16> : kIdescBwd<F16>;
+      t0 = clock64();
+#pragma unroll 1
+      for (int r = 0; r < reps; ++r) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mma_ts(d0, av + 8u * k, bd[k], idesc, k > 0);
+      }
+      n = reps * 8;
+    }
+    for (int r = 0; r < (variant >= 13 ? 0 : reps); ++r) {
+      const uint32_t d = (variant == 2 && (r & 1)) ? tb + 128 : d0;  // (variants 9, 11 use d + 64 / d + 128 too)
       for (int k = 0; k < 8; ++k, ++n) {
         if (variant == 0 || variant == 2)
           mma_ts(d, av + 8u * k, sdesc_sw128(sB + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024), kIdescFwd<F16>, k > 0);
@@ -590,9 +674,30 @@ __global__ void __launch_bounds__(128, 1) k_mma_probe(int variant, int reps, flo
               "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
               "l"(ad), "l"(bd), "r"(kIdescFwd<F16>), "r"((uint32_t)(k > 0))
               : "memory");
-        } else {
+        } else if (variant == 4) {
           mma_ts(d, av + 8u * k, sdesc_sw128(sB + (k >> 2) * 32768 + (k & 3) * 32, 16, 1024),
                  idesc_f16kind(128, 256, false, F16), k > 0);
+        } else if (variant == 8 || variant == 9) {  // N = 64 (9: two accumulators, k-step interleaved)
+          const uint64_t bd = sdesc_sw128(sB + (k >> 2) * 8192 + (k & 3) * 32, 16, 1024);
+          mma_ts(d, av + 8u * k, bd, idesc_f16kind(128, 64, false, F16), k > 0);
+          if (variant == 9) {
+            mma_ts(d + 64, av + 8u * k, bd, idesc_f16kind(128, 64, false, F16), k > 0);
+            ++n;
+          }
+        } else if (variant == 10) {  // N = 16
+          mma_ts(d, av + 8u * k, sdesc_sw128(sB + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024),
+                 idesc_f16kind(128, 16, false, F16), k > 0);
+        } else if (variant == 11) {  // N = 128, two accumulators (two tiles), k-step interleaved
+          const uint64_t bd = sdesc_sw128(sB + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
+          mma_ts(d, av + 8u * k, bd, kIdescFwd<F16>, k > 0);
+          mma_ts(d + 128, av + 64 + 8u * k, bd, kIdescFwd<F16>, k > 0);
+          ++n;
+        } else {  // 12: N = 128 K-major, A in TMEM, K = 32 per step pair issued as one phase of 9 incl. a no-swizzle step
+          mma_ts(d, av + 8u * k, sdesc_sw128(sB + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024), kIdescFwd<F16>, k > 0);
+          if (k == 7) {
+            mma_ts(d, av, sdesc_nosw(sA, 2048, 128), kIdescFwd<F16>, 1u);
+            ++n;
+          }
         }
       }
     }
@@ -690,7 +795,7 @@ cudaError_t launch_selftest_umma(int mode, const float *A, const float *B, float
     k<<<2, 128, smem, s>>>(variant, 200, D);
     return cudaGetLastError();
   }
-  if (mode >= 16) {  // UMMA throughput probe: mode = 16 + 2 * variant + f16
+  if (mode >= 16) {  // UMMA throughput probe: mode = 16 + 2 * variant + f16 (variants 0..4, 8..12)
     const int variant = (mode - 16) >> 1;
     const bool f16 = (mode & 1) != 0;
     const int smem = 96 * 1024 + 1024;

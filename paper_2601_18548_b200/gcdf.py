@@ -6,6 +6,7 @@ path: if libgcdf.so is missing or no B200 is present, construction raises.
 """
 from __future__ import annotations
 
+import os
 import ctypes as C
 from pathlib import Path
 
@@ -13,7 +14,7 @@ import numpy as np
 import torch
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libgcdf.so"
+LIB_PATH = Path(os.environ.get("GCDF_LIB", _PKG / "libgcdf.so"))  # GCDF_LIB: dev builds (tools/variants.py)
 
 FP32, BF16, FP16 = 0, 1, 2
 TGRAD_CHAINRULE, TGRAD_QCHANNEL = 0, 1
@@ -153,7 +154,7 @@ class Context:
         return int(self.lib.gcdf_launch_count(self._h))
 
     def debug_trace(self, buf: torch.Tensor | None) -> None:
-        """Diagnostics: pipeline clock64 trace of CTA 0 (int64 [624] on the device) or None."""
+        """Diagnostics: pipeline clock64 trace of CTA 0 (int64 [18*4*13*4] on the device) or None."""
         self._check(self.lib.gcdf_debug_trace(self._h, _ptr(buf)))
 
     def profile_enable(self, on: bool = True) -> None:

@@ -8,13 +8,16 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2601_18548_b200.gcdf import selftest_umma  # noqa: E402
 
 names = ["TS K-major N128", "TS MN-major N128", "TS N128 two accumulators", "SS K-major N128", "TS K-major N256",
-         "2CTA TS M256 N128", "2CTA SS M256 N128", "2CTA TS M256 N256"]
+         "2CTA TS M256 N128", "2CTA SS M256 N128", "2CTA TS M256 N256", "TS N64", "TS N64 two acc interleaved",
+         "TS N16", "TS N128 two acc k-interleaved", "TS N128 + nosw bias step", "TS K-major N128 lean issue",
+         "TS MN-major N128 lean issue"]
+NS = [128, 128, 128, 128, 256, 128, 128, 256, 64, 64, 16, 128, 128, 128, 128]
 A = torch.zeros(128, 128, device="cuda")
 for v, name in enumerate(names):
     for f16 in (1, 0):
         D = selftest_umma(16 + 2 * v + f16, A, A)
         cyc, n = D[0, 0].item(), D[0, 1].item()
-        N = 256 if v in (4, 7) else 128
+        N = NS[v]
         ideal = 128 * N / 256  # cycles per (M=128 per SM) x N x 16 MMA at 8192 dense flops/clk/SM
         print(f"{name:28s} {'fp16' if f16 else 'bf16'}: {cyc / n:7.1f} cycles/MMA (ideal {ideal:.0f}) "
               f"-> {100 * ideal / (cyc / n):5.1f}% of dense peak")
