@@ -202,7 +202,7 @@ int gcdf_profile_read(gcdf_ctx *ctx, double *mlp_ms, int64_t *mlp_launches, int 
    D_dev fp32 [128][128] output.  mode 0: D = A B^T, B [128][128] (K-major B);
    mode 1: D = A B, B [128][128] (MN-major B); mode 2: D[:, 0:16] = A B^T, B [16][128];
    mode | 4: the same with fp16 operands instead of bf16.
-   mode 16 + 2 v + f16 (v = 0..4, 8..12; 5..7 = CTA-pair probes): UMMA throughput probe,
+   mode 16 + 2 v + f16 (v = 0..4, 8..25; 5..7 = CTA-pair probes): UMMA throughput probe,
    A and B ignored, D[0] = cycles and D[1] = number of UMMAs (tools/mma_probe.py).
    Synchronizes the stream.  UNSUPPORTED without the tcgen05 build. */
 int gcdf_selftest_umma(int cuda_device, int mode, const float *A_dev, const float *B_dev, float *D_dev,

@@ -6,7 +6,7 @@
 // value + gradient :394 (dense gradient R^{NM x n}); constraint f - delta >= 0 :362-363;
 // union = min :164; c_gcdf step-major order :414-435.  DESIGN.md §5 "K2b".
 //
-// Design (H = 128, one persistent CTA per SM, 544 threads = 16 epilogue warps + 1 MMA warp):
+// Design (H = 128, one persistent CTA per SM, 576 threads = 16 epilogue warps + 2 MMA warps):
 //   * Every affine layer of a 128-pair tile is a UMMA with M = 128 pairs, A in TMEM and B
 //     resident in shared memory for the whole kernel:
 //       - layer 1 (12 -> 128): K = 32 of split hi/lo 16-bit operands (A = {x_hi, x_lo,
@@ -25,13 +25,14 @@
 //     1 (D [0,128), A [128,192), ones [192,200)).  Each slot has 8 epilogue warps: warp
 //     (h, q) owns TMEM lanes 32q..32q+31 (the tile's pairs) and accumulator columns
 //     64h..64h+63, so every SM sub-partition runs two warps per slot, and one slot's
-//     epilogue overlaps the other slot's tensor-core work.  Warp 16 is the MMA issuer:
-//     after each epilogue phase the slot's 8 warps arrive on the slot's "A ready"
-//     mbarrier; the converged MMA warp waits on it and an elected lane issues the slot's
-//     next UMMAs (operands in uniform registers) and commits them to the slot's "D ready"
-//     mbarrier.  The tensor core executes both slots' MMAs in issue order.  12 MMA phases
-//     per tile; the next tile's layer-1 operands are staged at the end of the current tile
-//     (its point prefetched by cp.async four phases earlier).
+//     epilogue overlaps the other slot's tensor-core work.  Warp 16 + s issues slot s's
+//     MMAs: after each epilogue phase the slot's 8 warps arrive on the slot's "A ready"
+//     mbarrier; the converged MMA warp waits on it (and on its turn: the slots alternate
+//     phase by phase) and an elected lane issues the slot's next UMMAs (operands in
+//     uniform registers) and commits them to the slot's "D ready" mbarrier.  One issuer
+//     per slot keeps the other slot's UMMAs flowing while a commit drains.  12 MMA
+//     phases per tile; the next tile's layer-1 operands are staged at the end of the
+//     current tile (its point prefetched by cp.async four phases earlier).
 //   * Measured (profiles/r1/mma_probe.txt, trace_tc_*.txt): a 128x128x16 UMMA runs at the
 //     dense rate (64 cycles) when the issue stream is lean; the kernel is bound by the
 //     per-slot chain MMA -> epilogue -> hand-off with two slots.
@@ -44,8 +45,17 @@ namespace {
 using namespace tc;
 
 constexpr int H = 128;
+#ifndef GCDF_TC_NOEPI
+#define GCDF_TC_NOEPI 0
+#endif
 constexpr int kEpiWarps = 16;             // warps 0..15: epilogue (8 per tile slot)
-constexpr int kWarps = kEpiWarps + 1;     // warp 16: MMA issuer
+// MMA issue (dev switch): 1 = one MMA warp per slot (default), 0 = one MMA warp for both
+// slots.  (Measured: 1 is ~1 % faster; the last epilogue warp issuing instead of an MMA
+// warp was 7 % slower.)
+#ifndef GCDF_TC_ISSUE
+#define GCDF_TC_ISSUE 1
+#endif
+constexpr int kWarps = kEpiWarps + (GCDF_TC_ISSUE == 0 ? 1 : 2);
 constexpr int kThreads = kWarps * 32;
 constexpr int kEpiPerSlot = 256;
 constexpr int kPhases = 12;               // MMA phases per tile
@@ -74,6 +84,7 @@ struct __align__(1024) SmemTC {
   uint32_t mask[2][kMasks][2][kEpiPerSlot];  // ReLU masks [slot][layer][32-unit word][thread]
   uint64_t mma_done[2];
   uint64_t epi_done[2];
+  uint32_t turn;               // (GCDF_TC_ISSUE 1) global issue-order counter
   unsigned act[2][4];
   unsigned long long kmin[2][4];
   int sbase[2];
@@ -125,10 +136,12 @@ DEVI uint32_t nz_halves(uint32_t pk, uint32_t one) { return prmt(add7fff(pk, one
 // stream to a few instructions per UMMA: a lane-0-only loop paid a register-to-uniform
 // move per operand and issued at ~75-90 cycles per UMMA, slower than the tensor pipe
 // (64 cycles per 128x128x16 UMMA, tools/mma_probe.py "lean issue").
-template <bool F16>
-DEVI void issue_phase(int p, uint32_t d, uint32_t sw, uint32_t sw1t, uint32_t sb1, uint32_t sbx, uint64_t *bar) {
+template <bool F16, bool kElect = true>
+DEVI void issue_phase(int p, uint32_t d, uint32_t sw, uint32_t sw1t, uint32_t sb1, uint32_t sbx, uint64_t *bar,
+                      volatile uint32_t *turn = nullptr, uint32_t next_turn = 0u) {
   auto mma_ts = [](uint32_t dt, uint32_t at, uint64_t bd, uint32_t id, uint32_t acc) {
-    tc::mma_ts_elect(dt, at, bd, id, acc);
+    if constexpr (kElect) tc::mma_ts_elect(dt, at, bd, id, acc);
+    else tc::mma_ts(dt, at, bd, id, acc);
   };
   const uint32_t av = d + kColA;
   if (p == 0) {  // layer 1: K = 32 split operands (bias included)
@@ -149,7 +162,9 @@ DEVI void issue_phase(int p, uint32_t d, uint32_t sw, uint32_t sw1t, uint32_t sb
     for (int k = 0; k < 8; ++k)
       mma_ts(d, av + 8u * k, sdesc_sw128(sw1t + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin<F16>, k > 0);
   }
-  commit_elect(bar);
+  if (turn) *turn = next_turn;  // (two MMA warps) the other slot may issue now
+  if constexpr (kElect) commit_elect(bar);
+  else tc::commit(bar);
 }
 
 template <bool F16>
@@ -184,6 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     mbar_init(&S.mma_done[1], 1);
     mbar_init(&S.epi_done[0], kEpiPerSlot);
     mbar_init(&S.epi_done[1], kEpiPerSlot);
+    S.turn = 0u;
     fence_barrier_init();
   }
   fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
@@ -195,7 +211,51 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   const int64_t lb = a.scene.local_bound;
   const int64_t stride = 2 * (int64_t)gridDim.x;
 
-  if (warp == kEpiWarps) {
+#if GCDF_TC_ISSUE == 1
+  if (warp >= kEpiWarps) {
+    // ===================== two MMA warps: warp 16 + s issues slot s's UMMAs ================
+    // A commit stalls its issuing thread until the committed MMAs drain; with one issuer per
+    // slot the other slot's UMMAs keep the tensor pipe busy meanwhile (tools/mma_probe.py
+    // "two issuers").  The slots still alternate: a shared turn counter orders slot 0's
+    // phase p before slot 1's phase p before slot 0's phase p + 1.
+    const int ss = warp - kEpiWarps;
+    const uint32_t sw = smem_u32(S.w), sw1t = smem_u32(S.w1t), sb1 = smem_u32(S.b1);
+    const uint32_t sbx = smem_u32(S.bext);
+    volatile uint32_t *turn = &S.turn;
+    uint32_t ph = 0u;
+    long long *tr0 = (a.trace && blockIdx.x == 0 && lane == 0) ? a.trace : nullptr;
+    uint32_t seq = (uint32_t)ss;  // this slot's position in the global issue order
+    int itt = 0;
+    for (int64_t base = (int64_t)blockIdx.x * 2; base < n_tiles; base += stride, ++itt) {
+      const bool two = base + 1 < n_tiles;
+      if (ss == 1 && !two) break;
+#pragma unroll 1
+      for (int p = 0; p < kPhases; ++p, seq += 2) {
+        long long *t = (tr0 && itt < kTraceTiles) ? tr0 + ((size_t)itt * kTracePhases + p) * 4 + 2 * ss : nullptr;
+        long long *t2 = t ? t + (size_t)(kTraceRoles - 1) * kTraceTiles * kTracePhases * 4 : nullptr;
+        if (t2) t2[0] = clock64();
+        mbar_wait(&S.epi_done[ss], ph);
+        ph ^= 1u;
+        if (two) {
+          const long long tw = clock64();
+          while (*turn != seq) {
+            if (clock64() - tw > (1ll << 34)) __trap();
+          }
+        }
+        if (t2) t2[1] = clock64();
+        fence_after();
+        if (t) t[0] = clock64();
+        issue_phase<F16>(p, tbase + (uint32_t)ss * 256u, sw, sw1t, sb1, sbx, &S.mma_done[ss], two ? turn : nullptr, seq + 1);
+        if (t) t[1] = clock64();
+      }
+    }
+    __syncwarp();
+    fence_before();
+    __syncthreads();
+    return;
+  }
+#endif
+  if (GCDF_TC_ISSUE == 0 && warp == kEpiWarps) {
     // ===================== dedicated MMA warp: issues both slots' UMMAs (elected lane) ======
     {
       const uint32_t sw = smem_u32(S.w), sw1t = smem_u32(S.w1t), sb1 = smem_u32(S.b1);
@@ -243,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     st8(tS + kColOnes, ones);
   }
   // epilogue phase done: TMEM stores complete and ordered before the MMA warp's UMMAs
-  auto hand_off = [&]() {
+  auto hand_off = [&](int, bool) {
     wait_st();
     fence_before();
     mbar_arrive(&S.epi_done[s]);
@@ -288,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
 #pragma unroll
     for (int i = 0; i < 8; ++i) a1[i] = pack2<F16>(v[2 * i], v[2 * i + 1]);
     st8(tS + kColA + 8u * hh, a1);
-    hand_off();
+    hand_off(0, s == 1 || TT + 1 < n_tiles);
     return lv;
   };
   const uint32_t one = S.one;
@@ -315,6 +375,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
       if (tr) tr[(p + 1) * 4 + 1] = clock64();
       ph ^= 1u;
       fence_after();
+#if GCDF_TC_NOEPI
+      // timing experiment only: no epilogue work (results are garbage)
+      if (p < 11) {
+        if (tr) tr[(p + 1) * 4 + 2] = clock64();
+        hand_off(p + 1, s == 1 || T + 1 < n_tiles);
+        if (tr) tr[(p + 1) * 4 + 3] = clock64();
+        continue;
+      }
+#endif
       if (p < 5) {
         // ---- forward layer l = p + 1: z = D (bias folded in); h = ReLU(z) -> A ----
 #pragma unroll
@@ -338,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
           mk[(p * 2 + c2) * kEpiPerSlot] = m;
         }
         if (tr) tr[(p + 1) * 4 + 2] = clock64();
-        hand_off();
+        hand_off(p + 1, s == 1 || T + 1 < n_tiles);
         if (tr) tr[(p + 1) * 4 + 3] = clock64();
       } else if (p == 5) {
         // ---- layer 6: e6 = w7 (.) 1[z6 > 0] -> A; f = w7 . ReLU(z6) + b7 (fp32) ----
@@ -367,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
           st8(tA + cb / 2, pk);
         }
         if (tr) tr[(p + 1) * 4 + 2] = clock64();
-        hand_off();
+        hand_off(p + 1, s == 1 || T + 1 < n_tiles);
         if (tr) tr[(p + 1) * 4 + 3] = clock64();
         // f = w7 . h6 + b7 (fp32, no output activation: signed value)
         S.fpart[s][hh][row] = (fa[0] + fa[1]) + (fa[2] + fa[3]);
@@ -403,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
           }
         }
         if (tr) tr[(p + 1) * 4 + 2] = clock64();
-        hand_off();
+        hand_off(p + 1, s == 1 || T + 1 < n_tiles);
         if (tr) tr[(p + 1) * 4 + 3] = clock64();
         if (p == 6 && hh == 0 && a.detect) {
           // A6/A7 (overlaps the tensor core): threshold, per-tile slots, per-waypoint min key
@@ -623,23 +692,89 @@ template <bool F16>
 __global__ void __launch_bounds__(128, 1) k_mma_probe(int variant, int reps, float *D) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *sb = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 64 KB B + 32 KB A
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2, bar3;
   __shared__ uint32_t tb;
   const int tid = threadIdx.x, warp = tid >> 5;
-  for (int i = tid; i < (96 * 1024) / 16; i += 128) reinterpret_cast<uint4 *>(sb)[i] = make_uint4(0, 0, 0, 0);
+  // operands: zeros, or (variant 18) random fp16 values in [-1, 1) like real weights
+  auto rnd16 = [](uint32_t x) -> uint32_t {
+    x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
+    return pack2<F16>((float)(x & 0xffff) / 32768.f - 1.f, (float)(x >> 16) / 32768.f - 1.f);
+  };
+  for (int i = tid; i < (96 * 1024) / 16; i += 128)
+    reinterpret_cast<uint4 *>(sb)[i] = variant == 18 ? make_uint4(rnd16(4 * i), rnd16(4 * i + 1), rnd16(4 * i + 2), rnd16(4 * i + 3))
+                                                     : make_uint4(0, 0, 0, 0);
   if (warp == 0) {
     tmem_alloc(&tb, 512);
     tmem_relinquish();
   }
   if (tid == 0) {
     mbar_init(&bar, 1);
+    mbar_init(&bar2, 1);
+    mbar_init(&bar3, 1);
     fence_barrier_init();
   }
   fence_proxy_async_smem();
   fence_before();
   __syncthreads();
   fence_after();
-  if (tid == 0) {
+  if (variant == 18) {  // random A operand in TMEM columns 256..319
+    uint32_t r[32];
+    for (int i = 0; i < 32; ++i) r[i] = rnd16(1000003u * tid + i);
+    st32(tb + ((uint32_t)(warp * 32) << 16) + 256u, r);
+    st32(tb + ((uint32_t)(warp * 32) << 16) + 288u, r);
+    wait_st();
+    fence_before();
+    __syncthreads();
+    fence_after();
+  }
+  __shared__ volatile int stop;
+  if (tid == 0) stop = 0;
+  __syncthreads();
+  if (tid >= 32 && (variant == 16 || variant == 17)) {
+    // TMEM traffic of "epilogue" warps (columns 384..511) while warp 0 streams UMMAs
+    const uint32_t tq = tb + ((uint32_t)(warp * 32) << 16) + 384u;
+    uint32_t r[32];
+    for (int i = 0; i < 32; ++i) r[i] = (uint32_t)i;
+    while (!stop) {
+      if (variant == 16) {
+        ld32(tq, r);
+        wait_ld();
+      } else {
+        st32(tq, r);
+        wait_st();
+      }
+    }
+    if (r[5] == 12345u) D[2] = 1.f;  // keep the loads alive
+  }
+  if (variant == 23 && warp < 2) {
+    // two issuing warps (one per slot), each: forward phases (8 K-major + bias) with a
+    // commit per phase to its own mbarrier; does a second issuer hide the commit bubble?
+    const uint32_t sB = smem_u32(sb), sA = sB + 65536;
+    const uint32_t dd = tb + (uint32_t)warp * 256u;
+    uint64_t bdk[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) bdk[k] = sdesc_sw128(sB + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
+    const uint64_t bx = sdesc_nosw(sA, 2048, 128);
+    uint64_t *mb = warp == 0 ? &bar2 : &bar3;
+    __syncwarp();
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+    const long long t0 = clock64();
+#pragma unroll 1
+    for (int r = 0; r < reps / 2; ++r) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mma_ts_elect(dd, dd + 128 + 8u * k, bdk[k], kIdescFwd<F16>, k > 0);
+      mma_ts_elect(dd, dd + 192, bx, kIdescFwd<F16>, 1u);
+      commit_elect(mb);
+    }
+    mbar_wait(mb, (uint32_t)((reps / 2 - 1) & 1));
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+    const long long t1 = clock64();
+    if (tid == 0 && blockIdx.x == 0) {
+      D[0] = (float)(t1 - t0);
+      D[1] = (float)((reps / 2) * 2 * 9);
+    }
+  }
+  if (tid == 0 && variant != 23) {
     const uint32_t sB = smem_u32(sb), sA = sB + 65536;
     const uint32_t d0 = tb, av = tb + 256;
     long long t0 = clock64();
@@ -648,16 +783,71 @@ __global__ void __launch_bounds__(128, 1) k_mma_probe(int variant, int reps, flo
       uint64_t bd[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        bd[k] = variant == 13 ? sdesc_sw128(sB + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024)
+        bd[k] = variant != 14 ? sdesc_sw128(sB + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024)
                               : sdesc_sw128(sB + k * 2048, 16384, 1024);
-      const uint32_t idesc = variant == 13 ? kIdescFwd<F16> : kIdescBwd<F16>;
+      const uint32_t idesc = variant != 14 ? kIdescFwd<F16> : kIdescBwd<F16>;
+      const uint64_t bx = sdesc_nosw(sA, 2048, 128);
       t0 = clock64();
+      if (variant == 19) {  // the kernel's forward phase: 8 K-major steps + a no-swizzle bias step
 #pragma unroll 1
-      for (int r = 0; r < reps; ++r) {
+        for (int r = 0; r < reps; ++r) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) mma_ts(d0, av + 8u * k, bd[k], idesc, k > 0);
+          for (int k = 0; k < 8; ++k) mma_ts(d0, d0 + 128 + 8u * k, bd[k], idesc, k > 0);
+          mma_ts(d0, d0 + 192, bx, idesc, 1u);
+        }
+        n = reps * 9;
+      } else if (variant == 24) {  // as 22 with a test_wait spin instead of try_wait
+#pragma unroll 1
+        for (int r = 0; r < reps; ++r) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mma_ts(d0, d0 + 128 + 8u * k, bd[k], idesc, k > 0);
+          mma_ts(d0, d0 + 192, bx, idesc, 1u);
+          commit(&bar2);
+          mbar_wait_spin(&bar2, (uint32_t)(r & 1));
+          fence_after();
+        }
+        n = reps * 9;
+      } else if (variant == 25) {  // lean N = 64 (two halves of a phase as separate accumulators)
+        uint64_t b64[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) b64[k] = sdesc_sw128(sB + (k >> 2) * 8192 + (k & 3) * 32, 16, 1024);
+#pragma unroll 1
+        for (int r = 0; r < reps; ++r) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mma_ts(d0 + (uint32_t)(r & 1) * 64u, d0 + 128 + 8u * k, b64[k], idesc_f16kind(128, 64, false, F16), k > 0);
+        }
+        n = reps * 8;
+      } else if (variant == 21 || variant == 22) {
+        // the kernel's forward phase + a commit to an mbarrier after each phase; 22 also
+        // waits for that commit (phase fully serialised: execution + commit latency)
+#pragma unroll 1
+        for (int r = 0; r < reps; ++r) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mma_ts(d0, d0 + 128 + 8u * k, bd[k], idesc, k > 0);
+          mma_ts(d0, d0 + 192, bx, idesc, 1u);
+          commit(&bar2);
+          if (variant == 22) {
+            mbar_wait(&bar2, (uint32_t)(r & 1));
+            fence_after();
+          }
+        }
+        n = reps * 9;
+      } else if (variant == 20) {  // two slots' phases alternating (D at 0 / 256, A at 128 / 384)
+#pragma unroll 1
+        for (int r = 0; r < reps; ++r) {
+          const uint32_t dd = d0 + (uint32_t)(r & 1) * 256u;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mma_ts(dd, dd + 128 + 8u * k, bd[k], idesc, k > 0);
+        }
+        n = reps * 8;
+      } else {
+#pragma unroll 1
+        for (int r = 0; r < reps; ++r) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mma_ts(d0, av + 8u * k, bd[k], idesc, k > 0);
+        }
+        n = reps * 8;
       }
-      n = reps * 8;
     }
     for (int r = 0; r < (variant >= 13 ? 0 : reps); ++r) {
       const uint32_t d = (variant == 2 && (r & 1)) ? tb + 128 : d0;  // (variants 9, 11 use d + 64 / d + 128 too)
@@ -704,8 +894,11 @@ __global__ void __launch_bounds__(128, 1) k_mma_probe(int variant, int reps, flo
     commit(&bar);
     mbar_wait(&bar, 0);
     const long long t1 = clock64();
-    D[0] = (float)(t1 - t0);
-    D[1] = (float)n;
+    stop = 1;
+    if (blockIdx.x == 0) {
+      D[0] = (float)(t1 - t0);
+      D[1] = (float)n;
+    }
   }
   fence_before();
   __syncthreads();
@@ -802,7 +995,7 @@ cudaError_t launch_selftest_umma(int mode, const float *A, const float *B, float
     auto k = f16 ? k_mma_probe<true> : k_mma_probe<false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    k<<<1, 128, smem, s>>>(variant, 200, D);
+    k<<<variant == 15 ? 148 : 1, 128, smem, s>>>(variant, 200, D);
     return cudaGetLastError();
   }
   return (mode & 4) ? selftest_t<true>(mode & 3, A, B, D, s) : selftest_t<false>(mode & 3, A, B, D, s);

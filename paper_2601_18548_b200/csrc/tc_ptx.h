@@ -57,6 +57,39 @@ DEVI void mbar_wait(uint64_t *bar, uint32_t parity) {
     if (clock64() - t0 > (1ll << 34)) __trap();
   }
 }
+// try_wait with an explicit suspend-time hint (ns)
+DEVI bool mbar_try_wait_hint(uint32_t addr, uint32_t parity, uint32_t hint_ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t"
+      ".reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t"
+      "}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(hint_ns)
+      : "memory");
+  return ok != 0;
+}
+template <uint32_t kHintNs>
+DEVI void mbar_wait_hint(uint64_t *bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try_wait_hint(addr, parity, kHintNs)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait_hint(addr, parity, kHintNs)) {
+    if (clock64() - t0 > (1ll << 34)) __trap();
+  }
+}
+// Spin with a short sleep between probes
+template <uint32_t kSleepNs>
+DEVI void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+  if (mbar_test(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_test(bar, parity)) {
+    if (kSleepNs) __nanosleep(kSleepNs);
+    if (clock64() - t0 > (1ll << 34)) __trap();
+  }
+}
 // Spin variant (test_wait, never suspends): lower wake-up latency for a single polling thread.
 DEVI void mbar_wait_spin(uint64_t *bar, uint32_t parity) {
   if (mbar_test(bar, parity)) return;

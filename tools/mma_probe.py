@@ -10,8 +10,8 @@ from paper_2601_18548_b200.gcdf import selftest_umma  # noqa: E402
 names = ["TS K-major N128", "TS MN-major N128", "TS N128 two accumulators", "SS K-major N128", "TS K-major N256",
          "2CTA TS M256 N128", "2CTA SS M256 N128", "2CTA TS M256 N256", "TS N64", "TS N64 two acc interleaved",
          "TS N16", "TS N128 two acc k-interleaved", "TS N128 + nosw bias step", "TS K-major N128 lean issue",
-         "TS MN-major N128 lean issue"]
-NS = [128, 128, 128, 128, 256, 128, 128, 256, 64, 64, 16, 128, 128, 128, 128]
+         "TS MN-major N128 lean issue", "lean, all 148 SMs busy", "lean + 3 warps tcgen05.ld", "lean + 3 warps tcgen05.st", "lean, random operands", "lean kernel fwd phase (8 + bias)", "lean, two slots alternating", "lean fwd phase + commit each", "lean fwd phase + commit + wait", "two issuers, commit each", "lean fwd phase + commit + spin", "lean N64"]
+NS = [128] * 4 + [256, 128, 128, 256, 64, 64, 16] + [128] * 14 + [64]
 A = torch.zeros(128, 128, device="cuda")
 for v, name in enumerate(names):
     for f16 in (1, 0):
