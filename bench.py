@@ -185,20 +185,27 @@ def main():
     ctx.update_scene(pts)
     q = torch.from_numpy(q_np).to(dev)
     outs = ctx.alloc_detect_outputs(n_wp, max_active)
-    upd_rng = np.random.default_rng([cfg.seed, 7])
-    alive = np.zeros(cfg.M + slack, dtype=bool)
-    alive[: cfg.M] = True
+    # Scene-update inputs of every step (A9: 200 removes + 200 adds of a moved box), made
+    # before any clock starts: adds are points of a randomly moved clutter box, removals
+    # disjoint sets of the initially live ids (valid whatever ids the adds reuse).
+    e2e_steps = a.e2e_steps or max(1, min(a.steps, 5))
+    n_upd = a.warmup + a.steps + e2e_steps
+    gen = np.random.default_rng([cfg.seed, 7])
+    adds = [synth.inputs.scene_update_batch(gen, boxes, np.zeros((0, 3)))[0] for _ in range(n_upd)]
+    rems = list(gen.choice(cfg.M, size=(n_upd, 200), replace=False))
+    upd_i = [0]
 
     def scene_step():
-        add, rem = synth.inputs.scene_update_batch_mask(upd_rng, boxes, alive)
-        ids = ctx.update_scene(add, rem)
-        alive[rem] = False
-        alive[ids] = True
-        return add, rem
+        i = upd_i[0]
+        upd_i[0] += 1
+        ctx.update_scene(adds[i], rems[i])
+        return adds[i], rems[i]
 
     def step():
         scene_step()
-        o = ctx.detect_active_set(q, delta, tau, outputs=outs, sync_count=True)
+        # single GPU: no host sync inside the device-timed step (the count is read after the
+        # timed region); the multi-GPU gather needs the per-rank counts on the host
+        o = ctx.detect_active_set(q, delta, tau, outputs=outs, sync_count=world > 1)
         if world > 1:
             o = gather_active_sets(ctx, o, n_wp, group=None)
         return o
@@ -242,7 +249,7 @@ def main():
         t_max = float(t.item())
     pairs_total = n_live_total * n_wp           # every (waypoint, live point) pair of the job
     value = pairs_total / (t_max / 1e3)
-    n_active = int(last["n"])
+    n_active = int(last["n"]) if "n" in last and world > 1 else int(last["count"].item())
 
     # roofline of the dominant kernel (fused MLP): algorithmic flops per launch / live duration
     peaks, peak_src = measured_peaks()
@@ -277,10 +284,18 @@ def main():
             roof["algorithmic_dram_bytes"] = int(16 * cfg.M + 48 * n_active + 8 * local_pairs / 128)
     kshare = mlp_ms / t_ms if t_ms > 0 else None
 
-    # e2e through the public API with host buffers: pinned q H2D + update + detect + D2H of results
-    e2e_steps = a.e2e_steps or max(1, min(a.steps, 5))
+    # e2e through the public API with host buffers: each step = the scene update (host
+    # arrays in) + the host-buffer detect call (q in from pinned host memory, records /
+    # offsets / min / argmin out to pinned host memory; the library does the copies).
     q_pin = torch.from_numpy(q_np).pin_memory()
-    q_dev = torch.empty_like(q_pin, device=dev)
+    if world == 1:
+        host_out = ctx.alloc_host_outputs(n_wp, max_active, pinned=True)
+    else:
+        host_out = {"records": torch.empty((max_active * world, 48), dtype=torch.uint8).pin_memory(),
+                    "wp_offsets": torch.empty(n_wp + 1, dtype=torch.int64).pin_memory(),
+                    "wp_min": torch.empty(n_wp, dtype=torch.float32).pin_memory(),
+                    "wp_argmin": torch.empty(n_wp, dtype=torch.int64).pin_memory()}
+        q_dev = torch.empty(q_pin.shape, dtype=torch.float32, device=dev)
     h2d = d2h = 0
     if world > 1:
         dist.barrier()
@@ -288,16 +303,22 @@ def main():
     t0 = time.perf_counter()
     e2e_pairs = 0
     for i in range(e2e_steps):
-        add, rem = scene_step()
-        q_dev.copy_(q_pin, non_blocking=True)
-        o = ctx.detect_active_set(q_dev, delta, tau, outputs=outs, sync_count=True)
-        if world > 1:
+        add_i, rem_i = scene_step()
+        if world == 1:
+            o = ctx.detect_active_set_host(q_pin, delta, tau, host_out)
+            n = int(o["n"])
+        else:
+            q_dev.copy_(q_pin, non_blocking=True)
+            o = ctx.detect_active_set(q_dev, delta, tau, outputs=outs, sync_count=True)
             o = gather_active_sets(ctx, o, n_wp)
-        n = int(o["n"])
-        rec_h = o["records"][:n].cpu()
-        wmin_h, warg_h, offs_h = o["wp_min"].cpu(), o["wp_argmin"].cpu(), o["wp_offsets"].cpu()
-        h2d += q_pin.numel() * 4 + add.nbytes + rem.nbytes
-        d2h += rec_h.numel() + wmin_h.numel() * 4 + warg_h.numel() * 8 + offs_h.numel() * 8 + 8
+            n = int(o["n"])
+            host_out["records"][:n].copy_(o["records"][:n], non_blocking=True)
+            for k in ("wp_offsets", "wp_min", "wp_argmin"):
+                host_out[k].copy_(o[k], non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+        h2d += q_pin.numel() * 4 + add_i.nbytes + rem_i.nbytes
+        d2h += n * 48 + host_out["wp_offsets"].numel() * 8 + host_out["wp_min"].numel() * 4 + \
+            host_out["wp_argmin"].numel() * 8 + 8
         e2e_pairs += ctx.scene_info()["n_live"] * n_wp
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0

@@ -164,6 +164,20 @@ int gcdf_detect_active_set(gcdf_ctx *ctx, const float *q_dev, int32_t B, int32_t
                            float *wp_min_dev, int64_t *wp_argmin_dev, int64_t *wp_key_dev,
                            int64_t *count_dev, int64_t *count_host_or_null, void *stream);
 
+/* Host-buffer form of gcdf_detect_active_set (the end-to-end call): q_host [B][N][9] is
+   copied to the device, the fused detect runs, and the results come back to host memory:
+   count_host (total active, always written), out_host [out_capacity] (the first
+   min(count, out_capacity) records), wp_offsets_host [B*N+1], wp_min_host [B*N] and
+   wp_argmin_host [B*N] (each may be NULL except wp_offsets_host).  Device staging sized
+   by the context options is allocated on the first call and owned by the context.  Host
+   buffers may be pageable; page-locked ones get the full link bandwidth.  Synchronizes
+   the stream.  CAPACITY when count > out_capacity or > max_active (records not copied in
+   the latter case). */
+int gcdf_detect_active_set_host(gcdf_ctx *ctx, const float *q_host, int32_t B, int32_t N, float delta,
+                                float tau, gcdf_active_t *out_host, int64_t out_capacity,
+                                int64_t *wp_offsets_host, float *wp_min_host, int64_t *wp_argmin_host,
+                                int64_t *count_host, void *stream);
+
 /* A6-A8 standalone over a dense value/gradient array (e.g. from
    gcdf_query_values_grads): same outputs as detect.  values_dev [n_wp][stride],
    grads_dev [n_wp][stride][9], column s = local slot s of this context's scene; stride
@@ -202,7 +216,7 @@ int gcdf_profile_read(gcdf_ctx *ctx, double *mlp_ms, int64_t *mlp_launches, int 
    D_dev fp32 [128][128] output.  mode 0: D = A B^T, B [128][128] (K-major B);
    mode 1: D = A B, B [128][128] (MN-major B); mode 2: D[:, 0:16] = A B^T, B [16][128];
    mode | 4: the same with fp16 operands instead of bf16.
-   mode 16 + 2 v + f16 (v = 0..4, 8..25; 5..7 = CTA-pair probes): UMMA throughput probe,
+   mode 16 + 2 v + f16 (v = 0..4, 8..25; 5..7 = CTA-pair probes; 26, 27 = sub-partition interference): UMMA throughput probe,
    A and B ignored, D[0] = cycles and D[1] = number of UMMAs (tools/mma_probe.py).
    Synchronizes the stream.  UNSUPPORTED without the tcgen05 build. */
 int gcdf_selftest_umma(int cuda_device, int mode, const float *A_dev, const float *B_dev, float *D_dev,

@@ -79,6 +79,9 @@ struct gcdf_ctx {
   double prof_ms = 0.0;
   int64_t prof_n = 0;
   long long *trace = nullptr;  // diagnostics buffer (device), see gcdf_debug_trace
+  // device staging of gcdf_detect_active_set_host (allocated on first use)
+  char *e2e = nullptr;
+  int64_t e2e_q = 0, e2e_out = 0, e2e_offs = 0, e2e_wmin = 0, e2e_warg = 0, e2e_count = 0;
 };
 
 namespace {
@@ -322,6 +325,7 @@ int gcdf_destroy(gcdf_ctx *c) {
   if (c->h_payload) cudaFreeHost(c->h_payload);
   if (c->h_slots) cudaFreeHost(c->h_slots);
   for (auto &e : c->ev) cudaEventDestroy(e);
+  if (c->e2e) cudaFree(c->e2e);
   delete c;
   return GCDF_OK;
 }
@@ -674,6 +678,53 @@ int gcdf_detect_active_set(gcdf_ctx *c, const float *q, int32_t B, int32_t N, fl
   return finish_detect(c, a.n_wp, a.tiles_per_wp, out, cap, offs, wmin, warg, wkey, count_dev, count_host, s);
 }
 
+int gcdf_detect_active_set_host(gcdf_ctx *c, const float *q_host, int32_t B, int32_t N, float delta, float tau,
+                                gcdf_active_t *out_host, int64_t cap, int64_t *offs_host, float *wmin_host,
+                                int64_t *warg_host, int64_t *count_host, void *stream) {
+  int rc = precheck(c);
+  if (rc) return rc;
+  if ((rc = check_wp(c, q_host, B, N))) return rc;
+  if (!out_host || cap < 0 || !offs_host || !count_host)
+    return fail(c, GCDF_ERR_INVALID_ARG, "detect_host: null output");
+  if (!c->e2e) {  // device staging sized by the context options, kept for later calls
+    const int64_t W = c->opt.max_waypoints;
+    int64_t off = 0;
+    c->e2e_q = off; off = align256(off + W * kNdof * 4);
+    c->e2e_out = off; off = align256(off + c->opt.max_active * (int64_t)sizeof(gcdf_active_t));
+    c->e2e_offs = off; off = align256(off + (W + 1) * 8);
+    c->e2e_wmin = off; off = align256(off + W * 4);
+    c->e2e_warg = off; off = align256(off + W * 8);
+    c->e2e_count = off; off = align256(off + 8);
+    CK(c, cudaMalloc(reinterpret_cast<void **>(&c->e2e), off), "detect_host staging");
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t nwp = (int64_t)B * N;
+  float *q = reinterpret_cast<float *>(c->e2e + c->e2e_q);
+  gcdf_active_t *out = reinterpret_cast<gcdf_active_t *>(c->e2e + c->e2e_out);
+  int64_t *offs = reinterpret_cast<int64_t *>(c->e2e + c->e2e_offs);
+  float *wmin = reinterpret_cast<float *>(c->e2e + c->e2e_wmin);
+  int64_t *warg = reinterpret_cast<int64_t *>(c->e2e + c->e2e_warg);
+  int64_t *cnt = reinterpret_cast<int64_t *>(c->e2e + c->e2e_count);
+  CK(c, cudaMemcpyAsync(q, q_host, nwp * kNdof * 4, cudaMemcpyHostToDevice, s), "q H2D");
+  int64_t n = -1;
+  rc = gcdf_detect_active_set(c, q, B, N, delta, tau, out, c->opt.max_active, offs, wmin, warg, nullptr, cnt, &n,
+                              stream);
+  *count_host = n;
+  if (rc && rc != GCDF_ERR_CAPACITY) return rc;
+  const int64_t nc = rc ? 0 : std::min(n, cap);
+  if (nc > 0)
+    CK(c, cudaMemcpyAsync(out_host, out, nc * (int64_t)sizeof(gcdf_active_t), cudaMemcpyDeviceToHost, s),
+       "records D2H");
+  CK(c, cudaMemcpyAsync(offs_host, offs, (nwp + 1) * 8, cudaMemcpyDeviceToHost, s), "offsets D2H");
+  if (wmin_host) CK(c, cudaMemcpyAsync(wmin_host, wmin, nwp * 4, cudaMemcpyDeviceToHost, s), "wp_min D2H");
+  if (warg_host) CK(c, cudaMemcpyAsync(warg_host, warg, nwp * 8, cudaMemcpyDeviceToHost, s), "wp_argmin D2H");
+  CK(c, cudaStreamSynchronize(s), "detect_host sync");
+  if (rc) return rc;
+  if (n > cap)
+    return fail(c, GCDF_ERR_CAPACITY, "active count %lld exceeds host capacity %lld", (long long)n, (long long)cap);
+  return GCDF_OK;
+}
+
 int gcdf_compact_dense(gcdf_ctx *c, const float *values, const float *grads, int32_t n_wp, int64_t stride,
                        float delta, float tau, gcdf_active_t *out, int64_t cap, int64_t *offs, float *wmin,
                        int64_t *warg, int64_t *wkey, int64_t *count_dev, int64_t *count_host, void *stream) {
@@ -715,7 +766,7 @@ int gcdf_debug_trace(gcdf_ctx *c, long long *trace_dev) {
 
 int gcdf_selftest_umma(int dev, int mode, const float *A, const float *B, float *D, void *stream) {
   if (!tc_compiled()) return GCDF_ERR_UNSUPPORTED;
-  if (mode < 0 || (mode < 16 && (mode > 6 || (mode & 3) > 2)) || mode > 67 || !A || !B || !D) return GCDF_ERR_INVALID_ARG;
+  if (mode < 0 || (mode < 16 && (mode > 6 || (mode & 3) > 2)) || mode > 71 || !A || !B || !D) return GCDF_ERR_INVALID_ARG;
   if (cudaSetDevice(dev) != cudaSuccess) return GCDF_ERR_CUDA;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (launch_selftest_umma(mode, A, B, D, s) != cudaSuccess) return GCDF_ERR_CUDA;

@@ -12,6 +12,7 @@ namespace gcdf {
 namespace tc {
 
 DEVI uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+DEVI uint32_t lane_id() { return threadIdx.x & 31u; }
 
 // ------------------------------------------------------------------ mbarrier
 DEVI void mbar_init(uint64_t *bar, uint32_t count) {

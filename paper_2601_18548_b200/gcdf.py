@@ -26,7 +26,7 @@ REC_BYTES = 48  # sizeof(gcdf_active_t)
 EXPORTED = ["gcdf_default_options", "gcdf_create", "gcdf_destroy", "gcdf_last_error", "gcdf_has_tcgen05",
             "gcdf_workspace_bytes", "gcdf_bind_workspace", "gcdf_load_weights", "gcdf_update_scene",
             "gcdf_scene_info", "gcdf_pairgen_transform", "gcdf_query_values_grads", "gcdf_detect_active_set",
-            "gcdf_compact_dense", "gcdf_merge_active_sets", "gcdf_launch_count", "gcdf_profile_enable",
+            "gcdf_detect_active_set_host", "gcdf_compact_dense", "gcdf_merge_active_sets", "gcdf_launch_count", "gcdf_profile_enable",
             "gcdf_profile_read", "gcdf_selftest_umma", "gcdf_debug_trace"]
 
 
@@ -71,6 +71,7 @@ def load_library(path: str | Path = LIB_PATH):
     lib.gcdf_pairgen_transform.argtypes = [P, P, I32, I32, P, P]
     lib.gcdf_query_values_grads.argtypes = [P, P, I32, I32, P, P, P]
     lib.gcdf_detect_active_set.argtypes = [P, P, I32, I32, F, F, P, I64, P, P, P, P, P, P, P]
+    lib.gcdf_detect_active_set_host.argtypes = [P, P, I32, I32, F, F, P, I64, P, P, P, P, P]
     lib.gcdf_compact_dense.argtypes = [P, P, P, I32, I64, F, F, P, I64, P, P, P, P, P, P, P]
     lib.gcdf_merge_active_sets.argtypes = [P, I32, I32, P, I64, P, P, P, I64, P, P, P, P, P]
     lib.gcdf_launch_count.argtypes = [P]
@@ -235,6 +236,31 @@ class Context:
             C.byref(nh) if sync_count else None, _stream(self.device)))
         if sync_count:
             o["n"] = nh.value
+        return o
+
+    @staticmethod
+    def alloc_host_outputs(n_wp: int, capacity: int, pinned: bool = True):
+        """Host (page-locked by default) buffers for detect_active_set_host."""
+        def e(shape, dt):
+            t = torch.empty(shape, dtype=dt)
+            return t.pin_memory() if pinned else t
+        return {"records": e((max(capacity, 1), REC_BYTES), torch.uint8), "wp_offsets": e(n_wp + 1, torch.int64),
+                "wp_min": e(n_wp, torch.float32), "wp_argmin": e(n_wp, torch.int64), "capacity": capacity}
+
+    def detect_active_set_host(self, q_host: torch.Tensor, delta: float, tau: float, outputs: dict):
+        """End-to-end fused detect through the host-buffer C-ABI call (q and results in host
+        memory; the library does the copies).  Returns outputs with 'n' = active count."""
+        if q_host.device.type != "cpu" or q_host.dim() != 3 or q_host.shape[2] != 9:
+            raise ValueError("q_host must be a CPU tensor [B, N, 9]")
+        q_host = q_host.to(torch.float32).contiguous()
+        o = outputs
+        nh = C.c_int64(-1)
+        self._check(self.lib.gcdf_detect_active_set_host(
+            self._h, C.c_void_p(q_host.data_ptr()), int(q_host.shape[0]), int(q_host.shape[1]), float(delta),
+            float(tau), C.c_void_p(o["records"].data_ptr()), int(o["capacity"]), C.c_void_p(o["wp_offsets"].data_ptr()),
+            C.c_void_p(o["wp_min"].data_ptr()), C.c_void_p(o["wp_argmin"].data_ptr()), C.byref(nh),
+            _stream(self.device)))
+        o["n"] = nh.value
         return o
 
     def compact_dense(self, values: torch.Tensor, grads: torch.Tensor, delta: float, tau: float,

@@ -253,3 +253,29 @@ def test_virtual_ranks_merge_bitexact(c2):
             assert np.array_equal(a[k], b[k]), (world, k)
         assert torch.equal(mg["wp_offsets"], r1["wp_offsets"])
         assert torch.equal(mg["wp_min"], r1["wp_min"]) and torch.equal(mg["wp_argmin"], r1["wp_argmin"])
+
+
+@pytest.mark.parametrize("prec", [0, 2])
+def test_detect_host_buffers_match_device_call(c2, prec):
+    """The end-to-end host-buffer call (q and results in host memory, copies inside the
+    library) returns exactly what the device call returns, on fp32 and fp16 contexts;
+    a too-small host capacity reports CAPACITY with the exact count."""
+    from paper_2601_18548_b200 import GcdfError
+    cfg, pts, q, m, full = c2
+    tau = synth.load_tau(cfg.name)
+    ctx = _ctx(cfg, precision=prec)
+    ctx.update_scene(pts)
+    qt = torch.from_numpy(q)
+    dev = ctx.detect_active_set(qt, DELTA, tau)
+    n = int(dev["n"])
+    assert n > 0
+    for pinned in (True, False):
+        ho = ctx.alloc_host_outputs(q.shape[0] * q.shape[1], n + 5, pinned=pinned)
+        h = ctx.detect_active_set_host(qt, DELTA, tau, ho)
+        assert h["n"] == n
+        assert torch.equal(h["records"][:n], dev["records"][:n].cpu())
+        for k in ("wp_offsets", "wp_min", "wp_argmin"):
+            assert torch.equal(h[k], dev[k].cpu()), k
+    small = ctx.alloc_host_outputs(q.shape[0] * q.shape[1], max(n // 2, 1), pinned=True)
+    with pytest.raises(GcdfError):
+        ctx.detect_active_set_host(qt, DELTA, tau, small)

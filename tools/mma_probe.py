@@ -21,3 +21,9 @@ for v, name in enumerate(names):
         ideal = 128 * N / 256  # cycles per (M=128 per SM) x N x 16 MMA at 8192 dense flops/clk/SM
         print(f"{name:28s} {'fp16' if f16 else 'bf16'}: {cyc / n:7.1f} cycles/MMA (ideal {ideal:.0f}) "
               f"-> {100 * ideal / (cyc / n):5.1f}% of dense peak")
+
+# sub-partition interference: warp 0 streams UMMAs (or idles); warps 4 (same SMSP) and 5 run ALU loops
+for v, name in ((26, "with UMMA stream"), (27, "without")):
+    D = selftest_umma(16 + 2 * v + 1, A, A)
+    print(f"ALU loop {name:18s}: warp 4 (same SMSP as issuer) {D[0, 0].item():9.0f} cyc, warp 5 {D[0, 1].item():9.0f} cyc,"
+          f" UMMA stream {D[0, 2].item():9.0f} cyc")
