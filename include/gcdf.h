@@ -168,9 +168,9 @@ int gcdf_detect_active_set(gcdf_ctx *ctx, const float *q_dev, int32_t B, int32_t
    copied to the device, the fused detect runs, and the results come back to host memory:
    count_host (total active, always written), out_host [out_capacity] (the first
    min(count, out_capacity) records), wp_offsets_host [B*N+1], wp_min_host [B*N] and
-   wp_argmin_host [B*N] (each may be NULL except wp_offsets_host).  Device staging sized
-   by the context options is allocated on the first call and owned by the context.  Host
-   buffers may be pageable; page-locked ones get the full link bandwidth.  Synchronizes
+   wp_argmin_host [B*N] (each may be NULL except wp_offsets_host).  The device side lives
+   in the bound workspace (sized by max_waypoints and max_active).  Host buffers may be
+   pageable; page-locked ones get the full link bandwidth.  Synchronizes
    the stream.  CAPACITY when count > out_capacity or > max_active (records not copied in
    the latter case). */
 int gcdf_detect_active_set_host(gcdf_ctx *ctx, const float *q_host, int32_t B, int32_t N, float delta,

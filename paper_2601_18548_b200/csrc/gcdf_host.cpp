@@ -31,7 +31,8 @@ constexpr int kEvPool = 64;
 inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
 struct Layout {
-  int64_t pts, wf32, wbf16, wf16, meta, staging, wp_key, wp_count, counter, upd_payload, upd_slots, total;
+  int64_t pts, wf32, wbf16, wf16, meta, staging, wp_key, wp_count, counter, upd_payload, upd_slots;
+  int64_t h_q, h_out, h_offs, h_wmin, h_warg, h_count, total;
   int64_t wf32_bytes, wbf16_bytes;
 };
 
@@ -79,9 +80,6 @@ struct gcdf_ctx {
   double prof_ms = 0.0;
   int64_t prof_n = 0;
   long long *trace = nullptr;  // diagnostics buffer (device), see gcdf_debug_trace
-  // device staging of gcdf_detect_active_set_host (allocated on first use)
-  char *e2e = nullptr;
-  int64_t e2e_q = 0, e2e_out = 0, e2e_offs = 0, e2e_wmin = 0, e2e_warg = 0, e2e_count = 0;
 };
 
 namespace {
@@ -306,6 +304,13 @@ int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out) {
   L.counter = off; off = align256(off + 16);
   L.upd_payload = off; off = align256(off + kUpdChunk * 16);
   L.upd_slots = off; off = align256(off + kUpdChunk * 8);
+  // device side of gcdf_detect_active_set_host
+  L.h_q = off; off = align256(off + (int64_t)o.max_waypoints * kNdof * 4);
+  L.h_out = off; off = align256(off + o.max_active * (int64_t)sizeof(gcdf_active_t));
+  L.h_offs = off; off = align256(off + ((int64_t)o.max_waypoints + 1) * 8);
+  L.h_wmin = off; off = align256(off + (int64_t)o.max_waypoints * 4);
+  L.h_warg = off; off = align256(off + (int64_t)o.max_waypoints * 8);
+  L.h_count = off; off = align256(off + 8);
   L.total = off;
   cudaSetDevice(cuda_device);
   if (cudaHostAlloc(&c->h_payload, kUpdChunk * 16, cudaHostAllocDefault) != cudaSuccess ||
@@ -325,7 +330,6 @@ int gcdf_destroy(gcdf_ctx *c) {
   if (c->h_payload) cudaFreeHost(c->h_payload);
   if (c->h_slots) cudaFreeHost(c->h_slots);
   for (auto &e : c->ev) cudaEventDestroy(e);
-  if (c->e2e) cudaFree(c->e2e);
   delete c;
   return GCDF_OK;
 }
@@ -686,25 +690,14 @@ int gcdf_detect_active_set_host(gcdf_ctx *c, const float *q_host, int32_t B, int
   if ((rc = check_wp(c, q_host, B, N))) return rc;
   if (!out_host || cap < 0 || !offs_host || !count_host)
     return fail(c, GCDF_ERR_INVALID_ARG, "detect_host: null output");
-  if (!c->e2e) {  // device staging sized by the context options, kept for later calls
-    const int64_t W = c->opt.max_waypoints;
-    int64_t off = 0;
-    c->e2e_q = off; off = align256(off + W * kNdof * 4);
-    c->e2e_out = off; off = align256(off + c->opt.max_active * (int64_t)sizeof(gcdf_active_t));
-    c->e2e_offs = off; off = align256(off + (W + 1) * 8);
-    c->e2e_wmin = off; off = align256(off + W * 4);
-    c->e2e_warg = off; off = align256(off + W * 8);
-    c->e2e_count = off; off = align256(off + 8);
-    CK(c, cudaMalloc(reinterpret_cast<void **>(&c->e2e), off), "detect_host staging");
-  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t nwp = (int64_t)B * N;
-  float *q = reinterpret_cast<float *>(c->e2e + c->e2e_q);
-  gcdf_active_t *out = reinterpret_cast<gcdf_active_t *>(c->e2e + c->e2e_out);
-  int64_t *offs = reinterpret_cast<int64_t *>(c->e2e + c->e2e_offs);
-  float *wmin = reinterpret_cast<float *>(c->e2e + c->e2e_wmin);
-  int64_t *warg = reinterpret_cast<int64_t *>(c->e2e + c->e2e_warg);
-  int64_t *cnt = reinterpret_cast<int64_t *>(c->e2e + c->e2e_count);
+  float *q = reinterpret_cast<float *>(c->ws + c->L.h_q);
+  gcdf_active_t *out = reinterpret_cast<gcdf_active_t *>(c->ws + c->L.h_out);
+  int64_t *offs = reinterpret_cast<int64_t *>(c->ws + c->L.h_offs);
+  float *wmin = reinterpret_cast<float *>(c->ws + c->L.h_wmin);
+  int64_t *warg = reinterpret_cast<int64_t *>(c->ws + c->L.h_warg);
+  int64_t *cnt = reinterpret_cast<int64_t *>(c->ws + c->L.h_count);
   CK(c, cudaMemcpyAsync(q, q_host, nwp * kNdof * 4, cudaMemcpyHostToDevice, s), "q H2D");
   int64_t n = -1;
   rc = gcdf_detect_active_set(c, q, B, N, delta, tau, out, c->opt.max_active, offs, wmin, warg, nullptr, cnt, &n,
