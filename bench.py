@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--latency-calls", type=int, default=50,
+                    help="detect-latency sample size (wall time q on device -> count on host); 0 = skip")
     return ap.parse_args()
 
 
@@ -99,7 +101,7 @@ def measured_peaks():
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def cpu_oracle_rate(cfg, pts, q, sample_pts=8192, nthreads=None, seed=12345):
+def cpu_oracle_rate(cfg, pts, q, sample_pts=8192, nthreads=None, seed=12345, single_thread=False):
     """The oracle as it stands on the host cores: detect over a bounded sample of the
     workload -- one waypoint row per core (the oracle threads over waypoint rows) x
     sample_pts points."""
@@ -116,9 +118,16 @@ def cpu_oracle_rate(cfg, pts, q, sample_pts=8192, nthreads=None, seed=12345):
              nthreads=used)
     dt = time.perf_counter() - t0
     n = len(wsel) * len(psel)
-    return {"value": n / dt, "unit": "queries/s", "cores": int(used), "kind": "oracle", "pairs": n, "seconds": dt,
-            "sample": f"{len(wsel)} waypoints x {len(psel)} points of {cfg.name} ({n} pairs, "
-                      f"float64 detect incl. gradients, one waypoint row per thread), {dt:.1f} s"}
+    r = {"value": n / dt, "unit": "queries/s", "cores": int(used), "kind": "oracle", "pairs": n, "seconds": dt,
+         "sample": f"{len(wsel)} waypoints x {len(psel)} points of {cfg.name} ({n} pairs, "
+                   f"float64 detect incl. gradients, one waypoint row per thread), {dt:.1f} s"}
+    if single_thread:
+        p1 = psel[: max(1, len(psel) // 8)]
+        t0 = time.perf_counter()
+        m.detect(pts[p1], p1.astype(np.int64), qs[wsel[:1]], synth.inputs.DELTA, synth.load_tau(cfg.name), nthreads=1)
+        d1 = time.perf_counter() - t0
+        r["single_thread"] = {"value": len(p1) / d1, "pairs": len(p1), "seconds": d1}
+    return r
 
 
 def run_reference(a):
@@ -327,9 +336,35 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
+    # active-set detect latency per SCO iteration = wall time of one detect
+    # call from q resident on the device to the count on the host (collectives included),
+    # p50 / p99 over `latency_calls` calls after 5 warm-ups
+    lat = None
+    if a.latency_calls > 0:
+        for _ in range(5):
+            o = ctx.detect_active_set(q, delta, tau, outputs=outs, sync_count=True)
+            if world > 1:
+                gather_active_sets(ctx, o, n_wp)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(a.latency_calls):
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            o = ctx.detect_active_set(q, delta, tau, outputs=outs, sync_count=True)
+            if world > 1:
+                gather_active_sets(ctx, o, n_wp)
+            ts.append(time.perf_counter() - t0)
+        tt = torch.tensor(ts, device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = np.sort(tt.cpu().numpy()) * 1e3
+        lat = {"p50_ms": float(np.percentile(ms, 50)), "p99_ms": float(np.percentile(ms, 99)),
+               "calls": a.latency_calls, "what": "wall time, q on device -> active count on host"}
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cpu = cpu_oracle_rate(cfg, pts, q_np, sample_pts=8192)
+        cpu = cpu_oracle_rate(cfg, pts, q_np, sample_pts=65536, single_thread=True)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": a.steps,
@@ -341,7 +376,7 @@ def main():
                        "parallelism": f"points sharded over {world} GPU(s)",
                        "l2": "256 MiB buffer written between timed steps (L2 flush)"},
             "roofline": roof, "mlp_kernel_share_of_step": kshare,
-            "detect_latency_ms": t_max / a.steps,
+            "detect_latency": lat,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_pairs / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": h2d // e2e_steps,
                     "d2h_bytes_per_step": d2h // e2e_steps, "steps": e2e_steps},

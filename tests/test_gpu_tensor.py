@@ -242,3 +242,45 @@ def test_c4_batched_replanning_with_updates():
     wrow = {int(w): k for k, w in enumerate(wsel)}
     fo = np.array([full[wrow[int(w)], pos[int(p)]] for w, p in zip(gpu["wp"][sel], gpu["pt"][sel])])
     assert len(fo) > 0 and np.all(np.abs(gpu["value"][sel] - fo) <= BF16_VAL_ATOL)
+
+
+def test_c3_dense_scene_full_rows():
+    """C3 (100 waypoints x 100k points of the dense 120-box scene, fp16): for 4 sampled
+    waypoints, the whole row against the oracle (values of every pair, exact active-set
+    membership outside the tolerance band, per-waypoint min / argmin), plus the record
+    order and offsets invariants of the full result."""
+    cfg = synth.get_config("C3")
+    pts, _ = synth.make_scene_points(cfg)
+    q = synth.make_waypoints(cfg)
+    tau = synth.load_tau(cfg.name)
+    ctx = _ctx(cfg, "fp16")
+    ids = ctx.update_scene(pts)
+    out = ctx.detect_active_set(torch.from_numpy(q), DELTA, tau)
+    torch.cuda.synchronize()
+    gpu = records_np(out)
+    n = int(out["n"])
+    key = gpu["wp"].astype(np.int64) * (1 << 32) + gpu["pt"].astype(np.int64)
+    assert np.all(np.diff(key) > 0), "records not in strict (wp, pt) order"
+    offs = out["wp_offsets"].cpu().numpy()
+    assert offs[0] == 0 and offs[-1] == n and np.all(np.diff(offs) >= 0)
+    assert np.array_equal(np.repeat(np.arange(len(offs) - 1), np.diff(offs)), gpu["wp"])
+    Q = q.reshape(-1, 9)
+    rng = np.random.default_rng(303)
+    wsel = np.sort(rng.choice(Q.shape[0], 4, replace=False))
+    m = oracle_mlp(cfg)
+    full = m.eval(pts, Q[wsel], want_grad=False, nthreads=NT)["f"]
+    v, _ = ctx.query_values_grads(torch.from_numpy(Q[wsel].reshape(1, -1, 9)), want_grads=False)
+    v = v.cpu().numpy()[:, ids]
+    assert np.abs(v - full).max() <= BF16_VAL_ATOL
+    thr = tau + DELTA
+    wmin = out["wp_min"].cpu().numpy()[wsel]
+    warg = out["wp_argmin"].cpu().numpy()[wsel]
+    assert np.all(np.abs(wmin - full.min(axis=1)) <= BF16_VAL_ATOL)
+    for k, w in enumerate(wsel):
+        rec = set(gpu["pt"][offs[w]:offs[w + 1]].tolist())
+        orc = set(ids[full[k] <= thr].tolist())
+        band = set(ids[np.abs(full[k] - thr) <= 1e-3 + BF16_VAL_ATOL].tolist())
+        assert (rec ^ orc) <= band, (w, len(rec ^ orc), len(band))
+        assert int(warg[k]) in set(ids[full[k] <= full[k].min() + 2 * BF16_VAL_ATOL].tolist())
+    frac = n / (len(pts) * Q.shape[0])
+    print(f"\nC3: {n} active ({frac:.4%})")
