@@ -62,6 +62,8 @@ def _L():
         lib.or_eval.argtypes = [P, P, I64, P, I64, I, P, P, P, P, I]
         lib.or_detect.argtypes = [P, P, P, I64, P, I64, I, D, D, P, P, P, P, I64, C.POINTER(I64),
                                   P, P, P, I]
+        lib.or_detect_part.argtypes = [P, P, P, I64, P, I64, I, D, D, D, P, P, P, P, I64, C.POINTER(I64),
+                                       P, P, P, P, I]
         lib.or_scene_new.argtypes = [I64, C.POINTER(P)]
         lib.or_scene_free.argtypes = [P]
         lib.or_scene_free.restype = None
@@ -119,8 +121,9 @@ class MLP:
             out["mask_hash"] = hsh
         return out
 
-    def detect(self, pts, ids, q, delta, tau, flags: int = 0, cap=None, nthreads: int = 1):
-        """O6-O7 over the live scene (ids ascending) and W = B*N waypoint rows."""
+    def detect(self, pts, ids, q, delta, tau, flags: int = 0, cap=None, nthreads: int = 1, radius: float = 0.0):
+        """O6-O7 over the live scene (ids ascending) and W = B*N waypoint rows; radius > 0
+        restricts step i to its range partition I_{M,i} (NEXT-1, gcdf_oracle.c)."""
         pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1, 3)
         ids = np.ascontiguousarray(ids, dtype=np.int64)
         q = np.ascontiguousarray(q, dtype=np.float64).reshape(-1, 9)
@@ -136,15 +139,16 @@ class MLP:
         off = np.empty(W + 1, dtype=np.int64)
         wmin = np.empty(W)
         warg = np.empty(W, dtype=np.int64)
-        rc = _L().or_detect(self._h, _p(pts), _p(ids), M, _p(q), W, flags, float(delta), float(tau),
-                            _p(rf), _p(rg), _p(rwp), _p(rpt), cap, C.byref(cnt), _p(off), _p(wmin),
-                            _p(warg), int(nthreads))
+        psz = np.empty(W, dtype=np.int64)
+        rc = _L().or_detect_part(self._h, _p(pts), _p(ids), M, _p(q), W, flags, float(radius), float(delta),
+                                 float(tau), _p(rf), _p(rg), _p(rwp), _p(rpt), cap, C.byref(cnt), _p(off),
+                                 _p(wmin), _p(warg), _p(psz), int(nthreads))
         if rc:
             raise OracleError(rc, "detect")
         n = cnt.value
         s = min(n, cap)
         return {"count": n, "value": rf[:s], "grad": rg[:s], "wp": rwp[:s], "pt": rpt[:s],
-                "wp_offsets": off, "wp_min": wmin, "wp_argmin": warg}
+                "wp_offsets": off, "wp_min": wmin, "wp_argmin": warg, "part_sizes": psz}
 
 
 class Scene:

@@ -322,11 +322,18 @@ int or_eval(const omlp_t *m, const double *pts, int64_t M, const double *q, int6
    q[W][9] with W = B*N rows, row index = wp = b*N + i.
    Records (value, grad[9], wp, pt) in (wp, pt) ascending order; at most cap are
    stored, *count receives the full count.  wp_offsets[W+1], wp_min[W], wp_argmin[W]. */
-int or_detect(const omlp_t *m, const double *pts, const int64_t *ids, int64_t M, const double *q,
-              int64_t W, int flags, double delta, double tau, double *rec_f, double *rec_g,
-              int64_t *rec_wp, int64_t *rec_pt, int64_t cap, int64_t *count, int64_t *wp_offsets,
-              double *wp_min, int64_t *wp_argmin, int nthreads) {
+/* NEXT-1 range partition: "only considering obstacle points
+   within a certain range of each reference base position" -- the partition of step i is
+   I_{M,i} = { j : (p_{j,x} - x_i)^2 + (p_{j,y} - y_i)^2 <= radius^2 } (planar distance to
+   the base position (x_i, y_i) = q_i[0:2], inclusive; reading R23).  radius <= 0
+   (or +INF) = no partition: every live point of every step.  part_sizes[W] (may be NULL)
+   receives m_i = |I_{M,i}|.  The value minimum and the records cover I_{M,i} only. */
+int or_detect_part(const omlp_t *m, const double *pts, const int64_t *ids, int64_t M, const double *q,
+                   int64_t W, int flags, double radius, double delta, double tau, double *rec_f, double *rec_g,
+                   int64_t *rec_wp, int64_t *rec_pt, int64_t cap, int64_t *count, int64_t *wp_offsets,
+                   double *wp_min, int64_t *wp_argmin, int64_t *part_sizes, int nthreads) {
   if (!m || M < 0 || W < 0) return OR_ERR_INVALID;
+  const int partitioned = radius > 0.0 && isfinite(radius);
   for (int64_t j = 1; j < M; ++j)
     if (ids[j] <= ids[j - 1]) return OR_ERR_INVALID;
   int64_t rows_per_chunk = M > 0 ? (4 * 1024 * 1024) / M : W;
@@ -342,10 +349,16 @@ int or_detect(const omlp_t *m, const double *pts, const int64_t *ids, int64_t M,
     if (rc) { free(f); free(g); return rc; }
     for (int64_t r = 0; r < nr; ++r) {
       int64_t w = w0 + r;
+      const double bx = q[w * OR_NDOF + 0], by = q[w * OR_NDOF + 1];
       wp_offsets[w] = n;
       double best = INFINITY;
-      int64_t arg = -1;
+      int64_t arg = -1, msize = 0;
       for (int64_t j = 0; j < M; ++j) {
+        if (partitioned) {
+          const double dx = pts[3 * j] - bx, dy = pts[3 * j + 1] - by;
+          if (dx * dx + dy * dy > radius * radius) continue;  /* j not in I_{M,i} */
+        }
+        ++msize;
         double v = f[r * M + j];
         if (v < best) { best = v; arg = ids[j]; } /* strict: first (smallest id) wins ties */
         if (v - delta <= tau) {                   /* O6 */
@@ -360,6 +373,7 @@ int or_detect(const omlp_t *m, const double *pts, const int64_t *ids, int64_t M,
       }
       wp_min[w] = best;
       wp_argmin[w] = arg;
+      if (part_sizes) part_sizes[w] = msize;
     }
   }
   wp_offsets[W] = n;
@@ -367,6 +381,14 @@ int or_detect(const omlp_t *m, const double *pts, const int64_t *ids, int64_t M,
   free(f);
   free(g);
   return OR_OK;
+}
+
+int or_detect(const omlp_t *m, const double *pts, const int64_t *ids, int64_t M, const double *q,
+              int64_t W, int flags, double delta, double tau, double *rec_f, double *rec_g,
+              int64_t *rec_wp, int64_t *rec_pt, int64_t cap, int64_t *count, int64_t *wp_offsets,
+              double *wp_min, int64_t *wp_argmin, int nthreads) {
+  return or_detect_part(m, pts, ids, M, q, W, flags, 0.0, delta, tau, rec_f, rec_g, rec_wp, rec_pt, cap, count,
+                        wp_offsets, wp_min, wp_argmin, NULL, nthreads);
 }
 
 /* ---------------------------------------------------------------- scene (O2) */

@@ -390,3 +390,49 @@ def test_emu_fp16_subnormal_and_range(tmp_path):
     m = oracle.MLP(_write(tmp_path, "sub.mlpw", 1, [12] + [1] * 6 + [1], layers))
     out = m.eval(np.array([[2.0, 0.0, 0.0]]), np.array([[1.0, 0, 0, 0, 0, 0, 0, 0, 0]]), flags=oracle.EMU_FP16)
     assert out["g"][0, 0, 0] == -(2.0 ** -20) and out["g"][0, 0, 2] == 0.5 * 2.0 ** -20
+
+
+def test_range_partition_bruteforce_C1():
+    """NEXT-1 pin: the partitioned detect equals brute force over
+    the pairs whose point lies within `radius` (planar distance, inclusive) of the step's
+    base position; partition sizes are brute-force counts; radius <= 0 / +inf reproduce
+    the unpartitioned detect exactly; a point placed exactly on the circle is included."""
+    cfg = synth.get_config("C1")
+    pts, _ = synth.make_scene_points(cfg)
+    q = synth.make_waypoints(cfg).reshape(-1, 9)
+    m = oracle.MLP(synth.weights_path(cfg.H))
+    ids = np.arange(pts.shape[0], dtype=np.int64) * 2 + 5
+    tau = synth.load_tau("C1")
+    full = m.detect(pts, ids, q, DELTA, tau)
+    for r in (0.0, np.inf):
+        d = m.detect(pts, ids, q, DELTA, tau, radius=r)
+        for k in ("value", "grad", "wp", "pt", "wp_offsets", "wp_min", "wp_argmin"):
+            np.testing.assert_array_equal(d[k], full[k])
+    # boundary point: exactly radius 2.5 from waypoint 3's base (a 3-4-5 triangle, exact in f64)
+    r = 2.5
+    qb = q.copy()
+    qb[3, 0:2] = [1.0, -2.0]
+    pts_b = np.concatenate([pts, [[1.0 + 1.5, -2.0 + 2.0, 0.7]]])
+    ids_b = np.concatenate([ids, [ids[-1] + 7]])
+    d = m.detect(pts_b, ids_b, qb, DELTA, 1e9, radius=r)   # tau huge: every partition pair is active
+    F = m.eval(pts_b, qb, want_grad=False)["f"]
+    inside = ((pts_b[None, :, 0] - qb[:, None, 0]) ** 2 + (pts_b[None, :, 1] - qb[:, None, 1]) ** 2) <= r * r
+    assert inside[3, -1]
+    np.testing.assert_array_equal(d["part_sizes"], inside.sum(axis=1))
+    pairs = [(w, int(ids_b[j])) for w in range(qb.shape[0]) for j in range(len(ids_b)) if inside[w, j]]
+    assert d["count"] == len(pairs) and [(int(a), int(b)) for a, b in zip(d["wp"], d["pt"])] == pairs
+    for w in range(qb.shape[0]):
+        js = np.flatnonzero(inside[w])
+        if js.size == 0:
+            assert np.isinf(d["wp_min"][w]) and d["wp_argmin"][w] == -1
+        else:
+            j = js[np.argmin(F[w, js])]
+            assert d["wp_min"][w] == F[w, j] and d["wp_argmin"][w] == ids_b[j]
+    # the real threshold: records = brute force on the partition pairs
+    d = m.detect(pts, ids, q, DELTA, tau, radius=1.8)
+    F = m.eval(pts, q, want_grad=False)["f"]
+    inside = ((pts[None, :, 0] - q[:, None, 0]) ** 2 + (pts[None, :, 1] - q[:, None, 1]) ** 2) <= 1.8 ** 2
+    pairs = [(w, int(ids[j])) for w in range(q.shape[0]) for j in range(len(ids))
+             if inside[w, j] and F[w, j] - DELTA <= tau]
+    assert d["count"] == len(pairs) and [(int(a), int(b)) for a, b in zip(d["wp"], d["pt"])] == pairs
+    assert 0 < d["part_sizes"].sum() < inside.size
