@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--partition-radius", type=float, default=1.8,
+                    help="also time the range-partitioned detect (NEXT-1) at this radius; 0 = skip")
     ap.add_argument("--latency-calls", type=int, default=50,
                     help="detect-latency sample size (wall time q on device -> count on host); 0 = skip")
     return ap.parse_args()
@@ -189,7 +191,8 @@ def main():
     slack = 4096
     max_active = int(min(cfg.pairs // world + 1024, max(4 * cfg.pairs // 100 // world, 1 << 16)))
     ctx = Context(local, precision={"fp16": FP16, "bf16": BF16, "fp32": FP32}[prec], scene_capacity=cfg.M + slack,
-                  max_waypoints=n_wp, max_active=max_active, rank=rank, world=world)
+                  max_waypoints=n_wp, max_active=max_active, rank=rank, world=world,
+                  max_candidates=(cfg.pairs // world + 4096) if a.partition_radius > 0 else 0)
     ctx.load_weights(synth.weights_path(cfg.H))
     ctx.update_scene(pts)
     q = torch.from_numpy(q_np).to(dev)
@@ -336,6 +339,35 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
+    # NEXT-1: the range-partitioned detect on the same workload (device time per call)
+    part = None
+    if a.partition_radius > 0 and world == 1:
+        for _ in range(3):
+            ctx.detect_active_set_partitioned(q, a.partition_radius, delta, tau, outputs=outs, sync_count=False)
+        torch.cuda.synchronize()
+        k = max(3, a.steps)
+        pe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+        ctx.profile_read(reset=True)
+        ctx.profile_enable(True)
+        for i in range(k):
+            flush.zero_()
+            pe[i][0].record()
+            po = ctx.detect_active_set_partitioned(q, a.partition_radius, delta, tau, outputs=outs, sync_count=False)
+            pe[i][1].record()
+        torch.cuda.synchronize()
+        p_mlp_ms, p_mlp_n = ctx.profile_read(reset=True)
+        ctx.profile_enable(False)
+        p_ms = sum(s_.elapsed_time(e_) for s_, e_ in pe) / k
+        p_pairs = int(po["part_sizes"].sum().item())
+        n_live = ctx.scene_info()["n_live"]
+        part = {"radius_m": a.partition_radius, "ms_per_step": p_ms, "pairs_per_step": p_pairs,
+                "pairs_fraction": p_pairs / (n_live * n_wp), "active_per_step": int(po["count"].item()),
+                "evaluated_pairs_per_s": p_pairs / (p_ms / 1e3),
+                "covered_pairs_per_s": n_live * n_wp / (p_ms / 1e3),
+                "mlp_kernel_ms": p_mlp_ms / max(p_mlp_n, 1),
+                "what": "detect over I_{M,i} (points within radius of each step's base, PAPER.md:401); "
+                        "covered = all B*N*M pairs of the step served by one partitioned call"}
+
     # active-set detect latency per SCO iteration = wall time of one detect
     # call from q resident on the device to the count on the host (collectives included),
     # p50 / p99 over `latency_calls` calls after 5 warm-ups
@@ -377,6 +409,7 @@ def main():
                        "l2": "256 MiB buffer written between timed steps (L2 flush)"},
             "roofline": roof, "mlp_kernel_share_of_step": kshare,
             "detect_latency": lat,
+            "partitioned": part,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_pairs / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": h2d // e2e_steps,
                     "d2h_bytes_per_step": d2h // e2e_steps, "steps": e2e_steps},

@@ -77,6 +77,8 @@ typedef struct {
   int64_t max_active;      /* staging capacity (records) of detect on this rank */
   int32_t rank;            /* point sharding: this rank owns ids whose 128-id block */
   int32_t world;           /*   (id / 128) satisfies block % world == rank; world >= 1 */
+  int64_t max_candidates;  /* range-partitioned detect: capacity of the per-step candidate
+                              lists (sum over steps of |I_{M,i}|); 0 = partitioned detect off */
 } gcdf_options;
 
 /* One active constraint (48 B): f, grad_q f (9), wp = b*N + i, pt = global point id. */
@@ -89,7 +91,7 @@ typedef struct {
 
 /* ------------------------------------------------------------------ lifecycle */
 /* Fills *opt with defaults (precision FP16, chain rule, capacity 1<<20, 256 waypoints,
-   max_active 1<<22, rank 0, world 1). */
+   max_active 1<<22, rank 0, world 1, max_candidates 0). */
 void gcdf_default_options(gcdf_options *opt);
 
 /* Creates a context on CUDA device cuda_device.  Fails with UNSUPPORTED unless the
@@ -163,6 +165,22 @@ int gcdf_detect_active_set(gcdf_ctx *ctx, const float *q_dev, int32_t B, int32_t
                            float tau, gcdf_active_t *out_dev, int64_t out_capacity, int64_t *wp_offsets_dev,
                            float *wp_min_dev, int64_t *wp_argmin_dev, int64_t *wp_key_dev,
                            int64_t *count_dev, int64_t *count_host_or_null, void *stream);
+
+/* NEXT-1 range partition (R23): the fused detect over
+   the pairs of each step i with the obstacle points of its partition
+   I_{M,i} = { j : |p_j,xy - (x_i, y_i)| <= radius } only (radius > 0, metres, planar
+   distance to the step's base position q_i[0:2]).  Outputs, order and errors as
+   gcdf_detect_active_set, with wp_min / wp_argmin over I_{M,i}; part_sizes_dev [B*N]
+   (may be NULL) receives m_i = |I_{M,i}| on this rank.  The planar grid (cell >= radius)
+   over this rank's live points is rebuilt on the device when the scene or the radius
+   changed since the last call; the partitions are built per call (bitmap + ordered
+   compaction).  Needs max_candidates > 0 (INVALID_ARG otherwise); when sum_i m_i exceeds
+   it the call evaluates nothing and returns CAPACITY (count 0). */
+int gcdf_detect_active_set_partitioned(gcdf_ctx *ctx, const float *q_dev, int32_t B, int32_t N, float radius,
+                                       float delta, float tau, gcdf_active_t *out_dev, int64_t out_capacity,
+                                       int64_t *wp_offsets_dev, float *wp_min_dev, int64_t *wp_argmin_dev,
+                                       int64_t *wp_key_dev, int64_t *part_sizes_dev, int64_t *count_dev,
+                                       int64_t *count_host_or_null, void *stream);
 
 /* Host-buffer form of gcdf_detect_active_set (the end-to-end call): q_host [B][N][9] is
    copied to the device, the fused detect runs, and the results come back to host memory:

@@ -32,7 +32,10 @@ inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
 struct Layout {
   int64_t pts, wf32, wbf16, wf16, meta, staging, wp_key, wp_count, counter, upd_payload, upd_slots;
-  int64_t h_q, h_out, h_offs, h_wmin, h_warg, h_count, total;
+  int64_t h_q, h_out, h_offs, h_wmin, h_warg, h_count;
+  int64_t p_grid, p_bbox, p_cell_count, p_cell_start, p_cell_fill, p_cell_items, p_bitmap, p_chunk_cnt, p_chunk_off,
+      p_scan_tmp, p_cand, p_cand_start, p_cand_count, p_tile_start, p_tile_wp, p_n_tiles, p_words, p_nchunk;
+  int64_t total;
   int64_t wf32_bytes, wbf16_bytes;
 };
 
@@ -80,6 +83,9 @@ struct gcdf_ctx {
   double prof_ms = 0.0;
   int64_t prof_n = 0;
   long long *trace = nullptr;  // diagnostics buffer (device), see gcdf_debug_trace
+  // range partition: the planar grid is rebuilt when the scene or the radius changed
+  bool part_dirty = true;
+  float part_r = -1.f;
 };
 
 namespace {
@@ -157,6 +163,31 @@ WeightsBF16 bf16_view(const gcdf_ctx *c) {
   w.w7 = f.w7;
   w.b7 = f.b7;
   return w;
+}
+
+PartScratch part_view(const gcdf_ctx *c) {
+  const Layout &L = c->L;
+  PartScratch p{};
+  p.grid = reinterpret_cast<float *>(c->ws + L.p_grid);
+  p.bbox = reinterpret_cast<unsigned *>(c->ws + L.p_bbox);
+  p.cell_count = reinterpret_cast<int32_t *>(c->ws + L.p_cell_count);
+  p.cell_start = reinterpret_cast<int64_t *>(c->ws + L.p_cell_start);
+  p.cell_fill = reinterpret_cast<int32_t *>(c->ws + L.p_cell_fill);
+  p.cell_items = reinterpret_cast<int32_t *>(c->ws + L.p_cell_items);
+  p.bitmap = reinterpret_cast<uint32_t *>(c->ws + L.p_bitmap);
+  p.words = L.p_words;
+  p.chunk_cnt = reinterpret_cast<int32_t *>(c->ws + L.p_chunk_cnt);
+  p.chunk_off = reinterpret_cast<int64_t *>(c->ws + L.p_chunk_off);
+  p.nchunk = L.p_nchunk;
+  p.scan_tmp = reinterpret_cast<int64_t *>(c->ws + L.p_scan_tmp);
+  p.cand = reinterpret_cast<int32_t *>(c->ws + L.p_cand);
+  p.max_candidates = c->opt.max_candidates;
+  p.cand_start = reinterpret_cast<int64_t *>(c->ws + L.p_cand_start);
+  p.cand_count = reinterpret_cast<int64_t *>(c->ws + L.p_cand_count);
+  p.tile_start = reinterpret_cast<int64_t *>(c->ws + L.p_tile_start);
+  p.tile_wp = reinterpret_cast<int32_t *>(c->ws + L.p_tile_wp);
+  p.n_tiles = reinterpret_cast<int64_t *>(c->ws + L.p_n_tiles);
+  return p;
 }
 
 DetectScratch scratch_view(const gcdf_ctx *c) {
@@ -260,6 +291,7 @@ void gcdf_default_options(gcdf_options *o) {
   o->max_active = 1 << 22;
   o->rank = 0;
   o->world = 1;
+  o->max_candidates = 0;
 }
 
 int gcdf_has_tcgen05(void) { return tc_compiled() ? 1 : 0; }
@@ -311,6 +343,29 @@ int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out) {
   L.h_wmin = off; off = align256(off + (int64_t)o.max_waypoints * 4);
   L.h_warg = off; off = align256(off + (int64_t)o.max_waypoints * 8);
   L.h_count = off; off = align256(off + 8);
+  // range-partitioned detect (k_partition.cu), only with max_candidates > 0
+  if (o.max_candidates > 0) {
+    const int64_t W = o.max_waypoints;
+    L.p_words = c->local_cap / 32;
+    L.p_nchunk = (L.p_words + kPartChunkWords - 1) / kPartChunkWords;
+    const int64_t max_tiles = std::min<int64_t>(W * c->tiles_cap, o.max_candidates / kTile + W);
+    L.p_grid = off; off = align256(off + 64);
+    L.p_bbox = off; off = align256(off + 64);
+    L.p_cell_count = off; off = align256(off + kPartMaxCells * 4);
+    L.p_cell_start = off; off = align256(off + (kPartMaxCells + 1) * 8);
+    L.p_cell_fill = off; off = align256(off + kPartMaxCells * 4);
+    L.p_cell_items = off; off = align256(off + c->local_cap * 4);
+    L.p_bitmap = off; off = align256(off + W * L.p_words * 4);
+    L.p_chunk_cnt = off; off = align256(off + W * L.p_nchunk * 4);
+    L.p_chunk_off = off; off = align256(off + (W * L.p_nchunk + 1) * 8);
+    L.p_scan_tmp = off; off = align256(off + part_scan_tmp_elems(std::max<int64_t>(kPartMaxCells, W * L.p_nchunk)) * 8);
+    L.p_cand = off; off = align256(off + o.max_candidates * 4);
+    L.p_cand_start = off; off = align256(off + (W + 1) * 8);
+    L.p_cand_count = off; off = align256(off + W * 8);
+    L.p_tile_start = off; off = align256(off + (W + 1) * 8);
+    L.p_tile_wp = off; off = align256(off + max_tiles * 4);
+    L.p_n_tiles = off; off = align256(off + 8);
+  }
   L.total = off;
   cudaSetDevice(cuda_device);
   if (cudaHostAlloc(&c->h_payload, kUpdChunk * 16, cudaHostAllocDefault) != cudaSuccess ||
@@ -524,6 +579,7 @@ int gcdf_update_scene(gcdf_ctx *c, const float *add_xyz, int64_t n_add, int64_t 
   if (n_rem > 0) c->cursor = std::min(c->cursor, rs[0]);
   c->n_live += n_add - n_rem;
   for (int64_t a = 0; a < n_add; ++a) c->id_bound = std::max(c->id_bound, out_ids[a] + 1);
+  if (n_add + n_rem > 0) c->part_dirty = true;
   // device scatter of this rank's share, in pinned chunks
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   float4 *d_pay = reinterpret_cast<float4 *>(c->ws + c->L.upd_payload);
@@ -644,10 +700,10 @@ int gcdf_query_values_grads(gcdf_ctx *c, const float *q, int32_t B, int32_t N, f
 
 static int finish_detect(gcdf_ctx *c, int32_t nwp, int32_t tpw, gcdf_active_t *out, int64_t cap, int64_t *offs,
                          float *wmin, int64_t *warg, int64_t *wkey, int64_t *count_dev, int64_t *count_host,
-                         cudaStream_t s) {
+                         cudaStream_t s, const int64_t *tile_start = nullptr) {
   DetectScratch ds = scratch_view(c);
   int nl = 0;
-  cudaError_t e = launch_finalize(ds, nwp, tpw, out, cap, offs, wmin, warg, wkey, count_dev,
+  cudaError_t e = launch_finalize(ds, nwp, tpw, tile_start, out, cap, offs, wmin, warg, wkey, count_dev,
                                   reinterpret_cast<int64_t *>(c->ws + c->L.wp_count), s, &nl);
   int rc = count_launch(c, e, "detect finalize", nl);
   if (rc) return rc;
@@ -680,6 +736,54 @@ int gcdf_detect_active_set(gcdf_ctx *c, const float *q, int32_t B, int32_t N, fl
   if ((rc = count_launch(c, launch_detect_init(a.ds, a.n_wp, s), "detect init"))) return rc;
   if ((rc = count_launch(c, run_mlp(c, a, s), "detect kernel"))) return rc;
   return finish_detect(c, a.n_wp, a.tiles_per_wp, out, cap, offs, wmin, warg, wkey, count_dev, count_host, s);
+}
+
+int gcdf_detect_active_set_partitioned(gcdf_ctx *c, const float *q, int32_t B, int32_t N, float radius, float delta,
+                                       float tau, gcdf_active_t *out, int64_t cap, int64_t *offs, float *wmin,
+                                       int64_t *warg, int64_t *wkey, int64_t *psizes, int64_t *count_dev,
+                                       int64_t *count_host, void *stream) {
+  int rc = precheck(c);
+  if (rc) return rc;
+  if ((rc = check_wp(c, q, B, N))) return rc;
+  if (!out || cap < 0 || !offs || !count_dev || !std::isfinite(delta) || !std::isfinite(tau))
+    return fail(c, GCDF_ERR_INVALID_ARG, "detect: null output or non-finite delta/tau");
+  if (!(radius > 0.f) || !std::isfinite(radius))
+    return fail(c, GCDF_ERR_INVALID_ARG, "partition radius must be finite and > 0");
+  if (c->opt.max_candidates <= 0)
+    return fail(c, GCDF_ERR_INVALID_ARG, "partitioned detect needs gcdf_options.max_candidates > 0");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const PartScratch ps = part_view(c);
+  const SceneView sv = scene_view(c);
+  int nl = 0;
+  if (c->part_dirty || c->part_r != radius) {
+    if ((rc = count_launch(c, launch_part_grid(sv.pts, sv.local_bound, radius, ps, s, &nl), "partition grid", 0)))
+      return rc;
+    c->launches += nl;
+    c->part_dirty = false;
+    c->part_r = radius;
+  }
+  QueryArgs a = make_args(c, q, B * N);
+  a.detect = 1;
+  a.delta = delta;
+  a.tau = tau;
+  a.ds = scratch_view(c);
+  if ((rc = count_launch(c, launch_detect_init(a.ds, a.n_wp, s), "detect init"))) return rc;
+  nl = 0;
+  if ((rc = count_launch(c, launch_part_build(sv.pts, q, a.n_wp, radius, ps, a.ds.counter + 1, s, &nl),
+                         "partition build", 0)))
+    return rc;
+  c->launches += nl;
+  a.part.tile_wp = ps.tile_wp;
+  a.part.tile_start = ps.tile_start;
+  a.part.cand_start = ps.cand_start;
+  a.part.cand_count = ps.cand_count;
+  a.part.cand = ps.cand;
+  a.part.n_tiles = ps.n_tiles;
+  if ((rc = count_launch(c, run_mlp(c, a, s), "detect kernel"))) return rc;
+  if (psizes)
+    CK(c, cudaMemcpyAsync(psizes, ps.cand_count, (int64_t)a.n_wp * 8, cudaMemcpyDeviceToDevice, s), "part sizes");
+  return finish_detect(c, a.n_wp, a.tiles_per_wp, out, cap, offs, wmin, warg, wkey, count_dev, count_host, s,
+                       ps.tile_start);
 }
 
 int gcdf_detect_active_set_host(gcdf_ctx *c, const float *q_host, int32_t B, int32_t N, float delta, float tau,

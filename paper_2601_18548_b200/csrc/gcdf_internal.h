@@ -64,6 +64,19 @@ struct DetectScratch {
   unsigned long long *wp_key;      // [max_waypoints] unsigned order key, ~0 = none
 };
 
+// Range-partitioned tile map (NEXT-1): tile T of step w = tile_wp[T] covers candidates
+// (T - tile_start[w]) * 128 + row of that step's list cand[cand_start[w] ...] (ascending
+// local slots), cand_count[w] of them; *n_tiles tiles in all.  tile_wp == nullptr: the
+// dense map (every step x every local slot).
+struct PartView {
+  const int32_t *tile_wp = nullptr;
+  const int64_t *tile_start = nullptr;
+  const int64_t *cand_start = nullptr;
+  const int64_t *cand_count = nullptr;
+  const int32_t *cand = nullptr;
+  const int64_t *n_tiles = nullptr;
+};
+
 struct QueryArgs {
   SceneView scene;
   const float *q;                  // [n_wp][9]
@@ -79,7 +92,26 @@ struct QueryArgs {
   DetectScratch ds;
   // diagnostics (gcdf_debug_trace): CTA 0 records clock64 stamps, NULL in normal runs
   long long *trace;
+  PartView part;                   // range partition (detect only), see PartView
 };
+
+// (step, local slot) of row `row` of tile T; valid = false for padding rows
+__device__ __forceinline__ void tile_pair(const QueryArgs &a, int64_t T, int row, int &w, int64_t &slot,
+                                          bool &valid) {
+  if (a.part.tile_wp) {
+    w = a.part.tile_wp[T];
+    const int64_t k = (T - a.part.tile_start[w]) * kTile + row;
+    valid = k < a.part.cand_count[w];
+    slot = valid ? (int64_t)a.part.cand[a.part.cand_start[w] + k] : 0;
+  } else {
+    w = (int)(T / a.tiles_per_wp);
+    slot = (T % a.tiles_per_wp) * kTile + row;
+    valid = slot < a.scene.local_bound;
+  }
+}
+__device__ __forceinline__ int64_t query_tiles(const QueryArgs &a) {
+  return a.part.tile_wp ? *a.part.n_tiles : (int64_t)a.n_wp * a.tiles_per_wp;
+}
 // trace layout: [role 0 = MMA thread (issue start / end per slot), 1 + w = epilogue warp w
 // (lane 0), w = 0..15, 17 = MMA thread (wait start / wait done per slot)][tile 0..3][phase 0..12][4]
 constexpr int kTraceTiles = 4, kTracePhases = 13, kTraceRoles = 18;
@@ -103,8 +135,39 @@ cudaError_t launch_selftest_umma(int mode, const float *A, const float *B, float
 cudaError_t launch_compact_dense(const float *values, const float *grads, int64_t stride, int32_t n_wp,
                                  int32_t tiles_per_wp, SceneView scene, float delta, float tau,
                                  DetectScratch ds, cudaStream_t s);
+// range partition (k_partition.cu).  Grid over this rank's live points, rebuilt on demand.
+struct PartScratch {
+  float *grid;            // [8]: ox, oy, inv_cs, cs, radius, nx, ny (as float bits), unused
+  unsigned *bbox;         // [4] ordered-uint min x, min y, max x, max y
+  int32_t *cell_count;    // [kPartMaxCells]
+  int64_t *cell_start;    // [kPartMaxCells + 1]
+  int32_t *cell_fill;     // [kPartMaxCells]
+  int32_t *cell_items;    // [local_cap]
+  uint32_t *bitmap;       // [max_wp][words]
+  int64_t words;          // local_cap / 32
+  int32_t *chunk_cnt;     // [max_wp * nchunk]
+  int64_t *chunk_off;     // [max_wp * nchunk + 1]
+  int64_t nchunk;         // words / kPartChunkWords (rounded up)
+  int64_t *scan_tmp;      // scan block sums
+  int32_t *cand;          // [max_candidates]
+  int64_t max_candidates;
+  int64_t *cand_start;    // [max_wp + 1]
+  int64_t *cand_count;    // [max_wp]
+  int64_t *tile_start;    // [max_wp + 1]
+  int32_t *tile_wp;       // [max_wp * tiles_cap]
+  int64_t *n_tiles;       // [1]
+};
+constexpr int64_t kPartMaxCells = 1025 * 1025;  // grid cells (cell size >= extent / 1024)
+constexpr int64_t kPartChunkWords = 1024;       // bitmap words per compaction chunk
+int64_t part_scan_tmp_elems(int64_t n);          // block-sum scratch of an n-element scan
+cudaError_t launch_part_grid(const float4 *pts, int64_t local_bound, float radius, PartScratch ps, cudaStream_t s,
+                             int *n_launches);
+cudaError_t launch_part_build(const float4 *pts, const float *q, int32_t n_wp, float radius, PartScratch ps,
+                              unsigned long long *overflow_flag, cudaStream_t s, int *n_launches);
 // finalize: tile counts -> wp_offsets, ordered copy staging -> out, wp_min/argmin/key, count
-cudaError_t launch_finalize(DetectScratch ds, int32_t n_wp, int32_t tiles_per_wp, gcdf_active_t *out,
+// (tile_start: per-step tile ranges of a partitioned detect, nullptr = tiles_per_wp per step)
+cudaError_t launch_finalize(DetectScratch ds, int32_t n_wp, int32_t tiles_per_wp, const int64_t *tile_start,
+                            gcdf_active_t *out,
                             int64_t out_capacity, int64_t *wp_offsets, float *wp_min, int64_t *wp_argmin,
                             int64_t *wp_key, int64_t *count, int64_t *wp_count_scratch, cudaStream_t s,
                             int *n_launches);

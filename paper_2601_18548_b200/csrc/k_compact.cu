@@ -8,6 +8,7 @@
 // Min keys: key = ord(f) << 32 | pt, ord() order-preserving float -> uint32, so the
 // unsigned minimum is (min f, smallest id on ties) -- one atomicMin per tile.
 #include "gcdf_internal.h"
+#include "k_scan.cuh"
 
 namespace gcdf {
 namespace {
@@ -25,32 +26,6 @@ __global__ void k_detect_init(unsigned long long *wp_key, unsigned long long *co
   if (blockIdx.x == 0 && threadIdx.x < 2) counter[threadIdx.x] = 0ull;
 }
 
-// exclusive scan of v over the block (blockDim.x multiple of 32, <= 1024)
-__device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t *total, int64_t *sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int64_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) sh[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    int64_t s = lane < nw ? sh[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int64_t y = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += y;
-    }
-    if (lane < nw) sh[lane] = s;  // inclusive prefix of warp totals
-  }
-  __syncthreads();
-  const int64_t res = x - v + (warp > 0 ? sh[warp - 1] : 0);
-  *total = sh[nw - 1];
-  __syncthreads();
-  return res;
-}
 
 // K3 standalone over dense values: one WARP per tile of 128 slots, 4 slots per lane
 // (one 16-B streaming load), no block barrier.  The tile's actives are ranked in slot
@@ -137,11 +112,14 @@ __global__ void __launch_bounds__(256) k_compact_dense(const float *__restrict__
 
 // per-waypoint active counts from the tile meta
 __global__ void __launch_bounds__(256) k_wp_count(const int2 *__restrict__ meta, int32_t tpw,
+                                                  const int64_t *__restrict__ tile_start,
                                                   int64_t *__restrict__ wp_count) {
   __shared__ int64_t sh[32];
   const int w = blockIdx.x;
+  const int64_t t0 = tile_start ? tile_start[w] : (int64_t)w * tpw;
+  const int64_t nt = tile_start ? tile_start[w + 1] - t0 : tpw;
   int64_t s = 0;
-  for (int t = threadIdx.x; t < tpw; t += blockDim.x) s += meta[(int64_t)w * tpw + t].y;
+  for (int64_t t = threadIdx.x; t < nt; t += blockDim.x) s += meta[t0 + t].y;
   int64_t tot;
   block_excl_scan(s, &tot, sh);
   if (threadIdx.x == 0) wp_count[w] = tot;
@@ -178,16 +156,19 @@ __global__ void __launch_bounds__(1024) k_wp_scan(const int64_t *__restrict__ wp
 
 // ordered copy staging -> out: one CTA per waypoint, tiles scanned in order
 __global__ void __launch_bounds__(256) k_wp_scatter(const int2 *__restrict__ meta, int32_t tpw,
+                                                    const int64_t *__restrict__ tile_start,
                                                     const gcdf_active_t *__restrict__ staging,
                                                     const int64_t *__restrict__ wp_offsets,
                                                     gcdf_active_t *__restrict__ out, int64_t cap) {
   __shared__ int64_t sh[32];
   const int w = blockIdx.x;
+  const int64_t tb = tile_start ? tile_start[w] : (int64_t)w * tpw;
+  const int64_t nt = tile_start ? tile_start[w + 1] - tb : tpw;
   int64_t carry = wp_offsets[w];
-  for (int t0 = 0; t0 < tpw; t0 += blockDim.x) {
-    const int t = t0 + threadIdx.x;
+  for (int64_t t0 = 0; t0 < nt; t0 += blockDim.x) {
+    const int64_t t = t0 + threadIdx.x;
     int2 m = make_int2(0, 0);
-    if (t < tpw) m = meta[(int64_t)w * tpw + t];
+    if (t < nt) m = meta[tb + t];
     int64_t tot;
     const int64_t ex = block_excl_scan(m.y, &tot, sh);
     if (m.y > 0 && m.x >= 0) {
@@ -280,14 +261,16 @@ cudaError_t launch_compact_dense(const float *values, const float *grads, int64_
   return cudaGetLastError();
 }
 
-cudaError_t launch_finalize(DetectScratch ds, int32_t n_wp, int32_t tiles_per_wp, gcdf_active_t *out,
+cudaError_t launch_finalize(DetectScratch ds, int32_t n_wp, int32_t tiles_per_wp, const int64_t *tile_start,
+                            gcdf_active_t *out,
                             int64_t out_capacity, int64_t *wp_offsets, float *wp_min, int64_t *wp_argmin,
                             int64_t *wp_key, int64_t *count, int64_t *wp_count_scratch, cudaStream_t s,
                             int *n_launches) {
   if (n_wp <= 0) return cudaSuccess;
-  k_wp_count<<<n_wp, 256, 0, s>>>(ds.tile_meta, tiles_per_wp, wp_count_scratch);
+  k_wp_count<<<n_wp, 256, 0, s>>>(ds.tile_meta, tiles_per_wp, tile_start, wp_count_scratch);
   k_wp_scan<<<1, 1024, 0, s>>>(wp_count_scratch, n_wp, wp_offsets, count, ds.wp_key, wp_min, wp_argmin, wp_key);
-  k_wp_scatter<<<n_wp, 256, 0, s>>>(ds.tile_meta, tiles_per_wp, ds.staging, wp_offsets, out, out_capacity);
+  k_wp_scatter<<<n_wp, 256, 0, s>>>(ds.tile_meta, tiles_per_wp, tile_start, ds.staging, wp_offsets, out,
+                                    out_capacity);
   *n_launches += 3;
   return cudaGetLastError();
 }

@@ -95,20 +95,25 @@ __global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const Q
 
   const int tid = threadIdx.x, tp = tid >> 4, tu = tid & 15;
   const int lane = tid & 31, warp = tid >> 5;
-  const int64_t n_tiles = (int64_t)a.n_wp * a.tiles_per_wp;
+  const int64_t n_tiles = query_tiles(a);  // (partitioned: read from the device)
   const int64_t lb = a.scene.local_bound;
 
   for (int64_t T = blockIdx.x; T < n_tiles; T += gridDim.x) {
-    const int w = (int)(T / a.tiles_per_wp);
-    const int t = (int)(T % a.tiles_per_wp);
-    const int64_t slot0 = (int64_t)t * kTile;
+    int w;
+    int64_t slot0;
+    bool v0;
+    tile_pair(a, T, 0, w, slot0, v0);  // step of this tile (slot0: dense map only)
+    (void)v0;
     __syncthreads();  // smem of the previous tile is free
     if (tid < kNdof) qv[tid] = __ldg(a.q + (int64_t)w * kNdof + tid);
     __syncthreads();
     // A2: pair generation + base-frame bias: p' = p - [q_x, q_y, 0]
     if (tid < kTile) {
-      const int64_t slot = slot0 + tid;
-      float4 p = slot < lb ? __ldg(a.scene.pts + slot) : make_float4(0.f, 0.f, 0.f, 0.f);
+      int wt;
+      int64_t slot;
+      bool valid;
+      tile_pair(a, T, tid, wt, slot, valid);
+      float4 p = valid ? __ldg(a.scene.pts + slot) : make_float4(0.f, 0.f, 0.f, 0.f);
       sp[tid] = make_float4(p.x - qv[0], p.y - qv[1], p.z, p.w);
     }
     // layer-1 constant of this waypoint: c = b1 + W1[:, 5:12] . [theta, j1..j6]
@@ -218,8 +223,11 @@ __global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const Q
     // A6/A7 (detect): threshold, per-tile compaction slots, per-waypoint min key
     if (a.detect) {
       if (tid < kTile) {
-        const int64_t slot = slot0 + tid;
-        const bool live = slot < lb && sp[tid].w > 0.f;
+        int wt;
+        int64_t slot;
+        bool valid;
+        tile_pair(a, T, tid, wt, slot, valid);
+        const bool live = valid && sp[tid].w > 0.f;
         const float f = fval[tid];
         const bool act = live && (f - a.delta <= a.tau);
         const unsigned bal = __ballot_sync(0xffffffffu, act);
@@ -343,7 +351,10 @@ __global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const Q
       if (base >= 0 && ((bits >> lane) & 1u)) {
         int r = __popc(bits & ((1u << lane) - 1u));
         for (int i = 0; i < warp; ++i) r += __popc(actw[i]);
-        const int64_t slot = slot0 + tid;
+        int wt;
+        int64_t slot;
+        bool valid;
+        tile_pair(a, T, tid, wt, slot, valid);
         float4 *dst = reinterpret_cast<float4 *>(a.ds.staging + base + r);
         const float *g = gst + tid * 9;
         dst[0] = make_float4(fval[tid], g[0], g[1], g[2]);
@@ -364,9 +375,11 @@ cudaError_t launch_h(const WeightsF32 &w, const QueryArgs &a, int num_sms, cudaS
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mlp_simt<H>, 256, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  const int64_t n_tiles = (int64_t)a.n_wp * a.tiles_per_wp;
   int64_t grid = (int64_t)num_sms * per_sm;
-  if (grid > n_tiles) grid = n_tiles;
+  if (!a.part.tile_wp) {  // (a partitioned detect knows its tile count on the device only)
+    const int64_t n_tiles = (int64_t)a.n_wp * a.tiles_per_wp;
+    if (grid > n_tiles) grid = n_tiles;
+  }
   if (grid < 1) return cudaSuccess;
   k_mlp_simt<H><<<(unsigned)grid, 256, smem, s>>>(w, a);
   return cudaGetLastError();

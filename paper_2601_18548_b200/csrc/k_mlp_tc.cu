@@ -57,14 +57,8 @@ constexpr int kEpiWarps = 16;             // warps 0..15: epilogue (8 per tile s
 #endif
 constexpr int kWarps = kEpiWarps + (GCDF_TC_ISSUE == 0 ? 1 : 2);
 constexpr int kThreads = kWarps * 32;
-// Epilogue layout (dev switch): 0 = 8 warps per tile slot (64 columns per thread),
-// 1 = all 16 warps serve each slot in turn (32 columns per thread)
-#ifndef GCDF_TC_EPI16
-#define GCDF_TC_EPI16 0
-#endif
 constexpr int kEpiPerSlot = 256;
-constexpr int kEpiThreads = kEpiWarps * 32;
-constexpr int kEpiArrivals = GCDF_TC_EPI16 ? kEpiThreads : kEpiPerSlot;  // epi_done count
+constexpr int kEpiArrivals = kEpiPerSlot;  // epi_done count
 constexpr int kPhases = 12;               // MMA phases per tile
 constexpr int kMasks = 5;                 // stored ReLU masks: layers 1..5
 constexpr int kWBytes = 5 * H * H * 2;    // 163,840
@@ -214,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   __syncthreads();
   fence_after();
   const uint32_t tbase = S.tmem_base;
-  const int64_t n_tiles = (int64_t)a.n_wp * a.tiles_per_wp;
+  const int64_t n_tiles = query_tiles(a);  // (partitioned: read from the device)
   const int64_t lb = a.scene.local_bound;
   const int64_t stride = 2 * (int64_t)gridDim.x;
 
@@ -295,281 +289,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     __syncthreads();
     return;  // (TMEM is freed by warp 0 after the final barrier)
   }
-#if GCDF_TC_EPI16
-  // ===================== epilogue: all 16 warps serve both slots, alternately ==============
-  // warp w reads TMEM lanes 32 (w % 4) .. + 31 and accumulator columns 32 cq .. + 31,
-  // cq = w / 4: four warps per SM sub-partition work on each slot's epilogue, which
-  // shortens it (it is on the slot's critical chain MMA -> epilogue -> next MMA).
-  const int qd = warp & 3;          // TMEM lane quarter (warp % 4, the tcgen05.ld rule)
-  const int cq = warp >> 2;         // accumulator column quarter: units 32 cq .. 32 cq + 31
-  const int row = qd * 32 + lane;   // pair within the tile = TMEM lane
-  const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-  const int u0 = 32 * cq;
-  uint32_t *mk = &S.mask[0][0][0][0];  // [slot][layer][512 threads], 32 units per word
-  if (cq == 0) {  // the constant "ones" A blocks of the bias GEMM steps: {1, 1, 0, ...}
-    uint32_t ones[8] = {pack2<F16>(1.f, 1.f), 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-    st8(tbase + lane_off + kColOnes, ones);
-    st8(tbase + 256u + lane_off + kColOnes, ones);
-  }
-  auto hand_off = [&](int ss) {
-    wait_st();
-    fence_before();
-    mbar_arrive(&S.epi_done[ss]);
-  };
-  auto prefetch_pt = [&](int ss, int64_t TT) {  // (column quarter 0 threads)
-    const int64_t sl = (TT % a.tiles_per_wp) * kTile + row;
-    const bool ok = TT < n_tiles && sl < lb;
-    cp_async16(&S.ptn[ss][row], ok ? (const void *)(a.scene.pts + sl) : (const void *)a.scene.pts, ok ? 16u : 0u);
-    cp_async_commit();
-  };
-  // A2 + A1 of tile TT in slot ss (quarter 0 writes K 0..15, quarter 1 K 16..31), hand off
-  auto stage_a1 = [&](int ss, int64_t TT) -> bool {
-    const int wn = (int)(TT / a.tiles_per_wp);
-    const int64_t sl = (TT % a.tiles_per_wp) * kTile + row;
-    const float *qw = a.q + (int64_t)wn * kNdof;
-    bool lv = false;
-    if (cq < 2) {
-      float v[16];
-      if (cq == 0) {  // K 0..15: p'_x, p'_y, p_z, theta, j1 (3 each), x_hi of j2
-        const float4 pt = S.ptn[ss][row];
-        lv = sl < lb && pt.w > 0.f;
-        split3<F16>(pt.x - __ldg(qw), v);
-        split3<F16>(pt.y - __ldg(qw + 1), v + 3);
-        split3<F16>(pt.z, v + 6);
-        split3<F16>(__ldg(qw + 2), v + 9);
-        split3<F16>(__ldg(qw + 3), v + 12);
-        v[15] = round16<F16>(__ldg(qw + 4));
-      } else {        // K 16..31: x_lo, x_hi of j2, j3..j6 (3 each), {1, 1} for b1
-        const float j2 = __ldg(qw + 4);
-        const float j2h = round16<F16>(j2);
-        v[0] = j2 - j2h;
-        v[1] = j2h;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) split3<F16>(__ldg(qw + 5 + i), v + 2 + 3 * i);
-        v[14] = 1.f;
-        v[15] = 1.f;
-      }
-      uint32_t a1[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) a1[i] = pack2<F16>(v[2 * i], v[2 * i + 1]);
-      st8(tbase + (uint32_t)ss * 256u + lane_off + kColA + 8u * cq, a1);
-    }
-    hand_off(ss);
-    return lv;
-  };
-  const uint32_t one = S.one;
-  const bool tracer = a.trace && blockIdx.x == 0 && lane == 0 && warp < 8;
-  int64_t Tt[2];
-  float fv[2] = {0.f, 0.f};     // value f of the slot's current pair (quarter 0)
-  int ridx[2] = {-1, -1};       // staging record index (detect), -1 = none
-  uint32_t fl = 0u;             // bit ss: live; bit 2 + ss: mma_done parity
-#pragma unroll
-  for (int ss = 0; ss < 2; ++ss) {
-    Tt[ss] = (int64_t)blockIdx.x * 2 + ss;
-    if (Tt[ss] < n_tiles) {
-      if (cq == 0) {
-        prefetch_pt(ss, Tt[ss]);
-        cp_async_wait_all();
-      }
-      if (stage_a1(ss, Tt[ss])) fl |= 1u << ss;
-    }
-  }
-  int it = 0;
-  for (; Tt[0] < n_tiles; ++it) {
-#pragma unroll 1
-    for (int p = 0; p < kPhases; ++p) {
-#pragma unroll
-      for (int ss = 0; ss < 2; ++ss) {
-        if (ss == 1 && Tt[1] >= n_tiles) continue;  // odd tail: slot 1 idle in the last round
-        long long *tr = (tracer && it < kTraceTiles)
-                            ? a.trace + (size_t)((1 + warp + 8 * ss) * kTraceTiles + it) * kTracePhases * 4 : nullptr;
-        const uint32_t tS = tbase + (uint32_t)ss * 256u + lane_off;
-        const uint32_t tD = tS + 32u * cq;
-        const uint32_t tA = tS + kColA + 16u * cq;
-        uint32_t *mks = mk + (size_t)ss * kMasks * kEpiThreads + tid;
-        mbar_wait(&S.mma_done[ss], (fl >> (2 + ss)) & 1u);
-        if (tr) tr[(p + 1) * 4 + 1] = clock64();
-        fl ^= 1u << (2 + ss);
-        fence_after();
-        if (p < 5) {
-          // ---- forward layer l = p + 1: z = D (bias folded in); h = ReLU(z) -> A ----
-          uint32_t m = 0u;
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            uint32_t pk[8], rr[16];
-            ld16(tD + 16 * hf, rr);
-            wait_ld();
-            if (tr && hf == 0) tr[(p + 1) * 4 + 0] = clock64();
-#pragma unroll
-            for (int j = 0; j < 16; j += 4) {
-              pk[j >> 1] = pack2_relu<F16>(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1]));
-              pk[(j >> 1) + 1] = pack2_relu<F16>(__uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3]));
-              m |= mask_group_f(pk[j >> 1], pk[(j >> 1) + 1], (hf * 16 + j) >> 2, one);
-            }
-            st8(tA + 8 * hf, pk);
-          }
-          mks[p * kEpiThreads] = m;
-          if (tr) tr[(p + 1) * 4 + 2] = clock64();
-          hand_off(ss);
-          if (tr) tr[(p + 1) * 4 + 3] = clock64();
-        } else if (p == 5) {
-          // ---- layer 6: e6 = w7 (.) 1[z6 > 0] -> A; f = w7 . ReLU(z6) + b7 (fp32) ----
-          float fa[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            uint32_t pk[8], rr[16];
-            ld16(tD + 16 * hf, rr);
-            wait_ld();
-            if (tr && hf == 0) tr[(p + 1) * 4 + 0] = clock64();
-#pragma unroll
-            for (int j = 0; j < 16; j += 4) {
-              const float4 w7 = *reinterpret_cast<const float4 *>(S.w7half + u0 + 16 * hf + j);
-              const uint2 w2 = *reinterpret_cast<const uint2 *>(S.w7h + (u0 + 16 * hf + j) / 2);
-              const float z0 = __uint_as_float(rr[j]), z1 = __uint_as_float(rr[j + 1]);
-              const float z2 = __uint_as_float(rr[j + 2]), z3 = __uint_as_float(rr[j + 3]);
-              pk[j >> 1] = w2.x & nz_halves(pack2_relu<F16>(z0, z1), one);
-              pk[(j >> 1) + 1] = w2.y & nz_halves(pack2_relu<F16>(z2, z3), one);
-              // (w7 / 2) (z + |z|) = w7 ReLU(z) exactly (z + |z| = 2 ReLU(z), halving is exact)
-              fa[0] = fmaf(w7.x, z0 + fabsf(z0), fa[0]);
-              fa[1] = fmaf(w7.y, z1 + fabsf(z1), fa[1]);
-              fa[2] = fmaf(w7.z, z2 + fabsf(z2), fa[2]);
-              fa[3] = fmaf(w7.w, z3 + fabsf(z3), fa[3]);
-            }
-            st8(tA + 8 * hf, pk);
-          }
-          if (tr) tr[(p + 1) * 4 + 2] = clock64();
-          hand_off(ss);
-          if (tr) tr[(p + 1) * 4 + 3] = clock64();
-          // f = w7 . h6 + b7 (fp32, no output activation: signed value)
-          S.fpart[ss][cq][row] = (fa[0] + fa[1]) + (fa[2] + fa[3]);
-          named_bar_sync(1 + ss, kEpiThreads);
-          if (cq == 0) {
-            fv[ss] = ((S.fpart[ss][0][row] + S.fpart[ss][1][row]) + (S.fpart[ss][2][row] + S.fpart[ss][3][row])) + W.b7;
-            if (!a.detect) {
-              const int w = (int)(Tt[ss] / a.tiles_per_wp);
-              const int64_t slot = (Tt[ss] % a.tiles_per_wp) * kTile + row;
-              if (slot < lb) a.values[(int64_t)w * lb + slot] = ((fl >> ss) & 1u) ? fv[ss] : __int_as_float(0x7f800000);
-            }
-          }
-        } else if (p < 11) {
-          // ---- backward: g_{l-1} = D; e_{l-1} = g (.) 1[z_{l-1} > 0] -> A ----
-          const uint32_t m = mks[(10 - p) * kEpiThreads];
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            uint32_t pk[8], rr[16];
-            ld16(tD + 16 * hf, rr);
-            wait_ld();
-            if (tr && hf == 0) tr[(p + 1) * 4 + 0] = clock64();
-#pragma unroll
-            for (int j = 0; j < 16; j += 4) {
-              uint32_t lo, hi;
-              mask_expand(m, (hf * 16 + j) >> 2, lo, hi);
-              pk[j >> 1] = pack2<F16>(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1])) & lo;
-              pk[(j >> 1) + 1] = pack2<F16>(__uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3])) & hi;
-            }
-            st8(tA + 8 * hf, pk);
-          }
-          if (tr) tr[(p + 1) * 4 + 2] = clock64();
-          hand_off(ss);
-          if (tr) tr[(p + 1) * 4 + 3] = clock64();
-          if (p == 6 && cq == 0 && a.detect) {
-            // A6/A7 (overlaps the tensor core): threshold, per-tile slots, per-waypoint min key
-            const int w = (int)(Tt[ss] / a.tiles_per_wp);
-            const int64_t slot = (Tt[ss] % a.tiles_per_wp) * kTile + row;
-            const bool live = (fl >> ss) & 1u;
-            const bool act = live && (fv[ss] - a.delta <= a.tau);
-            const unsigned bal = __ballot_sync(0xffffffffu, act);
-            unsigned long long key = ~0ull;
-            if (live)
-              key = ((unsigned long long)ord_f32(fv[ss]) << 32) |
-                    (unsigned long long)local_to_global(slot, a.scene.rank, a.scene.world);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-              key = other < key ? other : key;
-            }
-            if (lane == 0) {
-              S.act[ss][qd] = bal;
-              S.kmin[ss][qd] = key;
-            }
-            named_bar_sync(3 + ss, 128);
-            if (row == 0) {
-              unsigned long long km = S.kmin[ss][0];
-              int cnt = 0;
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                km = S.kmin[ss][i] < km ? S.kmin[ss][i] : km;
-                cnt += __popc(S.act[ss][i]);
-              }
-              if (km != ~0ull) atomicMin(a.ds.wp_key + w, km);
-              int b0 = 0;
-              if (cnt > 0) {
-                const unsigned long long b = atomicAdd(a.ds.counter, (unsigned long long)cnt);
-                if (b + cnt > (unsigned long long)a.ds.max_active) {
-                  atomicOr(a.ds.counter + 1, 1ull);
-                  b0 = -1;
-                } else {
-                  b0 = (int)b;
-                }
-              }
-              S.sbase[ss] = b0;
-              a.ds.tile_meta[Tt[ss]] = make_int2(b0, cnt);
-            }
-            named_bar_sync(3 + ss, 128);
-            const int b0 = S.sbase[ss];
-            int rk = __popc(bal & ((1u << lane) - 1u));
-            for (int i = 0; i < qd; ++i) rk += __popc(S.act[ss][i]);
-            ridx[ss] = (act && b0 >= 0) ? b0 + rk : -1;
-          }
-          if (p == 7 && cq == 0) prefetch_pt(ss, Tt[ss] + stride);  // lands during 4 phases
-        } else {
-          // ---- g0 = W1^T e1 (16 columns); d f / d q by the chain rule (R3) ----
-          // D is read first; the next tile's layer-1 operands are handed off before the
-          // outputs of this tile are written.
-          uint32_t r[16];
-          if (cq == 0) {
-            ld16(tS, r);
-            wait_ld();
-            cp_async_wait_all();  // this thread's prefetched point of the next tile
-          }
-          if (tr) tr[(p + 1) * 4 + 0] = clock64();
-          const bool live = (fl >> ss) & 1u;
-          const int64_t Tn = Tt[ss] + stride;
-          if (Tn < n_tiles) {
-            const bool ln = stage_a1(ss, Tn);
-            fl = (fl & ~(1u << ss)) | ((uint32_t)ln << ss);
-          }
-          if (tr) tr[(p + 1) * 4 + 2] = clock64();
-          if (cq == 0) {
-            const int w = (int)(Tt[ss] / a.tiles_per_wp);
-            const int64_t slot = (Tt[ss] % a.tiles_per_wp) * kTile + row;
-            float gq[kNdof];
-            gq[0] = a.tgrad ? __uint_as_float(r[3]) : -__uint_as_float(r[0]);
-            gq[1] = a.tgrad ? __uint_as_float(r[4]) : -__uint_as_float(r[1]);
-#pragma unroll
-            for (int i = 0; i < 7; ++i) gq[2 + i] = __uint_as_float(r[5 + i]);
-            if (a.detect) {
-              if (ridx[ss] >= 0) {
-                float4 *dst = reinterpret_cast<float4 *>(a.ds.staging + ridx[ss]);
-                dst[0] = make_float4(fv[ss], gq[0], gq[1], gq[2]);
-                dst[1] = make_float4(gq[3], gq[4], gq[5], gq[6]);
-                dst[2] = make_float4(gq[7], gq[8], __uint_as_float((unsigned)w),
-                                     __uint_as_float((unsigned)local_to_global(slot, a.scene.rank, a.scene.world)));
-              }
-            } else if (a.grads && slot < lb) {
-              float *o = a.grads + ((int64_t)w * lb + slot) * kNdof;
-#pragma unroll
-              for (int i = 0; i < kNdof; ++i) o[i] = live ? gq[i] : 0.f;
-            }
-          }
-          if (tr) tr[(p + 1) * 4 + 3] = clock64();
-          ridx[ss] = -1;
-          Tt[ss] = Tn;
-        }
-      }
-    }
-  }
-#else
   const int s = warp >> 3;          // tile slot
   const int hh = (warp >> 2) & 1;   // accumulator column half: units 64 hh .. 64 hh + 63
   const int qd = warp & 3;          // TMEM lane quarter of this warp (warp % 4)
@@ -593,8 +312,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   // cp.async prefetch of this lane's point of tile TT into S.ptn[s][row] (zero if none);
   // issued by the column-half-0 threads, which alone read it
   auto prefetch_pt = [&](int64_t TT) {
-    const int64_t sl = (TT % a.tiles_per_wp) * kTile + row;
-    const bool ok = TT < n_tiles && sl < lb;
+    int wn = 0;
+    int64_t sl = 0;
+    bool ok = false;
+    if (TT < n_tiles) tile_pair(a, TT, row, wn, sl, ok);
     cp_async16(&S.ptn[s][row], ok ? (const void *)(a.scene.pts + sl) : (const void *)a.scene.pts, ok ? 16u : 0u);
     cp_async_commit();
   };
@@ -602,14 +323,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   // and the split layer-1 operands -> TMEM A (K = 32: half 0 writes K 0..15,
   // half 1 K 16..31), then hand off.  Returns the pair's liveness (meaningful in half 0).
   auto stage_a1 = [&](int64_t TT) -> bool {
-    const int wn = (int)(TT / a.tiles_per_wp);
-    const int64_t sl = (TT % a.tiles_per_wp) * kTile + row;
+    int wn;
+    int64_t sl;
+    bool valid;
+    tile_pair(a, TT, row, wn, sl, valid);
     const float *qw = a.q + (int64_t)wn * kNdof;
     float v[16];
     bool lv = false;
     if (hh == 0) {  // K 0..15: p'_x, p'_y, p_z, theta, j1 (3 each), x_hi of j2
       const float4 pt = S.ptn[s][row];
-      lv = sl < lb && pt.w > 0.f;
+      lv = valid && pt.w > 0.f;
       split3<F16>(pt.x - __ldg(qw), v);
       split3<F16>(pt.y - __ldg(qw + 1), v + 3);
       split3<F16>(pt.z, v + 6);
@@ -741,8 +464,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         if (hh == 0) {
           f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
           if (!a.detect) {
-            const int w = (int)(T / a.tiles_per_wp);
-            const int64_t slot = (T % a.tiles_per_wp) * kTile + row;
+            int w;
+            int64_t slot;
+            bool valid;
+            tile_pair(a, T, row, w, slot, valid);
             if (slot < lb) a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
           }
         }
@@ -774,8 +499,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         if (tr) tr[(p + 1) * 4 + 3] = clock64();
         if (p == 6 && hh == 0 && a.detect) {
           // A6/A7 (overlaps the tensor core): threshold, per-tile slots, per-waypoint min key
-          const int w = (int)(T / a.tiles_per_wp);
-          const int64_t slot = (T % a.tiles_per_wp) * kTile + row;
+          int w;
+          int64_t slot;
+          bool valid;
+          tile_pair(a, T, row, w, slot, valid);
           const bool act = live && (f - a.delta <= a.tau);
           const unsigned bal = __ballot_sync(0xffffffffu, act);
           unsigned long long key = ~0ull;
@@ -835,8 +562,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         if (T + stride < n_tiles) live_n = stage_a1(T + stride);
         if (tr) tr[(p + 1) * 4 + 2] = clock64();
         if (hh == 0) {
-          const int w = (int)(T / a.tiles_per_wp);
-          const int64_t slot = (T % a.tiles_per_wp) * kTile + row;
+          int w;
+          int64_t slot;
+          bool valid;
+          tile_pair(a, T, row, w, slot, valid);
           float gq[kNdof];
           gq[0] = a.tgrad ? __uint_as_float(r[3]) : -__uint_as_float(r[0]);
           gq[1] = a.tgrad ? __uint_as_float(r[4]) : -__uint_as_float(r[1]);
@@ -860,7 +589,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
       }
     }
   }
-#endif
   fence_before();
   __syncthreads();
   fence_after();
@@ -954,7 +682,8 @@ cudaError_t launch_tc_t(const WeightsBF16 &w, const QueryArgs &a, int num_sms, c
   const int smem = (int)sizeof(SmemTC) + 1024;
   cudaError_t e = cudaFuncSetAttribute(k_mlp_tc<F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  const int64_t n_tiles = (int64_t)a.n_wp * a.tiles_per_wp;
+  // a partitioned detect knows its tile count on the device only: one CTA per SM
+  const int64_t n_tiles = a.part.tile_wp ? 2 * (int64_t)num_sms : (int64_t)a.n_wp * a.tiles_per_wp;
   int64_t grid = (n_tiles + 1) / 2;
   if (grid > num_sms) grid = num_sms;
   if (grid < 1) return cudaSuccess;

@@ -26,7 +26,7 @@ REC_BYTES = 48  # sizeof(gcdf_active_t)
 EXPORTED = ["gcdf_default_options", "gcdf_create", "gcdf_destroy", "gcdf_last_error", "gcdf_has_tcgen05",
             "gcdf_workspace_bytes", "gcdf_bind_workspace", "gcdf_load_weights", "gcdf_update_scene",
             "gcdf_scene_info", "gcdf_pairgen_transform", "gcdf_query_values_grads", "gcdf_detect_active_set",
-            "gcdf_detect_active_set_host", "gcdf_compact_dense", "gcdf_merge_active_sets", "gcdf_launch_count", "gcdf_profile_enable",
+            "gcdf_detect_active_set_partitioned", "gcdf_detect_active_set_host", "gcdf_compact_dense", "gcdf_merge_active_sets", "gcdf_launch_count", "gcdf_profile_enable",
             "gcdf_profile_read", "gcdf_selftest_umma", "gcdf_debug_trace"]
 
 
@@ -40,7 +40,7 @@ class GcdfError(RuntimeError):
 class Options(C.Structure):
     _fields_ = [("precision", C.c_int32), ("tgrad_mode", C.c_int32), ("scene_capacity", C.c_int64),
                 ("max_waypoints", C.c_int32), ("max_active", C.c_int64), ("rank", C.c_int32),
-                ("world", C.c_int32)]
+                ("world", C.c_int32), ("max_candidates", C.c_int64)]
 
 
 _lib = None
@@ -72,6 +72,7 @@ def load_library(path: str | Path = LIB_PATH):
     lib.gcdf_query_values_grads.argtypes = [P, P, I32, I32, P, P, P]
     lib.gcdf_detect_active_set.argtypes = [P, P, I32, I32, F, F, P, I64, P, P, P, P, P, P, P]
     lib.gcdf_detect_active_set_host.argtypes = [P, P, I32, I32, F, F, P, I64, P, P, P, P, P]
+    lib.gcdf_detect_active_set_partitioned.argtypes = [P, P, I32, I32, F, F, F, P, I64, P, P, P, P, P, P, P, P]
     lib.gcdf_compact_dense.argtypes = [P, P, P, I32, I64, F, F, P, I64, P, P, P, P, P, P, P]
     lib.gcdf_merge_active_sets.argtypes = [P, I32, I32, P, I64, P, P, P, I64, P, P, P, P, P]
     lib.gcdf_launch_count.argtypes = [P]
@@ -117,7 +118,7 @@ class Context:
 
     def __init__(self, device: int = 0, precision: int = FP16, tgrad_mode: int = TGRAD_CHAINRULE,
                  scene_capacity: int = 1 << 20, max_waypoints: int = 256, max_active: int = 1 << 22,
-                 rank: int = 0, world: int = 1):
+                 rank: int = 0, world: int = 1, max_candidates: int = 0):
         self.lib = load_library()
         if not torch.cuda.is_available():
             raise RuntimeError("libgcdf needs a CUDA device (B200); no CPU path exists")
@@ -126,6 +127,7 @@ class Context:
         self.lib.gcdf_default_options(C.byref(o))
         o.precision, o.tgrad_mode, o.scene_capacity = precision, tgrad_mode, scene_capacity
         o.max_waypoints, o.max_active, o.rank, o.world = max_waypoints, max_active, rank, world
+        o.max_candidates = max_candidates
         self.opts = o
         h = C.c_void_p()
         rc = self.lib.gcdf_create(device, C.byref(o), C.byref(h))
@@ -233,6 +235,27 @@ class Context:
         self._check(self.lib.gcdf_detect_active_set(
             self._h, _ptr(q), B, N, float(delta), float(tau), _ptr(o["records"]), int(o["capacity"]),
             _ptr(o["wp_offsets"]), _ptr(o["wp_min"]), _ptr(o["wp_argmin"]), _ptr(o["wp_key"]), _ptr(o["count"]),
+            C.byref(nh) if sync_count else None, _stream(self.device)))
+        if sync_count:
+            o["n"] = nh.value
+        return o
+
+    def detect_active_set_partitioned(self, q: torch.Tensor, radius: float, delta: float, tau: float,
+                                      capacity: int | None = None, outputs: dict | None = None,
+                                      sync_count: bool = True, part_sizes: bool = True):
+        """NEXT-1 range-partitioned fused detect (pairs within `radius` of each step's base
+        only).  Returns the output dict (+ 'n' when sync_count, + 'part_sizes' [B*N])."""
+        q, B, N = self._q(q)
+        if outputs is None:
+            outputs = self.alloc_detect_outputs(B * N, capacity if capacity is not None else self.max_active)
+        o = outputs
+        if part_sizes and o.get("part_sizes") is None:
+            o["part_sizes"] = torch.empty(B * N, dtype=torch.int64, device=self.device)
+        nh = C.c_int64(-1)
+        self._check(self.lib.gcdf_detect_active_set_partitioned(
+            self._h, _ptr(q), B, N, float(radius), float(delta), float(tau), _ptr(o["records"]), int(o["capacity"]),
+            _ptr(o["wp_offsets"]), _ptr(o["wp_min"]), _ptr(o["wp_argmin"]), _ptr(o["wp_key"]),
+            _ptr(o.get("part_sizes")) if part_sizes else None, _ptr(o["count"]),
             C.byref(nh) if sync_count else None, _stream(self.device)))
         if sync_count:
             o["n"] = nh.value

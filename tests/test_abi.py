@@ -33,7 +33,8 @@ def test_default_options_and_struct_layout(lib):
     lib.gcdf_default_options(C.byref(o))
     assert (o.precision, o.tgrad_mode, o.world, o.rank) == (2, 0, 1, 0)
     assert o.scene_capacity == 1 << 20 and o.max_waypoints == 256 and o.max_active == 1 << 22
-    assert C.sizeof(Options) == 40
+    assert o.max_candidates == 0
+    assert C.sizeof(Options) == 48  # int32, int32, int64, int32 (+4), int64, int32, int32, int64
 
 
 def test_create_without_gpu_fails_cleanly(lib):
