@@ -62,6 +62,7 @@ def _L():
         lib.or_eval.argtypes = [P, P, I64, P, I64, I, P, P, P, P, I]
         lib.or_detect.argtypes = [P, P, P, I64, P, I64, I, D, D, P, P, P, P, I64, C.POINTER(I64),
                                   P, P, P, I]
+        lib.or_sparse_jacobian.argtypes = [P, P, P, I64, D, P, P, P, P]
         lib.or_detect_part.argtypes = [P, P, P, I64, P, I64, I, D, D, D, P, P, P, P, I64, C.POINTER(I64),
                                        P, P, P, P, I]
         lib.or_scene_new.argtypes = [I64, C.POINTER(P)]
@@ -149,6 +150,23 @@ class MLP:
         s = min(n, cap)
         return {"count": n, "value": rf[:s], "grad": rg[:s], "wp": rwp[:s], "pt": rpt[:s],
                 "wp_offsets": off, "wp_min": wmin, "wp_argmin": warg, "part_sizes": psz}
+
+
+def sparse_jacobian(rec: dict, delta: float):
+    """NEXT-2 (Eq. 14-19): constraint vector c = f - delta and the CSR sparse Jacobian of
+    the active records (rec: value [K], grad [K, 9], wp [K] in (wp, pt) order)."""
+    f = np.ascontiguousarray(rec["value"], dtype=np.float64)
+    g = np.ascontiguousarray(rec["grad"], dtype=np.float64).reshape(-1, 9)
+    wp = np.ascontiguousarray(rec["wp"], dtype=np.int64)
+    K = f.shape[0]
+    c = np.empty(K)
+    row_ptr = np.empty(K + 1, dtype=np.int64)
+    col = np.empty(K * 9, dtype=np.int64)
+    val = np.empty(K * 9)
+    rc = _L().or_sparse_jacobian(_p(f), _p(g), _p(wp), K, float(delta), _p(c), _p(row_ptr), _p(col), _p(val))
+    if rc:
+        raise OracleError(rc, "sparse_jacobian")
+    return {"c": c, "row_ptr": row_ptr, "col": col, "val": val}
 
 
 class Scene:

@@ -391,6 +391,29 @@ int or_detect(const omlp_t *m, const double *pts, const int64_t *ids, int64_t M,
                         wp_offsets, wp_min, wp_argmin, NULL, nthreads);
 }
 
+/* ---------------------------------------------------------------- NEXT-2 sparse Jacobian */
+/* Eq. 14-19 for the active constraints, in the records' (wp, pt) order
+   (the step-major order of Eq. 14): c[k] = f_k - delta, and row k of the sparse Jacobian
+   nabla_q c = [nabla_{q_i} c_{q_i} P_i] holds the n = 9 gradient entries of record k at
+   columns 2 n wp_k + t, t = 0..n-1 (Eq. 19 with the reading of DESIGN.md R18: the
+   identity I_n of P_i starts at column 2 n (i - 1) + 1, 1-based, of the 2 N n decision
+   variables; trajectory b's block starts at 2 N n b, i.e. wp = b N + i).  CSR: row_ptr[k]
+   = n k.  rec_wp[count], rec_f[count], rec_g[count][9]. */
+int or_sparse_jacobian(const double *rec_f, const double *rec_g, const int64_t *rec_wp, int64_t count,
+                       double delta, double *c, int64_t *row_ptr, int64_t *col, double *val) {
+  if (count < 0) return OR_ERR_INVALID;
+  for (int64_t k = 0; k < count; ++k) {
+    c[k] = rec_f[k] - delta;
+    row_ptr[k] = (int64_t)OR_NDOF * k;
+    for (int t = 0; t < OR_NDOF; ++t) {
+      col[OR_NDOF * k + t] = 2 * (int64_t)OR_NDOF * rec_wp[k] + t;
+      val[OR_NDOF * k + t] = rec_g[OR_NDOF * k + t];
+    }
+  }
+  row_ptr[count] = (int64_t)OR_NDOF * count;
+  return OR_OK;
+}
+
 /* ---------------------------------------------------------------- scene (O2) */
 /* The oracle's own replay of the id-assignment rule of gcdf_update_scene
    (include/gcdf.h): removals first; ids freed by this call are not reused by

@@ -436,3 +436,42 @@ def test_range_partition_bruteforce_C1():
              if inside[w, j] and F[w, j] - DELTA <= tau]
     assert d["count"] == len(pairs) and [(int(a), int(b)) for a, b in zip(d["wp"], d["pt"])] == pairs
     assert 0 < d["part_sizes"].sum() < inside.size
+
+
+def test_sparse_jacobian_equals_projection_products():
+    """NEXT-2 pin (Eq. 17-19, reading R18): the CSR rows placed by direct
+    memory operations equal the stacked dense products grad_{q_i} c_{q_i} P_i with
+    (P_i)_{r,c} = 1 iff c = r + 2n(i-1) (1-based i), per trajectory block of 2Nn columns;
+    c = f - delta in the records' (step-major, Eq. 14) order."""
+    cfg = synth.get_config("C1")
+    pts, _ = synth.make_scene_points(cfg)
+    q = synth.make_waypoints(cfg).reshape(-1, 9)
+    m = oracle.MLP(synth.weights_path(cfg.H))
+    ids = np.arange(pts.shape[0], dtype=np.int64)
+    tau = synth.load_tau("C1")
+    d = m.detect(pts, ids, q, DELTA, tau)
+    n = 9
+    for B in (1, 2):                       # the 16 steps as 1 x 16 or 2 trajectories x 8
+        N = q.shape[0] // B
+        sj = oracle.sparse_jacobian(d, DELTA)
+        K = d["count"]
+        dense = np.zeros((K, 2 * B * N * n))
+        for k in range(K):
+            for t in range(sj["row_ptr"][k], sj["row_ptr"][k + 1]):
+                dense[k, sj["col"][t]] = sj["val"][t]
+        # the paper's construction, trajectory by trajectory
+        ref = np.zeros_like(dense)
+        for b in range(B):
+            for i in range(1, N + 1):              # 1-based step index as in Eq. 19
+                wp = b * N + (i - 1)
+                rows = np.flatnonzero(d["wp"] == wp)
+                P = np.zeros((n, 2 * N * n))
+                for r in range(n):
+                    P[r, r + 2 * n * (i - 1)] = 1.0
+                block = d["grad"][rows] @ P        # grad_{q_i} c_{q_i} P_i
+                ref[rows, b * 2 * N * n:(b + 1) * 2 * N * n] = block
+        np.testing.assert_array_equal(dense, ref)
+        np.testing.assert_array_equal(sj["c"], d["value"] - DELTA)
+        assert np.array_equal(sj["row_ptr"], np.arange(K + 1) * n)
+        # Eq. 14 order: rows grouped by step, steps ascending
+        assert np.all(np.diff(d["wp"]) >= 0)
