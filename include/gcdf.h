@@ -182,6 +182,17 @@ int gcdf_detect_active_set_partitioned(gcdf_ctx *ctx, const float *q_dev, int32_
                                        int64_t *wp_key_dev, int64_t *part_sizes_dev, int64_t *count_dev,
                                        int64_t *count_host_or_null, void *stream);
 
+/* NEXT-2 (Eq. 14-19; R18): the consumer-side constraint
+   vector and sparse Jacobian of an active set in (wp, pt) order (the output of a detect
+   or merge): c_dev [n] (may be NULL) = f - delta; CSR with n = min(*count_dev, capacity)
+   rows of 9 entries: row_ptr_dev [n+1] = 9 k, col_dev [9n] = 2*9*wp + t (the step's 9
+   configuration columns in a decision vector of 2 n_dof = 18 entries per step, the
+   trajectory blocks of 2*9*N columns back to back since wp = b*N + i), val_dev [9n] =
+   the record's gradient.  Device memory only; the count stays on the device. */
+int gcdf_sparse_jacobian(gcdf_ctx *ctx, const gcdf_active_t *recs_dev, const int64_t *count_dev,
+                         int64_t capacity, float delta, float *c_dev, int64_t *row_ptr_dev, int32_t *col_dev,
+                         float *val_dev, void *stream);
+
 /* Host-buffer form of gcdf_detect_active_set (the end-to-end call): q_host [B][N][9] is
    copied to the device, the fused detect runs, and the results come back to host memory:
    count_host (total active, always written), out_host [out_capacity] (the first

@@ -786,6 +786,17 @@ int gcdf_detect_active_set_partitioned(gcdf_ctx *c, const float *q, int32_t B, i
                        ps.tile_start);
 }
 
+int gcdf_sparse_jacobian(gcdf_ctx *c, const gcdf_active_t *recs, const int64_t *count_dev, int64_t cap,
+                         float delta, float *c_dev, int64_t *row_ptr, int32_t *col, float *val, void *stream) {
+  int rc = precheck(c, false);
+  if (rc) return rc;
+  if (!recs || !count_dev || cap < 0 || !row_ptr || !col || !val || !std::isfinite(delta))
+    return fail(c, GCDF_ERR_INVALID_ARG, "sparse_jacobian: bad arguments");
+  return count_launch(c, launch_sparse_jacobian(recs, count_dev, cap, delta, c_dev, row_ptr, col, val, c->num_sms,
+                                                static_cast<cudaStream_t>(stream)),
+                      "sparse jacobian");
+}
+
 int gcdf_detect_active_set_host(gcdf_ctx *c, const float *q_host, int32_t B, int32_t N, float delta, float tau,
                                 gcdf_active_t *out_host, int64_t cap, int64_t *offs_host, float *wmin_host,
                                 int64_t *warg_host, int64_t *count_host, void *stream) {

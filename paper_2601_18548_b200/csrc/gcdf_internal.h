@@ -135,6 +135,9 @@ cudaError_t launch_selftest_umma(int mode, const float *A, const float *B, float
 cudaError_t launch_compact_dense(const float *values, const float *grads, int64_t stride, int32_t n_wp,
                                  int32_t tiles_per_wp, SceneView scene, float delta, float tau,
                                  DetectScratch ds, cudaStream_t s);
+cudaError_t launch_sparse_jacobian(const gcdf_active_t *recs, const int64_t *count, int64_t cap, float delta,
+                                   float *c, int64_t *row_ptr, int32_t *col, float *val, int num_sms,
+                                   cudaStream_t s);
 // range partition (k_partition.cu).  Grid over this rank's live points, rebuilt on demand.
 struct PartScratch {
   float *grid;            // [8]: ox, oy, inv_cs, cs, radius, nx, ny (as float bits), unused

@@ -238,7 +238,38 @@ __global__ void k_keys_export(const int64_t *__restrict__ skeys, int32_t n_wp, f
   }
 }
 
+// NEXT-2 (Eq. 14-19, reading R18): c[k] = f_k - delta; CSR row k = the 9 gradient entries
+// of record k at columns 2 * 9 * wp_k + t; row_ptr[k] = 9 k.  count read on the device.
+__global__ void __launch_bounds__(256) k_sparse_jacobian(const gcdf_active_t *__restrict__ recs,
+                                                          const int64_t *__restrict__ count_dev, int64_t cap,
+                                                          float delta, float *__restrict__ c,
+                                                          int64_t *__restrict__ row_ptr, int32_t *__restrict__ col,
+                                                          float *__restrict__ val) {
+  const int64_t n = min(*count_dev, cap);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= n; k += (int64_t)gridDim.x * blockDim.x) {
+    row_ptr[k] = (int64_t)kNdof * k;
+    if (k == n) break;
+    const float4 *r = reinterpret_cast<const float4 *>(recs + k);
+    const float4 a = r[0], b = r[1], d = r[2];
+    const float g[kNdof] = {a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y};
+    const int32_t base = 2 * kNdof * (int32_t)__float_as_uint(d.z);
+    if (c) c[k] = a.x - delta;
+#pragma unroll
+    for (int t = 0; t < kNdof; ++t) {
+      col[(int64_t)kNdof * k + t] = base + t;
+      val[(int64_t)kNdof * k + t] = g[t];
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_sparse_jacobian(const gcdf_active_t *recs, const int64_t *count, int64_t cap, float delta,
+                                   float *c, int64_t *row_ptr, int32_t *col, float *val, int num_sms,
+                                   cudaStream_t s) {
+  k_sparse_jacobian<<<num_sms * 4, 256, 0, s>>>(recs, count, cap, delta, c, row_ptr, col, val);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_detect_init(DetectScratch ds, int32_t n_wp, cudaStream_t s) {
   int grid = (n_wp + 255) / 256;

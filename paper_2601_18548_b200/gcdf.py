@@ -26,7 +26,7 @@ REC_BYTES = 48  # sizeof(gcdf_active_t)
 EXPORTED = ["gcdf_default_options", "gcdf_create", "gcdf_destroy", "gcdf_last_error", "gcdf_has_tcgen05",
             "gcdf_workspace_bytes", "gcdf_bind_workspace", "gcdf_load_weights", "gcdf_update_scene",
             "gcdf_scene_info", "gcdf_pairgen_transform", "gcdf_query_values_grads", "gcdf_detect_active_set",
-            "gcdf_detect_active_set_partitioned", "gcdf_detect_active_set_host", "gcdf_compact_dense", "gcdf_merge_active_sets", "gcdf_launch_count", "gcdf_profile_enable",
+            "gcdf_detect_active_set_partitioned", "gcdf_detect_active_set_host", "gcdf_sparse_jacobian", "gcdf_compact_dense", "gcdf_merge_active_sets", "gcdf_launch_count", "gcdf_profile_enable",
             "gcdf_profile_read", "gcdf_selftest_umma", "gcdf_debug_trace"]
 
 
@@ -72,6 +72,7 @@ def load_library(path: str | Path = LIB_PATH):
     lib.gcdf_query_values_grads.argtypes = [P, P, I32, I32, P, P, P]
     lib.gcdf_detect_active_set.argtypes = [P, P, I32, I32, F, F, P, I64, P, P, P, P, P, P, P]
     lib.gcdf_detect_active_set_host.argtypes = [P, P, I32, I32, F, F, P, I64, P, P, P, P, P]
+    lib.gcdf_sparse_jacobian.argtypes = [P, P, P, I64, F, P, P, P, P, P]
     lib.gcdf_detect_active_set_partitioned.argtypes = [P, P, I32, I32, F, F, F, P, I64, P, P, P, P, P, P, P, P]
     lib.gcdf_compact_dense.argtypes = [P, P, P, I32, I64, F, F, P, I64, P, P, P, P, P, P, P]
     lib.gcdf_merge_active_sets.argtypes = [P, I32, I32, P, I64, P, P, P, I64, P, P, P, P, P]
@@ -260,6 +261,20 @@ class Context:
         if sync_count:
             o["n"] = nh.value
         return o
+
+    def sparse_jacobian(self, outputs: dict, delta: float):
+        """NEXT-2: constraint vector c = f - delta and the CSR Jacobian (Eq. 14-19) of a detect
+        result (records in (wp, pt) order; the count is read on the device)."""
+        cap = int(outputs["capacity"])
+        d = self.device
+        r = {"c": torch.empty(cap, dtype=torch.float32, device=d),
+             "row_ptr": torch.empty(cap + 1, dtype=torch.int64, device=d),
+             "col": torch.empty(cap * 9, dtype=torch.int32, device=d),
+             "val": torch.empty(cap * 9, dtype=torch.float32, device=d)}
+        self._check(self.lib.gcdf_sparse_jacobian(self._h, _ptr(outputs["records"]), _ptr(outputs["count"]), cap,
+                                                  float(delta), _ptr(r["c"]), _ptr(r["row_ptr"]), _ptr(r["col"]),
+                                                  _ptr(r["val"]), _stream(d)))
+        return r
 
     @staticmethod
     def alloc_host_outputs(n_wp: int, capacity: int, pinned: bool = True):
