@@ -63,6 +63,7 @@ def _L():
         lib.or_detect.argtypes = [P, P, P, I64, P, I64, I, D, D, P, P, P, P, I64, C.POINTER(I64),
                                   P, P, P, I]
         lib.or_sparse_jacobian.argtypes = [P, P, P, I64, D, P, P, P, P]
+        lib.or_project.argtypes = [P, P, P, P, I64, I64, P]
         lib.or_detect_part.argtypes = [P, P, P, I64, P, I64, I, D, D, D, P, P, P, P, I64, C.POINTER(I64),
                                        P, P, P, P, I]
         lib.or_scene_new.argtypes = [I64, C.POINTER(P)]
@@ -150,6 +151,21 @@ class MLP:
         s = min(n, cap)
         return {"count": n, "value": rf[:s], "grad": rg[:s], "wp": rwp[:s], "pt": rpt[:s],
                 "wp_offsets": off, "wp_min": wmin, "wp_argmin": warg, "part_sizes": psz}
+
+
+def project(f, g, q, minv):
+    """NEXT-3 (Theorem 1.2): q_z = q - f M^{-1} grad_q f for f [W, M], g [W, M, 9], q [W, 9],
+    minv [9] (the diagonal of M^{-1})."""
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    W, M = f.shape
+    g = np.ascontiguousarray(g, dtype=np.float64).reshape(W, M, 9)
+    q = np.ascontiguousarray(q, dtype=np.float64).reshape(W, 9)
+    minv = np.ascontiguousarray(minv, dtype=np.float64).reshape(9)
+    qz = np.empty((W, M, 9))
+    rc = _L().or_project(_p(f), _p(g), _p(q), _p(minv), W, M, _p(qz))
+    if rc:
+        raise OracleError(rc, "project")
+    return qz
 
 
 def sparse_jacobian(rec: dict, delta: float):

@@ -391,6 +391,25 @@ int or_detect(const omlp_t *m, const double *pts, const int64_t *ids, int64_t M,
                         wp_offsets, wp_min, wp_argmin, NULL, nthreads);
 }
 
+/* ---------------------------------------------------------------- NEXT-3 projection */
+/* Theorem 1.2: single-step projection onto the zero level set,
+   q_z = q_0 - lambda d with lambda = f(p, q_0) and d = M^{-1} grad_q f(p, q_0), M diagonal
+   (minv[9] = its inverse diagonal).  f[W][M], g[W][M][9] (from or_eval), q[W][9] ->
+   qz[W][M][9]. */
+int or_project(const double *f, const double *g, const double *q, const double *minv, int64_t W, int64_t M,
+               double *qz) {
+  if (W < 0 || M < 0) return OR_ERR_INVALID;
+  for (int64_t w = 0; w < W; ++w)
+    for (int64_t j = 0; j < M; ++j) {
+      const double lambda = f[w * M + j];
+      for (int t = 0; t < OR_NDOF; ++t) {
+        const double d = minv[t] * g[(w * M + j) * OR_NDOF + t];
+        qz[(w * M + j) * OR_NDOF + t] = q[w * OR_NDOF + t] - lambda * d;
+      }
+    }
+  return OR_OK;
+}
+
 /* ---------------------------------------------------------------- NEXT-2 sparse Jacobian */
 /* Eq. 14-19 for the active constraints, in the records' (wp, pt) order
    (the step-major order of Eq. 14): c[k] = f_k - delta, and row k of the sparse Jacobian

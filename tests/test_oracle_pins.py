@@ -475,3 +475,38 @@ def test_sparse_jacobian_equals_projection_products():
         assert np.array_equal(sj["row_ptr"], np.arange(K + 1) * n)
         # Eq. 14 order: rows grouped by step, steps ascending
         assert np.all(np.diff(d["wp"]) >= 0)
+
+
+def test_single_step_projection_reaches_zero_level_set(tmp_path):
+    """NEXT-3 pin (Theorem 1.2): for a field satisfying the weighted eikonal
+    equation ||grad_q f||_{M^-1} = 1 -- here a linear (identity-activation) network whose
+    output layer is scaled to unit M^-1-norm gradient -- one step q_z = q - f M^-1 grad f
+    lands on the zero level set: f(p, q_z) = 0.  With M = I and a unit gradient the step is
+    q - f grad f; the projection is the plain formula on random fields too."""
+    rng = np.random.default_rng(9)
+    dims = [12, 9, 7, 8, 6, 5, 4, 1]
+    layers = [(rng.normal(size=(dims[i + 1], dims[i])), rng.normal(size=dims[i + 1])) for i in range(7)]
+    minv = rng.uniform(0.2, 3.0, 9)
+    for mv in (minv, np.ones(9)):
+        m0 = oracle.MLP(_write(tmp_path, "lin0.mlpw", 0, dims, layers))
+        pts, q = _rand_inputs(rng, 7, 5)
+        g = m0.eval(pts, q)["g"][0, 0]                    # constant gradient of a linear field
+        s = 1.0 / np.sqrt(g @ (mv * g))                  # ||s g||_{M^-1} = 1
+        scaled = layers[:-1] + [(layers[-1][0] * s, layers[-1][1] * s)]
+        m = oracle.MLP(_write(tmp_path, "lin.mlpw", 0, dims, scaled))
+        out = m.eval(pts, q)
+        np.testing.assert_allclose(np.einsum("wjt,t,wjt->wj", out["g"], mv, out["g"]), 1.0, rtol=1e-12)
+        qz = oracle.project(out["f"], out["g"], q, mv)
+        for w in range(q.shape[0]):
+            fz = m.eval(pts, qz[w])["f"]                  # f(p_j, q_z[w, j]) on the diagonal
+            np.testing.assert_allclose(np.diag(fz), 0.0, atol=1e-10)
+    # random ReLU field: the formula itself, component by component
+    act, dims2, layers2 = synth.make_weights(32, seed=4)
+    m2 = oracle.MLP(_write(tmp_path, "r.mlpw", act, dims2, layers2))
+    pts, q = _rand_inputs(rng, 6, 3)
+    out = m2.eval(pts, q)
+    qz = oracle.project(out["f"], out["g"], q, minv)
+    for w in range(q.shape[0]):
+        for j in range(pts.shape[0]):
+            for t in range(9):
+                assert qz[w, j, t] == q[w, t] - out["f"][w, j] * (minv[t] * out["g"][w, j, t])
