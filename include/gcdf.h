@@ -150,6 +150,13 @@ int gcdf_pairgen_transform(gcdf_ctx *ctx, const float *q_dev, int32_t B, int32_t
 int gcdf_query_values_grads(gcdf_ctx *ctx, const float *q_dev, int32_t B, int32_t N, float *values_dev,
                             float *grads_dev, void *stream);
 
+/* NEXT-3 (Theorem 1.2): batched single-step projection onto the zero
+   level set, fused into the dense query: qz_dev [B*N][local_bound][9] receives
+   q_z = q - f(p, q) M^{-1} grad_q f(p, q) for every pair (0 for dead slots), values_dev as
+   in gcdf_query_values_grads; minv_host [9] = the diagonal of M^{-1} (finite, >= 0). */
+int gcdf_project_dense(gcdf_ctx *ctx, const float *q_dev, int32_t B, int32_t N, const float *minv_host,
+                       float *values_dev, float *qz_dev, void *stream);
+
 /* A2-A8 fused: query + threshold + per-waypoint min + stream compaction.
    out_dev [out_capacity] records in (wp, pt) order; wp_offsets_dev [B*N+1] (Eq. 14
    block structure); wp_min_dev [B*N] (+INF if no live point);

@@ -698,6 +698,24 @@ int gcdf_query_values_grads(gcdf_ctx *c, const float *q, int32_t B, int32_t N, f
   return count_launch(c, run_mlp(c, a, static_cast<cudaStream_t>(stream)), "query kernel");
 }
 
+int gcdf_project_dense(gcdf_ctx *c, const float *q, int32_t B, int32_t N, const float *minv_host, float *values,
+                       float *qz, void *stream) {
+  int rc = precheck(c);
+  if (rc) return rc;
+  if ((rc = check_wp(c, q, B, N))) return rc;
+  if (!values || !qz || !minv_host) return fail(c, GCDF_ERR_INVALID_ARG, "project: null argument");
+  for (int i = 0; i < kNdof; ++i)
+    if (!std::isfinite(minv_host[i]) || minv_host[i] < 0.f)
+      return fail(c, GCDF_ERR_INVALID_ARG, "project: M^-1 diagonal must be finite and >= 0");
+  QueryArgs a = make_args(c, q, B * N);
+  a.values = values;
+  a.grads = qz;
+  a.detect = 0;
+  a.project = 1;
+  for (int i = 0; i < kNdof; ++i) a.minv[i] = minv_host[i];
+  return count_launch(c, run_mlp(c, a, static_cast<cudaStream_t>(stream)), "project kernel");
+}
+
 static int finish_detect(gcdf_ctx *c, int32_t nwp, int32_t tpw, gcdf_active_t *out, int64_t cap, int64_t *offs,
                          float *wmin, int64_t *warg, int64_t *wkey, int64_t *count_dev, int64_t *count_host,
                          cudaStream_t s, const int64_t *tile_start = nullptr) {

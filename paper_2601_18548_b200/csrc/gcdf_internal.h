@@ -85,7 +85,10 @@ struct QueryArgs {
   int32_t tgrad;                   // gcdf_tgrad
   // dense outputs (query) -- NULL in detect mode
   float *values;
-  float *grads;
+  float *grads;                    // (project: the projected configurations q_z instead)
+  // NEXT-3 single-step projection (Theorem 1.2): q_z = q - f M^{-1} grad_q f, M diagonal
+  int32_t project;
+  float minv[kNdof];
   // detect mode
   int32_t detect;
   float delta, tau;

@@ -341,7 +341,10 @@ __global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const Q
         const int64_t gbase = ((int64_t)w * lb + slot0) * kNdof;
         for (int idx = tid; idx < kTile * kNdof; idx += 256) {
           const int p = idx / kNdof;
-          if (slot0 + p < lb) a.grads[gbase + idx] = sp[p].w > 0.f ? gst[idx] : 0.f;
+          const int k = idx - p * kNdof;
+          // (NEXT-3 projection: q_z = q - f M^{-1} grad_q f, Theorem 1.2)
+          const float o = a.project ? qv[k] - (fval[p] * gst[idx]) * a.minv[k] : gst[idx];
+          if (slot0 + p < lb) a.grads[gbase + idx] = sp[p].w > 0.f ? o : 0.f;
         }
       }
     } else if (tid < kTile) {

@@ -581,8 +581,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
             }
           } else if (a.grads && slot < lb) {
             float *o = a.grads + ((int64_t)w * lb + slot) * kNdof;
+            if (a.project) {  // NEXT-3: q_z = q - f M^{-1} grad_q f (Theorem 1.2)
+              const float *qw = a.q + (int64_t)w * kNdof;
 #pragma unroll
-            for (int i = 0; i < kNdof; ++i) o[i] = live ? gq[i] : 0.f;
+              for (int i = 0; i < kNdof; ++i) o[i] = live ? __ldg(qw + i) - (f * gq[i]) * a.minv[i] : 0.f;
+            } else {
+#pragma unroll
+              for (int i = 0; i < kNdof; ++i) o[i] = live ? gq[i] : 0.f;
+            }
           }
         }
         if (tr) tr[(p + 1) * 4 + 3] = clock64();

@@ -26,7 +26,8 @@ REC_BYTES = 48  # sizeof(gcdf_active_t)
 EXPORTED = ["gcdf_default_options", "gcdf_create", "gcdf_destroy", "gcdf_last_error", "gcdf_has_tcgen05",
             "gcdf_workspace_bytes", "gcdf_bind_workspace", "gcdf_load_weights", "gcdf_update_scene",
             "gcdf_scene_info", "gcdf_pairgen_transform", "gcdf_query_values_grads", "gcdf_detect_active_set",
-            "gcdf_detect_active_set_partitioned", "gcdf_detect_active_set_host", "gcdf_sparse_jacobian", "gcdf_compact_dense", "gcdf_merge_active_sets", "gcdf_launch_count", "gcdf_profile_enable",
+            "gcdf_detect_active_set_partitioned", "gcdf_detect_active_set_host", "gcdf_sparse_jacobian",
+            "gcdf_project_dense", "gcdf_compact_dense", "gcdf_merge_active_sets", "gcdf_launch_count", "gcdf_profile_enable",
             "gcdf_profile_read", "gcdf_selftest_umma", "gcdf_debug_trace"]
 
 
@@ -73,6 +74,7 @@ def load_library(path: str | Path = LIB_PATH):
     lib.gcdf_detect_active_set.argtypes = [P, P, I32, I32, F, F, P, I64, P, P, P, P, P, P, P]
     lib.gcdf_detect_active_set_host.argtypes = [P, P, I32, I32, F, F, P, I64, P, P, P, P, P]
     lib.gcdf_sparse_jacobian.argtypes = [P, P, P, I64, F, P, P, P, P, P]
+    lib.gcdf_project_dense.argtypes = [P, P, I32, I32, P, P, P, P]
     lib.gcdf_detect_active_set_partitioned.argtypes = [P, P, I32, I32, F, F, F, P, I64, P, P, P, P, P, P, P, P]
     lib.gcdf_compact_dense.argtypes = [P, P, P, I32, I64, F, F, P, I64, P, P, P, P, P, P, P]
     lib.gcdf_merge_active_sets.argtypes = [P, I32, I32, P, I64, P, P, P, I64, P, P, P, P, P]
@@ -261,6 +263,17 @@ class Context:
         if sync_count:
             o["n"] = nh.value
         return o
+
+    def project_dense(self, q: torch.Tensor, minv_diag):
+        """NEXT-3: values [B*N, lb] and q_z = q - f M^{-1} grad f [B*N, lb, 9] for every pair."""
+        q, B, N = self._q(q)
+        lb = self.scene_info()["local_bound"]
+        values = torch.empty((B * N, lb), dtype=torch.float32, device=self.device)
+        qz = torch.empty((B * N, lb, 9), dtype=torch.float32, device=self.device)
+        m = (C.c_float * 9)(*[float(x) for x in np.asarray(minv_diag, dtype=np.float64).ravel()])
+        self._check(self.lib.gcdf_project_dense(self._h, _ptr(q), B, N, m, _ptr(values), _ptr(qz),
+                                                _stream(self.device)))
+        return values, qz
 
     def sparse_jacobian(self, outputs: dict, delta: float):
         """NEXT-2: constraint vector c = f - delta and the CSR Jacobian (Eq. 14-19) of a detect

@@ -43,3 +43,46 @@ def test_sparse_jacobian_matches_oracle_definition(prec, partitioned):
     np.testing.assert_array_equal(sj["val"][: 9 * n].cpu().numpy(), ref["val"].astype(np.float32))
     # c = f - delta, evaluated in fp32 on the device
     np.testing.assert_array_equal(sj["c"][:n].cpu().numpy(), rec["value"] - np.float32(DELTA))
+
+
+@pytest.mark.parametrize("prec", [0, 2])
+def test_projection_fused_matches_formula_and_oracle(prec):
+    """NEXT-3: the fused projection equals q - f M^-1 grad f of the same kernel's dense
+    query (tight: only the three fp32 operations differ from f64), and the oracle's
+    projection within the path's value/gradient tolerances."""
+    from gpu_util import oracle_mlp
+    cfg = synth.get_config("C2")
+    pts, _ = synth.make_scene_points(cfg)
+    q = synth.make_waypoints(cfg)[:, :4]
+    ctx = _ctx(cfg, prec)
+    ids = ctx.update_scene(pts)
+    qt = torch.from_numpy(q)
+    minv = np.random.default_rng(3).uniform(0.2, 3.0, 9)
+    v, qz = ctx.project_dense(qt, minv)
+    v2, g2 = ctx.query_values_grads(qt)
+    torch.cuda.synchronize()
+    v, qz, v2, g2 = (x.cpu().numpy() for x in (v, qz, v2, g2))
+    np.testing.assert_array_equal(v, v2)
+    Q = q.reshape(-1, 9)
+    live = np.isfinite(v)
+    f64 = np.where(live, v2, 0.0).astype(np.float64)   # dead slots hold +INF
+    want = Q[:, None, :].astype(np.float64) - f64[..., None] * (minv * g2.astype(np.float64))
+    err = np.abs(qz - want)[live]
+    scale = np.abs(Q[:, None, :]).repeat(v.shape[1], 1)[live] + np.abs(f64[..., None] * minv * g2)[live]
+    assert np.all(err <= 1e-6 * scale + 1e-6), err.max()
+    assert np.all(qz[~live] == 0.0)
+    # vs the float64 oracle on a sample of pairs
+    m = oracle_mlp(cfg)
+    rng = np.random.default_rng(8)
+    psel = np.sort(rng.choice(len(pts), 512, replace=False))
+    ex = m.eval(pts[psel], Q, want_kappa=True)
+    oz = oracle.project(ex["f"], ex["g"], Q, minv)
+    gz = qz[:, ids[psel]]
+    if prec == 0:   # fp32 path: allclose on pairs away from ReLU kinks
+        ok = ex["kappa"] > 1e-4
+        d = np.abs(gz - oz)[ok]
+        assert np.all(d <= 1e-4 * (np.abs(oz[ok]) + np.abs((ex["f"][..., None] * minv * ex["g"]))[ok]) + 1e-5)
+    else:           # tensor path: |f| error <= 2e-2 and the gradient-norm gate bound the step
+        dz = np.linalg.norm(gz - oz, axis=-1)
+        step = np.abs(ex["f"]) * np.linalg.norm(minv * ex["g"], axis=-1)
+        assert np.median(dz / (step + 1e-3)) < 0.05
