@@ -892,7 +892,7 @@ int gcdf_debug_trace(gcdf_ctx *c, long long *trace_dev) {
 
 int gcdf_selftest_umma(int dev, int mode, const float *A, const float *B, float *D, void *stream) {
   if (!tc_compiled()) return GCDF_ERR_UNSUPPORTED;
-  if (mode < 0 || (mode < 16 && (mode > 6 || (mode & 3) > 2)) || mode > 71 || !A || !B || !D) return GCDF_ERR_INVALID_ARG;
+  if (mode < 0 || (mode < 16 && (mode > 6 || (mode & 3) > 2)) || mode > 75 || !A || !B || !D) return GCDF_ERR_INVALID_ARG;
   if (cudaSetDevice(dev) != cudaSuccess) return GCDF_ERR_CUDA;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (launch_selftest_umma(mode, A, B, D, s) != cudaSuccess) return GCDF_ERR_CUDA;

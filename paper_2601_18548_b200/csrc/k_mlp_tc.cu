@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
 #if GCDF_TC_NOEPI
       // timing experiment only: no epilogue work (2: only the TMEM loads; results are garbage)
       if (p < 11) {
-        if (GCDF_TC_NOEPI == 2) {
+        if (GCDF_TC_NOEPI == 2) {  // 4 x (ld16 + wait)
           uint32_t acc = 0u;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -393,6 +393,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
 #pragma unroll
             for (int j = 0; j < 16; ++j) acc += rr[j];
           }
+          if (acc == 0x12345678u) a.trace[0] = acc;
+        } else if (GCDF_TC_NOEPI == 3) {  // 2 x (ld32 + wait)
+          uint32_t acc = 0u;
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint32_t rr[32];
+            ld32(tD + 32 * c, rr);
+            wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc += rr[j];
+          }
+          if (acc == 0x12345678u) a.trace[0] = acc;
+        } else if (GCDF_TC_NOEPI == 4) {  // 4 x ld16, one wait
+          uint32_t r0[16], r1[16], r2[16], r3[16];
+          ld16(tD, r0);
+          ld16(tD + 16, r1);
+          ld16(tD + 32, r2);
+          ld16(tD + 48, r3);
+          wait_ld();
+          uint32_t acc = 0u;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc += r0[j] + r1[j] + r2[j] + r3[j];
           if (acc == 0x12345678u) a.trace[0] = acc;
         }
         if (tr) tr[(p + 1) * 4 + 2] = clock64();
@@ -841,6 +863,15 @@ __global__ void __launch_bounds__(128, 1) k_mma_probe(int variant, int reps, flo
           fence_after();
         }
         n = reps * 9;
+      } else if (variant == 28 || variant == 29) {  // lean M = 64 (28: one D; 29: two D at lanes 0 / 64 alternating)
+        const uint32_t id64 = idesc_f16kind(64, 128, false, F16);
+#pragma unroll 1
+        for (int r = 0; r < reps; ++r) {
+          const uint32_t dd = (variant == 29 && (r & 1)) ? d0 + (64u << 16) : d0;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) mma_ts(dd, av + 8u * k, bd[k], id64, k > 0);
+        }
+        n = reps * 8;
       } else if (variant == 25) {  // lean N = 64 (two halves of a phase as separate accumulators)
         uint64_t b64[8];
 #pragma unroll
@@ -1082,7 +1113,7 @@ cudaError_t launch_selftest_umma(int mode, const float *A, const float *B, float
     k<<<2, 128, smem, s>>>(variant, 200, D);
     return cudaGetLastError();
   }
-  if (mode >= 16 + 2 * 26) {  // sub-partition interference probe (variants 26, 27)
+  if (mode >= 16 + 2 * 26 && mode < 16 + 2 * 28) {  // sub-partition interference probe (variants 26, 27)
     const int variant = (mode - 16) >> 1;
     const bool f16 = (mode & 1) != 0;
     const int smem = 64 * 1024 + 1024;

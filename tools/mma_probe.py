@@ -11,6 +11,7 @@ names = ["TS K-major N128", "TS MN-major N128", "TS N128 two accumulators", "SS 
          "2CTA TS M256 N128", "2CTA SS M256 N128", "2CTA TS M256 N256", "TS N64", "TS N64 two acc interleaved",
          "TS N16", "TS N128 two acc k-interleaved", "TS N128 + nosw bias step", "TS K-major N128 lean issue",
          "TS MN-major N128 lean issue", "lean, all 148 SMs busy", "lean + 3 warps tcgen05.ld", "lean + 3 warps tcgen05.st", "lean, random operands", "lean kernel fwd phase (8 + bias)", "lean, two slots alternating", "lean fwd phase + commit each", "lean fwd phase + commit + wait", "two issuers, commit each", "lean fwd phase + commit + spin", "lean N64"]
+LEAN_M64 = [(28, "lean M64 N128"), (29, "lean M64 N128, D at lanes 0/64 alternating")]
 NS = [128] * 4 + [256, 128, 128, 256, 64, 64, 16] + [128] * 14 + [64]
 A = torch.zeros(128, 128, device="cuda")
 for v, name in enumerate(names):
@@ -27,3 +28,8 @@ for v, name in ((26, "with UMMA stream"), (27, "without")):
     D = selftest_umma(16 + 2 * v + 1, A, A)
     print(f"ALU loop {name:18s}: warp 4 (same SMSP as issuer) {D[0, 0].item():9.0f} cyc, warp 5 {D[0, 1].item():9.0f} cyc,"
           f" UMMA stream {D[0, 2].item():9.0f} cyc")
+
+for v, name in LEAN_M64:
+    D = selftest_umma(16 + 2 * v + 1, A, A)
+    cyc, n = D[0, 0].item(), D[0, 1].item()
+    print(f"{name:40s} fp16: {cyc / n:7.1f} cycles/MMA (ideal 32 at the dense rate)")
