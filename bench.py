@@ -180,9 +180,9 @@ def main():
     torch.cuda.set_device(dev)
     lib = load_library()
     prec = a.precision
-    if prec == "auto":
-        prec = "fp16" if lib.gcdf_has_tcgen05() else "fp32"
     cfg = synth.get_config(a.config)
+    if prec == "auto":  # the tensor-core path needs H = 128 (C1's H = 32 net runs on the fp32 path)
+        prec = "fp16" if lib.gcdf_has_tcgen05() and cfg.H == 128 else "fp32"
     tau = synth.load_tau(cfg.name)
     delta = synth.inputs.DELTA
     pts, boxes = synth.make_scene_points(cfg)
