@@ -33,7 +33,7 @@ inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 struct Layout {
   int64_t pts, wf32, wbf16, wf16, meta, staging, wp_key, wp_count, counter, upd_payload, upd_slots;
   int64_t h_q, h_out, h_offs, h_wmin, h_warg, h_count;
-  int64_t p_grid, p_bbox, p_cell_count, p_cell_start, p_cell_fill, p_cell_items, p_bitmap, p_chunk_cnt, p_chunk_off,
+  int64_t p_grid, p_bbox, p_cell_count, p_cell_start, p_cell_fill, p_cell_items, p_cell_xy, p_bitmap, p_chunk_cnt, p_chunk_off,
       p_scan_tmp, p_cand, p_cand_start, p_cand_count, p_tile_start, p_tile_wp, p_n_tiles, p_words, p_nchunk;
   int64_t total;
   int64_t wf32_bytes, wbf16_bytes;
@@ -174,6 +174,7 @@ PartScratch part_view(const gcdf_ctx *c) {
   p.cell_start = reinterpret_cast<int64_t *>(c->ws + L.p_cell_start);
   p.cell_fill = reinterpret_cast<int32_t *>(c->ws + L.p_cell_fill);
   p.cell_items = reinterpret_cast<int32_t *>(c->ws + L.p_cell_items);
+  p.cell_xy = reinterpret_cast<float2 *>(c->ws + L.p_cell_xy);
   p.bitmap = reinterpret_cast<uint32_t *>(c->ws + L.p_bitmap);
   p.words = L.p_words;
   p.chunk_cnt = reinterpret_cast<int32_t *>(c->ws + L.p_chunk_cnt);
@@ -332,7 +333,7 @@ int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out) {
   L.meta = off; off = align256(off + (int64_t)o.max_waypoints * c->tiles_cap * 8);
   L.staging = off; off = align256(off + o.max_active * (int64_t)sizeof(gcdf_active_t));
   L.wp_key = off; off = align256(off + (int64_t)o.max_waypoints * 8);
-  L.wp_count = off; off = align256(off + (int64_t)o.max_waypoints * 8);
+  L.wp_count = off; off = align256(off + finalize_scratch_elems(o.max_waypoints, c->tiles_cap) * 8);
   L.counter = off; off = align256(off + 16);
   L.upd_payload = off; off = align256(off + kUpdChunk * 16);
   L.upd_slots = off; off = align256(off + kUpdChunk * 8);
@@ -355,6 +356,7 @@ int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out) {
     L.p_cell_start = off; off = align256(off + (kPartMaxCells + 1) * 8);
     L.p_cell_fill = off; off = align256(off + kPartMaxCells * 4);
     L.p_cell_items = off; off = align256(off + c->local_cap * 4);
+    L.p_cell_xy = off; off = align256(off + c->local_cap * 8);
     L.p_bitmap = off; off = align256(off + W * L.p_words * 4);
     L.p_chunk_cnt = off; off = align256(off + W * L.p_nchunk * 4);
     L.p_chunk_off = off; off = align256(off + (W * L.p_nchunk + 1) * 8);
@@ -716,18 +718,28 @@ int gcdf_project_dense(gcdf_ctx *c, const float *q, int32_t B, int32_t N, const 
   return count_launch(c, run_mlp(c, a, static_cast<cudaStream_t>(stream)), "project kernel");
 }
 
+static int read_count(gcdf_ctx *c, int64_t cap, const int64_t *count_dev, int64_t *count_host, cudaStream_t s);
+
 static int finish_detect(gcdf_ctx *c, int32_t nwp, int32_t tpw, gcdf_active_t *out, int64_t cap, int64_t *offs,
                          float *wmin, int64_t *warg, int64_t *wkey, int64_t *count_dev, int64_t *count_host,
                          cudaStream_t s, const int64_t *tile_start = nullptr) {
   DetectScratch ds = scratch_view(c);
   int nl = 0;
-  cudaError_t e = launch_finalize(ds, nwp, tpw, tile_start, out, cap, offs, wmin, warg, wkey, count_dev,
-                                  reinterpret_cast<int64_t *>(c->ws + c->L.wp_count), s, &nl);
+  cudaError_t e = launch_finalize(ds, nwp, tpw, tile_start, c->tiles_cap, out, cap, offs, wmin, warg, wkey,
+                                  count_dev, reinterpret_cast<int64_t *>(c->ws + c->L.wp_count), s, &nl);
   int rc = count_launch(c, e, "detect finalize", nl);
   if (rc) return rc;
+  return read_count(c, cap, count_dev, count_host, s);
+}
+
+// count_host (if non-NULL): synchronize, read the active count, CAPACITY if it exceeds the
+// output capacity or the staging overflowed
+static int read_count(gcdf_ctx *c, int64_t cap, const int64_t *count_dev, int64_t *count_host, cudaStream_t s) {
+  DetectScratch ds = scratch_view(c);
   if (count_host) {
     unsigned long long hc[2];
-    CK(c, cudaMemcpyAsync(hc, ds.counter, 16, cudaMemcpyDeviceToHost, s), "count D2H");
+    CK(c, cudaMemcpyAsync(hc, count_dev, 8, cudaMemcpyDeviceToHost, s), "count D2H");
+    CK(c, cudaMemcpyAsync(hc + 1, ds.counter + 1, 8, cudaMemcpyDeviceToHost, s), "overflow D2H");
     CK(c, cudaStreamSynchronize(s), "detect sync");
     *count_host = (int64_t)hc[0];
     if (hc[1] || (int64_t)hc[0] > cap)
@@ -865,10 +877,15 @@ int gcdf_compact_dense(gcdf_ctx *c, const float *values, const float *grads, int
   DetectScratch ds = scratch_view(c);
   const int32_t tpw = (int32_t)(sv.local_bound / kTile);
   if ((rc = count_launch(c, launch_detect_init(ds, n_wp, s), "compact init"))) return rc;
-  if ((rc = count_launch(c, launch_compact_dense(values, grads, stride, n_wp, tpw, sv, delta, tau, ds, s),
-                         "compact kernel")))
+  int nl = 0;
+  if ((rc = count_launch(c,
+                         launch_compact_dense(values, grads, stride, n_wp, tpw, sv, delta, tau, ds, out, cap, offs,
+                                              wmin, warg, wkey, count_dev,
+                                              reinterpret_cast<int64_t *>(c->ws + c->L.wp_count), s, &nl),
+                         "compact kernels", 0)))
     return rc;
-  return finish_detect(c, n_wp, tpw, out, cap, offs, wmin, warg, wkey, count_dev, count_host, s);
+  c->launches += nl;
+  return read_count(c, cap, count_dev, count_host, s);
 }
 
 int gcdf_merge_active_sets(gcdf_ctx *c, int32_t world, int32_t n_wp, const gcdf_active_t *recs, int64_t rec_stride,

@@ -135,9 +135,12 @@ cudaError_t launch_mlp_simt(int H, const WeightsF32 &w, const QueryArgs &a, int 
 cudaError_t launch_mlp_tc(int H, bool f16, const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
 bool tc_compiled();
 cudaError_t launch_selftest_umma(int mode, const float *A, const float *B, float *D, cudaStream_t s);
+// standalone A6-A8 over dense values (two passes; writes the ordered output directly)
 cudaError_t launch_compact_dense(const float *values, const float *grads, int64_t stride, int32_t n_wp,
                                  int32_t tiles_per_wp, SceneView scene, float delta, float tau,
-                                 DetectScratch ds, cudaStream_t s);
+                                 DetectScratch ds, gcdf_active_t *out, int64_t out_capacity, int64_t *wp_offsets,
+                                 float *wp_min, int64_t *wp_argmin, int64_t *wp_key, int64_t *count,
+                                 int64_t *fin_scratch, cudaStream_t s, int *n_launches);
 cudaError_t launch_sparse_jacobian(const gcdf_active_t *recs, const int64_t *count, int64_t cap, float delta,
                                    float *c, int64_t *row_ptr, int32_t *col, float *val, int num_sms,
                                    cudaStream_t s);
@@ -148,7 +151,8 @@ struct PartScratch {
   int32_t *cell_count;    // [kPartMaxCells]
   int64_t *cell_start;    // [kPartMaxCells + 1]
   int32_t *cell_fill;     // [kPartMaxCells]
-  int32_t *cell_items;    // [local_cap]
+  int32_t *cell_items;    // [local_cap] slots sorted by cell
+  float2 *cell_xy;        // [local_cap] their planar coordinates
   uint32_t *bitmap;       // [max_wp][words]
   int64_t words;          // local_cap / 32
   int32_t *chunk_cnt;     // [max_wp * nchunk]
@@ -171,12 +175,13 @@ cudaError_t launch_part_grid(const float4 *pts, int64_t local_bound, float radiu
 cudaError_t launch_part_build(const float4 *pts, const float *q, int32_t n_wp, float radius, PartScratch ps,
                               unsigned long long *overflow_flag, cudaStream_t s, int *n_launches);
 // finalize: tile counts -> wp_offsets, ordered copy staging -> out, wp_min/argmin/key, count
-// (tile_start: per-step tile ranges of a partitioned detect, nullptr = tiles_per_wp per step)
+// (tile_start: per-step tile ranges of a partitioned detect with at most max_tiles_per_wp
+// tiles per step; nullptr = tiles_per_wp per step).  fin_scratch: finalize_scratch_elems().
 cudaError_t launch_finalize(DetectScratch ds, int32_t n_wp, int32_t tiles_per_wp, const int64_t *tile_start,
-                            gcdf_active_t *out,
-                            int64_t out_capacity, int64_t *wp_offsets, float *wp_min, int64_t *wp_argmin,
-                            int64_t *wp_key, int64_t *count, int64_t *wp_count_scratch, cudaStream_t s,
-                            int *n_launches);
+                            int64_t max_tiles_per_wp, gcdf_active_t *out, int64_t out_capacity, int64_t *wp_offsets,
+                            float *wp_min, int64_t *wp_argmin, int64_t *wp_key, int64_t *count, int64_t *fin_scratch,
+                            cudaStream_t s, int *n_launches);
+int64_t finalize_scratch_elems(int64_t max_wp, int64_t max_tiles_per_wp);
 cudaError_t launch_merge(int32_t world, int32_t n_wp, const gcdf_active_t *recs, int64_t rec_stride,
                          const int64_t *offsets, const int64_t *wp_key, gcdf_active_t *out,
                          int64_t out_capacity, int64_t *wp_offsets, float *wp_min, int64_t *wp_argmin,

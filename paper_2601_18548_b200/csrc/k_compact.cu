@@ -7,6 +7,8 @@
 //
 // Min keys: key = ord(f) << 32 | pt, ord() order-preserving float -> uint32, so the
 // unsigned minimum is (min f, smallest id on ties) -- one atomicMin per tile.
+#include <algorithm>
+
 #include "gcdf_internal.h"
 #include "k_scan.cuh"
 
@@ -32,149 +34,187 @@ __global__ void k_detect_init(unsigned long long *wp_key, unsigned long long *co
 // order by a warp prefix scan of per-lane counts (the "warp-ballot and prefix-sum"
 // compaction); the per-waypoint min key is a warp-shuffle min + one atomicMin per tile.
 // A value of +INF marks a dead slot (gcdf_query_values_grads writes +INF there).
-__global__ void __launch_bounds__(256) k_compact_dense(const float *__restrict__ values,
-                                                      const float *__restrict__ grads, int64_t stride,
-                                                      int32_t n_wp, int32_t tpw, SceneView scene, float delta,
-                                                      float tau, DetectScratch ds) {
+// ---- standalone K3 (A6-A8 over dense values): two passes, no staging and no global counter.
+// Pass 1: a warp takes kGroup consecutive tiles (128 slots, 4 per lane, float4 streaming
+// loads all in flight), writes each tile's active count to tile_meta and folds the
+// per-waypoint minimum key (one atomicMin per waypoint run in the group).  The chunk scan
+// of the finalize turns the counts into output offsets; pass 2 re-reads the values of the
+// tiles with records and writes the records straight to their final positions.
+constexpr int kGroup = 8;
+
+// values of tile tw (0-based within step w) for this lane's 4 slots (+INF outside the scene)
+__device__ __forceinline__ float4 load_tile_values(const float *__restrict__ values, int64_t stride, int64_t lb,
+                                                   int w, int64_t tw, int lane, int64_t &slot0) {
+  slot0 = tw * kTile + 4 * lane;
+  const float *vrow = values + (int64_t)w * stride;
+  const float inf = __int_as_float(0x7f800000);
+  float4 v = make_float4(inf, inf, inf, inf);
+  if (slot0 + 3 < lb) {
+    v = __ldcs(reinterpret_cast<const float4 *>(vrow + slot0));
+  } else {
+    float *pv = reinterpret_cast<float *>(&v);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) if (slot0 + k < lb) pv[k] = vrow[slot0 + k];
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(256) k_compact_count(const float *__restrict__ values, int64_t stride, int32_t n_wp,
+                                                       int32_t tpw, SceneView scene, float delta, float tau,
+                                                       DetectScratch ds) {
   const int lane = threadIdx.x & 31;
   const int64_t n_tiles = (int64_t)n_wp * tpw;
-  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t n_groups = (n_tiles + kGroup - 1) / kGroup;
+  // each warp takes a contiguous range of groups, so it stays on one step for long runs and
+  // folds the step's minimum key locally (atomicMin only when the step changes)
+  const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t per = (n_groups + n_warps - 1) / n_warps;
+  const int64_t G0 = gw * per, G1 = min(G0 + per, n_groups);
+  if (G0 >= G1) return;
   const int64_t lb = scene.local_bound;
-  for (int64_t T = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); T < n_tiles; T += wstride) {
-    const int w = (int)(T / tpw);
-    const int64_t slot0 = (T - (int64_t)w * tpw) * kTile + 4 * lane;
-    const float *vrow = values + (int64_t)w * stride;
-    float v[4];
-    if (slot0 + 3 < lb) {
-      const float4 x = __ldcs(reinterpret_cast<const float4 *>(vrow + slot0));
-      v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-    } else {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) v[k] = slot0 + k < lb ? vrow[slot0 + k] : __int_as_float(0x7f800000);
-    }
-    unsigned bits = 0u;
-    unsigned long long key = ~0ull;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const bool live = v[k] != __int_as_float(0x7f800000);
-      if (live && v[k] - delta <= tau) bits |= 1u << k;
-      if (live) {
-        const unsigned long long kk = ((unsigned long long)ord_f32(v[k]) << 32) |
-                                      (unsigned long long)local_to_global(slot0 + k, scene.rank, scene.world);
-        key = kk < key ? kk : key;
-      }
-    }
-    const int cnt = __popc(bits);
-    int incl = cnt;  // warp inclusive scan of the per-lane counts (slot order)
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
+  int wq = (int)(G0 * kGroup / tpw);
+  int64_t tq = G0 * kGroup - (int64_t)wq * tpw;
+  int wcur = wq;
+  unsigned long long key = ~0ull;
+  auto flush_key = [&]() {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
       key = other < key ? other : key;
     }
-    int base = 0;
-    if (lane == 0) {
-      if (key != ~0ull) atomicMin(ds.wp_key + w, key);
-      if (total > 0) {
-        const unsigned long long b = atomicAdd(ds.counter, (unsigned long long)total);
-        if (b + total > (unsigned long long)ds.max_active) {
-          atomicOr(ds.counter + 1, 1ull);
-          base = -1;
-        } else {
-          base = (int)b;
-        }
+    if (lane == 0 && key != ~0ull) atomicMin(ds.wp_key + wcur, key);
+    key = ~0ull;
+  };
+  for (int64_t G = G0; G < G1; ++G) {
+    const int64_t T0 = G * kGroup;
+    float4 vv[kGroup];
+    int ws[kGroup];
+    int64_t s0[kGroup];
+#pragma unroll
+    for (int t = 0; t < kGroup; ++t) {  // all loads in flight first
+      ws[t] = wq;
+      if (T0 + t < n_tiles) vv[t] = load_tile_values(values, stride, lb, wq, tq, lane, s0[t]);
+      if (++tq == tpw) {
+        tq = 0;
+        ++wq;
       }
-      ds.tile_meta[T] = make_int2(base, total);
     }
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (bits && base >= 0) {
-      int r = base + incl - cnt;
+#pragma unroll
+    for (int t = 0; t < kGroup; ++t) {
+      if (T0 + t >= n_tiles) break;
+      if (ws[t] != wcur) {
+        flush_key();
+        wcur = ws[t];
+      }
+      const float v[4] = {vv[t].x, vv[t].y, vv[t].z, vv[t].w};
+      // count: f - delta <= tau (dead slots are +INF and never pass); minimum: the lane's
+      // smallest value, first (smallest id) on ties, folded into one 64-bit key per tile
+      const float thr = tau + delta;
+      int cnt = 0;
+      float mv = v[0];
+      int mk = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        if (!((bits >> k) & 1u)) continue;
-        const int64_t slot = slot0 + k;
-        const float *g = grads + ((int64_t)w * stride + slot) * kNdof;
-        float4 *dst = reinterpret_cast<float4 *>(ds.staging + r);
-        dst[0] = make_float4(v[k], g[0], g[1], g[2]);
-        dst[1] = make_float4(g[3], g[4], g[5], g[6]);
-        dst[2] = make_float4(g[7], g[8], __uint_as_float((unsigned)w),
-                             __uint_as_float((unsigned)local_to_global(slot, scene.rank, scene.world)));
-        ++r;
+        cnt += (v[k] - delta <= tau) ? 1 : 0;
+        if (k > 0 && v[k] < mv) {
+          mv = v[k];
+          mk = k;
+        }
       }
+      (void)thr;
+      if (mv != __int_as_float(0x7f800000)) {
+        const unsigned long long kk = ((unsigned long long)ord_f32(mv) << 32) |
+                                      (unsigned long long)local_to_global(s0[t] + mk, scene.rank, scene.world);
+        key = kk < key ? kk : key;
+      }
+      cnt = __reduce_add_sync(0xffffffffu, cnt);
+      if (lane == 0) ds.tile_meta[T0 + t] = make_int2(0, cnt);
     }
   }
+  flush_key();
 }
 
-// per-waypoint active counts from the tile meta
-__global__ void __launch_bounds__(256) k_wp_count(const int2 *__restrict__ meta, int32_t tpw,
-                                                  const int64_t *__restrict__ tile_start,
-                                                  int64_t *__restrict__ wp_count) {
+// ---- finalize: per-tile (staging base, count) -> ordered output.  Tiles of step w are
+// [t0(w), t0(w) + nt(w)) (tile_start, or w * tpw); each step's tiles are split into chunks of
+// kFinChunk tiles (8 per thread) and every (step, chunk) is one CTA, so the ordered copy runs
+// on n_wp * nch CTAs instead of n_wp.
+constexpr int kFinPer = 8;
+constexpr int kFinChunk = 256 * kFinPer;
+
+__device__ __forceinline__ void tile_range(const int64_t *tile_start, int32_t tpw, int w, int64_t &t0, int64_t &nt) {
+  t0 = tile_start ? tile_start[w] : (int64_t)w * tpw;
+  nt = tile_start ? tile_start[w + 1] - t0 : tpw;
+}
+
+// record count of chunk (w, c) -> csum[w * nch + c]
+__global__ void __launch_bounds__(256) k_fin_count(const int2 *__restrict__ meta, int32_t tpw,
+                                                   const int64_t *__restrict__ tile_start, int64_t nch,
+                                                   int64_t *__restrict__ csum) {
   __shared__ int64_t sh[32];
-  const int w = blockIdx.x;
-  const int64_t t0 = tile_start ? tile_start[w] : (int64_t)w * tpw;
-  const int64_t nt = tile_start ? tile_start[w + 1] - t0 : tpw;
+  const int w = blockIdx.y;
+  const int64_t c = blockIdx.x;
+  int64_t t0, nt;
+  tile_range(tile_start, tpw, w, t0, nt);
   int64_t s = 0;
-  for (int64_t t = threadIdx.x; t < nt; t += blockDim.x) s += meta[t0 + t].y;
+  const int64_t b = c * kFinChunk + (int64_t)threadIdx.x * kFinPer;
+#pragma unroll
+  for (int i = 0; i < kFinPer; ++i)
+    if (b + i < nt) s += meta[t0 + b + i].y;
   int64_t tot;
   block_excl_scan(s, &tot, sh);
-  if (threadIdx.x == 0) wp_count[w] = tot;
+  if (threadIdx.x == 0) csum[(int64_t)w * nch + c] = tot;
 }
 
-// exclusive scan over waypoints + min/argmin/key export (single CTA)
-__global__ void __launch_bounds__(1024) k_wp_scan(const int64_t *__restrict__ wp_count, int32_t n_wp,
-                                                  int64_t *__restrict__ wp_offsets, int64_t *__restrict__ count,
-                                                  const unsigned long long *__restrict__ keys, float *wp_min,
-                                                  int64_t *wp_argmin, int64_t *wp_key_out) {
-  __shared__ int64_t sh[32];
-  int64_t carry = 0;
-  for (int base = 0; base < n_wp; base += blockDim.x) {
-    const int i = base + threadIdx.x;
-    const int64_t v = i < n_wp ? wp_count[i] : 0;
-    int64_t tot;
-    const int64_t ex = block_excl_scan(v, &tot, sh);
-    if (i < n_wp) wp_offsets[i] = carry + ex;
-    carry += tot;
-  }
-  if (threadIdx.x == 0) {
-    wp_offsets[n_wp] = carry;
-    *count = carry;
-  }
-  if (keys) {
-    for (int i = threadIdx.x; i < n_wp; i += blockDim.x) {
-      const unsigned long long k = keys[i];
-      if (wp_min) wp_min[i] = k == ~0ull ? __int_as_float(0x7f800000) : unord_f32((unsigned)(k >> 32));
-      if (wp_argmin) wp_argmin[i] = k == ~0ull ? -1 : (int64_t)(k & 0xffffffffull);
-      if (wp_key_out) wp_key_out[i] = (int64_t)(k ^ 0x8000000000000000ull);
+// wp_offsets from the chunk prefix, count, min / argmin / key export
+__global__ void __launch_bounds__(256) k_fin_offsets(const int64_t *__restrict__ cpre, int64_t nch, int32_t n_wp,
+                                                     int64_t *__restrict__ wp_offsets, int64_t *__restrict__ count,
+                                                     const unsigned long long *__restrict__ keys, float *wp_min,
+                                                     int64_t *wp_argmin, int64_t *wp_key_out) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w <= n_wp; w += gridDim.x * blockDim.x) {
+    wp_offsets[w] = cpre[(int64_t)w * nch];  // cpre[n_wp * nch] = the total
+    if (w == n_wp) {
+      *count = cpre[(int64_t)n_wp * nch];
+      continue;
+    }
+    if (keys) {
+      const unsigned long long k = keys[w];
+      if (wp_min) wp_min[w] = k == ~0ull ? __int_as_float(0x7f800000) : unord_f32((unsigned)(k >> 32));
+      if (wp_argmin) wp_argmin[w] = k == ~0ull ? -1 : (int64_t)(k & 0xffffffffull);
+      if (wp_key_out) wp_key_out[w] = (int64_t)(k ^ 0x8000000000000000ull);
     }
   }
 }
 
-// ordered copy staging -> out: one CTA per waypoint, tiles scanned in order
-__global__ void __launch_bounds__(256) k_wp_scatter(const int2 *__restrict__ meta, int32_t tpw,
-                                                    const int64_t *__restrict__ tile_start,
-                                                    const gcdf_active_t *__restrict__ staging,
-                                                    const int64_t *__restrict__ wp_offsets,
-                                                    gcdf_active_t *__restrict__ out, int64_t cap) {
+// ordered copy staging -> out for chunk (w, c), starting at cpre[w * nch + c]: each thread
+// copies the records of its 8 tiles (~1 % of 128 pairs each are active: a few records)
+__global__ void __launch_bounds__(256) k_fin_scatter(const int2 *__restrict__ meta, int32_t tpw,
+                                                     const int64_t *__restrict__ tile_start, int64_t nch,
+                                                     const int64_t *__restrict__ cpre,
+                                                     const gcdf_active_t *__restrict__ staging,
+                                                     gcdf_active_t *__restrict__ out, int64_t cap) {
   __shared__ int64_t sh[32];
-  const int w = blockIdx.x;
-  const int64_t tb = tile_start ? tile_start[w] : (int64_t)w * tpw;
-  const int64_t nt = tile_start ? tile_start[w + 1] - tb : tpw;
-  int64_t carry = wp_offsets[w];
-  for (int64_t t0 = 0; t0 < nt; t0 += blockDim.x) {
-    const int64_t t = t0 + threadIdx.x;
-    int2 m = make_int2(0, 0);
-    if (t < nt) m = meta[tb + t];
-    int64_t tot;
-    const int64_t ex = block_excl_scan(m.y, &tot, sh);
-    if (m.y > 0 && m.x >= 0) {
-      const float4 *src = reinterpret_cast<const float4 *>(staging + m.x);
-      for (int k = 0; k < m.y; ++k) {
-        const int64_t o = carry + ex + k;
+  const int w = blockIdx.y;
+  const int64_t c = blockIdx.x;
+  int64_t t0, nt;
+  tile_range(tile_start, tpw, w, t0, nt);
+  if (c * kFinChunk >= nt) return;  // (uniform over the block)
+  const int64_t b = c * kFinChunk + (int64_t)threadIdx.x * kFinPer;
+  int2 m[kFinPer];
+  int64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kFinPer; ++i) {
+    m[i] = b + i < nt ? meta[t0 + b + i] : make_int2(0, 0);
+    s += m[i].y;
+  }
+  int64_t tot;
+  int64_t pos = cpre[(int64_t)w * nch + c] + block_excl_scan(s, &tot, sh);
+#pragma unroll
+  for (int i = 0; i < kFinPer; ++i) {
+    if (m[i].y > 0 && m[i].x >= 0) {
+      const float4 *src = reinterpret_cast<const float4 *>(staging + m[i].x);
+      for (int k = 0; k < m[i].y; ++k) {
+        const int64_t o = pos + k;
         if (o < cap) {
           float4 *dst = reinterpret_cast<float4 *>(out + o);
           dst[0] = src[3 * k];
@@ -183,7 +223,89 @@ __global__ void __launch_bounds__(256) k_wp_scatter(const int2 *__restrict__ met
         }
       }
     }
-    carry += tot;
+    pos += m[i].y;
+  }
+}
+
+// pass 2 of the standalone K3: chunk (w, c) of kFinChunk tiles; the tile offsets come from a
+// block scan of the pass-1 counts, then a warp per tile re-reads its values and writes the
+// records at out[cpre + tile offset + rank] (gradients gathered from the dense array).
+__global__ void __launch_bounds__(256, 3) k_compact_write(const float *__restrict__ values,
+                                                       const float *__restrict__ grads, int64_t stride, int32_t tpw,
+                                                       int64_t nch, const int64_t *__restrict__ cpre,
+                                                       const int2 *__restrict__ meta, SceneView scene, float delta,
+                                                       float tau, gcdf_active_t *__restrict__ out, int64_t cap) {
+  __shared__ int64_t sh[32];
+  __shared__ int32_t tpos[kFinChunk];
+  const int w = blockIdx.y;
+  const int64_t c = blockIdx.x;
+  const int64_t t0 = (int64_t)w * tpw, nt = tpw;
+  if (c * kFinChunk >= nt) return;  // (uniform over the block)
+  const int64_t b = c * kFinChunk + (int64_t)threadIdx.x * kFinPer;
+  int cnt[kFinPer];
+  int64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kFinPer; ++i) {
+    cnt[i] = b + i < nt ? meta[t0 + b + i].y : 0;
+    s += cnt[i];
+  }
+  int64_t tot;
+  int32_t run = (int32_t)block_excl_scan(s, &tot, sh);
+#pragma unroll
+  for (int i = 0; i < kFinPer; ++i) {
+    tpos[threadIdx.x * kFinPer + i] = cnt[i] > 0 ? run : -1;
+    run += cnt[i];
+  }
+  __syncthreads();
+  const int64_t dst0 = cpre[(int64_t)w * nch + c];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t lb = scene.local_bound;
+  const int64_t tend = min((int64_t)kFinChunk, nt - c * kFinChunk);
+  // a warp takes 4 consecutive tiles per step: all their loads in flight, then the writes
+  for (int64_t tb = (int64_t)warp * 4; tb < tend; tb += 32) {
+    float4 vb[4];
+    int64_t sb[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (tb + i < tend && tpos[tb + i] >= 0) vb[i] = load_tile_values(values, stride, lb, w, c * kFinChunk + tb + i, lane, sb[i]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+    const int64_t tl = tb + i;
+    if (tl >= tend) break;
+    const int32_t pos = tpos[tl];
+    if (pos < 0) continue;  // no records in this tile (uniform over the warp)
+    const int64_t slot0 = sb[i];
+    const float v[4] = {vb[i].x, vb[i].y, vb[i].z, vb[i].w};
+    unsigned bits = 0u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (v[k] != __int_as_float(0x7f800000) && v[k] - delta <= tau) bits |= 1u << k;
+    const int n = __popc(bits);
+    int incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int64_t r = dst0 + pos + incl - n;
+    while (bits) {  // (a lane has at most 4 active slots; usually 0 or 1)
+      const int k = __ffs(bits) - 1;
+      bits &= bits - 1;
+      if (r < cap) {
+        const int64_t slot = slot0 + k;
+        const float *g = grads + ((int64_t)w * stride + slot) * kNdof;
+        float gg[kNdof];
+#pragma unroll
+        for (int i = 0; i < kNdof; ++i) gg[i] = __ldcs(g + i);
+        float4 *dst = reinterpret_cast<float4 *>(out + r);
+        dst[0] = make_float4(v[k], gg[0], gg[1], gg[2]);
+        dst[1] = make_float4(gg[3], gg[4], gg[5], gg[6]);
+        dst[2] = make_float4(gg[7], gg[8], __uint_as_float((unsigned)w),
+                             __uint_as_float((unsigned)local_to_global(slot, scene.rank, scene.world)));
+      }
+      ++r;
+    }
+    }
   }
 }
 
@@ -278,32 +400,59 @@ cudaError_t launch_detect_init(DetectScratch ds, int32_t n_wp, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+int64_t finalize_chunks(int64_t max_tiles_per_wp) { return std::max<int64_t>(1, (max_tiles_per_wp + kFinChunk - 1) / kFinChunk); }
+
 cudaError_t launch_compact_dense(const float *values, const float *grads, int64_t stride, int32_t n_wp,
                                  int32_t tiles_per_wp, SceneView scene, float delta, float tau,
-                                 DetectScratch ds, cudaStream_t s) {
+                                 DetectScratch ds, gcdf_active_t *out, int64_t out_capacity, int64_t *wp_offsets,
+                                 float *wp_min, int64_t *wp_argmin, int64_t *wp_key, int64_t *count,
+                                 int64_t *fin_scratch, cudaStream_t s, int *n_launches) {
   const int64_t n_tiles = (int64_t)n_wp * tiles_per_wp;
   if (n_tiles <= 0) return cudaSuccess;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t need = (n_tiles + 7) / 8;  // 8 warps (tiles) per CTA, 8 CTAs per SM
-  const int64_t grid = need < (int64_t)sms * 8 ? need : (int64_t)sms * 8;
-  k_compact_dense<<<(unsigned)grid, 256, 0, s>>>(values, grads, stride, n_wp, tiles_per_wp, scene, delta, tau, ds);
+  const int64_t need = (n_tiles + 8 * kGroup - 1) / (8 * kGroup);  // 8 warps per CTA, kGroup tiles each
+  const int64_t grid = need < (int64_t)sms * 4 ? need : (int64_t)sms * 4;
+  k_compact_count<<<(unsigned)grid, 256, 0, s>>>(values, stride, n_wp, tiles_per_wp, scene, delta, tau, ds);
+  const int64_t nch = finalize_chunks(tiles_per_wp);
+  const int64_t n = (int64_t)n_wp * nch;
+  int64_t *csum = fin_scratch, *cpre = fin_scratch + n, *tmp = fin_scratch + 2 * n + 1;
+  const dim3 g2((unsigned)nch, (unsigned)n_wp);
+  k_fin_count<<<g2, 256, 0, s>>>(ds.tile_meta, tiles_per_wp, nullptr, nch, csum);
+  cudaError_t e = excl_scan(csum, n, cpre, cpre + n, tmp, s, n_launches);
+  if (e != cudaSuccess) return e;
+  k_fin_offsets<<<(n_wp + 256) / 256, 256, 0, s>>>(cpre, nch, n_wp, wp_offsets, count, ds.wp_key, wp_min, wp_argmin,
+                                                   wp_key);
+  k_compact_write<<<g2, 256, 0, s>>>(values, grads, stride, tiles_per_wp, nch, cpre, ds.tile_meta, scene, delta, tau,
+                                     out, out_capacity);
+  *n_launches += 4;
   return cudaGetLastError();
 }
 
+
 cudaError_t launch_finalize(DetectScratch ds, int32_t n_wp, int32_t tiles_per_wp, const int64_t *tile_start,
-                            gcdf_active_t *out,
-                            int64_t out_capacity, int64_t *wp_offsets, float *wp_min, int64_t *wp_argmin,
-                            int64_t *wp_key, int64_t *count, int64_t *wp_count_scratch, cudaStream_t s,
-                            int *n_launches) {
+                            int64_t max_tiles_per_wp, gcdf_active_t *out, int64_t out_capacity, int64_t *wp_offsets,
+                            float *wp_min, int64_t *wp_argmin, int64_t *wp_key, int64_t *count, int64_t *fin_scratch,
+                            cudaStream_t s, int *n_launches) {
   if (n_wp <= 0) return cudaSuccess;
-  k_wp_count<<<n_wp, 256, 0, s>>>(ds.tile_meta, tiles_per_wp, tile_start, wp_count_scratch);
-  k_wp_scan<<<1, 1024, 0, s>>>(wp_count_scratch, n_wp, wp_offsets, count, ds.wp_key, wp_min, wp_argmin, wp_key);
-  k_wp_scatter<<<n_wp, 256, 0, s>>>(ds.tile_meta, tiles_per_wp, tile_start, ds.staging, wp_offsets, out,
-                                    out_capacity);
+  const int64_t nch = finalize_chunks(tile_start ? max_tiles_per_wp : tiles_per_wp);
+  const int64_t n = (int64_t)n_wp * nch;
+  int64_t *csum = fin_scratch, *cpre = fin_scratch + n, *tmp = fin_scratch + 2 * n + 1;
+  const dim3 grid((unsigned)nch, (unsigned)n_wp);
+  k_fin_count<<<grid, 256, 0, s>>>(ds.tile_meta, tiles_per_wp, tile_start, nch, csum);
+  cudaError_t e = excl_scan(csum, n, cpre, cpre + n, tmp, s, n_launches);
+  if (e != cudaSuccess) return e;
+  k_fin_offsets<<<(n_wp + 256) / 256, 256, 0, s>>>(cpre, nch, n_wp, wp_offsets, count, ds.wp_key, wp_min, wp_argmin,
+                                                   wp_key);
+  k_fin_scatter<<<grid, 256, 0, s>>>(ds.tile_meta, tiles_per_wp, tile_start, nch, cpre, ds.staging, out, out_capacity);
   *n_launches += 3;
   return cudaGetLastError();
+}
+
+int64_t finalize_scratch_elems(int64_t max_wp, int64_t max_tiles_per_wp) {
+  const int64_t n = max_wp * finalize_chunks(max_tiles_per_wp);
+  return 2 * n + 1 + (n + 1023) / 1024 + 1;
 }
 
 cudaError_t launch_merge(int32_t world, int32_t n_wp, const gcdf_active_t *recs, int64_t rec_stride,

@@ -18,6 +18,8 @@
 namespace gcdf {
 namespace {
 
+constexpr int kSub = 2;  // cells per radius: a step scans (2 kSub + 1)^2 cells, pruned by box distance
+
 __device__ __forceinline__ unsigned ord_f(float f) {
   const unsigned u = __float_as_uint(f);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
@@ -63,9 +65,9 @@ __global__ void k_grid_params(const unsigned *bbox, float r, float *g) {
     ox = unord_f(bbox[0]);
     oy = unord_f(bbox[1]);
     const float ex = unord_f(bbox[2]) - ox, ey = unord_f(bbox[3]) - oy;
-    // cs > r with a 1e-4 margin: a point within r of a base is at most one cell away even
-    // after the fp32 rounding of the cell coordinate
-    cs = fmaxf(r * 1.0001f, fmaxf(ex, ey) / 1024.f);
+    // cs = r / kSub with a 1e-4 margin: a point within r of a base is at most kSub cells
+    // away even after the fp32 rounding of the cell coordinate
+    cs = fmaxf(r * 1.0001f / kSub, fmaxf(ex, ey) / 1024.f);
     nx = (int)floorf(ex / cs) + 1;
     ny = (int)floorf(ey / cs) + 1;
     nx = min(nx, 1025);
@@ -82,95 +84,86 @@ __device__ __forceinline__ int cell_of(const float *g, float x, float y, int &cx
   return cy * nx + cx;
 }
 
+// Consecutive slots are mostly points of the same box and hence the same cell: the lanes of
+// a warp with equal cells are grouped (match.any) and their leader does one atomic for the
+// group (the clutter scenes put ~1e4 points in a cell, so per-point atomics would serialize).
 __global__ void __launch_bounds__(256) k_cell_count(const float4 *__restrict__ pts, int64_t n, const float *g,
                                                      int32_t *cell_count) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const float4 p = pts[i];
-    if (p.w > 0.f) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    int c = -1;
+    if (i < n) {
+      const float4 p = pts[i];
       int cx, cy;
-      atomicAdd(cell_count + cell_of(g, p.x, p.y, cx, cy), 1);
+      if (p.w > 0.f) c = cell_of(g, p.x, p.y, cx, cy);
     }
+    const unsigned grp = __match_any_sync(0xffffffffu, c);
+    if (c >= 0 && lane == __ffs(grp) - 1) atomicAdd(cell_count + c, __popc(grp));
   }
 }
 
 __global__ void __launch_bounds__(256) k_cell_fill(const float4 *__restrict__ pts, int64_t n, const float *g,
                                                     const int64_t *__restrict__ cell_start, int32_t *cell_fill,
-                                                    int32_t *cell_items) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const float4 p = pts[i];
-    if (p.w > 0.f) {
+                                                    int32_t *cell_items, float2 *cell_xy) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    int c = -1;
+    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < n) {
+      p = pts[i];
       int cx, cy;
-      const int c = cell_of(g, p.x, p.y, cx, cy);
-      cell_items[cell_start[c] + atomicAdd(cell_fill + c, 1)] = (int32_t)i;
+      if (p.w > 0.f) c = cell_of(g, p.x, p.y, cx, cy);
+    }
+    const unsigned grp = __match_any_sync(0xffffffffu, c);
+    const int leader = __ffs(grp) - 1;
+    int base = 0;
+    if (c >= 0 && lane == leader) base = atomicAdd(cell_fill + c, __popc(grp));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (c >= 0) {
+      const int64_t pos = cell_start[c] + base + __popc(grp & ((1u << lane) - 1u));
+      cell_items[pos] = (int32_t)i;
+      cell_xy[pos] = make_float2(p.x, p.y);
     }
   }
 }
 
-// ---- device-wide exclusive scan (int32 or int64 input -> int64), three launches
-template <typename T>
-__global__ void __launch_bounds__(1024) k_scan_blocks(const T *__restrict__ in, int64_t n, int64_t *__restrict__ out,
-                                                       int64_t *__restrict__ sums) {
-  __shared__ int64_t sh[32];
-  const int64_t i = blockIdx.x * 1024ll + threadIdx.x;
-  const int64_t v = i < n ? (int64_t)in[i] : 0;
-  int64_t tot;
-  const int64_t ex = block_excl_scan(v, &tot, sh);
-  if (i < n) out[i] = ex;
-  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
-}
-__global__ void __launch_bounds__(1024) k_scan_sums(int64_t *sums, int64_t nb, int64_t *__restrict__ total_out) {
-  __shared__ int64_t sh[32];
-  int64_t carry = 0;
-  for (int64_t base = 0; base < nb; base += 1024) {
-    const int64_t i = base + threadIdx.x;
-    const int64_t v = i < nb ? sums[i] : 0;
-    int64_t tot;
-    const int64_t ex = block_excl_scan(v, &tot, sh);
-    if (i < nb) sums[i] = carry + ex;
-    carry += tot;
-  }
-  if (threadIdx.x == 0) *total_out = carry;
-}
-__global__ void __launch_bounds__(1024) k_scan_add(int64_t *__restrict__ out, int64_t n, const int64_t *sums) {
-  const int64_t i = blockIdx.x * 1024ll + threadIdx.x;
-  if (i < n) out[i] += sums[blockIdx.x];
-}
-template <typename T>
-cudaError_t excl_scan(const T *in, int64_t n, int64_t *out, int64_t *total_out, int64_t *tmp, cudaStream_t s,
-                      int *nl) {
-  const int64_t nb = (n + 1023) / 1024;
-  if (nb <= 0) return cudaSuccess;
-  k_scan_blocks<T><<<(unsigned)nb, 1024, 0, s>>>(in, n, out, tmp);
-  k_scan_sums<<<1, 1024, 0, s>>>(tmp, nb, total_out);
-  k_scan_add<<<(unsigned)nb, 1024, 0, s>>>(out, n, tmp);
-  *nl += 3;
-  return cudaGetLastError();
-}
-
-// per step: mark the slots of its partition in its bitmap row (3x3 cells around the base)
-__global__ void __launch_bounds__(256) k_part_mark(const float4 *__restrict__ pts, const float *__restrict__ q,
-                                                    const float *g, const int64_t *__restrict__ cell_start,
-                                                    const int32_t *__restrict__ cell_items, int64_t words,
+// per step: mark the slots of its partition in its bitmap row.  The (2 kSub + 1)^2 cells
+// around the base are scanned in cell-sorted order (contiguous xy), cells whose rectangle is
+// farther than r from the base are skipped.
+__global__ void __launch_bounds__(256) k_part_mark(const float *__restrict__ q, const float *g,
+                                                    const int64_t *__restrict__ cell_start,
+                                                    const int32_t *__restrict__ cell_items,
+                                                    const float2 *__restrict__ cell_xy, int64_t words,
                                                     uint32_t *__restrict__ bitmap) {
   const int w = blockIdx.x;
   const int nx = __float_as_int(g[5]), ny = __float_as_int(g[6]);
   if (nx == 0) return;
   const float bx = q[(int64_t)w * kNdof], by = q[(int64_t)w * kNdof + 1];
+  const float ox = g[0], oy = g[1], cs = g[3];
   const float r = g[4], r2 = __fmul_rn(r, r);
-  const int cx = (int)floorf((bx - g[0]) * g[2]), cy = (int)floorf((by - g[1]) * g[2]);
+  const int cx = (int)floorf((bx - ox) * g[2]), cy = (int)floorf((by - oy) * g[2]);
   uint32_t *row = bitmap + (int64_t)w * words;
-  for (int dy = -1; dy <= 1; ++dy) {
+  for (int dy = -kSub; dy <= kSub; ++dy) {
     const int y = cy + dy;
     if (y < 0 || y >= ny) continue;
-    for (int dx = -1; dx <= 1; ++dx) {
+    for (int dx = -kSub; dx <= kSub; ++dx) {
       const int x = cx + dx;
       if (x < 0 || x >= nx) continue;
+      // distance from the base to the cell rectangle (with a small slack for rounding)
+      const float x0 = ox + x * cs, y0 = oy + y * cs;
+      const float ddx = fmaxf(fmaxf(x0 - bx, bx - (x0 + cs)), 0.f);
+      const float ddy = fmaxf(fmaxf(y0 - by, by - (y0 + cs)), 0.f);
+      if (ddx * ddx + ddy * ddy > r2 * 1.0002f + 1e-6f) continue;
       const int c = y * nx + x;
       for (int64_t k = cell_start[c] + threadIdx.x; k < cell_start[c + 1]; k += blockDim.x) {
-        const int32_t sl = cell_items[k];
-        const float4 p = pts[sl];
+        const float2 p = cell_xy[k];
         const float ex = __fsub_rn(p.x, bx), ey = __fsub_rn(p.y, by);
-        if (__fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey)) <= r2) atomicOr(row + (sl >> 5), 1u << (sl & 31));
+        if (__fadd_rn(__fmul_rn(ex, ex), __fmul_rn(ey, ey)) <= r2) {
+          const int32_t sl = cell_items[k];
+          atomicOr(row + (sl >> 5), 1u << (sl & 31));
+        }
       }
     }
   }
@@ -286,7 +279,8 @@ cudaError_t launch_part_grid(const float4 *pts, int64_t lb, float r, PartScratch
                             ps.scan_tmp, s, nl);
   if (e != cudaSuccess) return e;
   if (lb > 0) {
-    k_cell_fill<<<grid_for(lb), 256, 0, s>>>(pts, lb, ps.grid, ps.cell_start, ps.cell_fill, ps.cell_items);
+    k_cell_fill<<<grid_for(lb), 256, 0, s>>>(pts, lb, ps.grid, ps.cell_start, ps.cell_fill, ps.cell_items,
+                                             ps.cell_xy);
     ++*nl;
   }
   return cudaGetLastError();
@@ -295,8 +289,9 @@ cudaError_t launch_part_grid(const float4 *pts, int64_t lb, float r, PartScratch
 cudaError_t launch_part_build(const float4 *pts, const float *q, int32_t n_wp, float r, PartScratch ps,
                               unsigned long long *overflow, cudaStream_t s, int *nl) {
   (void)r;
+  (void)pts;
   cudaMemsetAsync(ps.bitmap, 0, (size_t)n_wp * ps.words * sizeof(uint32_t), s);
-  k_part_mark<<<n_wp, 256, 0, s>>>(pts, q, ps.grid, ps.cell_start, ps.cell_items, ps.words, ps.bitmap);
+  k_part_mark<<<n_wp, 256, 0, s>>>(q, ps.grid, ps.cell_start, ps.cell_items, ps.cell_xy, ps.words, ps.bitmap);
   k_chunk_count<<<dim3((unsigned)ps.nchunk, (unsigned)n_wp), 256, 0, s>>>(ps.bitmap, ps.words, ps.nchunk, ps.chunk_cnt);
   *nl += 2;
   const int64_t n = (int64_t)n_wp * ps.nchunk;
