@@ -374,6 +374,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     const bool live = live_n;
     float f = 0.f;
     int ridx = -1;  // staging record index (detect), -1 = none
+    unsigned long long pend_b = 0ull;  // (row 0) staging allocation of this tile, in flight
+    int pend_cnt = 0;
 #pragma unroll 1
     for (int p = 0; p < kPhases; ++p) {
       mbar_wait(&S.mma_done[s], ph);
@@ -541,6 +543,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
             S.kmin[s][qd] = key;
           }
           named_bar_sync(3 + s, 128);
+          int rk = __popc(bal & ((1u << lane) - 1u));
+          for (int i = 0; i < qd; ++i) rk += __popc(S.act[s][i]);
+          ridx = act ? rk : -1;  // rank in the tile; the tile's staging base is added at phase 11
           if (row == 0) {
             unsigned long long km = S.kmin[s][0];
             int cnt = 0;
@@ -550,24 +555,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
               cnt += __popc(S.act[s][i]);
             }
             if (km != ~0ull) atomicMin(a.ds.wp_key + w, km);
-            int base = 0;
-            if (cnt > 0) {
-              const unsigned long long b = atomicAdd(a.ds.counter, (unsigned long long)cnt);
-              if (b + cnt > (unsigned long long)a.ds.max_active) {
-                atomicOr(a.ds.counter + 1, 1ull);
-                base = -1;
-              } else {
-                base = (int)b;
-              }
-            }
-            S.sbase[s] = base;
-            a.ds.tile_meta[T] = make_int2(base, cnt);
+            // staging allocation: the (contended) atomic's result is consumed two phases
+            // later, so its latency stays off the epilogue's critical path
+            pend_cnt = cnt;
+            pend_b = cnt > 0 ? atomicAdd(a.ds.counter, (unsigned long long)cnt) : 0ull;
           }
-          named_bar_sync(3 + s, 128);
-          const int base = S.sbase[s];
-          int rk = __popc(bal & ((1u << lane) - 1u));
-          for (int i = 0; i < qd; ++i) rk += __popc(S.act[s][i]);
-          ridx = (act && base >= 0) ? base + rk : -1;
+        }
+        if (p == 8 && hh == 0 && a.detect && row == 0) {
+          int base = 0;
+          if (pend_cnt > 0) {
+            if (pend_b + pend_cnt > (unsigned long long)a.ds.max_active) {
+              atomicOr(a.ds.counter + 1, 1ull);
+              base = -1;
+            } else {
+              base = (int)pend_b;
+            }
+          }
+          S.sbase[s] = base;
+          a.ds.tile_meta[T] = make_int2(base, pend_cnt);
         }
         if (p == 7 && hh == 0) prefetch_pt(T + stride);  // lands during the next 4 phases
       } else {
@@ -594,6 +599,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
 #pragma unroll
           for (int i = 0; i < 7; ++i) gq[2 + i] = __uint_as_float(r[5 + i]);
           if (a.detect) {
+            named_bar_sync(3 + s, 128);  // S.sbase[s] (written at phase 8 by row 0) is visible
+            const int base = S.sbase[s];
+            ridx = (ridx >= 0 && base >= 0) ? base + ridx : -1;
             if (ridx >= 0) {
               float4 *dst = reinterpret_cast<float4 *>(a.ds.staging + ridx);
               dst[0] = make_float4(f, gq[0], gq[1], gq[2]);
