@@ -203,8 +203,9 @@ def main():
     e2e_steps = a.e2e_steps or max(1, min(a.steps, 5))
     n_upd = a.warmup + a.steps + e2e_steps
     gen = np.random.default_rng([cfg.seed, 7])
-    adds = [synth.inputs.scene_update_batch(gen, boxes, np.zeros((0, 3)))[0] for _ in range(n_upd)]
-    rems = list(gen.choice(cfg.M, size=(n_upd, 200), replace=False))
+    n_chg = int(max(1, min(200, cfg.M // (2 * n_upd))))  # 200 (C4 dynamics) unless the scene is tiny
+    adds = [synth.inputs.scene_update_batch(gen, boxes, np.zeros((0, 3)), n_add=n_chg)[0] for _ in range(n_upd)]
+    rems = list(gen.choice(cfg.M, size=(n_upd, n_chg), replace=False))
     upd_i = [0]
 
     def scene_step():
@@ -393,6 +394,21 @@ def main():
         ms = np.sort(tt.cpu().numpy()) * 1e3
         lat = {"p50_ms": float(np.percentile(ms, 50)), "p99_ms": float(np.percentile(ms, 99)),
                "calls": a.latency_calls, "what": "wall time, q on device -> active count on host"}
+        if world == 1:  # the same call chain replayed as a captured CUDA graph
+            for name, r in (("graph", 0.0), ("graph_partitioned", a.partition_radius)):
+                if name == "graph_partitioned" and r <= 0:
+                    continue
+                g = ctx.detect_graph(q, delta, tau, radius=r, capacity=max_active)
+                for _ in range(5):
+                    g.launch()
+                ts = []
+                for _ in range(a.latency_calls):
+                    t0 = time.perf_counter()
+                    g.launch()
+                    ts.append(time.perf_counter() - t0)
+                g.close()
+                ms = np.sort(np.array(ts)) * 1e3
+                lat[name] = {"p50_ms": float(np.percentile(ms, 50)), "p99_ms": float(np.percentile(ms, 99))}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -404,7 +420,7 @@ def main():
             "vs_baseline": None, "dtype": prec, "data": "synthetic (seeded clutter clouds + random-init weights)",
             "config": {"workload": f"{cfg.name}: {cfg.desc}", "B": cfg.B, "N": cfg.N, "points": cfg.M,
                        "hidden": cfg.H, "pairs_per_step": int(pairs_total / a.steps), "delta": delta, "tau": tau,
-                       "active_per_step": n_active, "scene_update_per_step": "200 removes + 200 adds",
+                       "active_per_step": n_active, "scene_update_per_step": f"{n_chg} removes + {n_chg} adds",
                        "parallelism": f"points sharded over {world} GPU(s)",
                        "l2": "256 MiB buffer written between timed steps (L2 flush)"},
             "roofline": roof, "mlp_kernel_share_of_step": kshare,

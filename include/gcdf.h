@@ -200,6 +200,23 @@ int gcdf_sparse_jacobian(gcdf_ctx *ctx, const gcdf_active_t *recs_dev, const int
                          int64_t capacity, float delta, float *c_dev, int64_t *row_ptr_dev, int32_t *col_dev,
                          float *val_dev, void *stream);
 
+/* CUDA-graph form of the detect for launch-bound (small) workloads: the whole call chain of
+   gcdf_detect_active_set (radius == 0) or gcdf_detect_active_set_partitioned (radius > 0)
+   with exactly these arguments is captured once into a CUDA graph; gcdf_graph_launch
+   replays it on `stream` (the contents of q_dev may change between launches, the pointers
+   may not) and, with count_host non-NULL, synchronizes and returns the count / CAPACITY
+   like the direct call.  After a scene update the next launch re-captures (the tile
+   counts and the partition grid depend on the scene); a partitioned graph's grid is built
+   outside the graph at capture time.  The graph owns a capture stream; it must be
+   destroyed before its context. */
+typedef struct gcdf_graph gcdf_graph;
+int gcdf_graph_create_detect(gcdf_ctx *ctx, const float *q_dev, int32_t B, int32_t N, float radius, float delta,
+                             float tau, gcdf_active_t *out_dev, int64_t out_capacity, int64_t *wp_offsets_dev,
+                             float *wp_min_dev, int64_t *wp_argmin_dev, int64_t *wp_key_dev,
+                             int64_t *part_sizes_dev, int64_t *count_dev, gcdf_graph **out);
+int gcdf_graph_launch(gcdf_graph *graph, int64_t *count_host_or_null, void *stream);
+int gcdf_graph_destroy(gcdf_graph *graph);
+
 /* Host-buffer form of gcdf_detect_active_set (the end-to-end call): q_host [B][N][9] is
    copied to the device, the fused detect runs, and the results come back to host memory:
    count_host (total active, always written), out_host [out_capacity] (the first

@@ -86,6 +86,23 @@ struct gcdf_ctx {
   // range partition: the planar grid is rebuilt when the scene or the radius changed
   bool part_dirty = true;
   float part_r = -1.f;
+  int64_t scene_version = 0;   // bumped by every scene change (captured graphs re-capture)
+};
+
+// A captured detect (gcdf_graph_create_detect): the arguments, the instantiated graph and
+// the scene version it was captured at.
+struct gcdf_graph {
+  gcdf_ctx *ctx = nullptr;
+  const float *q = nullptr;
+  int32_t B = 0, N = 0;
+  float radius = 0.f, delta = 0.f, tau = 0.f;
+  gcdf_active_t *out = nullptr;
+  int64_t cap = 0;
+  int64_t *offs = nullptr, *warg = nullptr, *wkey = nullptr, *psizes = nullptr, *count = nullptr;
+  float *wmin = nullptr;
+  cudaStream_t cs = nullptr;   // capture stream
+  cudaGraphExec_t exec = nullptr;
+  int64_t version = -1;
 };
 
 namespace {
@@ -581,7 +598,10 @@ int gcdf_update_scene(gcdf_ctx *c, const float *add_xyz, int64_t n_add, int64_t 
   if (n_rem > 0) c->cursor = std::min(c->cursor, rs[0]);
   c->n_live += n_add - n_rem;
   for (int64_t a = 0; a < n_add; ++a) c->id_bound = std::max(c->id_bound, out_ids[a] + 1);
-  if (n_add + n_rem > 0) c->part_dirty = true;
+  if (n_add + n_rem > 0) {
+    c->part_dirty = true;
+    ++c->scene_version;
+  }
   // device scatter of this rank's share, in pinned chunks
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   float4 *d_pay = reinterpret_cast<float4 *>(c->ws + c->L.upd_payload);
@@ -899,6 +919,97 @@ int gcdf_merge_active_sets(gcdf_ctx *c, int32_t world, int32_t n_wp, const gcdf_
   cudaError_t e = launch_merge(world, n_wp, recs, rec_stride, offsets, wp_key, out, cap, offs, wmin, warg, count,
                                static_cast<cudaStream_t>(stream), &nl);
   return count_launch(c, e, "merge", nl);
+}
+
+// ---------------------------------------------------------------- CUDA graphs
+static int graph_capture(gcdf_graph *g) {
+  gcdf_ctx *c = g->ctx;
+  if (g->exec) {
+    cudaGraphExecDestroy(g->exec);
+    g->exec = nullptr;
+  }
+  int rc = GCDF_OK;
+  if (g->radius > 0.f && (c->part_dirty || c->part_r != g->radius)) {  // grid built eagerly, not in the graph
+    const PartScratch ps = part_view(c);
+    const SceneView sv = scene_view(c);
+    int nl = 0;
+    if ((rc = count_launch(c, launch_part_grid(sv.pts, sv.local_bound, g->radius, ps, g->cs, &nl), "grid", 0)))
+      return rc;
+    c->launches += nl;
+    c->part_dirty = false;
+    c->part_r = g->radius;
+  }
+  const bool prof = c->prof;
+  c->prof = false;  // no profiling events inside a graph
+  CK(c, cudaStreamBeginCapture(g->cs, cudaStreamCaptureModeRelaxed), "begin capture");
+  if (g->radius > 0.f)
+    rc = gcdf_detect_active_set_partitioned(c, g->q, g->B, g->N, g->radius, g->delta, g->tau, g->out, g->cap, g->offs,
+                                            g->wmin, g->warg, g->wkey, g->psizes, g->count, nullptr, g->cs);
+  else
+    rc = gcdf_detect_active_set(c, g->q, g->B, g->N, g->delta, g->tau, g->out, g->cap, g->offs, g->wmin, g->warg,
+                                g->wkey, g->count, nullptr, g->cs);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(g->cs, &graph);
+  c->prof = prof;
+  if (rc) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (e != cudaSuccess) return cuda_fail(c, e, "end capture");
+  const cudaError_t e2 = cudaGraphInstantiate(&g->exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e2 != cudaSuccess) return cuda_fail(c, e2, "graph instantiate");
+  g->version = c->scene_version;
+  return GCDF_OK;
+}
+
+int gcdf_graph_create_detect(gcdf_ctx *c, const float *q, int32_t B, int32_t N, float radius, float delta, float tau,
+                             gcdf_active_t *out, int64_t cap, int64_t *offs, float *wmin, int64_t *warg, int64_t *wkey,
+                             int64_t *psizes, int64_t *count_dev, gcdf_graph **out_graph) {
+  int rc = precheck(c);
+  if (rc) return rc;
+  if (!out_graph) return fail(c, GCDF_ERR_INVALID_ARG, "graph: null output handle");
+  *out_graph = nullptr;
+  if (!(radius >= 0.f) || !std::isfinite(radius)) return fail(c, GCDF_ERR_INVALID_ARG, "graph: radius must be >= 0");
+  gcdf_graph *g = new gcdf_graph();
+  g->ctx = c;
+  g->q = q; g->B = B; g->N = N;
+  g->radius = radius; g->delta = delta; g->tau = tau;
+  g->out = out; g->cap = cap; g->offs = offs; g->wmin = wmin; g->warg = warg; g->wkey = wkey; g->psizes = psizes;
+  g->count = count_dev;
+  if (cudaStreamCreateWithFlags(&g->cs, cudaStreamNonBlocking) != cudaSuccess) {
+    delete g;
+    return fail(c, GCDF_ERR_CUDA, "graph: stream");
+  }
+  if ((rc = graph_capture(g)) || (rc = cudaStreamSynchronize(g->cs) == cudaSuccess ? GCDF_OK : GCDF_ERR_CUDA)) {
+    gcdf_graph_destroy(g);
+    return rc;
+  }
+  *out_graph = g;
+  return GCDF_OK;
+}
+
+int gcdf_graph_launch(gcdf_graph *g, int64_t *count_host, void *stream) {
+  if (!g) return GCDF_ERR_INVALID_ARG;
+  gcdf_ctx *c = g->ctx;
+  int rc = precheck(c);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (g->version != c->scene_version) {  // the scene changed: tile counts / grid differ
+    CK(c, cudaStreamSynchronize(s), "graph: order before re-capture");
+    if ((rc = graph_capture(g))) return rc;
+    CK(c, cudaStreamSynchronize(g->cs), "graph: grid build");
+  }
+  CK(c, cudaGraphLaunch(g->exec, s), "graph launch");
+  return read_count(c, g->cap, g->count, count_host, s);
+}
+
+int gcdf_graph_destroy(gcdf_graph *g) {
+  if (!g) return GCDF_OK;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->cs) cudaStreamDestroy(g->cs);
+  delete g;
+  return GCDF_OK;
 }
 
 int gcdf_debug_trace(gcdf_ctx *c, long long *trace_dev) {

@@ -27,7 +27,7 @@ EXPORTED = ["gcdf_default_options", "gcdf_create", "gcdf_destroy", "gcdf_last_er
             "gcdf_workspace_bytes", "gcdf_bind_workspace", "gcdf_load_weights", "gcdf_update_scene",
             "gcdf_scene_info", "gcdf_pairgen_transform", "gcdf_query_values_grads", "gcdf_detect_active_set",
             "gcdf_detect_active_set_partitioned", "gcdf_detect_active_set_host", "gcdf_sparse_jacobian",
-            "gcdf_project_dense", "gcdf_compact_dense", "gcdf_merge_active_sets", "gcdf_launch_count", "gcdf_profile_enable",
+            "gcdf_project_dense", "gcdf_graph_create_detect", "gcdf_graph_launch", "gcdf_graph_destroy", "gcdf_compact_dense", "gcdf_merge_active_sets", "gcdf_launch_count", "gcdf_profile_enable",
             "gcdf_profile_read", "gcdf_selftest_umma", "gcdf_debug_trace"]
 
 
@@ -75,6 +75,9 @@ def load_library(path: str | Path = LIB_PATH):
     lib.gcdf_detect_active_set_host.argtypes = [P, P, I32, I32, F, F, P, I64, P, P, P, P, P]
     lib.gcdf_sparse_jacobian.argtypes = [P, P, P, I64, F, P, P, P, P, P]
     lib.gcdf_project_dense.argtypes = [P, P, I32, I32, P, P, P, P]
+    lib.gcdf_graph_create_detect.argtypes = [P, P, I32, I32, F, F, F, P, I64, P, P, P, P, P, P, C.POINTER(P)]
+    lib.gcdf_graph_launch.argtypes = [P, P, P]
+    lib.gcdf_graph_destroy.argtypes = [P]
     lib.gcdf_detect_active_set_partitioned.argtypes = [P, P, I32, I32, F, F, F, P, I64, P, P, P, P, P, P, P, P]
     lib.gcdf_compact_dense.argtypes = [P, P, P, I32, I64, F, F, P, I64, P, P, P, P, P, P, P]
     lib.gcdf_merge_active_sets.argtypes = [P, I32, I32, P, I64, P, P, P, I64, P, P, P, P, P]
@@ -94,6 +97,40 @@ def _ptr(t):
 
 def _stream(device):
     return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+class DetectGraph:
+    """A captured detect (gcdf_graph_*); keeps its q and output tensors alive."""
+
+    def __init__(self, ctx: "Context", q: torch.Tensor, delta: float, tau: float, radius: float = 0.0,
+                 capacity: int | None = None):
+        q, B, N = ctx._q(q)
+        self.ctx, self.q = ctx, q
+        self.outputs = ctx.alloc_detect_outputs(B * N, capacity if capacity is not None else ctx.max_active)
+        o = self.outputs
+        o["part_sizes"] = torch.empty(B * N, dtype=torch.int64, device=ctx.device) if radius > 0 else None
+        h = C.c_void_p()
+        ctx._check(ctx.lib.gcdf_graph_create_detect(
+            ctx._h, _ptr(q), B, N, float(radius), float(delta), float(tau), _ptr(o["records"]), int(o["capacity"]),
+            _ptr(o["wp_offsets"]), _ptr(o["wp_min"]), _ptr(o["wp_argmin"]), _ptr(o["wp_key"]), _ptr(o["part_sizes"]),
+            _ptr(o["count"]), C.byref(h)))
+        self._g = h
+
+    def launch(self, sync_count: bool = True):
+        nh = C.c_int64(-1)
+        self.ctx._check(self.ctx.lib.gcdf_graph_launch(self._g, C.byref(nh) if sync_count else None,
+                                                       _stream(self.ctx.device)))
+        if sync_count:
+            self.outputs["n"] = nh.value
+        return self.outputs
+
+    def close(self):
+        if getattr(self, "_g", None) is not None and _lib is not None:
+            _lib.gcdf_graph_destroy(self._g)
+            self._g = None
+
+    def __del__(self):
+        self.close()
 
 
 def records_to_dict(rec: torch.Tensor, n: int) -> dict:
@@ -263,6 +300,12 @@ class Context:
         if sync_count:
             o["n"] = nh.value
         return o
+
+    def detect_graph(self, q: torch.Tensor, delta: float, tau: float, radius: float = 0.0,
+                     capacity: int | None = None):
+        """CUDA-graph form of detect (radius > 0: range-partitioned): returns a DetectGraph
+        whose launch() replays the captured call chain (refill q in place between launches)."""
+        return DetectGraph(self, q, delta, tau, radius, capacity)
 
     def project_dense(self, q: torch.Tensor, minv_diag):
         """NEXT-3: values [B*N, lb] and q_z = q - f M^{-1} grad f [B*N, lb, 9] for every pair."""

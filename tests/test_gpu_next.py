@@ -86,3 +86,37 @@ def test_projection_fused_matches_formula_and_oracle(prec):
         dz = np.linalg.norm(gz - oz, axis=-1)
         step = np.abs(ex["f"]) * np.linalg.norm(minv * ex["g"], axis=-1)
         assert np.median(dz / (step + 1e-3)) < 0.05
+
+
+@pytest.mark.parametrize("radius", [0.0, 1.8])
+def test_detect_graph_replays_direct_call(radius):
+    """The CUDA-graph detect equals the direct call bit for bit: for new q contents written
+    in place, and across scene updates (automatic re-capture)."""
+    cfg = synth.get_config("C2")
+    pts, boxes = synth.make_scene_points(cfg)
+    q = synth.make_waypoints(cfg)[:, :16]
+    tau = synth.load_tau(cfg.name)
+    ctx = _ctx(cfg, 2)
+    osc = oracle.Scene(cfg.M + 4096)
+    ctx.update_scene(pts)
+    osc.update(pts)
+    qd = torch.from_numpy(q).cuda()
+    g = ctx.detect_graph(qd, DELTA, tau, radius=radius)
+    rng = np.random.default_rng(5)
+    for it in range(4):
+        if it == 2:  # scene update -> re-capture at the next launch
+            ids, _ = osc.export()
+            add, rem = synth.scene_update_batch(rng, boxes, ids)
+            ctx.update_scene(add, rem)
+            osc.update(add, rem)
+        qn = q + rng.normal(0, 0.05, q.shape).astype(np.float32) * (it > 0)
+        qd.copy_(torch.from_numpy(qn))
+        go = g.launch()
+        d = (ctx.detect_active_set_partitioned(qd, radius, DELTA, tau) if radius > 0
+             else ctx.detect_active_set(qd, DELTA, tau))
+        assert go["n"] == d["n"] > 0
+        n = d["n"]
+        assert torch.equal(go["records"][:n], d["records"][:n])
+        for k in ("wp_offsets", "wp_min", "wp_argmin"):
+            assert torch.equal(go[k], d[k]), k
+    g.close()
