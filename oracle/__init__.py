@@ -25,6 +25,7 @@ EMU_BF16 = EMU_W | EMU_A
 TGRAD_QCHANNEL = 4
 EMU_FP16_FLAG = 8
 EMU_FP16 = EMU_W | EMU_A | EMU_FP16_FLAG
+FRAME_SE2 = 16   # NEXT-4 variant: points rotated into the base frame (R24)
 
 ERRORS = {0: "OK", -1: "INVALID", -2: "IO", -3: "BAD_MAGIC", -4: "VERSION", -5: "DIM_MISMATCH",
           -7: "CAPACITY", -12: "NOMEM"}

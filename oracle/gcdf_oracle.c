@@ -22,6 +22,8 @@
  *       by utilizing the gradients of obstacle point positions"):
  *       grad_q f = [-g0[0], -g0[1], g0[5], ..., g0[11]]   (TGRAD_QCHANNEL: g0[3], g0[4])
  *       ReLU'(0) = 0.
+ *       FRAME_SE2 (NEXT-4 variant, R24): p' = R(-theta)(p_xy - b) and the theta
+ *       channel fed zero; grad by the chain rule through the rotation.
  *   O6  active <=> f - delta <= tau  (constraint f - delta >= 0, PAPER.md:362-363;
  *       tau: DESIGN.md R12); records appended in loop order (wp ascending, point id
  *       ascending) = the step-major order of c_gcdf (Eq. 14).
@@ -49,6 +51,7 @@
 #define OR_EMU_W 1           /* round hidden W_2..W_{L-1} and W_1 (as used by the gradient) to bf16 */
 #define OR_EMU_A 2           /* round MMA A-operands h_1..h_{L-2}, e_{L-1}..e_1 to bf16 */
 #define OR_TGRAD_QCHANNEL 4  /* translational gradient from the q^t input channels */
+#define OR_FRAME_SE2 16      /* NEXT-4 variant (R24): rotate the points into the base frame too */
 #define OR_EMU_FP16 8        /* with OR_EMU_W / OR_EMU_A: round to fp16 instead of bf16 */
 
 #define OR_MAXL 16
@@ -174,12 +177,20 @@ static void eval_pair(const omlp_t *m, const double p[3], const double q[OR_NDOF
   double *const *Wround = fp16 ? m->Wh : m->Wr;
   double *h0 = s->h;
   /* O3: base-frame bias (translation only; q^t channels fed zero) */
-  h0[0] = p[0] - q[0];
-  h0[1] = p[1] - q[1];
+  const double dx = p[0] - q[0], dy = p[1] - q[1];
+  const double cth = cos(q[2]), sth = sin(q[2]);
+  if (flags & OR_FRAME_SE2) {  /* R24: p' = R(-theta) (p_xy - b), the theta channel fed zero */
+    h0[0] = cth * dx + sth * dy;
+    h0[1] = -sth * dx + cth * dy;
+  } else {
+    h0[0] = dx;
+    h0[1] = dy;
+  }
   h0[2] = p[2];
   h0[3] = 0.0;
   h0[4] = 0.0;
   for (int k = 0; k < 7; ++k) h0[5 + k] = q[2 + k];
+  if (flags & OR_FRAME_SE2) h0[5] = 0.0;
   /* O4: forward through the hidden layers l = 1..L-1 (array index l-1) */
   double kap = INFINITY;
   for (int l = 0; l < L - 1; ++l) {
@@ -242,14 +253,24 @@ static void eval_pair(const omlp_t *m, const double p[3], const double q[OR_NDOF
     }
   }
   /* s->g now holds dF/dx_in[0..11]; map to dF/dq (chain rule through the bias) */
-  if (flags & OR_TGRAD_QCHANNEL) {
-    grad[0] = s->g[3];
-    grad[1] = s->g[4];
+  if (flags & OR_FRAME_SE2) {
+    /* p' = R(-theta) d, d = p_xy - b:  dp'/db = -R(-theta), dp'/dtheta = [p'_y, -p'_x];
+       the theta channel is fed zero, so df/dtheta is the rotation term alone */
+    const double gx = s->g[0], gy = s->g[1];
+    grad[0] = -(cth * gx - sth * gy);
+    grad[1] = -(sth * gx + cth * gy);
+    grad[2] = gx * h0[1] - gy * h0[0];
+    for (int k = 1; k < 7; ++k) grad[2 + k] = s->g[5 + k];
   } else {
-    grad[0] = -s->g[0];
-    grad[1] = -s->g[1];
+    if (flags & OR_TGRAD_QCHANNEL) {
+      grad[0] = s->g[3];
+      grad[1] = s->g[4];
+    } else {
+      grad[0] = -s->g[0];
+      grad[1] = -s->g[1];
+    }
+    for (int k = 0; k < 7; ++k) grad[2 + k] = s->g[5 + k];
   }
-  for (int k = 0; k < 7; ++k) grad[2 + k] = s->g[5 + k];
   if (kappa) *kappa = kap;
   if (mhash) *mhash = hsh;
 }
@@ -298,6 +319,7 @@ done:
 int or_eval(const omlp_t *m, const double *pts, int64_t M, const double *q, int64_t W, int flags,
             double *f, double *g, double *kappa, uint64_t *mask_hash, int nthreads) {
   if (!m || M < 0 || W < 0 || (M > 0 && W > 0 && (!pts || !q || !f))) return OR_ERR_INVALID;
+  if ((flags & OR_FRAME_SE2) && (flags & OR_TGRAD_QCHANNEL)) return OR_ERR_INVALID;  /* no q^t channel in SE(2) */
   if (nthreads < 1) nthreads = 1;
   if (nthreads > 256) nthreads = 256;
   if (nthreads > W && W > 0) nthreads = (int)W;

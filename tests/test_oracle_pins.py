@@ -510,3 +510,52 @@ def test_single_step_projection_reaches_zero_level_set(tmp_path):
         for j in range(pts.shape[0]):
             for t in range(9):
                 assert qz[w, j, t] == q[w, t] - out["f"][w, j] * (minv[t] * out["g"][w, j, t])
+
+
+def test_se2_frame_variant(mlp32):
+    """NEXT-4 SE(2) frame pins (reading R24): (i) rigid-motion invariance -- rotating every
+    point and the base about an arbitrary centre by phi and adding phi to theta leaves f
+    unchanged, rotates the translational gradient by phi and keeps d f/d theta and the
+    joint gradients; (ii) central FD of the variant's forward, all 9 components; (iii) at
+    theta = 0 the variant equals the translation-only frame (R(0) = I, theta channel 0)."""
+    m, _ = mlp32
+    S = oracle.FRAME_SE2
+    rng = np.random.default_rng(21)
+    pts, q = _rand_inputs(rng, 30, 6)
+    base = m.eval(pts, q, flags=S, want_hash=True)
+    for phi, ctr in ((0.7, np.array([1.3, -2.1])), (-2.4, np.array([-3.0, 0.5]))):
+        c, s = np.cos(phi), np.sin(phi)
+        R = np.array([[c, -s], [s, c]])
+        pts2 = pts.copy()
+        pts2[:, :2] = (pts[:, :2] - ctr) @ R.T + ctr
+        q2 = q.copy()
+        q2[:, :2] = (q[:, :2] - ctr) @ R.T + ctr
+        q2[:, 2] = q[:, 2] + phi
+        o2 = m.eval(pts2, q2, flags=S)
+        np.testing.assert_allclose(o2["f"], base["f"], rtol=1e-11, atol=1e-11)
+        np.testing.assert_allclose(o2["g"][..., :2], base["g"][..., :2] @ R.T, rtol=1e-9, atol=1e-10)
+        np.testing.assert_allclose(o2["g"][..., 2:], base["g"][..., 2:], rtol=1e-9, atol=1e-10)
+    checked = skipped = 0
+    for k in range(9):
+        h = 1e-6 * np.maximum(1.0, np.abs(q[:, k]))
+        qp, qm = q.copy(), q.copy()
+        qp[:, k] += h
+        qm[:, k] -= h
+        op = m.eval(pts, qp, flags=S, want_grad=False, want_hash=True)
+        om = m.eval(pts, qm, flags=S, want_grad=False, want_hash=True)
+        fd = (op["f"] - om["f"]) / (2 * h[:, None])
+        same = (op["mask_hash"] == base["mask_hash"]) & (om["mask_hash"] == base["mask_hash"])
+        g = base["g"][:, :, k]
+        err = np.abs(fd - g) / np.maximum(1.0, np.abs(g))
+        assert np.all(err[same] <= 1e-6), (k, err[same].max())
+        checked += same.sum()
+        skipped += (~same).sum()
+    assert skipped <= 0.02 * (checked + skipped)
+    q0 = q.copy()
+    q0[:, 2] = 0.0
+    a0 = m.eval(pts, q0, flags=S)
+    b0 = m.eval(pts, q0)
+    np.testing.assert_array_equal(a0["f"], b0["f"])
+    np.testing.assert_array_equal(a0["g"][..., [0, 1, 3, 4, 5, 6, 7, 8]], b0["g"][..., [0, 1, 3, 4, 5, 6, 7, 8]])
+    with pytest.raises(oracle.OracleError):
+        m.eval(pts, q, flags=S | oracle.TGRAD_QCHANNEL)
