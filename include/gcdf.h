@@ -69,6 +69,12 @@ enum gcdf_tgrad {
   GCDF_TGRAD_QCHANNEL = 1   /* d f/d q_xy = d F/d x_in[3..4] (the network's q^t channels) */
 };
 
+enum gcdf_frame {
+  GCDF_FRAME_TRANSLATE = 0, /* p' = p - [x, y, 0], theta fed to the network (R1) */
+  GCDF_FRAME_SE2 = 1        /* NEXT-4 variant: p'_xy = R(-theta)(p_xy - [x, y]), theta channel fed 0
+                               (R24; not with GCDF_TGRAD_QCHANNEL) */
+};
+
 typedef struct {
   int32_t precision;       /* gcdf_precision (default GCDF_FP16) */
   int32_t tgrad_mode;      /* gcdf_tgrad */
@@ -79,6 +85,7 @@ typedef struct {
   int32_t world;           /*   (id / 128) satisfies block % world == rank; world >= 1 */
   int64_t max_candidates;  /* range-partitioned detect: capacity of the per-step candidate
                               lists (sum over steps of |I_{M,i}|); 0 = partitioned detect off */
+  int32_t frame;           /* gcdf_frame: base-frame transform of the points */
 } gcdf_options;
 
 /* One active constraint (48 B): f, grad_q f (9), wp = b*N + i, pt = global point id. */
@@ -91,7 +98,7 @@ typedef struct {
 
 /* ------------------------------------------------------------------ lifecycle */
 /* Fills *opt with defaults (precision FP16, chain rule, capacity 1<<20, 256 waypoints,
-   max_active 1<<22, rank 0, world 1, max_candidates 0). */
+   max_active 1<<22, rank 0, world 1, max_candidates 0, frame TRANSLATE). */
 void gcdf_default_options(gcdf_options *opt);
 
 /* Creates a context on CUDA device cuda_device.  Fails with UNSUPPORTED unless the

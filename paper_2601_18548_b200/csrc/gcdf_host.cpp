@@ -310,6 +310,7 @@ void gcdf_default_options(gcdf_options *o) {
   o->rank = 0;
   o->world = 1;
   o->max_candidates = 0;
+  o->frame = GCDF_FRAME_TRANSLATE;
 }
 
 int gcdf_has_tcgen05(void) { return tc_compiled() ? 1 : 0; }
@@ -323,7 +324,9 @@ int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out) {
   if (o.scene_capacity <= 0 || o.scene_capacity >= (1LL << 32) || o.max_waypoints <= 0 || o.max_active <= 0 ||
       o.max_active >= (1LL << 31) || o.world < 1 || o.rank < 0 || o.rank >= o.world ||
       (o.precision != GCDF_FP32 && o.precision != GCDF_BF16 && o.precision != GCDF_FP16) ||
-      (o.tgrad_mode != GCDF_TGRAD_CHAINRULE && o.tgrad_mode != GCDF_TGRAD_QCHANNEL))
+      (o.tgrad_mode != GCDF_TGRAD_CHAINRULE && o.tgrad_mode != GCDF_TGRAD_QCHANNEL) ||
+      (o.frame != GCDF_FRAME_TRANSLATE && o.frame != GCDF_FRAME_SE2) ||
+      (o.frame == GCDF_FRAME_SE2 && o.tgrad_mode == GCDF_TGRAD_QCHANNEL))  // R24: theta is not a channel in SE(2)
     return GCDF_ERR_INVALID_ARG;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev) return GCDF_ERR_UNSUPPORTED;
@@ -656,6 +659,7 @@ static QueryArgs make_args(gcdf_ctx *c, const float *q, int32_t nwp) {
   a.n_wp = nwp;
   a.tiles_per_wp = (int32_t)(a.scene.local_bound / kTile);
   a.tgrad = c->opt.tgrad_mode;
+  a.frame = c->opt.frame;
   a.trace = c->trace;
   return a;
 }
@@ -703,7 +707,7 @@ int gcdf_pairgen_transform(gcdf_ctx *c, const float *q, int32_t B, int32_t N, vo
   if ((rc = check_wp(c, q, B, N))) return rc;
   if (!out) return fail(c, GCDF_ERR_INVALID_ARG, "null output");
   SceneView sv = scene_view(c);
-  return count_launch(c, launch_pairgen(sv.pts, sv.local_bound, q, B * N, static_cast<float4 *>(out),
+  return count_launch(c, launch_pairgen(sv.pts, sv.local_bound, q, B * N, c->opt.frame, static_cast<float4 *>(out),
                                         static_cast<cudaStream_t>(stream)), "pairgen");
 }
 

@@ -83,6 +83,7 @@ struct QueryArgs {
   int32_t n_wp;
   int32_t tiles_per_wp;
   int32_t tgrad;                   // gcdf_tgrad
+  int32_t frame;                   // gcdf_frame (1: SE(2), R24)
   // dense outputs (query) -- NULL in detect mode
   float *values;
   float *grads;                    // (project: the projected configurations q_z instead)
@@ -112,6 +113,10 @@ __device__ __forceinline__ void tile_pair(const QueryArgs &a, int64_t T, int row
     valid = slot < a.scene.local_bound;
   }
 }
+// step (waypoint index) of tile T
+__device__ __forceinline__ int tile_step(const QueryArgs &a, int64_t T) {
+  return a.part.tile_wp ? a.part.tile_wp[T] : (int)(T / a.tiles_per_wp);
+}
 __device__ __forceinline__ int64_t query_tiles(const QueryArgs &a) {
   return a.part.tile_wp ? *a.part.n_tiles : (int64_t)a.n_wp * a.tiles_per_wp;
 }
@@ -128,7 +133,7 @@ __host__ __device__ inline int64_t local_to_global(int64_t slot, int rank, int w
 cudaError_t launch_scene_scatter(const float4 *payload, const int64_t *slots, int64_t n, float4 *pts,
                                  cudaStream_t s);
 cudaError_t launch_fill(float4 *pts, int64_t n, cudaStream_t s);
-cudaError_t launch_pairgen(const float4 *pts, int64_t local_bound, const float *q, int32_t n_wp,
+cudaError_t launch_pairgen(const float4 *pts, int64_t local_bound, const float *q, int32_t n_wp, int frame,
                            float4 *out, cudaStream_t s);
 cudaError_t launch_detect_init(DetectScratch ds, int32_t n_wp, cudaStream_t s);
 cudaError_t launch_mlp_simt(int H, const WeightsF32 &w, const QueryArgs &a, int num_sms, cudaStream_t s);

@@ -107,22 +107,27 @@ __global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const Q
     __syncthreads();  // smem of the previous tile is free
     if (tid < kNdof) qv[tid] = __ldg(a.q + (int64_t)w * kNdof + tid);
     __syncthreads();
-    // A2: pair generation + base-frame bias: p' = p - [q_x, q_y, 0]
+    // A2: pair generation + base-frame bias: p' = p - [q_x, q_y, 0];
+    // SE(2) frame (R24): p'_xy = R(-theta)(p_xy - [q_x, q_y])
+    float cth = 1.f, sth = 0.f;
+    if (a.frame) sincosf(qv[2], &sth, &cth);
     if (tid < kTile) {
       int wt;
       int64_t slot;
       bool valid;
       tile_pair(a, T, tid, wt, slot, valid);
       float4 p = valid ? __ldg(a.scene.pts + slot) : make_float4(0.f, 0.f, 0.f, 0.f);
-      sp[tid] = make_float4(p.x - qv[0], p.y - qv[1], p.z, p.w);
+      const float dx = p.x - qv[0], dy = p.y - qv[1];
+      sp[tid] = make_float4(cth * dx + sth * dy, -sth * dx + cth * dy, p.z, p.w);
     }
     // layer-1 constant of this waypoint: c = b1 + W1[:, 5:12] . [theta, j1..j6]
-    // (the q^t input channels are fed zero, R2)
+    // (the q^t input channels are fed zero, R2; the theta channel is fed zero in SE(2), R24)
     for (int u = tid; u < H; u += 256) {
       const float *wq = W.w1q + u * 8;
       float c = __ldg(&W.w1p[u].w);
+      if (!a.frame) c = fmaf(__ldg(wq), qv[2], c);
 #pragma unroll
-      for (int i = 0; i < 7; ++i) c = fmaf(__ldg(wq + i), qv[2 + i], c);
+      for (int i = 1; i < 7; ++i) c = fmaf(__ldg(wq + i), qv[2 + i], c);
       c1[u] = c;
     }
     __syncthreads();
@@ -311,7 +316,16 @@ __global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const Q
           g[3] = fmaf(e, __ldg(row + 6), g[3]);
           g[4] = fmaf(e, __ldg(row + 7), g[4]);
         }
-        if (!a.tgrad) { g[0] = -g[0]; g[1] = -g[1]; }
+        if (a.frame) {
+          // SE(2) (R24): df/db = -R(theta) g0_xy, df/dtheta = g0_x p'_y - g0_y p'_x
+          const float gx = g[0], gy = g[1];
+          g[0] = -(cth * gx - sth * gy);
+          g[1] = -(sth * gx + cth * gy);
+          g[2] = gx * sp[p].y - gy * sp[p].x;
+        } else if (!a.tgrad) {
+          g[0] = -g[0];
+          g[1] = -g[1];
+        }
 #pragma unroll
         for (int c = 0; c < 5; ++c) gst[p * 9 + c] = g[c];
       } else {

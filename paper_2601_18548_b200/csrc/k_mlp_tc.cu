@@ -55,10 +55,30 @@ constexpr int kEpiWarps = 16;             // warps 0..15: epilogue (8 per tile s
 #ifndef GCDF_TC_ISSUE
 #define GCDF_TC_ISSUE 1
 #endif
+// mbarrier waits (dev switch): 0 = try_wait (hardware suspend), 1 = test_wait spin,
+// 2 = try_wait with a 20 ns suspend hint; IWAIT: the MMA warps on epi_done, EWAIT: the
+// epilogue warps on mma_done
+#ifndef GCDF_TC_IWAIT
+#define GCDF_TC_IWAIT 0
+#endif
+#ifndef GCDF_TC_EWAIT
+#define GCDF_TC_EWAIT 0
+#endif
+template <int kMode>
+DEVI void mbar_wait_mode(uint64_t *bar, uint32_t parity) {
+  if constexpr (kMode == 1) mbar_wait_spin(bar, parity);
+  else if constexpr (kMode == 2) mbar_wait_hint<20u>(bar, parity);
+  else mbar_wait(bar, parity);
+}
 constexpr int kWarps = kEpiWarps + (GCDF_TC_ISSUE == 0 ? 1 : 2);
 constexpr int kThreads = kWarps * 32;
 constexpr int kEpiPerSlot = 256;
-constexpr int kEpiArrivals = kEpiPerSlot;  // epi_done count
+// epi_done arrivals (dev switch GCDF_TC_WARPARRIVE): 0 = every epilogue thread arrives,
+// 1 = one elected lane per warp after __syncwarp
+#ifndef GCDF_TC_WARPARRIVE
+#define GCDF_TC_WARPARRIVE 0
+#endif
+constexpr int kEpiArrivals = GCDF_TC_WARPARRIVE ? kEpiPerSlot / 32 : kEpiPerSlot;  // epi_done count
 constexpr int kPhases = 12;               // MMA phases per tile
 constexpr int kMasks = 5;                 // stored ReLU masks: layers 1..5
 constexpr int kWBytes = 5 * H * H * 2;    // 163,840
@@ -80,8 +100,13 @@ struct __align__(1024) SmemTC {
   float w7half[H];             // w7 / 2: f = sum w7half (z6 + |z6|) = w7 . ReLU(z6), all on the FMA pipe
   uint32_t w7h[H / 2];         // w7 as packed 16-bit pairs: e6 = w7 (.) 1[z6 > 0]
   uint32_t one;                // 1 (runtime constant, see add7fff)
-  float fpart[2][4][H];        // [slot][column half / quarter][row] partial output-layer sums
+  float fpart[2][2][H];        // [slot][column half][row] partial output-layer sums
   float4 ptn[2][H];            // [slot][row] prefetched point of the slot's next tile
+  float2 pprime[2][2][H];      // [slot][tile parity][row] SE(2) frame: p'_xy kept for d f / d theta (R24)
+  float qn[2][2][12];          // [slot][tile parity] q row of the slot's tile (cp.async, phases 1-3)
+  int wnx[2];                  // [slot] (partitioned) step of the slot's next tile, staged at phase 1
+  int wtile[2][2];             // [slot][tile parity] step (waypoint) of the slot's tile
+  uint32_t slotn[2][2][H];     // [slot][tile parity][row] local scene slot of the pair (~0: padding)
   uint32_t mask[2][kMasks][2][kEpiPerSlot];  // ReLU masks [slot][layer][32-unit word][thread]
   uint64_t mma_done[2];
   uint64_t epi_done[2];
@@ -91,6 +116,8 @@ struct __align__(1024) SmemTC {
   int sbase[2];
   uint32_t tmem_base;
 };
+
+static_assert(sizeof(SmemTC) + 1024 <= 232448, "SmemTC exceeds the 227 KB of shared memory per CTA");
 
 DEVI unsigned ord_f32(float f) {
   unsigned u = __float_as_uint(f);
@@ -168,7 +195,9 @@ DEVI void issue_phase(int p, uint32_t d, uint32_t sw, uint32_t sw1t, uint32_t sb
   else tc::commit(bar);
 }
 
-template <bool F16>
+// kSE2: the SE(2) frame variant (R24) as its own instantiation, so the default
+// translation-frame kernel carries none of its code or registers
+template <bool F16, bool kSE2>
 __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, const QueryArgs a) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned view (SWIZZLE_128B atoms); pointer arithmetic on the __shared__ array
@@ -203,6 +232,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     S.turn = 0u;
     fence_barrier_init();
   }
+  if (tid < 2 * kNdof) {  // q rows of the slots' first tiles (later tiles: cp.async, phases 1-3)
+    const int s0 = tid / kNdof, i = tid - s0 * kNdof;
+    const int64_t T0 = (int64_t)blockIdx.x * 2 + s0;
+    if (T0 < query_tiles(a)) {
+      const int w0 = tile_step(a, T0);
+      S.qn[s0][0][i] = __ldg(a.q + (int64_t)w0 * kNdof + i);
+      if (i == 0) S.wtile[s0][0] = w0;
+    }
+  }
   fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
   fence_before();
   __syncthreads();
@@ -235,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         long long *t = (tr0 && itt < kTraceTiles) ? tr0 + ((size_t)itt * kTracePhases + p) * 4 + 2 * ss : nullptr;
         long long *t2 = t ? t + (size_t)(kTraceRoles - 1) * kTraceTiles * kTracePhases * 4 : nullptr;
         if (t2) t2[0] = clock64();
-        mbar_wait(&S.epi_done[ss], ph);
+        mbar_wait_mode<GCDF_TC_IWAIT>(&S.epi_done[ss], ph);
         ph ^= 1u;
         if (two) {
           const long long tw = clock64();
@@ -307,45 +345,87 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   auto hand_off = [&](int, bool) {
     wait_st();
     fence_before();
+#if GCDF_TC_WARPARRIVE
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.epi_done[s]);
+#else
     mbar_arrive(&S.epi_done[s]);
+#endif
   };
   // cp.async prefetch of this lane's point of tile TT into S.ptn[s][row] (zero if none);
   // issued by the column-half-0 threads, which alone read it
-  auto prefetch_pt = [&](int64_t TT) {
+  // (the pair's local slot goes to S.slotn[s][par][row], read back by this same thread at
+  // phases 6 and 11 and by stage_a1: no per-tile index arithmetic on the critical path)
+  auto prefetch_pt = [&](int64_t TT, int par) {
     int wn = 0;
     int64_t sl = 0;
     bool ok = false;
     if (TT < n_tiles) tile_pair(a, TT, row, wn, sl, ok);
+    S.slotn[s][par][row] = ok ? (uint32_t)sl : ~0u;
     cp_async16(&S.ptn[s][row], ok ? (const void *)(a.scene.pts + sl) : (const void *)a.scene.pts, ok ? 16u : 0u);
     cp_async_commit();
+  };
+  // q row of the slot's next tile TT -> S.qn[s][par], by lanes 0..8 of warp (half 0,
+  // quarter 0) off the critical path: phase 1 stages the step of a partitioned tile, phase
+  // 3 copies the row; the copy is waited for before the phase-5 barrier of the slot's 256
+  // epilogue threads, which publishes it (stage_a1 reads it at phase 11)
+  auto stage_q = [&](int p, int64_t TT, int par) {
+    if (hh != 0 || qd != 0 || TT >= n_tiles) return;
+    if (p == 1) {
+      if (a.part.tile_wp && lane == 0) {
+        cp_async4(&S.wnx[s], a.part.tile_wp + TT);
+        cp_async_commit();
+      }
+    } else {
+      int wn;
+      if (a.part.tile_wp) {
+        if (lane == 0) cp_async_wait_all();
+        __syncwarp();
+        wn = S.wnx[s];
+      } else {
+        wn = (int)(TT / a.tiles_per_wp);
+      }
+      if (lane < kNdof) cp_async4(&S.qn[s][par][lane], a.q + (int64_t)wn * kNdof + lane);
+      cp_async_commit();
+      if (lane == 0) S.wtile[s][par] = wn;
+    }
   };
   // A2 + A1 of tile TT: pair generation, base-frame bias p' = p - [q_x, q_y, 0]
   // and the split layer-1 operands -> TMEM A (K = 32: half 0 writes K 0..15,
   // half 1 K 16..31), then hand off.  Returns the pair's liveness (meaningful in half 0).
-  auto stage_a1 = [&](int64_t TT) -> bool {
-    int wn;
-    int64_t sl;
-    bool valid;
-    tile_pair(a, TT, row, wn, sl, valid);
-    const float *qw = a.q + (int64_t)wn * kNdof;
+  // SE(2) frame (R24): p'_xy = R(-theta)(p_xy - b), theta channel fed 0; p'_xy is kept in
+  // S.pprime[s][par] for the theta gradient at phase 11 (__sincosf: abs error ~1e-6 on
+  // [-pi, pi], far below the 16-bit operand rounding).
+  auto stage_a1 = [&](int64_t TT, int par) -> bool {
+    const float *qw = S.qn[s][par];
     float v[16];
     bool lv = false;
     if (hh == 0) {  // K 0..15: p'_x, p'_y, p_z, theta, j1 (3 each), x_hi of j2
       const float4 pt = S.ptn[s][row];
-      lv = valid && pt.w > 0.f;
-      split3<F16>(pt.x - __ldg(qw), v);
-      split3<F16>(pt.y - __ldg(qw + 1), v + 3);
+      lv = S.slotn[s][par][row] != ~0u && pt.w > 0.f;
+      float dx = pt.x - qw[0], dy = pt.y - qw[1], th = qw[2];
+      if constexpr (kSE2) {
+        float sn, cs;
+        __sincosf(th, &sn, &cs);
+        const float rx = cs * dx + sn * dy;
+        dy = -sn * dx + cs * dy;
+        dx = rx;
+        th = 0.f;
+        S.pprime[s][par][row] = make_float2(dx, dy);
+      }
+      split3<F16>(dx, v);
+      split3<F16>(dy, v + 3);
       split3<F16>(pt.z, v + 6);
-      split3<F16>(__ldg(qw + 2), v + 9);
-      split3<F16>(__ldg(qw + 3), v + 12);
-      v[15] = round16<F16>(__ldg(qw + 4));
+      split3<F16>(th, v + 9);
+      split3<F16>(qw[3], v + 12);
+      v[15] = round16<F16>(qw[4]);
     } else {        // K 16..31: x_lo, x_hi of j2, j3..j6 (3 each), {1, 1} for b1
-      const float j2 = __ldg(qw + 4);
+      const float j2 = qw[4];
       const float j2h = round16<F16>(j2);
       v[0] = j2 - j2h;
       v[1] = j2h;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) split3<F16>(__ldg(qw + 5 + i), v + 2 + 3 * i);
+      for (int i = 0; i < 4; ++i) split3<F16>(qw[5 + i], v + 2 + 3 * i);
       v[14] = 1.f;
       v[15] = 1.f;
     }
@@ -363,10 +443,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   bool live_n = false;
   if ((int64_t)blockIdx.x * 2 + s < n_tiles) {
     if (hh == 0) {
-      prefetch_pt((int64_t)blockIdx.x * 2 + s);
+      prefetch_pt((int64_t)blockIdx.x * 2 + s, 0);
       cp_async_wait_all();
     }
-    live_n = stage_a1((int64_t)blockIdx.x * 2 + s);
+    live_n = stage_a1((int64_t)blockIdx.x * 2 + s, 0);
   }
   for (int64_t T = (int64_t)blockIdx.x * 2 + s; T < n_tiles; T += stride, ++it) {
     long long *tr = (tracer && it < kTraceTiles) ? a.trace + (size_t)((1 + warp) * kTraceTiles + it) * kTracePhases * 4 : nullptr;
@@ -378,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     int pend_cnt = 0;
 #pragma unroll 1
     for (int p = 0; p < kPhases; ++p) {
-      mbar_wait(&S.mma_done[s], ph);
+      mbar_wait_mode<GCDF_TC_EWAIT>(&S.mma_done[s], ph);
       if (tr) tr[(p + 1) * 4 + 1] = clock64();
       ph ^= 1u;
       fence_after();
@@ -453,22 +533,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         if (tr) tr[(p + 1) * 4 + 2] = clock64();
         hand_off(p + 1, s == 1 || T + 1 < n_tiles);
         if (tr) tr[(p + 1) * 4 + 3] = clock64();
+        if (p == 1 || p == 3) stage_q(p, T + stride, (it + 1) & 1);
       } else if (p == 5) {
         // ---- layer 6: e6 = w7 (.) 1[z6 > 0] -> A; f = w7 . ReLU(z6) + b7 (fp32) ----
+        // (16-column chunks; the TMEM load of chunk c + 1 in flight while chunk c is used)
         float fa[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t rb[2][16];
+        ld16(tD, rb[0]);
+        wait_ld();
+        if (tr) tr[(p + 1) * 4 + 0] = clock64();
 #pragma unroll
-        for (int cb = 0; cb < 64; cb += 16) {
-          uint32_t pk[8], rr[16];
-          ld16(tD + cb, rr);
-          wait_ld();
-          if (tr && cb == 0) tr[(p + 1) * 4 + 0] = clock64();
+        for (int c = 0; c < 4; ++c) {
+          const int cb = 16 * c;
+          if (c < 3) ld16(tD + cb + 16, rb[(c + 1) & 1]);
+          const uint32_t *rr = rb[c & 1];
+          uint32_t pk[8];
 #pragma unroll
           for (int j = 0; j < 16; j += 4) {
             const float4 w7 = *reinterpret_cast<const float4 *>(S.w7half + u0 + cb + j);
             const uint2 w2 = *reinterpret_cast<const uint2 *>(S.w7h + (u0 + cb + j) / 2);
-            const float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
-            const float z0 = __uint_as_float(rr[j]) + b4.x, z1 = __uint_as_float(rr[j + 1]) + b4.y;
-            const float z2 = __uint_as_float(rr[j + 2]) + b4.z, z3 = __uint_as_float(rr[j + 3]) + b4.w;
+            const float z0 = __uint_as_float(rr[j]), z1 = __uint_as_float(rr[j + 1]);
+            const float z2 = __uint_as_float(rr[j + 2]), z3 = __uint_as_float(rr[j + 3]);
             pk[j >> 1] = w2.x & nz_halves(pack2_relu<F16>(z0, z1), one);
             pk[(j >> 1) + 1] = w2.y & nz_halves(pack2_relu<F16>(z2, z3), one);
             // (w7 / 2) (z + |z|) = w7 ReLU(z) exactly (z + |z| = 2 ReLU(z), halving is exact)
@@ -478,20 +563,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
             fa[3] = fmaf(w7.w, z3 + fabsf(z3), fa[3]);
           }
           st8(tA + cb / 2, pk);
+          if (c < 3) wait_ld();
         }
         if (tr) tr[(p + 1) * 4 + 2] = clock64();
         hand_off(p + 1, s == 1 || T + 1 < n_tiles);
         if (tr) tr[(p + 1) * 4 + 3] = clock64();
         // f = w7 . h6 + b7 (fp32, no output activation: signed value)
         S.fpart[s][hh][row] = (fa[0] + fa[1]) + (fa[2] + fa[3]);
+        if (hh == 0 && qd == 0) cp_async_wait_all();  // S.qn of the next tile (stage_q)
         named_bar_sync(1 + s, kEpiPerSlot);
         if (hh == 0) {
           f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
           if (!a.detect) {
-            int w;
-            int64_t slot;
-            bool valid;
-            tile_pair(a, T, row, w, slot, valid);
+            const int w = S.wtile[s][it & 1];
+            const int64_t slot = S.slotn[s][it & 1][row];
             if (slot < lb) a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
           }
         }
@@ -523,10 +608,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         if (tr) tr[(p + 1) * 4 + 3] = clock64();
         if (p == 6 && hh == 0 && a.detect) {
           // A6/A7 (overlaps the tensor core): threshold, per-tile slots, per-waypoint min key
-          int w;
-          int64_t slot;
-          bool valid;
-          tile_pair(a, T, row, w, slot, valid);
+          const int w = S.wtile[s][it & 1];
+          const int64_t slot = S.slotn[s][it & 1][row];  // (live implies a real pair)
           const bool act = live && (f - a.delta <= a.tau);
           const unsigned bal = __ballot_sync(0xffffffffu, act);
           unsigned long long key = ~0ull;
@@ -574,7 +657,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
           S.sbase[s] = base;
           a.ds.tile_meta[T] = make_int2(base, pend_cnt);
         }
-        if (p == 7 && hh == 0) prefetch_pt(T + stride);  // lands during the next 4 phases
+        if (p == 7 && hh == 0) prefetch_pt(T + stride, (it + 1) & 1);  // lands during the next 4 phases
       } else {
         // ---- g0 = W1^T e1 (16 columns); d f / d q by the chain rule (R3) ----
         // D is read first; the next tile's layer-1 operands are handed off before the
@@ -586,20 +669,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
           cp_async_wait_all();  // this thread's prefetched point of the next tile
         }
         if (tr) tr[(p + 1) * 4 + 0] = clock64();
-        if (T + stride < n_tiles) live_n = stage_a1(T + stride);
+        if (T + stride < n_tiles) live_n = stage_a1(T + stride, (it + 1) & 1);
         if (tr) tr[(p + 1) * 4 + 2] = clock64();
         if (hh == 0) {
-          int w;
-          int64_t slot;
-          bool valid;
-          tile_pair(a, T, row, w, slot, valid);
+          const int w = S.wtile[s][it & 1];
+          const int64_t slot = S.slotn[s][it & 1][row];
+          if (tr) tr[1] = clock64();  // (phase-11 detail: step and slot read)
           float gq[kNdof];
           gq[0] = a.tgrad ? __uint_as_float(r[3]) : -__uint_as_float(r[0]);
           gq[1] = a.tgrad ? __uint_as_float(r[4]) : -__uint_as_float(r[1]);
 #pragma unroll
           for (int i = 0; i < 7; ++i) gq[2 + i] = __uint_as_float(r[5 + i]);
+          if constexpr (kSE2) {  // SE(2) (R24): df/db = -R(theta) g0_xy, df/dtheta = g0_x p'_y - g0_y p'_x
+            float sn, cs;
+            __sincosf(S.qn[s][it & 1][2], &sn, &cs);
+            const float gx = __uint_as_float(r[0]), gy = __uint_as_float(r[1]);
+            const float2 pp = S.pprime[s][it & 1][row];
+            gq[0] = -(cs * gx - sn * gy);
+            gq[1] = -(sn * gx + cs * gy);
+            gq[2] = gx * pp.y - gy * pp.x;
+          }
           if (a.detect) {
             named_bar_sync(3 + s, 128);  // S.sbase[s] (written at phase 8 by row 0) is visible
+            if (tr) tr[2] = clock64();  // (phase-11 detail: barrier passed)
             const int base = S.sbase[s];
             ridx = (ridx >= 0 && base >= 0) ? base + ridx : -1;
             if (ridx >= 0) {
@@ -612,9 +704,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
           } else if (a.grads && slot < lb) {
             float *o = a.grads + ((int64_t)w * lb + slot) * kNdof;
             if (a.project) {  // NEXT-3: q_z = q - f M^{-1} grad_q f (Theorem 1.2)
-              const float *qw = a.q + (int64_t)w * kNdof;
+              const float *qw = S.qn[s][it & 1];
 #pragma unroll
-              for (int i = 0; i < kNdof; ++i) o[i] = live ? __ldg(qw + i) - (f * gq[i]) * a.minv[i] : 0.f;
+              for (int i = 0; i < kNdof; ++i) o[i] = live ? qw[i] - (f * gq[i]) * a.minv[i] : 0.f;
             } else {
 #pragma unroll
               for (int i = 0; i < kNdof; ++i) o[i] = live ? gq[i] : 0.f;
@@ -716,14 +808,15 @@ __global__ void __launch_bounds__(128, 1) k_selftest_umma(const float *A, const 
 template <bool F16>
 cudaError_t launch_tc_t(const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s) {
   const int smem = (int)sizeof(SmemTC) + 1024;
-  cudaError_t e = cudaFuncSetAttribute(k_mlp_tc<F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  auto kern = a.frame ? k_mlp_tc<F16, true> : k_mlp_tc<F16, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   // a partitioned detect knows its tile count on the device only: one CTA per SM
   const int64_t n_tiles = a.part.tile_wp ? 2 * (int64_t)num_sms : (int64_t)a.n_wp * a.tiles_per_wp;
   int64_t grid = (n_tiles + 1) / 2;
   if (grid > num_sms) grid = num_sms;
   if (grid < 1) return cudaSuccess;
-  k_mlp_tc<F16><<<(unsigned)grid, kThreads, smem, s>>>(w, a);
+  kern<<<(unsigned)grid, kThreads, smem, s>>>(w, a);
   return cudaGetLastError();
 }
 

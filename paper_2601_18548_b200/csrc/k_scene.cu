@@ -27,17 +27,22 @@ __global__ void k_fill_dead(float4 *__restrict__ pts, int64_t n) {
 // point loads are issued before the stores (4 x 16 B in flight per thread), and the
 // pair index needs no 64-bit division.
 __global__ void __launch_bounds__(256) k_pairgen(const float4 *__restrict__ pts, int64_t lb,
-                                                 const float *__restrict__ q, float4 *__restrict__ out) {
+                                                 const float *__restrict__ q, int frame, float4 *__restrict__ out) {
   const int64_t w = blockIdx.y;
   const int64_t s0 = (int64_t)blockIdx.x * 1024 + threadIdx.x;
   const float qx = __ldg(q + w * kNdof), qy = __ldg(q + w * kNdof + 1);
+  float cth = 1.f, sth = 0.f;  // SE(2) frame (R24): p'_xy = R(-theta)(p_xy - b)
+  if (frame) sincosf(__ldg(q + w * kNdof + 2), &sth, &cth);
   float4 p[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) p[k] = s0 + 256 * k < lb ? __ldg(pts + s0 + 256 * k) : make_float4(0.f, 0.f, 0.f, 0.f);
   float4 *o = out + w * lb;
 #pragma unroll
   for (int k = 0; k < 4; ++k)
-    if (s0 + 256 * k < lb) __stcs(o + s0 + 256 * k, make_float4(p[k].x - qx, p[k].y - qy, p[k].z, p[k].w));
+    if (s0 + 256 * k < lb) {
+      const float dx = p[k].x - qx, dy = p[k].y - qy;
+      __stcs(o + s0 + 256 * k, make_float4(cth * dx + sth * dy, -sth * dx + cth * dy, p[k].z, p[k].w));
+    }
 }
 
 }  // namespace
@@ -59,11 +64,11 @@ cudaError_t launch_fill(float4 *pts, int64_t n, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_pairgen(const float4 *pts, int64_t local_bound, const float *q, int32_t n_wp, float4 *out,
+cudaError_t launch_pairgen(const float4 *pts, int64_t local_bound, const float *q, int32_t n_wp, int frame, float4 *out,
                            cudaStream_t s) {
   if (local_bound <= 0 || n_wp <= 0) return cudaSuccess;
   const dim3 grid((unsigned)((local_bound + 1023) / 1024), (unsigned)n_wp);
-  k_pairgen<<<grid, 256, 0, s>>>(pts, local_bound, q, out);
+  k_pairgen<<<grid, 256, 0, s>>>(pts, local_bound, q, frame, out);
   return cudaGetLastError();
 }
 

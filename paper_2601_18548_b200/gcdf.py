@@ -14,10 +14,11 @@ import numpy as np
 import torch
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = Path(os.environ.get("GCDF_LIB", _PKG / "libgcdf.so"))  # GCDF_LIB: dev builds (tools/variants.py)
+LIB_PATH = Path(os.environ.get("GCDF_LIB") or _PKG / "libgcdf.so")  # GCDF_LIB: dev builds (tools/variants.py)
 
 FP32, BF16, FP16 = 0, 1, 2
 TGRAD_CHAINRULE, TGRAD_QCHANNEL = 0, 1
+FRAME_TRANSLATE, FRAME_SE2 = 0, 1  # gcdf_frame (include/gcdf.h; R24)
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "IO", -3: "BAD_MAGIC", -4: "VERSION", -5: "DIM_MISMATCH",
           -6: "NOT_LOADED", -7: "CAPACITY", -8: "UNKNOWN_ID", -9: "NONFINITE", -10: "CUDA",
           -11: "UNSUPPORTED"}
@@ -41,7 +42,7 @@ class GcdfError(RuntimeError):
 class Options(C.Structure):
     _fields_ = [("precision", C.c_int32), ("tgrad_mode", C.c_int32), ("scene_capacity", C.c_int64),
                 ("max_waypoints", C.c_int32), ("max_active", C.c_int64), ("rank", C.c_int32),
-                ("world", C.c_int32), ("max_candidates", C.c_int64)]
+                ("world", C.c_int32), ("max_candidates", C.c_int64), ("frame", C.c_int32)]
 
 
 _lib = None
@@ -158,7 +159,7 @@ class Context:
 
     def __init__(self, device: int = 0, precision: int = FP16, tgrad_mode: int = TGRAD_CHAINRULE,
                  scene_capacity: int = 1 << 20, max_waypoints: int = 256, max_active: int = 1 << 22,
-                 rank: int = 0, world: int = 1, max_candidates: int = 0):
+                 rank: int = 0, world: int = 1, max_candidates: int = 0, frame: int = 0):
         self.lib = load_library()
         if not torch.cuda.is_available():
             raise RuntimeError("libgcdf needs a CUDA device (B200); no CPU path exists")
@@ -167,7 +168,7 @@ class Context:
         self.lib.gcdf_default_options(C.byref(o))
         o.precision, o.tgrad_mode, o.scene_capacity = precision, tgrad_mode, scene_capacity
         o.max_waypoints, o.max_active, o.rank, o.world = max_waypoints, max_active, rank, world
-        o.max_candidates = max_candidates
+        o.max_candidates, o.frame = max_candidates, frame
         self.opts = o
         h = C.c_void_p()
         rc = self.lib.gcdf_create(device, C.byref(o), C.byref(h))

@@ -33,8 +33,8 @@ def test_default_options_and_struct_layout(lib):
     lib.gcdf_default_options(C.byref(o))
     assert (o.precision, o.tgrad_mode, o.world, o.rank) == (2, 0, 1, 0)
     assert o.scene_capacity == 1 << 20 and o.max_waypoints == 256 and o.max_active == 1 << 22
-    assert o.max_candidates == 0
-    assert C.sizeof(Options) == 48  # int32, int32, int64, int32 (+4), int64, int32, int32, int64
+    assert o.max_candidates == 0 and o.frame == 0
+    assert C.sizeof(Options) == 56  # int32, int32, int64, int32 (+4), int64, int32, int32, int64, int32 (+4)
 
 
 def test_create_without_gpu_fails_cleanly(lib):
@@ -51,6 +51,13 @@ def test_create_without_gpu_fails_cleanly(lib):
     lib.gcdf_default_options(C.byref(o))
     o.world, o.rank = 2, 2
     assert lib.gcdf_create(0, C.byref(o), C.byref(h)) == -1
+    # frame: only TRANSLATE / SE2, and SE2 has no q^t channel (R24)
+    lib.gcdf_default_options(C.byref(o))
+    o.frame = 2
+    assert lib.gcdf_create(0, C.byref(o), C.byref(h)) == -1
+    o.frame, o.tgrad_mode = 1, 1
+    assert lib.gcdf_create(0, C.byref(o), C.byref(h)) == -1
+    assert not h.value
 
 
 def test_binding_refuses_without_gpu():

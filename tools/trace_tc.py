@@ -81,3 +81,16 @@ for s in (0, 1):
         print(f"  s{s} p{p:2d}: issue {v[2 * s]:7.0f} .. {v[2 * s + 1]:7.0f} | mma done {md - v[2 * s + 1]:+6.0f} after issue end"
               f" | epi {last - md:5.0f} | MMA thread wakes {nxt - last:+6.0f} after last arrival"
               f" (wait {w[2 * s] - last:+6.0f} .. {w[2 * s + 1] - last:+6.0f}, fence {nxt - w[2 * s + 1]:4.0f})")
+# per-warp view of the two long phases (k = 6: output layer, k = 12: tile boundary)
+print("per warp (slot 0, tiles 1..2 mean): k, warp: mma-done -> load-done, load-done -> compute-done, mma-done -> arrived")
+for k in (6, 12):
+    for w in range(8):
+        v = t[1 + w, 1:3, k]
+        print(f"  k{k:2d} w{w}: {np.nanmean(v[:, 0] - v[:, 1]):7.0f} {np.nanmean(v[:, 2] - v[:, 0]):7.0f} "
+              f"{np.nanmean(v[:, 3] - v[:, 1]):7.0f}")
+print("phase 11 detail (slot 0, tiles 1..2 mean), per warp: stage_a1 end -> tile_pair done -> barrier -> end")
+for w in range(4):
+    v = t[1 + w, 1:3]
+    a0 = v[:, 12, 2]
+    print(f"  w{w}: tile_pair {np.nanmean(v[:, 0, 1] - a0):6.0f}  barrier {np.nanmean(v[:, 0, 2] - a0):6.0f}  "
+          f"end {np.nanmean(v[:, 12, 3] - a0):6.0f}")
