@@ -1,6 +1,6 @@
 """bench.py -- GCDF value+grad queries/s with active-set detection on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--precision fp16|bf16|fp32]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--precision fp16|bf16|fp32|fp16x3]
     python bench.py --impl reference ...      # the float64 CPU oracle on host cores
 
 One step = one SCO iteration of the hot path (all SURVEY §8(a) rows): an incremental
@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C5")
-    ap.add_argument("--precision", default="auto", choices=["auto", "fp16", "bf16", "fp32"])
+    ap.add_argument("--precision", default="auto", choices=["auto", "fp16", "bf16", "fp32", "fp16x3"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -166,7 +166,7 @@ def main():
         return
     import torch
     import torch.distributed as dist
-    from paper_2601_18548_b200 import BF16, FP16, FP32, Context
+    from paper_2601_18548_b200 import BF16, FP16, FP16X3, FP32, Context
     from paper_2601_18548_b200.dist import gather_active_sets
     from paper_2601_18548_b200.gcdf import load_library
 
@@ -190,7 +190,7 @@ def main():
     n_wp = cfg.B * cfg.N
     slack = 4096
     max_active = int(min(cfg.pairs // world + 1024, max(4 * cfg.pairs // 100 // world, 1 << 16)))
-    ctx = Context(local, precision={"fp16": FP16, "bf16": BF16, "fp32": FP32}[prec], scene_capacity=cfg.M + slack,
+    ctx = Context(local, precision={"fp16": FP16, "bf16": BF16, "fp32": FP32, "fp16x3": FP16X3}[prec], scene_capacity=cfg.M + slack,
                   max_waypoints=n_wp, max_active=max_active, rank=rank, world=world,
                   max_candidates=(cfg.pairs // world + 4096) if a.partition_radius > 0 else 0)
     ctx.load_weights(synth.weights_path(cfg.H))
@@ -267,8 +267,10 @@ def main():
     # roofline of the dominant kernel (fused MLP): algorithmic flops per launch / live duration
     peaks, peak_src = measured_peaks()
     local_pairs = n_wp * (n_live_total / a.steps) / world
-    if prec in ("bf16", "fp16"):
-        flops = FLOPS_PAIR_TENSOR[cfg.H] * local_pairs
+    if prec in ("bf16", "fp16", "fp16x3"):
+        # fp16x3 (K2c): the split arithmetic runs every hidden GEMM 3 times (R25)
+        n_terms = 3 if prec == "fp16x3" else 1
+        flops = n_terms * FLOPS_PAIR_TENSOR[cfg.H] * local_pairs
         achieved = flops / (mlp_ms / mlp_n / 1e3) / 1e12
         # the kernel is timed back to back over the whole timed region: the sustained figure
         # applies once that region lasts seconds (B200_PROFILING.md); fp16 and bf16 share the
@@ -277,8 +279,9 @@ def main():
         peak = float(peaks.get(key))
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "traffic": None, "peak_source": f"{peak_src} {key} (MEASURED_PEAKS.json; fp16 dense = bf16 dense)",
-                "kernel": "k_mlp_tc (fused transform + MLP fwd/bwd + threshold/min/compaction)",
-                "kernel_ms_avg": mlp_ms / mlp_n, "flops_per_pair": FLOPS_PAIR_TENSOR[cfg.H]}
+                "kernel": ("k_mlp_tc3" if n_terms == 3 else "k_mlp_tc") +
+                          " (fused transform + MLP fwd/bwd + threshold/min/compaction)",
+                "kernel_ms_avg": mlp_ms / mlp_n, "flops_per_pair": n_terms * FLOPS_PAIR_TENSOR[cfg.H]}
     else:
         sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
         peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12   # FP32 FFMA: 148 SMs x 128 lanes x 2 flops x clock
@@ -289,7 +292,7 @@ def main():
                 "kernel": "k_mlp_simt (fused transform + MLP fwd/bwd + threshold/min/compaction)",
                 "kernel_ms_avg": mlp_ms / mlp_n, "flops_per_pair": FLOPS_PAIR_TOTAL[cfg.H]}
     tf = ROOT / "profiles" / "traffic.json"
-    if tf.exists() and prec in ("bf16", "fp16"):
+    if tf.exists() and prec in ("bf16", "fp16"):  # (measured for k_mlp_tc only)
         t = json.loads(tf.read_text()).get("k_mlp_tc")
         if t:
             roof["traffic"] = t["bytes"]

@@ -59,9 +59,12 @@ enum gcdf_status {
 enum gcdf_precision {
   GCDF_FP32 = 0, /* fp32 SIMT path: parity path, tolerance 1e-4 rel / 1e-5 abs */
   GCDF_BF16 = 1, /* tcgen05 tensor-core path, bf16 operands, fp32 accumulate */
-  GCDF_FP16 = 2  /* tcgen05 tensor-core path, fp16 operands, fp32 accumulate: same tensor peak as
+  GCDF_FP16 = 2, /* tcgen05 tensor-core path, fp16 operands, fp32 accumulate: same tensor peak as
                     bf16 with 3 more significand bits; meets the north-star tensor-path tolerance
                     (R17, §5); the default */
+  GCDF_FP16X3 = 3 /* fp32-accurate tcgen05 path (NEXT-4): every hidden GEMM on 3-term split fp16
+                    operands (a_hi w_hi + a_lo w_hi + a_hi w_lo), weights streamed from L2; meets
+                    the fp32 tolerance of GCDF_FP32 (R25, §5 "K2c"); needs H = 128 */
 };
 
 enum gcdf_tgrad {

@@ -31,7 +31,7 @@ constexpr int kEvPool = 64;
 inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
 struct Layout {
-  int64_t pts, wf32, wbf16, wf16, meta, staging, wp_key, wp_count, counter, upd_payload, upd_slots;
+  int64_t pts, wf32, wbf16, wf16, wf16x3, meta, staging, wp_key, wp_count, counter, upd_payload, upd_slots;
   int64_t h_q, h_out, h_offs, h_wmin, h_warg, h_count;
   int64_t p_grid, p_bbox, p_cell_count, p_cell_start, p_cell_fill, p_cell_items, p_cell_xy, p_bitmap, p_chunk_cnt, p_chunk_off,
       p_scan_tmp, p_cand, p_cand_start, p_cand_count, p_tile_start, p_tile_wp, p_n_tiles, p_words, p_nchunk;
@@ -49,6 +49,8 @@ constexpr int64_t kBfW1t = 16LL * kMaxH * 2;
 constexpr int64_t kBfB1 = 32LL * kMaxH * 2;    // layer-1 split weights [128][K = 32], no swizzle
 constexpr int64_t kBfBext = 16LL * kMaxH * 2;  // per hidden layer bias block [128][K = 16], no swizzle
 constexpr int64_t kBfTotal = 5 * kBfMat + kBfW1t + kBfB1 + 5 * kBfBext;
+// GCDF_FP16X3 block: 5 x [W_l hi | W_l lo] SW128 images, then W1^T hi, lo
+constexpr int64_t kX3Total = 5 * 2 * kBfMat + 2 * kBfW1t;
 
 }  // namespace
 
@@ -171,11 +173,13 @@ WeightsF32 f32_view(const gcdf_ctx *c) {
 WeightsBF16 bf16_view(const gcdf_ctx *c) {
   WeightsF32 f = f32_view(c);
   WeightsBF16 w{};
-  const int64_t wo = c->opt.precision == GCDF_FP16 ? c->L.wf16 : c->L.wbf16;
+  const int64_t wo = c->opt.precision == GCDF_BF16 ? c->L.wbf16 : c->L.wf16;
   w.w_sw128 = c->ws + wo;
   w.w1t_sw128 = c->ws + wo + 5 * kBfMat;
   w.b1_nosw = c->ws + wo + 5 * kBfMat + kBfW1t;
   w.bext_nosw = c->ws + wo + 5 * kBfMat + kBfW1t + kBfB1;
+  w.w3_sw128 = c->ws + c->L.wf16x3;
+  w.w1t3_sw128 = c->ws + c->L.wf16x3 + 5 * 2 * kBfMat;
   w.bh = f.bias[0];  // the five fp32 bias rows are contiguous in the fp32 block
   w.w7 = f.w7;
   w.b7 = f.b7;
@@ -323,7 +327,8 @@ int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out) {
   if (opt) o = *opt;
   if (o.scene_capacity <= 0 || o.scene_capacity >= (1LL << 32) || o.max_waypoints <= 0 || o.max_active <= 0 ||
       o.max_active >= (1LL << 31) || o.world < 1 || o.rank < 0 || o.rank >= o.world ||
-      (o.precision != GCDF_FP32 && o.precision != GCDF_BF16 && o.precision != GCDF_FP16) ||
+      (o.precision != GCDF_FP32 && o.precision != GCDF_BF16 && o.precision != GCDF_FP16 &&
+       o.precision != GCDF_FP16X3) ||
       (o.tgrad_mode != GCDF_TGRAD_CHAINRULE && o.tgrad_mode != GCDF_TGRAD_QCHANNEL) ||
       (o.frame != GCDF_FRAME_TRANSLATE && o.frame != GCDF_FRAME_SE2) ||
       (o.frame == GCDF_FRAME_SE2 && o.tgrad_mode == GCDF_TGRAD_QCHANNEL))  // R24: theta is not a channel in SE(2)
@@ -350,6 +355,7 @@ int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out) {
   L.wf32 = off; L.wf32_bytes = kF32Total * 4; off = align256(off + L.wf32_bytes);
   L.wbf16 = off; L.wbf16_bytes = kBfTotal; off = align256(off + kBfTotal);
   L.wf16 = off; off = align256(off + kBfTotal);
+  L.wf16x3 = off; off = align256(off + kX3Total);
   L.meta = off; off = align256(off + (int64_t)o.max_waypoints * c->tiles_cap * 8);
   L.staging = off; off = align256(off + o.max_active * (int64_t)sizeof(gcdf_active_t));
   L.wp_key = off; off = align256(off + (int64_t)o.max_waypoints * 8);
@@ -555,7 +561,32 @@ int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
       }
     }
   }
+  // ---- GCDF_FP16X3 (K2c): fp16 hi/lo split of the f64 weights, [W_l hi | W_l lo] per layer ----
+  std::vector<uint16_t> x3((size_t)kX3Total / 2, 0);
+  if (H == 128) {
+    std::vector<float> mh((size_t)H * H), ml((size_t)H * H);
+    float hi, lo;
+    for (int li = 0; li < 5; ++li) {
+      for (size_t i = 0; i < mh.size(); ++i) {
+        split16(Wd[li + 1][i], true, hi, lo);
+        mh[i] = hi;
+        ml[i] = lo;
+      }
+      pack_sw128(mh, H, H, x3.data() + (size_t)(2 * li) * kBfMat / 2, true);
+      pack_sw128(ml, H, H, x3.data() + (size_t)(2 * li + 1) * kBfMat / 2, true);
+    }
+    std::vector<float> th((size_t)16 * H, 0.f), tl((size_t)16 * H, 0.f);  // W1^T [n][k]
+    for (int n = 0; n < kNin; ++n)
+      for (int k = 0; k < H; ++k) {
+        split16(Wd[0][(size_t)k * kNin + n], true, hi, lo);
+        th[(size_t)n * H + k] = hi;
+        tl[(size_t)n * H + k] = lo;
+      }
+    pack_sw128(th, 16, H, x3.data() + (size_t)10 * kBfMat / 2, true);
+    pack_sw128(tl, 16, H, x3.data() + (size_t)(10 * kBfMat + kBfW1t) / 2, true);
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CK(c, cudaMemcpyAsync(c->ws + c->L.wf16x3, x3.data(), x3.size() * 2, cudaMemcpyHostToDevice, s), "weights H2D");
   CK(c, cudaMemcpyAsync(c->ws + c->L.wf32, f32.data(), f32.size() * 4, cudaMemcpyHostToDevice, s), "weights H2D");
   CK(c, cudaMemcpyAsync(c->ws + c->L.wbf16, bf.data(), bf.size() * 2, cudaMemcpyHostToDevice, s), "weights H2D");
   CK(c, cudaMemcpyAsync(c->ws + c->L.wf16, hf.data(), hf.size() * 2, cudaMemcpyHostToDevice, s), "weights H2D");
@@ -674,7 +705,9 @@ static cudaError_t run_mlp(gcdf_ctx *c, const QueryArgs &a, cudaStream_t s) {
   }
   cudaError_t e = c->opt.precision == GCDF_FP32
                       ? launch_mlp_simt(c->H, f32_view(c), a, c->num_sms, s)
-                      : launch_mlp_tc(c->H, c->opt.precision == GCDF_FP16, bf16_view(c), a, c->num_sms, s);
+                      : c->opt.precision == GCDF_FP16X3
+                            ? launch_mlp_tc3(bf16_view(c), a, c->num_sms, s)
+                            : launch_mlp_tc(c->H, c->opt.precision == GCDF_FP16, bf16_view(c), a, c->num_sms, s);
   if (slot >= 0) cudaEventRecord(c->ev[2 * slot + 1], s);
   return e;
 }

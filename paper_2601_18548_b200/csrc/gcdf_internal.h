@@ -45,6 +45,8 @@ struct WeightsBF16 {
   const void *b1_nosw;   // H * 32 * 2 bytes
   const void *bext_nosw; // 5 * H * 16 * 2 bytes
   const float *bh;       // [5][H] fp32 biases of layers 2..6 (epilogue-add variant)
+  const void *w3_sw128;  // (GCDF_FP16X3) 5 x [hi | lo] SW128 images of W_2..W_6, 64 KB each
+  const void *w1t3_sw128;  // (GCDF_FP16X3) W1^T [16][H] hi, lo (SW128), 4 KB each
   const float *w7;       // [H] fp32
   float b7;
 };
@@ -138,6 +140,7 @@ cudaError_t launch_pairgen(const float4 *pts, int64_t local_bound, const float *
 cudaError_t launch_detect_init(DetectScratch ds, int32_t n_wp, cudaStream_t s);
 cudaError_t launch_mlp_simt(int H, const WeightsF32 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
 cudaError_t launch_mlp_tc(int H, bool f16, const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
+cudaError_t launch_mlp_tc3(const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
 bool tc_compiled();
 cudaError_t launch_selftest_umma(int mode, const float *A, const float *B, float *D, cudaStream_t s);
 // standalone A6-A8 over dense values (two passes; writes the ordered output directly)

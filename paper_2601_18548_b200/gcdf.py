@@ -16,7 +16,7 @@ import torch
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ.get("GCDF_LIB") or _PKG / "libgcdf.so")  # GCDF_LIB: dev builds (tools/variants.py)
 
-FP32, BF16, FP16 = 0, 1, 2
+FP32, BF16, FP16, FP16X3 = 0, 1, 2, 3  # FP16X3: fp32-accurate tensor-core path (3-term split)
 TGRAD_CHAINRULE, TGRAD_QCHANNEL = 0, 1
 FRAME_TRANSLATE, FRAME_SE2 = 0, 1  # gcdf_frame (include/gcdf.h; R24)
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "IO", -3: "BAD_MAGIC", -4: "VERSION", -5: "DIM_MISMATCH",

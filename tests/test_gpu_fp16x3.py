@@ -1,0 +1,156 @@
+"""GPU parity of the fp32-accurate tensor-core path (GCDF_FP16X3, K2c, R25)
+against the float64 oracle, through the C ABI, at the fp32 path's tolerances
+(1e-4 relative / 1e-5 absolute, gradients except within 1e-4 of a ReLU kink).
+
+C2 on 24 waypoints (240,000 pairs; 79 tiles per waypoint with a ragged last tile, so each
+CTA runs several tile pairs and the weight-streaming ring wraps many times), plus the
+range-partitioned detect (device-side tile count), the SE(2) frame, and C5 at full size on
+sampled pairs.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import (BAND_FP32, DELTA, KINK_FP32, check_fp32_dense, compare_active_sets, fp32_close,
+                      oracle_detect, oracle_mlp, records_np)
+
+pytestmark = pytest.mark.gpu
+NT = max(1, min(os.cpu_count() or 1, 64))
+X3 = 3
+
+
+def _ctx(cfg, **kw):
+    from paper_2601_18548_b200 import Context
+    ctx = Context(0, precision=X3, scene_capacity=cfg.M + 4096, max_waypoints=cfg.B * cfg.N,
+                  max_active=min(cfg.pairs, 1 << 22), **kw)
+    ctx.load_weights(synth.weights_path(cfg.H))
+    return ctx
+
+
+@pytest.fixture(scope="module")
+def c2x():
+    cfg = synth.get_config("C2")
+    pts, _ = synth.make_scene_points(cfg)
+    q = synth.make_waypoints(cfg)[:, :24]
+    m = oracle_mlp(cfg)
+    full = m.eval(pts, q.reshape(-1, 9), want_kappa=True, nthreads=NT)
+    return cfg, pts, q, m, full
+
+
+def test_x3_dense(c2x):
+    cfg, pts, q, m, full = c2x
+    ctx = _ctx(cfg)
+    ctx.update_scene(pts)
+    v, g = ctx.query_values_grads(torch.from_numpy(q))
+    torch.cuda.synchronize()
+    M = len(pts)
+    vn, gn = v.cpu().numpy(), g.cpu().numpy()
+    nk = check_fp32_dense(vn[:, :M], gn[:, :M], full["f"], full["g"], full["kappa"], what="C2 fp16x3")
+    assert np.all(np.isinf(vn[:, M:])) and np.all(gn[:, M:] == 0)
+    # typical error far inside the tolerance (the 3-term split drops only a_lo w_lo)
+    rel = np.abs(vn[:, :M] - full["f"]) / (1e-5 + 1e-4 * np.abs(full["f"]))
+    print(f"\nfp16x3 C2 dense: {vn[:, :M].size} pairs, value error / tolerance max {rel.max():.3f}, "
+          f"{nk} gradients differ near kinks")
+    assert rel.max() <= 0.5
+
+
+def test_x3_detect(c2x):
+    cfg, pts, q, m, full = c2x
+    tau = synth.load_tau(cfg.name)
+    ctx = _ctx(cfg)
+    ids = ctx.update_scene(pts)
+    out = ctx.detect_active_set(torch.from_numpy(q), DELTA, tau)
+    torch.cuda.synchronize()
+    gpu = records_np(out)
+    orc = oracle_detect(m, pts, ids, q.reshape(-1, 9), tau, nthreads=NT)
+
+    def gchk(gg, og, kap):
+        bad = ~np.all(fp32_close(gg, og), axis=-1)
+        assert not (bad & (kap > KINK_FP32)).any()
+
+    nd, nc = compare_active_sets(gpu, orc, full["f"], ids, BAND_FP32, grad_check=gchk, kappa_full=full["kappa"],
+                                 what="fp16x3")
+    assert nc > 0 and nd <= 0.01 * nc + 2
+    assert np.all(fp32_close(out["wp_min"].cpu().numpy(), orc["wp_min"]))
+    # the fused detect equals the dense query + compaction of the same context
+    v, g = ctx.query_values_grads(torch.from_numpy(q))
+    a = records_np(ctx.compact_dense(v, g, DELTA, tau))
+    for k in ("wp", "pt", "value", "grad"):
+        assert np.array_equal(a[k], gpu[k]), k
+
+
+def test_x3_partitioned_matches_oracle(c2x):
+    cfg, pts, q, m, full = c2x
+    tau = synth.load_tau(cfg.name)
+    from paper_2601_18548_b200 import Context
+    ctx = Context(0, precision=X3, scene_capacity=cfg.M + 4096, max_waypoints=cfg.B * cfg.N,
+                  max_active=min(cfg.pairs, 1 << 22), max_candidates=cfg.pairs)
+    ctx.load_weights(synth.weights_path(cfg.H))
+    ids = ctx.update_scene(pts)
+    out = ctx.detect_active_set_partitioned(torch.from_numpy(q), 1.8, DELTA, tau)
+    torch.cuda.synchronize()
+    gpu = records_np(out)
+    orc = m.detect(pts, ids, q.reshape(-1, 9), DELTA, tau, nthreads=NT, radius=1.8)
+    orc["_tau"] = tau
+    nd, nc = compare_active_sets(gpu, orc, full["f"], ids, BAND_FP32, what="fp16x3 partitioned")
+    assert nc > 0 and nd <= 0.01 * nc + 2
+
+
+def test_x3_se2_dense(c2x):
+    from paper_2601_18548_b200 import FRAME_SE2
+    cfg, pts, q, m, _ = c2x
+    qq = q[:, :8]
+    ex = m.eval(pts, qq.reshape(-1, 9), flags=oracle.FRAME_SE2, want_kappa=True, nthreads=NT)
+    ctx = _ctx(cfg, frame=FRAME_SE2)
+    ctx.update_scene(pts)
+    v, g = ctx.query_values_grads(torch.from_numpy(qq))
+    torch.cuda.synchronize()
+    M = len(pts)
+    vn, gn = v.cpu().numpy()[:, :M], g.cpu().numpy()[:, :M]
+    # theta gradient = g0_x p'_y - g0_y p'_x: judged relative to its terms (test_gpu_se2.py)
+    check_fp32_dense(vn, np.delete(gn, 2, axis=-1), ex["f"], np.delete(ex["g"], 2, axis=-1), ex["kappa"],
+                     what="fp16x3 SE(2)")
+    Q = qq.reshape(-1, 9)
+    r = np.hypot(pts[None, :, 0] - Q[:, None, 0], pts[None, :, 1] - Q[:, None, 1])
+    gxy = np.hypot(ex["g"][..., 0], ex["g"][..., 1])
+    bad = np.abs(gn[..., 2] - ex["g"][..., 2]) > 1e-5 + 1e-4 * (np.abs(ex["g"][..., 2]) + r * gxy)
+    assert not (bad & (ex["kappa"] > KINK_FP32)).any()
+
+
+def test_x3_c5_full_size_sampled():
+    """C5 (256 waypoints x 1M points) in the launch configuration the bench times: the
+    full-size fused detect's memberships on sampled pairs (outside the fp32 band) and the
+    dense query of the sampled waypoints vs the oracle at the fp32 tolerance."""
+    cfg = synth.get_config("C5")
+    pts, _ = synth.make_scene_points(cfg)
+    q = synth.make_waypoints(cfg)
+    tau = synth.load_tau(cfg.name)
+    ctx = _ctx(cfg)
+    ids = ctx.update_scene(pts)
+    out = ctx.detect_active_set(torch.from_numpy(q), DELTA, tau)
+    torch.cuda.synchronize()
+    gpu = records_np(out)
+    rng = np.random.default_rng(11)
+    m = oracle_mlp(cfg)
+    Q = q.reshape(-1, 9)
+    wsel = np.sort(rng.choice(Q.shape[0], 3, replace=False))
+    psel = np.sort(rng.choice(len(pts), 4096, replace=False))
+    ex = m.eval(pts[psel], Q[wsel], want_kappa=True, nthreads=NT)
+    v, g = ctx.query_values_grads(torch.from_numpy(Q[wsel].reshape(1, -1, 9)))
+    check_fp32_dense(v.cpu().numpy()[:, psel], g.cpu().numpy()[:, psel], ex["f"], ex["g"], ex["kappa"],
+                     what="C5 fp16x3 sampled")
+    recset = set(zip(gpu["wp"].tolist(), gpu["pt"].tolist()))
+    thr = tau + DELTA
+    checked = 0
+    for wi, w in enumerate(wsel):
+        for pj, pid in enumerate(psel):
+            f = ex["f"][wi, pj]
+            if abs(f - thr) > BAND_FP32:
+                assert ((int(w), int(ids[pid])) in recset) == (f <= thr), (w, pid, f)
+                checked += 1
+    assert checked > 0.95 * len(wsel) * len(psel)
+    assert np.all(out["wp_min"].cpu().numpy()[wsel] <= ex["f"].min(axis=1) + 1e-4)
