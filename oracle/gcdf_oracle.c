@@ -22,6 +22,9 @@
  *       by utilizing the gradients of obstacle point positions"):
  *       grad_q f = [-g0[0], -g0[1], g0[5], ..., g0[11]]   (TGRAD_QCHANNEL: g0[3], g0[4])
  *       ReLU'(0) = 0.
+ *       Softplus variant (MLPW activation 2, NEXT-4, R26): h_l = log(1 + e^z_l),
+ *       sigma'(z) = 1 / (1 + e^-z) (SPEC.md:281 picks softplus for smoothness; the paper
+ *       names no activation).
  *       FRAME_SE2 (NEXT-4 variant, R24): p' = R(-theta)(p_xy - b) and the theta
  *       channel fed zero; grad by the chain rule through the rotation.
  *   O6  active <=> f - delta <= tau  (constraint f - delta >= 0, PAPER.md:362-363;
@@ -59,7 +62,7 @@
 #define OR_NIN 12
 
 typedef struct {
-  int act; /* 0 identity, 1 ReLU */
+  int act; /* 0 identity, 1 ReLU, 2 softplus (NEXT-4 variant, R26) */
   int L;   /* number of affine layers */
   int dims[OR_MAXL + 1];
   double *W[OR_MAXL]; /* [dims[l+1]][dims[l]] row-major */
@@ -88,6 +91,22 @@ static double f16r(double v) {
   float f = (float)v;
   _Float16 h = (_Float16)f;
   return (double)(float)h;
+}
+
+/* softplus(z) = log(1 + e^z), written as max(z, 0) + log1p(e^-|z|) so that neither
+   exp overflows nor log1p loses the small tail (R26); its derivative is the
+   logistic sigmoid 1 / (1 + e^-z). */
+static double softplus(double z) { return (z > 0.0 ? z : 0.0) + log1p(exp(-fabs(z))); }
+static double sigmoid(double z) {
+  if (z >= 0.0) return 1.0 / (1.0 + exp(-z));
+  const double t = exp(z);
+  return t / (1.0 + t);
+}
+
+static double act_fwd(int act, double z) {
+  if (act == 1) return z > 0.0 ? z : 0.0;
+  if (act == 2) return softplus(z);
+  return z;
 }
 
 void or_free(omlp_t *m) {
@@ -119,7 +138,7 @@ int or_load(const char *path, omlp_t **out) {
   if (dims[0] != OR_NIN || dims[L] != 1) { fclose(fh); return OR_ERR_DIM; }
   for (uint32_t l = 0; l <= L; ++l)
     if (dims[l] == 0 || dims[l] > 4096) { fclose(fh); return OR_ERR_DIM; }
-  if (hdr[1] > 1) { fclose(fh); return OR_ERR_DIM; }
+  if (hdr[1] > 2) { fclose(fh); return OR_ERR_DIM; } /* 0 identity, 1 ReLU, 2 softplus */
   omlp_t *m = (omlp_t *)calloc(1, sizeof(omlp_t));
   if (!m) { fclose(fh); return OR_ERR_NOMEM; }
   m->act = (int)hdr[1];
@@ -210,7 +229,7 @@ static void eval_pair(const omlp_t *m, const double p[3], const double q[OR_NDOF
       zl[k] = acc + m->b[l][k];
       double az = fabs(zl[k]);
       if (az < kap) kap = az;
-      hout[k] = (m->act == 1) ? (zl[k] > 0.0 ? zl[k] : 0.0) : zl[k];
+      hout[k] = act_fwd(m->act, zl[k]);
     }
   }
   /* output layer (no activation) */
@@ -241,6 +260,16 @@ static void eval_pair(const omlp_t *m, const double p[3], const double q[OR_NDOF
     const double *zl = s->z + (size_t)l * MW;
     for (int k = 0; k < dout; ++k) {
       double d = (m->act == 1) ? (zl[k] > 0.0 ? 1.0 : 0.0) : 1.0;
+      if (m->act == 2) {
+        /* softplus'(z) = sigmoid(z).  EMU (tensor path, R26): the kernel keeps
+           only the rounded activation h~ = rnd(softplus(z)) of layers 1..L-2 (its MMA A
+           operand) and recovers sigmoid(z) = 1 - e^-softplus(z) from it; the last hidden
+           layer's derivative is taken from the fp32 pre-activation. */
+        if (emu_a && l < L - 2)
+          d = -expm1(-rnd(s->h[(size_t)(l + 1) * MW + k]));
+        else
+          d = sigmoid(zl[k]);
+      }
       double e = s->g[k] * d;
       if (emu_a) e = rnd(e); /* A operand of the backward GEMM (O8) */
       s->e[k] = e;

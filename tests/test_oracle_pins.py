@@ -559,3 +559,132 @@ def test_se2_frame_variant(mlp32):
     np.testing.assert_array_equal(a0["g"][..., [0, 1, 3, 4, 5, 6, 7, 8]], b0["g"][..., [0, 1, 3, 4, 5, 6, 7, 8]])
     with pytest.raises(oracle.OracleError):
         m.eval(pts, q, flags=S | oracle.TGRAD_QCHANNEL)
+
+
+# ------------------------------------------------------------------ softplus variant (NEXT-4, R26)
+@pytest.fixture(scope="module")
+def mlp32_softplus(tmp_path_factory):
+    _, dims, layers = synth.make_weights(32, seed=12)
+    p = tmp_path_factory.mktemp("w") / "h32sp.mlpw"
+    synth.write_mlpw(p, 2, dims, layers)
+    return oracle.MLP(p), (2, dims, layers)
+
+
+def test_softplus_hand_worked_example(tmp_path):
+    """Hand-worked softplus network (tests/golden/softplus_hand_example.json): every
+    softplus / sigmoid value along the path is ln 2, ln 3, 1/2, 3/4, 2/3 or 1/4."""
+    g = json.loads((GOLD / "softplus_hand_example.json").read_text())
+    layers = [(np.array(l["W"], float), np.array(l["b"], float)) for l in g["layers"]]
+    m = oracle.MLP(_write(tmp_path, "sphand.mlpw", 2, [12] + [1] * 6 + [1], layers))
+    assert m.act == 2
+    for case in g["cases"]:
+        out = m.eval(np.array([case["p"]]), np.array([case["q"]]))
+        assert abs(out["f"][0, 0] - case["f"]) <= 1e-12
+        np.testing.assert_allclose(out["g"][0, 0], case["grad"], rtol=0, atol=1e-12)
+
+
+def test_softplus_saturated_is_affine_closed_form(tmp_path):
+    """Every pre-activation >= 40: softplus(z) = z + log1p(e^-z) = z (1 + O(1e-19)) and
+    sigmoid(z) = 1 - O(1e-18), so the network equals the affine composition and the
+    gradient the mapped row of the product (same closed form as the identity activation)."""
+    rng = np.random.default_rng(21)
+    dims = [12, 9, 7, 8, 6, 5, 4, 1]
+    layers = [(rng.uniform(0.0, 0.05, (dims[i + 1], dims[i])), np.full(dims[i + 1], 60.0)) for i in range(7)]
+    m = oracle.MLP(_write(tmp_path, "spsat.mlpw", 2, dims, layers))
+    A, c = np.eye(12), np.zeros(12)
+    for W, b in layers:
+        A, c = W @ A, W @ c + b
+    pts = np.stack([rng.uniform(0, 3, 11), rng.uniform(0, 3, 11), rng.uniform(0, 2, 11)], 1)
+    q = np.concatenate([rng.uniform(-3, 0, (4, 2)), rng.uniform(0, 1, (4, 7))], 1)
+    out = m.eval(pts, q)
+    for w in range(q.shape[0]):
+        for j in range(pts.shape[0]):
+            x = np.concatenate([[pts[j, 0] - q[w, 0], pts[j, 1] - q[w, 1], pts[j, 2], 0, 0], q[w, 2:]])
+            f = (A @ x + c)[0]
+            assert abs(out["f"][w, j] - f) <= 1e-12 * abs(f)
+            row = A[0]
+            np.testing.assert_allclose(out["g"][w, j], np.concatenate([[-row[0], -row[1]], row[5:]]),
+                                       rtol=1e-12, atol=1e-15)
+
+
+def test_softplus_cutoff_is_constant(tmp_path):
+    """Every first-layer pre-activation <= -745 (e^z underflows to 0 in f64): h1 = 0 exactly
+    and sigma'(z1) = 0, so f is the network evaluated on h1 = 0 (independent of the input)
+    and the gradient vanishes."""
+    rng = np.random.default_rng(22)
+    _, dims, layers = synth.make_weights(8, seed=4)
+    layers[0] = (np.zeros_like(layers[0][0]), np.full(8, -800.0))
+    m = oracle.MLP(_write(tmp_path, "spcut.mlpw", 2, dims, layers))
+    pts, q = _rand_inputs(rng, 9, 3)
+    out = m.eval(pts, q)
+    assert np.all(out["f"] == out["f"][0, 0])
+    assert np.all(out["g"] == 0.0)
+    # the constant: softplus network on h1 = 0, written with numpy (log1p(exp)) layer by layer
+    h = np.zeros(8)
+    for W, b in layers[1:-1]:
+        z = W @ h + b
+        h = np.log1p(np.exp(z))
+    f = (layers[-1][0] @ h + layers[-1][1])[0]
+    assert abs(out["f"][0, 0] - f) <= 1e-12 * max(1, abs(f))
+
+
+def test_softplus_torch_autograd_float64(mlp32_softplus):
+    """Independent differentiation: torch float64 autograd with torch's softplus (threshold
+    raised to 50 so it never switches to the identity)."""
+    torch = pytest.importorskip("torch")
+    m, (_, dims, layers) = mlp32_softplus
+    rng = np.random.default_rng(23)
+    pts, q = _rand_inputs(rng, 64, 5)
+    out = m.eval(pts, q)
+    Ws = [(torch.tensor(W), torch.tensor(b)) for W, b in layers]
+    P = torch.tensor(pts)
+    for w in range(q.shape[0]):
+        qt = torch.tensor(q[w]).repeat(P.shape[0], 1).requires_grad_(True)
+        h = torch.cat([P[:, :2] - qt[:, :2], P[:, 2:3], torch.zeros(P.shape[0], 2, dtype=torch.float64),
+                       qt[:, 2:]], 1)
+        for li, (W, b) in enumerate(Ws):
+            h = h @ W.T + b
+            if li < len(Ws) - 1:
+                h = torch.nn.functional.softplus(h, beta=1.0, threshold=50.0)
+        f = h[:, 0]
+        (gq,) = torch.autograd.grad(f.sum(), qt)
+        np.testing.assert_allclose(out["f"][w], f.detach().numpy(), rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(out["g"][w], gq.numpy(), rtol=1e-10, atol=1e-12)
+
+
+def test_softplus_central_fd_and_invariance(mlp32_softplus):
+    """Central FD of all 9 components (smooth network: nothing skipped) and base-translation
+    invariance (bit-identical on dyadic inputs)."""
+    m, _ = mlp32_softplus
+    rng = np.random.default_rng(24)
+    pts, q = _rand_inputs(rng, 40, 5)
+    base = m.eval(pts, q)
+    for k in range(9):
+        h = 1e-5 * np.maximum(1.0, np.abs(q[:, k]))
+        qp, qm = q.copy(), q.copy()
+        qp[:, k] += h
+        qm[:, k] -= h
+        fd = (m.eval(pts, qp, want_grad=False)["f"] - m.eval(pts, qm, want_grad=False)["f"]) / (2 * h[:, None])
+        g = base["g"][:, :, k]
+        assert np.all(np.abs(fd - g) <= 1e-7 * np.maximum(1.0, np.abs(g))), k
+    pts, q = _rand_inputs(rng, 30, 3, dyadic=True)
+    a = m.eval(pts, q)
+    p2, q2 = pts.copy(), q.copy()
+    p2[:, :2] += [2.75, -4.5]
+    q2[:, :2] += [2.75, -4.5]
+    b = m.eval(p2, q2)
+    assert np.array_equal(a["f"], b["f"]) and np.array_equal(a["g"], b["g"])
+
+
+def test_softplus_emu_consistency(mlp32_softplus):
+    """EMU_FP16 (tensor-path rounding points, R26: 16-bit A operands, sigma' of layers 1..5
+    recovered as 1 - exp(-h~) from the rounded activation) stays within the 16-bit error
+    scale of the exact result (the recovery is exact for unrounded h: 1 - e^-softplus(z) =
+    sigmoid(z))."""
+    m, _ = mlp32_softplus
+    pts, q = _rand_inputs(np.random.default_rng(25), 64, 4)
+    d = m.eval(pts, q)
+    c = m.eval(pts, q, flags=oracle.EMU_FP16)
+    assert np.max(np.abs(c["f"] - d["f"])) <= 5e-3 * max(1.0, np.abs(d["f"]).max())
+    gn = np.linalg.norm(d["g"], axis=-1)
+    assert np.all(np.linalg.norm(c["g"] - d["g"], axis=-1) <= 1e-2 * np.maximum(1.0, gn))
