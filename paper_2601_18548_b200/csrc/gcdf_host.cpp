@@ -70,6 +70,7 @@ struct gcdf_ctx {
   // weights
   bool loaded = false;
   int H = 0;
+  int act = 1;  // MLPW activation: 1 ReLU (R9), 2 softplus (R26)
   float b7 = 0.f;
   // scene (replicated on every rank)
   std::vector<uint64_t> live;  // global id bitmap
@@ -473,7 +474,10 @@ int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
   bool ok = dims[0] == (uint32_t)kNin && dims[7] == 1 && (H == 32 || H == 128);
   for (int l = 1; l <= 6; ++l) ok = ok && dims[l] == (uint32_t)H;
   if (!ok) return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: dims must be [12, H x 6, 1], H in {32, 128}", path);
-  if (act != 1) return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: activation %u (only ReLU = 1 is supported, R9)", path, act);
+  if (act != 1 && act != 2)
+    return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: activation %u (ReLU = 1, R9, or softplus = 2, R26)", path, act);
+  if (act == 2 && c->opt.precision != GCDF_FP32)
+    return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: softplus (R26) runs on GCDF_FP32", path);
   if (c->opt.precision != GCDF_FP32 && H != 128)
     return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: the tensor-core path needs H = 128 (use GCDF_FP32 for H = %d)", path, H);
   std::vector<std::vector<double>> Wd(7), bd(7);
@@ -592,6 +596,7 @@ int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
   CK(c, cudaMemcpyAsync(c->ws + c->L.wf16, hf.data(), hf.size() * 2, cudaMemcpyHostToDevice, s), "weights H2D");
   CK(c, cudaStreamSynchronize(s), "weights sync");
   c->H = H;
+  c->act = (int)act;
   c->b7 = (float)bd[6][0];
   c->loaded = true;
   return GCDF_OK;
@@ -691,6 +696,7 @@ static QueryArgs make_args(gcdf_ctx *c, const float *q, int32_t nwp) {
   a.tiles_per_wp = (int32_t)(a.scene.local_bound / kTile);
   a.tgrad = c->opt.tgrad_mode;
   a.frame = c->opt.frame;
+  a.act = c->act;
   a.trace = c->trace;
   return a;
 }

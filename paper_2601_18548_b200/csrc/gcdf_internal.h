@@ -86,6 +86,7 @@ struct QueryArgs {
   int32_t tiles_per_wp;
   int32_t tgrad;                   // gcdf_tgrad
   int32_t frame;                   // gcdf_frame (1: SE(2), R24)
+  int32_t act;                     // hidden activation (MLPW id): 1 ReLU (R9), 2 softplus (R26)
   // dense outputs (query) -- NULL in detect mode
   float *values;
   float *grads;                    // (project: the projected configurations q_z instead)

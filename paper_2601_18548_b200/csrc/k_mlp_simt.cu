@@ -78,9 +78,20 @@ constexpr int smem_bytes_simt() {
   return (2 * H * LD + 4 * kTile + H + 16 + kTile + 2 * 4 + 4 + 4) * 4 + 16;
 }
 
-template <int H>
+// Hidden activation (ACT = MLPW activation id): 1 = ReLU (R9; masks in registers),
+// 2 = softplus (NEXT-4 variant, R26): h = max(z, 0) + log1p(e^-|z|), sigma'(z) = 1/(1 + e^-z)
+// kept per element in a per-thread stash (local memory, 6 x 8 x H/16 fp32).
+__device__ __forceinline__ float softplus_f32(float z, float &dsig) {
+  const float t = expf(-fabsf(z));
+  const float r = 1.f / (1.f + t);
+  dsig = z >= 0.f ? r : t * r;
+  return fmaxf(z, 0.f) + log1pf(t);
+}
+
+template <int H, int ACT>
 __global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const QueryArgs a) {
   constexpr int UPT = H / 16;
+  static_assert(ACT == 1 || ACT == 2, "activation");
   constexpr int MW = (8 * UPT + 31) / 32;
   extern __shared__ __align__(16) float smem[];
   float *buf0 = smem;
@@ -137,6 +148,7 @@ __global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const Q
     for (int l = 0; l < kHidden; ++l)
 #pragma unroll
       for (int m = 0; m < MW; ++m) mask[l][m] = 0u;
+    float dsig[ACT == 2 ? kHidden : 1][8][UPT];  // softplus'(z_l) per element (ACT 2)
 
     float acc[8][UPT];
     // A3: layer 1 (12 -> H) in fp32: z1 = W1[:, 0:3] p' + c
@@ -155,8 +167,12 @@ __global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const Q
         for (int i = 0; i < UPT; ++i) {
           float z = fmaf(wv[i].x, x.x, fmaf(wv[i].y, x.y, fmaf(wv[i].z, x.z, cc[i])));
           const int b = i * 8 + pp;
-          if (z > 0.f) mask[0][b >> 5] |= 1u << (b & 31);
-          acc[pp][i] = fmaxf(z, 0.f);
+          if constexpr (ACT == 2) {
+            acc[pp][i] = softplus_f32(z, dsig[0][pp][i]);
+          } else {
+            if (z > 0.f) mask[0][b >> 5] |= 1u << (b & 31);
+            acc[pp][i] = fmaxf(z, 0.f);
+          }
         }
       }
     }
@@ -183,8 +199,12 @@ __global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const Q
 #pragma unroll
         for (int i = 0; i < UPT; ++i) {
           const int b = i * 8 + pp;
-          if (acc[pp][i] > 0.f) mask[li + 1][b >> 5] |= 1u << (b & 31);
-          acc[pp][i] = fmaxf(acc[pp][i], 0.f);
+          if constexpr (ACT == 2) {
+            acc[pp][i] = softplus_f32(acc[pp][i], dsig[li + 1][pp][i]);
+          } else {
+            if (acc[pp][i] > 0.f) mask[li + 1][b >> 5] |= 1u << (b & 31);
+            acc[pp][i] = fmaxf(acc[pp][i], 0.f);
+          }
         }
       if (li < 4) {
         store_tile<H>(nxt, tp, tu, acc);
@@ -218,7 +238,10 @@ __global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const Q
 #pragma unroll
         for (int i = 0; i < UPT; ++i) {
           const int b = i * 8 + pp;
-          acc[pp][i] = (mask[5][b >> 5] >> (b & 31)) & 1u ? w7v[i] : 0.f;
+          if constexpr (ACT == 2)
+            acc[pp][i] = w7v[i] * dsig[5][pp][i];
+          else
+            acc[pp][i] = (mask[5][b >> 5] >> (b & 31)) & 1u ? w7v[i] : 0.f;
         }
       store_tile<H>(nxt, tp, tu, acc);
       __syncthreads();
@@ -290,7 +313,10 @@ __global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const Q
 #pragma unroll
         for (int i = 0; i < UPT; ++i) {
           const int b = i * 8 + pp;
-          acc[pp][i] = (mask[li][b >> 5] >> (b & 31)) & 1u ? acc[pp][i] : 0.f;
+          if constexpr (ACT == 2)
+            acc[pp][i] *= dsig[li][pp][i];
+          else
+            acc[pp][i] = (mask[li][b >> 5] >> (b & 31)) & 1u ? acc[pp][i] : 0.f;
         }
       store_tile<H>(nxt, tp, tu, acc);
       __syncthreads();
@@ -383,13 +409,13 @@ __global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const Q
   }
 }
 
-template <int H>
+template <int H, int ACT>
 cudaError_t launch_h(const WeightsF32 &w, const QueryArgs &a, int num_sms, cudaStream_t s) {
   const int smem = smem_bytes_simt<H>();
-  cudaError_t e = cudaFuncSetAttribute(k_mlp_simt<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(k_mlp_simt<H, ACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   int per_sm = 1;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mlp_simt<H>, 256, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mlp_simt<H, ACT>, 256, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)num_sms * per_sm;
@@ -398,15 +424,20 @@ cudaError_t launch_h(const WeightsF32 &w, const QueryArgs &a, int num_sms, cudaS
     if (grid > n_tiles) grid = n_tiles;
   }
   if (grid < 1) return cudaSuccess;
-  k_mlp_simt<H><<<(unsigned)grid, 256, smem, s>>>(w, a);
+  k_mlp_simt<H, ACT><<<(unsigned)grid, 256, smem, s>>>(w, a);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_mlp_simt(int H, const WeightsF32 &w, const QueryArgs &a, int num_sms, cudaStream_t s) {
-  if (H == 128) return launch_h<128>(w, a, num_sms, s);
-  if (H == 32) return launch_h<32>(w, a, num_sms, s);
+  if (a.act == 2) {
+    if (H == 128) return launch_h<128, 2>(w, a, num_sms, s);
+    if (H == 32) return launch_h<32, 2>(w, a, num_sms, s);
+    return cudaErrorInvalidValue;
+  }
+  if (H == 128) return launch_h<128, 1>(w, a, num_sms, s);
+  if (H == 32) return launch_h<32, 1>(w, a, num_sms, s);
   return cudaErrorInvalidValue;
 }
 

@@ -231,11 +231,13 @@ def read_mlpw_raw(path):
     return act, dims, layers
 
 
-def weights_path(H: int, seed: int = 7) -> str:
-    """Deterministic weights file for hidden width H (generated on first use)."""
-    p = REPO / "build" / "inputs" / f"gcdf_H{H}_s{seed}.mlpw"
+def weights_path(H: int, seed: int = 7, act: int = 1) -> str:
+    """Deterministic weights file for hidden width H (generated on first use).  act = 2: the
+    same random-init weights under the softplus activation (NEXT-4 variant, R26)."""
+    name = f"gcdf_H{H}_s{seed}.mlpw" if act == 1 else f"gcdf_H{H}_s{seed}_act{act}.mlpw"
+    p = REPO / "build" / "inputs" / name
     if not p.exists():
-        act, dims, layers = make_weights(H, seed)
+        _, dims, layers = make_weights(H, seed)
         tmp = p.with_suffix(".tmp%d" % os.getpid())
         write_mlpw(tmp, act, dims, layers)
         os.replace(tmp, p)
