@@ -31,6 +31,7 @@ import synth  # noqa: E402
 METRIC = "GCDF value+grad queries/sec (with active-set detection)"
 FLOPS_PAIR_TOTAL = {128: 333_312, 32: 21_888}      # fwd 167,168 + bwd 166,144 (H=128)
 FLOPS_PAIR_TENSOR = {128: 327_680, 32: 20_480}     # the ten H x H GEMMs (tensor-eligible)
+ACT = {"relu": 1, "softplus": 2}                   # MLPW activation ids (R9, R26)
 
 
 def parse():
@@ -40,6 +41,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C5")
     ap.add_argument("--precision", default="auto", choices=["auto", "fp16", "bf16", "fp32", "fp16x3"])
+    ap.add_argument("--activation", default="relu", choices=["relu", "softplus"],
+                    help="hidden activation of the random-init network (softplus: NEXT-4 variant, DESIGN.md R26)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -103,21 +106,21 @@ def measured_peaks():
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def cpu_oracle_rate(cfg, pts, q, sample_pts=8192, nthreads=None, seed=12345, single_thread=False):
+def cpu_oracle_rate(cfg, pts, q, sample_pts=8192, nthreads=None, seed=12345, single_thread=False, act=1):
     """The oracle as it stands on the host cores: detect over a bounded sample of the
     workload -- one waypoint row per core (the oracle threads over waypoint rows) x
     sample_pts points."""
     import oracle
     nthreads = nthreads or os.cpu_count() or 1
-    m = oracle.MLP(synth.weights_path(cfg.H))
+    m = oracle.MLP(synth.weights_path(cfg.H, act=act))
+    tau = synth.load_tau(cfg.name, act)
     rng = np.random.default_rng(seed)
     qs = q.reshape(-1, 9)
     wsel = np.sort(rng.choice(qs.shape[0], size=min(nthreads, qs.shape[0]), replace=False))
     psel = np.sort(rng.choice(pts.shape[0], size=min(sample_pts, pts.shape[0]), replace=False))
     used = min(nthreads, len(wsel))
     t0 = time.perf_counter()
-    m.detect(pts[psel], psel.astype(np.int64), qs[wsel], synth.inputs.DELTA, synth.load_tau(cfg.name),
-             nthreads=used)
+    m.detect(pts[psel], psel.astype(np.int64), qs[wsel], synth.inputs.DELTA, tau, nthreads=used)
     dt = time.perf_counter() - t0
     n = len(wsel) * len(psel)
     r = {"value": n / dt, "unit": "queries/s", "cores": int(used), "kind": "oracle", "pairs": n, "seconds": dt,
@@ -126,7 +129,7 @@ def cpu_oracle_rate(cfg, pts, q, sample_pts=8192, nthreads=None, seed=12345, sin
     if single_thread:
         p1 = psel[: max(1, len(psel) // 8)]
         t0 = time.perf_counter()
-        m.detect(pts[p1], p1.astype(np.int64), qs[wsel[:1]], synth.inputs.DELTA, synth.load_tau(cfg.name), nthreads=1)
+        m.detect(pts[p1], p1.astype(np.int64), qs[wsel[:1]], synth.inputs.DELTA, tau, nthreads=1)
         d1 = time.perf_counter() - t0
         r["single_thread"] = {"value": len(p1) / d1, "pairs": len(p1), "seconds": d1}
     return r
@@ -142,7 +145,7 @@ def run_reference(a):
     q = synth.make_waypoints(cfg)
     times, n_pairs, r = [], 0, None
     for i in range(a.warmup + a.steps):
-        r = cpu_oracle_rate(cfg, pts, q, sample_pts=2048, seed=1000 + i)
+        r = cpu_oracle_rate(cfg, pts, q, sample_pts=2048, seed=1000 + i, act=ACT[a.activation])
         if i >= a.warmup:
             times.append(r["seconds"])
             n_pairs += r["pairs"]
@@ -183,7 +186,8 @@ def main():
     cfg = synth.get_config(a.config)
     if prec == "auto":  # the tensor-core path needs H = 128 (C1's H = 32 net runs on the fp32 path)
         prec = "fp16" if lib.gcdf_has_tcgen05() and cfg.H == 128 else "fp32"
-    tau = synth.load_tau(cfg.name)
+    act = ACT[a.activation]
+    tau = synth.load_tau(cfg.name, act)
     delta = synth.inputs.DELTA
     pts, boxes = synth.make_scene_points(cfg)
     q_np = synth.make_waypoints(cfg)
@@ -193,7 +197,7 @@ def main():
     ctx = Context(local, precision={"fp16": FP16, "bf16": BF16, "fp32": FP32, "fp16x3": FP16X3}[prec], scene_capacity=cfg.M + slack,
                   max_waypoints=n_wp, max_active=max_active, rank=rank, world=world,
                   max_candidates=(cfg.pairs // world + 4096) if a.partition_radius > 0 else 0)
-    ctx.load_weights(synth.weights_path(cfg.H))
+    ctx.load_weights(synth.weights_path(cfg.H, act=act))
     ctx.update_scene(pts)
     q = torch.from_numpy(q_np).to(dev)
     outs = ctx.alloc_detect_outputs(n_wp, max_active)
@@ -279,7 +283,7 @@ def main():
         peak = float(peaks.get(key))
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "traffic": None, "peak_source": f"{peak_src} {key} (MEASURED_PEAKS.json; fp16 dense = bf16 dense)",
-                "kernel": ("k_mlp_tc3" if n_terms == 3 else "k_mlp_tc") +
+                "kernel": ("k_mlp_tc3" if n_terms == 3 else "k_mlp_tc_sp" if act == 2 else "k_mlp_tc") +
                           " (fused transform + MLP fwd/bwd + threshold/min/compaction)",
                 "kernel_ms_avg": mlp_ms / mlp_n, "flops_per_pair": n_terms * FLOPS_PAIR_TENSOR[cfg.H]}
     else:
@@ -292,7 +296,7 @@ def main():
                 "kernel": "k_mlp_simt (fused transform + MLP fwd/bwd + threshold/min/compaction)",
                 "kernel_ms_avg": mlp_ms / mlp_n, "flops_per_pair": FLOPS_PAIR_TOTAL[cfg.H]}
     tf = ROOT / "profiles" / "traffic.json"
-    if tf.exists() and prec in ("bf16", "fp16"):  # (measured for k_mlp_tc only)
+    if tf.exists() and prec in ("bf16", "fp16") and act == 1:  # (measured for k_mlp_tc only)
         t = json.loads(tf.read_text()).get("k_mlp_tc")
         if t:
             roof["traffic"] = t["bytes"]
@@ -415,14 +419,14 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cpu = cpu_oracle_rate(cfg, pts, q_np, sample_pts=65536, single_thread=True)
+        cpu = cpu_oracle_rate(cfg, pts, q_np, sample_pts=65536, single_thread=True, act=act)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": t_max / a.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": prec, "data": "synthetic (seeded clutter clouds + random-init weights)",
             "config": {"workload": f"{cfg.name}: {cfg.desc}", "B": cfg.B, "N": cfg.N, "points": cfg.M,
-                       "hidden": cfg.H, "pairs_per_step": int(pairs_total / a.steps), "delta": delta, "tau": tau,
+                       "hidden": cfg.H, "activation": a.activation, "pairs_per_step": int(pairs_total / a.steps), "delta": delta, "tau": tau,
                        "active_per_step": n_active, "scene_update_per_step": f"{n_chg} removes + {n_chg} adds",
                        "parallelism": f"points sharded over {world} GPU(s)",
                        "l2": "256 MiB buffer written between timed steps (L2 flush)"},

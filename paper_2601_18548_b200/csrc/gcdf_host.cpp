@@ -476,8 +476,10 @@ int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
   if (!ok) return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: dims must be [12, H x 6, 1], H in {32, 128}", path);
   if (act != 1 && act != 2)
     return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: activation %u (ReLU = 1, R9, or softplus = 2, R26)", path, act);
-  if (act == 2 && c->opt.precision != GCDF_FP32)
-    return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: softplus (R26) runs on GCDF_FP32", path);
+  if (act == 2 && c->opt.precision != GCDF_FP32 &&
+      (c->opt.precision != GCDF_FP16 || c->opt.frame != GCDF_FRAME_TRANSLATE))
+    return fail(c, GCDF_ERR_DIM_MISMATCH,
+                "%s: softplus (R26) runs on GCDF_FP32, or on GCDF_FP16 in the translation frame", path);
   if (c->opt.precision != GCDF_FP32 && H != 128)
     return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: the tensor-core path needs H = 128 (use GCDF_FP32 for H = %d)", path, H);
   std::vector<std::vector<double>> Wd(7), bd(7);
@@ -713,6 +715,7 @@ static cudaError_t run_mlp(gcdf_ctx *c, const QueryArgs &a, cudaStream_t s) {
                       ? launch_mlp_simt(c->H, f32_view(c), a, c->num_sms, s)
                       : c->opt.precision == GCDF_FP16X3
                             ? launch_mlp_tc3(bf16_view(c), a, c->num_sms, s)
+                        : a.act == 2 ? launch_mlp_tc_sp(bf16_view(c), a, c->num_sms, s)
                             : launch_mlp_tc(c->H, c->opt.precision == GCDF_FP16, bf16_view(c), a, c->num_sms, s);
   if (slot >= 0) cudaEventRecord(c->ev[2 * slot + 1], s);
   return e;

@@ -141,6 +141,8 @@ cudaError_t launch_pairgen(const float4 *pts, int64_t local_bound, const float *
 cudaError_t launch_detect_init(DetectScratch ds, int32_t n_wp, cudaStream_t s);
 cudaError_t launch_mlp_simt(int H, const WeightsF32 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
 cudaError_t launch_mlp_tc(int H, bool f16, const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
+// softplus variant of the tensor-core path (fp16 operands, translation frame; R26)
+cudaError_t launch_mlp_tc_sp(const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
 cudaError_t launch_mlp_tc3(const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
 bool tc_compiled();
 cudaError_t launch_selftest_umma(int mode, const float *A, const float *B, float *D, cudaStream_t s);

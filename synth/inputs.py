@@ -68,10 +68,11 @@ def get_config(name: str) -> Config:
     return CONFIGS[name]
 
 
-def load_tau(name: str) -> float:
-    """tau frozen by tools/calibrate_tau.py (which calls only oracle/)."""
+def load_tau(name: str, act: int = 1) -> float:
+    """tau frozen by tools/calibrate_tau.py (which calls only oracle/); act = 2: the softplus
+    network's margin (key "<name>_softplus")."""
     with open(REPO / "configs" / "tau.json") as fh:
-        return float(json.load(fh)[name]["tau"])
+        return float(json.load(fh)[name if act == 1 else name + "_softplus"]["tau"])
 
 
 # ----------------------------------------------------------------------------- scene

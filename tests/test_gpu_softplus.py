@@ -83,11 +83,115 @@ def test_softplus_detect_fp32(which, request):
 
 
 def test_softplus_rejected_by_unsupported_precisions():
-    """Softplus runs on GCDF_FP32 and GCDF_FP16; the bf16 and split-fp16 paths refuse it
-    (DIM_MISMATCH) instead of silently evaluating ReLU."""
-    from paper_2601_18548_b200 import BF16, FP16X3, Context, GcdfError
-    for prec in (BF16, FP16X3):
-        ctx = Context(0, precision=prec, scene_capacity=1024, max_waypoints=16, max_active=1024)
+    """Softplus runs on GCDF_FP32 and on GCDF_FP16 in the translation frame; the bf16 and
+    split-fp16 paths and the SE(2) tensor path refuse it (DIM_MISMATCH) instead of silently
+    evaluating ReLU."""
+    from paper_2601_18548_b200 import BF16, FP16, FP16X3, FRAME_SE2, Context, GcdfError
+    for prec, kw in ((BF16, {}), (FP16X3, {}), (FP16, {"frame": FRAME_SE2})):
+        ctx = Context(0, precision=prec, scene_capacity=1024, max_waypoints=16, max_active=1024, **kw)
         with pytest.raises(GcdfError) as e:
             ctx.load_weights(synth.weights_path(128, act=2))
         assert e.value.name == "DIM_MISMATCH"
+
+
+# ------------------------------------------------------------------ tensor-core path (K2s)
+# Gates (R17 / R26): vs the oracle's EMU_FP16 mode (same rounding points: 16-bit A operands,
+# sigma' of layers 1..5 from the rounded activation) median |df| at fp32 noise, max |df| <=
+# 5e-3 and ||dg|| <= 1e-2 max(1, ||g||) on every pair; vs the exact oracle the north-star tensor-path tolerances
+# |df| <= 2e-2 and | ||g|| - ||g_exact|| | <= 5e-2 -- on every pair, since the softplus
+# field has no kinks.
+TC_EMU_VAL_MAX, TC_EMU_GREL, TC_VAL, TC_GNORM = 5e-3, 1e-2, 2e-2, 5e-2
+
+
+def _tc_gates(v, g, exact, emu, what):
+    dv_emu = np.abs(v - emu["f"])
+    dg_emu = np.linalg.norm(g - emu["g"], axis=-1)
+    gn_emu = np.linalg.norm(emu["g"], axis=-1)
+    dv = np.abs(v - exact["f"])
+    dgn = np.abs(np.linalg.norm(g, axis=-1) - np.linalg.norm(exact["g"], axis=-1))
+    print(f"{what}: |df| vs EMU median {np.median(dv_emu):.2e} p99 {np.quantile(dv_emu, 0.99):.2e} max "
+          f"{dv_emu.max():.2e}; vs exact max {dv.max():.2e}; ||dg|| vs EMU median {np.median(dg_emu):.2e} max "
+          f"{dg_emu.max():.2e}; gnorm diff vs exact max {dgn.max():.2e}")
+    # same rounding points: fp32 noise in the median; the tail is where the MUFU-approximated
+    # softplus lands on the other side of a 16-bit rounding boundary than the f64 one
+    assert np.median(dv_emu) <= 1e-6 and dv_emu.max() <= TC_EMU_VAL_MAX, what
+    assert np.median(dg_emu) <= 1e-5 and np.all(dg_emu <= TC_EMU_GREL * np.maximum(1.0, gn_emu)), what
+    assert dv.max() <= TC_VAL, (what, dv.max())
+    assert dgn.max() <= TC_GNORM, (what, dgn.max())
+
+
+@pytest.fixture(scope="module")
+def c2_tc():
+    cfg, pts, q, m, full = _case("C2", 8)
+    emu = m.eval(pts, q.reshape(-1, 9), flags=oracle.EMU_FP16, nthreads=NT)
+    return cfg, pts, q, m, full, emu
+
+
+def test_softplus_query_dense_tensor(c2_tc):
+    from paper_2601_18548_b200 import FP16
+    cfg, pts, q, m, full, emu = c2_tc
+    ctx = _ctx(cfg, precision=FP16)
+    ctx.update_scene(pts)
+    v, g = ctx.query_values_grads(torch.from_numpy(q))
+    torch.cuda.synchronize()
+    vt, gt = v.cpu().numpy(), g.cpu().numpy()
+    M = len(pts)
+    assert np.all(np.isinf(vt[:, M:])) and np.all(gt[:, M:] == 0)  # dead tail slots
+    _tc_gates(vt[:, :M], gt[:, :M], full, emu, "C2/8 dense fp16 softplus")
+
+
+def test_softplus_detect_tensor(c2_tc):
+    from paper_2601_18548_b200 import FP16
+    cfg, pts, q, m, full, emu = c2_tc
+    tau = float(np.quantile(full["f"], 0.01)) - DELTA
+    ctx = _ctx(cfg, precision=FP16)
+    ids = ctx.update_scene(pts)
+    qt = torch.from_numpy(q)
+    out = ctx.detect_active_set(qt, DELTA, tau)
+    v, g = ctx.query_values_grads(qt)
+    torch.cuda.synchronize()
+    gpu = records_np(out)
+    orc = oracle_detect(m, pts, ids, q.reshape(-1, 9), tau, nthreads=NT)
+
+    def gchk(gg, og, kap):
+        assert np.all(np.abs(np.linalg.norm(gg, axis=-1) - np.linalg.norm(og, axis=-1)) <= TC_GNORM)
+
+    nd, nc = compare_active_sets(gpu, orc, full["f"], ids, BAND_FP32 + TC_VAL, val_atol=TC_VAL, grad_check=gchk,
+                                 what="C2/8 detect fp16 softplus")
+    assert nc > 0
+    # the fused detect's records are the dense query's values and gradients, bit for bit
+    vn, gn = v.cpu().numpy(), g.cpu().numpy()
+    assert np.array_equal(gpu["value"], vn[gpu["wp"], gpu["pt"]])
+    assert np.array_equal(gpu["grad"], gn[gpu["wp"], gpu["pt"]])
+    assert np.all(np.abs(out["wp_min"].cpu().numpy() - orc["wp_min"]) <= TC_VAL)
+
+
+def test_softplus_tensor_c1_shape_and_partition():
+    """Ragged tails on the tensor path: C1 points (256 = 2 tiles) under the H = 128
+    softplus network, dense and range-partitioned detect vs the EMU oracle."""
+    from paper_2601_18548_b200 import FP16
+    cfg = synth.get_config("C1")
+    pts, _ = synth.make_scene_points(cfg)
+    q = synth.make_waypoints(cfg)
+    m = oracle.MLP(synth.weights_path(128, act=2))
+    full = m.eval(pts, q.reshape(-1, 9), nthreads=NT)
+    emu = m.eval(pts, q.reshape(-1, 9), flags=oracle.EMU_FP16, nthreads=NT)
+    from paper_2601_18548_b200 import Context
+    ctx = Context(0, precision=FP16, scene_capacity=4096, max_waypoints=64, max_active=1 << 16,
+                  max_candidates=1 << 16)
+    ctx.load_weights(synth.weights_path(128, act=2))
+    ids = ctx.update_scene(pts[:200])  # 200 live points: a ragged second tile
+    v, g = ctx.query_values_grads(torch.from_numpy(q))
+    torch.cuda.synchronize()
+    sub = {k: full[k][:, :200] for k in ("f", "g")}
+    esub = {k: emu[k][:, :200] for k in ("f", "g")}
+    _tc_gates(v.cpu().numpy()[:, :200], g.cpu().numpy()[:, :200], sub, esub, "C1 dense fp16 softplus")
+    tau = float(np.quantile(sub["f"], 0.2)) - DELTA
+    part = ctx.detect_active_set_partitioned(torch.from_numpy(q), 3.0, DELTA, tau)
+    torch.cuda.synchronize()
+    gp = records_np(part)
+    orc = m.detect(pts[:200], ids, q.reshape(-1, 9), DELTA, tau, nthreads=NT, radius=3.0)
+    orc["_tau"] = tau
+    nd, nc = compare_active_sets(gp, orc, sub["f"], ids, BAND_FP32 + TC_VAL, val_atol=TC_VAL,
+                                 what="C1 partitioned fp16 softplus")
+    assert nc > 0

@@ -27,20 +27,24 @@ def main():
     ap.add_argument("--pts", type=int, default=16384)
     a = ap.parse_args()
     out = {}
-    for name, cfg in synth.CONFIGS.items():
-        pts, _ = synth.make_scene_points(cfg)
-        q = synth.make_waypoints(cfg).reshape(-1, 9)
-        rng = np.random.default_rng([cfg.seed, 99])
-        wsel = np.sort(rng.choice(q.shape[0], size=min(a.wp, q.shape[0]), replace=False))
-        psel = np.sort(rng.choice(pts.shape[0], size=min(a.pts, pts.shape[0]), replace=False))
-        m = oracle.MLP(synth.weights_path(cfg.H))
-        f = m.eval(pts[psel], q[wsel], want_grad=False, nthreads=a.threads)["f"].ravel()
-        quant = float(np.quantile(f, cfg.quantile))
-        tau = quant - synth.inputs.DELTA
-        frac = float(np.mean(f - synth.inputs.DELTA <= tau))
-        out[name] = {"tau": tau, "quantile": cfg.quantile, "sample_pairs": int(f.size),
-                     "sample_active_fraction": frac, "f_mean": float(f.mean()), "f_std": float(f.std())}
-        print(name, out[name], flush=True)
+    # act 1: the ReLU network (R9); act 2: the same weights under softplus (NEXT-4, R26),
+    # stored as "<config>_softplus"
+    for act in (1, 2):
+        for name, cfg in synth.CONFIGS.items():
+            pts, _ = synth.make_scene_points(cfg)
+            q = synth.make_waypoints(cfg).reshape(-1, 9)
+            rng = np.random.default_rng([cfg.seed, 99])
+            wsel = np.sort(rng.choice(q.shape[0], size=min(a.wp, q.shape[0]), replace=False))
+            psel = np.sort(rng.choice(pts.shape[0], size=min(a.pts, pts.shape[0]), replace=False))
+            m = oracle.MLP(synth.weights_path(cfg.H, act=act))
+            f = m.eval(pts[psel], q[wsel], want_grad=False, nthreads=a.threads)["f"].ravel()
+            quant = float(np.quantile(f, cfg.quantile))
+            tau = quant - synth.inputs.DELTA
+            frac = float(np.mean(f - synth.inputs.DELTA <= tau))
+            key = name if act == 1 else name + "_softplus"
+            out[key] = {"tau": tau, "quantile": cfg.quantile, "sample_pairs": int(f.size),
+                        "sample_active_fraction": frac, "f_mean": float(f.mean()), "f_std": float(f.std())}
+            print(key, out[key], flush=True)
     out["_provenance"] = ("written by tools/calibrate_tau.py from oracle/ float64 values on a seeded "
                           "subsample (rng seed [cfg.seed, 99]); delta = %.2f" % synth.inputs.DELTA)
     (ROOT / "configs").mkdir(exist_ok=True)
