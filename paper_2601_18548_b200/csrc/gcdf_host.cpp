@@ -25,13 +25,14 @@ using namespace gcdf;
 namespace {
 
 constexpr int64_t kUpdChunk = 65536;  // points per scene-update scatter chunk
-constexpr int kMaxH = 128;
+constexpr int kMaxH = 256;   // fp32 block (SIMT layout, and w7 / biases for every path)
+constexpr int kTcH = 128;    // the K2b / K2c / K2s 16-bit blocks (weights resident in smem)
 constexpr int kEvPool = 64;
 
 inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
 struct Layout {
-  int64_t pts, wf32, wbf16, wf16, wf16x3, meta, staging, wp_key, wp_count, counter, upd_payload, upd_slots;
+  int64_t pts, wf32, wbf16, wf16, wf16x3, wf16w, meta, staging, wp_key, wp_count, counter, upd_payload, upd_slots;
   int64_t h_q, h_out, h_offs, h_wmin, h_warg, h_count;
   int64_t p_grid, p_bbox, p_cell_count, p_cell_start, p_cell_fill, p_cell_items, p_cell_xy, p_bitmap, p_chunk_cnt, p_chunk_off,
       p_scan_tmp, p_cand, p_cand_start, p_cand_count, p_tile_start, p_tile_wp, p_n_tiles, p_words, p_nchunk;
@@ -44,13 +45,22 @@ constexpr int64_t kF32W1p = kMaxH * 4, kF32W1q = kMaxH * 8, kF32W1full = kMaxH *
 constexpr int64_t kF32Mat = (int64_t)kMaxH * kMaxH;
 constexpr int64_t kF32Total = kF32W1p + kF32W1q + kF32W1full + 10 * kF32Mat + 5 * kMaxH + kMaxH;
 // bf16 block sizes (bytes)
-constexpr int64_t kBfMat = (int64_t)kMaxH * kMaxH * 2;
-constexpr int64_t kBfW1t = 16LL * kMaxH * 2;
-constexpr int64_t kBfB1 = 32LL * kMaxH * 2;    // layer-1 split weights [128][K = 32], no swizzle
-constexpr int64_t kBfBext = 16LL * kMaxH * 2;  // per hidden layer bias block [128][K = 16], no swizzle
+constexpr int64_t kBfMat = (int64_t)kTcH * kTcH * 2;
+constexpr int64_t kBfW1t = 16LL * kTcH * 2;
+constexpr int64_t kBfB1 = 32LL * kTcH * 2;    // layer-1 split weights [128][K = 32], no swizzle
+constexpr int64_t kBfBext = 16LL * kTcH * 2;  // per hidden layer bias block [128][K = 16], no swizzle
 constexpr int64_t kBfTotal = 5 * kBfMat + kBfW1t + kBfB1 + 5 * kBfBext;
 // GCDF_FP16X3 block: 5 x [W_l hi | W_l lo] SW128 images, then W1^T hi, lo
 constexpr int64_t kX3Total = 5 * 2 * kBfMat + 2 * kBfW1t;
+// H = 256 block (K2w, fp16): the 40 streamed 32 KB chunks of a tile in consumption order
+// (W_2..W_6 forward, K-major [out][in]; then W_6^T..W_2^T, K-major [in][out]; 4 chunks of
+// 64 K-columns each, SW128), then W1^T [16][256] SW128, layer-1 split [256][32] and the five
+// bias blocks [256][16] (no swizzle)
+constexpr int kWideH = 256;
+constexpr int64_t kWideChunk = (int64_t)kWideH * 128;
+constexpr int64_t kWideSeq = 40 * kWideChunk;
+constexpr int64_t kWideW1t = 16LL * kWideH * 2, kWideB1 = 32LL * kWideH * 2, kWideBext = 16LL * kWideH * 2;
+constexpr int64_t kWideTotal = kWideSeq + kWideW1t + kWideB1 + 5 * kWideBext;
 
 }  // namespace
 
@@ -179,6 +189,13 @@ WeightsBF16 bf16_view(const gcdf_ctx *c) {
   w.w1t_sw128 = c->ws + wo + 5 * kBfMat;
   w.b1_nosw = c->ws + wo + 5 * kBfMat + kBfW1t;
   w.bext_nosw = c->ws + wo + 5 * kBfMat + kBfW1t + kBfB1;
+  if (c->H == kWideH) {  // K2w: streamed chunk sequence + resident small blocks
+    const char *b = c->ws + c->L.wf16w;
+    w.w_sw128 = b;
+    w.w1t_sw128 = b + kWideSeq;
+    w.b1_nosw = b + kWideSeq + kWideW1t;
+    w.bext_nosw = b + kWideSeq + kWideW1t + kWideB1;
+  }
   w.w3_sw128 = c->ws + c->L.wf16x3;
   w.w1t3_sw128 = c->ws + c->L.wf16x3 + 5 * 2 * kBfMat;
   w.bh = f.bias[0];  // the five fp32 bias rows are contiguous in the fp32 block
@@ -357,6 +374,7 @@ int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out) {
   L.wbf16 = off; L.wbf16_bytes = kBfTotal; off = align256(off + kBfTotal);
   L.wf16 = off; off = align256(off + kBfTotal);
   L.wf16x3 = off; off = align256(off + kX3Total);
+  L.wf16w = off; off = align256(off + kWideTotal);
   L.meta = off; off = align256(off + (int64_t)o.max_waypoints * c->tiles_cap * 8);
   L.staging = off; off = align256(off + o.max_active * (int64_t)sizeof(gcdf_active_t));
   L.wp_key = off; off = align256(off + (int64_t)o.max_waypoints * 8);
@@ -471,17 +489,21 @@ int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
   uint32_t dims[8];
   if (!rd(dims, 32)) return fail(c, GCDF_ERR_IO, "%s: truncated dims", path);
   const int H = (int)dims[1];
-  bool ok = dims[0] == (uint32_t)kNin && dims[7] == 1 && (H == 32 || H == 128);
+  bool ok = dims[0] == (uint32_t)kNin && dims[7] == 1 && (H == 32 || H == 128 || H == kWideH);
   for (int l = 1; l <= 6; ++l) ok = ok && dims[l] == (uint32_t)H;
-  if (!ok) return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: dims must be [12, H x 6, 1], H in {32, 128}", path);
+  if (!ok) return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: dims must be [12, H x 6, 1], H in {32, 128, 256}", path);
+  if (H == kWideH && (c->opt.precision != GCDF_FP16 || act != 1 || c->opt.frame != GCDF_FRAME_TRANSLATE))
+    return fail(c, GCDF_ERR_DIM_MISMATCH,
+                "%s: H = 256 (NEXT-4) runs on GCDF_FP16 with ReLU in the translation frame (K2w)", path);
   if (act != 1 && act != 2)
     return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: activation %u (ReLU = 1, R9, or softplus = 2, R26)", path, act);
   if (act == 2 && c->opt.precision != GCDF_FP32 &&
       (c->opt.precision != GCDF_FP16 || c->opt.frame != GCDF_FRAME_TRANSLATE))
     return fail(c, GCDF_ERR_DIM_MISMATCH,
                 "%s: softplus (R26) runs on GCDF_FP32, or on GCDF_FP16 in the translation frame", path);
-  if (c->opt.precision != GCDF_FP32 && H != 128)
-    return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: the tensor-core path needs H = 128 (use GCDF_FP32 for H = %d)", path, H);
+  if (c->opt.precision != GCDF_FP32 && H == 32)
+    return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: the tensor-core path needs H = 128 or 256 (use GCDF_FP32 for H = %d)",
+                path, H);
   std::vector<std::vector<double>> Wd(7), bd(7);
   for (int l = 0; l < 7; ++l) {
     Wd[l].resize((size_t)dims[l + 1] * dims[l]);
@@ -591,7 +613,54 @@ int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
     pack_sw128(th, 16, H, x3.data() + (size_t)10 * kBfMat / 2, true);
     pack_sw128(tl, 16, H, x3.data() + (size_t)(10 * kBfMat + kBfW1t) / 2, true);
   }
+  // ---- H = 256 (K2w) ----
+  std::vector<uint16_t> wide;
+  if (H == kWideH) {
+    wide.assign((size_t)kWideTotal / 2, 0);
+    std::vector<float> m((size_t)H * H), mt((size_t)H * H);
+    const int64_t mat = 4 * kWideChunk;  // one layer image = 4 chunks
+    for (int li = 0; li < 5; ++li) {
+      for (int r = 0; r < H; ++r)
+        for (int col = 0; col < H; ++col) {
+          m[(size_t)r * H + col] = W(li + 1, r, col);   // [out][in]: forward B, K = in
+          mt[(size_t)r * H + col] = W(li + 1, col, r);  // [in][out]: backward B, K = out
+        }
+      pack_sw128(m, H, H, wide.data() + (size_t)(li * mat) / 2, true);
+      pack_sw128(mt, H, H, wide.data() + (size_t)((5 + (4 - li)) * mat) / 2, true);
+    }
+    std::vector<float> w1t((size_t)16 * H, 0.f);
+    for (int n = 0; n < kNin; ++n)
+      for (int k = 0; k < H; ++k) w1t[(size_t)n * H + k] = W(0, k, n);
+    pack_sw128(w1t, 16, H, wide.data() + kWideSeq / 2, true);
+    const int xin[10] = {0, 1, 2, 5, 6, 7, 8, 9, 10, 11};
+    std::vector<float> b1((size_t)H * 32, 0.f);
+    for (int u = 0; u < H; ++u) {
+      float hi, lo;
+      for (int i = 0; i < 10; ++i) {
+        split16(Wd[0][(size_t)u * kNin + xin[i]], true, hi, lo);
+        b1[(size_t)u * 32 + 3 * i + 0] = hi;
+        b1[(size_t)u * 32 + 3 * i + 1] = hi;
+        b1[(size_t)u * 32 + 3 * i + 2] = lo;
+      }
+      split16(bd[0][u], true, hi, lo);
+      b1[(size_t)u * 32 + 30] = hi;
+      b1[(size_t)u * 32 + 31] = lo;
+    }
+    pack_nosw(b1, H, 32, wide.data() + (kWideSeq + kWideW1t) / 2, true);
+    for (int li = 0; li < 5; ++li) {
+      std::vector<float> be((size_t)H * 16, 0.f);
+      for (int u = 0; u < H; ++u) {
+        float hi, lo;
+        split16(bd[li + 1][u], true, hi, lo);
+        be[(size_t)u * 16 + 0] = hi;
+        be[(size_t)u * 16 + 1] = lo;
+      }
+      pack_nosw(be, H, 16, wide.data() + (kWideSeq + kWideW1t + kWideB1 + li * kWideBext) / 2, true);
+    }
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!wide.empty())
+    CK(c, cudaMemcpyAsync(c->ws + c->L.wf16w, wide.data(), wide.size() * 2, cudaMemcpyHostToDevice, s), "weights H2D");
   CK(c, cudaMemcpyAsync(c->ws + c->L.wf16x3, x3.data(), x3.size() * 2, cudaMemcpyHostToDevice, s), "weights H2D");
   CK(c, cudaMemcpyAsync(c->ws + c->L.wf32, f32.data(), f32.size() * 4, cudaMemcpyHostToDevice, s), "weights H2D");
   CK(c, cudaMemcpyAsync(c->ws + c->L.wbf16, bf.data(), bf.size() * 2, cudaMemcpyHostToDevice, s), "weights H2D");
@@ -715,6 +784,7 @@ static cudaError_t run_mlp(gcdf_ctx *c, const QueryArgs &a, cudaStream_t s) {
                       ? launch_mlp_simt(c->H, f32_view(c), a, c->num_sms, s)
                       : c->opt.precision == GCDF_FP16X3
                             ? launch_mlp_tc3(bf16_view(c), a, c->num_sms, s)
+                        : c->H == kWideH ? launch_mlp_tc_wide(bf16_view(c), a, c->num_sms, s)
                         : a.act == 2 ? launch_mlp_tc_sp(bf16_view(c), a, c->num_sms, s)
                             : launch_mlp_tc(c->H, c->opt.precision == GCDF_FP16, bf16_view(c), a, c->num_sms, s);
   if (slot >= 0) cudaEventRecord(c->ev[2 * slot + 1], s);

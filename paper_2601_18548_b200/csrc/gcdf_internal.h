@@ -39,6 +39,7 @@ struct WeightsF32 {
 // b1: layer 1 as a K = 32 GEMM on split hi/lo 16-bit operands (exact to ~fp32), and
 // bext: per hidden layer a K = 16 block {b_hi, b_lo, 0...} multiplied by a constant
 // "ones" A block -- both in the UMMA SWIZZLE_NONE K-major layout (gcdf_host.cpp).
+// (H = 256, K2w: w_sw128 = the 40 streamed 32 KB chunks of a tile, w1t / b1 / bext at H = 256)
 struct WeightsBF16 {
   const void *w_sw128;   // 5 * H * H * 2 bytes
   const void *w1t_sw128; // 16 * H * 2 bytes
@@ -141,6 +142,8 @@ cudaError_t launch_pairgen(const float4 *pts, int64_t local_bound, const float *
 cudaError_t launch_detect_init(DetectScratch ds, int32_t n_wp, cudaStream_t s);
 cudaError_t launch_mlp_simt(int H, const WeightsF32 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
 cudaError_t launch_mlp_tc(int H, bool f16, const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
+// H = 256 variant of the tensor-core path (fp16, ReLU, translation frame; weights streamed; R27)
+cudaError_t launch_mlp_tc_wide(const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
 // softplus variant of the tensor-core path (fp16 operands, translation frame; R26)
 cudaError_t launch_mlp_tc_sp(const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
 cudaError_t launch_mlp_tc3(const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);

@@ -1,0 +1,490 @@
+// k_mlp_tc_wide.cu -- K2w: the H = 256 variant (NEXT-4, R27) of the fused tcgen05
+// path: pair generation + base-frame bias + 7-layer MLP [12, 256 x 6, 1] forward + input-
+// gradient backward (+ threshold / min / per-tile compaction in detect mode), fp16 operands,
+// fp32 accumulation in TMEM.
+//
+// Paper steps (PAPER.md lines): base-frame bias :388/:171; "7-layer MLP" on [p, q] :284
+// (width not given: H = 256 is the wide reading of R8); value + gradient :394; constraint
+// f - delta >= 0 :362-363; union = min :164; c_gcdf order :414-435.
+//
+// What differs from K2b (k_mlp_tc.cu, H = 128):
+//   * the five hidden layers are 5 x 128 KB in fp16 -- more than shared memory -- so they are
+//     streamed from L2 (where the 1.25 MB chunk sequence stays resident) through a ring of
+//     four 32 KB slots by a producer warp (1-D cp.async.bulk completing on the slot's "full"
+//     mbarrier); the MMA warp releases a slot with a tcgen05.commit on its "empty" mbarrier
+//     once the four UMMAs that read it complete.  The chunk sequence of a tile is laid out in
+//     consumption order: W_2..W_6 K-major [out][in] (forward), then W_6^T..W_2^T K-major
+//     [in][out] (backward), 4 chunks of 64 K-columns per layer -- so forward and backward
+//     UMMAs use the same descriptor pattern and the producer streams one contiguous image.
+//   * every UMMA is M = 128, N = 256, K = 16 (128 cycles at the dense rate); a layer is 16.
+//   * TMEM: D [0, 256) fp32, A [256, 384) fp16 (K = 256), layer-1 operands [384, 400), ones
+//     block [400, 408): one tile in flight (two would need 2 x 384 columns).  16 epilogue
+//     warps own 32 rows x 64 units each (the K2b per-thread work), ReLU masks in shared
+//     memory in K2b's byte-sign form.
+// Rounding points: those of K2b (EMU_FP16 in the oracle: W_2..W_6, W_1 (gradient), h_1..h_5,
+// e_6..e_1 rounded to fp16; layer 1 split hi/lo; f = w7 . h6 in fp32).
+#include "gcdf_internal.h"
+#include "tc_ptx.h"
+
+namespace gcdf {
+namespace {
+
+using namespace tc;
+
+constexpr int H = 256;
+constexpr int kEpiWarps = 16;
+constexpr int kMmaWarp = 16, kProdWarp = 17;
+constexpr int kThreads = 18 * 32;
+constexpr int kEpi = kEpiWarps * 32;
+constexpr int kPhases = 12;
+constexpr int kMasks = 5;
+constexpr int kNS = 4;                      // ring slots
+constexpr int kChunk = H * 128;             // 32 KB: [256 rows][64 K-columns] fp16, SW128
+constexpr int kChunksPerTile = 40;          // 5 layers x 4 forward + 5 x 4 backward
+constexpr int kW1tBytes = 16 * H * 2;       // 8 KB
+constexpr int kB1Bytes = 32 * H * 2;        // 16 KB
+constexpr int kBextBytes = 16 * H * 2;      // 8 KB per hidden layer
+constexpr uint32_t kColA = 256, kColX = 384, kColOnes = 400;
+constexpr uint32_t kIdescW = idesc_f16kind(128, 256, false, true);
+constexpr uint32_t kIdescFin = idesc_f16kind(128, 16, false, true);
+
+struct __align__(1024) SmemW {
+  uint8_t ring[kNS][kChunk];
+  uint8_t w1t[kW1tBytes];
+  uint8_t b1[kB1Bytes];
+  uint8_t bext[5][kBextBytes];
+  uint32_t mask[kMasks][2][kEpi];  // ReLU masks [layer][32-unit word][thread]
+  float w7half[H];
+  uint32_t w7h[H / 2];
+  uint32_t one;
+  float fpart[4][128];
+  float4 ptn[128];
+  float qn[2][12];
+  int wtile[2];
+  uint32_t slotn[2][128];
+  uint64_t mma_done, epi_done;
+  uint64_t full[kNS], empty[kNS];
+  unsigned act[4];
+  unsigned long long kmin[4];
+  int sbase;
+  uint32_t tmem_base;
+};
+static_assert(sizeof(SmemW) + 1024 <= 232448, "SmemW exceeds the 227 KB of shared memory per CTA");
+
+DEVI unsigned ord_f32(float f) {
+  unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+DEVI float round16(float x) {
+  const uint32_t p = pack_f16(x, 0.f);
+  float f;
+  asm("{\n\t.reg .b16 t;\n\tmov.b16 t, %1;\n\tcvt.f32.f16 %0, t;\n\t}" : "=f"(f) : "h"((unsigned short)(p & 0xffffu)));
+  return f;
+}
+DEVI void split3(float x, float *o) {
+  const float hi = round16(x);
+  o[0] = hi;
+  o[1] = x - hi;
+  o[2] = hi;
+}
+// K2b's mask helpers (the "+ 0x7fff7fff" on the FMA pipe through a runtime one)
+DEVI uint32_t add7fff(uint32_t pk, uint32_t one) { return pk * one + 0x7fff7fffu; }
+DEVI uint32_t mask_group_f(uint32_t pk01, uint32_t pk23, int k, uint32_t one) {
+  const uint32_t x = prmt(add7fff(pk01, one), add7fff(pk23, one), 0x7531u);
+  return (x >> k) & (0x80808080u >> k);
+}
+DEVI uint32_t nz_halves(uint32_t pk, uint32_t one) { return prmt(add7fff(pk, one), 0u, 0xbb99u); }
+
+__global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W, const QueryArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  SmemW &S = *reinterpret_cast<SmemW *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  {
+    auto copy16 = [&](void *dst, const void *src, int bytes) {
+      const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+      uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+      for (int i = tid; i < bytes / 16; i += kThreads) d4[i] = __ldg(s4 + i);
+    };
+    copy16(S.w1t, W.w1t_sw128, kW1tBytes);
+    copy16(S.b1, W.b1_nosw, kB1Bytes);
+    copy16(S.bext, W.bext_nosw, 5 * kBextBytes);
+    for (int i = tid; i < H; i += kThreads) S.w7half[i] = 0.5f * __ldg(W.w7 + i);
+    for (int i = tid; i < H / 2; i += kThreads) S.w7h[i] = pack_f16(__ldg(W.w7 + 2 * i), __ldg(W.w7 + 2 * i + 1));
+    if (tid == 0) S.one = 1u;
+  }
+  if (warp == 0) {
+    tmem_alloc(&S.tmem_base, 512);
+    tmem_relinquish();
+  }
+  if (tid == 32) {
+    mbar_init(&S.mma_done, 1);
+    mbar_init(&S.epi_done, kEpi);
+    for (int i = 0; i < kNS; ++i) {
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  const int64_t n_tiles = query_tiles(a);
+  fence_proxy_async_smem();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = S.tmem_base;
+  const int64_t lb = a.scene.local_bound;
+  const int64_t stride = gridDim.x;
+  const int64_t my_tiles = (int64_t)blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / stride + 1 : 0;
+
+  if (warp == kProdWarp) {
+    // ===================== producer: the chunk sequence of every tile through the ring ======
+    if (lane == 0) {
+      const uint8_t *src = static_cast<const uint8_t *>(W.w_sw128);
+      const int64_t total = my_tiles * kChunksPerTile;
+      for (int64_t i = 0; i < total; ++i) {
+        const int slot = (int)(i % kNS);
+        if (i >= kNS) mbar_wait(&S.empty[slot], (uint32_t)((i / kNS - 1) & 1));
+        mbar_expect_tx(&S.full[slot], kChunk);
+        bulk_g2s(S.ring[slot], src + (i % kChunksPerTile) * kChunk, kChunk, &S.full[slot]);
+      }
+    }
+    __syncwarp();
+    fence_before();
+    __syncthreads();
+    return;
+  }
+  if (warp == kMmaWarp) {
+    // ===================== MMA warp (converged; an elected lane issues) ======================
+    const uint32_t sw1t = smem_u32(S.w1t), sb1 = smem_u32(S.b1), sbx = smem_u32(S.bext);
+    const uint32_t d = tbase, av = tbase + kColA;
+    uint32_t ph = 0u;
+    int64_t ci = 0;  // chunks consumed
+    for (int64_t t = 0; t < my_tiles; ++t) {
+#pragma unroll 1
+      for (int p = 0; p < kPhases; ++p) {
+        mbar_wait(&S.epi_done, ph);
+        ph ^= 1u;
+        fence_after();
+        if (p == 0) {  // layer 1: K = 32 split operands (bias included)
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            mma_ts_elect(d, tbase + kColX + 8u * k, sdesc_nosw(sb1 + k * 2 * (H * 16), H * 16, 128), kIdescW, k > 0);
+        } else if (p < 11) {  // hidden layer (forward p = 1..5, backward p = 6..10): 4 streamed chunks
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c, ++ci) {
+            const int slot = (int)(ci % kNS);
+            mbar_wait(&S.full[slot], (uint32_t)((ci / kNS) & 1));
+            const uint32_t base = smem_u32(S.ring[slot]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_ts_elect(d, av + 8u * (uint32_t)(4 * c + k), sdesc_sw128(base + k * 32, 16, 1024), kIdescW,
+                           (c | k) > 0);
+            commit_elect(&S.empty[slot]);
+          }
+          if (p < 6)  // + ones x {b_hi, b_lo}
+            mma_ts_elect(d, tbase + kColOnes, sdesc_nosw(sbx + (uint32_t)(p - 1) * kBextBytes, H * 16, 128), kIdescW, 1u);
+        } else {  // g0 = e1 W1 (N = 16 rows of W1^T)
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            mma_ts_elect(d, av + 8u * k, sdesc_sw128(sw1t + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin, k > 0);
+        }
+        commit_elect(&S.mma_done);
+      }
+    }
+    __syncwarp();
+    fence_before();
+    __syncthreads();
+    return;
+  }
+
+  // ===================== epilogue warps ===============================================
+  const int qd = warp & 3;   // TMEM lane quarter
+  const int cq = warp >> 2;  // unit quarter: units 64 cq .. 64 cq + 63
+  const int row = qd * 32 + lane;
+  const int u0 = 64 * cq;
+  const uint32_t tL = tbase + ((uint32_t)(qd * 32) << 16);
+  const uint32_t tD = tL + (uint32_t)u0;
+  const uint32_t tA = tL + kColA + 32u * (uint32_t)cq;
+  uint32_t *mk = &S.mask[0][0][tid];  // + (layer * 2 + word) * kEpi
+  const uint32_t one = S.one;
+  if (cq == 2) {  // the constant ones block of the bias steps: {1, 1, 0, ...} (never overwritten)
+    const uint32_t ones[8] = {pack_f16(1.f, 1.f), 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    st8(tL + kColOnes, ones);
+  }
+  auto hand_off = [&]() {
+    wait_st();
+    fence_before();
+    mbar_arrive(&S.epi_done);
+  };
+  auto prefetch = [&](int64_t TT, int par) {  // (unit quarter 0) point, slot and q row of tile TT
+    int wn = 0;
+    int64_t sl = 0;
+    bool ok = false;
+    if (TT < n_tiles) tile_pair(a, TT, row, wn, sl, ok);
+    S.slotn[par][row] = ok ? (uint32_t)sl : ~0u;
+    cp_async16(&S.ptn[row], ok ? (const void *)(a.scene.pts + sl) : (const void *)a.scene.pts, ok ? 16u : 0u);
+    if (warp == 0 && TT < n_tiles) {
+      wn = tile_step(a, TT);
+      if (lane < kNdof) cp_async4(&S.qn[par][lane], a.q + (int64_t)wn * kNdof + lane);
+      if (lane == 0) S.wtile[par] = wn;
+    }
+    cp_async_commit();
+  };
+  auto stage_a1 = [&](int par) -> bool {  // layer-1 operands (K2b's split layout) -> TMEM
+    const float *qw = S.qn[par];
+    bool lv = false;
+    if (cq == 0) {
+      float v[16];
+      const float4 pt = S.ptn[row];
+      lv = S.slotn[par][row] != ~0u && pt.w > 0.f;
+      split3(pt.x - qw[0], v);  // A2: p' = p - [q_x, q_y, 0]
+      split3(pt.y - qw[1], v + 3);
+      split3(pt.z, v + 6);
+      split3(qw[2], v + 9);
+      split3(qw[3], v + 12);
+      v[15] = round16(qw[4]);
+      uint32_t a1[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a1[i] = pack_f16(v[2 * i], v[2 * i + 1]);
+      st8(tL + kColX, a1);
+    } else if (cq == 1) {
+      float v[16];
+      const float j2 = qw[4];
+      const float j2h = round16(j2);
+      v[0] = j2 - j2h;
+      v[1] = j2h;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) split3(qw[5 + i], v + 2 + 3 * i);
+      v[14] = 1.f;
+      v[15] = 1.f;
+      uint32_t a1[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a1[i] = pack_f16(v[2 * i], v[2 * i + 1]);
+      st8(tL + kColX + 8u, a1);
+    }
+    hand_off();
+    return lv;
+  };
+
+  uint32_t ph = 0u;
+  int it = 0;
+  bool live_n = false;
+  if (my_tiles > 0) {
+    if (cq == 0) prefetch(blockIdx.x, 0);
+    cp_async_wait_all();
+    named_bar_sync(1, kEpi);
+    live_n = stage_a1(0);
+  }
+  for (int64_t T = blockIdx.x; T < n_tiles; T += stride, ++it) {
+    const int par = it & 1;
+    const bool live = live_n;
+    float f = 0.f;
+    int ridx = -1;
+    unsigned long long pend_b = 0ull;
+    int pend_cnt = 0;
+#pragma unroll 1
+    for (int p = 0; p < kPhases; ++p) {
+      mbar_wait(&S.mma_done, ph);
+      ph ^= 1u;
+      fence_after();
+      if (p < 5) {
+        // ---- forward layer l = p + 1: h = ReLU(z) -> A (fp16), 1-bit masks -> smem ----
+        uint32_t rb[2][16], m = 0u;
+        ld16(tD, rb[0]);
+        wait_ld();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c < 3) ld16(tD + 16 * (c + 1), rb[(c + 1) & 1]);
+          const uint32_t *rr = rb[c & 1];
+          uint32_t pk[8];
+#pragma unroll
+          for (int j = 0; j < 16; j += 4) {
+            pk[j >> 1] = pack_f16_relu(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1]));
+            pk[(j >> 1) + 1] = pack_f16_relu(__uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3]));
+            m |= mask_group_f(pk[j >> 1], pk[(j >> 1) + 1], ((c & 1) * 16 + j) >> 2, one);
+          }
+          st8(tA + 8 * c, pk);
+          if (c & 1) {
+            mk[(p * 2 + (c >> 1)) * kEpi] = m;
+            m = 0u;
+          }
+          if (c < 3) wait_ld();
+        }
+        hand_off();
+      } else if (p == 5) {
+        // ---- layer 6: e6 = w7 (.) 1[z6 > 0] -> A; f = w7 . ReLU(z6) + b7 (fp32) ----
+        float fa[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t rb[2][16];
+        ld16(tD, rb[0]);
+        wait_ld();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int cb = 16 * c;
+          if (c < 3) ld16(tD + cb + 16, rb[(c + 1) & 1]);
+          const uint32_t *rr = rb[c & 1];
+          uint32_t pk[8];
+#pragma unroll
+          for (int j = 0; j < 16; j += 4) {
+            const float4 w7 = *reinterpret_cast<const float4 *>(S.w7half + u0 + cb + j);
+            const uint2 w2 = *reinterpret_cast<const uint2 *>(S.w7h + (u0 + cb + j) / 2);
+            const float z0 = __uint_as_float(rr[j]), z1 = __uint_as_float(rr[j + 1]);
+            const float z2 = __uint_as_float(rr[j + 2]), z3 = __uint_as_float(rr[j + 3]);
+            pk[j >> 1] = w2.x & nz_halves(pack_f16_relu(z0, z1), one);
+            pk[(j >> 1) + 1] = w2.y & nz_halves(pack_f16_relu(z2, z3), one);
+            fa[0] = fmaf(w7.x, z0 + fabsf(z0), fa[0]);
+            fa[1] = fmaf(w7.y, z1 + fabsf(z1), fa[1]);
+            fa[2] = fmaf(w7.z, z2 + fabsf(z2), fa[2]);
+            fa[3] = fmaf(w7.w, z3 + fabsf(z3), fa[3]);
+          }
+          st8(tA + cb / 2, pk);
+          if (c < 3) wait_ld();
+        }
+        hand_off();
+        S.fpart[cq][row] = (fa[0] + fa[1]) + (fa[2] + fa[3]);
+        named_bar_sync(1, kEpi);
+        if (cq == 0) {
+          f = (S.fpart[0][row] + S.fpart[1][row]) + (S.fpart[2][row] + S.fpart[3][row]) + W.b7;
+          if (!a.detect) {
+            const int w = S.wtile[par];
+            const int64_t slot = S.slotn[par][row];
+            if (slot < lb) a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
+          }
+        }
+      } else if (p < 11) {
+        // ---- backward: g_{l-1} = D; e_{l-1} = g (.) 1[z_{l-1} > 0] -> A ----
+        const int mi = 10 - p;
+        const uint32_t mw[2] = {mk[(mi * 2) * kEpi], mk[(mi * 2 + 1) * kEpi]};
+        uint32_t rb[2][16];
+        ld16(tD, rb[0]);
+        wait_ld();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c < 3) ld16(tD + 16 * (c + 1), rb[(c + 1) & 1]);
+          const uint32_t *rr = rb[c & 1];
+          uint32_t pk[8];
+#pragma unroll
+          for (int j = 0; j < 16; j += 4) {
+            uint32_t lo, hi;
+            mask_expand(mw[c >> 1], ((c & 1) * 16 + j) >> 2, lo, hi);
+            pk[j >> 1] = pack_f16(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1])) & lo;
+            pk[(j >> 1) + 1] = pack_f16(__uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3])) & hi;
+          }
+          st8(tA + 8 * c, pk);
+          if (c < 3) wait_ld();
+        }
+        hand_off();
+        if (p == 6 && cq == 0 && a.detect) {
+          // A6/A7: threshold, per-tile slots, per-waypoint min key
+          const int w = S.wtile[par];
+          const int64_t slot = S.slotn[par][row];
+          const bool act = live && (f - a.delta <= a.tau);
+          const unsigned bal = __ballot_sync(0xffffffffu, act);
+          unsigned long long key = ~0ull;
+          if (live)
+            key = ((unsigned long long)ord_f32(f) << 32) |
+                  (unsigned long long)local_to_global(slot, a.scene.rank, a.scene.world);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+            key = other < key ? other : key;
+          }
+          if (lane == 0) {
+            S.act[qd] = bal;
+            S.kmin[qd] = key;
+          }
+          named_bar_sync(2, 128);
+          int rk = __popc(bal & ((1u << lane) - 1u));
+          for (int i = 0; i < qd; ++i) rk += __popc(S.act[i]);
+          ridx = act ? rk : -1;
+          if (row == 0) {
+            unsigned long long km = S.kmin[0];
+            int cnt = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              km = S.kmin[i] < km ? S.kmin[i] : km;
+              cnt += __popc(S.act[i]);
+            }
+            if (km != ~0ull) atomicMin(a.ds.wp_key + w, km);
+            pend_cnt = cnt;
+            pend_b = cnt > 0 ? atomicAdd(a.ds.counter, (unsigned long long)cnt) : 0ull;
+          }
+        }
+        if (p == 7 && cq == 0) prefetch(T + stride, par ^ 1);
+        if (p == 8 && cq == 0 && a.detect && row == 0) {
+          int base = 0;
+          if (pend_cnt > 0) {
+            if (pend_b + pend_cnt > (unsigned long long)a.ds.max_active) {
+              atomicOr(a.ds.counter + 1, 1ull);
+              base = -1;
+            } else {
+              base = (int)pend_b;
+            }
+          }
+          S.sbase = base;
+          a.ds.tile_meta[T] = make_int2(base, pend_cnt);
+        }
+        if (p == 10 && cq <= 1) {
+          if (cq == 0) cp_async_wait_all();
+          named_bar_sync(3, 256);
+        }
+      } else {
+        // ---- g0 = W1^T e1 (16 columns); d f / d q by the chain rule (R3) ----
+        uint32_t r[16];
+        if (cq == 0) {
+          ld16(tL, r);
+          wait_ld();
+        }
+        if (T + stride < n_tiles) live_n = stage_a1(par ^ 1);
+        if (cq == 0) {
+          const int w = S.wtile[par];
+          const int64_t slot = S.slotn[par][row];
+          float gq[kNdof];
+          gq[0] = a.tgrad ? __uint_as_float(r[3]) : -__uint_as_float(r[0]);
+          gq[1] = a.tgrad ? __uint_as_float(r[4]) : -__uint_as_float(r[1]);
+#pragma unroll
+          for (int i = 0; i < 7; ++i) gq[2 + i] = __uint_as_float(r[5 + i]);
+          if (a.detect) {
+            const int base = S.sbase;
+            ridx = (ridx >= 0 && base >= 0) ? base + ridx : -1;
+            if (ridx >= 0) {
+              float4 *dst = reinterpret_cast<float4 *>(a.ds.staging + ridx);
+              dst[0] = make_float4(f, gq[0], gq[1], gq[2]);
+              dst[1] = make_float4(gq[3], gq[4], gq[5], gq[6]);
+              dst[2] = make_float4(gq[7], gq[8], __uint_as_float((unsigned)w),
+                                   __uint_as_float((unsigned)local_to_global(slot, a.scene.rank, a.scene.world)));
+            }
+          } else if (a.grads && slot < lb) {
+            float *o = a.grads + ((int64_t)w * lb + slot) * kNdof;
+            if (a.project) {  // NEXT-3: q_z = q - f M^{-1} grad_q f (Theorem 1.2)
+              const float *qw = S.qn[par];
+#pragma unroll
+              for (int i = 0; i < kNdof; ++i) o[i] = live ? qw[i] - (f * gq[i]) * a.minv[i] : 0.f;
+            } else {
+#pragma unroll
+              for (int i = 0; i < kNdof; ++i) o[i] = live ? gq[i] : 0.f;
+            }
+          }
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0) tmem_dealloc(tbase, 512);
+}
+
+}  // namespace
+
+cudaError_t launch_mlp_tc_wide(const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s) {
+  if (a.frame || a.act != 1) return cudaErrorInvalidValue;  // (H = 256: ReLU, translation frame)
+  const int smem = (int)sizeof(SmemW) + 1024;
+  cudaError_t e = cudaFuncSetAttribute(k_mlp_tc_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t n_tiles = a.part.tile_wp ? (int64_t)num_sms : (int64_t)a.n_wp * a.tiles_per_wp;
+  int64_t grid = n_tiles < num_sms ? n_tiles : num_sms;
+  if (grid < 1) return cudaSuccess;
+  k_mlp_tc_wide<<<(unsigned)grid, kThreads, smem, s>>>(w, a);
+  return cudaGetLastError();
+}
+
+}  // namespace gcdf

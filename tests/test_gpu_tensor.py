@@ -57,7 +57,7 @@ def test_selftest_umma(mode, prec):
     assert err <= 1e-4 * max(1.0, ref.abs().max().item()), err
 
 
-def stats_and_gates(v, g, exact, emu, prec, what=""):
+def stats_and_gates(v, g, exact, emu, prec, what="", agree_min=0.85):
     dv = np.abs(v - emu["f"])
     de = np.abs(v - exact["f"])
     gn_g = np.linalg.norm(g, axis=-1)
@@ -75,7 +75,7 @@ def stats_and_gates(v, g, exact, emu, prec, what=""):
     # gate 1: the bulk agrees with the emulation to fp32-accumulation noise; the tail is
     # 16-bit rounding-boundary / ReLU-kink flips (8x more frequent but 8x smaller for fp16)
     assert st["emu_val_p50"] <= 1e-6, st
-    assert st["emu_val_agree_1e-5"] >= 0.85, st
+    assert st["emu_val_agree_1e-5"] >= agree_min, st
     assert st["emu_val_max"] <= (1e-2 if prec == "fp16" else 3e-2), st
     # bf16: layer 1 runs on split bf16 operands (~16-bit effective precision, not the EMU
     # model's exact layer 1), which moves a few more ReLU kinks
