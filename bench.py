@@ -13,6 +13,7 @@ job per second.  Prints ONE JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import subprocess
@@ -29,8 +30,8 @@ sys.path.insert(0, str(ROOT))
 import synth  # noqa: E402
 
 METRIC = "GCDF value+grad queries/sec (with active-set detection)"
-FLOPS_PAIR_TOTAL = {128: 333_312, 32: 21_888}      # fwd 167,168 + bwd 166,144 (H=128)
-FLOPS_PAIR_TENSOR = {128: 327_680, 32: 20_480}     # the ten H x H GEMMs (tensor-eligible)
+FLOPS_PAIR_TOTAL = {128: 333_312, 32: 21_888, 256: 1_321_984}   # fwd 167,168 + bwd 166,144 (H=128)
+FLOPS_PAIR_TENSOR = {128: 327_680, 32: 20_480, 256: 1_310_720}   # the ten H x H GEMMs (tensor-eligible)
 ACT = {"relu": 1, "softplus": 2}                   # MLPW activation ids (R9, R26)
 
 
@@ -41,6 +42,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C5")
     ap.add_argument("--precision", default="auto", choices=["auto", "fp16", "bf16", "fp32", "fp16x3"])
+    ap.add_argument("--hidden", type=int, default=None, choices=[128, 256],
+                    help="hidden width override for the H = 128 configs (256: NEXT-4 variant, DESIGN.md R27)")
     ap.add_argument("--activation", default="relu", choices=["relu", "softplus"],
                     help="hidden activation of the random-init network (softplus: NEXT-4 variant, DESIGN.md R26)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -106,14 +109,14 @@ def measured_peaks():
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def cpu_oracle_rate(cfg, pts, q, sample_pts=8192, nthreads=None, seed=12345, single_thread=False, act=1):
+def cpu_oracle_rate(cfg, pts, q, sample_pts=8192, nthreads=None, seed=12345, single_thread=False, act=1, hidden=None):
     """The oracle as it stands on the host cores: detect over a bounded sample of the
     workload -- one waypoint row per core (the oracle threads over waypoint rows) x
     sample_pts points."""
     import oracle
     nthreads = nthreads or os.cpu_count() or 1
     m = oracle.MLP(synth.weights_path(cfg.H, act=act))
-    tau = synth.load_tau(cfg.name, act)
+    tau = synth.load_tau(cfg.name, act, hidden)
     rng = np.random.default_rng(seed)
     qs = q.reshape(-1, 9)
     wsel = np.sort(rng.choice(qs.shape[0], size=min(nthreads, qs.shape[0]), replace=False))
@@ -141,11 +144,15 @@ def run_reference(a):
     if rank != 0:
         return
     cfg = synth.get_config(a.config)
+    hidden = a.hidden if a.hidden and a.hidden != cfg.H else None
+    if hidden:
+        cfg = dataclasses.replace(cfg, H=hidden)
     pts, _ = synth.make_scene_points(cfg)
     q = synth.make_waypoints(cfg)
     times, n_pairs, r = [], 0, None
     for i in range(a.warmup + a.steps):
-        r = cpu_oracle_rate(cfg, pts, q, sample_pts=2048, seed=1000 + i, act=ACT[a.activation])
+        r = cpu_oracle_rate(cfg, pts, q, sample_pts=2048 if cfg.H <= 128 else 512, seed=1000 + i,
+                            act=ACT[a.activation], hidden=hidden)
         if i >= a.warmup:
             times.append(r["seconds"])
             n_pairs += r["pairs"]
@@ -184,10 +191,13 @@ def main():
     lib = load_library()
     prec = a.precision
     cfg = synth.get_config(a.config)
+    hidden = a.hidden if a.hidden and a.hidden != cfg.H else None
+    if hidden:
+        cfg = dataclasses.replace(cfg, H=hidden)
     if prec == "auto":  # the tensor-core path needs H = 128 (C1's H = 32 net runs on the fp32 path)
-        prec = "fp16" if lib.gcdf_has_tcgen05() and cfg.H == 128 else "fp32"
+        prec = "fp16" if lib.gcdf_has_tcgen05() and cfg.H >= 128 else "fp32"
     act = ACT[a.activation]
-    tau = synth.load_tau(cfg.name, act)
+    tau = synth.load_tau(cfg.name, act, hidden)
     delta = synth.inputs.DELTA
     pts, boxes = synth.make_scene_points(cfg)
     q_np = synth.make_waypoints(cfg)
@@ -283,7 +293,8 @@ def main():
         peak = float(peaks.get(key))
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "traffic": None, "peak_source": f"{peak_src} {key} (MEASURED_PEAKS.json; fp16 dense = bf16 dense)",
-                "kernel": ("k_mlp_tc3" if n_terms == 3 else "k_mlp_tc_sp" if act == 2 else "k_mlp_tc") +
+                "kernel": ("k_mlp_tc3" if n_terms == 3 else "k_mlp_tc_sp" if act == 2 else
+                           "k_mlp_tc_wide" if cfg.H == 256 else "k_mlp_tc") +
                           " (fused transform + MLP fwd/bwd + threshold/min/compaction)",
                 "kernel_ms_avg": mlp_ms / mlp_n, "flops_per_pair": n_terms * FLOPS_PAIR_TENSOR[cfg.H]}
     else:
@@ -296,7 +307,7 @@ def main():
                 "kernel": "k_mlp_simt (fused transform + MLP fwd/bwd + threshold/min/compaction)",
                 "kernel_ms_avg": mlp_ms / mlp_n, "flops_per_pair": FLOPS_PAIR_TOTAL[cfg.H]}
     tf = ROOT / "profiles" / "traffic.json"
-    if tf.exists() and prec in ("bf16", "fp16") and act == 1:  # (measured for k_mlp_tc only)
+    if tf.exists() and prec in ("bf16", "fp16") and act == 1 and cfg.H == 128:  # (measured for k_mlp_tc only)
         t = json.loads(tf.read_text()).get("k_mlp_tc")
         if t:
             roof["traffic"] = t["bytes"]
@@ -419,7 +430,8 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cpu = cpu_oracle_rate(cfg, pts, q_np, sample_pts=65536, single_thread=True, act=act)
+        cpu = cpu_oracle_rate(cfg, pts, q_np, sample_pts=65536 if cfg.H <= 128 else 16384, single_thread=True,
+                              act=act, hidden=hidden)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world, "steps": a.steps,

@@ -6,8 +6,8 @@ parity test read what it produces.  Recipe: DESIGN.md "Input recipe".
 """
 from .inputs import (CONFIGS, Config, get_config, make_scene_points, make_waypoints,
                      make_weights, write_mlpw, read_mlpw_raw, weights_path, scene_update_batch,
-                     load_tau)
+                     load_tau, tau_key)
 
 __all__ = ["CONFIGS", "Config", "get_config", "make_scene_points", "make_waypoints",
            "make_weights", "write_mlpw", "read_mlpw_raw", "weights_path", "scene_update_batch",
-           "load_tau"]
+           "load_tau", "tau_key"]

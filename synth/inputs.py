@@ -68,11 +68,17 @@ def get_config(name: str) -> Config:
     return CONFIGS[name]
 
 
-def load_tau(name: str, act: int = 1) -> float:
-    """tau frozen by tools/calibrate_tau.py (which calls only oracle/); act = 2: the softplus
-    network's margin (key "<name>_softplus")."""
+def tau_key(name: str, act: int = 1, hidden=None) -> str:
+    """configs/tau.json key: "<name>", "<name>_softplus" (act 2, R26) or "<name>_H256" (R27)."""
+    if hidden is not None and hidden != get_config(name).H:
+        return f"{name}_H{hidden}"
+    return name if act == 1 else name + "_softplus"
+
+
+def load_tau(name: str, act: int = 1, hidden=None) -> float:
+    """tau frozen by tools/calibrate_tau.py (which calls only oracle/)."""
     with open(REPO / "configs" / "tau.json") as fh:
-        return float(json.load(fh)[name if act == 1 else name + "_softplus"]["tau"])
+        return float(json.load(fh)[tau_key(name, act, hidden)]["tau"])
 
 
 # ----------------------------------------------------------------------------- scene

@@ -6,6 +6,7 @@ about a fraction q of pairs is active.  f comes ONLY from the float64 oracle
 Usage: python tools/calibrate_tau.py [--threads T]
 """
 import argparse
+import dataclasses
 import json
 import os
 import sys
@@ -28,9 +29,13 @@ def main():
     a = ap.parse_args()
     out = {}
     # act 1: the ReLU network (R9); act 2: the same weights under softplus (NEXT-4, R26),
-    # stored as "<config>_softplus"
-    for act in (1, 2):
+    # stored as "<config>_softplus"; hidden 256: the wide network (NEXT-4, R27), "<config>_H256"
+    for act, hidden in ((1, None), (2, None), (1, 256)):
         for name, cfg in synth.CONFIGS.items():
+            if hidden is not None:
+                if cfg.H != 128:
+                    continue
+                cfg = dataclasses.replace(cfg, H=hidden)
             pts, _ = synth.make_scene_points(cfg)
             q = synth.make_waypoints(cfg).reshape(-1, 9)
             rng = np.random.default_rng([cfg.seed, 99])
@@ -41,7 +46,7 @@ def main():
             quant = float(np.quantile(f, cfg.quantile))
             tau = quant - synth.inputs.DELTA
             frac = float(np.mean(f - synth.inputs.DELTA <= tau))
-            key = name if act == 1 else name + "_softplus"
+            key = synth.tau_key(name, act, hidden)
             out[key] = {"tau": tau, "quantile": cfg.quantile, "sample_pairs": int(f.size),
                         "sample_active_fraction": frac, "f_mean": float(f.mean()), "f_std": float(f.std())}
             print(key, out[key], flush=True)
