@@ -59,7 +59,8 @@ constexpr int64_t kX3Total = 5 * 2 * kBfMat + 2 * kBfW1t;
 constexpr int kWideH = 256;
 constexpr int64_t kWideChunk = (int64_t)kWideH * 128;
 constexpr int64_t kWideSeq = 40 * kWideChunk;
-constexpr int64_t kWideW1t = 16LL * kWideH * 2, kWideB1 = 32LL * kWideH * 2, kWideBext = 16LL * kWideH * 2;
+constexpr int64_t kWideW1t = 16LL * kWideH * 2, kWideB1 = 32LL * kWideH * 2;
+constexpr int64_t kWideBext = 8LL * kWideH * 2;  // K-core 0 of [256][16] {b_hi, b_lo, 0..}; core 1 is zero
 constexpr int64_t kWideTotal = kWideSeq + kWideW1t + kWideB1 + 5 * kWideBext;
 
 }  // namespace
@@ -648,14 +649,14 @@ int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
     }
     pack_nosw(b1, H, 32, wide.data() + (kWideSeq + kWideW1t) / 2, true);
     for (int li = 0; li < 5; ++li) {
-      std::vector<float> be((size_t)H * 16, 0.f);
+      std::vector<float> be((size_t)H * 8, 0.f);
       for (int u = 0; u < H; ++u) {
         float hi, lo;
         split16(bd[li + 1][u], true, hi, lo);
-        be[(size_t)u * 16 + 0] = hi;
-        be[(size_t)u * 16 + 1] = lo;
+        be[(size_t)u * 8 + 0] = hi;
+        be[(size_t)u * 8 + 1] = lo;
       }
-      pack_nosw(be, H, 16, wide.data() + (kWideSeq + kWideW1t + kWideB1 + li * kWideBext) / 2, true);
+      pack_nosw(be, H, 8, wide.data() + (kWideSeq + kWideW1t + kWideB1 + li * kWideBext) / 2, true);
     }
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -12,15 +12,21 @@
 //     streamed from L2 (where the 1.25 MB chunk sequence stays resident) through a ring of
 //     four 32 KB slots by a producer warp (1-D cp.async.bulk completing on the slot's "full"
 //     mbarrier); the MMA warp releases a slot with a tcgen05.commit on its "empty" mbarrier
-//     once the four UMMAs that read it complete.  The chunk sequence of a tile is laid out in
+//     once the UMMAs of both output halves that read it complete.  The chunk sequence of a tile is laid out in
 //     consumption order: W_2..W_6 K-major [out][in] (forward), then W_6^T..W_2^T K-major
 //     [in][out] (backward), 4 chunks of 64 K-columns per layer -- so forward and backward
 //     UMMAs use the same descriptor pattern and the producer streams one contiguous image.
-//   * every UMMA is M = 128, N = 256, K = 16 (128 cycles at the dense rate); a layer is 16.
-//   * TMEM: D [0, 256) fp32, A [256, 384) fp16 (K = 256), layer-1 operands [384, 400), ones
-//     block [400, 408): one tile in flight (two would need 2 x 384 columns).  16 epilogue
-//     warps own 32 rows x 64 units each (the K2b per-thread work), ReLU masks in shared
-//     memory in K2b's byte-sign form.
+//   * one tile in flight (two would need 2 x 384 TMEM columns), pipelined by output half:
+//     a layer is two N = 128 UMMA chains (units 0..127, then 128..255; 16 K-steps of
+//     128 x 128 x 16 each).  The epilogue warps of half 0 start as soon as half 0's chain
+//     completes, while the tensor core runs half 1; the next layer's half-0 chain starts
+//     its first 8 K-steps (which read only the units half 0 produced) before half 1's
+//     epilogue is done.  That needs the A operand double-buffered by phase parity:
+//     TMEM = D [0, 256) fp32 (half h at 128 h) + A[0] [256, 384) + A[1] [384, 512) fp16;
+//     the layer-1 operands live in A[0]'s first 16 columns, and the bias steps take their
+//     constant "ones" A block from shared memory (SS-mode UMMA).
+//   * 16 epilogue warps own 32 rows x 64 units each (warps 8 h .. 8 h + 7: output half h;
+//     the K2b per-thread work), ReLU masks in shared memory in K2b's byte-sign form.
 // Rounding points: those of K2b (EMU_FP16 in the oracle: W_2..W_6, W_1 (gradient), h_1..h_5,
 // e_6..e_1 rounded to fp16; layer 1 split hi/lo; f = w7 . h6 in fp32).
 #include "gcdf_internal.h"
@@ -43,16 +49,20 @@ constexpr int kChunk = H * 128;             // 32 KB: [256 rows][64 K-columns] f
 constexpr int kChunksPerTile = 40;          // 5 layers x 4 forward + 5 x 4 backward
 constexpr int kW1tBytes = 16 * H * 2;       // 8 KB
 constexpr int kB1Bytes = 32 * H * 2;        // 16 KB
-constexpr int kBextBytes = 16 * H * 2;      // 8 KB per hidden layer
-constexpr uint32_t kColA = 256, kColX = 384, kColOnes = 400;
-constexpr uint32_t kIdescW = idesc_f16kind(128, 256, false, true);
+constexpr int kBextCore = H * 16;           // 4 KB per hidden layer: K-core 0 {b_hi, b_lo, 0..} of [256][16]
+constexpr int kZeroBytes = 4096;            // shared all-zero K-core 1 of the bias and ones blocks
+constexpr int kOnesBytes = 128 * 16;        // K-core 0 of the ones block [128][16] {1, 1, 0..}
+constexpr uint32_t kColA = 256;             // A[b] at 256 + 128 b
+constexpr uint32_t kIdescW = idesc_f16kind(128, 128, false, true);
 constexpr uint32_t kIdescFin = idesc_f16kind(128, 16, false, true);
 
 struct __align__(1024) SmemW {
   uint8_t ring[kNS][kChunk];
   uint8_t w1t[kW1tBytes];
   uint8_t b1[kB1Bytes];
-  uint8_t bext[5][kBextBytes];
+  uint8_t bext[5][kBextCore];
+  uint8_t ones[kOnesBytes];
+  uint8_t zero[kZeroBytes];        // (after bext and ones: the descriptors' LBO offsets are positive)
   uint32_t mask[kMasks][2][kEpi];  // ReLU masks [layer][32-unit word][thread]
   float w7half[H];
   uint32_t w7h[H / 2];
@@ -62,7 +72,7 @@ struct __align__(1024) SmemW {
   float qn[2][12];
   int wtile[2];
   uint32_t slotn[2][128];
-  uint64_t mma_done, epi_done;
+  uint64_t mma_done[2], epi_done[2];  // [output half]
   uint64_t full[kNS], empty[kNS];
   unsigned act[4];
   unsigned long long kmin[4];
@@ -107,7 +117,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
     };
     copy16(S.w1t, W.w1t_sw128, kW1tBytes);
     copy16(S.b1, W.b1_nosw, kB1Bytes);
-    copy16(S.bext, W.bext_nosw, 5 * kBextBytes);
+    copy16(S.bext, W.bext_nosw, 5 * kBextCore);
+    for (int i = tid; i < kZeroBytes / 16; i += kThreads) reinterpret_cast<uint4 *>(S.zero)[i] = make_uint4(0, 0, 0, 0);
+    for (int r = tid; r < 128; r += kThreads)  // ones block, no-swizzle K-major: row r at (r / 8) * 128 + (r % 8) * 16
+      *reinterpret_cast<uint4 *>(S.ones + (r >> 3) * 128 + (r & 7) * 16) = make_uint4(pack_f16(1.f, 1.f), 0u, 0u, 0u);
     for (int i = tid; i < H; i += kThreads) S.w7half[i] = 0.5f * __ldg(W.w7 + i);
     for (int i = tid; i < H / 2; i += kThreads) S.w7h[i] = pack_f16(__ldg(W.w7 + 2 * i), __ldg(W.w7 + 2 * i + 1));
     if (tid == 0) S.one = 1u;
@@ -117,8 +130,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
     tmem_relinquish();
   }
   if (tid == 32) {
-    mbar_init(&S.mma_done, 1);
-    mbar_init(&S.epi_done, kEpi);
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&S.mma_done[h], 1);
+      mbar_init(&S.epi_done[h], kEpi / 2);
+    }
     for (int i = 0; i < kNS; ++i) {
       mbar_init(&S.full[i], 1);
       mbar_init(&S.empty[i], 1);
@@ -155,39 +170,75 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
   if (warp == kMmaWarp) {
     // ===================== MMA warp (converged; an elected lane issues) ======================
     const uint32_t sw1t = smem_u32(S.w1t), sb1 = smem_u32(S.b1), sbx = smem_u32(S.bext);
-    const uint32_t d = tbase, av = tbase + kColA;
-    uint32_t ph = 0u;
+    const uint32_t szero = smem_u32(S.zero), sones = smem_u32(S.ones);
+    // bias step of layer l (1..5 = W_2..W_6) for output half h: A = ones (smem), B = rows
+    // 128 h.. of the layer's bias block; both K-core 1 halves point at the shared zero block
+    const uint64_t a_ones = sdesc_nosw(sones, szero - sones, 128);
+    auto b_bias = [&](int l, int h) {
+      const uint32_t st = sbx + (uint32_t)(l - 1) * kBextCore + 2048u * (uint32_t)h;
+      return sdesc_nosw(st, szero - st, 128);
+    };
+    uint32_t ph0 = 0u, ph1 = 0u;
     int64_t ci = 0;  // chunks consumed
+    auto wait_epi = [&](int h) {
+      if (h == 0) { mbar_wait(&S.epi_done[0], ph0); ph0 ^= 1u; }
+      else { mbar_wait(&S.epi_done[1], ph1); ph1 ^= 1u; }
+      fence_after();
+    };
     for (int64_t t = 0; t < my_tiles; ++t) {
 #pragma unroll 1
       for (int p = 0; p < kPhases; ++p) {
-        mbar_wait(&S.epi_done, ph);
-        ph ^= 1u;
-        fence_after();
-        if (p == 0) {  // layer 1: K = 32 split operands (bias included)
+        const uint32_t ab = tbase + kColA + 128u * (uint32_t)(p & 1);  // A buffer read by phase p
+        wait_epi(0);
+        if (p == 0) {  // layer 1: K = 32 split operands (bias included), A = A[0] columns 0..15
+          wait_epi(1);
 #pragma unroll
-          for (int k = 0; k < 2; ++k)
-            mma_ts_elect(d, tbase + kColX + 8u * k, sdesc_nosw(sb1 + k * 2 * (H * 16), H * 16, 128), kIdescW, k > 0);
-        } else if (p < 11) {  // hidden layer (forward p = 1..5, backward p = 6..10): 4 streamed chunks
+          for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+              mma_ts_elect(tbase + 128u * h, ab + 8u * k, sdesc_nosw(sb1 + k * 2 * (H * 16) + 2048 * h, H * 16, 128),
+                           kIdescW, k > 0);
+            commit_elect(&S.mma_done[h]);
+          }
+        } else if (p < 11) {
+          // hidden layer (forward p = 1..5, backward p = 6..10), 4 streamed chunks of 64 K
+          // output half 0: K-steps 0..7 need only the units half 0's epilogue wrote
 #pragma unroll 1
-          for (int c = 0; c < 4; ++c, ++ci) {
-            const int slot = (int)(ci % kNS);
-            mbar_wait(&S.full[slot], (uint32_t)((ci / kNS) & 1));
-            const uint32_t base = smem_u32(S.ring[slot]);
+          for (int c = 0; c < 4; ++c) {
+            if (c == 2) wait_epi(1);
+            const int64_t cc = ci + c;
+            mbar_wait(&S.full[cc % kNS], (uint32_t)((cc / kNS) & 1));
+            const uint32_t base = smem_u32(S.ring[cc % kNS]);
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-              mma_ts_elect(d, av + 8u * (uint32_t)(4 * c + k), sdesc_sw128(base + k * 32, 16, 1024), kIdescW,
+              mma_ts_elect(tbase, ab + 8u * (uint32_t)(4 * c + k), sdesc_sw128(base + k * 32, 16, 1024), kIdescW,
                            (c | k) > 0);
-            commit_elect(&S.empty[slot]);
           }
-          if (p < 6)  // + ones x {b_hi, b_lo}
-            mma_ts_elect(d, tbase + kColOnes, sdesc_nosw(sbx + (uint32_t)(p - 1) * kBextBytes, H * 16, 128), kIdescW, 1u);
-        } else {  // g0 = e1 W1 (N = 16 rows of W1^T)
+          if (p < 6) mma_ss_elect(tbase, a_ones, b_bias(p, 0), kIdescW, 1u);
+          commit_elect(&S.mma_done[0]);
+          // output half 1: B rows 128..255 of the same chunks; each chunk's slot is released
+          // once these (its last readers) complete
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            const int64_t cc = ci + c;
+            const uint32_t base = smem_u32(S.ring[cc % kNS]) + 16384u;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              mma_ts_elect(tbase + 128u, ab + 8u * (uint32_t)(4 * c + k), sdesc_sw128(base + k * 32, 16, 1024),
+                           kIdescW, (c | k) > 0);
+            commit_elect(&S.empty[cc % kNS]);
+          }
+          if (p < 6) mma_ss_elect(tbase + 128u, a_ones, b_bias(p, 1), kIdescW, 1u);
+          commit_elect(&S.mma_done[1]);
+          ci += 4;
+        } else {  // g0 = e1 W1 (N = 16 rows of W1^T) -> D columns 0..15
+          wait_epi(1);
 #pragma unroll
           for (int k = 0; k < 16; ++k)
-            mma_ts_elect(d, av + 8u * k, sdesc_sw128(sw1t + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin, k > 0);
+            mma_ts_elect(tbase, ab + 8u * k, sdesc_sw128(sw1t + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin, k > 0);
+          commit_elect(&S.mma_done[0]);
+          commit_elect(&S.mma_done[1]);
         }
-        commit_elect(&S.mma_done);
       }
     }
     __syncwarp();
@@ -202,18 +253,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
   const int row = qd * 32 + lane;
   const int u0 = 64 * cq;
   const uint32_t tL = tbase + ((uint32_t)(qd * 32) << 16);
+  const int half = cq >> 1;  // output half of this warp's units
   const uint32_t tD = tL + (uint32_t)u0;
-  const uint32_t tA = tL + kColA + 32u * (uint32_t)cq;
+  auto tA = [&](int p) {     // A buffer written by the epilogue of phase p (read by phase p + 1)
+    return tL + kColA + 128u * (uint32_t)((p + 1) & 1) + 32u * (uint32_t)cq;
+  };
   uint32_t *mk = &S.mask[0][0][tid];  // + (layer * 2 + word) * kEpi
   const uint32_t one = S.one;
-  if (cq == 2) {  // the constant ones block of the bias steps: {1, 1, 0, ...} (never overwritten)
-    const uint32_t ones[8] = {pack_f16(1.f, 1.f), 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-    st8(tL + kColOnes, ones);
-  }
   auto hand_off = [&]() {
     wait_st();
     fence_before();
-    mbar_arrive(&S.epi_done);
+    mbar_arrive(&S.epi_done[half]);
   };
   auto prefetch = [&](int64_t TT, int par) {  // (unit quarter 0) point, slot and q row of tile TT
     int wn = 0;
@@ -245,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
       uint32_t a1[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) a1[i] = pack_f16(v[2 * i], v[2 * i + 1]);
-      st8(tL + kColX, a1);
+      st8(tL + kColA, a1);  // (A[0] columns 0..7: read by phase 0)
     } else if (cq == 1) {
       float v[16];
       const float j2 = qw[4];
@@ -259,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
       uint32_t a1[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) a1[i] = pack_f16(v[2 * i], v[2 * i + 1]);
-      st8(tL + kColX + 8u, a1);
+      st8(tL + kColA + 8u, a1);
     }
     hand_off();
     return lv;
@@ -283,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
     int pend_cnt = 0;
 #pragma unroll 1
     for (int p = 0; p < kPhases; ++p) {
-      mbar_wait(&S.mma_done, ph);
+      mbar_wait(&S.mma_done[half], ph);
       ph ^= 1u;
       fence_after();
       if (p < 5) {
@@ -302,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
             pk[(j >> 1) + 1] = pack_f16_relu(__uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3]));
             m |= mask_group_f(pk[j >> 1], pk[(j >> 1) + 1], ((c & 1) * 16 + j) >> 2, one);
           }
-          st8(tA + 8 * c, pk);
+          st8(tA(p) + 8 * c, pk);
           if (c & 1) {
             mk[(p * 2 + (c >> 1)) * kEpi] = m;
             m = 0u;
@@ -335,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
             fa[2] = fmaf(w7.z, z2 + fabsf(z2), fa[2]);
             fa[3] = fmaf(w7.w, z3 + fabsf(z3), fa[3]);
           }
-          st8(tA + cb / 2, pk);
+          st8(tA(p) + cb / 2, pk);
           if (c < 3) wait_ld();
         }
         hand_off();
@@ -368,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
             pk[j >> 1] = pack_f16(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1])) & lo;
             pk[(j >> 1) + 1] = pack_f16(__uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3])) & hi;
           }
-          st8(tA + 8 * c, pk);
+          st8(tA(p) + 8 * c, pk);
           if (c < 3) wait_ld();
         }
         hand_off();
