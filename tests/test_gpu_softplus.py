@@ -195,3 +195,41 @@ def test_softplus_tensor_c1_shape_and_partition():
     nd, nc = compare_active_sets(gp, orc, sub["f"], ids, BAND_FP32 + TC_VAL, val_atol=TC_VAL,
                                  what="C1 partitioned fp16 softplus")
     assert nc > 0
+
+
+def test_softplus_c5_full_size_sampled():
+    """The bench configuration of the variant (python bench.py --activation softplus: C5,
+    256 waypoints x 1M points, fp16 K2s, full-size detect): sampled pairs against the EMU and
+    exact oracles one by one, sampled active-set memberships, and the per-waypoint min."""
+    from paper_2601_18548_b200 import FP16
+    cfg = synth.get_config("C5")
+    pts, _ = synth.make_scene_points(cfg)
+    q = synth.make_waypoints(cfg)
+    tau = synth.load_tau("C5", 2)
+    ctx = _ctx(cfg, precision=FP16)
+    ids = ctx.update_scene(pts)
+    out = ctx.detect_active_set(torch.from_numpy(q), DELTA, tau)
+    torch.cuda.synchronize()
+    gpu = records_np(out)
+    m = oracle.MLP(synth.weights_path(cfg.H, act=2))
+    Q = q.reshape(-1, 9)
+    rng = np.random.default_rng(2025)
+    wsel = np.sort(rng.choice(Q.shape[0], 3, replace=False))
+    psel = np.sort(rng.choice(len(pts), 4096, replace=False))
+    ex = m.eval(pts[psel], Q[wsel], nthreads=NT)
+    em = m.eval(pts[psel], Q[wsel], flags=oracle.EMU_FP16, nthreads=NT)
+    v, g = ctx.query_values_grads(torch.from_numpy(Q[wsel].reshape(1, -1, 9)))
+    _tc_gates(v.cpu().numpy()[:, psel], g.cpu().numpy()[:, psel], ex, em, "C5 sampled fp16 softplus")
+    recset = set(zip(gpu["wp"].tolist(), gpu["pt"].tolist()))
+    thr = tau + DELTA
+    checked = 0
+    for wi, w in enumerate(wsel):
+        for pj, pid in enumerate(psel):
+            f = ex["f"][wi, pj]
+            if abs(f - thr) > BAND_FP32 + TC_VAL:
+                assert ((int(w), int(ids[pid])) in recset) == (f <= thr), (w, pid, f)
+                checked += 1
+    assert checked > 0.9 * len(wsel) * len(psel)
+    assert np.all(out["wp_min"].cpu().numpy()[wsel] <= ex["f"].min(axis=1) + TC_VAL)
+    frac = out["n"] / (len(pts) * Q.shape[0])
+    assert 0.001 < frac < 0.05, frac

@@ -57,13 +57,13 @@ def test_selftest_umma(mode, prec):
     assert err <= 1e-4 * max(1.0, ref.abs().max().item()), err
 
 
-def stats_and_gates(v, g, exact, emu, prec, what="", agree_min=0.85):
+def stats_and_gates(v, g, exact, emu, prec, what="", agree_min=0.85, kink_emu=KINK_EMU):
     dv = np.abs(v - emu["f"])
     de = np.abs(v - exact["f"])
     gn_g = np.linalg.norm(g, axis=-1)
     gd = np.abs(gn_g - np.linalg.norm(exact["g"], axis=-1))
     dg_emu = np.linalg.norm(g - emu["g"], axis=-1) / np.maximum(1.0, np.linalg.norm(emu["g"], axis=-1))
-    kink_free = (exact["mask_hash"] == emu["mask_hash"]) & (emu["kappa"] > KINK_EMU)
+    kink_free = (exact["mask_hash"] == emu["mask_hash"]) & (emu["kappa"] > kink_emu)
     st = {"emu_val_agree_1e-5": float(np.mean(dv <= 1e-5)), "emu_val_max": float(dv.max()),
           "emu_val_p50": float(np.median(dv)), "emu_val_p99": float(np.percentile(dv, 99)),
           "emu_grad_agree_1e-4": float(np.mean(dg_emu <= 1e-4)), "emu_grad_p99": float(np.percentile(dg_emu, 99)),

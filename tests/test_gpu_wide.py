@@ -25,7 +25,7 @@ H = 256
 
 def _ctx(M, n_wp, **kw):
     from paper_2601_18548_b200 import FP16, Context
-    ctx = Context(0, precision=FP16, scene_capacity=M + 4096, max_waypoints=n_wp, max_active=1 << 20, **kw)
+    ctx = Context(0, precision=FP16, scene_capacity=M + 4096, max_waypoints=n_wp, max_active=1 << 22, **kw)
     ctx.load_weights(synth.weights_path(H))
     return ctx
 
@@ -54,7 +54,8 @@ def test_wide_query_dense(c2w):
     # twice the units per layer of H = 128 -> twice the chances for a 16-bit rounding boundary or
     # a ReLU kink to flip between the GPU's fp32 accumulation order and the emulation's: the
     # fraction of pairs agreeing to 1e-5 is ~0.85^2 (measured 0.76) instead of H = 128's >= 0.85
-    stats_and_gates(vn[:, :M], gn[:, :M], exact, emu, "fp16", "H=256 C2/8 dense (80k pairs)", agree_min=0.7)
+    stats_and_gates(vn[:, :M], gn[:, :M], exact, emu, "fp16", "H=256 C2/8 dense (80k pairs)", agree_min=0.7,
+                    kink_emu=5e-3)
     assert np.all(np.isinf(vn[:, M:])) and np.all(gn[:, M:] == 0)
 
 
@@ -128,3 +129,46 @@ def test_wide_rejects_other_modes():
         with pytest.raises(GcdfError) as e:
             ctx.load_weights(synth.weights_path(H))
         assert e.value.name == "DIM_MISMATCH"
+
+
+def test_wide_c5_full_size_sampled():
+    """The bench configuration of the variant (python bench.py --hidden 256: C5, 256
+    waypoints x 1M points, fp16 K2w, full-size detect): sampled pairs against the oracle
+    one by one, sampled active-set memberships and the per-waypoint min property."""
+    cfg = synth.get_config("C5")
+    pts, _ = synth.make_scene_points(cfg)
+    q = synth.make_waypoints(cfg)
+    tau = synth.load_tau("C5", 1, H)
+    ctx = _ctx(cfg.M, cfg.B * cfg.N)
+    ids = ctx.update_scene(pts)
+    out = ctx.detect_active_set(torch.from_numpy(q), DELTA, tau)
+    torch.cuda.synchronize()
+    gpu = records_np(out)
+    m = oracle.MLP(synth.weights_path(H))
+    Q = q.reshape(-1, 9)
+    rng = np.random.default_rng(2026)
+    wsel = np.sort(rng.choice(Q.shape[0], 2, replace=False))
+    psel = np.sort(rng.choice(len(pts), 2048, replace=False))
+    ex = m.eval(pts[psel], Q[wsel], want_kappa=True, want_hash=True, nthreads=NT)
+    em = m.eval(pts[psel], Q[wsel], flags=oracle.EMU_FP16, want_kappa=True, want_hash=True, nthreads=NT)
+    v, g = ctx.query_values_grads(torch.from_numpy(Q[wsel].reshape(1, -1, 9)))
+    # kink proximity 5e-3 instead of 1e-3: with 256 units per layer a 16-bit rounding flip of one
+    # upstream activation moves a downstream pre-activation by up to a few 1e-3 (diagnosed with
+    # tools/probes/wide_c5_diag.py: the only kink-free pairs off by > 5e-2 had EMU kappa 1.7e-3 to
+    # 3e-3 and a GPU ReLU mask different from the emulation's; the GPU result is independent of
+    # the scene size / tiling)
+    stats_and_gates(v.cpu().numpy()[:, psel], g.cpu().numpy()[:, psel], ex, em, "fp16", "H=256 C5 sampled",
+                    agree_min=0.7, kink_emu=5e-3)
+    recset = set(zip(gpu["wp"].tolist(), gpu["pt"].tolist()))
+    thr = tau + DELTA
+    checked = 0
+    for wi, w in enumerate(wsel):
+        for pj, pid in enumerate(psel):
+            f = ex["f"][wi, pj]
+            if abs(f - thr) > 1e-3 + BF16_VAL_ATOL:
+                assert ((int(w), int(ids[pid])) in recset) == (f <= thr), (w, pid, f)
+                checked += 1
+    assert checked > 0.9 * len(wsel) * len(psel)
+    assert np.all(out["wp_min"].cpu().numpy()[wsel] <= ex["f"].min(axis=1) + BF16_VAL_ATOL)
+    frac = out["n"] / (len(pts) * Q.shape[0])
+    assert 0.001 < frac < 0.05, frac
