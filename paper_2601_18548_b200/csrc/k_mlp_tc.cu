@@ -85,7 +85,10 @@ constexpr int kWBytes = 5 * H * H * 2;    // 163,840
 constexpr int kW1tBytes = 16 * H * 2;     // 4,096
 constexpr int kB1Bytes = 32 * H * 2;      // 8,192
 constexpr int kBextBytes = 16 * H * 2;    // 4,096 per hidden layer
-constexpr uint32_t kColA = 128, kColOnes = 192;
+// per slot: D [0,128), A [128,192), ones [192,200), g0 [200,216), layer-1 operands x [216,232)
+// (g0 and x have columns of their own so that the last GEMM of a tile and the first of the
+// next one are issued as one phase, see issue_phase)
+constexpr uint32_t kColA = 128, kColOnes = 192, kColG0 = 200, kColX = 216;
 // or an fp32 add in the epilogue (1).
 // mbarrier waits: bit 0 = MMA thread spins with test_wait, bit 1 = epilogue warps spin
 template <bool F16> constexpr uint32_t kIdescFwd = idesc_f16kind(128, 128, false, F16);
@@ -164,17 +167,24 @@ DEVI uint32_t nz_halves(uint32_t pk, uint32_t one) { return prmt(add7fff(pk, one
 // stream to a few instructions per UMMA: a lane-0-only loop paid a register-to-uniform
 // move per operand and issued at ~75-90 cycles per UMMA, slower than the tensor pipe
 // (64 cycles per 128x128x16 UMMA, tools/mma_probe.py "lean issue").
+// Phase 11 (g0 of this tile, into columns kColG0..) also issues phase 0 of the slot's next
+// tile (layer 1, A = x staged at kColX by phase 10's epilogue) when next_l1: one commit,
+// one epilogue and one hand-off fewer per tile (11 phases per tile after the first).
 template <bool F16, bool kElect = true>
 DEVI void issue_phase(int p, uint32_t d, uint32_t sw, uint32_t sw1t, uint32_t sb1, uint32_t sbx, uint64_t *bar,
-                      volatile uint32_t *turn = nullptr, uint32_t next_turn = 0u) {
+                      volatile uint32_t *turn = nullptr, uint32_t next_turn = 0u, bool next_l1 = false) {
   auto mma_ts = [](uint32_t dt, uint32_t at, uint64_t bd, uint32_t id, uint32_t acc) {
     if constexpr (kElect) tc::mma_ts_elect(dt, at, bd, id, acc);
     else tc::mma_ts(dt, at, bd, id, acc);
   };
   const uint32_t av = d + kColA;
-  if (p == 0) {  // layer 1: K = 32 split operands (bias included)
+  auto layer1 = [&]() {  // layer 1: K = 32 split operands (bias included), A = x
 #pragma unroll
-    for (int k = 0; k < 2; ++k) mma_ts(d, av + 8u * k, sdesc_nosw(sb1 + k * 2 * 2048, 2048, 128), kIdescFwd<F16>, k > 0);
+    for (int k = 0; k < 2; ++k)
+      mma_ts(d, d + kColX + 8u * k, sdesc_nosw(sb1 + k * 2 * 2048, 2048, 128), kIdescFwd<F16>, k > 0);
+  };
+  if (p == 0) {
+    layer1();
   } else if (p < 6) {  // layer l = p + 1: D = A W_l^T (B = W_l K-major) + ones x bias
     const uint32_t wb = sw + (uint32_t)(p - 1) * (H * H * 2);
 #pragma unroll
@@ -185,10 +195,12 @@ DEVI void issue_phase(int p, uint32_t d, uint32_t sw, uint32_t sw1t, uint32_t sb
     const uint32_t wb = sw + (uint32_t)(10 - p) * (H * H * 2);
 #pragma unroll
     for (int k = 0; k < 8; ++k) mma_ts(d, av + 8u * k, sdesc_sw128(wb + k * 2048, 16384, 1024), kIdescBwd<F16>, k > 0);
-  } else {  // g0 = e1 W1 (N = 16 rows of W1^T)
+  } else {  // g0 = e1 W1 (N = 16 rows of W1^T) -> columns kColG0..; then the next tile's layer 1
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      mma_ts(d, av + 8u * k, sdesc_sw128(sw1t + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin<F16>, k > 0);
+      mma_ts(d + kColG0, av + 8u * k, sdesc_sw128(sw1t + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin<F16>,
+             k > 0);
+    if (next_l1) layer1();
   }
   if (turn) *turn = next_turn;  // (two MMA warps) the other slot may issue now
   if constexpr (kElect) commit_elect(bar);
@@ -268,8 +280,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     for (int64_t base = (int64_t)blockIdx.x * 2; base < n_tiles; base += stride, ++itt) {
       const bool two = base + 1 < n_tiles;
       if (ss == 1 && !two) break;
+      const bool next_l1 = base + stride + ss < n_tiles;  // this slot has a next tile
 #pragma unroll 1
-      for (int p = 0; p < kPhases; ++p, seq += 2) {
+      for (int p = itt == 0 ? 0 : 1; p < kPhases; ++p, seq += 2) {
         long long *t = (tr0 && itt < kTraceTiles) ? tr0 + ((size_t)itt * kTracePhases + p) * 4 + 2 * ss : nullptr;
         long long *t2 = t ? t + (size_t)(kTraceRoles - 1) * kTraceTiles * kTracePhases * 4 : nullptr;
         if (t2) t2[0] = clock64();
@@ -284,7 +297,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         if (t2) t2[1] = clock64();
         fence_after();
         if (t) t[0] = clock64();
-        issue_phase<F16>(p, tbase + (uint32_t)ss * 256u, sw, sw1t, sb1, sbx, &S.mma_done[ss], two ? turn : nullptr, seq + 1);
+        issue_phase<F16>(p, tbase + (uint32_t)ss * 256u, sw, sw1t, sb1, sbx, &S.mma_done[ss], two ? turn : nullptr, seq + 1,
+                         next_l1);
         if (t) t[1] = clock64();
       }
     }
@@ -305,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
       for (int64_t base = (int64_t)blockIdx.x * 2; base < n_tiles; base += stride, ++itt) {
         const int nslots = (base + 1 < n_tiles) ? 2 : 1;
 #pragma unroll 1
-        for (int p = 0; p < kPhases; ++p) {
+        for (int p = itt == 0 ? 0 : 1; p < kPhases; ++p) {
 #pragma unroll 1
           for (int ss = 0; ss < nslots; ++ss) {
             long long *t = (tr0 && itt < kTraceTiles) ? tr0 + ((size_t)itt * kTracePhases + p) * 4 + 2 * ss : nullptr;
@@ -316,7 +330,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
             phbits ^= 1u << ss;
             fence_after();
             if (t) t[0] = clock64();
-            issue_phase<F16>(p, tbase + (uint32_t)ss * 256u, sw, sw1t, sb1, sbx, &S.mma_done[ss]);
+            issue_phase<F16>(p, tbase + (uint32_t)ss * 256u, sw, sw1t, sb1, sbx, &S.mma_done[ss], nullptr, 0u,
+                             base + stride + ss < n_tiles);
             if (t) t[1] = clock64();
           }
         }
@@ -432,11 +447,41 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     uint32_t a1[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) a1[i] = pack2<F16>(v[2 * i], v[2 * i + 1]);
-    st8(tS + kColA + 8u * hh, a1);
-    hand_off(0, s == 1 || TT + 1 < n_tiles);
+    st8(tS + kColX + 8u * hh, a1);
     return lv;
   };
   const uint32_t one = S.one;
+  // forward epilogue of layer l = p + 1 (p = 0..4): z = D (bias folded in); h = ReLU(z) -> A,
+  // 1-bit masks -> smem, then hand off.  (16-column chunks, the TMEM load of chunk c + 1 in
+  // flight while chunk c is packed.)  Phase 0 of every tile after the first runs inside the
+  // previous tile's phase 11.
+  auto fwd_epi = [&](int p, long long *tr) {
+    uint32_t rb[2][16], m = 0u;
+    ld16(tD, rb[0]);
+    wait_ld();
+    if (tr) tr[(p + 1) * 4 + 0] = clock64();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (c < 3) ld16(tD + 16 * (c + 1), rb[(c + 1) & 1]);
+      const uint32_t *rr = rb[c & 1];
+      uint32_t pk[8];
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) {
+        pk[j >> 1] = pack2_relu<F16>(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1]));
+        pk[(j >> 1) + 1] = pack2_relu<F16>(__uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3]));
+        m |= mask_group_f(pk[j >> 1], pk[(j >> 1) + 1], ((c & 1) * 16 + j) >> 2, one);
+      }
+      st8(tA + 8 * c, pk);
+      if (c & 1) {
+        mk[(p * 2 + (c >> 1)) * kEpiPerSlot] = m;
+        m = 0u;
+      }
+      if (c < 3) wait_ld();
+    }
+    if (tr) tr[(p + 1) * 4 + 2] = clock64();
+    hand_off(p + 1, true);
+    if (tr) tr[(p + 1) * 4 + 3] = clock64();
+  };
   uint32_t ph = 0u;
   int it = 0;
   const bool tracer = a.trace && blockIdx.x == 0 && lane == 0;  // lane 0 of every epilogue warp of CTA 0
@@ -447,6 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
       cp_async_wait_all();
     }
     live_n = stage_a1((int64_t)blockIdx.x * 2 + s, 0);
+    hand_off(0, true);
   }
   for (int64_t T = (int64_t)blockIdx.x * 2 + s; T < n_tiles; T += stride, ++it) {
     long long *tr = (tracer && it < kTraceTiles) ? a.trace + (size_t)((1 + warp) * kTraceTiles + it) * kTracePhases * 4 : nullptr;
@@ -457,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     unsigned long long pend_b = 0ull;  // (row 0) staging allocation of this tile, in flight
     int pend_cnt = 0;
 #pragma unroll 1
-    for (int p = 0; p < kPhases; ++p) {
+    for (int p = it == 0 ? 0 : 1; p < kPhases; ++p) {
       mbar_wait_mode<GCDF_TC_EWAIT>(&S.mma_done[s], ph);
       if (tr) tr[(p + 1) * 4 + 1] = clock64();
       ph ^= 1u;
@@ -506,33 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
       }
 #endif
       if (p < 5) {
-        // ---- forward layer l = p + 1: z = D (bias folded in); h = ReLU(z) -> A ----
-        // (16-column chunks, the TMEM load of chunk c + 1 in flight while chunk c is packed)
-        uint32_t rb[2][16], m = 0u;
-        ld16(tD, rb[0]);
-        wait_ld();
-        if (tr) tr[(p + 1) * 4 + 0] = clock64();
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (c < 3) ld16(tD + 16 * (c + 1), rb[(c + 1) & 1]);
-          const uint32_t *rr = rb[c & 1];
-          uint32_t pk[8];
-#pragma unroll
-          for (int j = 0; j < 16; j += 4) {
-            pk[j >> 1] = pack2_relu<F16>(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1]));
-            pk[(j >> 1) + 1] = pack2_relu<F16>(__uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3]));
-            m |= mask_group_f(pk[j >> 1], pk[(j >> 1) + 1], ((c & 1) * 16 + j) >> 2, one);
-          }
-          st8(tA + 8 * c, pk);
-          if (c & 1) {
-            mk[(p * 2 + (c >> 1)) * kEpiPerSlot] = m;
-            m = 0u;
-          }
-          if (c < 3) wait_ld();
-        }
-        if (tr) tr[(p + 1) * 4 + 2] = clock64();
-        hand_off(p + 1, s == 1 || T + 1 < n_tiles);
-        if (tr) tr[(p + 1) * 4 + 3] = clock64();
+        fwd_epi(p, tr);
         if (p == 1 || p == 3) stage_q(p, T + stride, (it + 1) & 1);
       } else if (p == 5) {
         // ---- layer 6: e6 = w7 (.) 1[z6 > 0] -> A; f = w7 . ReLU(z6) + b7 (fp32) ----
@@ -579,6 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
             const int64_t slot = S.slotn[s][it & 1][row];
             if (slot < lb) a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
           }
+          prefetch_pt(T + stride, (it + 1) & 1);  // the next tile's point, needed at phase 10
         }
       } else if (p < 11) {
         // ---- backward: g_{l-1} = D; e_{l-1} = g (.) 1[z_{l-1} > 0] -> A ----
@@ -602,6 +623,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
           }
           st8(tA + 8 * c, pk);
           if (c < 3) wait_ld();
+        }
+        if (p == 10 && T + stride < n_tiles) {
+          // A2 + A1 of the slot's next tile -> x (kColX), issued with this tile's g0 GEMM
+          if (hh == 0) cp_async_wait_all();  // this thread's point of the next tile (phase 5)
+          live_n = stage_a1(T + stride, (it + 1) & 1);
         }
         if (tr) tr[(p + 1) * 4 + 2] = clock64();
         hand_off(p + 1, s == 1 || T + 1 < n_tiles);
@@ -657,19 +683,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
           S.sbase[s] = base;
           a.ds.tile_meta[T] = make_int2(base, pend_cnt);
         }
-        if (p == 7 && hh == 0) prefetch_pt(T + stride, (it + 1) & 1);  // lands during the next 4 phases
       } else {
-        // ---- g0 = W1^T e1 (16 columns); d f / d q by the chain rule (R3) ----
-        // D is read first; the next tile's layer-1 operands are handed off before the
-        // outputs of this tile are written (short tile-boundary critical path).
+        // ---- phase 11 + phase 0 of the slot's next tile: the UMMAs were issued together ----
+        // first the next tile's layer-1 epilogue (so its phase 1 can be issued), then g0 =
+        // W1^T e1 (16 columns at kColG0) -> d f / d q by the chain rule (R3) and the outputs
+        if (T + stride < n_tiles) fwd_epi(0, nullptr);
         uint32_t r[16];
         if (hh == 0) {
-          ld16(tS, r);
+          ld16(tS + kColG0, r);
           wait_ld();
-          cp_async_wait_all();  // this thread's prefetched point of the next tile
         }
         if (tr) tr[(p + 1) * 4 + 0] = clock64();
-        if (T + stride < n_tiles) live_n = stage_a1(T + stride, (it + 1) & 1);
         if (tr) tr[(p + 1) * 4 + 2] = clock64();
         if (hh == 0) {
           const int w = S.wtile[s][it & 1];
