@@ -775,15 +775,6 @@ static QueryArgs make_args(gcdf_ctx *c, const float *q, int32_t nwp) {
   return a;
 }
 
-// (dev switch) GCDF_K2T=1: the three-tile K2t kernel for the H = 128 ReLU translation-frame path
-static bool use_k2t() {
-  static const bool on = [] {
-    const char *e = std::getenv("GCDF_K2T");
-    return e && std::atoi(e) != 0;
-  }();
-  return on;
-}
-
 static cudaError_t run_mlp(gcdf_ctx *c, const QueryArgs &a, cudaStream_t s) {
   if ((int64_t)a.n_wp * a.tiles_per_wp == 0) return cudaSuccess;
   int slot = -1;
@@ -798,8 +789,6 @@ static cudaError_t run_mlp(gcdf_ctx *c, const QueryArgs &a, cudaStream_t s) {
                             ? launch_mlp_tc3(bf16_view(c), a, c->num_sms, s)
                         : c->H == kWideH ? launch_mlp_tc_wide(bf16_view(c), a, c->num_sms, s)
                         : a.act == 2 ? launch_mlp_tc_sp(bf16_view(c), a, c->num_sms, s)
-                        : (use_k2t() && !a.frame) ? launch_mlp_tc3t(c->opt.precision == GCDF_FP16, bf16_view(c), a,
-                                                                    c->num_sms, s)
                             : launch_mlp_tc(c->H, c->opt.precision == GCDF_FP16, bf16_view(c), a, c->num_sms, s);
   if (slot >= 0) cudaEventRecord(c->ev[2 * slot + 1], s);
   return e;

@@ -142,8 +142,6 @@ cudaError_t launch_pairgen(const float4 *pts, int64_t local_bound, const float *
 cudaError_t launch_detect_init(DetectScratch ds, int32_t n_wp, cudaStream_t s);
 cudaError_t launch_mlp_simt(int H, const WeightsF32 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
 cudaError_t launch_mlp_tc(int H, bool f16, const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
-// K2t: K2b with three tiles in flight sharing two TMEM accumulators (translation frame, ReLU)
-cudaError_t launch_mlp_tc3t(bool f16, const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
 // H = 256 variant of the tensor-core path (fp16, ReLU, translation frame; weights streamed; R27)
 cudaError_t launch_mlp_tc_wide(const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
 // softplus variant of the tensor-core path (fp16 operands, translation frame; R26)
