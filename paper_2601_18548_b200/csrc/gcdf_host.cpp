@@ -34,7 +34,7 @@ constexpr int kEvPool = 64;
 inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
 struct Layout {
-  int64_t pts, wf32, wbf16, wf16, wf16x3, wf16w, meta, staging, wp_key, wp_count, counter, upd_payload, upd_slots;
+  int64_t pts, wf32, wbf16, wf16, wf16x3, wf16w, meta, cbits, staging, wp_key, wp_count, counter, upd_payload, upd_slots;
   int64_t h_q, h_out, h_offs, h_wmin, h_warg, h_count;
   int64_t p_grid, p_bbox, p_cell_count, p_cell_start, p_cell_fill, p_cell_items, p_cell_xy, p_bitmap, p_chunk_cnt, p_chunk_off,
       p_scan_tmp, p_cand, p_cand_start, p_cand_count, p_tile_start, p_tile_wp, p_n_tiles, p_words, p_nchunk;
@@ -236,6 +236,7 @@ PartScratch part_view(const gcdf_ctx *c) {
 DetectScratch scratch_view(const gcdf_ctx *c) {
   DetectScratch d{};
   d.tile_meta = reinterpret_cast<int2 *>(c->ws + c->L.meta);
+  d.tile_bits = reinterpret_cast<uint4 *>(c->ws + c->L.cbits);
   d.staging = reinterpret_cast<gcdf_active_t *>(c->ws + c->L.staging);
   d.max_active = c->opt.max_active;
   d.counter = reinterpret_cast<unsigned long long *>(c->ws + c->L.counter);
@@ -379,6 +380,7 @@ int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out) {
   L.wf16x3 = off; off = align256(off + kX3Total);
   L.wf16w = off; off = align256(off + kWideTotal);
   L.meta = off; off = align256(off + (int64_t)o.max_waypoints * c->tiles_cap * 8);
+  L.cbits = off; off = align256(off + (int64_t)o.max_waypoints * c->tiles_cap * 16);
   L.staging = off; off = align256(off + o.max_active * (int64_t)sizeof(gcdf_active_t));
   L.wp_key = off; off = align256(off + (int64_t)o.max_waypoints * 8);
   L.wp_count = off; off = align256(off + finalize_scratch_elems(o.max_waypoints, c->tiles_cap) * 8);

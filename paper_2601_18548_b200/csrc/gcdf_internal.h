@@ -65,6 +65,8 @@ struct DetectScratch {
   int64_t max_active;
   unsigned long long *counter;     // [2]: staging allocation counter, overflow flag
   unsigned long long *wp_key;      // [max_waypoints] unsigned order key, ~0 = none
+  uint4 *tile_bits;                // [n_wp * tiles_per_wp] (standalone K3) active-slot bitmap of a
+                                   // tile: word k bit l = slot 4 l + k
 };
 
 // Range-partitioned tile map (NEXT-1): tile T of step w = tile_wp[T] covers candidates

@@ -40,7 +40,7 @@ __global__ void k_detect_init(unsigned long long *wp_key, unsigned long long *co
 // per-waypoint minimum key (one atomicMin per waypoint run in the group).  The chunk scan
 // of the finalize turns the counts into output offsets; pass 2 re-reads the values of the
 // tiles with records and writes the records straight to their final positions.
-constexpr int kGroup = 8;
+constexpr int kGroup = 4;
 
 // values of tile tw (0-based within step w) for this lane's 4 slots (+INF outside the scene)
 __device__ __forceinline__ float4 load_tile_values(const float *__restrict__ values, int64_t stride, int64_t lb,
@@ -59,9 +59,9 @@ __device__ __forceinline__ float4 load_tile_values(const float *__restrict__ val
   return v;
 }
 
-__global__ void __launch_bounds__(256) k_compact_count(const float *__restrict__ values, int64_t stride, int32_t n_wp,
-                                                       int32_t tpw, SceneView scene, float delta, float tau,
-                                                       DetectScratch ds) {
+__global__ void __launch_bounds__(256, 4) k_compact_count(const float *__restrict__ values, int64_t stride,
+                                                          int32_t n_wp, int32_t tpw, SceneView scene, float delta,
+                                                          float tau, DetectScratch ds) {
   const int lane = threadIdx.x & 31;
   const int64_t n_tiles = (int64_t)n_wp * tpw;
   const int64_t n_groups = (n_tiles + kGroup - 1) / kGroup;
@@ -73,11 +73,15 @@ __global__ void __launch_bounds__(256) k_compact_count(const float *__restrict__
   const int64_t G0 = gw * per, G1 = min(G0 + per, n_groups);
   if (G0 >= G1) return;
   const int64_t lb = scene.local_bound;
-  int wq = (int)(G0 * kGroup / tpw);
-  int64_t tq = G0 * kGroup - (int64_t)wq * tpw;
-  int wcur = wq;
+  int wcur = (int)(G0 * kGroup / tpw);
   unsigned long long key = ~0ull;
+  float lmin = __int_as_float(0x7f800000);  // this lane's minimum of the current step and its slot
+  int64_t lslot = 0;
   auto flush_key = [&]() {
+    if (lmin != __int_as_float(0x7f800000))
+      key = ((unsigned long long)ord_f32(lmin) << 32) |
+            (unsigned long long)local_to_global(lslot, scene.rank, scene.world);
+    lmin = __int_as_float(0x7f800000);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
@@ -86,51 +90,67 @@ __global__ void __launch_bounds__(256) k_compact_count(const float *__restrict__
     if (lane == 0 && key != ~0ull) atomicMin(ds.wp_key + wcur, key);
     key = ~0ull;
   };
-  for (int64_t G = G0; G < G1; ++G) {
-    const int64_t T0 = G * kGroup;
-    float4 vv[kGroup];
-    int ws[kGroup];
-    int64_t s0[kGroup];
-#pragma unroll
-    for (int t = 0; t < kGroup; ++t) {  // all loads in flight first
-      ws[t] = wq;
-      if (T0 + t < n_tiles) vv[t] = load_tile_values(values, stride, lb, wq, tq, lane, s0[t]);
-      if (++tq == tpw) {
-        tq = 0;
-        ++wq;
-      }
-    }
+  // software-pipelined: the loads of group G + 1 are in flight while group G is processed;
+  // tile positions (step, tile in step) advance incrementally (no 64-bit divisions per tile)
+  int lw = wcur, pw = wcur;                    // step of the next tile to load / to process
+  int lt = (int)(G0 * kGroup - (int64_t)lw * tpw), pt = lt;
+  auto load_group = [&](int64_t G, float4 (&vv)[kGroup]) {
 #pragma unroll
     for (int t = 0; t < kGroup; ++t) {
-      if (T0 + t >= n_tiles) break;
-      if (ws[t] != wcur) {
+      if (G < G1 && G * kGroup + t < n_tiles) {
+        int64_t s0;
+        vv[t] = load_tile_values(values, stride, lb, lw, lt, lane, s0);
+      }
+      if (++lt == tpw) {
+        lt = 0;
+        ++lw;
+      }
+    }
+  };
+  auto process = [&](int64_t G, const float4 (&vv)[kGroup]) {
+    const int64_t T0 = G * kGroup;
+#pragma unroll
+    for (int t = 0; t < kGroup; ++t) {
+      const int64_t T = T0 + t;
+      if (T >= n_tiles) break;
+      const int w = pw;
+      const int64_t s0 = (int64_t)pt * kTile + 4 * lane;
+      if (++pt == tpw) {
+        pt = 0;
+        ++pw;
+      }
+      if (w != wcur) {
         flush_key();
-        wcur = ws[t];
+        wcur = w;
       }
       const float v[4] = {vv[t].x, vv[t].y, vv[t].z, vv[t].w};
-      // count: f - delta <= tau (dead slots are +INF and never pass); minimum: the lane's
-      // smallest value, first (smallest id) on ties, folded into one 64-bit key per tile
-      const float thr = tau + delta;
-      int cnt = 0;
-      float mv = v[0];
-      int mk = 0;
+      // active: f - delta <= tau (dead slots are +INF and never pass); the tile's bitmap (word
+      // k = ballot of slot 4 lane + k) lets pass 2 skip re-reading the values; minimum: the
+      // lane's smallest value and its slot (first = smallest slot on ties: slots ascend), folded
+      // into the 64-bit key only when the step changes
+      uint32_t b[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        cnt += (v[k] - delta <= tau) ? 1 : 0;
-        if (k > 0 && v[k] < mv) {
-          mv = v[k];
-          mk = k;
+        b[k] = __ballot_sync(0xffffffffu, v[k] - delta <= tau);
+        if (v[k] < lmin) {
+          lmin = v[k];
+          lslot = s0 + k;
         }
       }
-      (void)thr;
-      if (mv != __int_as_float(0x7f800000)) {
-        const unsigned long long kk = ((unsigned long long)ord_f32(mv) << 32) |
-                                      (unsigned long long)local_to_global(s0[t] + mk, scene.rank, scene.world);
-        key = kk < key ? kk : key;
+      if (lane == 0) {
+        ds.tile_meta[T] = make_int2(0, __popc(b[0]) + __popc(b[1]) + __popc(b[2]) + __popc(b[3]));
+        ds.tile_bits[T] = make_uint4(b[0], b[1], b[2], b[3]);
       }
-      cnt = __reduce_add_sync(0xffffffffu, cnt);
-      if (lane == 0) ds.tile_meta[T0 + t] = make_int2(0, cnt);
     }
+  };
+  // two register sets in ping-pong (no register copies, which would wait for the loads)
+  float4 va[kGroup], vb[kGroup];
+  load_group(G0, va);
+  for (int64_t G = G0; G < G1; G += 2) {
+    load_group(G + 1, vb);
+    process(G, va);
+    load_group(G + 2, va);
+    if (G + 1 < G1) process(G + 1, vb);
   }
   flush_key();
 }
@@ -228,13 +248,16 @@ __global__ void __launch_bounds__(256) k_fin_scatter(const int2 *__restrict__ me
 }
 
 // pass 2 of the standalone K3: chunk (w, c) of kFinChunk tiles; the tile offsets come from a
-// block scan of the pass-1 counts, then a warp per tile re-reads its values and writes the
-// records at out[cpre + tile offset + rank] (gradients gathered from the dense array).
+// block scan of the pass-1 counts, then a warp per tile reads the tile's 16-B active bitmap
+// (pass 1) -- not its values -- ranks the actives with popcounts of the bitmap words, and the
+// lanes with actives read their values and gradients and write the records at
+// out[cpre + tile offset + rank].
 __global__ void __launch_bounds__(256, 3) k_compact_write(const float *__restrict__ values,
                                                        const float *__restrict__ grads, int64_t stride, int32_t tpw,
                                                        int64_t nch, const int64_t *__restrict__ cpre,
-                                                       const int2 *__restrict__ meta, SceneView scene, float delta,
-                                                       float tau, gcdf_active_t *__restrict__ out, int64_t cap) {
+                                                       const int2 *__restrict__ meta,
+                                                       const uint4 *__restrict__ tbits, SceneView scene,
+                                                       gcdf_active_t *__restrict__ out, int64_t cap) {
   __shared__ int64_t sh[32];
   __shared__ int32_t tpos[kFinChunk];
   const int w = blockIdx.y;
@@ -259,36 +282,27 @@ __global__ void __launch_bounds__(256, 3) k_compact_write(const float *__restric
   __syncthreads();
   const int64_t dst0 = cpre[(int64_t)w * nch + c];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t lb = scene.local_bound;
+  const uint32_t lt = (1u << lane) - 1u;
   const int64_t tend = min((int64_t)kFinChunk, nt - c * kFinChunk);
-  // a warp takes 4 consecutive tiles per step: all their loads in flight, then the writes
-  for (int64_t tb = (int64_t)warp * 4; tb < tend; tb += 32) {
-    float4 vb[4];
-    int64_t sb[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (tb + i < tend && tpos[tb + i] >= 0) vb[i] = load_tile_values(values, stride, lb, w, c * kFinChunk + tb + i, lane, sb[i]);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-    const int64_t tl = tb + i;
-    if (tl >= tend) break;
+  const float *vrow = values + (int64_t)w * stride;
+  for (int64_t tl = warp; tl < tend; tl += 8) {
     const int32_t pos = tpos[tl];
     if (pos < 0) continue;  // no records in this tile (uniform over the warp)
-    const int64_t slot0 = sb[i];
-    const float v[4] = {vb[i].x, vb[i].y, vb[i].z, vb[i].w};
+    const int64_t tw = c * kFinChunk + tl;
+    const uint4 bw = __ldg(tbits + t0 + tw);
+    const uint32_t wd[4] = {bw.x, bw.y, bw.z, bw.w};
     unsigned bits = 0u;
+    int64_t r = dst0 + pos;
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (v[k] != __int_as_float(0x7f800000) && v[k] - delta <= tau) bits |= 1u << k;
-    const int n = __popc(bits);
-    int incl = n;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
+    for (int k = 0; k < 4; ++k) {
+      bits |= ((wd[k] >> lane) & 1u) << k;
+      r += __popc(wd[k] & lt);  // actives of the lower lanes (all their slots precede this lane's)
     }
-    int64_t r = dst0 + pos + incl - n;
-    while (bits) {  // (a lane has at most 4 active slots; usually 0 or 1)
+    if (!bits) continue;
+    const int64_t slot0 = tw * kTile + 4 * lane;
+    const float4 v4 = __ldg(reinterpret_cast<const float4 *>(vrow + slot0));
+    const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+    while (bits) {  // (a lane has at most 4 active slots; usually 1)
       const int k = __ffs(bits) - 1;
       bits &= bits - 1;
       if (r < cap) {
@@ -304,7 +318,6 @@ __global__ void __launch_bounds__(256, 3) k_compact_write(const float *__restric
                              __uint_as_float((unsigned)local_to_global(slot, scene.rank, scene.world)));
       }
       ++r;
-    }
     }
   }
 }
@@ -412,8 +425,12 @@ cudaError_t launch_compact_dense(const float *values, const float *grads, int64_
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // one wave: the warps' contiguous tile ranges are sized for the CTAs that are resident at once
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_compact_count, 256, 0) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
   const int64_t need = (n_tiles + 8 * kGroup - 1) / (8 * kGroup);  // 8 warps per CTA, kGroup tiles each
-  const int64_t grid = need < (int64_t)sms * 4 ? need : (int64_t)sms * 4;
+  const int64_t grid = need < (int64_t)sms * per_sm ? need : (int64_t)sms * per_sm;
   k_compact_count<<<(unsigned)grid, 256, 0, s>>>(values, stride, n_wp, tiles_per_wp, scene, delta, tau, ds);
   const int64_t nch = finalize_chunks(tiles_per_wp);
   const int64_t n = (int64_t)n_wp * nch;
@@ -424,7 +441,7 @@ cudaError_t launch_compact_dense(const float *values, const float *grads, int64_
   if (e != cudaSuccess) return e;
   k_fin_offsets<<<(n_wp + 256) / 256, 256, 0, s>>>(cpre, nch, n_wp, wp_offsets, count, ds.wp_key, wp_min, wp_argmin,
                                                    wp_key);
-  k_compact_write<<<g2, 256, 0, s>>>(values, grads, stride, tiles_per_wp, nch, cpre, ds.tile_meta, scene, delta, tau,
+  k_compact_write<<<g2, 256, 0, s>>>(values, grads, stride, tiles_per_wp, nch, cpre, ds.tile_meta, ds.tile_bits, scene,
                                      out, out_capacity);
   *n_launches += 4;
   return cudaGetLastError();

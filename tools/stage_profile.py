@@ -16,6 +16,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("stage")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--config", default="C5")
+ap.add_argument("--time", action="store_true", help="CUDA-event timing instead of a profiler target")
 a = ap.parse_args()
 cfg = synth.get_config(a.config)
 pts, _ = synth.make_scene_points(cfg)
@@ -28,6 +29,30 @@ ctx.update_scene(pts)
 outs = ctx.alloc_detect_outputs(cfg.B * cfg.N, 1 << 23)
 if a.stage == "compact":
     v, g = ctx.query_values_grads(q)
+def one():
+    if a.stage == "partitioned":
+        ctx.detect_active_set_partitioned(q, 1.8, 0.1, tau, outputs=outs)
+    elif a.stage == "compact":
+        ctx.compact_dense(v, g, 0.1, tau, outputs=outs)
+    elif a.stage == "pairgen":
+        ctx.pairgen_transform(q)
+
+
+if a.time:  # CUDA-event time per call (after 3 warm-ups), L2 flushed before each call
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        one()
+    ts = []
+    for _ in range(a.reps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        one()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    print(a.stage, "ms per call: median %.4f min %.4f" % (sorted(ts)[len(ts) // 2], min(ts)))
+    sys.exit(0)
 for _ in range(a.reps):
     if a.stage == "partitioned":
         ctx.detect_active_set_partitioned(q, 1.8, 0.1, tau, outputs=outs)
