@@ -62,17 +62,20 @@ __device__ __forceinline__ float4 load_tile_values(const float *__restrict__ val
 __global__ void __launch_bounds__(256, 4) k_compact_count(const float *__restrict__ values, int64_t stride,
                                                           int32_t n_wp, int32_t tpw, SceneView scene, float delta,
                                                           float tau, DetectScratch ds) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwb = blockDim.x >> 5;  // warps per CTA
   const int64_t n_tiles = (int64_t)n_wp * tpw;
   const int64_t n_groups = (n_tiles + kGroup - 1) / kGroup;
-  // each warp takes a contiguous range of groups, so it stays on one step for long runs and
-  // folds the step's minimum key locally (atomicMin only when the step changes)
-  const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int64_t per = (n_groups + n_warps - 1) / n_warps;
-  const int64_t G0 = gw * per, G1 = min(G0 + per, n_groups);
-  if (G0 >= G1) return;
+  // each CTA takes a contiguous range of groups and its warps interleave over it (warp j takes
+  // groups j, j + 8, ...): the CTA streams contiguous memory (DRAM row locality, as a grid-
+  // stride reduction does), while each warp stays on one step for long runs and folds the
+  // step's minimum locally (atomicMin only when the step changes)
+  const int64_t per = (n_groups + gridDim.x - 1) / gridDim.x;
+  const int64_t C0 = (int64_t)blockIdx.x * per, C1 = min(C0 + per, n_groups);
+  const int64_t G0 = C0 + warp;
+  if (G0 >= C1) return;
   const int64_t lb = scene.local_bound;
+  const int step_tiles = kGroup * nwb;  // tile advance between a warp's consecutive groups
   int wcur = (int)(G0 * kGroup / tpw);
   unsigned long long key = ~0ull;
   float lmin = __int_as_float(0x7f800000);  // this lane's minimum of the current step and its slot
@@ -90,44 +93,49 @@ __global__ void __launch_bounds__(256, 4) k_compact_count(const float *__restric
     if (lane == 0 && key != ~0ull) atomicMin(ds.wp_key + wcur, key);
     key = ~0ull;
   };
-  // software-pipelined: the loads of group G + 1 are in flight while group G is processed;
-  // tile positions (step, tile in step) advance incrementally (no 64-bit divisions per tile)
-  int lw = wcur, pw = wcur;                    // step of the next tile to load / to process
+  // (step, tile in step) of the first tile of the next group to load / to process; advanced
+  // incrementally (no 64-bit divisions per tile)
+  int lw = wcur, pw = wcur;
   int lt = (int)(G0 * kGroup - (int64_t)lw * tpw), pt = lt;
+  auto advance = [&](int &w, int &t, int by) {
+    t += by;
+    while (t >= tpw) {
+      t -= tpw;
+      ++w;
+    }
+  };
   auto load_group = [&](int64_t G, float4 (&vv)[kGroup]) {
+    if (G < C1) {
+      int w = lw, t = lt;
 #pragma unroll
-    for (int t = 0; t < kGroup; ++t) {
-      if (G < G1 && G * kGroup + t < n_tiles) {
-        int64_t s0;
-        vv[t] = load_tile_values(values, stride, lb, lw, lt, lane, s0);
-      }
-      if (++lt == tpw) {
-        lt = 0;
-        ++lw;
+      for (int i = 0; i < kGroup; ++i) {
+        if (G * kGroup + i < n_tiles) {
+          int64_t s0;
+          vv[i] = load_tile_values(values, stride, lb, w, t, lane, s0);
+        }
+        advance(w, t, 1);
       }
     }
+    advance(lw, lt, step_tiles);
   };
   auto process = [&](int64_t G, const float4 (&vv)[kGroup]) {
     const int64_t T0 = G * kGroup;
+    int w = pw, tt = pt;
+    advance(pw, pt, step_tiles);
 #pragma unroll
-    for (int t = 0; t < kGroup; ++t) {
-      const int64_t T = T0 + t;
+    for (int i = 0; i < kGroup; ++i) {
+      const int64_t T = T0 + i;
       if (T >= n_tiles) break;
-      const int w = pw;
-      const int64_t s0 = (int64_t)pt * kTile + 4 * lane;
-      if (++pt == tpw) {
-        pt = 0;
-        ++pw;
-      }
       if (w != wcur) {
         flush_key();
         wcur = w;
       }
-      const float v[4] = {vv[t].x, vv[t].y, vv[t].z, vv[t].w};
+      const int64_t s0 = (int64_t)tt * kTile + 4 * lane;
+      advance(w, tt, 1);
+      const float v[4] = {vv[i].x, vv[i].y, vv[i].z, vv[i].w};
       // active: f - delta <= tau (dead slots are +INF and never pass); the tile's bitmap (word
       // k = ballot of slot 4 lane + k) lets pass 2 skip re-reading the values; minimum: the
-      // lane's smallest value and its slot (first = smallest slot on ties: slots ascend), folded
-      // into the 64-bit key only when the step changes
+      // lane's smallest value and its slot (first = smallest slot on ties: slots ascend)
       uint32_t b[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -146,11 +154,11 @@ __global__ void __launch_bounds__(256, 4) k_compact_count(const float *__restric
   // two register sets in ping-pong (no register copies, which would wait for the loads)
   float4 va[kGroup], vb[kGroup];
   load_group(G0, va);
-  for (int64_t G = G0; G < G1; G += 2) {
-    load_group(G + 1, vb);
+  for (int64_t G = G0; G < C1; G += 2 * nwb) {
+    load_group(G + nwb, vb);
     process(G, va);
-    load_group(G + 2, va);
-    if (G + 1 < G1) process(G + 1, vb);
+    load_group(G + 2 * nwb, va);
+    if (G + nwb < C1) process(G + nwb, vb);
   }
   flush_key();
 }
