@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(256, 4) k_compact_count(const float *__restric
   int wcur = (int)(G0 * kGroup / tpw);
   unsigned long long key = ~0ull;
   float lmin = __int_as_float(0x7f800000);  // this lane's minimum of the current step and its slot
-  int64_t lslot = 0;
+  uint32_t lslot = 0u;
   auto flush_key = [&]() {
     if (lmin != __int_as_float(0x7f800000))
       key = ((unsigned long long)ord_f32(lmin) << 32) |
@@ -120,35 +120,36 @@ __global__ void __launch_bounds__(256, 4) k_compact_count(const float *__restric
   };
   auto process = [&](int64_t G, const float4 (&vv)[kGroup]) {
     const int64_t T0 = G * kGroup;
+    const int nt = (int)min((int64_t)kGroup, n_tiles - T0);  // tiles of this group in range
     int w = pw, tt = pt;
     advance(pw, pt, step_tiles);
 #pragma unroll
     for (int i = 0; i < kGroup; ++i) {
-      const int64_t T = T0 + i;
-      if (T >= n_tiles) break;
+      if (i >= nt) break;
       if (w != wcur) {
         flush_key();
         wcur = w;
       }
-      const int64_t s0 = (int64_t)tt * kTile + 4 * lane;
-      advance(w, tt, 1);
-      const float v[4] = {vv[i].x, vv[i].y, vv[i].z, vv[i].w};
+      const float4 x = vv[i];
+      // minimum: the lane's smallest value and its slot, first (smallest slot) on ties -- a
+      // min of the four values, and the slot search only when it improves (rare)
+      const float m4 = fminf(fminf(x.x, x.y), fminf(x.z, x.w));
+      if (m4 < lmin) {
+        lmin = m4;
+        lslot = (uint32_t)tt * kTile + 4u * lane + (x.x == m4 ? 0u : x.y == m4 ? 1u : x.z == m4 ? 2u : 3u);
+      }
       // active: f - delta <= tau (dead slots are +INF and never pass); the tile's bitmap (word
-      // k = ballot of slot 4 lane + k) lets pass 2 skip re-reading the values; minimum: the
-      // lane's smallest value and its slot (first = smallest slot on ties: slots ascend)
-      uint32_t b[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        b[k] = __ballot_sync(0xffffffffu, v[k] - delta <= tau);
-        if (v[k] < lmin) {
-          lmin = v[k];
-          lslot = s0 + k;
-        }
-      }
+      // k = ballot of slot 4 lane + k) lets pass 2 skip re-reading the values
+      const uint32_t b0 = __ballot_sync(0xffffffffu, x.x - delta <= tau);
+      const uint32_t b1 = __ballot_sync(0xffffffffu, x.y - delta <= tau);
+      const uint32_t b2 = __ballot_sync(0xffffffffu, x.z - delta <= tau);
+      const uint32_t b3 = __ballot_sync(0xffffffffu, x.w - delta <= tau);
       if (lane == 0) {
-        ds.tile_meta[T] = make_int2(0, __popc(b[0]) + __popc(b[1]) + __popc(b[2]) + __popc(b[3]));
-        ds.tile_bits[T] = make_uint4(b[0], b[1], b[2], b[3]);
+        const int64_t T = T0 + i;
+        ds.tile_meta[T] = make_int2(0, __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3));
+        ds.tile_bits[T] = make_uint4(b0, b1, b2, b3);
       }
+      advance(w, tt, 1);
     }
   };
   // two register sets in ping-pong (no register copies, which would wait for the loads)
@@ -169,6 +170,7 @@ __global__ void __launch_bounds__(256, 4) k_compact_count(const float *__restric
 // on n_wp * nch CTAs instead of n_wp.
 constexpr int kFinPer = 8;
 constexpr int kFinChunk = 256 * kFinPer;
+constexpr int kWB = 2;  // tiles per warp step of the standalone K3 write pass
 
 __device__ __forceinline__ void tile_range(const int64_t *tile_start, int32_t tpw, int w, int64_t &t0, int64_t &nt) {
   t0 = tile_start ? tile_start[w] : (int64_t)w * tpw;
@@ -293,39 +295,69 @@ __global__ void __launch_bounds__(256, 3) k_compact_write(const float *__restric
   const uint32_t lt = (1u << lane) - 1u;
   const int64_t tend = min((int64_t)kFinChunk, nt - c * kFinChunk);
   const float *vrow = values + (int64_t)w * stride;
-  for (int64_t tl = warp; tl < tend; tl += 8) {
-    const int32_t pos = tpos[tl];
-    if (pos < 0) continue;  // no records in this tile (uniform over the warp)
-    const int64_t tw = c * kFinChunk + tl;
-    const uint4 bw = __ldg(tbits + t0 + tw);
-    const uint32_t wd[4] = {bw.x, bw.y, bw.z, bw.w};
-    unsigned bits = 0u;
-    int64_t r = dst0 + pos;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      bits |= ((wd[k] >> lane) & 1u) << k;
-      r += __popc(wd[k] & lt);  // actives of the lower lanes (all their slots precede this lane's)
+  // kWB tiles per step: their bitmaps, then their value and gradient loads are in flight
+  // before the records are written (a lane has usually 0 or 1 active slot per tile;
+  // further ones take the loop at the end)
+  auto write_rec = [&](int64_t r, int64_t slot, float v, const float *gg) {
+    if (r < cap) {
+      float4 *dst = reinterpret_cast<float4 *>(out + r);
+      dst[0] = make_float4(v, gg[0], gg[1], gg[2]);
+      dst[1] = make_float4(gg[3], gg[4], gg[5], gg[6]);
+      dst[2] = make_float4(gg[7], gg[8], __uint_as_float((unsigned)w),
+                           __uint_as_float((unsigned)local_to_global(slot, scene.rank, scene.world)));
     }
-    if (!bits) continue;
-    const int64_t slot0 = tw * kTile + 4 * lane;
-    const float4 v4 = __ldg(reinterpret_cast<const float4 *>(vrow + slot0));
-    const float v[4] = {v4.x, v4.y, v4.z, v4.w};
-    while (bits) {  // (a lane has at most 4 active slots; usually 1)
-      const int k = __ffs(bits) - 1;
-      bits &= bits - 1;
-      if (r < cap) {
-        const int64_t slot = slot0 + k;
-        const float *g = grads + ((int64_t)w * stride + slot) * kNdof;
-        float gg[kNdof];
+  };
+  for (int64_t tl0 = warp; tl0 < tend; tl0 += 8 * kWB) {
+    unsigned bits[kWB];
+    int64_t r[kWB];
 #pragma unroll
-        for (int i = 0; i < kNdof; ++i) gg[i] = __ldcs(g + i);
-        float4 *dst = reinterpret_cast<float4 *>(out + r);
-        dst[0] = make_float4(v[k], gg[0], gg[1], gg[2]);
-        dst[1] = make_float4(gg[3], gg[4], gg[5], gg[6]);
-        dst[2] = make_float4(gg[7], gg[8], __uint_as_float((unsigned)w),
-                             __uint_as_float((unsigned)local_to_global(slot, scene.rank, scene.world)));
+    for (int j = 0; j < kWB; ++j) {
+      bits[j] = 0u;
+      r[j] = 0;
+      const int64_t tl = tl0 + 8 * j;
+      const int32_t pos = tl < tend ? tpos[tl] : -1;
+      if (pos < 0) continue;  // no records in this tile (uniform over the warp)
+      const uint4 bw = __ldg(tbits + t0 + c * kFinChunk + tl);
+      const uint32_t wd[4] = {bw.x, bw.y, bw.z, bw.w};
+      r[j] = dst0 + pos;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        bits[j] |= ((wd[k] >> lane) & 1u) << k;
+        r[j] += __popc(wd[k] & lt);  // actives of the lower lanes (all their slots precede this lane's)
       }
-      ++r;
+    }
+    float4 v4[kWB];
+    float gg[kWB][kNdof];
+    int kf[kWB];
+#pragma unroll
+    for (int j = 0; j < kWB; ++j) {  // the first active slot of each tile: value + gradient loads
+      kf[j] = __ffs(bits[j]) - 1;
+      if (bits[j]) {
+        const int64_t slot0 = (c * kFinChunk + tl0 + 8 * j) * kTile + 4 * lane;
+        v4[j] = __ldg(reinterpret_cast<const float4 *>(vrow + slot0));
+        const float *g = grads + ((int64_t)w * stride + slot0 + kf[j]) * kNdof;
+#pragma unroll
+        for (int i = 0; i < kNdof; ++i) gg[j][i] = __ldcs(g + i);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kWB; ++j) {
+      if (!bits[j]) continue;
+      const int64_t slot0 = (c * kFinChunk + tl0 + 8 * j) * kTile + 4 * lane;
+      const float v[4] = {v4[j].x, v4[j].y, v4[j].z, v4[j].w};
+      write_rec(r[j], slot0 + kf[j], v[kf[j]], gg[j]);
+      unsigned rest = bits[j] & (bits[j] - 1u);
+      int64_t rr = r[j] + 1;
+      while (rest) {  // rare: more than one active slot in this lane's four
+        const int k = __ffs(rest) - 1;
+        rest &= rest - 1u;
+        const float *g = grads + ((int64_t)w * stride + slot0 + k) * kNdof;
+        float g2[kNdof];
+#pragma unroll
+        for (int i = 0; i < kNdof; ++i) g2[i] = __ldcs(g + i);
+        write_rec(rr, slot0 + k, v[k], g2);
+        ++rr;
+      }
     }
   }
 }
