@@ -497,9 +497,11 @@ int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
   bool ok = dims[0] == (uint32_t)kNin && dims[7] == 1 && (H == 32 || H == 128 || H == kWideH);
   for (int l = 1; l <= 6; ++l) ok = ok && dims[l] == (uint32_t)H;
   if (!ok) return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: dims must be [12, H x 6, 1], H in {32, 128, 256}", path);
-  if (H == kWideH && (c->opt.precision != GCDF_FP16 || act != 1 || c->opt.frame != GCDF_FRAME_TRANSLATE))
+  if (H == kWideH && c->opt.precision != GCDF_FP32 &&
+      (c->opt.precision != GCDF_FP16 || act != 1 || c->opt.frame != GCDF_FRAME_TRANSLATE))
     return fail(c, GCDF_ERR_DIM_MISMATCH,
-                "%s: H = 256 (NEXT-4) runs on GCDF_FP16 with ReLU in the translation frame (K2w)", path);
+                "%s: H = 256 (NEXT-4) runs on GCDF_FP32, or on GCDF_FP16 with ReLU in the translation frame (K2w)",
+                path);
   if (act != 1 && act != 2)
     return fail(c, GCDF_ERR_DIM_MISMATCH, "%s: activation %u (ReLU = 1, R9, or softplus = 2, R26)", path, act);
   if (act == 2 && c->opt.precision != GCDF_FP32 &&

@@ -73,9 +73,14 @@ __device__ __forceinline__ void store_tile(float *__restrict__ Y, int tp, int tu
   }
 }
 
+// H = 256: one activation buffer updated in place (two would exceed shared memory) plus a
+// separate [128][9] gradient staging area; H <= 128: two buffers in ping-pong
+template <int H>
+constexpr bool in_place() { return H > 128; }
 template <int H>
 constexpr int smem_bytes_simt() {
-  return (2 * H * LD + 4 * kTile + H + 16 + kTile + 2 * 4 + 4 + 4) * 4 + 16;
+  return ((in_place<H>() ? 1 : 2) * H * LD + (in_place<H>() ? kTile * kNdof : 0) + 4 * kTile + H + 16 + kTile + 2 * 4 +
+          4 + 4) * 4 + 16;
 }
 
 // Hidden activation (ACT = MLPW activation id): 1 = ReLU (R9; masks in registers),
@@ -94,9 +99,11 @@ __global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const Q
   static_assert(ACT == 1 || ACT == 2, "activation");
   constexpr int MW = (8 * UPT + 31) / 32;
   extern __shared__ __align__(16) float smem[];
+  constexpr bool kInPlace = in_place<H>();
   float *buf0 = smem;
-  float *buf1 = smem + H * LD;
-  float4 *sp = reinterpret_cast<float4 *>(smem + 2 * H * LD);  // [128] transformed points
+  float *buf1 = kInPlace ? smem : smem + H * LD;
+  float *gstb = smem + (kInPlace ? H * LD : 0);                   // (in place) [128][9] staging
+  float4 *sp = reinterpret_cast<float4 *>(smem + (kInPlace ? H * LD + kTile * kNdof : 2 * H * LD));  // [128] points
   float *c1 = reinterpret_cast<float *>(sp + kTile);            // [H] layer-1 per-waypoint constant
   float *qv = c1 + H;                                            // [16]
   float *fval = qv + 16;                                         // [128]
@@ -207,6 +214,7 @@ __global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const Q
           }
         }
       if (li < 4) {
+        if constexpr (kInPlace) __syncthreads();  // every thread has read cur
         store_tile<H>(nxt, tp, tu, acc);
         __syncthreads();
         float *tmp = cur; cur = nxt; nxt = tmp;
@@ -243,6 +251,7 @@ __global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const Q
           else
             acc[pp][i] = (mask[5][b >> 5] >> (b & 31)) & 1u ? w7v[i] : 0.f;
         }
+      if constexpr (kInPlace) __syncthreads();  // every thread has read cur
       store_tile<H>(nxt, tp, tu, acc);
       __syncthreads();
       float *tmp = cur; cur = nxt; nxt = tmp;
@@ -318,13 +327,14 @@ __global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const Q
           else
             acc[pp][i] = (mask[li][b >> 5] >> (b & 31)) & 1u ? acc[pp][i] : 0.f;
         }
+      if constexpr (kInPlace) __syncthreads();  // every thread has read cur
       store_tile<H>(nxt, tp, tu, acc);
       __syncthreads();
       float *tmp = cur; cur = nxt; nxt = tmp;
     }
     // g0 = W1^T e1 restricted to the inputs that depend on q; map to d f / d q (R3):
     //   chain rule:  [-g0[0], -g0[1], g0[5..11]];  q-channel: [g0[3], g0[4], g0[5..11]]
-    float *gst = nxt;  // [128][9] staging
+    float *gst = kInPlace ? gstb : nxt;  // [128][9] staging
     {
       const int p = tid & (kTile - 1);
       const int half = tid >> 7;  // warp-uniform
@@ -434,10 +444,12 @@ cudaError_t launch_mlp_simt(int H, const WeightsF32 &w, const QueryArgs &a, int 
   if (a.act == 2) {
     if (H == 128) return launch_h<128, 2>(w, a, num_sms, s);
     if (H == 32) return launch_h<32, 2>(w, a, num_sms, s);
+    if (H == 256) return launch_h<256, 2>(w, a, num_sms, s);
     return cudaErrorInvalidValue;
   }
   if (H == 128) return launch_h<128, 1>(w, a, num_sms, s);
   if (H == 32) return launch_h<32, 1>(w, a, num_sms, s);
+  if (H == 256) return launch_h<256, 1>(w, a, num_sms, s);
   return cudaErrorInvalidValue;
 }
 

@@ -1,5 +1,6 @@
 """GPU parity of the H = 256 variant (NEXT-4, R27; K2w: hidden weights streamed
-from L2 through a shared-memory ring) against the float64 oracle, through the C ABI.
+from L2 through a shared-memory ring; and the fp32 SIMT path at H = 256) against the float64
+oracle, through the C ABI.
 
 Same gates as the H = 128 tensor path (tests/test_gpu_tensor.py, R17): vs the oracle's
 EMU_FP16 mode (same rounding points) the median value error is fp32 noise; vs the exact
@@ -122,9 +123,54 @@ def test_wide_partitioned_ragged_and_updates():
     assert nc > 0
 
 
+def test_wide_fp32_path(c2w):
+    """The fp32 SIMT path at H = 256 (one activation buffer updated in place): the north-star
+    fp32 tolerance against the exact oracle (gradients of pairs within 1e-4 of a ReLU kink
+    exempt, < 0.1 %), and the same records from the fused detect."""
+    from paper_2601_18548_b200 import FP32, Context
+    from gpu_util import check_fp32_dense
+    cfg, pts, q, m, exact, emu = c2w
+    ctx = Context(0, precision=FP32, scene_capacity=cfg.M + 4096, max_waypoints=q.shape[1], max_active=1 << 20)
+    ctx.load_weights(synth.weights_path(H))
+    ids = ctx.update_scene(pts)
+    qt = torch.from_numpy(q)
+    v, g = ctx.query_values_grads(qt)
+    torch.cuda.synchronize()
+    M = len(pts)
+    check_fp32_dense(v.cpu().numpy()[:, :M], g.cpu().numpy()[:, :M], exact["f"], exact["g"], exact["kappa"],
+                     what="H=256 fp32")
+    tau = float(np.quantile(exact["f"], 0.01)) - DELTA
+    out = ctx.detect_active_set(qt, DELTA, tau)
+    torch.cuda.synchronize()
+    gpu = records_np(out)
+    orc = oracle_detect(m, pts, ids, q.reshape(-1, 9), tau, nthreads=NT)
+    nd, nc = compare_active_sets(gpu, orc, exact["f"], ids, 1e-3, what="H=256 fp32 detect")
+    assert nc > 0 and nd <= 0.01 * nc + 2
+
+
+def test_wide_softplus_fp32_path():
+    """Softplus at H = 256 on the fp32 path: every value and gradient within the fp32
+    tolerance of the exact oracle (no kink exemptions)."""
+    from paper_2601_18548_b200 import FP32, Context
+    from gpu_util import fp32_close
+    cfg = synth.get_config("C1")
+    pts, _ = synth.make_scene_points(cfg)
+    q = synth.make_waypoints(cfg)
+    m = oracle.MLP(synth.weights_path(H, act=2))
+    full = m.eval(pts, q.reshape(-1, 9), nthreads=NT)
+    ctx = Context(0, precision=FP32, scene_capacity=1024, max_waypoints=64, max_active=1 << 14)
+    ctx.load_weights(synth.weights_path(H, act=2))
+    ctx.update_scene(pts)
+    v, g = ctx.query_values_grads(torch.from_numpy(q))
+    torch.cuda.synchronize()
+    M = len(pts)
+    assert np.all(fp32_close(v.cpu().numpy()[:, :M], full["f"]))
+    assert np.all(fp32_close(g.cpu().numpy()[:, :M], full["g"]))
+
+
 def test_wide_rejects_other_modes():
-    from paper_2601_18548_b200 import BF16, FP16, FP32, FRAME_SE2, Context, GcdfError
-    for prec, kw in ((FP32, {}), (BF16, {}), (FP16, {"frame": FRAME_SE2})):
+    from paper_2601_18548_b200 import BF16, FP16, FRAME_SE2, Context, GcdfError
+    for prec, kw in ((BF16, {}), (FP16, {"frame": FRAME_SE2})):
         ctx = Context(0, precision=prec, scene_capacity=1024, max_waypoints=16, max_active=1024, **kw)
         with pytest.raises(GcdfError) as e:
             ctx.load_weights(synth.weights_path(H))
