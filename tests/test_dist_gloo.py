@@ -1,7 +1,7 @@
-"""Multi-process (world_size 2, gloo, CPU) test of the multi-GPU gather protocol.
+"""Multi-process (world_size 2 and 3, gloo, CPU) test of the multi-GPU gather protocol.
 
 The product's collective step (paper_2601_18548_b200/dist.py gather_parts) runs on CPU
-tensors under gloo with 2 ranks.  Each rank's local detect result is produced by the
+tensors under gloo with 2 or 3 ranks.  Each rank's local detect result is produced by the
 float64 oracle over the points whose 128-id block the rank owns (block % world == rank,
 the library's sharding rule); the gathered pieces must reassemble the single-rank
 oracle result: MIN of the per-waypoint keys = global min / argmin, gathered offsets =
@@ -77,8 +77,9 @@ def _worker(rank, world, port, q):
 
 
 @pytest.mark.timeout(300)
-def test_gather_protocol_world2():
-    world = 2
+@pytest.mark.parametrize("world", [2, 3])
+def test_gather_protocol(world):
+    """world 3 on C1 (256 points = two 128-id blocks): rank 2 owns no point (an empty shard)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

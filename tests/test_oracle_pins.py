@@ -688,3 +688,50 @@ def test_softplus_emu_consistency(mlp32_softplus):
     assert np.max(np.abs(c["f"] - d["f"])) <= 5e-3 * max(1.0, np.abs(d["f"]).max())
     gn = np.linalg.norm(d["g"], axis=-1)
     assert np.all(np.linalg.norm(c["g"] - d["g"], axis=-1) <= 1e-2 * np.maximum(1.0, gn))
+
+
+# ------------------------------------------------------------------ randomized brute force
+def test_detect_equals_bruteforce_randomized(tmp_path):
+    """Property check on many tiny random problems (hypothesis): the oracle's detect (O6, O7)
+    equals enumerate-filter-sort-min over its own pairwise evaluation, for random widths,
+    activations, ids with holes, duplicated points (exact value ties), thresholds (incl. one
+    that hits a value exactly) and range partitions."""
+    hyp = pytest.importorskip("hypothesis")
+    st = hyp.strategies
+
+    @hyp.settings(max_examples=40, deadline=None, derandomize=True)
+    @hyp.given(seed=st.integers(0, 2**31 - 1), act=st.sampled_from([1, 2]), H=st.sampled_from([2, 5, 8]),
+               M=st.integers(0, 12), W=st.integers(1, 4), radius=st.sampled_from([0.0, 2.5, 6.0]))
+    def check(seed, act, H, M, W, radius):
+        rng = np.random.default_rng(seed)
+        _, dims, layers = synth.make_weights(H, seed=seed % 1000)
+        path = tmp_path / f"r{seed}_{act}_{H}.mlpw"
+        synth.write_mlpw(path, act, dims, layers)
+        m = oracle.MLP(path)
+        pts, q = _rand_inputs(rng, M, W)
+        if M >= 2:
+            pts[M - 1] = pts[0]  # a duplicated point: equal values, smaller id must win
+        ids = np.sort(rng.choice(10 * M + 1, size=M, replace=False)).astype(np.int64)
+        full = m.eval(pts, q)
+        f = full["f"]
+        tau = float(f.ravel()[rng.integers(f.size)]) - DELTA if f.size else 0.5  # hits a value exactly
+        d = m.detect(pts, ids, q, DELTA, tau, radius=radius)
+        inr = np.ones((W, M), bool)
+        if radius > 0:
+            inr = (pts[None, :, 0] - q[:, None, 0]) ** 2 + (pts[None, :, 1] - q[:, None, 1]) ** 2 <= radius ** 2
+        want = [(w, ids[j]) for w in range(W) for j in range(M) if inr[w, j] and f[w, j] - DELTA <= tau]
+        want.sort()
+        got = list(zip(d["wp"].tolist(), d["pt"].tolist()))
+        assert got == [(int(a), int(b)) for a, b in want]
+        assert d["count"] == len(want)
+        for w in range(W):
+            cand = [(f[w, j], ids[j]) for j in range(M) if inr[w, j]]
+            if cand:
+                fm, im = min(cand)
+                assert d["wp_min"][w] == fm and d["wp_argmin"][w] == im
+            else:
+                assert np.isinf(d["wp_min"][w]) and d["wp_argmin"][w] == -1
+        assert np.array_equal(np.diff(d["wp_offsets"]), np.bincount(d["wp"], minlength=W)[:W] if len(want) else
+                              np.zeros(W, np.int64))
+
+    check()
