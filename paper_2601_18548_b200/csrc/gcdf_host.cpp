@@ -84,6 +84,7 @@ struct gcdf_ctx {
   bool loaded = false;
   int H = 0;
   int act = 1;  // MLPW activation: 1 ReLU (R9), 2 softplus (R26)
+  std::vector<float> w7host;  // output row (fp32) for the kernel-parameter copy (bf16_view)
   float b7 = 0.f;
   // scene (replicated on every rank)
   std::vector<uint64_t> live;  // global id bitmap
@@ -184,6 +185,9 @@ WeightsF32 f32_view(const gcdf_ctx *c) {
   return w;
 }
 
+uint16_t to_bf16_rne(float f);
+uint16_t to_f16_rne(float f);
+
 WeightsBF16 bf16_view(const gcdf_ctx *c) {
   WeightsF32 f = f32_view(c);
   WeightsBF16 w{};
@@ -201,6 +205,16 @@ WeightsBF16 bf16_view(const gcdf_ctx *c) {
   }
   w.w3_sw128 = c->ws + c->L.wf16x3;
   w.w1t3_sw128 = c->ws + c->L.wf16x3 + 5 * 2 * kBfMat;
+  if (c->H == 128 && c->w7host.size() == 128) {
+    const bool f16 = c->opt.precision != GCDF_BF16;
+    for (int i = 0; i < 128; ++i) w.w7half_p[i] = 0.5f * c->w7host[i];
+    for (int i = 0; i < 64; ++i) {
+      const float a0 = c->w7host[2 * i], a1 = c->w7host[2 * i + 1];
+      const uint32_t lo = f16 ? to_f16_rne(a0) : to_bf16_rne(a0);
+      const uint32_t hi = f16 ? to_f16_rne(a1) : to_bf16_rne(a1);
+      w.w7h_p[i] = lo | (hi << 16);
+    }
+  }
   w.bh = f.bias[0];  // the five fp32 bias rows are contiguous in the fp32 block
   w.w7 = f.w7;
   w.b7 = f.b7;
@@ -675,6 +689,8 @@ int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
   CK(c, cudaStreamSynchronize(s), "weights sync");
   c->H = H;
   c->act = (int)act;
+  c->w7host.assign(H, 0.f);
+  for (int u = 0; u < H; ++u) c->w7host[u] = W(6, 0, u);
   c->b7 = (float)bd[6][0];
   c->loaded = true;
   return GCDF_OK;

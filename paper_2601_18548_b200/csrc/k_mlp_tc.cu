@@ -36,6 +36,8 @@
 //   * Measured (profiles/r1/mma_probe.txt, trace_tc_*.txt): a 128x128x16 UMMA runs at the
 //     dense rate (64 cycles) when the issue stream is lean; the kernel is bound by the
 //     per-slot chain MMA -> epilogue -> hand-off with two slots.
+#include <type_traits>
+
 #include "gcdf_internal.h"
 #include "tc_ptx.h"
 
@@ -350,7 +352,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   const uint32_t tS = tbase + (uint32_t)s * 256u + lane_off;  // this slot, this lane quarter
   const uint32_t tD = tS + 64u * hh;
   const uint32_t tA = tS + kColA + 32u * hh;
-  const int u0 = 64 * hh;           // first unit of this thread's columns
   uint32_t *mk = &S.mask[s][0][0][hh * 128 + row];  // + (layer * 2 + word) * kEpiPerSlot
   if (hh == 0) {  // the constant "ones" A block of the bias GEMM step: {1, 1, 0, ...}
     uint32_t ones[8] = {pack2<F16>(1.f, 1.f), 0u, 0u, 0u, 0u, 0u, 0u, 0u};
@@ -558,33 +559,39 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         // ---- layer 6: e6 = w7 (.) 1[z6 > 0] -> A; f = w7 . ReLU(z6) + b7 (fp32) ----
         // (16-column chunks; the TMEM load of chunk c + 1 in flight while chunk c is used)
         float fa[4] = {0.f, 0.f, 0.f, 0.f};
-        uint32_t rb[2][16];
-        ld16(tD, rb[0]);
-        wait_ld();
-        if (tr) tr[(p + 1) * 4 + 0] = clock64();
+        // the output row comes from the kernel parameters with compile-time offsets (one body
+        // per column half), i.e. as direct constant-bank operands: no shared-memory loads
+        auto layer6 = [&](auto u0c) {
+          constexpr int U0 = decltype(u0c)::value;
+          uint32_t rb[2][16];
+          ld16(tD, rb[0]);
+          wait_ld();
+          if (tr) tr[(p + 1) * 4 + 0] = clock64();
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int cb = 16 * c;
-          if (c < 3) ld16(tD + cb + 16, rb[(c + 1) & 1]);
-          const uint32_t *rr = rb[c & 1];
-          uint32_t pk[8];
+          for (int c = 0; c < 4; ++c) {
+            const int cb = 16 * c;
+            if (c < 3) ld16(tD + cb + 16, rb[(c + 1) & 1]);
+            const uint32_t *rr = rb[c & 1];
+            uint32_t pk[8];
 #pragma unroll
-          for (int j = 0; j < 16; j += 4) {
-            const float4 w7 = *reinterpret_cast<const float4 *>(S.w7half + u0 + cb + j);
-            const uint2 w2 = *reinterpret_cast<const uint2 *>(S.w7h + (u0 + cb + j) / 2);
-            const float z0 = __uint_as_float(rr[j]), z1 = __uint_as_float(rr[j + 1]);
-            const float z2 = __uint_as_float(rr[j + 2]), z3 = __uint_as_float(rr[j + 3]);
-            pk[j >> 1] = w2.x & nz_halves(pack2_relu<F16>(z0, z1), one);
-            pk[(j >> 1) + 1] = w2.y & nz_halves(pack2_relu<F16>(z2, z3), one);
-            // (w7 / 2) (z + |z|) = w7 ReLU(z) exactly (z + |z| = 2 ReLU(z), halving is exact)
-            fa[0] = fmaf(w7.x, z0 + fabsf(z0), fa[0]);
-            fa[1] = fmaf(w7.y, z1 + fabsf(z1), fa[1]);
-            fa[2] = fmaf(w7.z, z2 + fabsf(z2), fa[2]);
-            fa[3] = fmaf(w7.w, z3 + fabsf(z3), fa[3]);
+            for (int j = 0; j < 16; j += 4) {
+              const int u = U0 + cb + j;
+              const float z0 = __uint_as_float(rr[j]), z1 = __uint_as_float(rr[j + 1]);
+              const float z2 = __uint_as_float(rr[j + 2]), z3 = __uint_as_float(rr[j + 3]);
+              pk[j >> 1] = W.w7h_p[u / 2] & nz_halves(pack2_relu<F16>(z0, z1), one);
+              pk[(j >> 1) + 1] = W.w7h_p[u / 2 + 1] & nz_halves(pack2_relu<F16>(z2, z3), one);
+              // (w7 / 2) (z + |z|) = w7 ReLU(z) exactly (z + |z| = 2 ReLU(z), halving is exact)
+              fa[0] = fmaf(W.w7half_p[u], z0 + fabsf(z0), fa[0]);
+              fa[1] = fmaf(W.w7half_p[u + 1], z1 + fabsf(z1), fa[1]);
+              fa[2] = fmaf(W.w7half_p[u + 2], z2 + fabsf(z2), fa[2]);
+              fa[3] = fmaf(W.w7half_p[u + 3], z3 + fabsf(z3), fa[3]);
+            }
+            st8(tA + cb / 2, pk);
+            if (c < 3) wait_ld();
           }
-          st8(tA + cb / 2, pk);
-          if (c < 3) wait_ld();
-        }
+        };
+        if (hh == 0) layer6(std::integral_constant<int, 0>{});
+        else layer6(std::integral_constant<int, 64>{});
         if (tr) tr[(p + 1) * 4 + 2] = clock64();
         hand_off(p + 1, s == 1 || T + 1 < n_tiles);
         if (tr) tr[(p + 1) * 4 + 3] = clock64();
