@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--partition-radius", type=float, default=1.8,
                     help="also time the range-partitioned detect (NEXT-1) at this radius; 0 = skip")
+    ap.add_argument("--no-variants", dest="variants", action="store_false",
+                    help="skip the softplus / H = 256 variant measurements (NEXT-4) of the default run")
     ap.add_argument("--latency-calls", type=int, default=50,
                     help="detect-latency sample size (wall time q on device -> count on host); 0 = skip")
     return ap.parse_args()
@@ -428,6 +430,48 @@ def main():
                 ms = np.sort(np.array(ts)) * 1e3
                 lat[name] = {"p50_ms": float(np.percentile(ms, 50)), "p99_ms": float(np.percentile(ms, 99))}
 
+    # NEXT-4 variants on the same workload (single GPU, default run only): device time per
+    # detect over the whole scene with the softplus network (K2s) and the H = 256 network
+    # (K2w), each in a context of its own; tensor roofline against the same peak
+    variants = None
+    if world == 1 and a.variants and a.activation == "relu" and not hidden and prec == "fp16":
+        variants = {}
+        for name, act_v, h_v in (("softplus", 2, None), ("hidden256", 1, 256)):
+            cfg_v = dataclasses.replace(cfg, H=h_v) if h_v else cfg
+            ctx_v = Context(local, precision=FP16, scene_capacity=cfg.M + slack, max_waypoints=n_wp,
+                            max_active=max_active)
+            ctx_v.load_weights(synth.weights_path(cfg_v.H, act=act_v))
+            ctx_v.update_scene(pts)
+            tau_v = synth.load_tau(cfg.name, act_v, h_v)
+            outs_v = ctx_v.alloc_detect_outputs(n_wp, max_active)
+            for _ in range(2):
+                ctx_v.detect_active_set(q, delta, tau_v, outputs=outs_v, sync_count=False)
+            torch.cuda.synchronize()
+            ctx_v.profile_read(reset=True)
+            ctx_v.profile_enable(True)
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+            for e0, e1 in evs:
+                flush.zero_()
+                e0.record()
+                ov = ctx_v.detect_active_set(q, delta, tau_v, outputs=outs_v, sync_count=False)
+                e1.record()
+            torch.cuda.synchronize()
+            k_ms, k_n = ctx_v.profile_read(reset=True)
+            ctx_v.profile_enable(False)
+            ms_v = sum(e0.elapsed_time(e1) for e0, e1 in evs) / len(evs)
+            pairs_v = ctx_v.scene_info()["n_live"] * n_wp
+            ach = FLOPS_PAIR_TENSOR[cfg_v.H] * pairs_v / (k_ms / k_n / 1e3) / 1e12
+            pk = float(peaks.get("bf16_tflops"))
+            variants[name] = {"kernel": "k_mlp_tc_sp" if act_v == 2 else "k_mlp_tc_wide", "hidden": cfg_v.H,
+                              "activation": "softplus" if act_v == 2 else "relu", "ms_per_step": ms_v,
+                              "value": pairs_v / (ms_v / 1e3), "unit": "queries/s", "tau": tau_v,
+                              "active_per_step": int(ov["count"].item()),
+                              "roofline": {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+                                           "frac": ach / pk, "flops_per_pair": FLOPS_PAIR_TENSOR[cfg_v.H]}}
+            ctx_v.close()
+            del outs_v
+            torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         cpu = cpu_oracle_rate(cfg, pts, q_np, sample_pts=65536 if cfg.H <= 128 else 16384, single_thread=True,
@@ -445,6 +489,7 @@ def main():
             "roofline": roof, "mlp_kernel_share_of_step": kshare,
             "detect_latency": lat,
             "partitioned": part,
+            "variants": variants,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_pairs / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": h2d // e2e_steps,
                     "d2h_bytes_per_step": d2h // e2e_steps, "steps": e2e_steps},

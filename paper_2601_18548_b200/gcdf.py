@@ -182,11 +182,17 @@ class Context:
         self.max_active = max_active
         self.rank, self.world = rank, world
 
-    def __del__(self):
+    def close(self):
+        """Destroy the library context and release its workspace (idempotent)."""
         h = getattr(self, "_h", None)
         if h is not None and _lib is not None:
+            torch.cuda.synchronize(self.device)
             _lib.gcdf_destroy(h)
             self._h = None
+        self.workspace = None
+
+    def __del__(self):
+        self.close()
 
     def _check(self, rc):
         if rc:
