@@ -205,10 +205,10 @@ WeightsBF16 bf16_view(const gcdf_ctx *c) {
   }
   w.w3_sw128 = c->ws + c->L.wf16x3;
   w.w1t3_sw128 = c->ws + c->L.wf16x3 + 5 * 2 * kBfMat;
-  if (c->H == 128 && c->w7host.size() == 128) {
+  if ((c->H == 128 || c->H == 256) && (int)c->w7host.size() == c->H) {
     const bool f16 = c->opt.precision != GCDF_BF16;
-    for (int i = 0; i < 128; ++i) w.w7half_p[i] = 0.5f * c->w7host[i];
-    for (int i = 0; i < 64; ++i) {
+    for (int i = 0; i < c->H; ++i) w.w7half_p[i] = 0.5f * c->w7host[i];
+    for (int i = 0; i < c->H / 2; ++i) {
       const float a0 = c->w7host[2 * i], a1 = c->w7host[2 * i + 1];
       const uint32_t lo = f16 ? to_f16_rne(a0) : to_bf16_rne(a0);
       const uint32_t hi = f16 ? to_f16_rne(a1) : to_bf16_rne(a1);

@@ -50,11 +50,11 @@ struct WeightsBF16 {
   const void *w1t3_sw128;  // (GCDF_FP16X3) W1^T [16][H] hi, lo (SW128), 4 KB each
   const float *w7;       // [H] fp32
   float b7;
-  // (K2b, H = 128) the output row in the kernel parameters (constant bank): w7 / 2 in fp32 and
-  // w7 as packed 16-bit pairs of the context's operand type; the layer-6 epilogue reads them
-  // as direct constant operands instead of shared-memory loads
-  float w7half_p[128];
-  uint32_t w7h_p[64];
+  // (K2b, K2w: H = 128, 256) the output row in the kernel parameters (constant bank): w7 / 2
+  // in fp32 and w7 as packed 16-bit pairs of the context's operand type; the layer-6
+  // epilogue reads them as direct constant operands instead of shared-memory loads
+  float w7half_p[256];
+  uint32_t w7h_p[128];
 };
 
 struct SceneView {

@@ -29,6 +29,8 @@
 //     the K2b per-thread work), ReLU masks in shared memory in K2b's byte-sign form.
 // Rounding points: those of K2b (EMU_FP16 in the oracle: W_2..W_6, W_1 (gradient), h_1..h_5,
 // e_6..e_1 rounded to fp16; layer 1 split hi/lo; f = w7 . h6 in fp32).
+#include <type_traits>
+
 #include "gcdf_internal.h"
 #include "tc_ptx.h"
 
@@ -64,8 +66,6 @@ struct __align__(1024) SmemW {
   uint8_t ones[kOnesBytes];
   uint8_t zero[kZeroBytes];        // (after bext and ones: the descriptors' LBO offsets are positive)
   uint32_t mask[kMasks][2][kEpi];  // ReLU masks [layer][32-unit word][thread]
-  float w7half[H];
-  uint32_t w7h[H / 2];
   uint32_t one;
   float fpart[4][128];
   float4 ptn[128];
@@ -121,8 +121,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
     for (int i = tid; i < kZeroBytes / 16; i += kThreads) reinterpret_cast<uint4 *>(S.zero)[i] = make_uint4(0, 0, 0, 0);
     for (int r = tid; r < 128; r += kThreads)  // ones block, no-swizzle K-major: row r at (r / 8) * 128 + (r % 8) * 16
       *reinterpret_cast<uint4 *>(S.ones + (r >> 3) * 128 + (r & 7) * 16) = make_uint4(pack_f16(1.f, 1.f), 0u, 0u, 0u);
-    for (int i = tid; i < H; i += kThreads) S.w7half[i] = 0.5f * __ldg(W.w7 + i);
-    for (int i = tid; i < H / 2; i += kThreads) S.w7h[i] = pack_f16(__ldg(W.w7 + 2 * i), __ldg(W.w7 + 2 * i + 1));
     if (tid == 0) S.one = 1u;
   }
   if (warp == 0) {
@@ -363,30 +361,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
       } else if (p == 5) {
         // ---- layer 6: e6 = w7 (.) 1[z6 > 0] -> A; f = w7 . ReLU(z6) + b7 (fp32) ----
         float fa[4] = {0.f, 0.f, 0.f, 0.f};
-        uint32_t rb[2][16];
-        ld16(tD, rb[0]);
-        wait_ld();
+        // the output row from the kernel parameters at compile-time offsets (one body per unit
+        // quarter): direct constant-bank operands, no shared-memory loads (as in K2b)
+        auto layer6 = [&](auto u0c) {
+          constexpr int U0 = decltype(u0c)::value;
+          uint32_t rb[2][16];
+          ld16(tD, rb[0]);
+          wait_ld();
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int cb = 16 * c;
-          if (c < 3) ld16(tD + cb + 16, rb[(c + 1) & 1]);
-          const uint32_t *rr = rb[c & 1];
-          uint32_t pk[8];
+          for (int c = 0; c < 4; ++c) {
+            const int cb = 16 * c;
+            if (c < 3) ld16(tD + cb + 16, rb[(c + 1) & 1]);
+            const uint32_t *rr = rb[c & 1];
+            uint32_t pk[8];
 #pragma unroll
-          for (int j = 0; j < 16; j += 4) {
-            const float4 w7 = *reinterpret_cast<const float4 *>(S.w7half + u0 + cb + j);
-            const uint2 w2 = *reinterpret_cast<const uint2 *>(S.w7h + (u0 + cb + j) / 2);
-            const float z0 = __uint_as_float(rr[j]), z1 = __uint_as_float(rr[j + 1]);
-            const float z2 = __uint_as_float(rr[j + 2]), z3 = __uint_as_float(rr[j + 3]);
-            pk[j >> 1] = w2.x & nz_halves(pack_f16_relu(z0, z1), one);
-            pk[(j >> 1) + 1] = w2.y & nz_halves(pack_f16_relu(z2, z3), one);
-            fa[0] = fmaf(w7.x, z0 + fabsf(z0), fa[0]);
-            fa[1] = fmaf(w7.y, z1 + fabsf(z1), fa[1]);
-            fa[2] = fmaf(w7.z, z2 + fabsf(z2), fa[2]);
-            fa[3] = fmaf(w7.w, z3 + fabsf(z3), fa[3]);
+            for (int j = 0; j < 16; j += 4) {
+              const int u = U0 + cb + j;
+              const float z0 = __uint_as_float(rr[j]), z1 = __uint_as_float(rr[j + 1]);
+              const float z2 = __uint_as_float(rr[j + 2]), z3 = __uint_as_float(rr[j + 3]);
+              pk[j >> 1] = W.w7h_p[u / 2] & nz_halves(pack_f16_relu(z0, z1), one);
+              pk[(j >> 1) + 1] = W.w7h_p[u / 2 + 1] & nz_halves(pack_f16_relu(z2, z3), one);
+              fa[0] = fmaf(W.w7half_p[u], z0 + fabsf(z0), fa[0]);
+              fa[1] = fmaf(W.w7half_p[u + 1], z1 + fabsf(z1), fa[1]);
+              fa[2] = fmaf(W.w7half_p[u + 2], z2 + fabsf(z2), fa[2]);
+              fa[3] = fmaf(W.w7half_p[u + 3], z3 + fabsf(z3), fa[3]);
+            }
+            st8(tA(p) + cb / 2, pk);
+            if (c < 3) wait_ld();
           }
-          st8(tA(p) + cb / 2, pk);
-          if (c < 3) wait_ld();
+        };
+        switch (cq) {
+          case 0: layer6(std::integral_constant<int, 0>{}); break;
+          case 1: layer6(std::integral_constant<int, 64>{}); break;
+          case 2: layer6(std::integral_constant<int, 128>{}); break;
+          default: layer6(std::integral_constant<int, 192>{}); break;
         }
         hand_off();
         S.fpart[cq][row] = (fa[0] + fa[1]) + (fa[2] + fa[3]);
