@@ -66,6 +66,16 @@ constexpr int kEpiWarps = 16;             // warps 0..15: epilogue (8 per tile s
 #ifndef GCDF_TC_EWAIT
 #define GCDF_TC_EWAIT 0
 #endif
+// epilogue -> MMA-warp hand-off (dev switch): 0 = mbarrier epi_done[s] (256 arrivals, the
+// MMA warp try_waits), 1 = named barrier 5 + s (bar.arrive by the 256 epilogue threads,
+// bar.sync by the slot's MMA warp).  Measured the same (C5 3.04-3.06e9 either way): the
+// hand-off is not where the per-slot chain waits
+#ifndef GCDF_TC_NAMEDBAR
+#define GCDF_TC_NAMEDBAR 0
+#endif
+#if GCDF_TC_NAMEDBAR && GCDF_TC_ISSUE == 0
+#error "GCDF_TC_NAMEDBAR needs one MMA warp per slot (GCDF_TC_ISSUE 1)"
+#endif
 template <int kMode>
 DEVI void mbar_wait_mode(uint64_t *bar, uint32_t parity) {
   if constexpr (kMode == 1) mbar_wait_spin(bar, parity);
@@ -288,7 +298,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         long long *t = (tr0 && itt < kTraceTiles) ? tr0 + ((size_t)itt * kTracePhases + p) * 4 + 2 * ss : nullptr;
         long long *t2 = t ? t + (size_t)(kTraceRoles - 1) * kTraceTiles * kTracePhases * 4 : nullptr;
         if (t2) t2[0] = clock64();
+#if GCDF_TC_NAMEDBAR
+        named_bar_sync(5 + ss, kEpiPerSlot + 32);
+#else
         mbar_wait_mode<GCDF_TC_IWAIT>(&S.epi_done[ss], ph);
+#endif
         ph ^= 1u;
         if (two) {
           const long long tw = clock64();
@@ -361,7 +375,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   auto hand_off = [&](int, bool) {
     wait_st();
     fence_before();
-#if GCDF_TC_WARPARRIVE
+#if GCDF_TC_NAMEDBAR
+    named_bar_arrive(5 + s, kEpiPerSlot + 32);
+#elif GCDF_TC_WARPARRIVE
     __syncwarp();
     if (lane == 0) mbar_arrive(&S.epi_done[s]);
 #else

@@ -113,6 +113,7 @@ DEVI void bulk_g2s(void *dst_smem, const void *src, uint32_t bytes, uint64_t *ba
 DEVI void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 DEVI void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 DEVI void named_bar_sync(uint32_t id, uint32_t n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+DEVI void named_bar_arrive(uint32_t id, uint32_t n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // ------------------------------------------------------------------ cp.async (global -> smem, no registers)
 // 16-byte copy; src_bytes = 0 zero-fills the destination (out-of-range source)
