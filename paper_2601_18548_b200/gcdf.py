@@ -186,7 +186,10 @@ class Context:
         """Destroy the library context and release its workspace (idempotent)."""
         h = getattr(self, "_h", None)
         if h is not None and _lib is not None:
-            torch.cuda.synchronize(self.device)
+            try:  # (at interpreter shutdown torch.cuda may already be torn down)
+                torch.cuda.synchronize(self.device)
+            except Exception:
+                pass
             _lib.gcdf_destroy(h)
             self._h = None
         self.workspace = None
