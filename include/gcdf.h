@@ -47,7 +47,7 @@ enum gcdf_status {
   GCDF_ERR_IO = -2,
   GCDF_ERR_BAD_MAGIC = -3,     /* weights file does not start with "MLPW" */
   GCDF_ERR_VERSION = -4,       /* MLPW version != 1 */
-  GCDF_ERR_DIM_MISMATCH = -5,  /* dims not [12, H x 6, 1] with H in {32, 128}, or an activation
+  GCDF_ERR_DIM_MISMATCH = -5,  /* dims not [12, H x 6, 1] with H in {32, 128, 256}, or an activation / width
                                   the context's precision does not run */
   GCDF_ERR_NOT_LOADED = -6,    /* no weights loaded / no workspace bound */
   GCDF_ERR_CAPACITY = -7,      /* scene, waypoint, staging or output capacity exceeded */
@@ -122,7 +122,9 @@ int gcdf_bind_workspace(gcdf_ctx *ctx, void *dev_ptr, int64_t bytes);
 /* ------------------------------------------------------------------ weights */
 /* Loads an MLPW v1 file: "MLPW", u32 version = 1, u32 activation
    (1 = ReLU, R9; 2 = softplus log(1 + e^z), the NEXT-4 variant of R26 --
-   GCDF_FP32 and GCDF_FP16 only), u32 L = 7, u32 dims[8] = [12, H, H, H, H, H, H, 1] with H in {32, 128},
+   GCDF_FP32 and GCDF_FP16 only), u32 L = 7, u32 dims[8] = [12, H, H, H, H, H, H, 1] with H in {32, 128, 256}
+   (H = 32: GCDF_FP32; H = 256, the NEXT-4 width variant of DESIGN.md R27: GCDF_FP32, or GCDF_FP16
+   with ReLU in the translation frame),
    then per layer f64 W[out][in] row-major and f64 b[out].  Packs fp32 and bf16
    (UMMA SWIZZLE_128B) copies into the workspace (enqueued on `stream`, host staging
    synchronized before return).  Errors: IO (missing/truncated), BAD_MAGIC, VERSION,
