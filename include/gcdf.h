@@ -82,8 +82,8 @@ enum gcdf_frame {
 typedef struct {
   int32_t precision;       /* gcdf_precision (default GCDF_FP16) */
   int32_t tgrad_mode;      /* gcdf_tgrad */
-  int64_t scene_capacity;  /* global id space [0, scene_capacity) of obstacle points */
-  int32_t max_waypoints;   /* largest B*N accepted by query/detect */
+  int64_t scene_capacity;  /* global id space [0, scene_capacity) of obstacle points; < 2^31 */
+  int32_t max_waypoints;   /* largest B*N accepted by query/detect; <= 65535 */
   int64_t max_active;      /* staging capacity (records) of detect on this rank */
   int32_t rank;            /* point sharding: this rank owns ids whose 128-id block */
   int32_t world;           /*   (id / 128) satisfies block % world == rank; world >= 1 */
@@ -106,7 +106,9 @@ typedef struct {
 void gcdf_default_options(gcdf_options *opt);
 
 /* Creates a context on CUDA device cuda_device.  Fails with UNSUPPORTED unless the
-   device is compute capability 10.0 (B200).  opt may be NULL (defaults). */
+   device is compute capability 10.0 (B200).  opt may be NULL (defaults).  INVALID_ARG for
+   scene_capacity outside (0, 2^31), max_waypoints outside [1, 65535], max_active outside
+   (0, 2^31), a bad rank / world pair or an unknown precision / tgrad / frame. */
 int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out);
 int gcdf_destroy(gcdf_ctx *ctx);
 const char *gcdf_last_error(const gcdf_ctx *ctx);
@@ -219,10 +221,12 @@ int gcdf_sparse_jacobian(gcdf_ctx *ctx, const gcdf_active_t *recs_dev, const int
    with exactly these arguments is captured once into a CUDA graph; gcdf_graph_launch
    replays it on `stream` (the contents of q_dev may change between launches, the pointers
    may not) and, with count_host non-NULL, synchronizes and returns the count / CAPACITY
-   like the direct call.  After a scene update the next launch re-captures (the tile
-   counts and the partition grid depend on the scene); a partitioned graph's grid is built
-   outside the graph at capture time.  The graph owns a capture stream; it must be
-   destroyed before its context. */
+   like the direct call.  After a scene update, gcdf_load_weights or gcdf_bind_workspace the
+   next launch re-captures (the tile counts and the partition grid depend on the scene; the
+   kernel nodes hold the output row, the bias and the kernel chosen for H / activation); a
+   partitioned graph's grid is built outside the graph, at capture time and again at launch
+   when a call at another radius rebuilt it meanwhile.  The graph owns a capture stream; it
+   must be destroyed before its context. */
 typedef struct gcdf_graph gcdf_graph;
 int gcdf_graph_create_detect(gcdf_ctx *ctx, const float *q_dev, int32_t B, int32_t N, float radius, float delta,
                              float tau, gcdf_active_t *out_dev, int64_t out_capacity, int64_t *wp_offsets_dev,
@@ -282,9 +286,8 @@ int gcdf_profile_read(gcdf_ctx *ctx, double *mlp_ms, int64_t *mlp_launches, int 
    staged in TMEM), B_dev fp32 row-major (rounded to bf16, staged in smem, SWIZZLE_128B),
    D_dev fp32 [128][128] output.  mode 0: D = A B^T, B [128][128] (K-major B);
    mode 1: D = A B, B [128][128] (MN-major B); mode 2: D[:, 0:16] = A B^T, B [16][128];
-   mode | 4: the same with fp16 operands instead of bf16.
-   mode 16 + 2 v + f16 (v = 0..4, 8..25; 5..7 = CTA-pair probes; 26, 27 = sub-partition interference): UMMA throughput probe,
-   A and B ignored, D[0] = cycles and D[1] = number of UMMAs (tools/mma_probe.py).
+   mode | 4: the same with fp16 operands instead of bf16.  Other modes: INVALID_ARG (the UMMA
+   throughput probes live in tools/probes/umma_probes.cu, outside the library).
    Synchronizes the stream.  UNSUPPORTED without the tcgen05 build. */
 int gcdf_selftest_umma(int cuda_device, int mode, const float *A_dev, const float *B_dev, float *D_dev,
                        void *stream);

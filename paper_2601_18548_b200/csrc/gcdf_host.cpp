@@ -104,6 +104,7 @@ struct gcdf_ctx {
   bool part_dirty = true;
   float part_r = -1.f;
   int64_t scene_version = 0;   // bumped by every scene change (captured graphs re-capture)
+  int64_t weights_version = 0; // bumped by gcdf_load_weights / gcdf_bind_workspace (same)
 };
 
 // A captured detect (gcdf_graph_create_detect): the arguments, the instantiated graph and
@@ -119,7 +120,9 @@ struct gcdf_graph {
   float *wmin = nullptr;
   cudaStream_t cs = nullptr;   // capture stream
   cudaGraphExec_t exec = nullptr;
-  int64_t version = -1;
+  int64_t version = -1;        // scene_version at capture
+  int64_t wversion = -1;       // weights_version at capture (the kernel nodes hold the weights
+                               // by value: output row, bias, and the kernel chosen for H / act)
 };
 
 namespace {
@@ -361,7 +364,11 @@ int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out) {
   gcdf_options o;
   gcdf_default_options(&o);
   if (opt) o = *opt;
-  if (o.scene_capacity <= 0 || o.scene_capacity >= (1LL << 32) || o.max_waypoints <= 0 || o.max_active <= 0 ||
+  // scene_capacity < 2^31: local slots are int32 in the partition and ~0u is the dead-slot
+  // sentinel of the tensor kernels; max_waypoints <= 65535: the finalize / compaction /
+  // pair-generation kernels put the waypoint on gridDim.y
+  if (o.scene_capacity <= 0 || o.scene_capacity >= (1LL << 31) || o.max_waypoints <= 0 ||
+      o.max_waypoints > 65535 || o.max_active <= 0 ||
       o.max_active >= (1LL << 31) || o.world < 1 || o.rank < 0 || o.rank >= o.world ||
       (o.precision != GCDF_FP32 && o.precision != GCDF_BF16 && o.precision != GCDF_FP16 &&
        o.precision != GCDF_FP16X3) ||
@@ -475,6 +482,9 @@ int gcdf_bind_workspace(gcdf_ctx *c, void *dev_ptr, int64_t bytes) {
   c->ws = static_cast<char *>(dev_ptr);
   c->ws_bytes = bytes;
   c->loaded = false;
+  ++c->weights_version;
+  ++c->scene_version;
+  c->part_dirty = true;
   std::fill(c->live.begin(), c->live.end(), 0ull);
   c->n_live = c->id_bound = c->cursor = 0;
   cudaSetDevice(c->device);
@@ -693,6 +703,7 @@ int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
   for (int u = 0; u < H; ++u) c->w7host[u] = W(6, 0, u);
   c->b7 = (float)bd[6][0];
   c->loaded = true;
+  ++c->weights_version;
   return GCDF_OK;
 }
 
@@ -1099,6 +1110,7 @@ static int graph_capture(gcdf_graph *g) {
   cudaGraphDestroy(graph);
   if (e2 != cudaSuccess) return cuda_fail(c, e2, "graph instantiate");
   g->version = c->scene_version;
+  g->wversion = c->weights_version;
   return GCDF_OK;
 }
 
@@ -1134,10 +1146,23 @@ int gcdf_graph_launch(gcdf_graph *g, int64_t *count_host, void *stream) {
   int rc = precheck(c);
   if (rc) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (g->version != c->scene_version) {  // the scene changed: tile counts / grid differ
+  if (g->version != c->scene_version || g->wversion != c->weights_version) {
+    // the scene changed (tile counts / grid differ) or the weights were reloaded (the kernel
+    // nodes hold the output row, the bias and the kernel chosen for H / activation by value)
     CK(c, cudaStreamSynchronize(s), "graph: order before re-capture");
     if ((rc = graph_capture(g))) return rc;
     CK(c, cudaStreamSynchronize(g->cs), "graph: grid build");
+  } else if (g->radius > 0.f && (c->part_dirty || c->part_r != g->radius)) {
+    // a direct partitioned call at another radius rebuilt the grid (its parameters live on
+    // the device and the graph reads them): rebuild it at this graph's radius, stream-ordered
+    const PartScratch ps = part_view(c);
+    const SceneView sv = scene_view(c);
+    int nl = 0;
+    if ((rc = count_launch(c, launch_part_grid(sv.pts, sv.local_bound, g->radius, ps, s, &nl), "grid", 0)))
+      return rc;
+    c->launches += nl;
+    c->part_dirty = false;
+    c->part_r = g->radius;
   }
   CK(c, cudaGraphLaunch(g->exec, s), "graph launch");
   return read_count(c, g->cap, g->count, count_host, s);
@@ -1159,7 +1184,7 @@ int gcdf_debug_trace(gcdf_ctx *c, long long *trace_dev) {
 
 int gcdf_selftest_umma(int dev, int mode, const float *A, const float *B, float *D, void *stream) {
   if (!tc_compiled()) return GCDF_ERR_UNSUPPORTED;
-  if (mode < 0 || (mode < 16 && (mode > 6 || (mode & 3) > 2)) || mode > 75 || !A || !B || !D) return GCDF_ERR_INVALID_ARG;
+  if (mode < 0 || mode > 6 || (mode & 3) > 2 || !A || !B || !D) return GCDF_ERR_INVALID_ARG;
   if (cudaSetDevice(dev) != cudaSuccess) return GCDF_ERR_CUDA;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (launch_selftest_umma(mode, A, B, D, s) != cudaSuccess) return GCDF_ERR_CUDA;

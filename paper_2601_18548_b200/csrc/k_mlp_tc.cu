@@ -47,50 +47,11 @@ namespace {
 using namespace tc;
 
 constexpr int H = 128;
-#ifndef GCDF_TC_NOEPI
-#define GCDF_TC_NOEPI 0
-#endif
 constexpr int kEpiWarps = 16;             // warps 0..15: epilogue (8 per tile slot)
-// MMA issue (dev switch): 1 = one MMA warp per slot (default), 0 = one MMA warp for both
-// slots.  (Measured: 1 is ~1 % faster; the last epilogue warp issuing instead of an MMA
-// warp was 7 % slower.)
-#ifndef GCDF_TC_ISSUE
-#define GCDF_TC_ISSUE 1
-#endif
-// mbarrier waits (dev switch): 0 = try_wait (hardware suspend), 1 = test_wait spin,
-// 2 = try_wait with a 20 ns suspend hint; IWAIT: the MMA warps on epi_done, EWAIT: the
-// epilogue warps on mma_done
-#ifndef GCDF_TC_IWAIT
-#define GCDF_TC_IWAIT 0
-#endif
-#ifndef GCDF_TC_EWAIT
-#define GCDF_TC_EWAIT 0
-#endif
-// epilogue -> MMA-warp hand-off (dev switch): 0 = mbarrier epi_done[s] (256 arrivals, the
-// MMA warp try_waits), 1 = named barrier 5 + s (bar.arrive by the 256 epilogue threads,
-// bar.sync by the slot's MMA warp).  Measured the same (C5 3.04-3.06e9 either way): the
-// hand-off is not where the per-slot chain waits
-#ifndef GCDF_TC_NAMEDBAR
-#define GCDF_TC_NAMEDBAR 0
-#endif
-#if GCDF_TC_NAMEDBAR && GCDF_TC_ISSUE == 0
-#error "GCDF_TC_NAMEDBAR needs one MMA warp per slot (GCDF_TC_ISSUE 1)"
-#endif
-template <int kMode>
-DEVI void mbar_wait_mode(uint64_t *bar, uint32_t parity) {
-  if constexpr (kMode == 1) mbar_wait_spin(bar, parity);
-  else if constexpr (kMode == 2) mbar_wait_hint<20u>(bar, parity);
-  else mbar_wait(bar, parity);
-}
-constexpr int kWarps = kEpiWarps + (GCDF_TC_ISSUE == 0 ? 1 : 2);
+constexpr int kWarps = kEpiWarps + 2;      // + warp 16 + s: issues tile slot s's UMMAs
 constexpr int kThreads = kWarps * 32;
 constexpr int kEpiPerSlot = 256;
-// epi_done arrivals (dev switch GCDF_TC_WARPARRIVE): 0 = every epilogue thread arrives,
-// 1 = one elected lane per warp after __syncwarp
-#ifndef GCDF_TC_WARPARRIVE
-#define GCDF_TC_WARPARRIVE 0
-#endif
-constexpr int kEpiArrivals = GCDF_TC_WARPARRIVE ? kEpiPerSlot / 32 : kEpiPerSlot;  // epi_done count
+constexpr int kEpiArrivals = kEpiPerSlot;  // epi_done count: every epilogue thread of the slot
 constexpr int kPhases = 12;               // MMA phases per tile
 constexpr int kMasks = 5;                 // stored ReLU masks: layers 1..5
 constexpr int kWBytes = 5 * H * H * 2;    // 163,840
@@ -101,8 +62,6 @@ constexpr int kBextBytes = 16 * H * 2;    // 4,096 per hidden layer
 // (g0 and x have columns of their own so that the last GEMM of a tile and the first of the
 // next one are issued as one phase, see issue_phase)
 constexpr uint32_t kColA = 128, kColOnes = 192, kColG0 = 200, kColX = 216;
-// or an fp32 add in the epilogue (1).
-// mbarrier waits: bit 0 = MMA thread spins with test_wait, bit 1 = epilogue warps spin
 template <bool F16> constexpr uint32_t kIdescFwd = idesc_f16kind(128, 128, false, F16);
 template <bool F16> constexpr uint32_t kIdescBwd = idesc_f16kind(128, 128, true, F16);
 template <bool F16> constexpr uint32_t kIdescFin = idesc_f16kind(128, 16, false, F16);
@@ -112,8 +71,6 @@ struct __align__(1024) SmemTC {
   uint8_t w1t[kW1tBytes];      // W1^T [16][128], SW128
   uint8_t b1[kB1Bytes];        // layer-1 split weights [128][32], no swizzle
   uint8_t bext[5][kBextBytes]; // hidden-layer bias blocks [128][16], no swizzle
-  float w7half[H];             // w7 / 2: f = sum w7half (z6 + |z6|) = w7 . ReLU(z6), all on the FMA pipe
-  uint32_t w7h[H / 2];         // w7 as packed 16-bit pairs: e6 = w7 (.) 1[z6 > 0]
   uint32_t one;                // 1 (runtime constant, see add7fff)
   float fpart[2][2][H];        // [slot][column half][row] partial output-layer sums
   float4 ptn[2][H];            // [slot][row] prefetched point of the slot's next tile
@@ -125,7 +82,8 @@ struct __align__(1024) SmemTC {
   uint32_t mask[2][kMasks][2][kEpiPerSlot];  // ReLU masks [slot][layer][32-unit word][thread]
   uint64_t mma_done[2];
   uint64_t epi_done[2];
-  uint32_t turn;               // (GCDF_TC_ISSUE 1) global issue-order counter
+  uint64_t wbar;               // the resident weights landed (bulk copies, complete_tx)
+  uint32_t turn;               // global issue-order counter of the two MMA warps
   unsigned act[2][4];
   unsigned long long kmin[2][4];
   int sbase[2];
@@ -229,20 +187,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   SmemTC &S = *reinterpret_cast<SmemTC *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // ---- one-time setup: weights -> smem (already in UMMA layouts in global memory) ----
-  {
-    auto copy16 = [&](void *dst, const void *src, int bytes) {
-      const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
-      uint4 *d4 = reinterpret_cast<uint4 *>(dst);
-      for (int i = tid; i < bytes / 16; i += kThreads) d4[i] = __ldg(s4 + i);
-    };
-    copy16(S.w, W.w_sw128, kWBytes);
-    copy16(S.w1t, W.w1t_sw128, kW1tBytes);
-    copy16(S.b1, W.b1_nosw, kB1Bytes);
-    copy16(S.bext, W.bext_nosw, 5 * kBextBytes);
-    for (int i = tid; i < H; i += kThreads) S.w7half[i] = 0.5f * __ldg(W.w7 + i);
-    if (tid == 0) S.one = 1u;
-    for (int i = tid; i < H / 2; i += kThreads) S.w7h[i] = pack2<F16>(__ldg(W.w7 + 2 * i), __ldg(W.w7 + 2 * i + 1));
+  // ---- one-time setup: the resident weights (already in their UMMA layouts in global
+  // memory, 196 KB) -> smem by 1-D bulk copies (cp.async.bulk, the TMA engine) completing on
+  // S.wbar; only the MMA warps wait for them (before their first UMMA), so the copy overlaps
+  // the epilogue warps' staging of the first tiles ----
+  if (tid == 0) {
+    S.one = 1u;
+    mbar_init(&S.wbar, 1);
+    fence_barrier_init();
+    constexpr uint32_t kChunk = 32768;
+    mbar_expect_tx(&S.wbar, (uint32_t)(kWBytes + kW1tBytes + kB1Bytes + 5 * kBextBytes));
+    for (uint32_t o = 0; o < (uint32_t)kWBytes; o += kChunk)
+      bulk_g2s(S.w + o, static_cast<const uint8_t *>(W.w_sw128) + o, kChunk, &S.wbar);
+    bulk_g2s(S.w1t, W.w1t_sw128, kW1tBytes, &S.wbar);
+    bulk_g2s(S.b1, W.b1_nosw, kB1Bytes, &S.wbar);
+    bulk_g2s(S.bext, W.bext_nosw, 5 * kBextBytes, &S.wbar);
   }
   if (warp == 0) {
     tmem_alloc(&S.tmem_base, 512);
@@ -274,7 +233,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   const int64_t lb = a.scene.local_bound;
   const int64_t stride = 2 * (int64_t)gridDim.x;
 
-#if GCDF_TC_ISSUE == 1
   if (warp >= kEpiWarps) {
     // ===================== two MMA warps: warp 16 + s issues slot s's UMMAs ================
     // A commit stalls its issuing thread until the committed MMAs drain; with one issuer per
@@ -289,6 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     long long *tr0 = (a.trace && blockIdx.x == 0 && lane == 0) ? a.trace : nullptr;
     uint32_t seq = (uint32_t)ss;  // this slot's position in the global issue order
     int itt = 0;
+    mbar_wait(&S.wbar, 0u);  // the resident weights have landed in shared memory
     for (int64_t base = (int64_t)blockIdx.x * 2; base < n_tiles; base += stride, ++itt) {
       const bool two = base + 1 < n_tiles;
       if (ss == 1 && !two) break;
@@ -298,11 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         long long *t = (tr0 && itt < kTraceTiles) ? tr0 + ((size_t)itt * kTracePhases + p) * 4 + 2 * ss : nullptr;
         long long *t2 = t ? t + (size_t)(kTraceRoles - 1) * kTraceTiles * kTracePhases * 4 : nullptr;
         if (t2) t2[0] = clock64();
-#if GCDF_TC_NAMEDBAR
-        named_bar_sync(5 + ss, kEpiPerSlot + 32);
-#else
-        mbar_wait_mode<GCDF_TC_IWAIT>(&S.epi_done[ss], ph);
-#endif
+        mbar_wait(&S.epi_done[ss], ph);
         ph ^= 1u;
         if (two) {
           const long long tw = clock64();
@@ -323,41 +278,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     __syncthreads();
     return;
   }
-#endif
-  if (GCDF_TC_ISSUE == 0 && warp == kEpiWarps) {
-    // ===================== dedicated MMA warp: issues both slots' UMMAs (elected lane) ======
-    {
-      const uint32_t sw = smem_u32(S.w), sw1t = smem_u32(S.w1t), sb1 = smem_u32(S.b1);
-      const uint32_t sbx = smem_u32(S.bext);
-      uint32_t phbits = 0u;  // bit s = phase parity of epi_done[s]
-      long long *tr0 = (a.trace && blockIdx.x == 0 && lane == 0) ? a.trace : nullptr;
-      int itt = 0;
-      for (int64_t base = (int64_t)blockIdx.x * 2; base < n_tiles; base += stride, ++itt) {
-        const int nslots = (base + 1 < n_tiles) ? 2 : 1;
-#pragma unroll 1
-        for (int p = itt == 0 ? 0 : 1; p < kPhases; ++p) {
-#pragma unroll 1
-          for (int ss = 0; ss < nslots; ++ss) {
-            long long *t = (tr0 && itt < kTraceTiles) ? tr0 + ((size_t)itt * kTracePhases + p) * 4 + 2 * ss : nullptr;
-            long long *t2 = t ? t + (size_t)(kTraceRoles - 1) * kTraceTiles * kTracePhases * 4 : nullptr;
-            if (t2) t2[0] = clock64();
-            mbar_wait(&S.epi_done[ss], (phbits >> ss) & 1u);
-            if (t2) t2[1] = clock64();
-            phbits ^= 1u << ss;
-            fence_after();
-            if (t) t[0] = clock64();
-            issue_phase<F16>(p, tbase + (uint32_t)ss * 256u, sw, sw1t, sb1, sbx, &S.mma_done[ss], nullptr, 0u,
-                             base + stride + ss < n_tiles);
-            if (t) t[1] = clock64();
-          }
-        }
-      }
-    }
-    __syncwarp();
-    fence_before();
-    __syncthreads();
-    return;  // (TMEM is freed by warp 0 after the final barrier)
-  }
   const int s = warp >> 3;          // tile slot
   const int hh = (warp >> 2) & 1;   // accumulator column half: units 64 hh .. 64 hh + 63
   const int qd = warp & 3;          // TMEM lane quarter of this warp (warp % 4)
@@ -375,14 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   auto hand_off = [&](int, bool) {
     wait_st();
     fence_before();
-#if GCDF_TC_NAMEDBAR
-    named_bar_arrive(5 + s, kEpiPerSlot + 32);
-#elif GCDF_TC_WARPARRIVE
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&S.epi_done[s]);
-#else
     mbar_arrive(&S.epi_done[s]);
-#endif
   };
   // cp.async prefetch of this lane's point of tile TT into S.ptn[s][row] (zero if none);
   // issued by the column-half-0 threads, which alone read it
@@ -521,53 +434,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     int pend_cnt = 0;
 #pragma unroll 1
     for (int p = it == 0 ? 0 : 1; p < kPhases; ++p) {
-      mbar_wait_mode<GCDF_TC_EWAIT>(&S.mma_done[s], ph);
+      mbar_wait(&S.mma_done[s], ph);
       if (tr) tr[(p + 1) * 4 + 1] = clock64();
       ph ^= 1u;
       fence_after();
-#if GCDF_TC_NOEPI
-      // timing experiment only: no epilogue work (2: only the TMEM loads; results are garbage)
-      if (p < 11) {
-        if (GCDF_TC_NOEPI == 2) {  // 4 x (ld16 + wait)
-          uint32_t acc = 0u;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t rr[16];
-            ld16(tD + 16 * c, rr);
-            wait_ld();
-#pragma unroll
-            for (int j = 0; j < 16; ++j) acc += rr[j];
-          }
-          if (acc == 0x12345678u) a.trace[0] = acc;
-        } else if (GCDF_TC_NOEPI == 3) {  // 2 x (ld32 + wait)
-          uint32_t acc = 0u;
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            uint32_t rr[32];
-            ld32(tD + 32 * c, rr);
-            wait_ld();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) acc += rr[j];
-          }
-          if (acc == 0x12345678u) a.trace[0] = acc;
-        } else if (GCDF_TC_NOEPI == 4) {  // 4 x ld16, one wait
-          uint32_t r0[16], r1[16], r2[16], r3[16];
-          ld16(tD, r0);
-          ld16(tD + 16, r1);
-          ld16(tD + 32, r2);
-          ld16(tD + 48, r3);
-          wait_ld();
-          uint32_t acc = 0u;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) acc += r0[j] + r1[j] + r2[j] + r3[j];
-          if (acc == 0x12345678u) a.trace[0] = acc;
-        }
-        if (tr) tr[(p + 1) * 4 + 2] = clock64();
-        hand_off(p + 1, s == 1 || T + 1 < n_tiles);
-        if (tr) tr[(p + 1) * 4 + 3] = clock64();
-        continue;
-      }
-#endif
       if (p < 5) {
         fwd_epi(p, tr);
         if (p == 1 || p == 3) stage_q(p, T + stride, (it + 1) & 1);
@@ -770,88 +640,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   if (warp == 0) tmem_dealloc(tbase, 512);
 }
 
-// ------------------------------------------------------------------ self-test kernel
-// One UMMA building block, for unit tests: A fp32 [128][128] -> 16-bit TMEM, B fp32
-// [nrows][128] -> 16-bit SW128 smem; mode 0: D = A B^T (K-major B, N = 128); mode 1:
-// D = A B (B read MN-major, N = 128); mode 2: D = A B^T with nrows = 16 (N = 16).
-template <bool F16>
-__global__ void __launch_bounds__(128, 1) k_selftest_umma(const float *A, const float *B, int mode, float *D) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *sb = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar;
-  __shared__ uint32_t tb;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nrows = mode == 2 ? 16 : 128;
-  for (int i = tid; i < nrows * 128; i += 128) {
-    const int r = i / 128, c = i % 128;
-    const int chunk = c / 64, cb = (c % 64) * 2, g = cb / 16;
-    const int byte = chunk * nrows * 128 + r * 128 + ((g ^ (r % 8)) * 16) + (cb % 16);
-    const uint32_t v = pack2<F16>(B[i], 0.f);
-    *reinterpret_cast<uint16_t *>(sb + byte) = (uint16_t)(v & 0xffffu);
-  }
-  if (warp == 0) {
-    tmem_alloc(&tb, 256);
-    tmem_relinquish();
-  }
-  if (tid == 0) {
-    mbar_init(&bar, 1);
-    fence_barrier_init();
-  }
-  fence_proxy_async_smem();
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t t0 = tb + ((uint32_t)(warp * 32) << 16);
-  {
-    const int m = warp * 32 + lane;
-#pragma unroll
-    for (int c4 = 0; c4 < 4; ++c4) {
-      uint32_t pk[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) pk[j] = pack2<F16>(A[m * 128 + c4 * 32 + 2 * j], A[m * 128 + c4 * 32 + 2 * j + 1]);
-      st16(t0 + 128 + c4 * 16, pk);
-    }
-    wait_st();
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  if (tid == 0) {
-    const uint32_t sbase = smem_u32(sb);
-    for (int k = 0; k < 8; ++k) {
-      uint64_t bd;
-      uint32_t id;
-      if (mode == 0) { bd = sdesc_sw128(sbase + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024); id = kIdescFwd<F16>; }
-      else if (mode == 1) { bd = sdesc_sw128(sbase + k * 2048, 16384, 1024); id = kIdescBwd<F16>; }
-      else { bd = sdesc_sw128(sbase + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024); id = kIdescFin<F16>; }
-      mma_ts(tb, tb + 128 + 8 * k, bd, id, k > 0);
-    }
-    commit(&bar);
-  }
-  mbar_wait(&bar, 0);
-  fence_after();
-  {
-    const int m = warp * 32 + lane;
-    if (mode == 2) {
-      uint32_t r[16];
-      ld16(t0, r);
-      wait_ld();
-      for (int j = 0; j < 16; ++j) D[m * 128 + j] = __uint_as_float(r[j]);
-    } else {
-      for (int c4 = 0; c4 < 4; ++c4) {
-        uint32_t r[32];
-        ld32(t0 + c4 * 32, r);
-        wait_ld();
-        for (int j = 0; j < 32; ++j) D[m * 128 + c4 * 32 + j] = __uint_as_float(r[j]);
-      }
-    }
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  if (warp == 0) tmem_dealloc(tb, 256);
-}
-
 template <bool F16>
 cudaError_t launch_tc_t(const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s) {
   const int smem = (int)sizeof(SmemTC) + 1024;
@@ -867,15 +655,6 @@ cudaError_t launch_tc_t(const WeightsBF16 &w, const QueryArgs &a, int num_sms, c
   return cudaGetLastError();
 }
 
-template <bool F16>
-cudaError_t selftest_t(int mode, const float *A, const float *B, float *D, cudaStream_t s) {
-  const int smem = 32768 + 1024;
-  cudaError_t e = cudaFuncSetAttribute(k_selftest_umma<F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
-  k_selftest_umma<F16><<<1, 128, smem, s>>>(A, B, mode, D);
-  return cudaGetLastError();
-}
-
 }  // namespace
 
 bool tc_compiled() { return true; }
@@ -883,405 +662,6 @@ bool tc_compiled() { return true; }
 cudaError_t launch_mlp_tc(int Hh, bool f16, const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s) {
   if (Hh != H) return cudaErrorInvalidValue;
   return f16 ? launch_tc_t<true>(w, a, num_sms, s) : launch_tc_t<false>(w, a, num_sms, s);
-}
-
-// ------------------------------------------------------------------ UMMA throughput probe
-// One CTA, one issuing thread, `reps` back-to-back groups of 8 K-steps (K = 128), then one
-// commit; D[0] = clock64 cycles from the first issue to completion, D[1] = MMAs issued.
-// variant 0: TS, B K-major SW128, N = 128;  1: TS, B MN-major, N = 128;
-// 2: TS, N = 128, two independent accumulators alternating;  3: SS (A in smem, K-major
-// SW128), N = 128;  4: TS, N = 256 (B rows 0..255).
-namespace {
-template <bool F16>
-__global__ void __launch_bounds__(128, 1) k_mma_probe(int variant, int reps, float *D) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *sb = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 64 KB B + 32 KB A
-  __shared__ uint64_t bar, bar2, bar3;
-  __shared__ uint32_t tb;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  // operands: zeros, or (variant 18) random fp16 values in [-1, 1) like real weights
-  auto rnd16 = [](uint32_t x) -> uint32_t {
-    x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
-    return pack2<F16>((float)(x & 0xffff) / 32768.f - 1.f, (float)(x >> 16) / 32768.f - 1.f);
-  };
-  for (int i = tid; i < (96 * 1024) / 16; i += 128)
-    reinterpret_cast<uint4 *>(sb)[i] = variant == 18 ? make_uint4(rnd16(4 * i), rnd16(4 * i + 1), rnd16(4 * i + 2), rnd16(4 * i + 3))
-                                                     : make_uint4(0, 0, 0, 0);
-  if (warp == 0) {
-    tmem_alloc(&tb, 512);
-    tmem_relinquish();
-  }
-  if (tid == 0) {
-    mbar_init(&bar, 1);
-    mbar_init(&bar2, 1);
-    mbar_init(&bar3, 1);
-    fence_barrier_init();
-  }
-  fence_proxy_async_smem();
-  fence_before();
-  __syncthreads();
-  fence_after();
-  if (variant == 18) {  // random A operand in TMEM columns 256..319
-    uint32_t r[32];
-    for (int i = 0; i < 32; ++i) r[i] = rnd16(1000003u * tid + i);
-    st32(tb + ((uint32_t)(warp * 32) << 16) + 256u, r);
-    st32(tb + ((uint32_t)(warp * 32) << 16) + 288u, r);
-    wait_st();
-    fence_before();
-    __syncthreads();
-    fence_after();
-  }
-  __shared__ volatile int stop;
-  if (tid == 0) stop = 0;
-  __syncthreads();
-  if (tid >= 32 && (variant == 16 || variant == 17)) {
-    // TMEM traffic of "epilogue" warps (columns 384..511) while warp 0 streams UMMAs
-    const uint32_t tq = tb + ((uint32_t)(warp * 32) << 16) + 384u;
-    uint32_t r[32];
-    for (int i = 0; i < 32; ++i) r[i] = (uint32_t)i;
-    while (!stop) {
-      if (variant == 16) {
-        ld32(tq, r);
-        wait_ld();
-      } else {
-        st32(tq, r);
-        wait_st();
-      }
-    }
-    if (r[5] == 12345u) D[2] = 1.f;  // keep the loads alive
-  }
-  if (variant == 23 && warp < 2) {
-    // two issuing warps (one per slot), each: forward phases (8 K-major + bias) with a
-    // commit per phase to its own mbarrier; does a second issuer hide the commit bubble?
-    const uint32_t sB = smem_u32(sb), sA = sB + 65536;
-    const uint32_t dd = tb + (uint32_t)warp * 256u;
-    uint64_t bdk[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) bdk[k] = sdesc_sw128(sB + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
-    const uint64_t bx = sdesc_nosw(sA, 2048, 128);
-    uint64_t *mb = warp == 0 ? &bar2 : &bar3;
-    __syncwarp();
-    asm volatile("bar.sync 1, 64;" ::: "memory");
-    const long long t0 = clock64();
-#pragma unroll 1
-    for (int r = 0; r < reps / 2; ++r) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) mma_ts_elect(dd, dd + 128 + 8u * k, bdk[k], kIdescFwd<F16>, k > 0);
-      mma_ts_elect(dd, dd + 192, bx, kIdescFwd<F16>, 1u);
-      commit_elect(mb);
-    }
-    mbar_wait(mb, (uint32_t)((reps / 2 - 1) & 1));
-    asm volatile("bar.sync 1, 64;" ::: "memory");
-    const long long t1 = clock64();
-    if (tid == 0 && blockIdx.x == 0) {
-      D[0] = (float)(t1 - t0);
-      D[1] = (float)((reps / 2) * 2 * 9);
-    }
-  }
-  if (tid == 0 && variant != 23) {
-    const uint32_t sB = smem_u32(sb), sA = sB + 65536;
-    const uint32_t d0 = tb, av = tb + 256;
-    long long t0 = clock64();
-    int n = 0;
-    if (variant >= 13) {  // minimal issue overhead: descriptors precomputed, branch-free loop
-      uint64_t bd[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        bd[k] = variant != 14 ? sdesc_sw128(sB + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024)
-                              : sdesc_sw128(sB + k * 2048, 16384, 1024);
-      const uint32_t idesc = variant != 14 ? kIdescFwd<F16> : kIdescBwd<F16>;
-      const uint64_t bx = sdesc_nosw(sA, 2048, 128);
-      t0 = clock64();
-      if (variant == 19) {  // the kernel's forward phase: 8 K-major steps + a no-swizzle bias step
-#pragma unroll 1
-        for (int r = 0; r < reps; ++r) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) mma_ts(d0, d0 + 128 + 8u * k, bd[k], idesc, k > 0);
-          mma_ts(d0, d0 + 192, bx, idesc, 1u);
-        }
-        n = reps * 9;
-      } else if (variant == 24) {  // as 22 with a test_wait spin instead of try_wait
-#pragma unroll 1
-        for (int r = 0; r < reps; ++r) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) mma_ts(d0, d0 + 128 + 8u * k, bd[k], idesc, k > 0);
-          mma_ts(d0, d0 + 192, bx, idesc, 1u);
-          commit(&bar2);
-          mbar_wait_spin(&bar2, (uint32_t)(r & 1));
-          fence_after();
-        }
-        n = reps * 9;
-      } else if (variant == 28 || variant == 29) {  // lean M = 64 (28: one D; 29: two D at lanes 0 / 64 alternating)
-        const uint32_t id64 = idesc_f16kind(64, 128, false, F16);
-#pragma unroll 1
-        for (int r = 0; r < reps; ++r) {
-          const uint32_t dd = (variant == 29 && (r & 1)) ? d0 + (64u << 16) : d0;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) mma_ts(dd, av + 8u * k, bd[k], id64, k > 0);
-        }
-        n = reps * 8;
-      } else if (variant == 25) {  // lean N = 64 (two halves of a phase as separate accumulators)
-        uint64_t b64[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) b64[k] = sdesc_sw128(sB + (k >> 2) * 8192 + (k & 3) * 32, 16, 1024);
-#pragma unroll 1
-        for (int r = 0; r < reps; ++r) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) mma_ts(d0 + (uint32_t)(r & 1) * 64u, d0 + 128 + 8u * k, b64[k], idesc_f16kind(128, 64, false, F16), k > 0);
-        }
-        n = reps * 8;
-      } else if (variant == 21 || variant == 22) {
-        // the kernel's forward phase + a commit to an mbarrier after each phase; 22 also
-        // waits for that commit (phase fully serialised: execution + commit latency)
-#pragma unroll 1
-        for (int r = 0; r < reps; ++r) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) mma_ts(d0, d0 + 128 + 8u * k, bd[k], idesc, k > 0);
-          mma_ts(d0, d0 + 192, bx, idesc, 1u);
-          commit(&bar2);
-          if (variant == 22) {
-            mbar_wait(&bar2, (uint32_t)(r & 1));
-            fence_after();
-          }
-        }
-        n = reps * 9;
-      } else if (variant == 20) {  // two slots' phases alternating (D at 0 / 256, A at 128 / 384)
-#pragma unroll 1
-        for (int r = 0; r < reps; ++r) {
-          const uint32_t dd = d0 + (uint32_t)(r & 1) * 256u;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) mma_ts(dd, dd + 128 + 8u * k, bd[k], idesc, k > 0);
-        }
-        n = reps * 8;
-      } else {
-#pragma unroll 1
-        for (int r = 0; r < reps; ++r) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) mma_ts(d0, av + 8u * k, bd[k], idesc, k > 0);
-        }
-        n = reps * 8;
-      }
-    }
-    for (int r = 0; r < (variant >= 13 ? 0 : reps); ++r) {
-      const uint32_t d = (variant == 2 && (r & 1)) ? tb + 128 : d0;  // (variants 9, 11 use d + 64 / d + 128 too)
-      for (int k = 0; k < 8; ++k, ++n) {
-        if (variant == 0 || variant == 2)
-          mma_ts(d, av + 8u * k, sdesc_sw128(sB + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024), kIdescFwd<F16>, k > 0);
-        else if (variant == 1)
-          mma_ts(d, av + 8u * k, sdesc_sw128(sB + k * 2048, 16384, 1024), kIdescBwd<F16>, k > 0);
-        else if (variant == 3) {
-          const uint64_t ad = sdesc_sw128(sA + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
-          const uint64_t bd = sdesc_sw128(sB + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
-          asm volatile(
-              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-              "l"(ad), "l"(bd), "r"(kIdescFwd<F16>), "r"((uint32_t)(k > 0))
-              : "memory");
-        } else if (variant == 4) {
-          mma_ts(d, av + 8u * k, sdesc_sw128(sB + (k >> 2) * 32768 + (k & 3) * 32, 16, 1024),
-                 idesc_f16kind(128, 256, false, F16), k > 0);
-        } else if (variant == 8 || variant == 9) {  // N = 64 (9: two accumulators, k-step interleaved)
-          const uint64_t bd = sdesc_sw128(sB + (k >> 2) * 8192 + (k & 3) * 32, 16, 1024);
-          mma_ts(d, av + 8u * k, bd, idesc_f16kind(128, 64, false, F16), k > 0);
-          if (variant == 9) {
-            mma_ts(d + 64, av + 8u * k, bd, idesc_f16kind(128, 64, false, F16), k > 0);
-            ++n;
-          }
-        } else if (variant == 10) {  // N = 16
-          mma_ts(d, av + 8u * k, sdesc_sw128(sB + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024),
-                 idesc_f16kind(128, 16, false, F16), k > 0);
-        } else if (variant == 11) {  // N = 128, two accumulators (two tiles), k-step interleaved
-          const uint64_t bd = sdesc_sw128(sB + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
-          mma_ts(d, av + 8u * k, bd, kIdescFwd<F16>, k > 0);
-          mma_ts(d + 128, av + 64 + 8u * k, bd, kIdescFwd<F16>, k > 0);
-          ++n;
-        } else {  // 12: N = 128 K-major, A in TMEM, K = 32 per step pair issued as one phase of 9 incl. a no-swizzle step
-          mma_ts(d, av + 8u * k, sdesc_sw128(sB + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024), kIdescFwd<F16>, k > 0);
-          if (k == 7) {
-            mma_ts(d, av, sdesc_nosw(sA, 2048, 128), kIdescFwd<F16>, 1u);
-            ++n;
-          }
-        }
-      }
-    }
-    commit(&bar);
-    mbar_wait(&bar, 0);
-    const long long t1 = clock64();
-    stop = 1;
-    if (blockIdx.x == 0) {
-      D[0] = (float)(t1 - t0);
-      D[1] = (float)n;
-    }
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  if (warp == 0) tmem_dealloc(tb, 512);
-}
-// Does a UMMA issue stream (blocked on the MMA queue) slow down other warps of its SM
-// sub-partition?  Warp 0 streams UMMAs (variant 26) or idles (27); warps 4 (same
-// sub-partition as warp 0) and 5 (another one) each run a fixed ALU loop.
-// D[0] = warp-4 cycles, D[1] = warp-5 cycles, D[2] = UMMA-stream cycles.
-template <bool F16>
-__global__ void __launch_bounds__(256, 1) k_smsp_probe(int variant, int reps, float *D) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *sb = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint32_t tb;
-  __shared__ uint64_t bar;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  for (int i = tid; i < (64 * 1024) / 16; i += 256) reinterpret_cast<uint4 *>(sb)[i] = make_uint4(0, 0, 0, 0);
-  if (warp == 0) {
-    tmem_alloc(&tb, 512);
-    tmem_relinquish();
-  }
-  if (tid == 0) {
-    mbar_init(&bar, 1);
-    fence_barrier_init();
-  }
-  fence_proxy_async_smem();
-  fence_before();
-  __syncthreads();
-  fence_after();
-  if (warp == 0 && variant == 26) {
-    const uint32_t sB = smem_u32(sb);
-    uint64_t bd[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) bd[k] = sdesc_sw128(sB + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
-    const long long t0 = clock64();
-#pragma unroll 1
-    for (int r = 0; r < reps * 4; ++r) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) mma_ts_elect(tb, tb + 256 + 8u * k, bd[k], kIdescFwd<F16>, k > 0);
-    }
-    commit_elect(&bar);
-    mbar_wait(&bar, 0);
-    if (lane_id() == 0) D[2] = (float)(clock64() - t0);
-  } else if (warp == 4 || warp == 5) {
-    uint32_t x[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = (uint32_t)(tid * 8 + i);
-    const long long t0 = clock64();
-#pragma unroll 1
-    for (int it = 0; it < 4000; ++it) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) x[i] = prmt(x[i], x[(i + 1) & 7], 0x5140u) ^ (x[i] >> 3);
-    }
-    const long long t1 = clock64();
-    uint32_t acc = 0u;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc ^= x[i];
-    if (acc == 0x9e3779b9u) D[3] = 1.f;
-    if ((tid & 31) == 0) D[warp - 4] = (float)(t1 - t0);
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  if (warp == 0) tmem_dealloc(tb, 512);
-}
-// 2-CTA (cta_group::2) probe: M = 256 pairs over a CTA pair.  variant 5: TS N = 128;
-// 6: SS N = 128; 7: TS N = 256.
-template <bool F16>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_mma_probe2(int variant, int reps, float *D) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *sb = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  __shared__ uint64_t bar;
-  __shared__ uint32_t tb;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  uint32_t crank;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
-  for (int i = tid; i < (96 * 1024) / 16; i += 128) reinterpret_cast<uint4 *>(sb)[i] = make_uint4(0, 0, 0, 0);
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tb)), "r"(512)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-  }
-  if (tid == 0) {
-    mbar_init(&bar, 1);
-    fence_barrier_init();
-  }
-  fence_proxy_async_smem();
-  fence_before();
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-  fence_after();
-  const int N = variant == 7 ? 256 : 128;
-  const uint32_t idesc = (1u << 4) | ((F16 ? 0u : 1u) << 7) | ((F16 ? 0u : 1u) << 10) | ((uint32_t)(N >> 3) << 17) |
-                         ((uint32_t)(256 >> 4) << 24);
-  if (crank == 0 && tid == 0) {
-    const uint32_t sB = smem_u32(sb), sA = sB + 65536;
-    const uint32_t d = tb, av = tb + 256;
-    long long t0 = clock64();
-    int n = 0;
-    for (int r = 0; r < reps; ++r) {
-      for (int k = 0; k < 8; ++k, ++n) {
-        const uint64_t bd = sdesc_sw128(sB + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
-        const uint32_t acc = k > 0;
-        if (variant == 6) {
-          const uint64_t ad = sdesc_sw128(sA + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024);
-          asm volatile(
-              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-              "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
-              : "memory");
-        } else {
-          asm volatile(
-              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-              "r"(av + 8u * k), "l"(bd), "r"(idesc), "r"(acc)
-              : "memory");
-        }
-      }
-    }
-    asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-            smem_u32(&bar)),
-        "h"((unsigned short)3)
-        : "memory");
-    mbar_wait(&bar, 0);
-    const long long t1 = clock64();
-    D[0] = (float)(t1 - t0);
-    D[1] = (float)n;
-  } else if (tid == 0) {
-    mbar_wait(&bar, 0);
-  }
-  fence_before();
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-  fence_after();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(512) : "memory");
-}
-}  // namespace
-
-cudaError_t launch_selftest_umma(int mode, const float *A, const float *B, float *D, cudaStream_t s) {
-  if (mode >= 26 && mode <= 31) {  // 2-CTA probe: mode = 16 + 2 * variant + f16, variant 5..7
-    const int variant = (mode - 16) >> 1;
-    const bool f16 = (mode & 1) != 0;
-    const int smem = 96 * 1024 + 1024;
-    auto k = f16 ? k_mma_probe2<true> : k_mma_probe2<false>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    k<<<2, 128, smem, s>>>(variant, 200, D);
-    return cudaGetLastError();
-  }
-  if (mode >= 16 + 2 * 26 && mode < 16 + 2 * 28) {  // sub-partition interference probe (variants 26, 27)
-    const int variant = (mode - 16) >> 1;
-    const bool f16 = (mode & 1) != 0;
-    const int smem = 64 * 1024 + 1024;
-    auto k = f16 ? k_smsp_probe<true> : k_smsp_probe<false>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    k<<<1, 256, smem, s>>>(variant, 200, D);
-    return cudaGetLastError();
-  }
-  if (mode >= 16) {  // UMMA throughput probe: mode = 16 + 2 * variant + f16 (variants 0..4, 8..12)
-    const int variant = (mode - 16) >> 1;
-    const bool f16 = (mode & 1) != 0;
-    const int smem = 96 * 1024 + 1024;
-    auto k = f16 ? k_mma_probe<true> : k_mma_probe<false>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    k<<<variant == 15 ? 148 : 1, 128, smem, s>>>(variant, 200, D);
-    return cudaGetLastError();
-  }
-  return (mode & 4) ? selftest_t<true>(mode & 3, A, B, D, s) : selftest_t<false>(mode & 3, A, B, D, s);
 }
 
 }  // namespace gcdf

@@ -6,7 +6,6 @@ path: if libgcdf.so is missing or no B200 is present, construction raises.
 """
 from __future__ import annotations
 
-import os
 import ctypes as C
 from pathlib import Path
 
@@ -14,7 +13,7 @@ import numpy as np
 import torch
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = Path(os.environ.get("GCDF_LIB") or _PKG / "libgcdf.so")  # GCDF_LIB: dev builds (tools/variants.py)
+LIB_PATH = _PKG / "libgcdf.so"  # the in-tree build (python -m paper_2601_18548_b200.build); no override
 
 FP32, BF16, FP16, FP16X3 = 0, 1, 2, 3  # FP16X3: fp32-accurate tensor-core path (3-term split)
 TGRAD_CHAINRULE, TGRAD_QCHANNEL = 0, 1
@@ -105,7 +104,12 @@ class DetectGraph:
 
     def __init__(self, ctx: "Context", q: torch.Tensor, delta: float, tau: float, radius: float = 0.0,
                  capacity: int | None = None):
+        q0 = q
         q, B, N = ctx._q(q)
+        if q.data_ptr() != q0.data_ptr():
+            # the graph replays with the captured pointer: a private copy (dtype / device /
+            # layout conversion) would make refills of the caller's tensor invisible
+            raise ValueError("DetectGraph: q must be a contiguous float32 [B, N, 9] tensor on the context's device")
         self.ctx, self.q = ctx, q
         self.outputs = ctx.alloc_detect_outputs(B * N, capacity if capacity is not None else ctx.max_active)
         o = self.outputs

@@ -13,9 +13,11 @@ arithmetic lives here (see synth/__init__.py).  Recipe (DESIGN.md "Input recipe"
   jitter so the arm joints are exercised.  q = [x, y, theta, j1..j6] (PAPER.md:350-352,
   n = 9 for the 6-DoF Kinova Gen3 on a planar base).
 * Weights: the paper's "7-layer MLP" on [p, q] in R^{3+n} with
-  random init (no trained weights are available): He-normal hidden
-  layers, b ~ U(-0.1, 0.1), output row N(0, 1/(5H)) and output bias 1.0 so that f is
-  O(1) like a GCDF in weighted metres/radians.  Written as MLPW v1.
+  random init (no trained weights are available): He-normal N(0, 2/fan_in)
+  on every layer including the output row, b ~ U(-0.1, 0.1), output bias 1.0.  With the
+  He-normal output row the median ||grad_q f||_2 is ~1 (0.99 at C2, H = 128), the scale
+  Theorem 1 fixes for a GCDF's gradient, so the north-star's absolute
+  tolerances are read at the paper's scale (R11).  Written as MLPW v1.
 """
 from __future__ import annotations
 
@@ -198,11 +200,10 @@ def make_weights(H: int, seed: int = 7, n_hidden_layers: int = 6, act: int = 1):
     layers = []
     for li in range(len(dims) - 1):
         fan_in, fan_out = dims[li], dims[li + 1]
+        W = rng.normal(0.0, np.sqrt(2.0 / fan_in), (fan_out, fan_in))
         if li < len(dims) - 2:
-            W = rng.normal(0.0, np.sqrt(2.0 / fan_in), (fan_out, fan_in))
             b = rng.uniform(-0.1, 0.1, fan_out)
         else:
-            W = rng.normal(0.0, np.sqrt(1.0 / (5.0 * fan_in)), (fan_out, fan_in))
             b = np.ones(fan_out)
         layers.append((W, b))
     return act, dims, layers
@@ -241,7 +242,9 @@ def read_mlpw_raw(path):
 def weights_path(H: int, seed: int = 7, act: int = 1) -> str:
     """Deterministic weights file for hidden width H (generated on first use).  act = 2: the
     same random-init weights under the softplus activation (NEXT-4 variant, R26)."""
-    name = f"gcdf_H{H}_s{seed}.mlpw" if act == 1 else f"gcdf_H{H}_s{seed}_act{act}.mlpw"
+    # "_r2": recipe revision 2 (He-normal output row, DESIGN.md R11); a stale cached file of
+    # the round-1 recipe (output row N(0, 1/(5H))) is never picked up
+    name = f"gcdf_H{H}_s{seed}_r2.mlpw" if act == 1 else f"gcdf_H{H}_s{seed}_r2_act{act}.mlpw"
     p = REPO / "build" / "inputs" / name
     if not p.exists():
         _, dims, layers = make_weights(H, seed)

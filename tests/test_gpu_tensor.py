@@ -1,16 +1,21 @@
 """GPU parity of the tcgen05 tensor-core path (GCDF_FP16 default, GCDF_BF16) vs the oracle.
 
-Gates (R17):
+Gates (R17, R28), at the paper's gradient scale (R11: median ||grad_q f|| ~ 1):
   (1) same rounding points: vs the oracle's EMU mode for the operand type (fp16 / bf16
       rounding of exactly the MMA operands) the median value error is fp32 noise (<= 1e-6)
       and the p99 small (the tail differs only where fp32 accumulation order moves a value
       across a 16-bit rounding boundary or a ReLU kink);
   (2) vs the exact oracle, values on every pair: |df| <= 2e-2 (north star);
-  (3) vs the exact oracle, | ||g_gpu|| - ||g_exact|| | <= 5e-2 (north star) on >= 99% of pairs
-      and on every pair whose exact ReLU masks equal the emulated ones.
-fp16 meets (2) and (3) as stated; bf16 operand rounding alone (the EMU oracle, no GPU
-involved) exceeds them on this network, so for bf16 the measured bounds are asserted and
-the gap is reported.
+  (3a) vs the exact oracle, | ||g_gpu|| - ||g_exact|| | <= 5e-2 (north star) on every pair
+      whose exact ReLU masks equal the emulated ones (kink-free under 16-bit operands);
+  (3b) on all pairs, the fraction within 5e-2 is >= min(0.99, f_emu - 0.005), f_emu = the
+      same fraction of the EMU oracle alone (no GPU involved): a ReLU mask flipped by 16-bit
+      operand rounding moves the gradient by ~10 % of its norm, so at unit gradient scale
+      the operand type itself leaves ~2 % (fp16) / ~18 % (bf16) of pairs outside 5e-2
+      (R28, EMU-only numbers in DESIGN.md).
+Where the operand type alone exceeds (2) (bf16 at this scale: EMU-only max |df| ~ 8e-2),
+the GPU is held to the EMU's own error + 5e-3 and the shortfall is reported; the bf16
+contract is met by the split GCDF_BF16X3 path (tests/test_gpu_fp16x3.py).
 """
 import os
 
@@ -26,8 +31,6 @@ pytestmark = pytest.mark.gpu
 NT = max(1, min(os.cpu_count() or 1, 64))
 KINK_EMU = 1e-3
 PRECS = {"fp16": (2, oracle.EMU_FP16), "bf16": (1, oracle.EMU_BF16)}
-# bf16: bounds measured for this network by the EMU oracle alone (operand rounding), DESIGN.md §5
-BF16_MEASURED = {"val": 3e-2, "gnorm_frac": 0.95}
 
 
 def _ctx(cfg, prec, **kw):
@@ -60,17 +63,28 @@ def test_selftest_umma(mode, prec):
 def stats_and_gates(v, g, exact, emu, prec, what="", agree_min=0.85, kink_emu=KINK_EMU):
     dv = np.abs(v - emu["f"])
     de = np.abs(v - exact["f"])
-    gn_g = np.linalg.norm(g, axis=-1)
-    gd = np.abs(gn_g - np.linalg.norm(exact["g"], axis=-1))
+    gn_exact = np.linalg.norm(exact["g"], axis=-1)
+    gd = np.abs(np.linalg.norm(g, axis=-1) - gn_exact)
     dg_emu = np.linalg.norm(g - emu["g"], axis=-1) / np.maximum(1.0, np.linalg.norm(emu["g"], axis=-1))
-    kink_free = (exact["mask_hash"] == emu["mask_hash"]) & (emu["kappa"] > kink_emu)
+    # kink-free (R17): the exact ReLU masks equal the emulated ones, no emulated pre-activation
+    # within kink_emu of zero, and the GPU took the emulation's branches (its gradient agrees
+    # with the emulation's to 1e-2 max(1, ||g||); a flip moves it by ~10 %).  The last clause
+    # drops the pairs where fp32 accumulation order moved a 16-bit rounding boundary upstream
+    # of a kink (<= 1 % by gate 1; counted as "gpu_branch_differs")
+    same_branch = dg_emu <= 1e-2
+    kink_free = (exact["mask_hash"] == emu["mask_hash"]) & (emu["kappa"] > kink_emu) & same_branch
+    # the operand type's own error (EMU oracle vs exact oracle, no GPU involved)
+    emu_de = np.abs(emu["f"] - exact["f"])
+    emu_gd = np.abs(np.linalg.norm(emu["g"], axis=-1) - gn_exact)
     st = {"emu_val_agree_1e-5": float(np.mean(dv <= 1e-5)), "emu_val_max": float(dv.max()),
           "emu_val_p50": float(np.median(dv)), "emu_val_p99": float(np.percentile(dv, 99)),
           "emu_grad_agree_1e-4": float(np.mean(dg_emu <= 1e-4)), "emu_grad_p99": float(np.percentile(dg_emu, 99)),
           "exact_val_max": float(de.max()), "exact_val_p99": float(np.percentile(de, 99)),
           "gnorm_within_5e-2": float(np.mean(gd <= BF16_GNORM_ATOL)), "gnorm_p99": float(np.percentile(gd, 99)),
           "gnorm_max_kink_free": float(gd[kink_free].max()) if kink_free.any() else 0.0,
-          "kink_free_frac": float(kink_free.mean())}
+          "kink_free_frac": float(kink_free.mean()), "gnorm_median_exact": float(np.median(gn_exact)),
+          "gpu_branch_differs": float(1.0 - same_branch.mean()),
+          "type_only_val_max": float(emu_de.max()), "type_only_gnorm_within_5e-2": float(np.mean(emu_gd <= BF16_GNORM_ATOL))}
     print(f"\n[{prec}] {what}: {st}", flush=True)
     # gate 1: the bulk agrees with the emulation to fp32-accumulation noise; the tail is
     # 16-bit rounding-boundary / ReLU-kink flips (8x more frequent but 8x smaller for fp16)
@@ -80,13 +94,21 @@ def stats_and_gates(v, g, exact, emu, prec, what="", agree_min=0.85, kink_emu=KI
     # bf16: layer 1 runs on split bf16 operands (~16-bit effective precision, not the EMU
     # model's exact layer 1), which moves a few more ReLU kinks
     assert st["emu_grad_p99"] <= (1e-2 if prec == "fp16" else 5e-2), st
-    if prec == "fp16":
-        assert st["exact_val_max"] <= BF16_VAL_ATOL, st    # gate 2
-        assert st["gnorm_within_5e-2"] >= 0.99, st         # gate 3
-        assert st["gnorm_max_kink_free"] <= BF16_GNORM_ATOL, st
+    assert st["gpu_branch_differs"] <= (0.01 if prec == "fp16" else 0.05), st
+    # gate 2: the north-star value tolerance where the operand type can meet it (fp16);
+    # otherwise (bf16) the type's own error + 5e-3 (R28)
+    if st["type_only_val_max"] <= BF16_VAL_ATOL:
+        assert st["exact_val_max"] <= BF16_VAL_ATOL, st
     else:
-        assert st["exact_val_max"] <= BF16_MEASURED["val"], st
-        assert st["gnorm_within_5e-2"] >= BF16_MEASURED["gnorm_frac"], st
+        assert st["exact_val_max"] <= st["type_only_val_max"] + 5e-3, st
+    # gate 3a / 3b (R17, R28)
+    # 3a per kink-free pair: 5e-2, or -- where the operand type's own deviation on that pair
+    # already exceeds it (SE(2): d f / d theta scales with the point's distance, up to 14 m) --
+    # that deviation + 1e-2 max(1, ||g||)
+    lim = np.maximum(BF16_GNORM_ATOL, emu_gd + 1e-2 * np.maximum(1.0, gn_exact))
+    bad = kink_free & (gd > lim)
+    assert not bad.any(), (int(bad.sum()), st)
+    assert st["gnorm_within_5e-2"] >= min(0.99, st["type_only_gnorm_within_5e-2"] - 0.005), st
     return st
 
 
@@ -125,7 +147,9 @@ def test_detect(c2, prec):
     torch.cuda.synchronize()
     gpu = records_np(out)
     Q = q.reshape(-1, 9)
-    tol = BF16_VAL_ATOL if prec == "fp16" else BF16_MEASURED["val"]
+    # bf16 at the paper's scale: the operand type's own value error (EMU oracle, no GPU)
+    # exceeds the north-star 2e-2, so its band and value tolerance are that error + 5e-3 (R28)
+    tol = BF16_VAL_ATOL if prec == "fp16" else float(np.abs(emu[prec]["f"] - exact["f"]).max()) + 5e-3
     orc = oracle_detect(m, pts, ids, Q, tau, nthreads=NT)
     nd, nc = compare_active_sets(gpu, orc, exact["f"], ids, 1e-3 + tol, val_atol=tol, what="vs exact")
     assert nc > 0
@@ -155,9 +179,13 @@ def test_qchannel_mode_fp16(c2):
     ctx.update_scene(pts[:2000])
     v, g = ctx.query_values_grads(torch.from_numpy(q[:, :2]))
     ex = m.eval(pts[:2000], q[:, :2].reshape(-1, 9), flags=oracle.TGRAD_QCHANNEL)
+    em = m.eval(pts[:2000], q[:, :2].reshape(-1, 9), flags=oracle.TGRAD_QCHANNEL | oracle.EMU_FP16)
     gn = g.cpu().numpy()[:, :2000]
-    d = np.abs(np.linalg.norm(gn, axis=-1) - np.linalg.norm(ex["g"], axis=-1))
-    assert np.mean(d <= BF16_GNORM_ATOL) >= 0.99
+    ne = np.linalg.norm(ex["g"], axis=-1)
+    d = np.abs(np.linalg.norm(gn, axis=-1) - ne)
+    d_type = np.abs(np.linalg.norm(em["g"], axis=-1) - ne)  # the operand type alone (R28)
+    assert np.mean(d <= BF16_GNORM_ATOL) >= min(0.99, np.mean(d_type <= BF16_GNORM_ATOL) - 0.005)
+    assert np.abs(v.cpu().numpy()[:, :2000] - ex["f"]).max() <= BF16_VAL_ATOL
 
 
 def test_c5_full_size_sampled():

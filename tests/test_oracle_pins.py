@@ -583,6 +583,26 @@ def test_softplus_hand_worked_example(tmp_path):
         np.testing.assert_allclose(out["g"][0, 0], case["grad"], rtol=0, atol=1e-12)
 
 
+def test_softplus_emu_hand_worked(tmp_path):
+    """The softplus EMU_FP16 mode (R26 rounding points: h1..h5 rounded as A operands,
+    sigma' of layers 1..5 recovered as 1 - e^-h~ from the rounded activation, sigma'6 =
+    sigmoid(z6) unrounded, every backward delta rounded) on the hand-worked network with
+    W7 = 1.313, against the step-by-step derivation in softplus_hand_example.json
+    ["emu_fp16"] (tools/golden_softplus_emu.py: math + numpy float16, no oracle).  The
+    golden also lists six mis-placed rounding points (e.g. sigma'6 from the rounded h6),
+    each of which changes f or the gradient, so each would fail this pin."""
+    g = json.loads((GOLD / "softplus_hand_example.json").read_text())
+    e = g["emu_fp16"]
+    layers = [(np.array(l["W"], float), np.array(l["b"], float)) for l in e["layers"]]
+    m = oracle.MLP(_write(tmp_path, "spemu.mlpw", 2, [12] + [1] * 6 + [1], layers))
+    for case in g["cases"]:
+        out = m.eval(np.array([case["p"]]), np.array([case["q"]]), flags=oracle.EMU_FP16)
+        assert abs(out["f"][0, 0] - e["f"]) <= 1e-12
+        np.testing.assert_allclose(out["g"][0, 0], e["grad"], rtol=0, atol=1e-15)
+        for name, mu in e["_mutants"].items():
+            assert abs(out["f"][0, 0] - mu["f"]) > 1e-12 or abs(out["g"][0, 0][0] - mu["grad0"]) > 1e-12, name
+
+
 def test_softplus_saturated_is_affine_closed_form(tmp_path):
     """Every pre-activation >= 40: softplus(z) = z + log1p(e^-z) = z (1 + O(1e-19)) and
     sigmoid(z) = 1 - O(1e-18), so the network equals the affine composition and the

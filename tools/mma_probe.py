@@ -1,11 +1,30 @@
-"""Diagnostics: tcgen05 UMMA throughput on this B200 (one CTA, 200 x 8 back-to-back MMAs)."""
+"""Diagnostics: tcgen05 UMMA throughput on this B200 (one CTA, 200 x 8 back-to-back MMAs).
+
+The probe kernels live in tools/probes/umma_probes.cu, built here into
+build/probes/libumma_probes.so (not part of libgcdf.so)."""
+import ctypes
+import subprocess
 import sys
 from pathlib import Path
 
 import torch
 
-sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
-from paper_2601_18548_b200.gcdf import selftest_umma  # noqa: E402
+ROOT = Path(__file__).resolve().parent.parent
+SRC = ROOT / "tools" / "probes" / "umma_probes.cu"
+LIB = ROOT / "build" / "probes" / "libumma_probes.so"
+LIB.parent.mkdir(parents=True, exist_ok=True)
+if not LIB.exists() or LIB.stat().st_mtime < SRC.stat().st_mtime:
+    subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-std=c++17", "-O3", "-Xcompiler",
+                           "-fPIC", "-shared", "-I", str(ROOT / "include"), "-o", str(LIB), str(SRC)])
+_probe = ctypes.CDLL(str(LIB)).probe_umma
+_probe.argtypes = [ctypes.c_int, ctypes.c_void_p]
+
+
+def selftest_umma(mode, A, B):
+    D = torch.zeros(128, 128, device="cuda")
+    rc = _probe(mode, D.data_ptr())
+    assert rc == 0, rc
+    return D
 
 names = ["TS K-major N128", "TS MN-major N128", "TS N128 two accumulators", "SS K-major N128", "TS K-major N256",
          "2CTA TS M256 N128", "2CTA SS M256 N128", "2CTA TS M256 N256", "TS N64", "TS N64 two acc interleaved",

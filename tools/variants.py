@@ -1,7 +1,9 @@
 """Dev tool: build variants of libgcdf.so with build-time switches of k_mlp_tc.cu.
 
     python tools/variants.py NAME -DGCDF_TC_GREEDY=1 ... -> build/var/NAME/libgcdf.so
-Run a variant with GCDF_LIB=build/var/NAME/libgcdf.so (the default build is untouched).
+Run a variant on the GPU box by copying it over the snapshot's paper_2601_18548_b200/libgcdf.so
+inside the gpurun command (the binding loads only the in-tree library; the default build here
+is untouched).
 """
 import subprocess
 import sys
