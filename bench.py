@@ -6,8 +6,10 @@
 One step = one SCO iteration of the hot path (all SURVEY §8(a) rows): an incremental
 scene update (A9: 200 removes + 200 adds on a moved box) followed by the fused
 detect over every (waypoint, live point) pair (A2-A8) with the count read back on the
-host; at N > 1 the points are sharded by rank and the active sets are gathered with
-NCCL + the merge kernel.  `value` counts every (waypoint, live point) pair of the whole
+host; at N > 1 the points are sharded by rank and every rank's detect call returns the
+gathered active set (the library's NCCL all-gather group + merge kernel on the call's
+stream).  `--gpus N` without WORLD_SIZE re-launches itself under torch.distributed.run
+with N ranks; under a launcher WORLD_SIZE must equal --gpus.  `value` counts every (waypoint, live point) pair of the whole
 job per second.  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
@@ -55,7 +57,24 @@ def parse():
                     help="skip the softplus / H = 256 variant measurements (NEXT-4) of the default run")
     ap.add_argument("--latency-calls", type=int, default=50,
                     help="detect-latency sample size (wall time q on device -> count on host); 0 = skip")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "host"],
+                    help="exchange backend at N > 1: nccl (product) or host (TEST backend: gloo all-gather "
+                         "on the host, for the dry run of the N > 1 path on one GPU)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="DRY RUN: every rank on cuda:0 (needs --comm host); the line is marked dry_run")
     return ap.parse_args()
+
+
+def relaunch_under_torchrun(a):
+    """--gpus N > 1 without a launcher: run this script under torch.distributed.run."""
+    import socket
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -176,18 +195,28 @@ def main():
     if a.impl == "reference":
         run_reference(a)
         return
+    if "WORLD_SIZE" not in os.environ and a.gpus > 1:
+        relaunch_under_torchrun(a)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != a.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={world} but --gpus {a.gpus}: launch one rank per GPU "
+                 f"(torchrun --nproc-per-node {a.gpus} bench.py --gpus {a.gpus})")
+    if a.same_device and a.comm != "host":
+        sys.exit("bench.py: --same-device (dry run) needs --comm host (one GPU cannot host two NCCL ranks)")
     import torch
     import torch.distributed as dist
     from paper_2601_18548_b200 import BF16, FP16, FP16X3, FP32, Context
-    from paper_2601_18548_b200.dist import gather_active_sets
     from paper_2601_18548_b200.gcdf import load_library
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if a.same_device else int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if a.comm == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    red_dev = "cpu" if (world > 1 and a.comm == "host") else None  # where max-over-ranks reductions run
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     lib = load_library()
@@ -211,8 +240,23 @@ def main():
                   max_candidates=(cfg.pairs // world + 4096) if a.partition_radius > 0 else 0)
     ctx.load_weights(synth.weights_path(cfg.H, act=act))
     ctx.update_scene(pts)
+    if world > 1:
+        if a.comm == "nccl":
+            ctx.dist_init()   # NCCL communicator inside the library (id broadcast by torch.distributed)
+        else:
+            def gloo_allgather(send, recv):
+                n_ = send.shape[0]
+                parts = [torch.empty(n_, dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(parts, torch.from_numpy(send.copy()))
+                for r_ in range(world):
+                    recv[r_ * n_:(r_ + 1) * n_] = parts[r_].numpy()
+            ctx.dist_init_host(gloo_allgather)
     q = torch.from_numpy(q_np).to(dev)
-    outs = ctx.alloc_detect_outputs(n_wp, max_active)
+    # output capacity of the (gathered) result; at N > 1 it also sets the exchange stride
+    # (ceil(capacity / N) records per rank), so after the first warm-up step it is the
+    # observed count + 10 % (the scene updates move it by ~0.01 %)
+    cap = [max_active * world]
+    outs = ctx.alloc_detect_outputs(n_wp, max_active * world)
     # Scene-update inputs of every step (A9: 200 removes + 200 adds of a moved box), made
     # before any clock starts: adds are points of a randomly moved clutter box, removals
     # disjoint sets of the initially live ids (valid whatever ids the adds reuse).
@@ -232,17 +276,25 @@ def main():
 
     def step():
         scene_step()
-        # single GPU: no host sync inside the device-timed step (the count is read after the
-        # timed region); the multi-GPU gather needs the per-rank counts on the host
-        o = ctx.detect_active_set(q, delta, tau, outputs=outs, sync_count=world > 1)
-        if world > 1:
-            o = gather_active_sets(ctx, o, n_wp, group=None)
+        # no host sync inside the device-timed step (the count is read after the timed
+        # region); at N > 1 the exchange runs on the call's stream inside the library
+        o = ctx.detect_active_set(q, delta, tau, outputs=outs, capacity=cap[0], sync_count=False)
         return o
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=red_dev or dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     # L2 flush buffer (> 126 MB L2) written between timed steps
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    for _ in range(a.warmup):
-        step()
+    for i in range(a.warmup):
+        o = step()
+        if i == 0:
+            n0 = int(o["count"].item())
+            cap[0] = min(max_active * world, world * (int(1.1 * n0 / world) + 2048))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -268,17 +320,22 @@ def main():
         dist.barrier()
     launches = ctx.launches - l0
     mlp_ms, mlp_n = ctx.profile_read(reset=True)
+    x_ms, x_n = ctx.profile_read_exchange(reset=True)
     ctx.profile_enable(False)
     clk = clocks.stop()
     t_ms = sum(s.elapsed_time(e) for s, e in ev)
-    t_max = t_ms
-    if world > 1:
-        t = torch.tensor([t_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_max = float(t.item())
+    t_max = max_over_ranks(t_ms)
+    # n_live is the global live count (the id rule is replicated on every rank)
     pairs_total = n_live_total * n_wp           # every (waypoint, live point) pair of the job
     value = pairs_total / (t_max / 1e3)
-    n_active = int(last["n"]) if "n" in last and world > 1 else int(last["count"].item())
+    n_active = int(last["count"].item())
+    exchange = None
+    if world > 1:
+        exchange = {"backend": ctx.dist_info(), "ms_per_step": (x_ms / x_n) if x_n else None,
+                    "share_of_step": (x_ms / t_ms) if (x_n and t_ms > 0) else None,
+                    "capacity": cap[0], "stride_records_per_rank": -(-cap[0] // world),
+                    "bytes_received_per_rank": (world - 1) * (48 * -(-cap[0] // world) + 8 * (2 * n_wp + 1)),
+                    "what": "all-gather group (headers + records) + merge kernel, CUDA events on the call's stream"}
 
     # roofline of the dominant kernel (fused MLP): algorithmic flops per launch / live duration
     peaks, peak_src = measured_peaks()
@@ -321,14 +378,7 @@ def main():
     # arrays in) + the host-buffer detect call (q in from pinned host memory, records /
     # offsets / min / argmin out to pinned host memory; the library does the copies).
     q_pin = torch.from_numpy(q_np).pin_memory()
-    if world == 1:
-        host_out = ctx.alloc_host_outputs(n_wp, max_active, pinned=True)
-    else:
-        host_out = {"records": torch.empty((max_active * world, 48), dtype=torch.uint8).pin_memory(),
-                    "wp_offsets": torch.empty(n_wp + 1, dtype=torch.int64).pin_memory(),
-                    "wp_min": torch.empty(n_wp, dtype=torch.float32).pin_memory(),
-                    "wp_argmin": torch.empty(n_wp, dtype=torch.int64).pin_memory()}
-        q_dev = torch.empty(q_pin.shape, dtype=torch.float32, device=dev)
+    host_out = ctx.alloc_host_outputs(n_wp, cap[0], pinned=True)
     h2d = d2h = 0
     if world > 1:
         dist.barrier()
@@ -337,28 +387,14 @@ def main():
     e2e_pairs = 0
     for i in range(e2e_steps):
         add_i, rem_i = scene_step()
-        if world == 1:
-            o = ctx.detect_active_set_host(q_pin, delta, tau, host_out)
-            n = int(o["n"])
-        else:
-            q_dev.copy_(q_pin, non_blocking=True)
-            o = ctx.detect_active_set(q_dev, delta, tau, outputs=outs, sync_count=True)
-            o = gather_active_sets(ctx, o, n_wp)
-            n = int(o["n"])
-            host_out["records"][:n].copy_(o["records"][:n], non_blocking=True)
-            for k in ("wp_offsets", "wp_min", "wp_argmin"):
-                host_out[k].copy_(o[k], non_blocking=True)
-            torch.cuda.current_stream(dev).synchronize()
+        o = ctx.detect_active_set_host(q_pin, delta, tau, host_out)
+        n = int(o["n"])
         h2d += q_pin.numel() * 4 + add_i.nbytes + rem_i.nbytes
         d2h += n * 48 + host_out["wp_offsets"].numel() * 8 + host_out["wp_min"].numel() * 4 + \
             host_out["wp_argmin"].numel() * 8 + 8
         e2e_pairs += ctx.scene_info()["n_live"] * n_wp
     torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
 
     # NEXT-1: the range-partitioned detect on the same workload (device time per call)
     part = None
@@ -395,20 +431,16 @@ def main():
     lat = None
     if a.latency_calls > 0:
         for _ in range(5):
-            o = ctx.detect_active_set(q, delta, tau, outputs=outs, sync_count=True)
-            if world > 1:
-                gather_active_sets(ctx, o, n_wp)
+            ctx.detect_active_set(q, delta, tau, outputs=outs, capacity=cap[0], sync_count=True)
         torch.cuda.synchronize()
         ts = []
         for _ in range(a.latency_calls):
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
-            o = ctx.detect_active_set(q, delta, tau, outputs=outs, sync_count=True)
-            if world > 1:
-                gather_active_sets(ctx, o, n_wp)
+            ctx.detect_active_set(q, delta, tau, outputs=outs, capacity=cap[0], sync_count=True)
             ts.append(time.perf_counter() - t0)
-        tt = torch.tensor(ts, device=dev, dtype=torch.float64)
+        tt = torch.tensor(ts, device=red_dev or dev, dtype=torch.float64)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = np.sort(tt.cpu().numpy()) * 1e3
@@ -486,7 +518,7 @@ def main():
                        "active_per_step": n_active, "scene_update_per_step": f"{n_chg} removes + {n_chg} adds",
                        "parallelism": f"points sharded over {world} GPU(s)",
                        "l2": "256 MiB buffer written between timed steps (L2 flush)"},
-            "roofline": roof, "mlp_kernel_share_of_step": kshare,
+            "roofline": roof, "mlp_kernel_share_of_step": kshare, "exchange": exchange,
             "detect_latency": lat,
             "partitioned": part,
             "variants": variants,
@@ -495,6 +527,9 @@ def main():
                     "d2h_bytes_per_step": d2h // e2e_steps, "steps": e2e_steps},
             "gpu_launches": launches, "clocks": clk,
         }
+        if a.same_device:
+            line["dry_run"] = ("all ranks on cuda:0 with the host test exchange backend: checks the N > 1 "
+                               "code path, NOT a measurement")
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

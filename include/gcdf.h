@@ -54,7 +54,8 @@ enum gcdf_status {
   GCDF_ERR_UNKNOWN_ID = -8,    /* remove of an id that is not live (or duplicated in the call) */
   GCDF_ERR_NONFINITE = -9,     /* NaN / Inf in points or weights */
   GCDF_ERR_CUDA = -10,         /* CUDA runtime error (message has the CUDA string); sticky */
-  GCDF_ERR_UNSUPPORTED = -11   /* e.g. no sm_100 device */
+  GCDF_ERR_UNSUPPORTED = -11,  /* e.g. no sm_100 device */
+  GCDF_ERR_NCCL = -12          /* NCCL (or the test exchange backend) failed; message has the NCCL string; sticky */
 };
 
 enum gcdf_precision {
@@ -90,6 +91,10 @@ typedef struct {
   int64_t max_candidates;  /* range-partitioned detect: capacity of the per-step candidate
                               lists (sum over steps of |I_{M,i}|); 0 = partitioned detect off */
   int32_t frame;           /* gcdf_frame: base-frame transform of the points */
+  int32_t exchange;        /* reserve the exchange buffers of the sharded detect (gcdf_dist_init*)
+                              also at world == 1 (at world > 1 they are always reserved):
+                              header 2 x (world + 1) x (2 max_waypoints + 1) x 8 B and records
+                              (world + 1) x max_active x 48 B */
 } gcdf_options;
 
 /* One active constraint (48 B): f, grad_q f (9), wp = b*N + i, pt = global point id. */
@@ -181,9 +186,20 @@ int gcdf_project_dense(gcdf_ctx *ctx, const float *q_dev, int32_t B, int32_t N, 
    none, for a cross-rank MIN reduction; count_dev [1] (total active).
    count_host_or_null: if non-NULL the stream is synchronized and the count written.
    CAPACITY is returned (count still exact, out content unspecified) when the count
-   exceeds out_capacity or the staging capacity max_active; grow and retry.  On a
-   sharded scene (world > 1) the result covers this rank's points only; see
-   gcdf_merge_active_sets. */
+   exceeds out_capacity or the staging capacity max_active; grow and retry.
+   Sharded scene: once gcdf_dist_init / gcdf_dist_init_host ran, every rank
+   calls with the same q, delta, tau and out_capacity (SPMD) and every rank receives the
+   FULL, canonically ordered result over all ranks' points -- bit-identical to one GPU
+   holding the whole scene.  On the stream, with no host synchronization (NCCL backend):
+   the local fused detect writes this rank's records (at most S = min(max_active,
+   ceil(out_capacity / world)); the ids of a rank are dealt round-robin by 128-id block, so
+   the ranks' counts are balanced) and its header (wp_offsets + per-waypoint keys) into the
+   exchange buffers; one NCCL group all-gathers the headers ((2 B*N + 1) x 8 B per rank) and
+   the records (S x 48 B per rank); the merge kernel (K5) reduces the keys (MIN = global min
+   / smallest-id argmin), sums the offsets and places every record by binary search.  A rank
+   with more than S actives makes the call return CAPACITY (count_dev still the exact total;
+   records unspecified).  Without a communicator, the result covers this rank's points
+   only (gcdf_merge_active_sets merges such results). */
 int gcdf_detect_active_set(gcdf_ctx *ctx, const float *q_dev, int32_t B, int32_t N, float delta,
                            float tau, gcdf_active_t *out_dev, int64_t out_capacity, int64_t *wp_offsets_dev,
                            float *wp_min_dev, int64_t *wp_argmin_dev, int64_t *wp_key_dev,
@@ -263,12 +279,36 @@ int gcdf_compact_dense(gcdf_ctx *ctx, const float *values_dev, const float *grad
    `world` ranks into one canonical (wp, pt) ordered set.
    recs_dev [world][rec_stride] (rank r's records at r*rec_stride, in its own order);
    offsets_dev [world][n_wp+1] (each rank's wp_offsets); wp_key_dev [n_wp] the MIN over
-   ranks of wp_key.  Outputs as in detect.  Pure device work; no collective inside
-   (the collectives run through torch.distributed / NCCL around it). */
+   ranks of wp_key.  Outputs as in detect.  Pure device work, no collective inside (the
+   sharded detect runs the same merge kernel after its own NCCL exchange). */
 int gcdf_merge_active_sets(gcdf_ctx *ctx, int32_t world, int32_t n_wp, const gcdf_active_t *recs_dev,
                            int64_t rec_stride, const int64_t *offsets_dev, const int64_t *wp_key_dev,
                            gcdf_active_t *out_dev, int64_t out_capacity, int64_t *wp_offsets_dev,
                            float *wp_min_dev, int64_t *wp_argmin_dev, int64_t *count_dev, void *stream);
+
+/* ------------------------------------------------------------------ sharded scene */
+/* NCCL unique id for gcdf_dist_init (call on one rank; the caller broadcasts the 128 bytes,
+   e.g. through its torch.distributed process group).  NCCL is opened at run time
+   (dlopen libnccl.so.2: the process's NCCL when torch loaded it); NCCL if that fails. */
+int gcdf_nccl_unique_id(unsigned char out_id[128]);
+/* Creates this context's NCCL communicator (ncclCommInitRank on the context's device):
+   rank / world must equal gcdf_options.rank / world, and the exchange buffers must be
+   reserved (world > 1 or gcdf_options.exchange).  Collective over the world: every rank
+   calls it with the same id.  From then on detect / detect_partitioned / detect_host /
+   the CUDA-graph detect return the gathered result (see gcdf_detect_active_set).  The
+   communicator is destroyed with the context.  INVALID_ARG (mismatch, no buffers, already
+   initialized), NCCL. */
+int gcdf_dist_init(gcdf_ctx *ctx, const unsigned char id[128], int32_t rank, int32_t world);
+/* TEST BACKEND of the same exchange: fn is a blocking host all-gather -- rank r's
+   bytes_per_rank bytes of send_host land at recv_host + r * bytes_per_rank on every rank;
+   it returns 0 on success.  The library synchronizes the stream and stages through pinned
+   host memory, so several processes can share ONE GPU (no kernel waits on another rank).
+   Not for production and not capturable into a CUDA graph. */
+typedef int (*gcdf_host_allgather_fn)(const void *send_host, void *recv_host, int64_t bytes_per_rank, void *user);
+int gcdf_dist_init_host(gcdf_ctx *ctx, gcdf_host_allgather_fn fn, void *user);
+/* Communicator state: *kind 0 = none, 1 = NCCL, 2 = host test backend; *nccl_version (may be
+   NULL) = ncclGetVersion of the opened library (0 if none). */
+int gcdf_dist_info(const gcdf_ctx *ctx, int32_t *kind, int32_t *nccl_version);
 
 /* Number of kernels this context launched since creation (for bench accounting). */
 int64_t gcdf_launch_count(const gcdf_ctx *ctx);
@@ -276,9 +316,11 @@ int64_t gcdf_launch_count(const gcdf_ctx *ctx);
 /* Optional live timing of the fused MLP kernel (the dominant kernel): when enabled,
    query/detect record a CUDA event pair around that launch on the call's stream.
    gcdf_profile_read synchronizes on the last pair and returns the accumulated kernel
-   milliseconds and launch count since the last reset. */
+   milliseconds and launch count since the last reset.  gcdf_profile_read_exchange does the
+   same for the exchange step of the sharded detect (the all-gather group + merge kernel). */
 int gcdf_profile_enable(gcdf_ctx *ctx, int enable);
 int gcdf_profile_read(gcdf_ctx *ctx, double *mlp_ms, int64_t *mlp_launches, int reset);
+int gcdf_profile_read_exchange(gcdf_ctx *ctx, double *ms, int64_t *calls, int reset);
 
 /* ------------------------------------------------------------------ diagnostics */
 /* Runs one tcgen05 UMMA building block of the bf16 kernel on device `cuda_device`

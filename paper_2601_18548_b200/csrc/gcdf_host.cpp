@@ -20,6 +20,7 @@
 
 #include <cstdlib>
 
+#include "gcdf_comm.h"
 #include "gcdf_internal.h"
 
 using namespace gcdf;
@@ -36,6 +37,9 @@ inline int64_t align256(int64_t x) { return (x + 255) & ~int64_t(255); }
 struct Layout {
   int64_t pts, wf32, wbf16, wf16, wf16x3, wf16w, meta, cbits, staging, wp_key, wp_count, counter, upd_payload, upd_slots;
   int64_t h_q, h_out, h_offs, h_wmin, h_warg, h_count;
+  // exchange buffers of the sharded detect (gcdf_comm.cpp): per-rank header
+  // [wp_offsets (n_wp + 1) | wp_key (n_wp)] int64 and records, send + gathered
+  int64_t x_hdr_send, x_hdr_recv, x_rec_send, x_rec_recv, x_count;
   int64_t p_grid, p_bbox, p_cell_count, p_cell_start, p_cell_fill, p_cell_items, p_cell_xy, p_bitmap, p_chunk_cnt, p_chunk_off,
       p_scan_tmp, p_cand, p_cand_start, p_cand_count, p_tile_start, p_tile_wp, p_n_tiles, p_words, p_nchunk;
   int64_t total;
@@ -105,6 +109,12 @@ struct gcdf_ctx {
   float part_r = -1.f;
   int64_t scene_version = 0;   // bumped by every scene change (captured graphs re-capture)
   int64_t weights_version = 0; // bumped by gcdf_load_weights / gcdf_bind_workspace (same)
+  bool exchange = false;       // exchange buffers reserved (world > 1 or opt.exchange)
+  Comm comm;                   // gcdf_dist_init* (kind kCommNone until then)
+  std::vector<cudaEvent_t> xev;  // exchange-step timing pairs (gcdf_profile_read_exchange)
+  int xev_used = 0;
+  double xprof_ms = 0.0;
+  int64_t xprof_n = 0;
 };
 
 // A captured detect (gcdf_graph_create_detect): the arguments, the instantiated graph and
@@ -335,6 +345,14 @@ int prof_drain(gcdf_ctx *c) {
     ++c->prof_n;
   }
   c->ev_used = 0;
+  for (int i = 0; i < c->xev_used; ++i) {
+    CK(c, cudaEventSynchronize(c->xev[2 * i + 1]), "profile sync");
+    float ms = 0.f;
+    CK(c, cudaEventElapsedTime(&ms, c->xev[2 * i], c->xev[2 * i + 1]), "profile elapsed");
+    c->xprof_ms += ms;
+    ++c->xprof_n;
+  }
+  c->xev_used = 0;
   return GCDF_OK;
 }
 
@@ -354,6 +372,7 @@ void gcdf_default_options(gcdf_options *o) {
   o->world = 1;
   o->max_candidates = 0;
   o->frame = GCDF_FRAME_TRANSLATE;
+  o->exchange = 0;
 }
 
 int gcdf_has_tcgen05(void) { return tc_compiled() ? 1 : 0; }
@@ -410,11 +429,21 @@ int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out) {
   L.upd_slots = off; off = align256(off + kUpdChunk * 8);
   // device side of gcdf_detect_active_set_host
   L.h_q = off; off = align256(off + (int64_t)o.max_waypoints * kNdof * 4);
-  L.h_out = off; off = align256(off + o.max_active * (int64_t)sizeof(gcdf_active_t));
+  // (the gathered result of a sharded detect holds up to world x max_active records)
+  L.h_out = off; off = align256(off + o.max_active * (int64_t)sizeof(gcdf_active_t) * o.world);
   L.h_offs = off; off = align256(off + ((int64_t)o.max_waypoints + 1) * 8);
   L.h_wmin = off; off = align256(off + (int64_t)o.max_waypoints * 4);
   L.h_warg = off; off = align256(off + (int64_t)o.max_waypoints * 8);
   L.h_count = off; off = align256(off + 8);
+  c->exchange = o.world > 1 || o.exchange != 0;
+  if (c->exchange) {
+    const int64_t hdr = (2 * (int64_t)o.max_waypoints + 1) * 8;
+    L.x_hdr_send = off; off = align256(off + hdr);
+    L.x_hdr_recv = off; off = align256(off + hdr * o.world);
+    L.x_rec_send = off; off = align256(off + o.max_active * (int64_t)sizeof(gcdf_active_t));
+    L.x_rec_recv = off; off = align256(off + o.max_active * (int64_t)sizeof(gcdf_active_t) * o.world);
+    L.x_count = off; off = align256(off + 8);
+  }
   // range-partitioned detect (k_partition.cu), only with max_candidates > 0
   if (o.max_candidates > 0) {
     const int64_t W = o.max_waypoints;
@@ -458,6 +487,8 @@ int gcdf_destroy(gcdf_ctx *c) {
   if (c->h_payload) cudaFreeHost(c->h_payload);
   if (c->h_slots) cudaFreeHost(c->h_slots);
   for (auto &e : c->ev) cudaEventDestroy(e);
+  for (auto &e : c->xev) cudaEventDestroy(e);
+  comm_destroy(c->comm);
   delete c;
   return GCDF_OK;
 }
@@ -831,8 +862,21 @@ int gcdf_profile_enable(gcdf_ctx *c, int enable) {
   if (enable && c->ev.empty()) {
     c->ev.resize(2 * kEvPool);
     for (auto &e : c->ev) CK(c, cudaEventCreate(&e), "event create");
+    c->xev.resize(2 * kEvPool);
+    for (auto &e : c->xev) CK(c, cudaEventCreate(&e), "event create");
   }
   c->prof = enable != 0;
+  return GCDF_OK;
+}
+
+int gcdf_profile_read_exchange(gcdf_ctx *c, double *ms, int64_t *n, int reset) {
+  if (!c) return GCDF_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  int rc = prof_drain(c);
+  if (rc) return rc;
+  if (ms) *ms = c->xprof_ms;
+  if (n) *n = c->xprof_n;
+  if (reset) { c->xprof_ms = 0.0; c->xprof_n = 0; }
   return GCDF_OK;
 }
 
@@ -890,9 +934,56 @@ int gcdf_project_dense(gcdf_ctx *c, const float *q, int32_t B, int32_t N, const 
 
 static int read_count(gcdf_ctx *c, int64_t cap, const int64_t *count_dev, int64_t *count_host, cudaStream_t s);
 
+static int comm_rc(gcdf_ctx *c, int r, const std::string &msg) {
+  if (r == kCommErrCuda) c->cuda_failed = true;
+  return fail(c, r == kCommErrCuda ? GCDF_ERR_CUDA : GCDF_ERR_NCCL, "exchange: %s", msg.c_str());
+}
+
+// The sharded detect's exchange: the local finalize writes this rank's
+// records and header into the send buffers, one all-gather group moves them, the merge
+// kernel assembles the canonical result in the caller's buffers.  All on s.
+static int exchange_detect(gcdf_ctx *c, int32_t nwp, int32_t tpw, gcdf_active_t *out, int64_t cap, int64_t *offs,
+                           float *wmin, int64_t *warg, int64_t *wkey, int64_t *count_dev, int64_t *count_host,
+                           cudaStream_t s, const int64_t *tile_start) {
+  DetectScratch ds = scratch_view(c);
+  const int W = c->comm.world;
+  const int64_t S = std::max<int64_t>(1, std::min<int64_t>(c->opt.max_active, (cap + W - 1) / W));
+  const int64_t hdr = 2 * (int64_t)nwp + 1;
+  int64_t *hs = reinterpret_cast<int64_t *>(c->ws + c->L.x_hdr_send);
+  int64_t *hr = reinterpret_cast<int64_t *>(c->ws + c->L.x_hdr_recv);
+  gcdf_active_t *rs = reinterpret_cast<gcdf_active_t *>(c->ws + c->L.x_rec_send);
+  gcdf_active_t *rr = reinterpret_cast<gcdf_active_t *>(c->ws + c->L.x_rec_recv);
+  int64_t *lc = reinterpret_cast<int64_t *>(c->ws + c->L.x_count);
+  int nl = 0;
+  cudaError_t e = launch_finalize(ds, nwp, tpw, tile_start, c->tiles_cap, rs, S, hs, nullptr, nullptr, hs + nwp + 1,
+                                  lc, reinterpret_cast<int64_t *>(c->ws + c->L.wp_count), s, &nl);
+  int rc = count_launch(c, e, "detect finalize", nl);
+  if (rc) return rc;
+  int slot = -1;
+  if (c->prof && c->comm.kind == kCommNccl) {
+    if (c->xev_used == kEvPool && prof_drain(c)) return GCDF_ERR_CUDA;
+    slot = c->xev_used++;
+    CK(c, cudaEventRecord(c->xev[2 * slot], s), "profile event");
+  }
+  const void *send[2] = {hs, rs};
+  void *recv[2] = {hr, rr};
+  const int64_t bytes[2] = {hdr * 8, S * (int64_t)sizeof(gcdf_active_t)};
+  std::string msg;
+  const int r = comm_allgather(c->comm, 2, send, recv, bytes, s, &msg);
+  if (r) return comm_rc(c, r, msg);
+  nl = 0;
+  e = launch_merge(W, nwp, rr, S, hr, hdr, hr + nwp + 1, hdr, out, cap, offs, wmin, warg, wkey, count_dev,
+                   ds.counter + 1, s, &nl);
+  if ((rc = count_launch(c, e, "exchange merge", nl))) return rc;
+  if (slot >= 0) CK(c, cudaEventRecord(c->xev[2 * slot + 1], s), "profile event");
+  return read_count(c, cap, count_dev, count_host, s);
+}
+
 static int finish_detect(gcdf_ctx *c, int32_t nwp, int32_t tpw, gcdf_active_t *out, int64_t cap, int64_t *offs,
                          float *wmin, int64_t *warg, int64_t *wkey, int64_t *count_dev, int64_t *count_host,
                          cudaStream_t s, const int64_t *tile_start = nullptr) {
+  if (c->comm.kind != kCommNone)
+    return exchange_detect(c, nwp, tpw, out, cap, offs, wmin, warg, wkey, count_dev, count_host, s, tile_start);
   DetectScratch ds = scratch_view(c);
   int nl = 0;
   cudaError_t e = launch_finalize(ds, nwp, tpw, tile_start, c->tiles_cap, out, cap, offs, wmin, warg, wkey,
@@ -1015,8 +1106,12 @@ int gcdf_detect_active_set_host(gcdf_ctx *c, const float *q_host, int32_t B, int
   int64_t *cnt = reinterpret_cast<int64_t *>(c->ws + c->L.h_count);
   CK(c, cudaMemcpyAsync(q, q_host, nwp * kNdof * 4, cudaMemcpyHostToDevice, s), "q H2D");
   int64_t n = -1;
-  rc = gcdf_detect_active_set(c, q, B, N, delta, tau, out, c->opt.max_active, offs, wmin, warg, nullptr, cnt, &n,
-                              stream);
+  // device capacity: max_active (one rank), or with a communicator the caller's capacity
+  // (which sets the exchange stride), at most world x max_active
+  const int64_t icap = c->comm.kind == kCommNone ? c->opt.max_active
+                                                 : std::min<int64_t>(std::max<int64_t>(cap, 1),
+                                                                     c->opt.max_active * c->comm.world);
+  rc = gcdf_detect_active_set(c, q, B, N, delta, tau, out, icap, offs, wmin, warg, nullptr, cnt, &n, stream);
   *count_host = n;
   if (rc && rc != GCDF_ERR_CAPACITY) return rc;
   const int64_t nc = rc ? 0 : std::min(n, cap);
@@ -1066,8 +1161,8 @@ int gcdf_merge_active_sets(gcdf_ctx *c, int32_t world, int32_t n_wp, const gcdf_
   if (world < 1 || n_wp <= 0 || !recs || rec_stride < 0 || !offsets || !wp_key || !out || !offs || !count)
     return fail(c, GCDF_ERR_INVALID_ARG, "merge: bad arguments");
   int nl = 0;
-  cudaError_t e = launch_merge(world, n_wp, recs, rec_stride, offsets, wp_key, out, cap, offs, wmin, warg, count,
-                               static_cast<cudaStream_t>(stream), &nl);
+  cudaError_t e = launch_merge(world, n_wp, recs, rec_stride, offsets, (int64_t)n_wp + 1, wp_key, 0, out, cap, offs,
+                               wmin, warg, nullptr, count, nullptr, static_cast<cudaStream_t>(stream), &nl);
   return count_launch(c, e, "merge", nl);
 }
 
@@ -1089,6 +1184,8 @@ static int graph_capture(gcdf_graph *g) {
     c->part_dirty = false;
     c->part_r = g->radius;
   }
+  if (c->comm.kind == kCommHost)
+    return fail(c, GCDF_ERR_INVALID_ARG, "graph: the host exchange backend (tests) cannot be captured");
   const bool prof = c->prof;
   c->prof = false;  // no profiling events inside a graph
   CK(c, cudaStreamBeginCapture(g->cs, cudaStreamCaptureModeRelaxed), "begin capture");
@@ -1173,6 +1270,48 @@ int gcdf_graph_destroy(gcdf_graph *g) {
   if (g->exec) cudaGraphExecDestroy(g->exec);
   if (g->cs) cudaStreamDestroy(g->cs);
   delete g;
+  return GCDF_OK;
+}
+
+int gcdf_nccl_unique_id(unsigned char out_id[128]) {
+  if (!out_id) return GCDF_ERR_INVALID_ARG;
+  std::string msg;
+  return comm_unique_id(out_id, &msg) ? GCDF_ERR_NCCL : GCDF_OK;
+}
+
+static int dist_precheck(gcdf_ctx *c) {
+  int rc = precheck(c, false);
+  if (rc) return rc;
+  if (!c->exchange)
+    return fail(c, GCDF_ERR_INVALID_ARG, "dist_init: no exchange buffers (world == 1 needs gcdf_options.exchange)");
+  if (c->comm.kind != kCommNone) return fail(c, GCDF_ERR_INVALID_ARG, "dist_init: communicator already initialized");
+  return GCDF_OK;
+}
+
+int gcdf_dist_init(gcdf_ctx *c, const unsigned char id[128], int32_t rank, int32_t world) {
+  int rc = dist_precheck(c);
+  if (rc) return rc;
+  if (!id || rank != c->opt.rank || world != c->opt.world)
+    return fail(c, GCDF_ERR_INVALID_ARG, "dist_init: rank %d / world %d differ from the context's %d / %d", rank, world,
+                c->opt.rank, c->opt.world);
+  std::string msg;
+  const int r = comm_init_nccl(c->comm, id, rank, world, &msg);
+  if (r) return fail(c, GCDF_ERR_NCCL, "dist_init: %s", msg.c_str());
+  return GCDF_OK;
+}
+
+int gcdf_dist_init_host(gcdf_ctx *c, gcdf_host_allgather_fn fn, void *user) {
+  int rc = dist_precheck(c);
+  if (rc) return rc;
+  if (!fn) return fail(c, GCDF_ERR_INVALID_ARG, "dist_init_host: null all-gather");
+  comm_init_host(c->comm, c->opt.rank, c->opt.world, fn, user);
+  return GCDF_OK;
+}
+
+int gcdf_dist_info(const gcdf_ctx *c, int32_t *kind, int32_t *nccl_version) {
+  if (!c) return GCDF_ERR_INVALID_ARG;
+  if (kind) *kind = c->comm.kind;
+  if (nccl_version) *nccl_version = c->comm.nccl_version;
   return GCDF_OK;
 }
 

@@ -203,9 +203,13 @@ cudaError_t launch_finalize(DetectScratch ds, int32_t n_wp, int32_t tiles_per_wp
                             float *wp_min, int64_t *wp_argmin, int64_t *wp_key, int64_t *count, int64_t *fin_scratch,
                             cudaStream_t s, int *n_launches);
 int64_t finalize_scratch_elems(int64_t max_wp, int64_t max_tiles_per_wp);
+// Merge of gathered rank pieces (K5): rank r's wp_offsets at offsets[r * off_stride ..],
+// its per-waypoint keys at keys[r * key_stride ..] (key_stride 0: keys already reduced),
+// its records at recs[r * rec_stride ..]; a rank count above rec_stride sets *overflow.
 cudaError_t launch_merge(int32_t world, int32_t n_wp, const gcdf_active_t *recs, int64_t rec_stride,
-                         const int64_t *offsets, const int64_t *wp_key, gcdf_active_t *out,
-                         int64_t out_capacity, int64_t *wp_offsets, float *wp_min, int64_t *wp_argmin,
-                         int64_t *count, cudaStream_t s, int *n_launches);
+                         const int64_t *offsets, int64_t off_stride, const int64_t *keys, int64_t key_stride,
+                         gcdf_active_t *out, int64_t out_capacity, int64_t *wp_offsets, float *wp_min,
+                         int64_t *wp_argmin, int64_t *wp_key, int64_t *count, unsigned long long *overflow,
+                         cudaStream_t s, int *n_launches);
 
 }  // namespace gcdf

@@ -363,23 +363,45 @@ __global__ void __launch_bounds__(256, 3) k_compact_write(const float *__restric
 }
 
 // ---- multi-rank merge ----
-__global__ void k_merge_offsets(int32_t world, int32_t n_wp, const int64_t *__restrict__ offsets,
-                                int64_t *__restrict__ wp_offsets, int64_t *__restrict__ count) {
+// Rank r's gathered pieces: offsets at offsets[r * off_stride + 0..n_wp] (its wp_offsets),
+// per-waypoint keys at keys[r * key_stride + 0..n_wp-1] (key_stride 0: one already-reduced
+// key array), records at recs[r * rec_stride + k] for k < min(its count, rec_stride).
+// k_merge_offsets: merged wp_offsets / count (sums over ranks), the MIN of the keys
+// (global min / smallest-id argmin) and a rank whose count exceeds rec_stride -> *overflow.
+__global__ void k_merge_offsets(int32_t world, int32_t n_wp, const int64_t *__restrict__ offsets, int64_t off_stride,
+                                const int64_t *__restrict__ keys, int64_t key_stride, int64_t rec_stride,
+                                int64_t *__restrict__ wp_offsets, int64_t *__restrict__ count, int64_t *wp_key,
+                                float *wp_min, int64_t *wp_argmin, unsigned long long *overflow) {
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w <= n_wp; w += gridDim.x * blockDim.x) {
     int64_t s = 0;
-    for (int r = 0; r < world; ++r) s += offsets[(int64_t)r * (n_wp + 1) + w];
+    for (int r = 0; r < world; ++r) s += offsets[(int64_t)r * off_stride + w];
     wp_offsets[w] = s;
-    if (w == n_wp) *count = s;
+    if (w == n_wp) {
+      *count = s;
+      for (int r = 0; r < world; ++r)
+        if (overflow && offsets[(int64_t)r * off_stride + n_wp] > rec_stride) atomicOr(overflow, 1ull);
+      continue;
+    }
+    int64_t key = keys[w];
+    for (int r = 1; r < world && key_stride; ++r) key = min(key, keys[(int64_t)r * key_stride + w]);
+    if (wp_key) wp_key[w] = key;
+    const unsigned long long k = (unsigned long long)key ^ 0x8000000000000000ull;
+    if (wp_min) wp_min[w] = k == ~0ull ? __int_as_float(0x7f800000) : unord_f32((unsigned)(k >> 32));
+    if (wp_argmin) wp_argmin[w] = k == ~0ull ? -1 : (int64_t)(k & 0xffffffffull);
   }
 }
 
+// Every rank's records are in canonical (wp, pt) order over its own ids; record k of rank r
+// in waypoint w goes to wp_offsets[w] + (k - off_r[w]) + (number of records of the other
+// ranks in w with a smaller id), found by binary search -- the merged set equals the
+// single-rank result bit for bit (ids are unique across ranks).
 __global__ void k_merge_records(int32_t world, int32_t n_wp, const gcdf_active_t *__restrict__ recs,
-                                int64_t rec_stride, const int64_t *__restrict__ offsets,
+                                int64_t rec_stride, const int64_t *__restrict__ offsets, int64_t off_stride,
                                 const int64_t *__restrict__ wp_offsets, gcdf_active_t *__restrict__ out,
                                 int64_t cap) {
   const int r = blockIdx.y;
-  const int64_t *off = offsets + (int64_t)r * (n_wp + 1);
-  const int64_t n = off[n_wp];
+  const int64_t *off = offsets + (int64_t)r * off_stride;
+  const int64_t n = min(off[n_wp], rec_stride);  // (a truncated rank is flagged by k_merge_offsets)
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     // waypoint of record k: last w with off[w] <= k
     int lo = 0, hi = n_wp - 1;
@@ -392,24 +414,17 @@ __global__ void k_merge_records(int32_t world, int32_t n_wp, const gcdf_active_t
     int64_t pos = wp_offsets[w] + (k - off[w]);
     for (int s = 0; s < world; ++s) {
       if (s == r) continue;
-      const int64_t *os = offsets + (int64_t)s * (n_wp + 1);
-      int64_t a = os[w], b = os[w + 1];  // count records of rank s in wp w with pt < rec.pt
+      const int64_t *os = offsets + (int64_t)s * off_stride;
+      const int64_t a0 = min(os[w], rec_stride);
+      int64_t a = a0, b = min(os[w + 1], rec_stride);  // records of rank s in wp w with pt < rec.pt
       const gcdf_active_t *rs = recs + (int64_t)s * rec_stride;
       while (a < b) {
         const int64_t mid = (a + b) >> 1;
         if (rs[mid].pt < rec.pt) a = mid + 1; else b = mid;
       }
-      pos += a - os[w];
+      pos += a - a0;
     }
     if (pos < cap) out[pos] = rec;
-  }
-}
-
-__global__ void k_keys_export(const int64_t *__restrict__ skeys, int32_t n_wp, float *wp_min, int64_t *wp_argmin) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_wp; i += gridDim.x * blockDim.x) {
-    const unsigned long long k = (unsigned long long)skeys[i] ^ 0x8000000000000000ull;
-    if (wp_min) wp_min[i] = k == ~0ull ? __int_as_float(0x7f800000) : unord_f32((unsigned)(k >> 32));
-    if (wp_argmin) wp_argmin[i] = k == ~0ull ? -1 : (int64_t)(k & 0xffffffffull);
   }
 }
 
@@ -513,18 +528,19 @@ int64_t finalize_scratch_elems(int64_t max_wp, int64_t max_tiles_per_wp) {
 }
 
 cudaError_t launch_merge(int32_t world, int32_t n_wp, const gcdf_active_t *recs, int64_t rec_stride,
-                         const int64_t *offsets, const int64_t *wp_key, gcdf_active_t *out, int64_t out_capacity,
-                         int64_t *wp_offsets, float *wp_min, int64_t *wp_argmin, int64_t *count, cudaStream_t s,
-                         int *n_launches) {
+                         const int64_t *offsets, int64_t off_stride, const int64_t *keys, int64_t key_stride,
+                         gcdf_active_t *out, int64_t out_capacity, int64_t *wp_offsets, float *wp_min,
+                         int64_t *wp_argmin, int64_t *wp_key, int64_t *count, unsigned long long *overflow,
+                         cudaStream_t s, int *n_launches) {
   int g = (n_wp + 1 + 255) / 256;
-  k_merge_offsets<<<g, 256, 0, s>>>(world, n_wp, offsets, wp_offsets, count);
+  k_merge_offsets<<<g, 256, 0, s>>>(world, n_wp, offsets, off_stride, keys, key_stride, rec_stride, wp_offsets, count,
+                                    wp_key, wp_min, wp_argmin, overflow);
   int gx = (int)((rec_stride + 255) / 256);
   if (gx > 2048) gx = 2048;
   if (gx < 1) gx = 1;
-  k_merge_records<<<dim3(gx, world), 256, 0, s>>>(world, n_wp, recs, rec_stride, offsets, wp_offsets, out,
+  k_merge_records<<<dim3(gx, world), 256, 0, s>>>(world, n_wp, recs, rec_stride, offsets, off_stride, wp_offsets, out,
                                                    out_capacity);
-  k_keys_export<<<(n_wp + 255) / 256 > 0 ? (n_wp + 255) / 256 : 1, 256, 0, s>>>(wp_key, n_wp, wp_min, wp_argmin);
-  *n_launches += 3;
+  *n_launches += 2;
   return cudaGetLastError();
 }
 

@@ -20,7 +20,7 @@ TGRAD_CHAINRULE, TGRAD_QCHANNEL = 0, 1
 FRAME_TRANSLATE, FRAME_SE2 = 0, 1  # gcdf_frame (include/gcdf.h; R24)
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "IO", -3: "BAD_MAGIC", -4: "VERSION", -5: "DIM_MISMATCH",
           -6: "NOT_LOADED", -7: "CAPACITY", -8: "UNKNOWN_ID", -9: "NONFINITE", -10: "CUDA",
-          -11: "UNSUPPORTED"}
+          -11: "UNSUPPORTED", -12: "NCCL"}
 REC_BYTES = 48  # sizeof(gcdf_active_t)
 
 EXPORTED = ["gcdf_default_options", "gcdf_create", "gcdf_destroy", "gcdf_last_error", "gcdf_has_tcgen05",
@@ -28,7 +28,11 @@ EXPORTED = ["gcdf_default_options", "gcdf_create", "gcdf_destroy", "gcdf_last_er
             "gcdf_scene_info", "gcdf_pairgen_transform", "gcdf_query_values_grads", "gcdf_detect_active_set",
             "gcdf_detect_active_set_partitioned", "gcdf_detect_active_set_host", "gcdf_sparse_jacobian",
             "gcdf_project_dense", "gcdf_graph_create_detect", "gcdf_graph_launch", "gcdf_graph_destroy", "gcdf_compact_dense", "gcdf_merge_active_sets", "gcdf_launch_count", "gcdf_profile_enable",
-            "gcdf_profile_read", "gcdf_selftest_umma", "gcdf_debug_trace"]
+            "gcdf_profile_read", "gcdf_profile_read_exchange", "gcdf_selftest_umma", "gcdf_debug_trace",
+            "gcdf_nccl_unique_id", "gcdf_dist_init", "gcdf_dist_init_host", "gcdf_dist_info"]
+COMM_KINDS = {0: "none", 1: "nccl", 2: "host"}
+# gcdf_host_allgather_fn (include/gcdf.h): the test backend's blocking host all-gather
+HOST_ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
 
 
 class GcdfError(RuntimeError):
@@ -41,7 +45,7 @@ class GcdfError(RuntimeError):
 class Options(C.Structure):
     _fields_ = [("precision", C.c_int32), ("tgrad_mode", C.c_int32), ("scene_capacity", C.c_int64),
                 ("max_waypoints", C.c_int32), ("max_active", C.c_int64), ("rank", C.c_int32),
-                ("world", C.c_int32), ("max_candidates", C.c_int64), ("frame", C.c_int32)]
+                ("world", C.c_int32), ("max_candidates", C.c_int64), ("frame", C.c_int32), ("exchange", C.c_int32)]
 
 
 _lib = None
@@ -85,6 +89,11 @@ def load_library(path: str | Path = LIB_PATH):
     lib.gcdf_launch_count.restype = I64
     lib.gcdf_profile_enable.argtypes = [P, C.c_int]
     lib.gcdf_profile_read.argtypes = [P, C.POINTER(C.c_double), PI64, C.c_int]
+    lib.gcdf_profile_read_exchange.argtypes = [P, C.POINTER(C.c_double), PI64, C.c_int]
+    lib.gcdf_nccl_unique_id.argtypes = [C.c_char_p]
+    lib.gcdf_dist_init.argtypes = [P, C.c_char_p, I32, I32]
+    lib.gcdf_dist_init_host.argtypes = [P, HOST_ALLGATHER_FN, P]
+    lib.gcdf_dist_info.argtypes = [P, C.POINTER(I32), C.POINTER(I32)]
     lib.gcdf_selftest_umma.argtypes = [C.c_int, C.c_int, P, P, P, P]
     lib.gcdf_debug_trace.argtypes = [P, P]
     _lib = lib
@@ -163,7 +172,7 @@ class Context:
 
     def __init__(self, device: int = 0, precision: int = FP16, tgrad_mode: int = TGRAD_CHAINRULE,
                  scene_capacity: int = 1 << 20, max_waypoints: int = 256, max_active: int = 1 << 22,
-                 rank: int = 0, world: int = 1, max_candidates: int = 0, frame: int = 0):
+                 rank: int = 0, world: int = 1, max_candidates: int = 0, frame: int = 0, exchange: bool = False):
         self.lib = load_library()
         if not torch.cuda.is_available():
             raise RuntimeError("libgcdf needs a CUDA device (B200); no CPU path exists")
@@ -172,7 +181,7 @@ class Context:
         self.lib.gcdf_default_options(C.byref(o))
         o.precision, o.tgrad_mode, o.scene_capacity = precision, tgrad_mode, scene_capacity
         o.max_waypoints, o.max_active, o.rank, o.world = max_waypoints, max_active, rank, world
-        o.max_candidates, o.frame = max_candidates, frame
+        o.max_candidates, o.frame, o.exchange = max_candidates, frame, int(exchange)
         self.opts = o
         h = C.c_void_p()
         rc = self.lib.gcdf_create(device, C.byref(o), C.byref(h))
@@ -221,6 +230,58 @@ class Context:
         ms, n = C.c_double(), C.c_int64()
         self._check(self.lib.gcdf_profile_read(self._h, C.byref(ms), C.byref(n), int(reset)))
         return ms.value, n.value
+
+    def profile_read_exchange(self, reset: bool = True):
+        ms, n = C.c_double(), C.c_int64()
+        self._check(self.lib.gcdf_profile_read_exchange(self._h, C.byref(ms), C.byref(n), int(reset)))
+        return ms.value, n.value
+
+    # -------------------------------------------------------------- sharded scene
+    def dist_init(self, group=None) -> None:
+        """NCCL communicator of the sharded detect (gcdf_dist_init): rank 0 draws the NCCL
+        unique id in the library, the 128 bytes travel through the torch.distributed group
+        (plumbing), every rank creates its communicator."""
+        import torch.distributed as dist
+        buf = C.create_string_buffer(128)
+        if self.rank == 0:
+            rc = self.lib.gcdf_nccl_unique_id(buf)
+            if rc:
+                raise GcdfError(rc, "gcdf_nccl_unique_id")
+        obj = [buf.raw if self.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        self._check(self.lib.gcdf_dist_init(self._h, obj[0], self.rank, self.world))
+
+    def dist_init_local_nccl(self) -> None:
+        """world == 1 with the exchange buffers (exchange=True): a one-rank NCCL communicator,
+        so the whole exchange path (all-gather group + merge kernel) runs on one GPU."""
+        buf = C.create_string_buffer(128)
+        rc = self.lib.gcdf_nccl_unique_id(buf)
+        if rc:
+            raise GcdfError(rc, "gcdf_nccl_unique_id")
+        self._check(self.lib.gcdf_dist_init(self._h, buf.raw, self.rank, self.world))
+
+    def dist_init_host(self, allgather) -> None:
+        """TEST BACKEND (gcdf_dist_init_host): allgather(send: bytes-like numpy uint8 [n],
+        recv: numpy uint8 [world * n]) -> None, a blocking host all-gather (e.g. gloo)."""
+        world = self.world
+
+        def _cb(send, recv, nbytes, user):
+            try:
+                s = np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_uint8)), shape=(max(int(nbytes), 1),))
+                r = np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_uint8)), shape=(max(world * int(nbytes), 1),))
+                allgather(s[: int(nbytes)], r[: world * int(nbytes)])
+                return 0
+            except Exception:  # noqa: BLE001 -- reported to the library as a failed exchange
+                import traceback
+                traceback.print_exc()
+                return 1
+        self._host_cb = HOST_ALLGATHER_FN(_cb)  # kept alive with the context
+        self._check(self.lib.gcdf_dist_init_host(self._h, self._host_cb, None))
+
+    def dist_info(self):
+        k, v = C.c_int32(), C.c_int32()
+        self._check(self.lib.gcdf_dist_info(self._h, C.byref(k), C.byref(v)))
+        return {"kind": COMM_KINDS.get(k.value, k.value), "nccl_version": v.value}
 
     # -------------------------------------------------------------- weights / scene
     def load_weights(self, path) -> None:

@@ -33,8 +33,8 @@ def test_default_options_and_struct_layout(lib):
     lib.gcdf_default_options(C.byref(o))
     assert (o.precision, o.tgrad_mode, o.world, o.rank) == (2, 0, 1, 0)
     assert o.scene_capacity == 1 << 20 and o.max_waypoints == 256 and o.max_active == 1 << 22
-    assert o.max_candidates == 0 and o.frame == 0
-    assert C.sizeof(Options) == 56  # int32, int32, int64, int32 (+4), int64, int32, int32, int64, int32 (+4)
+    assert o.max_candidates == 0 and o.frame == 0 and o.exchange == 0
+    assert C.sizeof(Options) == 56  # int32, int32, int64, int32 (+4), int64, int32, int32, int64, int32, int32
 
 
 def test_create_without_gpu_fails_cleanly(lib):
@@ -57,7 +57,24 @@ def test_create_without_gpu_fails_cleanly(lib):
     assert lib.gcdf_create(0, C.byref(o), C.byref(h)) == -1
     o.frame, o.tgrad_mode = 1, 1
     assert lib.gcdf_create(0, C.byref(o), C.byref(h)) == -1
+    # capacity bounds: int32 local slots / ~0u sentinel; waypoints on gridDim.y
+    lib.gcdf_default_options(C.byref(o))
+    o.scene_capacity = 1 << 31
+    assert lib.gcdf_create(0, C.byref(o), C.byref(h)) == -1
+    lib.gcdf_default_options(C.byref(o))
+    o.max_waypoints = 65536
+    assert lib.gcdf_create(0, C.byref(o), C.byref(h)) == -1
     assert not h.value
+
+
+def test_nccl_unique_id_host_only(lib):
+    """gcdf_nccl_unique_id opens the process's NCCL at run time (dlopen libnccl.so.2) and
+    draws a 128-byte id -- host-only work (bootstrap socket), no GPU needed."""
+    import torch  # noqa: F401  (loads torch's NCCL first, as in the product processes)
+    a, b = C.create_string_buffer(128), C.create_string_buffer(128)
+    assert lib.gcdf_nccl_unique_id(a) == 0 and lib.gcdf_nccl_unique_id(b) == 0
+    assert a.raw != bytes(128) and a.raw != b.raw
+    assert lib.gcdf_nccl_unique_id(None) == -1
 
 
 def test_binding_refuses_without_gpu():

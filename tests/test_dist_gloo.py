@@ -1,12 +1,15 @@
-"""Multi-process (world_size 2 and 3, gloo, CPU) test of the multi-GPU gather protocol.
+"""Multi-process (world_size 2 and 3, gloo, CPU) test of the sharded detect's exchange
+protocol (include/gcdf.h gcdf_detect_active_set "Sharded scene").
 
-The product's collective step (paper_2601_18548_b200/dist.py gather_parts) runs on CPU
-tensors under gloo with 2 or 3 ranks.  Each rank's local detect result is produced by the
-float64 oracle over the points whose 128-id block the rank owns (block % world == rank,
-the library's sharding rule); the gathered pieces must reassemble the single-rank
-oracle result: MIN of the per-waypoint keys = global min / argmin, gathered offsets =
-per-rank block structure, padded records = each rank's records.  The device merge kernel
-itself is checked bit-exactly on the GPU (test_gpu_fp32.py::test_virtual_ranks_merge_bitexact).
+Each rank's local detect result comes from the float64 oracle over the points whose
+128-id block the rank owns (block % world == rank, the library's sharding rule).  The rank
+packs it exactly as the library's exchange does -- header = [wp_offsets (n_wp + 1) |
+wp_key (n_wp)] int64, records padded to the stride S = ceil(capacity / world) -- and
+one host all-gather per piece runs through the same gloo callback the GPU dry run and
+bench.py --comm host install (gcdf_dist_init_host).  The gathered bytes must reassemble
+the single-rank oracle result by the merge rule (MIN of the keys = global min / smallest-id
+argmin, summed offsets, records merged by (wp, pt)).  The library's merge kernel itself is
+checked bit for bit on the GPU (test_gpu_dist.py, test_gpu_fp32.py).
 """
 import os
 import socket
@@ -50,11 +53,21 @@ def _records(d, n_wp):
     return torch.from_numpy(rec.view(np.uint8).reshape(-1, 48).copy())
 
 
+def gloo_allgather(world):
+    """The host all-gather of the test exchange backend (also in bench.py --comm host)."""
+    def allgather(send, recv):
+        n = send.shape[0]
+        parts = [torch.empty(n, dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(send.copy()))
+        for r in range(world):
+            recv[r * n:(r + 1) * n] = parts[r].numpy()
+    return allgather
+
+
 def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2601_18548_b200.dist import gather_parts
         cfg = synth.get_config("C1")
         pts, _ = synth.make_scene_points(cfg)
         Q = synth.make_waypoints(cfg).reshape(-1, 9)
@@ -67,11 +80,19 @@ def _worker(rank, world, port, q):
         key = np.full(n_wp, np.iinfo(np.int64).max, dtype=np.int64)
         ok = d["wp_argmin"] >= 0
         key[ok] = _ord_key(d["wp_min"][ok], d["wp_argmin"][ok])
-        local = {"records": _records(d, n_wp), "wp_offsets": torch.from_numpy(d["wp_offsets"]),
-                 "wp_key": torch.from_numpy(key)}
-        parts = gather_parts(local, n_wp)
+        capacity = 400                       # the caller's capacity of the gathered result
+        S = -(-capacity // world)            # exchange stride (records per rank)
+        hdr = np.concatenate([d["wp_offsets"].astype(np.int64), key]).view(np.uint8)
+        rec = _records(d, n_wp).numpy()[:S]
+        rec = np.concatenate([rec, np.zeros((S - rec.shape[0], 48), np.uint8)]) if rec.shape[0] < S else rec
+        ag = gloo_allgather(world)
+        hdr_all = np.empty(world * hdr.size, np.uint8)
+        rec_all = np.empty(world * S * 48, np.uint8)
+        ag(hdr, hdr_all)
+        ag(rec.reshape(-1), rec_all)
         if rank == 0:
-            q.put({k: (v.numpy() if torch.is_tensor(v) else v) for k, v in parts.items()})
+            q.put({"world": world, "stride": S, "hdr": hdr_all.view(np.int64).reshape(world, 2 * n_wp + 1),
+                   "records": rec_all.reshape(world, S, 48)})
     finally:
         dist.destroy_process_group()
 
@@ -98,15 +119,17 @@ def test_gather_protocol(world):
     m = oracle.MLP(synth.weights_path(cfg.H))
     ref = m.detect(pts, ids, Q, DELTA, synth.load_tau("C1"))
     n_wp = Q.shape[0]
-    assert parts["world"] == world and parts["count"] == ref["count"]
+    hdr = parts["hdr"]
+    offs = hdr[:, : n_wp + 1]
+    assert parts["world"] == world and offs[:, -1].sum() == ref["count"]
+    assert np.all(offs[:, -1] <= parts["stride"])
     # MIN-reduced keys = global min / smallest-id argmin (the per-rank min is over owned ids)
-    key = parts["wp_key"].astype(np.int64).view(np.uint64) ^ np.uint64(1 << 63)
+    key = hdr[:, n_wp + 1:].min(axis=0).view(np.uint64) ^ np.uint64(1 << 63)
     arg = (key & np.uint64(0xFFFFFFFF)).astype(np.int64)
-    assert np.array_equal(arg, ref["wp_argmin"])
-    offs = parts["offsets"].reshape(world, n_wp + 1)
+    assert np.array_equal(np.where(key == np.uint64(0xFFFFFFFFFFFFFFFF), -1, arg), ref["wp_argmin"])
     assert np.array_equal(offs.sum(0), ref["wp_offsets"])
     # the padded gathered records of each rank, merged by (wp, pt), equal the reference
-    rec = parts["records"].reshape(world, parts["stride"], 48)
+    rec = parts["records"]
     allrec = []
     for r in range(world):
         n = offs[r, -1]

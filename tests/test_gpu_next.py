@@ -156,7 +156,7 @@ def test_detect_graph_recaptures_after_weight_reload():
     cfg = synth.get_config("C2")
     pts, _ = synth.make_scene_points(cfg)
     q = synth.make_waypoints(cfg)[:, :8]
-    tau = synth.load_tau(cfg.name)
+    tau = 2.0  # f - delta <= 2 holds for a large share of the pairs of all three networks
     ctx = _ctx(cfg, 2)
     ctx.update_scene(pts)
     qd = torch.from_numpy(q).cuda()

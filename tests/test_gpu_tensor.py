@@ -90,10 +90,18 @@ def stats_and_gates(v, g, exact, emu, prec, what="", agree_min=0.85, kink_emu=KI
     # 16-bit rounding-boundary / ReLU-kink flips (8x more frequent but 8x smaller for fp16)
     assert st["emu_val_p50"] <= 1e-6, st
     assert st["emu_val_agree_1e-5"] >= agree_min, st
-    assert st["emu_val_max"] <= (1e-2 if prec == "fp16" else 3e-2), st
-    # bf16: layer 1 runs on split bf16 operands (~16-bit effective precision, not the EMU
-    # model's exact layer 1), which moves a few more ReLU kinks
-    assert st["emu_grad_p99"] <= (1e-2 if prec == "fp16" else 5e-2), st
+    # fp16: fixed bounds; bf16 (R28): the GPU may differ from the emulation by no more than the
+    # operand type itself differs from the exact network (layer 1 runs on split bf16 operands,
+    # ~16-bit effective precision, not the EMU model's exact layer 1, which moves more kinks)
+    if prec == "fp16":
+        assert st["emu_val_max"] <= 1e-2, st
+        assert st["emu_grad_p99"] <= 1e-2, st
+    else:
+        type_grad_p99 = float(np.percentile(np.linalg.norm(emu["g"] - exact["g"], axis=-1)
+                                            / np.maximum(1.0, gn_exact), 99))
+        st["type_only_grad_p99"] = type_grad_p99
+        assert st["emu_val_max"] <= st["type_only_val_max"], st
+        assert st["emu_grad_p99"] <= type_grad_p99, st
     assert st["gpu_branch_differs"] <= (0.01 if prec == "fp16" else 0.05), st
     # gate 2: the north-star value tolerance where the operand type can meet it (fp16);
     # otherwise (bf16) the type's own error + 5e-3 (R28)
