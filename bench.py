@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--partition-radius", type=float, default=1.8,
                     help="also time the range-partitioned detect (NEXT-1) at this radius; 0 = skip")
+    ap.add_argument("--no-kernels", dest="kernels", action="store_false",
+                    help="skip the standalone K1 / K3 HBM measurements of the default run")
     ap.add_argument("--no-variants", dest="variants", action="store_false",
                     help="skip the softplus / H = 256 variant measurements (NEXT-4) of the default run")
     ap.add_argument("--latency-calls", type=int, default=50,
@@ -341,21 +343,26 @@ def main():
     peaks, peak_src = measured_peaks()
     local_pairs = n_wp * (n_live_total / a.steps) / world
     if prec in ("bf16", "fp16", "fp16x3"):
-        # fp16x3 (K2c): the split arithmetic runs every hidden GEMM 3 times (R25)
+        # algorithmic flops: the method's ten H x H GEMMs per pair; fp16x3 (K2c)
+        # executes each of them 3 times (the split, R25): reported as a side field
         n_terms = 3 if prec == "fp16x3" else 1
-        flops = n_terms * FLOPS_PAIR_TENSOR[cfg.H] * local_pairs
+        flops = FLOPS_PAIR_TENSOR[cfg.H] * local_pairs
         achieved = flops / (mlp_ms / mlp_n / 1e3) / 1e12
-        # the kernel is timed back to back over the whole timed region: the sustained figure
-        # applies once that region lasts seconds (B200_PROFILING.md); fp16 and bf16 share the
-        # same dense tensor peak on B200 (nominal 2.25 PFLOP/s each), so the bf16 figure is used
-        key = "bf16_tflops_sustained" if t_max > 2000 else "bf16_tflops"
-        peak = float(peaks.get(key))
+        # peak: the measured BURST dense figure (the higher, stricter one) whatever the length of
+        # the timed region; the fraction of the sustained figure is a side field.  fp16 and bf16
+        # share the same dense tensor peak on B200 (nominal 2.25 PFLOP/s each)
+        peak = float(peaks.get("bf16_tflops"))
+        peak_s = float(peaks.get("bf16_tflops_sustained", peak))
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": None, "peak_source": f"{peak_src} {key} (MEASURED_PEAKS.json; fp16 dense = bf16 dense)",
+                "frac_of_sustained_peak": achieved / peak_s,
+                "traffic": None, "peak_source": f"{peak_src} bf16_tflops (MEASURED_PEAKS.json burst; fp16 dense = bf16 dense)",
                 "kernel": ("k_mlp_tc3" if n_terms == 3 else "k_mlp_tc_sp" if act == 2 else
                            "k_mlp_tc_wide" if cfg.H == 256 else "k_mlp_tc") +
                           " (fused transform + MLP fwd/bwd + threshold/min/compaction)",
-                "kernel_ms_avg": mlp_ms / mlp_n, "flops_per_pair": n_terms * FLOPS_PAIR_TENSOR[cfg.H]}
+                "kernel_ms_avg": mlp_ms / mlp_n, "flops_per_pair": FLOPS_PAIR_TENSOR[cfg.H]}
+        if n_terms > 1:
+            roof["executed_flops_per_pair"] = n_terms * FLOPS_PAIR_TENSOR[cfg.H]
+            roof["executed_frac"] = n_terms * achieved / peak
     else:
         sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
         peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12   # FP32 FFMA: 148 SMs x 128 lanes x 2 flops x clock
@@ -468,9 +475,10 @@ def main():
     variants = None
     if world == 1 and a.variants and a.activation == "relu" and not hidden and prec == "fp16":
         variants = {}
-        for name, act_v, h_v in (("softplus", 2, None), ("hidden256", 1, 256)):
+        for name, act_v, h_v, prec_v in (("softplus", 2, None, FP16), ("hidden256", 1, 256, FP16),
+                                         ("fp16x3", 1, None, FP16X3)):
             cfg_v = dataclasses.replace(cfg, H=h_v) if h_v else cfg
-            ctx_v = Context(local, precision=FP16, scene_capacity=cfg.M + slack, max_waypoints=n_wp,
+            ctx_v = Context(local, precision=prec_v, scene_capacity=cfg.M + slack, max_waypoints=n_wp,
                             max_active=max_active)
             ctx_v.load_weights(synth.weights_path(cfg_v.H, act=act_v))
             ctx_v.update_scene(pts)
@@ -494,15 +502,63 @@ def main():
             pairs_v = ctx_v.scene_info()["n_live"] * n_wp
             ach = FLOPS_PAIR_TENSOR[cfg_v.H] * pairs_v / (k_ms / k_n / 1e3) / 1e12
             pk = float(peaks.get("bf16_tflops"))
-            variants[name] = {"kernel": "k_mlp_tc_sp" if act_v == 2 else "k_mlp_tc_wide", "hidden": cfg_v.H,
+            variants[name] = {"kernel": "k_mlp_tc_sp" if act_v == 2 else "k_mlp_tc3" if prec_v == FP16X3
+                              else "k_mlp_tc_wide", "hidden": cfg_v.H,
                               "activation": "softplus" if act_v == 2 else "relu", "ms_per_step": ms_v,
+                              "precision": "fp16x3 (fp32-accurate split, R25)" if prec_v == FP16X3 else "fp16",
                               "value": pairs_v / (ms_v / 1e3), "unit": "queries/s", "tau": tau_v,
                               "active_per_step": int(ov["count"].item()),
                               "roofline": {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
                                            "frac": ach / pk, "flops_per_pair": FLOPS_PAIR_TENSOR[cfg_v.H]}}
+            if prec_v == FP16X3:
+                variants[name]["roofline"].update(executed_flops_per_pair=3 * FLOPS_PAIR_TENSOR[cfg_v.H],
+                                                  executed_frac=3 * ach / pk)
             ctx_v.close()
             del outs_v
             torch.cuda.empty_cache()
+
+    # the HBM-bound standalone stages on the same workload: K1 pair generation +
+    # base-frame transform (16 B written per pair, points read once) and K3 threshold + min +
+    # compaction over the dense values / gradients of one query (4 B read per pair + 36 B
+    # gradient read + 48 B record written per active).  Device time per call (CUDA events,
+    # L2 flushed before each), achieved algorithmic GB/s vs the measured copy bandwidth.
+    kernels = None
+    if world == 1 and a.kernels:
+        kernels = {}
+        hbm = float(peaks.get("hbm_gbs"))
+        lbnd = ctx.scene_info()["local_bound"]
+        n_live = ctx.scene_info()["n_live"]
+
+        def time_calls(fn, k=5):
+            fn()
+            torch.cuda.synchronize()
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+            for e0, e1 in evs:
+                flush.zero_()
+                e0.record()
+                fn()
+                e1.record()
+            torch.cuda.synchronize()
+            return sorted(e0.elapsed_time(e1) for e0, e1 in evs)[k // 2]
+        pg = torch.empty((n_wp, lbnd, 4), dtype=torch.float32, device=dev)
+        ms1 = time_calls(lambda: ctx.pairgen_transform(q, out=pg))
+        b1 = 16 * n_wp * lbnd + 16 * lbnd
+        kernels["k1_pairgen_transform"] = {"ms": ms1, "algorithmic_bytes": b1, "achieved_gbs": b1 / ms1 / 1e6,
+                                           "peak_gbs": hbm, "frac": b1 / ms1 / 1e6 / hbm,
+                                           "bytes_per_unit": "16 B written per (waypoint, slot) pair + 16 B per slot read"}
+        del pg
+        vals, grs = ctx.query_values_grads(q)
+        outs_k = ctx.alloc_detect_outputs(n_wp, max_active)
+        ms3 = time_calls(lambda: ctx.compact_dense(vals, grs, delta, tau, outputs=outs_k, sync_count=False))
+        n3 = int(outs_k["count"].item())
+        b3 = 4 * n_wp * lbnd + n3 * (36 + 48)
+        kernels["k3_compact_dense"] = {"ms": ms3, "algorithmic_bytes": b3, "achieved_gbs": b3 / ms3 / 1e6,
+                                       "peak_gbs": hbm, "frac": b3 / ms3 / 1e6 / hbm, "active": n3,
+                                       "live_pairs": n_live * n_wp,
+                                       "bytes_per_unit": "4 B value read per pair + (36 B gradient read + 48 B record "
+                                                         "written) per active"}
+        del vals, grs, outs_k
+        torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -522,6 +578,7 @@ def main():
             "detect_latency": lat,
             "partitioned": part,
             "variants": variants,
+            "kernels": kernels,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_pairs / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": h2d // e2e_steps,
                     "d2h_bytes_per_step": d2h // e2e_steps, "steps": e2e_steps},

@@ -109,6 +109,7 @@ struct gcdf_ctx {
   float part_r = -1.f;
   int64_t scene_version = 0;   // bumped by every scene change (captured graphs re-capture)
   int64_t weights_version = 0; // bumped by gcdf_load_weights / gcdf_bind_workspace (same)
+  uint32_t k3_epoch = 0;       // call epoch of the standalone K3's look-back status words
   bool exchange = false;       // exchange buffers reserved (world > 1 or opt.exchange)
   Comm comm;                   // gcdf_dist_init* (kind kCommNone until then)
   std::vector<cudaEvent_t> xev;  // exchange-step timing pairs (gcdf_profile_read_exchange)
@@ -1128,6 +1129,13 @@ int gcdf_detect_active_set_host(gcdf_ctx *c, const float *q_host, int32_t B, int
   return GCDF_OK;
 }
 
+// 24-bit call epoch of the K3 look-back (never 0: zeroed memory is "not published")
+static uint32_t next_epoch(gcdf_ctx *c) {
+  c->k3_epoch = (c->k3_epoch + 1) & 0xffffffu;
+  if (c->k3_epoch == 0) c->k3_epoch = 1;
+  return c->k3_epoch;
+}
+
 int gcdf_compact_dense(gcdf_ctx *c, const float *values, const float *grads, int32_t n_wp, int64_t stride,
                        float delta, float tau, gcdf_active_t *out, int64_t cap, int64_t *offs, float *wmin,
                        int64_t *warg, int64_t *wkey, int64_t *count_dev, int64_t *count_host, void *stream) {
@@ -1145,8 +1153,7 @@ int gcdf_compact_dense(gcdf_ctx *c, const float *values, const float *grads, int
   int nl = 0;
   if ((rc = count_launch(c,
                          launch_compact_dense(values, grads, stride, n_wp, tpw, sv, delta, tau, ds, out, cap, offs,
-                                              wmin, warg, wkey, count_dev,
-                                              reinterpret_cast<int64_t *>(c->ws + c->L.wp_count), s, &nl),
+                                              wmin, warg, wkey, count_dev, next_epoch(c), s, &nl),
                          "compact kernels", 0)))
     return rc;
   c->launches += nl;

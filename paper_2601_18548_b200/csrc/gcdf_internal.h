@@ -161,7 +161,7 @@ cudaError_t launch_compact_dense(const float *values, const float *grads, int64_
                                  int32_t tiles_per_wp, SceneView scene, float delta, float tau,
                                  DetectScratch ds, gcdf_active_t *out, int64_t out_capacity, int64_t *wp_offsets,
                                  float *wp_min, int64_t *wp_argmin, int64_t *wp_key, int64_t *count,
-                                 int64_t *fin_scratch, cudaStream_t s, int *n_launches);
+                                 uint32_t epoch, cudaStream_t s, int *n_launches);
 cudaError_t launch_sparse_jacobian(const gcdf_active_t *recs, const int64_t *count, int64_t cap, float delta,
                                    float *c, int64_t *row_ptr, int32_t *col, float *val, int num_sms,
                                    cudaStream_t s);

@@ -29,23 +29,37 @@ __global__ void k_detect_init(unsigned long long *wp_key, unsigned long long *co
 }
 
 
-// K3 standalone over dense values: one WARP per tile of 128 slots, 4 slots per lane
-// (one 16-B streaming load), no block barrier.  The tile's actives are ranked in slot
-// order by a warp prefix scan of per-lane counts (the "warp-ballot and prefix-sum"
-// compaction); the per-waypoint min key is a warp-shuffle min + one atomicMin per tile.
-// A value of +INF marks a dead slot (gcdf_query_values_grads writes +INF there).
-// ---- standalone K3 (A6-A8 over dense values): two passes, no staging and no global counter.
-// Pass 1: a warp takes kGroup consecutive tiles (128 slots, 4 per lane, float4 streaming
-// loads all in flight), writes each tile's active count to tile_meta and folds the
-// per-waypoint minimum key (one atomicMin per waypoint run in the group).  The chunk scan
-// of the finalize turns the counts into output offsets; pass 2 re-reads the values of the
-// tiles with records and writes the records straight to their final positions.
-constexpr int kGroup = 4;
+// ---- standalone K3 (A6-A8 over dense values): ONE pass, decoupled look-back.
+// A partition = kLbWarps warps x kLbTW consecutive tiles (128 slots, 4 per lane, one 16-B
+// streaming load each) of the flat (step, tile) order; partitions are taken in order from
+// a global counter, so a partition only ever waits on partitions already running.  Each
+// warp ballots its tiles' actives (f - delta <= tau; dead slots hold +INF and never pass)
+// and folds the per-step minimum key; the CTA publishes its active count, looks back over
+// the predecessors' published counts / inclusive prefixes (32 at a time, one per lane) for
+// its exclusive prefix, publishes its own inclusive prefix, and the lanes with actives read
+// their 36-B gradient rows and write their records straight to their final positions --
+// the values are read once, the gradients only for actives, nothing else touches HBM.
+// Records in (step, slot) order = the canonical (wp, pt) order; wp_offsets[w] is the prefix
+// at the step's first tile.
+constexpr int kLbWarps = 8, kLbTW = 4, kLbTiles = kLbWarps * kLbTW;
+// status word of a partition: [63:40] call epoch, [39:38] 1 = count, 2 = inclusive prefix, [37:0] value
+constexpr int kLbAgg = 1, kLbPre = 2;
+__device__ __forceinline__ unsigned long long lb_word(uint32_t epoch, int flag, int64_t v) {
+  return ((unsigned long long)(epoch & 0xffffffu) << 40) | ((unsigned long long)flag << 38) | (unsigned long long)v;
+}
+__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // values of tile tw (0-based within step w) for this lane's 4 slots (+INF outside the scene)
 __device__ __forceinline__ float4 load_tile_values(const float *__restrict__ values, int64_t stride, int64_t lb,
-                                                   int w, int64_t tw, int lane, int64_t &slot0) {
-  slot0 = tw * kTile + 4 * lane;
+                                                   int w, int64_t tw, int lane) {
+  const int64_t slot0 = tw * kTile + 4 * lane;
   const float *vrow = values + (int64_t)w * stride;
   const float inf = __int_as_float(0x7f800000);
   float4 v = make_float4(inf, inf, inf, inf);
@@ -59,109 +73,178 @@ __device__ __forceinline__ float4 load_tile_values(const float *__restrict__ val
   return v;
 }
 
-__global__ void __launch_bounds__(256, 4) k_compact_count(const float *__restrict__ values, int64_t stride,
+__global__ void __launch_bounds__(256) k_compact_lookback(const float *__restrict__ values,
+                                                          const float *__restrict__ grads, int64_t stride,
                                                           int32_t n_wp, int32_t tpw, SceneView scene, float delta,
-                                                          float tau, DetectScratch ds) {
+                                                          float tau, unsigned long long *__restrict__ wp_key,
+                                                          unsigned long long *part_ctr, unsigned long long *status,
+                                                          uint32_t epoch, gcdf_active_t *__restrict__ out, int64_t cap,
+                                                          int64_t *__restrict__ wp_offsets, int64_t *__restrict__ count) {
+  __shared__ int64_t s_part, s_excl;
+  __shared__ int32_t s_wcnt[kLbWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nwb = blockDim.x >> 5;  // warps per CTA
+  if (threadIdx.x == 0) s_part = (int64_t)atomicAdd(part_ctr, 1ull);
+  __syncthreads();
+  const int64_t p = s_part;
   const int64_t n_tiles = (int64_t)n_wp * tpw;
-  const int64_t n_groups = (n_tiles + kGroup - 1) / kGroup;
-  // each CTA takes a contiguous range of groups and its warps interleave over it (warp j takes
-  // groups j, j + 8, ...): the CTA streams contiguous memory (DRAM row locality, as a grid-
-  // stride reduction does), while each warp stays on one step for long runs and folds the
-  // step's minimum locally (atomicMin only when the step changes)
-  const int64_t per = (n_groups + gridDim.x - 1) / gridDim.x;
-  const int64_t C0 = (int64_t)blockIdx.x * per, C1 = min(C0 + per, n_groups);
-  const int64_t G0 = C0 + warp;
-  if (G0 >= C1) return;
+  const int64_t T0 = p * kLbTiles + (int64_t)warp * kLbTW;  // this warp's first flat tile
   const int64_t lb = scene.local_bound;
-  const int step_tiles = kGroup * nwb;  // tile advance between a warp's consecutive groups
-  int wcur = (int)(G0 * kGroup / tpw);
-  unsigned long long key = ~0ull;
-  float lmin = __int_as_float(0x7f800000);  // this lane's minimum of the current step and its slot
-  uint32_t lslot = 0u;
-  auto flush_key = [&]() {
-    if (lmin != __int_as_float(0x7f800000))
-      key = ((unsigned long long)ord_f32(lmin) << 32) |
-            (unsigned long long)local_to_global(lslot, scene.rank, scene.world);
-    lmin = __int_as_float(0x7f800000);
+  const uint32_t lt = (1u << lane) - 1u;
+  int w0 = (int)(T0 / tpw);
+  int t0 = (int)(T0 - (int64_t)w0 * tpw);
+  // ---- loads: the warp's kLbTW tiles, all in flight
+  float4 v[kLbTW];
+  {
+    int w = w0, t = t0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-      key = other < key ? other : key;
+    for (int i = 0; i < kLbTW; ++i) {
+      if (T0 + i < n_tiles) v[i] = load_tile_values(values, stride, lb, w, t, lane);
+      if (++t == tpw) { t = 0; ++w; }
     }
-    if (lane == 0 && key != ~0ull) atomicMin(ds.wp_key + wcur, key);
-    key = ~0ull;
-  };
-  // (step, tile in step) of the first tile of the next group to load / to process; advanced
-  // incrementally (no 64-bit divisions per tile)
-  int lw = wcur, pw = wcur;
-  int lt = (int)(G0 * kGroup - (int64_t)lw * tpw), pt = lt;
-  auto advance = [&](int &w, int &t, int by) {
-    t += by;
-    while (t >= tpw) {
-      t -= tpw;
-      ++w;
-    }
-  };
-  auto load_group = [&](int64_t G, float4 (&vv)[kGroup]) {
-    if (G < C1) {
-      int w = lw, t = lt;
-#pragma unroll
-      for (int i = 0; i < kGroup; ++i) {
-        if (G * kGroup + i < n_tiles) {
-          int64_t s0;
-          vv[i] = load_tile_values(values, stride, lb, w, t, lane, s0);
-        }
-        advance(w, t, 1);
-      }
-    }
-    advance(lw, lt, step_tiles);
-  };
-  auto process = [&](int64_t G, const float4 (&vv)[kGroup]) {
-    const int64_t T0 = G * kGroup;
-    const int nt = (int)min((int64_t)kGroup, n_tiles - T0);  // tiles of this group in range
-    int w = pw, tt = pt;
-    advance(pw, pt, step_tiles);
-#pragma unroll
-    for (int i = 0; i < kGroup; ++i) {
-      if (i >= nt) break;
-      if (w != wcur) {
-        flush_key();
-        wcur = w;
-      }
-      const float4 x = vv[i];
-      // minimum: the lane's smallest value and its slot, first (smallest slot) on ties -- a
-      // min of the four values, and the slot search only when it improves (rare)
-      const float m4 = fminf(fminf(x.x, x.y), fminf(x.z, x.w));
-      if (m4 < lmin) {
-        lmin = m4;
-        lslot = (uint32_t)tt * kTile + 4u * lane + (x.x == m4 ? 0u : x.y == m4 ? 1u : x.z == m4 ? 2u : 3u);
-      }
-      // active: f - delta <= tau (dead slots are +INF and never pass); the tile's bitmap (word
-      // k = ballot of slot 4 lane + k) lets pass 2 skip re-reading the values
-      const uint32_t b0 = __ballot_sync(0xffffffffu, x.x - delta <= tau);
-      const uint32_t b1 = __ballot_sync(0xffffffffu, x.y - delta <= tau);
-      const uint32_t b2 = __ballot_sync(0xffffffffu, x.z - delta <= tau);
-      const uint32_t b3 = __ballot_sync(0xffffffffu, x.w - delta <= tau);
-      if (lane == 0) {
-        const int64_t T = T0 + i;
-        ds.tile_meta[T] = make_int2(0, __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3));
-        ds.tile_bits[T] = make_uint4(b0, b1, b2, b3);
-      }
-      advance(w, tt, 1);
-    }
-  };
-  // two register sets in ping-pong (no register copies, which would wait for the loads)
-  float4 va[kGroup], vb[kGroup];
-  load_group(G0, va);
-  for (int64_t G = G0; G < C1; G += 2 * nwb) {
-    load_group(G + nwb, vb);
-    process(G, va);
-    load_group(G + 2 * nwb, va);
-    if (G + nwb < C1) process(G + nwb, vb);
   }
-  flush_key();
+  // ---- ballots, counts, per-step minimum (one atomicMin per step run of the warp)
+  uint32_t bits[kLbTW];  // this lane's 4 active flags per tile (bit k = slot 4 lane + k)
+  int below[kLbTW];      // actives of the lower lanes in the tile
+  int cnt[kLbTW];        // actives of the tile
+  int wtot = 0;
+  {
+    int w = w0, t = t0;
+    unsigned long long key = ~0ull;
+    int wk = w0;
+    auto flush = [&]() {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+        key = other < key ? other : key;
+      }
+      if (lane == 0 && key != ~0ull) atomicMin(wp_key + wk, key);
+      key = ~0ull;
+    };
+#pragma unroll
+    for (int i = 0; i < kLbTW; ++i) {
+      bits[i] = 0u;
+      below[i] = cnt[i] = 0;
+      if (T0 + i < n_tiles) {  // (uniform over the warp)
+        if (w != wk) {
+          flush();
+          wk = w;
+        }
+        const float x[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t b = __ballot_sync(0xffffffffu, x[k] - delta <= tau);
+          bits[i] |= ((b >> lane) & 1u) << k;
+          below[i] += __popc(b & lt);
+          cnt[i] += __popc(b);
+        }
+        // minimum of the lane's four (first slot on ties), as a key with the global id
+        const float m4 = fminf(fminf(x[0], x[1]), fminf(x[2], x[3]));
+        if (m4 != __int_as_float(0x7f800000)) {
+          const int kk = x[0] == m4 ? 0 : x[1] == m4 ? 1 : x[2] == m4 ? 2 : 3;
+          const unsigned long long kx =
+              ((unsigned long long)ord_f32(m4) << 32) |
+              (unsigned long long)local_to_global((int64_t)t * kTile + 4 * lane + kk, scene.rank, scene.world);
+          key = kx < key ? kx : key;
+        }
+        wtot += cnt[i];
+      }
+      if (++t == tpw) { t = 0; ++w; }
+    }
+    flush();
+  }
+  if (lane == 0) s_wcnt[warp] = wtot;
+  __syncthreads();
+  // ---- decoupled look-back (warp 0): exclusive prefix of this partition
+  if (warp == 0) {
+    int64_t agg = 0;
+#pragma unroll
+    for (int j = 0; j < kLbWarps; ++j) agg += s_wcnt[j];
+    unsigned long long *const st = status + p;
+    if (p == 0) {
+      if (lane == 0) st_release(st, lb_word(epoch, kLbPre, agg));
+      if (lane == 0) s_excl = 0;
+    } else {
+      if (lane == 0) st_release(st, lb_word(epoch, kLbAgg, agg));
+      int64_t excl = 0;
+      for (int64_t base = p - 1;; base -= 32) {
+        const int64_t idx = base - lane;
+        unsigned long long wd = lb_word(epoch, kLbPre, 0);  // (idx < 0: never reached past partition 0)
+        if (idx >= 0) {
+          do {
+            wd = ld_acquire(status + idx);
+          } while ((uint32_t)(wd >> 40) != (epoch & 0xffffffu) || ((wd >> 38) & 3u) == 0u);
+        }
+        __syncwarp();
+        const unsigned pm = __ballot_sync(0xffffffffu, ((wd >> 38) & 3u) == (unsigned)kLbPre);
+        const int stop = pm ? __ffs(pm) - 1 : 32;
+        int64_t val = lane <= stop ? (int64_t)(wd & ((1ull << 38) - 1ull)) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        excl += val;
+        if (pm) break;
+      }
+      if (lane == 0) {
+        st_release(st, lb_word(epoch, kLbPre, excl + agg));
+        s_excl = excl;
+      }
+    }
+  }
+  __syncthreads();
+  int64_t pos = s_excl;
+  for (int j = 0; j < warp; ++j) pos += s_wcnt[j];
+  // ---- offsets and records
+  int w = w0, t = t0;
+#pragma unroll
+  for (int i = 0; i < kLbTW; ++i) {
+    const int64_t T = T0 + i;
+    if (T < n_tiles) {
+      if (t == 0 && lane == 0) wp_offsets[w] = pos;
+      if (T == n_tiles - 1 && lane == 0) {
+        wp_offsets[n_wp] = pos + cnt[i];
+        *count = pos + cnt[i];
+      }
+      unsigned b = bits[i];
+      int64_t r = pos + below[i];
+      while (b) {  // (a lane has ~0.04 actives per tile at 1 % active)
+        const int k = __ffs(b) - 1;
+        b &= b - 1u;
+        const float xk = k == 0 ? v[i].x : k == 1 ? v[i].y : k == 2 ? v[i].z : v[i].w;
+        const int64_t slot = (int64_t)t * kTile + 4 * lane + k;
+        if (r < cap) {
+          const float *g = grads + ((int64_t)w * stride + slot) * kNdof;
+          float gg[kNdof];
+#pragma unroll
+          for (int e = 0; e < kNdof; ++e) gg[e] = __ldcs(g + e);
+          float4 *dst = reinterpret_cast<float4 *>(out + r);
+          dst[0] = make_float4(xk, gg[0], gg[1], gg[2]);
+          dst[1] = make_float4(gg[3], gg[4], gg[5], gg[6]);
+          dst[2] = make_float4(gg[7], gg[8], __uint_as_float((unsigned)w),
+                               __uint_as_float((unsigned)local_to_global(slot, scene.rank, scene.world)));
+        }
+        ++r;
+      }
+      pos += cnt[i];
+    }
+    if (++t == tpw) { t = 0; ++w; }
+  }
+}
+
+// per-step min / argmin / key export of the standalone K3; with no tile at all (empty
+// scene) also the zero offsets and count
+__global__ void k_compact_keys(const unsigned long long *__restrict__ keys, int32_t n_wp, bool no_tiles,
+                               float *wp_min, int64_t *wp_argmin, int64_t *wp_key_out, int64_t *wp_offsets,
+                               int64_t *count) {
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w <= n_wp; w += gridDim.x * blockDim.x) {
+    if (no_tiles) {
+      wp_offsets[w] = 0;
+      if (w == n_wp) *count = 0;
+    }
+    if (w == n_wp) continue;
+    const unsigned long long k = keys[w];
+    if (wp_min) wp_min[w] = k == ~0ull ? __int_as_float(0x7f800000) : unord_f32((unsigned)(k >> 32));
+    if (wp_argmin) wp_argmin[w] = k == ~0ull ? -1 : (int64_t)(k & 0xffffffffull);
+    if (wp_key_out) wp_key_out[w] = (int64_t)(k ^ 0x8000000000000000ull);
+  }
 }
 
 // ---- finalize: per-tile (staging base, count) -> ordered output.  Tiles of step w are
@@ -170,7 +253,6 @@ __global__ void __launch_bounds__(256, 4) k_compact_count(const float *__restric
 // on n_wp * nch CTAs instead of n_wp.
 constexpr int kFinPer = 8;
 constexpr int kFinChunk = 256 * kFinPer;
-constexpr int kWB = 2;  // tiles per warp step of the standalone K3 write pass
 
 __device__ __forceinline__ void tile_range(const int64_t *tile_start, int32_t tpw, int w, int64_t &t0, int64_t &nt) {
   t0 = tile_start ? tile_start[w] : (int64_t)w * tpw;
@@ -254,111 +336,6 @@ __global__ void __launch_bounds__(256) k_fin_scatter(const int2 *__restrict__ me
       }
     }
     pos += m[i].y;
-  }
-}
-
-// pass 2 of the standalone K3: chunk (w, c) of kFinChunk tiles; the tile offsets come from a
-// block scan of the pass-1 counts, then a warp per tile reads the tile's 16-B active bitmap
-// (pass 1) -- not its values -- ranks the actives with popcounts of the bitmap words, and the
-// lanes with actives read their values and gradients and write the records at
-// out[cpre + tile offset + rank].
-__global__ void __launch_bounds__(256, 3) k_compact_write(const float *__restrict__ values,
-                                                       const float *__restrict__ grads, int64_t stride, int32_t tpw,
-                                                       int64_t nch, const int64_t *__restrict__ cpre,
-                                                       const int2 *__restrict__ meta,
-                                                       const uint4 *__restrict__ tbits, SceneView scene,
-                                                       gcdf_active_t *__restrict__ out, int64_t cap) {
-  __shared__ int64_t sh[32];
-  __shared__ int32_t tpos[kFinChunk];
-  const int w = blockIdx.y;
-  const int64_t c = blockIdx.x;
-  const int64_t t0 = (int64_t)w * tpw, nt = tpw;
-  if (c * kFinChunk >= nt) return;  // (uniform over the block)
-  const int64_t b = c * kFinChunk + (int64_t)threadIdx.x * kFinPer;
-  int cnt[kFinPer];
-  int64_t s = 0;
-#pragma unroll
-  for (int i = 0; i < kFinPer; ++i) {
-    cnt[i] = b + i < nt ? meta[t0 + b + i].y : 0;
-    s += cnt[i];
-  }
-  int64_t tot;
-  int32_t run = (int32_t)block_excl_scan(s, &tot, sh);
-#pragma unroll
-  for (int i = 0; i < kFinPer; ++i) {
-    tpos[threadIdx.x * kFinPer + i] = cnt[i] > 0 ? run : -1;
-    run += cnt[i];
-  }
-  __syncthreads();
-  const int64_t dst0 = cpre[(int64_t)w * nch + c];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t lt = (1u << lane) - 1u;
-  const int64_t tend = min((int64_t)kFinChunk, nt - c * kFinChunk);
-  const float *vrow = values + (int64_t)w * stride;
-  // kWB tiles per step: their bitmaps, then their value and gradient loads are in flight
-  // before the records are written (a lane has usually 0 or 1 active slot per tile;
-  // further ones take the loop at the end)
-  auto write_rec = [&](int64_t r, int64_t slot, float v, const float *gg) {
-    if (r < cap) {
-      float4 *dst = reinterpret_cast<float4 *>(out + r);
-      dst[0] = make_float4(v, gg[0], gg[1], gg[2]);
-      dst[1] = make_float4(gg[3], gg[4], gg[5], gg[6]);
-      dst[2] = make_float4(gg[7], gg[8], __uint_as_float((unsigned)w),
-                           __uint_as_float((unsigned)local_to_global(slot, scene.rank, scene.world)));
-    }
-  };
-  for (int64_t tl0 = warp; tl0 < tend; tl0 += 8 * kWB) {
-    unsigned bits[kWB];
-    int64_t r[kWB];
-#pragma unroll
-    for (int j = 0; j < kWB; ++j) {
-      bits[j] = 0u;
-      r[j] = 0;
-      const int64_t tl = tl0 + 8 * j;
-      const int32_t pos = tl < tend ? tpos[tl] : -1;
-      if (pos < 0) continue;  // no records in this tile (uniform over the warp)
-      const uint4 bw = __ldg(tbits + t0 + c * kFinChunk + tl);
-      const uint32_t wd[4] = {bw.x, bw.y, bw.z, bw.w};
-      r[j] = dst0 + pos;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        bits[j] |= ((wd[k] >> lane) & 1u) << k;
-        r[j] += __popc(wd[k] & lt);  // actives of the lower lanes (all their slots precede this lane's)
-      }
-    }
-    float4 v4[kWB];
-    float gg[kWB][kNdof];
-    int kf[kWB];
-#pragma unroll
-    for (int j = 0; j < kWB; ++j) {  // the first active slot of each tile: value + gradient loads
-      kf[j] = __ffs(bits[j]) - 1;
-      if (bits[j]) {
-        const int64_t slot0 = (c * kFinChunk + tl0 + 8 * j) * kTile + 4 * lane;
-        v4[j] = __ldg(reinterpret_cast<const float4 *>(vrow + slot0));
-        const float *g = grads + ((int64_t)w * stride + slot0 + kf[j]) * kNdof;
-#pragma unroll
-        for (int i = 0; i < kNdof; ++i) gg[j][i] = __ldcs(g + i);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kWB; ++j) {
-      if (!bits[j]) continue;
-      const int64_t slot0 = (c * kFinChunk + tl0 + 8 * j) * kTile + 4 * lane;
-      const float v[4] = {v4[j].x, v4[j].y, v4[j].z, v4[j].w};
-      write_rec(r[j], slot0 + kf[j], v[kf[j]], gg[j]);
-      unsigned rest = bits[j] & (bits[j] - 1u);
-      int64_t rr = r[j] + 1;
-      while (rest) {  // rare: more than one active slot in this lane's four
-        const int k = __ffs(rest) - 1;
-        rest &= rest - 1u;
-        const float *g = grads + ((int64_t)w * stride + slot0 + k) * kNdof;
-        float g2[kNdof];
-#pragma unroll
-        for (int i = 0; i < kNdof; ++i) g2[i] = __ldcs(g + i);
-        write_rec(rr, slot0 + k, v[k], g2);
-        ++rr;
-      }
-    }
   }
 }
 
@@ -474,31 +451,18 @@ cudaError_t launch_compact_dense(const float *values, const float *grads, int64_
                                  int32_t tiles_per_wp, SceneView scene, float delta, float tau,
                                  DetectScratch ds, gcdf_active_t *out, int64_t out_capacity, int64_t *wp_offsets,
                                  float *wp_min, int64_t *wp_argmin, int64_t *wp_key, int64_t *count,
-                                 int64_t *fin_scratch, cudaStream_t s, int *n_launches) {
+                                 uint32_t epoch, cudaStream_t s, int *n_launches) {
   const int64_t n_tiles = (int64_t)n_wp * tiles_per_wp;
-  if (n_tiles <= 0) return cudaSuccess;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // one wave: the warps' contiguous tile ranges are sized for the CTAs that are resident at once
-  int per_sm = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_compact_count, 256, 0) != cudaSuccess || per_sm < 1)
-    per_sm = 1;
-  const int64_t need = (n_tiles + 8 * kGroup - 1) / (8 * kGroup);  // 8 warps per CTA, kGroup tiles each
-  const int64_t grid = need < (int64_t)sms * per_sm ? need : (int64_t)sms * per_sm;
-  k_compact_count<<<(unsigned)grid, 256, 0, s>>>(values, stride, n_wp, tiles_per_wp, scene, delta, tau, ds);
-  const int64_t nch = finalize_chunks(tiles_per_wp);
-  const int64_t n = (int64_t)n_wp * nch;
-  int64_t *csum = fin_scratch, *cpre = fin_scratch + n, *tmp = fin_scratch + 2 * n + 1;
-  const dim3 g2((unsigned)nch, (unsigned)n_wp);
-  k_fin_count<<<g2, 256, 0, s>>>(ds.tile_meta, tiles_per_wp, nullptr, nch, csum);
-  cudaError_t e = excl_scan(csum, n, cpre, cpre + n, tmp, s, n_launches);
-  if (e != cudaSuccess) return e;
-  k_fin_offsets<<<(n_wp + 256) / 256, 256, 0, s>>>(cpre, nch, n_wp, wp_offsets, count, ds.wp_key, wp_min, wp_argmin,
-                                                   wp_key);
-  k_compact_write<<<g2, 256, 0, s>>>(values, grads, stride, tiles_per_wp, nch, cpre, ds.tile_meta, ds.tile_bits, scene,
-                                     out, out_capacity);
-  *n_launches += 4;
+  const int64_t n_parts = (n_tiles + kLbTiles - 1) / kLbTiles;
+  // the partition counter is ds.counter[0] (zeroed by k_detect_init); the status words live
+  // in the tile-bitmap scratch (16 B per tile >= 8 B per partition) and carry the call epoch
+  if (n_parts > 0)
+    k_compact_lookback<<<(unsigned)n_parts, kLbWarps * 32, 0, s>>>(
+        values, grads, stride, n_wp, tiles_per_wp, scene, delta, tau, ds.wp_key, ds.counter,
+        reinterpret_cast<unsigned long long *>(ds.tile_bits), epoch, out, out_capacity, wp_offsets, count);
+  k_compact_keys<<<(n_wp + 256) / 256, 256, 0, s>>>(ds.wp_key, n_wp, n_parts == 0, wp_min, wp_argmin, wp_key,
+                                                    wp_offsets, count);
+  *n_launches += n_parts > 0 ? 2 : 1;
   return cudaGetLastError();
 }
 

@@ -433,7 +433,7 @@ class Context:
         return o
 
     def compact_dense(self, values: torch.Tensor, grads: torch.Tensor, delta: float, tau: float,
-                      capacity: int | None = None, outputs: dict | None = None):
+                      capacity: int | None = None, outputs: dict | None = None, sync_count: bool = True):
         n_wp, stride = int(values.shape[0]), int(values.shape[1])
         if outputs is None:
             outputs = self.alloc_detect_outputs(n_wp, capacity if capacity is not None else self.max_active)
@@ -442,8 +442,9 @@ class Context:
         self._check(self.lib.gcdf_compact_dense(
             self._h, _ptr(values), _ptr(grads), n_wp, stride, float(delta), float(tau), _ptr(o["records"]),
             int(o["capacity"]), _ptr(o["wp_offsets"]), _ptr(o["wp_min"]), _ptr(o["wp_argmin"]), _ptr(o["wp_key"]),
-            _ptr(o["count"]), C.byref(nh), _stream(self.device)))
-        o["n"] = nh.value
+            _ptr(o["count"]), C.byref(nh) if sync_count else None, _stream(self.device)))
+        if sync_count:
+            o["n"] = nh.value
         return o
 
     def merge_active_sets(self, world: int, n_wp: int, recs: torch.Tensor, rec_stride: int,
