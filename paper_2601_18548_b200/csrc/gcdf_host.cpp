@@ -109,7 +109,6 @@ struct gcdf_ctx {
   float part_r = -1.f;
   int64_t scene_version = 0;   // bumped by every scene change (captured graphs re-capture)
   int64_t weights_version = 0; // bumped by gcdf_load_weights / gcdf_bind_workspace (same)
-  uint32_t k3_epoch = 0;       // call epoch of the standalone K3's look-back status words
   bool exchange = false;       // exchange buffers reserved (world > 1 or opt.exchange)
   Comm comm;                   // gcdf_dist_init* (kind kCommNone until then)
   std::vector<cudaEvent_t> xev;  // exchange-step timing pairs (gcdf_profile_read_exchange)
@@ -264,7 +263,6 @@ PartScratch part_view(const gcdf_ctx *c) {
 DetectScratch scratch_view(const gcdf_ctx *c) {
   DetectScratch d{};
   d.tile_meta = reinterpret_cast<int2 *>(c->ws + c->L.meta);
-  d.tile_bits = reinterpret_cast<uint4 *>(c->ws + c->L.cbits);
   d.staging = reinterpret_cast<gcdf_active_t *>(c->ws + c->L.staging);
   d.max_active = c->opt.max_active;
   d.counter = reinterpret_cast<unsigned long long *>(c->ws + c->L.counter);
@@ -421,7 +419,7 @@ int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out) {
   L.wf16x3 = off; off = align256(off + kX3Total);
   L.wf16w = off; off = align256(off + kWideTotal);
   L.meta = off; off = align256(off + (int64_t)o.max_waypoints * c->tiles_cap * 8);
-  L.cbits = off; off = align256(off + (int64_t)o.max_waypoints * c->tiles_cap * 16);
+  L.cbits = off; off = align256(off + k3_scratch_elems(o.max_waypoints, c->tiles_cap) * 8);  // standalone K3
   L.staging = off; off = align256(off + o.max_active * (int64_t)sizeof(gcdf_active_t));
   L.wp_key = off; off = align256(off + (int64_t)o.max_waypoints * 8);
   L.wp_count = off; off = align256(off + finalize_scratch_elems(o.max_waypoints, c->tiles_cap) * 8);
@@ -1129,13 +1127,6 @@ int gcdf_detect_active_set_host(gcdf_ctx *c, const float *q_host, int32_t B, int
   return GCDF_OK;
 }
 
-// 24-bit call epoch of the K3 look-back (never 0: zeroed memory is "not published")
-static uint32_t next_epoch(gcdf_ctx *c) {
-  c->k3_epoch = (c->k3_epoch + 1) & 0xffffffu;
-  if (c->k3_epoch == 0) c->k3_epoch = 1;
-  return c->k3_epoch;
-}
-
 int gcdf_compact_dense(gcdf_ctx *c, const float *values, const float *grads, int32_t n_wp, int64_t stride,
                        float delta, float tau, gcdf_active_t *out, int64_t cap, int64_t *offs, float *wmin,
                        int64_t *warg, int64_t *wkey, int64_t *count_dev, int64_t *count_host, void *stream) {
@@ -1153,7 +1144,8 @@ int gcdf_compact_dense(gcdf_ctx *c, const float *values, const float *grads, int
   int nl = 0;
   if ((rc = count_launch(c,
                          launch_compact_dense(values, grads, stride, n_wp, tpw, sv, delta, tau, ds, out, cap, offs,
-                                              wmin, warg, wkey, count_dev, next_epoch(c), s, &nl),
+                                              wmin, warg, wkey, count_dev,
+                                              reinterpret_cast<int64_t *>(c->ws + c->L.cbits), s, &nl),
                          "compact kernels", 0)))
     return rc;
   c->launches += nl;

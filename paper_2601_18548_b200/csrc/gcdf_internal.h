@@ -70,8 +70,6 @@ struct DetectScratch {
   int64_t max_active;
   unsigned long long *counter;     // [2]: staging allocation counter, overflow flag
   unsigned long long *wp_key;      // [max_waypoints] unsigned order key, ~0 = none
-  uint4 *tile_bits;                // [n_wp * tiles_per_wp] (standalone K3) active-slot bitmap of a
-                                   // tile: word k bit l = slot 4 l + k
 };
 
 // Range-partitioned tile map (NEXT-1): tile T of step w = tile_wp[T] covers candidates
@@ -161,7 +159,8 @@ cudaError_t launch_compact_dense(const float *values, const float *grads, int64_
                                  int32_t tiles_per_wp, SceneView scene, float delta, float tau,
                                  DetectScratch ds, gcdf_active_t *out, int64_t out_capacity, int64_t *wp_offsets,
                                  float *wp_min, int64_t *wp_argmin, int64_t *wp_key, int64_t *count,
-                                 uint32_t epoch, cudaStream_t s, int *n_launches);
+                                 int64_t *k3_scratch, cudaStream_t s, int *n_launches);
+int64_t k3_scratch_elems(int64_t n_wp, int64_t tiles_per_wp);
 cudaError_t launch_sparse_jacobian(const gcdf_active_t *recs, const int64_t *count, int64_t cap, float delta,
                                    float *c, int64_t *row_ptr, int32_t *col, float *val, int num_sms,
                                    cudaStream_t s);

@@ -29,32 +29,21 @@ __global__ void k_detect_init(unsigned long long *wp_key, unsigned long long *co
 }
 
 
-// ---- standalone K3 (A6-A8 over dense values): ONE pass, decoupled look-back.
-// A partition = kLbWarps warps x kLbTW consecutive tiles (128 slots, 4 per lane, one 16-B
-// streaming load each) of the flat (step, tile) order; partitions are taken in order from
-// a global counter, so a partition only ever waits on partitions already running.  Each
-// warp ballots its tiles' actives (f - delta <= tau; dead slots hold +INF and never pass)
-// and folds the per-step minimum key; the CTA publishes its active count, looks back over
-// the predecessors' published counts / inclusive prefixes (32 at a time, one per lane) for
-// its exclusive prefix, publishes its own inclusive prefix, and the lanes with actives read
-// their 36-B gradient rows and write their records straight to their final positions --
-// the values are read once, the gradients only for actives, nothing else touches HBM.
-// Records in (step, slot) order = the canonical (wp, pt) order; wp_offsets[w] is the prefix
-// at the step's first tile.
-constexpr int kLbWarps = 8, kLbTW = 4, kLbTiles = kLbWarps * kLbTW;
-// status word of a partition: [63:40] call epoch, [39:38] 1 = count, 2 = inclusive prefix, [37:0] value
-constexpr int kLbAgg = 1, kLbPre = 2;
-__device__ __forceinline__ unsigned long long lb_word(uint32_t epoch, int flag, int64_t v) {
-  return ((unsigned long long)(epoch & 0xffffffu) << 40) | ((unsigned long long)flag << 38) | (unsigned long long)v;
-}
-__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
+// ---- standalone K3 (A6-A8 over dense values): values read ONCE.
+// Stage kernel: a partition = kK3Warps warps x kK3TW consecutive tiles (128 slots, 4 per lane,
+// one 16-B streaming load each) of the flat (step, tile) order.  Each warp ballots its
+// tiles' actives (f - delta <= tau; dead slots hold +INF and never pass) and folds the
+// per-step minimum key (one atomicMin per step run); the CTA takes ONE staging allocation
+// for its actives (atomicAdd), the lanes with actives read their 36-B gradient rows and
+// write their records to the staging area in the partition's (step, slot) order, and the
+// partition's (base, count) -- plus, for a step starting inside it, that step's offset in
+// the partition -- go to the scratch.  No CTA waits on another (no look-back chain).
+// Place kernel: after a scan of the partition counts, every partition's records move from
+// staging to their final position (partitions are contiguous tile ranges, so partition order
+// = (wp, pt) order), and wp_offsets[w] = prefix of the partition holding step w's first tile
+// + that step's offset inside it.  HBM traffic: the values once, the active gradient rows,
+// the records twice (staging write + read) and once in the output.
+constexpr int kK3Warps = 8, kK3TW = 8, kK3Tiles = kK3Warps * kK3TW;
 
 // values of tile tw (0-based within step w) for this lane's 4 slots (+INF outside the scene)
 __device__ __forceinline__ float4 load_tile_values(const float *__restrict__ values, int64_t stride, int64_t lb,
@@ -73,173 +62,218 @@ __device__ __forceinline__ float4 load_tile_values(const float *__restrict__ val
   return v;
 }
 
-__global__ void __launch_bounds__(256) k_compact_lookback(const float *__restrict__ values,
-                                                          const float *__restrict__ grads, int64_t stride,
-                                                          int32_t n_wp, int32_t tpw, SceneView scene, float delta,
-                                                          float tau, unsigned long long *__restrict__ wp_key,
-                                                          unsigned long long *part_ctr, unsigned long long *status,
-                                                          uint32_t epoch, gcdf_active_t *__restrict__ out, int64_t cap,
-                                                          int64_t *__restrict__ wp_offsets, int64_t *__restrict__ count) {
-  __shared__ int64_t s_part, s_excl;
-  __shared__ int32_t s_wcnt[kLbWarps];
+struct K3Scratch {
+  int64_t *part_base;   // [n_parts] staging base of the partition (-1: staging overflow)
+  int64_t *part_cnt;    // [n_parts] actives of the partition
+  int64_t *part_pre;    // [n_parts + 1] exclusive prefix of part_cnt (+ total)
+  int64_t *wstart;      // [n_wp] (partition << 16 | offset of the step's first record in it)
+  int64_t *scan_tmp;
+};
+
+constexpr int kK3List = 128;  // per-warp record list (entries per pass)
+
+__global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__restrict__ values,
+                                                            const float *__restrict__ grads, int64_t stride,
+                                                            int32_t n_wp, int32_t tpw, SceneView scene, float delta,
+                                                            float tau, DetectScratch ds, K3Scratch ks) {
+  __shared__ int32_t s_wcnt[kK3Warps];
+  __shared__ int64_t s_base;
+  __shared__ uint2 s_list[kK3Warps][kK3List];  // (slot in the warp's range, value bits)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_part = (int64_t)atomicAdd(part_ctr, 1ull);
-  __syncthreads();
-  const int64_t p = s_part;
+  const int64_t p = blockIdx.x;
   const int64_t n_tiles = (int64_t)n_wp * tpw;
-  const int64_t T0 = p * kLbTiles + (int64_t)warp * kLbTW;  // this warp's first flat tile
+  const int64_t T0 = p * kK3Tiles + (int64_t)warp * kK3TW;  // this warp's first flat tile
   const int64_t lb = scene.local_bound;
-  const uint32_t lt = (1u << lane) - 1u;
-  int w0 = (int)(T0 / tpw);
-  int t0 = (int)(T0 - (int64_t)w0 * tpw);
-  // ---- loads: the warp's kLbTW tiles, all in flight
-  float4 v[kLbTW];
+  const int w0 = (int)(T0 / tpw);
+  const int t0 = (int)(T0 - (int64_t)w0 * tpw);
+  const int nt = (int)max((int64_t)0, min((int64_t)kK3TW, n_tiles - T0));  // tiles of this warp
+  // ---- loads: the warp's tiles, all in flight
+  float4 v[kK3TW];
   {
     int w = w0, t = t0;
 #pragma unroll
-    for (int i = 0; i < kLbTW; ++i) {
-      if (T0 + i < n_tiles) v[i] = load_tile_values(values, stride, lb, w, t, lane);
+    for (int i = 0; i < kK3TW; ++i) {
+      if (i < nt) v[i] = load_tile_values(values, stride, lb, w, t, lane);
       if (++t == tpw) { t = 0; ++w; }
     }
   }
-  // ---- ballots, counts, per-step minimum (one atomicMin per step run of the warp)
-  uint32_t bits[kLbTW];  // this lane's 4 active flags per tile (bit k = slot 4 lane + k)
-  int below[kLbTW];      // actives of the lower lanes in the tile
-  int cnt[kLbTW];        // actives of the tile
-  int wtot = 0;
+  // ---- per tile: this lane's 4 active flags (4 bits of `bits`), their count (8-bit fields of
+  // cnt_lo / cnt_hi for the one warp scan below), and the lane's running minimum of the step
+  uint32_t bits = 0u, cnt_lo = 0u, cnt_hi = 0u;
+  const float inf = __int_as_float(0x7f800000);
+  float lmin = inf;
+  uint32_t lslot = 0u;
   {
-    int w = w0, t = t0;
-    unsigned long long key = ~0ull;
-    int wk = w0;
-    auto flush = [&]() {
+    int w = w0, t = t0, wk = w0;
+    auto flush = [&]() {  // the step's minimum over the warp: (min value, then smallest slot)
+      float m = lmin;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-        key = other < key ? other : key;
-      }
-      if (lane == 0 && key != ~0ull) atomicMin(wp_key + wk, key);
-      key = ~0ull;
+      for (int o = 16; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      uint32_t sl = lmin == m ? lslot : 0xffffffffu;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sl = min(sl, __shfl_xor_sync(0xffffffffu, sl, o));
+      if (lane == 0 && m < inf)
+        atomicMin(ds.wp_key + wk, ((unsigned long long)ord_f32(m) << 32) |
+                                      (unsigned long long)local_to_global(sl, scene.rank, scene.world));
+      lmin = inf;
     };
 #pragma unroll
-    for (int i = 0; i < kLbTW; ++i) {
-      bits[i] = 0u;
-      below[i] = cnt[i] = 0;
-      if (T0 + i < n_tiles) {  // (uniform over the warp)
+    for (int i = 0; i < kK3TW; ++i) {
+      if (i < nt) {  // (uniform over the warp)
         if (w != wk) {
           flush();
           wk = w;
         }
-        const float x[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const uint32_t b = __ballot_sync(0xffffffffu, x[k] - delta <= tau);
-          bits[i] |= ((b >> lane) & 1u) << k;
-          below[i] += __popc(b & lt);
-          cnt[i] += __popc(b);
+        const float4 x = v[i];
+        const uint32_t b = (uint32_t)(x.x - delta <= tau) | ((uint32_t)(x.y - delta <= tau) << 1) |
+                           ((uint32_t)(x.z - delta <= tau) << 2) | ((uint32_t)(x.w - delta <= tau) << 3);
+        bits |= b << (4 * i);
+        const uint32_t c = __popc(b);
+        if (i < 4) cnt_lo |= c << (8 * i); else cnt_hi |= c << (8 * (i - 4));
+        const float m4 = fminf(fminf(x.x, x.y), fminf(x.z, x.w));
+        if (m4 < lmin) {  // (rare after the first tiles of a step)
+          lmin = m4;
+          lslot = (uint32_t)t * kTile + 4u * lane + (x.x == m4 ? 0u : x.y == m4 ? 1u : x.z == m4 ? 2u : 3u);
         }
-        // minimum of the lane's four (first slot on ties), as a key with the global id
-        const float m4 = fminf(fminf(x[0], x[1]), fminf(x[2], x[3]));
-        if (m4 != __int_as_float(0x7f800000)) {
-          const int kk = x[0] == m4 ? 0 : x[1] == m4 ? 1 : x[2] == m4 ? 2 : 3;
-          const unsigned long long kx =
-              ((unsigned long long)ord_f32(m4) << 32) |
-              (unsigned long long)local_to_global((int64_t)t * kTile + 4 * lane + kk, scene.rank, scene.world);
-          key = kx < key ? kx : key;
-        }
-        wtot += cnt[i];
       }
       if (++t == tpw) { t = 0; ++w; }
     }
     flush();
   }
-  if (lane == 0) s_wcnt[warp] = wtot;
-  __syncthreads();
-  // ---- decoupled look-back (warp 0): exclusive prefix of this partition
-  if (warp == 0) {
-    int64_t agg = 0;
+  // ---- one inclusive warp scan of the packed per-tile counts (fields <= 128 fit 8 bits)
+  uint32_t sc_lo = cnt_lo, sc_hi = cnt_hi;
 #pragma unroll
-    for (int j = 0; j < kLbWarps; ++j) agg += s_wcnt[j];
-    unsigned long long *const st = status + p;
-    if (p == 0) {
-      if (lane == 0) st_release(st, lb_word(epoch, kLbPre, agg));
-      if (lane == 0) s_excl = 0;
-    } else {
-      if (lane == 0) st_release(st, lb_word(epoch, kLbAgg, agg));
-      int64_t excl = 0;
-      for (int64_t base = p - 1;; base -= 32) {
-        const int64_t idx = base - lane;
-        unsigned long long wd = lb_word(epoch, kLbPre, 0);  // (idx < 0: never reached past partition 0)
-        if (idx >= 0) {
-          do {
-            wd = ld_acquire(status + idx);
-          } while ((uint32_t)(wd >> 40) != (epoch & 0xffffffu) || ((wd >> 38) & 3u) == 0u);
-        }
-        __syncwarp();
-        const unsigned pm = __ballot_sync(0xffffffffu, ((wd >> 38) & 3u) == (unsigned)kLbPre);
-        const int stop = pm ? __ffs(pm) - 1 : 32;
-        int64_t val = lane <= stop ? (int64_t)(wd & ((1ull << 38) - 1ull)) : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-        excl += val;
-        if (pm) break;
-      }
-      if (lane == 0) {
-        st_release(st, lb_word(epoch, kLbPre, excl + agg));
-        s_excl = excl;
-      }
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t a = __shfl_up_sync(0xffffffffu, sc_lo, o), b = __shfl_up_sync(0xffffffffu, sc_hi, o);
+    if (lane >= o) {
+      sc_lo += a;
+      sc_hi += b;
     }
   }
-  __syncthreads();
-  int64_t pos = s_excl;
-  for (int j = 0; j < warp; ++j) pos += s_wcnt[j];
-  // ---- offsets and records
-  int w = w0, t = t0;
+  const uint32_t tot_lo = __shfl_sync(0xffffffffu, sc_lo, 31), tot_hi = __shfl_sync(0xffffffffu, sc_hi, 31);
+  // tile i: total T_i = field i of tot, this lane's exclusive prefix = field i of (sc - cnt)
+  int tile_pre[kK3TW];  // actives of the warp's tiles before tile i
+  int wtot = 0;
 #pragma unroll
-  for (int i = 0; i < kLbTW; ++i) {
-    const int64_t T = T0 + i;
-    if (T < n_tiles) {
-      if (t == 0 && lane == 0) wp_offsets[w] = pos;
-      if (T == n_tiles - 1 && lane == 0) {
-        wp_offsets[n_wp] = pos + cnt[i];
-        *count = pos + cnt[i];
-      }
-      unsigned b = bits[i];
-      int64_t r = pos + below[i];
-      while (b) {  // (a lane has ~0.04 actives per tile at 1 % active)
+  for (int i = 0; i < kK3TW; ++i) {
+    tile_pre[i] = wtot;
+    wtot += (int)(((i < 4 ? tot_lo : tot_hi) >> (8 * (i & 3))) & 0xffu);
+  }
+  const uint32_t ex_lo = sc_lo - cnt_lo, ex_hi = sc_hi - cnt_hi;
+  uint2 *list = s_list[warp];
+  // the warp's actives in (tile, slot) order into its list: entries [c0, c0 + kK3List) of the
+  // warp's ranks (c0 = 0 here, while the values are in registers; more than kK3List actives
+  // per warp -- rare -- take later passes that re-read the values, which are in L2)
+  auto fill = [&](int c0, const float4 *vv) {
+    if (!bits) return;
+#pragma unroll
+    for (int i = 0; i < kK3TW; ++i) {
+      uint32_t b = (bits >> (4 * i)) & 0xfu;
+      if (!b) continue;
+      int r = tile_pre[i] + (int)(((i < 4 ? ex_lo : ex_hi) >> (8 * (i & 3))) & 0xffu) - c0;
+      const float4 x = vv ? vv[i] : load_tile_values(values, stride, lb, w0 + (t0 + i) / tpw, (t0 + i) % tpw, lane);
+      while (b) {
         const int k = __ffs(b) - 1;
         b &= b - 1u;
-        const float xk = k == 0 ? v[i].x : k == 1 ? v[i].y : k == 2 ? v[i].z : v[i].w;
-        const int64_t slot = (int64_t)t * kTile + 4 * lane + k;
-        if (r < cap) {
-          const float *g = grads + ((int64_t)w * stride + slot) * kNdof;
-          float gg[kNdof];
-#pragma unroll
-          for (int e = 0; e < kNdof; ++e) gg[e] = __ldcs(g + e);
-          float4 *dst = reinterpret_cast<float4 *>(out + r);
-          dst[0] = make_float4(xk, gg[0], gg[1], gg[2]);
-          dst[1] = make_float4(gg[3], gg[4], gg[5], gg[6]);
-          dst[2] = make_float4(gg[7], gg[8], __uint_as_float((unsigned)w),
-                               __uint_as_float((unsigned)local_to_global(slot, scene.rank, scene.world)));
+        if (r >= 0 && r < kK3List) {
+          const float xk = k == 0 ? x.x : k == 1 ? x.y : k == 2 ? x.z : x.w;
+          list[r] = make_uint2((uint32_t)(i * kTile + 4 * lane + k), __float_as_uint(xk));
         }
         ++r;
       }
-      pos += cnt[i];
     }
-    if (++t == tpw) { t = 0; ++w; }
+  };
+  fill(0, v);
+  __syncwarp();
+  if (lane == 0) s_wcnt[warp] = wtot;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t agg = 0;
+#pragma unroll
+    for (int j = 0; j < kK3Warps; ++j) agg += s_wcnt[j];
+    int64_t base = agg > 0 ? (int64_t)atomicAdd(ds.counter, (unsigned long long)agg) : 0;
+    if (base + agg > ds.max_active) {
+      atomicOr(ds.counter + 1, 1ull);
+      base = -1;
+    }
+    ks.part_base[p] = base;
+    ks.part_cnt[p] = agg;
+    s_base = base;
+  }
+  __syncthreads();
+  const int64_t base = s_base;
+  int64_t pos = 0;  // this warp's first record in the partition
+  for (int j = 0; j < warp; ++j) pos += s_wcnt[j];
+  // step starts inside this warp's tiles
+  if (lane == 0) {
+    int t = t0, w = w0;
+    for (int i = 0; i < nt; ++i) {
+      if (t == 0) ks.wstart[w] = (p << 20) | (pos + tile_pre[i]);
+      if (++t == tpw) { t = 0; ++w; }
+    }
+  }
+  if (base < 0 || wtot == 0) return;
+  // ---- records: one active per lane (the gradient row loads and record stores spread over
+  // the lanes)
+  for (int c0 = 0; c0 < wtot; c0 += kK3List) {
+    if (c0 > 0) {
+      __syncwarp();
+      fill(c0, nullptr);
+    }
+    __syncwarp();
+    const int n = min(kK3List, wtot - c0);
+    for (int e = lane; e < n; e += 32) {
+      const uint2 it = list[e];
+      const int i = (int)(it.x >> 7);
+      int t = t0 + i, w = w0;
+      while (t >= tpw) { t -= tpw; ++w; }
+      const int64_t slot = (int64_t)t * kTile + (it.x & 127u);
+      const float *g = grads + ((int64_t)w * stride + slot) * kNdof;
+      float gg[kNdof];
+#pragma unroll
+      for (int q = 0; q < kNdof; ++q) gg[q] = __ldcs(g + q);
+      float4 *dst = reinterpret_cast<float4 *>(ds.staging + base + pos + c0 + e);
+      dst[0] = make_float4(__uint_as_float(it.y), gg[0], gg[1], gg[2]);
+      dst[1] = make_float4(gg[3], gg[4], gg[5], gg[6]);
+      dst[2] = make_float4(gg[7], gg[8], __uint_as_float((unsigned)w),
+                           __uint_as_float((unsigned)local_to_global(slot, scene.rank, scene.world)));
+    }
   }
 }
 
-// per-step min / argmin / key export of the standalone K3; with no tile at all (empty
-// scene) also the zero offsets and count
-__global__ void k_compact_keys(const unsigned long long *__restrict__ keys, int32_t n_wp, bool no_tiles,
-                               float *wp_min, int64_t *wp_argmin, int64_t *wp_key_out, int64_t *wp_offsets,
-                               int64_t *count) {
+// one warp per partition: its records from staging to out[part_pre[p] ..]
+__global__ void __launch_bounds__(256) k_k3_place(int64_t n_parts, K3Scratch ks, const gcdf_active_t *__restrict__ staging,
+                                                  gcdf_active_t *__restrict__ out, int64_t cap) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < n_parts;
+       p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t base = ks.part_base[p], n = ks.part_cnt[p], dst0 = ks.part_pre[p];
+    if (base < 0) continue;
+    const float4 *src = reinterpret_cast<const float4 *>(staging + base);
+    float4 *dst = reinterpret_cast<float4 *>(out + dst0);
+    const int64_t nv = 3 * n, lim = 3 * (cap - dst0);
+    for (int64_t e = lane; e < nv; e += 32)
+      if (e < lim) dst[e] = __ldcs(src + e);
+  }
+}
+
+// per-step offsets from the partition prefix (+ the total) and the min / argmin / key export
+__global__ void k_k3_offsets(const unsigned long long *__restrict__ keys, int32_t n_wp, int64_t n_parts, K3Scratch ks,
+                             float *wp_min, int64_t *wp_argmin, int64_t *wp_key_out, int64_t *wp_offsets,
+                             int64_t *count) {
   for (int w = blockIdx.x * blockDim.x + threadIdx.x; w <= n_wp; w += gridDim.x * blockDim.x) {
-    if (no_tiles) {
-      wp_offsets[w] = 0;
-      if (w == n_wp) *count = 0;
+    if (w == n_wp) {
+      const int64_t tot = n_parts > 0 ? ks.part_pre[n_parts] : 0;
+      wp_offsets[n_wp] = tot;
+      *count = tot;
+      continue;
     }
-    if (w == n_wp) continue;
+    if (n_parts > 0) {
+      const int64_t ws = ks.wstart[w];
+      wp_offsets[w] = ks.part_pre[ws >> 20] + (ws & ((1ll << 20) - 1));
+    } else {
+      wp_offsets[w] = 0;
+    }
     const unsigned long long k = keys[w];
     if (wp_min) wp_min[w] = k == ~0ull ? __int_as_float(0x7f800000) : unord_f32((unsigned)(k >> 32));
     if (wp_argmin) wp_argmin[w] = k == ~0ull ? -1 : (int64_t)(k & 0xffffffffull);
@@ -451,19 +485,39 @@ cudaError_t launch_compact_dense(const float *values, const float *grads, int64_
                                  int32_t tiles_per_wp, SceneView scene, float delta, float tau,
                                  DetectScratch ds, gcdf_active_t *out, int64_t out_capacity, int64_t *wp_offsets,
                                  float *wp_min, int64_t *wp_argmin, int64_t *wp_key, int64_t *count,
-                                 uint32_t epoch, cudaStream_t s, int *n_launches) {
+                                 int64_t *k3_scratch, cudaStream_t s, int *n_launches) {
   const int64_t n_tiles = (int64_t)n_wp * tiles_per_wp;
-  const int64_t n_parts = (n_tiles + kLbTiles - 1) / kLbTiles;
-  // the partition counter is ds.counter[0] (zeroed by k_detect_init); the status words live
-  // in the tile-bitmap scratch (16 B per tile >= 8 B per partition) and carry the call epoch
-  if (n_parts > 0)
-    k_compact_lookback<<<(unsigned)n_parts, kLbWarps * 32, 0, s>>>(
-        values, grads, stride, n_wp, tiles_per_wp, scene, delta, tau, ds.wp_key, ds.counter,
-        reinterpret_cast<unsigned long long *>(ds.tile_bits), epoch, out, out_capacity, wp_offsets, count);
-  k_compact_keys<<<(n_wp + 256) / 256, 256, 0, s>>>(ds.wp_key, n_wp, n_parts == 0, wp_min, wp_argmin, wp_key,
-                                                    wp_offsets, count);
-  *n_launches += n_parts > 0 ? 2 : 1;
+  const int64_t n_parts = (n_tiles + kK3Tiles - 1) / kK3Tiles;
+  K3Scratch ks;
+  ks.part_base = k3_scratch;
+  ks.part_cnt = ks.part_base + n_parts;
+  ks.part_pre = ks.part_cnt + n_parts;
+  ks.wstart = ks.part_pre + n_parts + 1;
+  ks.scan_tmp = ks.wstart + n_wp;
+  if (n_parts > 0) {
+    // (ds.counter[0] = the staging allocation counter and [1] the overflow flag, zeroed by k_detect_init)
+    k_k3_stage<<<(unsigned)n_parts, kK3Warps * 32, 0, s>>>(values, grads, stride, n_wp, tiles_per_wp, scene, delta,
+                                                            tau, ds, ks);
+    ++*n_launches;
+    cudaError_t e = excl_scan(ks.part_cnt, n_parts, ks.part_pre, ks.part_pre + n_parts, ks.scan_tmp, s, n_launches);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t blocks = std::min<int64_t>((n_parts + 7) / 8, (int64_t)sms * 8);
+    k_k3_place<<<(unsigned)blocks, 256, 0, s>>>(n_parts, ks, ds.staging, out, out_capacity);
+    ++*n_launches;
+  }
+  k_k3_offsets<<<(n_wp + 256) / 256, 256, 0, s>>>(ds.wp_key, n_wp, n_parts, ks, wp_min, wp_argmin, wp_key, wp_offsets,
+                                                  count);
+  ++*n_launches;
   return cudaGetLastError();
+}
+
+// scratch (int64 elements) of the standalone K3 for n_wp steps of tiles_per_wp tiles
+int64_t k3_scratch_elems(int64_t n_wp, int64_t tiles_per_wp) {
+  const int64_t n_parts = (n_wp * tiles_per_wp + kK3Tiles - 1) / kK3Tiles;
+  return 3 * n_parts + 1 + n_wp + (n_parts + 1023) / 1024 + 1;
 }
 
 
