@@ -6,7 +6,7 @@
 // value + gradient :394 (dense gradient R^{NM x n}); constraint f - delta >= 0 :362-363;
 // union = min :164; c_gcdf step-major order :414-435.  DESIGN.md §5 "K2b".
 //
-// Design (H = 128, one persistent CTA per SM, 576 threads = 16 epilogue warps + 2 MMA warps):
+// Design (H = 128, one persistent CTA per SM, 864 threads = 24 epilogue warps + 3 MMA warps):
 //   * Every affine layer of a 128-pair tile is a UMMA with M = 128 pairs, A in TMEM and B
 //     resident in shared memory for the whole kernel:
 //       - layer 1 (12 -> 128): K = 32 of split hi/lo 16-bit operands (A = {x_hi, x_lo,
@@ -17,25 +17,27 @@
 //       - backward layers 6..2: D = E W_l with the same smem bytes read MN-major;
 //       - g0 = e1 W1: N = 16 rows of W1^T.
 //     W_2..W_6 use the UMMA SWIZZLE_128B layout (5 x 32 KB); the small K = 16 / 32 blocks
-//     the SWIZZLE_NONE layout.
-//   * Activations never leave the chip: accumulator D (fp32, 128 TMEM columns) ->
-//     epilogue registers (ReLU + 16-bit pack + byte-sign mask) -> A (64 TMEM columns) ->
-//     next UMMA.  ReLU masks go to shared memory for the backward pass.
-//   * Two tiles in flight: TMEM columns [0,256) belong to slot 0 and [256,512) to slot
-//     1 (D [0,128), A [128,192), ones [192,200)).  Each slot has 8 epilogue warps: warp
-//     (h, q) owns TMEM lanes 32q..32q+31 (the tile's pairs) and accumulator columns
-//     64h..64h+63, so every SM sub-partition runs two warps per slot, and one slot's
-//     epilogue overlaps the other slot's tensor-core work.  Warp 16 + s issues slot s's
-//     MMAs: after each epilogue phase the slot's 8 warps arrive on the slot's "A ready"
-//     mbarrier; the converged MMA warp waits on it (and on its turn: the slots alternate
-//     phase by phase) and an elected lane issues the slot's next UMMAs (operands in
-//     uniform registers) and commits them to the slot's "D ready" mbarrier.  One issuer
-//     per slot keeps the other slot's UMMAs flowing while a commit drains.  12 MMA
-//     phases per tile; the next tile's layer-1 operands are staged at the end of the
-//     current tile (its point prefetched by cp.async four phases earlier).
-//   * Measured (profiles/r1/mma_probe.txt, trace_tc_*.txt): a 128x128x16 UMMA runs at the
-//     dense rate (64 cycles) when the issue stream is lean; the kernel is bound by the
-//     per-slot chain MMA -> epilogue -> hand-off with two slots.
+//     the SWIZZLE_NONE layout (the five bias blocks share one all-zero second K core).
+//   * Three tiles in flight (slots), 12 MMA phases per tile (layer 1, layers 2..6, backward
+//     6..2, g0).  TMEM is four 128-column regions used round robin: the k-th MMA phase of the
+//     CTA (phases interleave slot 0, 1, 2, 0, ...) writes its accumulator D into region k % 4
+//     and reads its A operand from region (k + 1) % 4 = the region of the slot's previous
+//     phase, where that phase's epilogue wrote the 16-bit activations IN PLACE over the
+//     accumulator columns it had already loaded (A of K step k at AK(k)).  So a slot holds
+//     one region between phases and a phase needs one fresh region: 3 slots x 128 + 128 =
+//     512 columns, where a fixed D + A per slot (192 columns) fits only two slots.  Region
+//     k % 4 was last read (as A) by phase k - 1, issued just before phase k by the turn order.
+//   * Each slot has 8 epilogue warps: warp (h, q) owns TMEM lanes 32q..32q+31 (the tile's
+//     pairs) and accumulator columns 32h + {0..31, 64..95}; one MMA warp per slot issues its
+//     phases: it waits on the slot's "A ready" mbarrier (one arrival per epilogue warp) and
+//     on its turn (an mbarrier per slot orders the CTA's phases round robin, which the region
+//     rotation relies on), an elected lane issues the UMMAs (operands in uniform registers)
+//     and commits them to the slot's "D ready" mbarrier.  With three tiles in flight the
+//     per-slot chain MMA -> commit -> epilogue -> hand-off (~2k cycles) is
+//     covered by the other two slots' tensor work (2 x 576 cycles per phase).
+//   * Activations never leave the chip: accumulator D (fp32) -> epilogue registers (ReLU +
+//     16-bit pack + byte-sign mask) -> A (TMEM, in place) -> next UMMA.  ReLU masks go to
+//     shared memory for the backward pass.
 #include <type_traits>
 
 #include "gcdf_internal.h"
@@ -46,22 +48,43 @@ namespace {
 
 using namespace tc;
 
+// Waits of the epilogue / detect / MMA warps.  A plain try_wait returns after a short
+// system-defined time, so an idle warp re-polls (~9 instructions per poll) and takes issue
+// slots from the busy epilogue warps of its SM sub-partition; with a suspend-time hint the
+// warp sleeps until the phase completes (or the hint expires).
+DEVI void wait_bar(uint64_t *bar, uint32_t parity) { mbar_wait_hint<20000>(bar, parity); }
+
 constexpr int H = 128;
-constexpr int kEpiWarps = 16;             // warps 0..15: epilogue (8 per tile slot)
-constexpr int kWarps = kEpiWarps + 2;      // + warp 16 + s: issues tile slot s's UMMAs
-constexpr int kThreads = kWarps * 32;
-constexpr int kEpiPerSlot = 256;
-constexpr int kEpiArrivals = kEpiPerSlot;  // epi_done count: every epilogue thread of the slot
-constexpr int kPhases = 12;               // MMA phases per tile
-constexpr int kMasks = 5;                 // stored ReLU masks: layers 1..5
-constexpr int kWBytes = 5 * H * H * 2;    // 163,840
-constexpr int kW1tBytes = 16 * H * 2;     // 4,096
-constexpr int kB1Bytes = 32 * H * 2;      // 8,192
-constexpr int kBextBytes = 16 * H * 2;    // 4,096 per hidden layer
-// per slot: D [0,128), A [128,192), ones [192,200), g0 [200,216), layer-1 operands x [216,232)
-// (g0 and x have columns of their own so that the last GEMM of a tile and the first of the
-// next one are issued as one phase, see issue_phase)
-constexpr uint32_t kColA = 128, kColOnes = 192, kColG0 = 200, kColX = 216;
+constexpr int kSlots = 3;                         // tiles in flight
+constexpr int kEpiPerSlot = 256;                  // 8 epilogue warps per slot
+constexpr int kEpiWarps = kSlots * kEpiPerSlot / 32;  // warps 0..23
+constexpr int kMmaWarp0 = kEpiWarps;              // warp 24 + s issues slot s's UMMAs
+constexpr int kDetectWarp = kEpiWarps + kSlots;   // warp 27: per-tile detect bookkeeping (A6-A8 atomics)
+constexpr int kWarps = kDetectWarp + 1;
+constexpr int kThreads = kWarps * 32;             // 896
+constexpr int kEpiArrivals = kEpiPerSlot / 32;    // epi_done count: one arrival per epilogue warp
+constexpr int kPhases = 12;                       // MMA phases per tile
+constexpr int kMasks = 5;                         // stored ReLU masks: layers 1..5
+constexpr int kWBytes = 5 * H * H * 2;            // 163,840
+constexpr int kW1tBytes = 16 * H * 2;             // 4,096
+constexpr int kB1Bytes = 32 * H * 2;              // 8,192
+constexpr int kBextBytes = 16 * H * 2;            // global bias block per hidden layer (2 K cores)
+constexpr int kBiasCore = 8 * H * 2;              // 2,048: one K core (8 k) of a bias block
+// Region layout (columns relative to the region): the A operand's K step k (16 units, 8
+// columns of 16-bit pairs) at AK(k); the "ones" A block of the bias step at kColOnes (written
+// by forward epilogues); in a g0 phase's region: g0 at [0, 16) and the next tile's layer-1
+// operands x at [kColX, kColX + 16).  All of these are columns the writing warp has loaded.
+constexpr uint32_t kColOnes = 48, kColX = 16;
+__host__ __device__ constexpr uint32_t AK(int k) {
+  return (uint32_t)((k >> 2) * 64 + ((k >> 1) & 1) * 32 + (k & 1) * 8);
+}
+// epilogue chunk c = 0..3 of column half h: accumulator columns 32h + DC(c) .. + 15 (units of
+// the same numbers); their 16-bit activations go to 32h + AC(c) .. + 7 (= AK of their K step)
+__host__ __device__ constexpr uint32_t DC(int c) { return (uint32_t)((c >> 1) * 64 + (c & 1) * 16); }
+__host__ __device__ constexpr uint32_t AC(int c) { return (uint32_t)((c >> 1) * 64 + (c & 1) * 8); }
+static_assert(AK(0) == AC(0) && AK(1) == AC(1) && AK(2) == 32 + AC(0) && AK(3) == 32 + AC(1) && AK(4) == AC(2) &&
+                  AK(5) == AC(3) && AK(6) == 32 + AC(2) && AK(7) == 32 + AC(3),
+              "K step k holds units 16k..16k+15");
 template <bool F16> constexpr uint32_t kIdescFwd = idesc_f16kind(128, 128, false, F16);
 template <bool F16> constexpr uint32_t kIdescBwd = idesc_f16kind(128, 128, true, F16);
 template <bool F16> constexpr uint32_t kIdescFin = idesc_f16kind(128, 16, false, F16);
@@ -70,27 +93,34 @@ struct __align__(1024) SmemTC {
   uint8_t w[kWBytes];          // W_2..W_6, SW128 [2 chunks][128 rows][128 B] each
   uint8_t w1t[kW1tBytes];      // W1^T [16][128], SW128
   uint8_t b1[kB1Bytes];        // layer-1 split weights [128][32], no swizzle
-  uint8_t bext[5][kBextBytes]; // hidden-layer bias blocks [128][16], no swizzle
-  uint32_t one;                // 1 (runtime constant, see add7fff)
-  float fpart[2][2][H];        // [slot][column half][row] partial output-layer sums
-  float4 ptn[2][H];            // [slot][row] prefetched point of the slot's next tile
-  float2 pprime[2][2][H];      // [slot][tile parity][row] SE(2) frame: p'_xy kept for d f / d theta (R24)
-  float qn[2][2][12];          // [slot][tile parity] q row of the slot's tile (cp.async, phases 1-3)
-  int wnx[2];                  // [slot] (partitioned) step of the slot's next tile, staged at phase 1
-  int wtile[2][2];             // [slot][tile parity] step (waypoint) of the slot's tile
-  uint32_t slotn[2][2][H];     // [slot][tile parity][row] local scene slot of the pair (~0: padding)
-  uint32_t mask[2][kMasks][2][kEpiPerSlot];  // ReLU masks [slot][layer][32-unit word][thread]
-  uint64_t mma_done[2];
-  uint64_t epi_done[2];
+  uint8_t bext[5][kBiasCore];  // hidden-layer bias blocks: K core 0 ({b_hi, b_lo, 0..})
+  uint8_t bzero[kBiasCore];    // K core 1 of every bias block (zeros)
+  float fpart[kSlots][2][H];   // [slot][column half][row] partial output-layer sums
+  float4 ptn[kSlots][H];       // [slot][row] prefetched point of the slot's next tile
+  float qn[kSlots][2][12];     // [slot][tile parity] q row of the slot's tile (cp.async, phases 1-3)
+  int wnx[kSlots];             // [slot] (partitioned) step of the slot's next tile, staged at phase 1
+  int wtile[kSlots][2];        // [slot][tile parity] step (waypoint) of the slot's tile
+  uint32_t slotn[kSlots][2][H];  // [slot][tile parity][row] local scene slot of the pair (~0: padding;
+                                 // bit 31: a removed point, set when x is staged)
+  uint32_t mask[kSlots][kMasks][2][kEpiPerSlot];  // ReLU masks [slot][layer][32-unit word][thread]
+  uint64_t mma_done[kSlots];
+  uint64_t epi_done[kSlots];
   uint64_t wbar;               // the resident weights landed (bulk copies, complete_tx)
-  uint32_t turn;               // global issue-order counter of the two MMA warps
-  unsigned act[2][4];
-  unsigned long long kmin[2][4];
-  int sbase[2];
+  uint64_t turn[kSlots];       // [slot] "your turn": the previous slot's phase is issued (round robin)
+  uint32_t one;                // 1 (runtime constant, see add7fff)
+  uint64_t det_in[kSlots];     // [slot] the 4 column-half-1 warps posted the tile's ballots / min keys
+  uint64_t det_out[kSlots];    // [slot] the detect warp posted the tile's staging base
+  unsigned act[kSlots][4];
+  unsigned long long kmin[kSlots][4];
+  int sbase[kSlots];
   uint32_t tmem_base;
 };
 
-static_assert(sizeof(SmemTC) + 1024 <= 232448, "SmemTC exceeds the 227 KB of shared memory per CTA");
+static_assert(2 * kSlots * kTraceTiles * kTracePhases * 4 + kEpiWarps * kTraceTiles * kPhases <= kTraceLen,
+              "trace buffer layout");
+// (the dynamic shared memory of a CTA starts 1024-B aligned, after the 1 KB the system
+// reserves: checked at kernel entry, so no alignment pad is allocated)
+static_assert(sizeof(SmemTC) <= 232448, "SmemTC exceeds the 227 KB of shared memory per CTA");
 
 DEVI unsigned ord_f32(float f) {
   unsigned u = __float_as_uint(f);
@@ -131,50 +161,176 @@ DEVI uint32_t mask_group_f(uint32_t pk01, uint32_t pk23, int k, uint32_t one) {
 // values (bit 15 of v + 0x7fff is set iff v != 0; sign-replicate bytes 1 and 3)
 DEVI uint32_t nz_halves(uint32_t pk, uint32_t one) { return prmt(add7fff(pk, one), 0u, 0xbb99u); }
 
-// UMMAs of MMA phase p of the tile whose accumulator starts at TMEM column d, committed
-// to bar.  Executed by the whole (converged) MMA warp with warp-uniform operands; one
-// elected lane issues.  Uniform operands stay in uniform registers, which keeps the issue
-// stream to a few instructions per UMMA: a lane-0-only loop paid a register-to-uniform
-// move per operand and issued at ~75-90 cycles per UMMA, slower than the tensor pipe
-// (64 cycles per 128x128x16 UMMA, tools/mma_probe.py "lean issue").
-// Phase 11 (g0 of this tile, into columns kColG0..) also issues phase 0 of the slot's next
-// tile (layer 1, A = x staged at kColX by phase 10's epilogue) when next_l1: one commit,
-// one epilogue and one hand-off fewer per tile (11 phases per tile after the first).
-template <bool F16, bool kElect = true>
-DEVI void issue_phase(int p, uint32_t d, uint32_t sw, uint32_t sw1t, uint32_t sb1, uint32_t sbx, uint64_t *bar,
-                      volatile uint32_t *turn = nullptr, uint32_t next_turn = 0u, bool next_l1 = false) {
-  auto mma_ts = [](uint32_t dt, uint32_t at, uint64_t bd, uint32_t id, uint32_t acc) {
-    if constexpr (kElect) tc::mma_ts_elect(dt, at, bd, id, acc);
-    else tc::mma_ts(dt, at, bd, id, acc);
-  };
-  const uint32_t av = d + kColA;
-  auto layer1 = [&]() {  // layer 1: K = 32 split operands (bias included), A = x
-#pragma unroll
-    for (int k = 0; k < 2; ++k)
-      mma_ts(d, d + kColX + 8u * k, sdesc_nosw(sb1 + k * 2 * 2048, 2048, 128), kIdescFwd<F16>, k > 0);
-  };
+// UMMAs of MMA phase p: accumulator in the region at TMEM address d, A operand in the region
+// at av (the slot's previous phase's region).  Executed by the whole (converged) MMA warp;
+// one elected lane issues all UMMAs of the phase from ONE asm block, the per-UMMA operands
+// formed by adds of immediates to the phase's base values (the descriptor's start-address
+// field is its low 14 bits, so desc(base + off) = desc(base) + off / 16 for off < 256 KB).
+// The issue stream is the tensor pipe's feed: at ~16 instructions per UMMA (operands built
+// per UMMA and moved to uniform registers one by one) the MMA warp, sharing its SM
+// sub-partition with six busy epilogue warps, issued a 64-cycle UMMA every ~90 cycles.
+#define GCDF_UMMA(AOFF, DOFF, ACC)                                         \
+  "add.u32 ra, %1, " #AOFF ";\n\t"                                         \
+  "add.u64 rb, %2, " #DOFF ";\n\t"                                         \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ra], rb, %3, " ACC ";\n\t"
+#define GCDF_UMMA_HEAD                                                     \
+  "{\n\t.reg .pred e, pf, pt;\n\t.reg .b32 ra;\n\t.reg .b64 rb;\n\t"       \
+  "elect.sync _|e, 0xffffffff;\n\t"                                        \
+  "setp.ne.b32 pf, %4, %4;\n\tsetp.eq.b32 pt, %4, %4;\n\t"
+// forward layer (K-major SW128 B, 2 x 64-column chunks of 16 KB): K step k at A column AK(k),
+// B at + (k / 4) * 16384 + (k % 4) * 32 bytes; then the bias step (ones at kColOnes)
+DEVI void umma_fwd(uint32_t d, uint32_t av, uint64_t b0, uint32_t idesc, uint64_t bias) {
+  asm volatile(GCDF_UMMA_HEAD
+               GCDF_UMMA(0, 0, "pf") GCDF_UMMA(8, 2, "pt") GCDF_UMMA(32, 4, "pt") GCDF_UMMA(40, 6, "pt")
+               GCDF_UMMA(64, 1024, "pt") GCDF_UMMA(72, 1026, "pt") GCDF_UMMA(96, 1028, "pt") GCDF_UMMA(104, 1030, "pt")
+               "add.u32 ra, %1, 48;\n\t"
+               "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ra], %5, %3, pt;\n\t"
+               "}" ::"r"(d), "r"(av), "l"(b0), "r"(idesc), "r"(0u), "l"(bias)
+               : "memory");
+}
+static_assert(kColOnes == 48, "umma_fwd's bias step reads the ones block at column 48");
+// backward layer (MN-major SW128 B): K step k at B + k * 2048 bytes
+DEVI void umma_bwd(uint32_t d, uint32_t av, uint64_t b0, uint32_t idesc) {
+  asm volatile(GCDF_UMMA_HEAD
+               GCDF_UMMA(0, 0, "pf") GCDF_UMMA(8, 128, "pt") GCDF_UMMA(32, 256, "pt") GCDF_UMMA(40, 384, "pt")
+               GCDF_UMMA(64, 512, "pt") GCDF_UMMA(72, 640, "pt") GCDF_UMMA(96, 768, "pt") GCDF_UMMA(104, 896, "pt")
+               "}" ::"r"(d), "r"(av), "l"(b0), "r"(idesc), "r"(0u)
+               : "memory");
+}
+// g0 = e1 W1 (N = 16, W1^T K-major SW128 in 2 chunks of 2 KB)
+DEVI void umma_g0(uint32_t d, uint32_t av, uint64_t b0, uint32_t idesc) {
+  asm volatile(GCDF_UMMA_HEAD
+               GCDF_UMMA(0, 0, "pf") GCDF_UMMA(8, 2, "pt") GCDF_UMMA(32, 4, "pt") GCDF_UMMA(40, 6, "pt")
+               GCDF_UMMA(64, 128, "pt") GCDF_UMMA(72, 130, "pt") GCDF_UMMA(96, 132, "pt") GCDF_UMMA(104, 134, "pt")
+               "}" ::"r"(d), "r"(av), "l"(b0), "r"(idesc), "r"(0u)
+               : "memory");
+}
+// layer 1: K = 32 split operands at A columns kColX, kColX + 8; B (no swizzle) at + k * 4096 bytes
+DEVI void umma_l1(uint32_t d, uint32_t av, uint64_t b0, uint32_t idesc) {
+  asm volatile(GCDF_UMMA_HEAD
+               GCDF_UMMA(16, 0, "pf") GCDF_UMMA(24, 256, "pt")
+               "}" ::"r"(d), "r"(av), "l"(b0), "r"(idesc), "r"(0u)
+               : "memory");
+}
+static_assert(kColX == 16, "umma_l1 reads x at columns 16..31");
+#undef GCDF_UMMA
+#undef GCDF_UMMA_HEAD
+static_assert(AK(1) == 8 && AK(2) == 32 && AK(3) == 40 && AK(4) == 64 && AK(5) == 72 && AK(6) == 96 && AK(7) == 104,
+              "A column offsets in the umma_* blocks");
+
+// Phase p's UMMAs once the wait returns: the operands (descriptor bases) are formed before
+// the wait, so the phase's first UMMA follows the turn by a few instructions.
+template <bool F16, typename Wait>
+DEVI void issue_phase(int p, uint32_t d, uint32_t av, uint32_t sw, uint32_t sw1t, uint32_t sb1, uint32_t sbx,
+                      uint32_t sbz, Wait &&wait) {
   if (p == 0) {
-    layer1();
+    const uint64_t b0 = sdesc_nosw(sb1, 2048, 128);
+    wait();
+    umma_l1(d, av, b0, kIdescFwd<F16>);
   } else if (p < 6) {  // layer l = p + 1: D = A W_l^T (B = W_l K-major) + ones x bias
-    const uint32_t wb = sw + (uint32_t)(p - 1) * (H * H * 2);
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      mma_ts(d, av + 8u * k, sdesc_sw128(wb + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024), kIdescFwd<F16>, k > 0);
-    mma_ts(d, d + kColOnes, sdesc_nosw(sbx + (uint32_t)(p - 1) * kBextBytes, 2048, 128), kIdescFwd<F16>, 1u);
+    const uint32_t bb = sbx + (uint32_t)(p - 1) * kBiasCore;
+    const uint64_t b0 = sdesc_sw128(sw + (uint32_t)(p - 1) * (H * H * 2), 16, 1024), bx = sdesc_nosw(bb, sbz - bb, 128);
+    wait();
+    umma_fwd(d, av, b0, kIdescFwd<F16>, bx);
   } else if (p < 11) {  // backward through layer l = 12 - p: D = E W_l, B = W_l MN-major
-    const uint32_t wb = sw + (uint32_t)(10 - p) * (H * H * 2);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) mma_ts(d, av + 8u * k, sdesc_sw128(wb + k * 2048, 16384, 1024), kIdescBwd<F16>, k > 0);
-  } else {  // g0 = e1 W1 (N = 16 rows of W1^T) -> columns kColG0..; then the next tile's layer 1
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      mma_ts(d + kColG0, av + 8u * k, sdesc_sw128(sw1t + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin<F16>,
-             k > 0);
-    if (next_l1) layer1();
+    const uint64_t b0 = sdesc_sw128(sw + (uint32_t)(10 - p) * (H * H * 2), 16384, 1024);
+    wait();
+    umma_bwd(d, av, b0, kIdescBwd<F16>);
+  } else {  // g0 = e1 W1 (N = 16 rows of W1^T) -> columns 0..15 of the region
+    const uint64_t b0 = sdesc_sw128(sw1t, 16, 1024);
+    wait();
+    umma_g0(d, av, b0, kIdescFin<F16>);
   }
-  if (turn) *turn = next_turn;  // (two MMA warps) the other slot may issue now
-  if constexpr (kElect) commit_elect(bar);
-  else tc::commit(bar);
+}
+
+// The MMA warp of slot SS.  A commit stalls its issuing thread until the committed MMAs
+// drain; with one issuer per slot the other slots' UMMAs keep the tensor pipe busy meanwhile
+// (tools/mma_probe.py "two issuers").  Phase k of the CTA (k = 3 j + SS for the slot's j-th
+// phase) is issued after phase k - 1 (S.turn[SS], arrived on by the previous slot's MMA warp);
+// a slot without a tile in the last round passes its turns.
+// TMEM base address 0 (the kernel's single 512-column allocation, checked at setup).
+template <bool F16, int SS>
+DEVI void mma_loop(SmemTC &S, const QueryArgs &a, int64_t n_tiles, int64_t stride, int lane) {
+  const uint32_t sw = smem_u32(S.w), sw1t = smem_u32(S.w1t), sb1 = smem_u32(S.b1);
+  const uint32_t sbx = smem_u32(S.bext), sbz = smem_u32(S.bzero);
+  uint32_t ph = 0u, seq = (uint32_t)SS;
+  long long *tr = (a.trace && blockIdx.x == 0 && lane == 0) ? a.trace + (size_t)SS * kTraceTiles * kTracePhases * 4
+                                                           : nullptr;
+  mbar_wait(&S.wbar, 0u);  // the resident weights have landed in shared memory
+  int it = 0;
+  for (int64_t base = (int64_t)blockIdx.x * kSlots; base < n_tiles; base += stride, ++it) {
+    const bool real = base + SS < n_tiles;
+    // the slot's last tile hands off once more after its g0 readout: the phase after it (a
+    // passed turn) must not let the next phases overwrite the region g0 is read from
+    const bool last_was_real = it > 0 && base - stride + SS < n_tiles;
+#pragma unroll 1
+    for (int p = 0; p < kPhases; ++p, seq += kSlots) {
+      long long *t = (tr && it < kTraceTiles) ? tr + ((size_t)it * kTracePhases + p) * 4 : nullptr;
+      if (real || (p == 0 && last_was_real)) {
+        wait_bar(&S.epi_done[SS], ph);
+        ph ^= 1u;
+      }
+      if (t) t[0] = clock64();
+      // the turn (an mbarrier, so a waiting MMA warp sleeps instead of taking issue slots
+      // from the epilogue warps of its SM sub-partition)
+      auto wait_turn = [&]() {
+        wait_bar(&S.turn[SS], (seq / kSlots) & 1u);
+        if (t) t[1] = clock64();
+        fence_after();
+      };
+      if (real) issue_phase<F16>(p, 128u * (seq & 3u), 128u * ((seq + 1u) & 3u), sw, sw1t, sb1, sbx, sbz, wait_turn);
+      else wait_turn();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.turn[(SS + 1) % kSlots]);  // the next slot may issue now
+      if (real) commit_elect(&S.mma_done[SS]);
+      if (t) t[2] = clock64();
+    }
+  }
+}
+
+// The detect warp (A6-A8 bookkeeping, detect mode): per tile, in the CTA's slot order, it
+// combines the four column-half-1 warps' ballots and min keys (posted after their phase-6
+// hand-off), publishes the per-waypoint min key (atomicMin) and allocates the tile's staging
+// records (atomicAdd), then posts the tile's staging base for the phase-11 record writes.
+// Its global atomics' latency is on no epilogue warp's path.
+DEVI void detect_loop(SmemTC &S, const QueryArgs &a, int64_t n_tiles, int64_t stride, int lane) {
+  uint32_t ph = 0u;  // bit s: parity of slot s's det_in
+  int it = 0;
+  for (int64_t base = (int64_t)blockIdx.x * kSlots; base < n_tiles; base += stride, ++it) {
+    for (int s = 0; s < kSlots; ++s) {
+      const int64_t T = base + s;
+      if (T >= n_tiles) break;
+      wait_bar(&S.det_in[s], (ph >> s) & 1u);
+      ph ^= 1u << s;
+      unsigned long long km = lane < 4 ? S.kmin[s][lane] : ~0ull;
+      int cnt = lane < 4 ? __popc(S.act[s][lane]) : 0;
+#pragma unroll
+      for (int o = 2; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, km, o);
+        km = other < km ? other : km;
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+      }
+      if (lane == 0) {
+        const int w = S.wtile[s][it & 1];
+        if (km != ~0ull) atomicMin(a.ds.wp_key + w, km);
+        int b = 0;
+        if (cnt > 0) {
+          const unsigned long long pb = atomicAdd(a.ds.counter, (unsigned long long)cnt);
+          if (pb + cnt > (unsigned long long)a.ds.max_active) {
+            atomicOr(a.ds.counter + 1, 1ull);
+            b = -1;
+          } else {
+            b = (int)pb;
+          }
+        }
+        S.sbase[s] = b;
+        a.ds.tile_meta[T] = make_int2(b, cnt);
+        mbar_arrive(&S.det_out[s]);
+      }
+      __syncwarp();
+    }
+  }
 }
 
 // kSE2: the SE(2) frame variant (R24) as its own instantiation, so the default
@@ -184,118 +340,101 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned view (SWIZZLE_128B atoms); pointer arithmetic on the __shared__ array
   // keeps the shared address space visible to the compiler (LDS/STS, not generic LD/ST)
-  SmemTC &S = *reinterpret_cast<SmemTC *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+  SmemTC &S = *reinterpret_cast<SmemTC *>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (smem_u32(smem_raw) & 1023u) __trap();  // SWIZZLE_128B operands need 1024-B alignment
 
   // ---- one-time setup: the resident weights (already in their UMMA layouts in global
-  // memory, 196 KB) -> smem by 1-D bulk copies (cp.async.bulk, the TMA engine) completing on
-  // S.wbar; only the MMA warps wait for them (before their first UMMA), so the copy overlaps
-  // the epilogue warps' staging of the first tiles ----
+  // memory) -> smem by 1-D bulk copies (cp.async.bulk, the TMA engine) completing on S.wbar;
+  // only the MMA warps wait for them (before their first UMMA), so the copy overlaps the
+  // epilogue warps' staging of the first tiles ----
   if (tid == 0) {
     S.one = 1u;
     mbar_init(&S.wbar, 1);
     fence_barrier_init();
     constexpr uint32_t kChunk = 32768;
-    mbar_expect_tx(&S.wbar, (uint32_t)(kWBytes + kW1tBytes + kB1Bytes + 5 * kBextBytes));
+    mbar_expect_tx(&S.wbar, (uint32_t)(kWBytes + kW1tBytes + kB1Bytes + 5 * kBiasCore));
     for (uint32_t o = 0; o < (uint32_t)kWBytes; o += kChunk)
       bulk_g2s(S.w + o, static_cast<const uint8_t *>(W.w_sw128) + o, kChunk, &S.wbar);
     bulk_g2s(S.w1t, W.w1t_sw128, kW1tBytes, &S.wbar);
     bulk_g2s(S.b1, W.b1_nosw, kB1Bytes, &S.wbar);
-    bulk_g2s(S.bext, W.bext_nosw, 5 * kBextBytes, &S.wbar);
+    for (int l = 0; l < 5; ++l)  // K core 0 of each bias block (its K core 1 is all zeros)
+      bulk_g2s(S.bext[l], static_cast<const uint8_t *>(W.bext_nosw) + l * kBextBytes, kBiasCore, &S.wbar);
   }
+  for (int i = tid; i < kBiasCore / 16; i += kThreads) reinterpret_cast<uint4 *>(S.bzero)[i] = make_uint4(0, 0, 0, 0);
   if (warp == 0) {
     tmem_alloc(&S.tmem_base, 512);
     tmem_relinquish();
   }
   if (tid == 32) {
-    mbar_init(&S.mma_done[0], 1);
-    mbar_init(&S.mma_done[1], 1);
-    mbar_init(&S.epi_done[0], kEpiArrivals);
-    mbar_init(&S.epi_done[1], kEpiArrivals);
-    S.turn = 0u;
+    for (int i = 0; i < kSlots; ++i) {
+      mbar_init(&S.mma_done[i], 1);
+      mbar_init(&S.epi_done[i], kEpiArrivals);
+    }
+    for (int i = 0; i < kSlots; ++i) {
+      mbar_init(&S.turn[i], 1);
+      mbar_init(&S.det_in[i], 4);
+      mbar_init(&S.det_out[i], 1);
+    }
+    mbar_arrive(&S.turn[0]);  // slot 0 issues the CTA's first phase
     fence_barrier_init();
   }
-  if (tid < 2 * kNdof) {  // q rows of the slots' first tiles (later tiles: cp.async, phases 1-3)
+  if (tid < kSlots * kNdof) {  // q rows of the slots' first tiles (later tiles: cp.async, phases 1-3)
     const int s0 = tid / kNdof, i = tid - s0 * kNdof;
-    const int64_t T0 = (int64_t)blockIdx.x * 2 + s0;
+    const int64_t T0 = (int64_t)blockIdx.x * kSlots + s0;
     if (T0 < query_tiles(a)) {
       const int w0 = tile_step(a, T0);
       S.qn[s0][0][i] = __ldg(a.q + (int64_t)w0 * kNdof + i);
       if (i == 0) S.wtile[s0][0] = w0;
     }
   }
-  fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+  fence_proxy_async_smem();  // generic-proxy smem writes (zero K core) -> visible to the tensor core
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tbase = S.tmem_base;
+  if (tbase != 0u) __trap();  // the MMA warps address TMEM from column 0 (see mma_loop)
   const int64_t n_tiles = query_tiles(a);  // (partitioned: read from the device)
   const int64_t lb = a.scene.local_bound;
-  const int64_t stride = 2 * (int64_t)gridDim.x;
+  const int64_t stride = kSlots * (int64_t)gridDim.x;
 
   if (warp >= kEpiWarps) {
-    // ===================== two MMA warps: warp 16 + s issues slot s's UMMAs ================
-    // A commit stalls its issuing thread until the committed MMAs drain; with one issuer per
-    // slot the other slot's UMMAs keep the tensor pipe busy meanwhile (tools/mma_probe.py
-    // "two issuers").  The slots still alternate: a shared turn counter orders slot 0's
-    // phase p before slot 1's phase p before slot 0's phase p + 1.
-    const int ss = warp - kEpiWarps;
-    const uint32_t sw = smem_u32(S.w), sw1t = smem_u32(S.w1t), sb1 = smem_u32(S.b1);
-    const uint32_t sbx = smem_u32(S.bext);
-    volatile uint32_t *turn = &S.turn;
-    uint32_t ph = 0u;
-    long long *tr0 = (a.trace && blockIdx.x == 0 && lane == 0) ? a.trace : nullptr;
-    uint32_t seq = (uint32_t)ss;  // this slot's position in the global issue order
-    int itt = 0;
-    mbar_wait(&S.wbar, 0u);  // the resident weights have landed in shared memory
-    for (int64_t base = (int64_t)blockIdx.x * 2; base < n_tiles; base += stride, ++itt) {
-      const bool two = base + 1 < n_tiles;
-      if (ss == 1 && !two) break;
-      const bool next_l1 = base + stride + ss < n_tiles;  // this slot has a next tile
-#pragma unroll 1
-      for (int p = itt == 0 ? 0 : 1; p < kPhases; ++p, seq += 2) {
-        long long *t = (tr0 && itt < kTraceTiles) ? tr0 + ((size_t)itt * kTracePhases + p) * 4 + 2 * ss : nullptr;
-        long long *t2 = t ? t + (size_t)(kTraceRoles - 1) * kTraceTiles * kTracePhases * 4 : nullptr;
-        if (t2) t2[0] = clock64();
-        mbar_wait(&S.epi_done[ss], ph);
-        ph ^= 1u;
-        if (two) {
-          const long long tw = clock64();
-          while (*turn != seq) {
-            if (clock64() - tw > (1ll << 34)) __trap();
-          }
-        }
-        if (t2) t2[1] = clock64();
-        fence_after();
-        if (t) t[0] = clock64();
-        issue_phase<F16>(p, tbase + (uint32_t)ss * 256u, sw, sw1t, sb1, sbx, &S.mma_done[ss], two ? turn : nullptr, seq + 1,
-                         next_l1);
-        if (t) t[1] = clock64();
-      }
-    }
+    // ============ three MMA warps: warp 24 + s issues slot s's phases, in CTA order ============
+    // (the slot is a template argument, so that the issue loop's operands are warp-uniform to
+    // the compiler and live in uniform registers)
+    if (warp == kMmaWarp0) mma_loop<F16, 0>(S, a, n_tiles, stride, lane);
+    else if (warp == kMmaWarp0 + 1) mma_loop<F16, 1>(S, a, n_tiles, stride, lane);
+    else if (warp == kMmaWarp0 + 2) mma_loop<F16, 2>(S, a, n_tiles, stride, lane);
+    else if (a.detect) detect_loop(S, a, n_tiles, stride, lane);
     __syncwarp();
     fence_before();
     __syncthreads();
     return;
   }
   const int s = warp >> 3;          // tile slot
-  const int hh = (warp >> 2) & 1;   // accumulator column half: units 64 hh .. 64 hh + 63
+  const int hh = (warp >> 2) & 1;   // column half: accumulator columns 32 hh + {0..31, 64..95}
   const int qd = warp & 3;          // TMEM lane quarter of this warp (warp % 4)
   const int row = qd * 32 + lane;   // pair within the tile = TMEM lane
-  const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-  const uint32_t tS = tbase + (uint32_t)s * 256u + lane_off;  // this slot, this lane quarter
-  const uint32_t tD = tS + 64u * hh;
-  const uint32_t tA = tS + kColA + 32u * hh;
+  const uint32_t tL = tbase + ((uint32_t)(qd * 32) << 16);  // region 0, this lane quarter
+  uint32_t seq = (uint32_t)s;       // CTA phase index of the slot's next MMA phase
+  auto region = [&](uint32_t k) { return tL + 128u * (k & 3u); };
   uint32_t *mk = &S.mask[s][0][0][hh * 128 + row];  // + (layer * 2 + word) * kEpiPerSlot
-  if (hh == 0) {  // the constant "ones" A block of the bias GEMM step: {1, 1, 0, ...}
-    uint32_t ones[8] = {pack2<F16>(1.f, 1.f), 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-    st8(tS + kColOnes, ones);
-  }
-  // epilogue phase done: TMEM stores complete and ordered before the MMA warp's UMMAs
-  auto hand_off = [&](int, bool) {
+  // epilogue phase done: this warp's TMEM stores complete and ordered before the MMA warp's
+  // UMMAs (every lane waits for its stores and fences, then one lane arrives)
+  int it = 0;
+  // (diagnostics) per-warp hand-off stamps [warp][tile][phase] after the role blocks
+  long long *twarp = (a.trace && blockIdx.x == 0 && lane == 0)
+                         ? a.trace + (size_t)(2 * kSlots) * kTraceTiles * kTracePhases * 4 + (size_t)warp * kTraceTiles * kPhases
+                         : nullptr;
+  long long *trc = nullptr;  // (diagnostics) this phase's stamps of epilogue warp 0 of the slot
+  auto hand_off = [&](int p) {
+    if (trc) trc[2] = clock64();
     wait_st();
     fence_before();
-    mbar_arrive(&S.epi_done[s]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.epi_done[s]);
+    if (twarp && p >= 0 && it < kTraceTiles) twarp[it * kPhases + p] = clock64();
+    if (trc) trc[3] = clock64();
   };
   // cp.async prefetch of this lane's point of tile TT into S.ptn[s][row] (zero if none);
   // issued by the column-half-0 threads, which alone read it
@@ -336,18 +475,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     }
   };
   // A2 + A1 of tile TT: pair generation, base-frame bias p' = p - [q_x, q_y, 0]
-  // and the split layer-1 operands -> TMEM A (K = 32: half 0 writes K 0..15,
-  // half 1 K 16..31), then hand off.  Returns the pair's liveness (meaningful in half 0).
-  // SE(2) frame (R24): p'_xy = R(-theta)(p_xy - b), theta channel fed 0; p'_xy is kept in
-  // S.pprime[s][par] for the theta gradient at phase 11 (__sincosf: abs error ~1e-6 on
-  // [-pi, pi], far below the 16-bit operand rounding).
-  auto stage_a1 = [&](int64_t TT, int par) -> bool {
+  // and the split layer-1 operands -> TMEM columns kColX.. of region tx
+  // (K = 32: half 0 writes K 0..15, half 1 K 16..31).  Returns the pair's liveness
+  // (meaningful in half 0).  SE(2) frame (R24): p'_xy = R(-theta)(p_xy - b), theta channel
+  // fed 0; p'_xy is kept in pp (half 0's registers) for the theta gradient at phase 11
+  // (__sincosf: abs error ~1e-6 on [-pi, pi], far below the 16-bit operand rounding).
+  float2 pp = make_float2(0.f, 0.f);
+  auto stage_a1 = [&](int par, uint32_t tx) -> bool {
     const float *qw = S.qn[s][par];
     float v[16];
     bool lv = false;
     if (hh == 0) {  // K 0..15: p'_x, p'_y, p_z, theta, j1 (3 each), x_hi of j2
       const float4 pt = S.ptn[s][row];
-      lv = S.slotn[s][par][row] != ~0u && pt.w > 0.f;
+      const uint32_t sl = S.slotn[s][par][row];
+      lv = sl != ~0u && pt.w > 0.f;
+      if (sl != ~0u && !lv) S.slotn[s][par][row] = sl | 0x80000000u;
       float dx = pt.x - qw[0], dy = pt.y - qw[1], th = qw[2];
       if constexpr (kSE2) {
         float sn, cs;
@@ -356,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         dy = -sn * dx + cs * dy;
         dx = rx;
         th = 0.f;
-        S.pprime[s][par][row] = make_float2(dx, dy);
+        pp = make_float2(dx, dy);
       }
       split3<F16>(dx, v);
       split3<F16>(dy, v + 3);
@@ -377,22 +519,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     uint32_t a1[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) a1[i] = pack2<F16>(v[2 * i], v[2 * i + 1]);
-    st8(tS + kColX + 8u * hh, a1);
+    st8(tx + kColX + 8u * hh, a1);
     return lv;
   };
   const uint32_t one = S.one;
-  // forward epilogue of layer l = p + 1 (p = 0..4): z = D (bias folded in); h = ReLU(z) -> A,
-  // 1-bit masks -> smem, then hand off.  (16-column chunks, the TMEM load of chunk c + 1 in
-  // flight while chunk c is packed.)  Phase 0 of every tile after the first runs inside the
-  // previous tile's phase 11.
-  auto fwd_epi = [&](int p, long long *tr) {
+  // forward epilogue of layer l = p + 1 (p = 0..4): z = D (bias folded in); h = ReLU(z) -> A
+  // (in place), 1-bit masks -> smem; half 1 also writes the "ones" block of the next phase's
+  // bias step; then hand off.  (16-column chunks, the TMEM load of chunk c + 1 in flight
+  // while chunk c is packed.)
+  auto fwd_epi = [&](int p, uint32_t rD) {
+    const uint32_t tD = rD + 32u * hh;
     uint32_t rb[2][16], m = 0u;
-    ld16(tD, rb[0]);
+    ld16(tD + DC(0), rb[0]);
     wait_ld();
-    if (tr) tr[(p + 1) * 4 + 0] = clock64();
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      if (c < 3) ld16(tD + 16 * (c + 1), rb[(c + 1) & 1]);
+      if (c < 3) ld16(tD + DC(c + 1), rb[(c + 1) & 1]);
       const uint32_t *rr = rb[c & 1];
       uint32_t pk[8];
 #pragma unroll
@@ -401,62 +543,64 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         pk[(j >> 1) + 1] = pack2_relu<F16>(__uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3]));
         m |= mask_group_f(pk[j >> 1], pk[(j >> 1) + 1], ((c & 1) * 16 + j) >> 2, one);
       }
-      st8(tA + 8 * c, pk);
+      st8(tD + AC(c), pk);
       if (c & 1) {
         mk[(p * 2 + (c >> 1)) * kEpiPerSlot] = m;
         m = 0u;
       }
       if (c < 3) wait_ld();
     }
-    if (tr) tr[(p + 1) * 4 + 2] = clock64();
-    hand_off(p + 1, true);
-    if (tr) tr[(p + 1) * 4 + 3] = clock64();
+    if (hh == 1) {  // the constant "ones" A block of the bias step: {1, 1, 0, ...} (columns 48..55,
+                    // loaded by this half's chunk 1)
+      const uint32_t ones[8] = {pack2<F16>(1.f, 1.f), 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+      st8(rD + kColOnes, ones);
+    }
+    hand_off(p);
   };
   uint32_t ph = 0u;
-  int it = 0;
-  const bool tracer = a.trace && blockIdx.x == 0 && lane == 0;  // lane 0 of every epilogue warp of CTA 0
+  long long *trb = (a.trace && blockIdx.x == 0 && lane == 0 && hh == 0 && qd == 0)
+                       ? a.trace + (size_t)(kSlots + s) * kTraceTiles * kTracePhases * 4
+                       : nullptr;
   bool live_n = false;
-  if ((int64_t)blockIdx.x * 2 + s < n_tiles) {
+  if ((int64_t)blockIdx.x * kSlots + s < n_tiles) {
     if (hh == 0) {
-      prefetch_pt((int64_t)blockIdx.x * 2 + s, 0);
+      prefetch_pt((int64_t)blockIdx.x * kSlots + s, 0);
       cp_async_wait_all();
     }
-    live_n = stage_a1((int64_t)blockIdx.x * 2 + s, 0);
-    hand_off(0, true);
+    live_n = stage_a1(0, region(seq + 1u));  // phase 0's A region
+    hand_off(-1);
   }
-  for (int64_t T = (int64_t)blockIdx.x * 2 + s; T < n_tiles; T += stride, ++it) {
-    long long *tr = (tracer && it < kTraceTiles) ? a.trace + (size_t)((1 + warp) * kTraceTiles + it) * kTracePhases * 4 : nullptr;
-    if (tr) tr[0] = clock64();
-    const bool live = live_n;
+  for (int64_t T = (int64_t)blockIdx.x * kSlots + s; T < n_tiles; T += stride, ++it) {
+    bool live = live_n;  // (half 1: re-read at phase 5 from S.livef)
     float f = 0.f;
-    int ridx = -1;  // staging record index (detect), -1 = none
-    unsigned long long pend_b = 0ull;  // (row 0) staging allocation of this tile, in flight
-    int pend_cnt = 0;
 #pragma unroll 1
-    for (int p = it == 0 ? 0 : 1; p < kPhases; ++p) {
-      mbar_wait(&S.mma_done[s], ph);
-      if (tr) tr[(p + 1) * 4 + 1] = clock64();
+    for (int p = 0; p < kPhases; ++p, seq += kSlots) {
+      long long *tr = (trb && it < kTraceTiles) ? trb + ((size_t)it * kTracePhases + p) * 4 : nullptr;
+      wait_bar(&S.mma_done[s], ph);
+      if (tr) tr[0] = clock64();
+      trc = tr;
       ph ^= 1u;
       fence_after();
+      const uint32_t rD = region(seq);
       if (p < 5) {
-        fwd_epi(p, tr);
+        fwd_epi(p, rD);
         if (p == 1 || p == 3) stage_q(p, T + stride, (it + 1) & 1);
       } else if (p == 5) {
         // ---- layer 6: e6 = w7 (.) 1[z6 > 0] -> A; f = w7 . ReLU(z6) + b7 (fp32) ----
         // (16-column chunks; the TMEM load of chunk c + 1 in flight while chunk c is used)
         float fa[4] = {0.f, 0.f, 0.f, 0.f};
+        const uint32_t tD = rD + 32u * hh;
         // the output row comes from the kernel parameters with compile-time offsets (one body
         // per column half), i.e. as direct constant-bank operands: no shared-memory loads
         auto layer6 = [&](auto u0c) {
           constexpr int U0 = decltype(u0c)::value;
           uint32_t rb[2][16];
-          ld16(tD, rb[0]);
+          ld16(tD + DC(0), rb[0]);
           wait_ld();
-          if (tr) tr[(p + 1) * 4 + 0] = clock64();
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const int cb = 16 * c;
-            if (c < 3) ld16(tD + cb + 16, rb[(c + 1) & 1]);
+            const int cb = (int)DC(c);
+            if (c < 3) ld16(tD + DC(c + 1), rb[(c + 1) & 1]);
             const uint32_t *rr = rb[c & 1];
             uint32_t pk[8];
 #pragma unroll
@@ -472,39 +616,42 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
               fa[2] = fmaf(W.w7half_p[u + 2], z2 + fabsf(z2), fa[2]);
               fa[3] = fmaf(W.w7half_p[u + 3], z3 + fabsf(z3), fa[3]);
             }
-            st8(tA + cb / 2, pk);
+            st8(tD + AC(c), pk);
             if (c < 3) wait_ld();
           }
         };
         if (hh == 0) layer6(std::integral_constant<int, 0>{});
-        else layer6(std::integral_constant<int, 64>{});
-        if (tr) tr[(p + 1) * 4 + 2] = clock64();
-        hand_off(p + 1, s == 1 || T + 1 < n_tiles);
-        if (tr) tr[(p + 1) * 4 + 3] = clock64();
-        // f = w7 . h6 + b7 (fp32, no output activation: signed value)
+        else layer6(std::integral_constant<int, 32>{});
+        hand_off(p);
+        // f = w7 . h6 + b7 (fp32, no output activation: signed value); both
+        // column halves form it from the two partial sums (half 0 writes the records, half 1
+        // thresholds)
         S.fpart[s][hh][row] = (fa[0] + fa[1]) + (fa[2] + fa[3]);
         if (hh == 0 && qd == 0) cp_async_wait_all();  // S.qn of the next tile (stage_q)
         named_bar_sync(1 + s, kEpiPerSlot);
-        if (hh == 0) {
-          f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
+        f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
+        if (hh == 1) {
+          const uint32_t sl = S.slotn[s][it & 1][row];
+          live = (sl >> 31) == 0u;
           if (!a.detect) {
             const int w = S.wtile[s][it & 1];
-            const int64_t slot = S.slotn[s][it & 1][row];
+            const int64_t slot = sl & 0x7fffffffu;
             if (slot < lb) a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
           }
-          prefetch_pt(T + stride, (it + 1) & 1);  // the next tile's point, needed at phase 10
+        } else {
+          prefetch_pt(T + stride, (it + 1) & 1);  // the next tile's point, needed at phase 11
         }
       } else if (p < 11) {
-        // ---- backward: g_{l-1} = D; e_{l-1} = g (.) 1[z_{l-1} > 0] -> A ----
+        // ---- backward: g_{l-1} = D; e_{l-1} = g (.) 1[z_{l-1} > 0] -> A (in place) ----
         const int mi = 10 - p;
         const uint32_t mw[2] = {mk[(mi * 2) * kEpiPerSlot], mk[(mi * 2 + 1) * kEpiPerSlot]};
+        const uint32_t tD = rD + 32u * hh;
         uint32_t rb[2][16];
-        ld16(tD, rb[0]);
+        ld16(tD + DC(0), rb[0]);
         wait_ld();
-        if (tr) tr[(p + 1) * 4 + 0] = clock64();
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          if (c < 3) ld16(tD + 16 * (c + 1), rb[(c + 1) & 1]);
+          if (c < 3) ld16(tD + DC(c + 1), rb[(c + 1) & 1]);
           const uint32_t *rr = rb[c & 1];
           uint32_t pk[8];
 #pragma unroll
@@ -514,21 +661,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
             pk[j >> 1] = pack2<F16>(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1])) & lo;
             pk[(j >> 1) + 1] = pack2<F16>(__uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3])) & hi;
           }
-          st8(tA + 8 * c, pk);
+          st8(tD + AC(c), pk);
           if (c < 3) wait_ld();
         }
-        if (p == 10 && T + stride < n_tiles) {
-          // A2 + A1 of the slot's next tile -> x (kColX), issued with this tile's g0 GEMM
-          if (hh == 0) cp_async_wait_all();  // this thread's point of the next tile (phase 5)
-          live_n = stage_a1(T + stride, (it + 1) & 1);
-        }
-        if (tr) tr[(p + 1) * 4 + 2] = clock64();
-        hand_off(p + 1, s == 1 || T + 1 < n_tiles);
-        if (tr) tr[(p + 1) * 4 + 3] = clock64();
-        if (p == 6 && hh == 0 && a.detect) {
-          // A6/A7 (overlaps the tensor core): threshold, per-tile slots, per-waypoint min key
-          const int w = S.wtile[s][it & 1];
-          const int64_t slot = S.slotn[s][it & 1][row];  // (live implies a real pair)
+        hand_off(p);
+        if (p == 6 && hh == 1 && a.detect) {
+          // A6/A7 (overlaps the tensor core): threshold and the warp's min key -> the detect warp
+          const int64_t slot = S.slotn[s][it & 1][row] & 0x7fffffffu;  // (live implies a real pair)
           const bool act = live && (f - a.delta <= a.tau);
           const unsigned bal = __ballot_sync(0xffffffffu, act);
           unsigned long long key = ~0ull;
@@ -543,55 +682,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
           if (lane == 0) {
             S.act[s][qd] = bal;
             S.kmin[s][qd] = key;
+            mbar_arrive(&S.det_in[s]);
           }
-          named_bar_sync(3 + s, 128);
-          int rk = __popc(bal & ((1u << lane) - 1u));
-          for (int i = 0; i < qd; ++i) rk += __popc(S.act[s][i]);
-          ridx = act ? rk : -1;  // rank in the tile; the tile's staging base is added at phase 11
-          if (row == 0) {
-            unsigned long long km = S.kmin[s][0];
-            int cnt = 0;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              km = S.kmin[s][i] < km ? S.kmin[s][i] : km;
-              cnt += __popc(S.act[s][i]);
-            }
-            if (km != ~0ull) atomicMin(a.ds.wp_key + w, km);
-            // staging allocation: the (contended) atomic's result is consumed two phases
-            // later, so its latency stays off the epilogue's critical path
-            pend_cnt = cnt;
-            pend_b = cnt > 0 ? atomicAdd(a.ds.counter, (unsigned long long)cnt) : 0ull;
-          }
-        }
-        if (p == 8 && hh == 0 && a.detect && row == 0) {
-          int base = 0;
-          if (pend_cnt > 0) {
-            if (pend_b + pend_cnt > (unsigned long long)a.ds.max_active) {
-              atomicOr(a.ds.counter + 1, 1ull);
-              base = -1;
-            } else {
-              base = (int)pend_b;
-            }
-          }
-          S.sbase[s] = base;
-          a.ds.tile_meta[T] = make_int2(base, pend_cnt);
         }
       } else {
-        // ---- phase 11 + phase 0 of the slot's next tile: the UMMAs were issued together ----
-        // first the next tile's layer-1 epilogue (so its phase 1 can be issued), then g0 =
-        // W1^T e1 (16 columns at kColG0) -> d f / d q by the chain rule (R3) and the outputs
-        if (T + stride < n_tiles) fwd_epi(0, nullptr);
+        // ---- phase 11: g0 = W1^T e1 (columns 0..15) -> d f / d q by the chain rule (R3) and
+        // the outputs.  Half 0 loads g0 and both halves stage the next tile's layer-1 operands
+        // (columns kColX.. of this region, the A operand of the next phase) before the hand-off;
+        // the outputs are written after it.  (The hand-off also follows the slot's last tile:
+        // it keeps the region, g0 included, from being reused before the load.) ----
         uint32_t r[16];
         if (hh == 0) {
-          ld16(tS + kColG0, r);
+          ld16(rD, r);
           wait_ld();
         }
-        if (tr) tr[(p + 1) * 4 + 0] = clock64();
-        if (tr) tr[(p + 1) * 4 + 2] = clock64();
+        const float2 pp_t = pp;  // (SE(2)) p'_xy of this tile; stage_a1 overwrites pp
+        if (T + stride < n_tiles) {
+          if (hh == 0) cp_async_wait_all();  // this thread's point of the next tile (phase 5)
+          live_n = stage_a1((it + 1) & 1, rD);
+        }
+        hand_off(p);
         if (hh == 0) {
           const int w = S.wtile[s][it & 1];
-          const int64_t slot = S.slotn[s][it & 1][row];
-          if (tr) tr[1] = clock64();  // (phase-11 detail: step and slot read)
+          const int64_t slot = S.slotn[s][it & 1][row] & 0x7fffffffu;
           float gq[kNdof];
           gq[0] = a.tgrad ? __uint_as_float(r[3]) : -__uint_as_float(r[0]);
           gq[1] = a.tgrad ? __uint_as_float(r[4]) : -__uint_as_float(r[1]);
@@ -601,18 +714,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
             float sn, cs;
             __sincosf(S.qn[s][it & 1][2], &sn, &cs);
             const float gx = __uint_as_float(r[0]), gy = __uint_as_float(r[1]);
-            const float2 pp = S.pprime[s][it & 1][row];
             gq[0] = -(cs * gx - sn * gy);
             gq[1] = -(sn * gx + cs * gy);
-            gq[2] = gx * pp.y - gy * pp.x;
+            gq[2] = gx * pp_t.y - gy * pp_t.x;
           }
           if (a.detect) {
-            named_bar_sync(3 + s, 128);  // S.sbase[s] (written at phase 8 by row 0) is visible
-            if (tr) tr[2] = clock64();  // (phase-11 detail: barrier passed)
+            // rank of the pair among the tile's actives (the ballots of the four lane quarters)
+            // + the tile's staging base, posted by the detect warp
+            wait_bar(&S.det_out[s], (uint32_t)it & 1u);
+            const bool act = live && (f - a.delta <= a.tau);
+            int rk = __popc(S.act[s][qd] & ((1u << lane) - 1u));
+            for (int i = 0; i < qd; ++i) rk += __popc(S.act[s][i]);
             const int base = S.sbase[s];
-            ridx = (ridx >= 0 && base >= 0) ? base + ridx : -1;
-            if (ridx >= 0) {
-              float4 *dst = reinterpret_cast<float4 *>(a.ds.staging + ridx);
+            if (act && base >= 0) {
+              float4 *dst = reinterpret_cast<float4 *>(a.ds.staging + base + rk);
               dst[0] = make_float4(f, gq[0], gq[1], gq[2]);
               dst[1] = make_float4(gq[3], gq[4], gq[5], gq[6]);
               dst[2] = make_float4(gq[7], gq[8], __uint_as_float((unsigned)w),
@@ -630,8 +745,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
             }
           }
         }
-        if (tr) tr[(p + 1) * 4 + 3] = clock64();
       }
+      if (tr) tr[1] = clock64();
     }
   }
   fence_before();
@@ -642,13 +757,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
 
 template <bool F16>
 cudaError_t launch_tc_t(const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s) {
-  const int smem = (int)sizeof(SmemTC) + 1024;
+  const int smem = (int)sizeof(SmemTC);
   auto kern = a.frame ? k_mlp_tc<F16, true> : k_mlp_tc<F16, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   // a partitioned detect knows its tile count on the device only: one CTA per SM
-  const int64_t n_tiles = a.part.tile_wp ? 2 * (int64_t)num_sms : (int64_t)a.n_wp * a.tiles_per_wp;
-  int64_t grid = (n_tiles + 1) / 2;
+  const int64_t n_tiles = a.part.tile_wp ? kSlots * (int64_t)num_sms : (int64_t)a.n_wp * a.tiles_per_wp;
+  int64_t grid = (n_tiles + kSlots - 1) / kSlots;
   if (grid > num_sms) grid = num_sms;
   if (grid < 1) return cudaSuccess;
   kern<<<(unsigned)grid, kThreads, smem, s>>>(w, a);
