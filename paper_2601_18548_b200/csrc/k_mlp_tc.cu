@@ -53,6 +53,13 @@ using namespace tc;
 // slots from the busy epilogue warps of its SM sub-partition; with a suspend-time hint the
 // warp sleeps until the phase completes (or the hint expires).
 DEVI void wait_bar(uint64_t *bar, uint32_t parity) { mbar_wait_hint<20000>(bar, parity); }
+DEVI void wait_bar_addr(uint32_t addr, uint32_t parity) {
+  if (mbar_try_wait_hint(addr, parity, 20000)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait_hint(addr, parity, 20000)) {
+    if (clock64() - t0 > (1ll << 34)) __trap();
+  }
+}
 
 constexpr int H = 128;
 constexpr int kSlots = 3;                         // tiles in flight
@@ -249,13 +256,14 @@ DEVI void issue_phase(int p, uint32_t d, uint32_t av, uint32_t sw, uint32_t sw1t
 // phase) is issued after phase k - 1 (S.turn[SS], arrived on by the previous slot's MMA warp);
 // a slot without a tile in the last round passes its turns.
 // TMEM base address 0 (the kernel's single 512-column allocation, checked at setup).
-template <bool F16, int SS>
+template <bool F16, int SS, bool kTrace>
 DEVI void mma_loop(SmemTC &S, const QueryArgs &a, int64_t n_tiles, int64_t stride, int lane) {
   const uint32_t sw = smem_u32(S.w), sw1t = smem_u32(S.w1t), sb1 = smem_u32(S.b1);
   const uint32_t sbx = smem_u32(S.bext), sbz = smem_u32(S.bzero);
   uint32_t ph = 0u, seq = (uint32_t)SS;
-  long long *tr = (a.trace && blockIdx.x == 0 && lane == 0) ? a.trace + (size_t)SS * kTraceTiles * kTracePhases * 4
-                                                           : nullptr;
+  long long *tr = (kTrace && a.trace && blockIdx.x == 0 && lane == 0)
+                      ? a.trace + (size_t)SS * kTraceTiles * kTracePhases * 4
+                      : nullptr;
   mbar_wait(&S.wbar, 0u);  // the resident weights have landed in shared memory
   int it = 0;
   for (int64_t base = (int64_t)blockIdx.x * kSlots; base < n_tiles; base += stride, ++it) {
@@ -335,7 +343,8 @@ DEVI void detect_loop(SmemTC &S, const QueryArgs &a, int64_t n_tiles, int64_t st
 
 // kSE2: the SE(2) frame variant (R24) as its own instantiation, so the default
 // translation-frame kernel carries none of its code or registers
-template <bool F16, bool kSE2>
+// kTrace: the diagnostics instantiation (gcdf_debug_trace), the only one with clock64 stamps
+template <bool F16, bool kSE2, bool kTrace>
 __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, const QueryArgs a) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned view (SWIZZLE_128B atoms); pointer arithmetic on the __shared__ array
@@ -402,9 +411,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     // ============ three MMA warps: warp 24 + s issues slot s's phases, in CTA order ============
     // (the slot is a template argument, so that the issue loop's operands are warp-uniform to
     // the compiler and live in uniform registers)
-    if (warp == kMmaWarp0) mma_loop<F16, 0>(S, a, n_tiles, stride, lane);
-    else if (warp == kMmaWarp0 + 1) mma_loop<F16, 1>(S, a, n_tiles, stride, lane);
-    else if (warp == kMmaWarp0 + 2) mma_loop<F16, 2>(S, a, n_tiles, stride, lane);
+    if (warp == kMmaWarp0) mma_loop<F16, 0, kTrace>(S, a, n_tiles, stride, lane);
+    else if (warp == kMmaWarp0 + 1) mma_loop<F16, 1, kTrace>(S, a, n_tiles, stride, lane);
+    else if (warp == kMmaWarp0 + 2) mma_loop<F16, 2, kTrace>(S, a, n_tiles, stride, lane);
     else if (a.detect) detect_loop(S, a, n_tiles, stride, lane);
     __syncwarp();
     fence_before();
@@ -415,31 +424,38 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   const int hh = (warp >> 2) & 1;   // column half: accumulator columns 32 hh + {0..31, 64..95}
   const int qd = warp & 3;          // TMEM lane quarter of this warp (warp % 4)
   const int row = qd * 32 + lane;   // pair within the tile = TMEM lane
-  const uint32_t tL = tbase + ((uint32_t)(qd * 32) << 16);  // region 0, this lane quarter
+  const uint32_t tL = tbase + ((uint32_t)(qd * 32) << 16) + 32u * hh;  // region 0, this lane quarter, column half
   uint32_t seq = (uint32_t)s;       // CTA phase index of the slot's next MMA phase
   auto region = [&](uint32_t k) { return tL + 128u * (k & 3u); };
   uint32_t *mk = &S.mask[s][0][0][hh * 128 + row];  // + (layer * 2 + word) * kEpiPerSlot
+  const uint32_t bar_mma = smem_u32(&S.mma_done[s]), bar_epi = smem_u32(&S.epi_done[s]);
+  int it = 0;
+  // (diagnostics, kTrace only) per-warp hand-off stamps [warp][tile][phase] after the role
+  // blocks, and epilogue warp 0's stamps per phase
+  long long *twarp = nullptr, *trb = nullptr, *trc = nullptr;
+  if constexpr (kTrace) {
+    if (a.trace && blockIdx.x == 0 && lane == 0) {
+      twarp = a.trace + (size_t)(2 * kSlots) * kTraceTiles * kTracePhases * 4 + (size_t)warp * kTraceTiles * kPhases;
+      if (hh == 0 && qd == 0) trb = a.trace + (size_t)(kSlots + s) * kTraceTiles * kTracePhases * 4;
+    }
+  }
   // epilogue phase done: this warp's TMEM stores complete and ordered before the MMA warp's
   // UMMAs (every lane waits for its stores and fences, then one lane arrives)
-  int it = 0;
-  // (diagnostics) per-warp hand-off stamps [warp][tile][phase] after the role blocks
-  long long *twarp = (a.trace && blockIdx.x == 0 && lane == 0)
-                         ? a.trace + (size_t)(2 * kSlots) * kTraceTiles * kTracePhases * 4 + (size_t)warp * kTraceTiles * kPhases
-                         : nullptr;
-  long long *trc = nullptr;  // (diagnostics) this phase's stamps of epilogue warp 0 of the slot
   auto hand_off = [&](int p) {
-    if (trc) trc[2] = clock64();
+    if constexpr (kTrace) if (trc) trc[2] = clock64();
     wait_st();
     fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&S.epi_done[s]);
-    if (twarp && p >= 0 && it < kTraceTiles) twarp[it * kPhases + p] = clock64();
-    if (trc) trc[3] = clock64();
+    if (lane == 0) mbar_arrive_addr(bar_epi);
+    if constexpr (kTrace) {
+      if (twarp && p >= 0 && it < kTraceTiles) twarp[it * kPhases + p] = clock64();
+      if (trc) trc[3] = clock64();
+    }
   };
   // cp.async prefetch of this lane's point of tile TT into S.ptn[s][row] (zero if none);
   // issued by the column-half-0 threads, which alone read it
-  // (the pair's local slot goes to S.slotn[s][par][row], read back by this same thread at
-  // phases 6 and 11 and by stage_a1: no per-tile index arithmetic on the critical path)
+  // (the pair's local slot goes to S.slotn[s][par][row], read back at phases 5, 6 and 11 and
+  // by stage_a1: no per-tile index arithmetic on the critical path)
   auto prefetch_pt = [&](int64_t TT, int par) {
     int wn = 0;
     int64_t sl = 0;
@@ -475,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     }
   };
   // A2 + A1 of tile TT: pair generation, base-frame bias p' = p - [q_x, q_y, 0]
-  // and the split layer-1 operands -> TMEM columns kColX.. of region tx
+  // and the split layer-1 operands -> TMEM columns kColX.. of the region at tx
   // (K = 32: half 0 writes K 0..15, half 1 K 16..31).  Returns the pair's liveness
   // (meaningful in half 0).  SE(2) frame (R24): p'_xy = R(-theta)(p_xy - b), theta channel
   // fed 0; p'_xy is kept in pp (half 0's registers) for the theta gradient at phase 11
@@ -519,48 +535,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     uint32_t a1[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) a1[i] = pack2<F16>(v[2 * i], v[2 * i + 1]);
-    st8(tx + kColX + 8u * hh, a1);
+    st8(tx - 32u * hh + kColX + 8u * hh, a1);
     return lv;
   };
   const uint32_t one = S.one;
-  // forward epilogue of layer l = p + 1 (p = 0..4): z = D (bias folded in); h = ReLU(z) -> A
-  // (in place), 1-bit masks -> smem; half 1 also writes the "ones" block of the next phase's
-  // bias step; then hand off.  (16-column chunks, the TMEM load of chunk c + 1 in flight
-  // while chunk c is packed.)
-  auto fwd_epi = [&](int p, uint32_t rD) {
-    const uint32_t tD = rD + 32u * hh;
-    uint32_t rb[2][16], m = 0u;
-    ld16(tD + DC(0), rb[0]);
-    wait_ld();
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      if (c < 3) ld16(tD + DC(c + 1), rb[(c + 1) & 1]);
-      const uint32_t *rr = rb[c & 1];
-      uint32_t pk[8];
-#pragma unroll
-      for (int j = 0; j < 16; j += 4) {
-        pk[j >> 1] = pack2_relu<F16>(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1]));
-        pk[(j >> 1) + 1] = pack2_relu<F16>(__uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3]));
-        m |= mask_group_f(pk[j >> 1], pk[(j >> 1) + 1], ((c & 1) * 16 + j) >> 2, one);
-      }
-      st8(tD + AC(c), pk);
-      if (c & 1) {
-        mk[(p * 2 + (c >> 1)) * kEpiPerSlot] = m;
-        m = 0u;
-      }
-      if (c < 3) wait_ld();
-    }
-    if (hh == 1) {  // the constant "ones" A block of the bias step: {1, 1, 0, ...} (columns 48..55,
-                    // loaded by this half's chunk 1)
-      const uint32_t ones[8] = {pack2<F16>(1.f, 1.f), 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-      st8(rD + kColOnes, ones);
-    }
-    hand_off(p);
-  };
   uint32_t ph = 0u;
-  long long *trb = (a.trace && blockIdx.x == 0 && lane == 0 && hh == 0 && qd == 0)
-                       ? a.trace + (size_t)(kSlots + s) * kTraceTiles * kTracePhases * 4
-                       : nullptr;
   bool live_n = false;
   if ((int64_t)blockIdx.x * kSlots + s < n_tiles) {
     if (hh == 0) {
@@ -571,25 +550,54 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     hand_off(-1);
   }
   for (int64_t T = (int64_t)blockIdx.x * kSlots + s; T < n_tiles; T += stride, ++it) {
-    bool live = live_n;  // (half 1: re-read at phase 5 from S.livef)
+    bool live = live_n;  // (half 1: re-read at phase 5 from S.slotn)
     float f = 0.f;
-#pragma unroll 1
-    for (int p = 0; p < kPhases; ++p, seq += kSlots) {
-      long long *tr = (trb && it < kTraceTiles) ? trb + ((size_t)it * kTracePhases + p) * 4 : nullptr;
-      wait_bar(&S.mma_done[s], ph);
-      if (tr) tr[0] = clock64();
-      trc = tr;
+    // one MMA phase of the tile (compile-time phase number: every phase is its own straight
+    // code, no run-time dispatch)
+    auto phase = [&](auto pc) {
+      constexpr int p = decltype(pc)::value;
+      if constexpr (kTrace) trc = (trb && it < kTraceTiles) ? trb + ((size_t)it * kTracePhases + p) * 4 : nullptr;
+      wait_bar_addr(bar_mma, ph);
+      if constexpr (kTrace) if (trc) trc[0] = clock64();
       ph ^= 1u;
       fence_after();
-      const uint32_t rD = region(seq);
-      if (p < 5) {
-        fwd_epi(p, rD);
-        if (p == 1 || p == 3) stage_q(p, T + stride, (it + 1) & 1);
-      } else if (p == 5) {
+      const uint32_t tD = region(seq);  // this lane quarter's and column half's accumulator
+      if constexpr (p < 5) {
+        // ---- forward epilogue of layer l = p + 1: z = D (bias folded in); h = ReLU(z) -> A
+        // (in place), 1-bit masks -> smem; half 1 also writes the "ones" block of the next
+        // phase's bias step.  (16-column chunks, the TMEM load of chunk c + 1 in flight while
+        // chunk c is packed) ----
+        uint32_t rb[2][16], m = 0u;
+        ld16(tD + DC(0), rb[0]);
+        wait_ld();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c < 3) ld16(tD + DC(c + 1), rb[(c + 1) & 1]);
+          const uint32_t *rr = rb[c & 1];
+          uint32_t pk[8];
+#pragma unroll
+          for (int j = 0; j < 16; j += 4) {
+            pk[j >> 1] = pack2_relu<F16>(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1]));
+            pk[(j >> 1) + 1] = pack2_relu<F16>(__uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3]));
+            m |= mask_group_f(pk[j >> 1], pk[(j >> 1) + 1], ((c & 1) * 16 + j) >> 2, one);
+          }
+          st8(tD + AC(c), pk);
+          if (c & 1) {
+            mk[(p * 2 + (c >> 1)) * kEpiPerSlot] = m;
+            m = 0u;
+          }
+          if (c < 3) wait_ld();
+        }
+        if (hh == 1) {  // the constant "ones" A block of the bias step: {1, 1, 0, ...} (columns
+                        // 48..55, loaded by this half's chunk 1)
+          const uint32_t ones[8] = {pack2<F16>(1.f, 1.f), 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+          st8(tD - 32u + kColOnes, ones);
+        }
+        hand_off(p);
+        if constexpr (p == 1 || p == 3) stage_q(p, T + stride, (it + 1) & 1);
+      } else if constexpr (p == 5) {
         // ---- layer 6: e6 = w7 (.) 1[z6 > 0] -> A; f = w7 . ReLU(z6) + b7 (fp32) ----
-        // (16-column chunks; the TMEM load of chunk c + 1 in flight while chunk c is used)
         float fa[4] = {0.f, 0.f, 0.f, 0.f};
-        const uint32_t tD = rD + 32u * hh;
         // the output row comes from the kernel parameters with compile-time offsets (one body
         // per column half), i.e. as direct constant-bank operands: no shared-memory loads
         auto layer6 = [&](auto u0c) {
@@ -641,11 +649,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         } else {
           prefetch_pt(T + stride, (it + 1) & 1);  // the next tile's point, needed at phase 11
         }
-      } else if (p < 11) {
+      } else if constexpr (p < 11) {
         // ---- backward: g_{l-1} = D; e_{l-1} = g (.) 1[z_{l-1} > 0] -> A (in place) ----
-        const int mi = 10 - p;
+        constexpr int mi = 10 - p;
         const uint32_t mw[2] = {mk[(mi * 2) * kEpiPerSlot], mk[(mi * 2 + 1) * kEpiPerSlot]};
-        const uint32_t tD = rD + 32u * hh;
         uint32_t rb[2][16];
         ld16(tD + DC(0), rb[0]);
         wait_ld();
@@ -665,41 +672,43 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
           if (c < 3) wait_ld();
         }
         hand_off(p);
-        if (p == 6 && hh == 1 && a.detect) {
-          // A6/A7 (overlaps the tensor core): threshold and the warp's min key -> the detect warp
-          const int64_t slot = S.slotn[s][it & 1][row] & 0x7fffffffu;  // (live implies a real pair)
-          const bool act = live && (f - a.delta <= a.tau);
-          const unsigned bal = __ballot_sync(0xffffffffu, act);
-          unsigned long long key = ~0ull;
-          if (live)
-            key = ((unsigned long long)ord_f32(f) << 32) |
-                  (unsigned long long)local_to_global(slot, a.scene.rank, a.scene.world);
+        if constexpr (p == 6) {
+          if (hh == 1 && a.detect) {
+            // A6/A7 (overlaps the tensor core): threshold and the warp's min key -> the detect warp
+            const int64_t slot = S.slotn[s][it & 1][row] & 0x7fffffffu;  // (live implies a real pair)
+            const bool act = live && (f - a.delta <= a.tau);
+            const unsigned bal = __ballot_sync(0xffffffffu, act);
+            unsigned long long key = ~0ull;
+            if (live)
+              key = ((unsigned long long)ord_f32(f) << 32) |
+                    (unsigned long long)local_to_global(slot, a.scene.rank, a.scene.world);
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-            key = other < key ? other : key;
-          }
-          if (lane == 0) {
-            S.act[s][qd] = bal;
-            S.kmin[s][qd] = key;
-            mbar_arrive(&S.det_in[s]);
+            for (int o = 16; o > 0; o >>= 1) {
+              const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+              key = other < key ? other : key;
+            }
+            if (lane == 0) {
+              S.act[s][qd] = bal;
+              S.kmin[s][qd] = key;
+              mbar_arrive(&S.det_in[s]);
+            }
           }
         }
       } else {
         // ---- phase 11: g0 = W1^T e1 (columns 0..15) -> d f / d q by the chain rule (R3) and
         // the outputs.  Half 0 loads g0 and both halves stage the next tile's layer-1 operands
-        // (columns kColX.. of this region, the A operand of the next phase) before the hand-off;
-        // the outputs are written after it.  (The hand-off also follows the slot's last tile:
-        // it keeps the region, g0 included, from being reused before the load.) ----
+        // (columns kColX.. of this region, the A operand of the next phase) before the
+        // hand-off; the outputs are written after it.  (The hand-off also follows the slot's
+        // last tile: it keeps the region, g0 included, from being reused before the load.) ----
         uint32_t r[16];
         if (hh == 0) {
-          ld16(rD, r);
+          ld16(tD, r);
           wait_ld();
         }
         const float2 pp_t = pp;  // (SE(2)) p'_xy of this tile; stage_a1 overwrites pp
         if (T + stride < n_tiles) {
           if (hh == 0) cp_async_wait_all();  // this thread's point of the next tile (phase 5)
-          live_n = stage_a1((it + 1) & 1, rD);
+          live_n = stage_a1((it + 1) & 1, tD);
         }
         hand_off(p);
         if (hh == 0) {
@@ -719,8 +728,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
             gq[2] = gx * pp_t.y - gy * pp_t.x;
           }
           if (a.detect) {
-            // rank of the pair among the tile's actives (the ballots of the four lane quarters)
-            // + the tile's staging base, posted by the detect warp
+            // rank of the pair among the tile's actives (the ballots of the four lane
+            // quarters) + the tile's staging base, posted by the detect warp
             wait_bar(&S.det_out[s], (uint32_t)it & 1u);
             const bool act = live && (f - a.delta <= a.tau);
             int rk = __popc(S.act[s][qd] & ((1u << lane) - 1u));
@@ -746,8 +755,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
           }
         }
       }
-      if (tr) tr[1] = clock64();
-    }
+      if constexpr (kTrace) if (trc) trc[1] = clock64();
+      seq += kSlots;
+    };
+    phase(std::integral_constant<int, 0>{});
+    phase(std::integral_constant<int, 1>{});
+    phase(std::integral_constant<int, 2>{});
+    phase(std::integral_constant<int, 3>{});
+    phase(std::integral_constant<int, 4>{});
+    phase(std::integral_constant<int, 5>{});
+    phase(std::integral_constant<int, 6>{});
+    phase(std::integral_constant<int, 7>{});
+    phase(std::integral_constant<int, 8>{});
+    phase(std::integral_constant<int, 9>{});
+    phase(std::integral_constant<int, 10>{});
+    phase(std::integral_constant<int, 11>{});
   }
   fence_before();
   __syncthreads();
@@ -758,7 +780,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
 template <bool F16>
 cudaError_t launch_tc_t(const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s) {
   const int smem = (int)sizeof(SmemTC);
-  auto kern = a.frame ? k_mlp_tc<F16, true> : k_mlp_tc<F16, false>;
+  auto kern = a.trace ? (a.frame ? k_mlp_tc<F16, true, true> : k_mlp_tc<F16, false, true>)
+                      : (a.frame ? k_mlp_tc<F16, true, false> : k_mlp_tc<F16, false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   // a partitioned detect knows its tile count on the device only: one CTA per SM
