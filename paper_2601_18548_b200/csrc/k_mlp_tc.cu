@@ -48,15 +48,15 @@ namespace {
 
 using namespace tc;
 
-// Waits of the epilogue / detect / MMA warps.  A plain try_wait returns after a short
-// system-defined time, so an idle warp re-polls (~9 instructions per poll) and takes issue
-// slots from the busy epilogue warps of its SM sub-partition; with a suspend-time hint the
-// warp sleeps until the phase completes (or the hint expires).
-DEVI void wait_bar(uint64_t *bar, uint32_t parity) { mbar_wait_hint<20000>(bar, parity); }
+// Waits of the epilogue / detect / MMA warps: plain try_wait polling.  (A suspend-time hint
+// compiles to a NANOSLEEP between polls, which spares the issue slots an idle warp's polls take
+// from the busy epilogue warps of its SM sub-partition, but its wake-up latency sits on the
+// per-slot chain: measured 105.4M vs 99.8M SM cycles per C5 launch, tools/_runab.sh.)
+DEVI void wait_bar(uint64_t *bar, uint32_t parity) { mbar_wait(bar, parity); }
 DEVI void wait_bar_addr(uint32_t addr, uint32_t parity) {
-  if (mbar_try_wait_hint(addr, parity, 20000)) return;
+  if (mbar_try_wait(addr, parity)) return;
   const long long t0 = clock64();
-  while (!mbar_try_wait_hint(addr, parity, 20000)) {
+  while (!mbar_try_wait(addr, parity)) {
     if (clock64() - t0 > (1ll << 34)) __trap();
   }
 }
@@ -265,52 +265,35 @@ DEVI void mma_loop(SmemTC &S, const QueryArgs &a, int64_t n_tiles, int64_t strid
                       ? a.trace + (size_t)SS * kTraceTiles * kTracePhases * 4
                       : nullptr;
   mbar_wait(&S.wbar, 0u);  // the resident weights have landed in shared memory
-  // every MMA warp takes part in every round until the last real phase of any slot (the slots
-  // run in lockstep: consecutive UMMA phases read the same weights, which measured faster than
-  // offsetting the slots so that their short tile-boundary phases fall in different rounds)
-  int64_t rounds = 0, mine = 0;
-#pragma unroll
-  for (int s2 = 0; s2 < kSlots; ++s2) {
-    const int64_t T0 = (int64_t)blockIdx.x * kSlots + s2;
-    const int64_t nt = T0 < n_tiles ? (n_tiles - T0 + stride - 1) / stride : 0;
-    if (s2 == SS) mine = nt * kPhases;
-    const int64_t r = nt > 0 ? nt * kPhases + 1 : 0;
-    rounds = r > rounds ? r : rounds;
-  }
-  int p = 0, it = 0;
-#pragma unroll 1
-  for (int64_t j = 0; j < rounds; ++j, seq += kSlots) {
-    const int64_t jr = j;                       // the slot's phase number
-    const bool real = jr >= 0 && jr < mine;
+  int it = 0;
+  for (int64_t base = (int64_t)blockIdx.x * kSlots; base < n_tiles; base += stride, ++it) {
+    const bool real = base + SS < n_tiles;
     // the slot's last tile hands off once more after its g0 readout: the phase after it (a
     // passed turn) must not let the next phases overwrite the region g0 is read from
-    const bool after_last = mine > 0 && jr == mine;
-    long long *t = (tr && real && it < kTraceTiles) ? tr + ((size_t)it * kTracePhases + p) * 4 : nullptr;
-    if (real || after_last) {
-      wait_bar(&S.epi_done[SS], ph);
-      ph ^= 1u;
-    }
-    if (t) t[0] = clock64();
-    // the turn (an mbarrier, so a waiting MMA warp sleeps instead of taking issue slots from
-    // the epilogue warps of its SM sub-partition)
-    auto wait_turn = [&]() {
-      wait_bar(&S.turn[SS], (seq / kSlots) & 1u);
-      if (t) t[1] = clock64();
-      fence_after();
-    };
-    if (real) issue_phase<F16>(p, 128u * (seq & 3u), 128u * ((seq + 1u) & 3u), sw, sw1t, sb1, sbx, sbz, wait_turn);
-    else wait_turn();
-    fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&S.turn[(SS + 1) % kSlots]);  // the next slot may issue now
-    if (real) {
-      commit_elect(&S.mma_done[SS]);
-      if (++p == kPhases) {
-        p = 0;
-        ++it;
+    const bool last_was_real = it > 0 && base - stride + SS < n_tiles;
+#pragma unroll 1
+    for (int p = 0; p < kPhases; ++p, seq += kSlots) {
+      long long *t = (tr && it < kTraceTiles) ? tr + ((size_t)it * kTracePhases + p) * 4 : nullptr;
+      if (real || (p == 0 && last_was_real)) {
+        wait_bar(&S.epi_done[SS], ph);
+        ph ^= 1u;
       }
+      if (t) t[0] = clock64();
+      // the turn (an mbarrier, so a waiting MMA warp sleeps instead of taking issue slots
+      // from the epilogue warps of its SM sub-partition)
+      auto wait_turn = [&]() {
+        wait_bar(&S.turn[SS], (seq / kSlots) & 1u);
+        if (t) t[1] = clock64();
+        fence_after();
+      };
+      if (real) issue_phase<F16>(p, 128u * (seq & 3u), 128u * ((seq + 1u) & 3u), sw, sw1t, sb1, sbx, sbz, wait_turn);
+      else wait_turn();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.turn[(SS + 1) % kSlots]);  // the next slot may issue now
+      if (real) commit_elect(&S.mma_done[SS]);
+      if (t) t[2] = clock64();
     }
-    if (t) t[2] = clock64();
   }
 }
 
@@ -442,7 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   const int qd = warp & 3;          // TMEM lane quarter of this warp (warp % 4)
   const int row = qd * 32 + lane;   // pair within the tile = TMEM lane
   const uint32_t tL = tbase + ((uint32_t)(qd * 32) << 16) + 32u * hh;  // region 0, this lane quarter, column half
-  uint32_t seq = (uint32_t)s;  // CTA phase index of the slot's next MMA phase
+  uint32_t seq = (uint32_t)s;       // CTA phase index of the slot's next MMA phase
   auto region = [&](uint32_t k) { return tL + 128u * (k & 3u); };
   uint32_t *mk = &S.mask[s][0][0][hh * 128 + row];  // + (layer * 2 + word) * kEpiPerSlot
   const uint32_t bar_mma = smem_u32(&S.mma_done[s]), bar_epi = smem_u32(&S.epi_done[s]);
@@ -473,24 +456,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   // issued by the column-half-0 threads, which alone read it
   // (the pair's local slot goes to S.slotn[s][par][row], read back at phases 5, 6 and 11 and
   // by stage_a1: no per-tile index arithmetic on the critical path)
-  // (dense map) the slot's next tile as (step, tile of the step), advanced by the stride every
-  // tile instead of divided out of the tile index
-  const int tpw = a.tiles_per_wp;
-  const int64_t T0 = (int64_t)blockIdx.x * kSlots + s;
-  int nx_w = a.part.tile_wp ? 0 : (int)((T0 + stride) / tpw), nx_r = a.part.tile_wp ? 0 : (int)((T0 + stride) % tpw);
-  const int st_w = a.part.tile_wp ? 0 : (int)(stride / tpw), st_r = a.part.tile_wp ? 0 : (int)(stride % tpw);
   auto prefetch_pt = [&](int64_t TT, int par) {
     int wn = 0;
     int64_t sl = 0;
     bool ok = false;
-    if (TT < n_tiles) {
-      if (a.part.tile_wp) {
-        tile_pair(a, TT, row, wn, sl, ok);
-      } else {
-        sl = (int64_t)nx_r * kTile + row;
-        ok = sl < lb;
-      }
-    }
+    if (TT < n_tiles) tile_pair(a, TT, row, wn, sl, ok);
     S.slotn[s][par][row] = ok ? (uint32_t)sl : ~0u;
     cp_async16(&S.ptn[s][row], ok ? (const void *)(a.scene.pts + sl) : (const void *)a.scene.pts, ok ? 16u : 0u);
     cp_async_commit();
@@ -513,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         __syncwarp();
         wn = S.wnx[s];
       } else {
-        wn = nx_w;
+        wn = (int)(TT / a.tiles_per_wp);
       }
       if (lane < kNdof) cp_async4(&S.qn[s][par][lane], a.q + (int64_t)wn * kNdof + lane);
       cp_async_commit();
@@ -573,13 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   bool live_n = false;
   if ((int64_t)blockIdx.x * kSlots + s < n_tiles) {
     if (hh == 0) {
-      int wn;
-      int64_t sl;
-      bool ok;
-      tile_pair(a, T0, row, wn, sl, ok);
-      S.slotn[s][0][row] = ok ? (uint32_t)sl : ~0u;
-      cp_async16(&S.ptn[s][row], ok ? (const void *)(a.scene.pts + sl) : (const void *)a.scene.pts, ok ? 16u : 0u);
-      cp_async_commit();
+      prefetch_pt((int64_t)blockIdx.x * kSlots + s, 0);
       cp_async_wait_all();
     }
     live_n = stage_a1(0, region(seq + 1u));  // phase 0's A region
@@ -667,8 +631,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         if (hh == 0) layer6(std::integral_constant<int, 0>{});
         else layer6(std::integral_constant<int, 32>{});
         hand_off(p);
-        // the partial sums of f = w7 . h6 + b7 (combined at phase 6, off this phase's chain)
+        // f = w7 . h6 + b7 (fp32, no output activation: signed value); both
+        // column halves form it from the two partial sums (half 0 writes the records, half 1
+        // thresholds)
         S.fpart[s][hh][row] = (fa[0] + fa[1]) + (fa[2] + fa[3]);
+        if (hh == 0 && qd == 0) cp_async_wait_all();  // S.qn of the next tile (stage_q)
+        named_bar_sync(1 + s, kEpiPerSlot);
+        f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
+        if (hh == 1) {
+          const uint32_t sl = S.slotn[s][it & 1][row];
+          live = (sl >> 31) == 0u;
+          if (!a.detect) {
+            const int w = S.wtile[s][it & 1];
+            const int64_t slot = sl & 0x7fffffffu;
+            if (slot < lb) a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
+          }
+        } else {
+          prefetch_pt(T + stride, (it + 1) & 1);  // the next tile's point, needed at phase 11
+        }
       } else if constexpr (p < 11) {
         // ---- backward: g_{l-1} = D; e_{l-1} = g (.) 1[z_{l-1} > 0] -> A (in place) ----
         constexpr int mi = 10 - p;
@@ -693,23 +673,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         }
         hand_off(p);
         if constexpr (p == 6) {
-          // f = w7 . h6 + b7 (fp32, no output activation: signed value); both
-          // column halves form it from the two partial sums (half 0 writes the records, half
-          // 1 thresholds)
-          if (hh == 0 && qd == 0) cp_async_wait_all();  // S.qn of the next tile (stage_q)
-          named_bar_sync(1 + s, kEpiPerSlot);
-          f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
-          if (hh == 1) {
-            const uint32_t sl = S.slotn[s][it & 1][row];
-            live = (sl >> 31) == 0u;
-            if (!a.detect) {
-              const int w = S.wtile[s][it & 1];
-              const int64_t slot = sl & 0x7fffffffu;
-              if (slot < lb) a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
-            }
-          } else {
-            prefetch_pt(T + stride, (it + 1) & 1);  // the next tile's point, needed at phase 11
-          }
           if (hh == 1 && a.detect) {
             // A6/A7 (overlaps the tensor core): threshold and the warp's min key -> the detect warp
             const int64_t slot = S.slotn[s][it & 1][row] & 0x7fffffffu;  // (live implies a real pair)
@@ -742,7 +705,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
           ld16(tD, r);
           wait_ld();
         }
-        [[maybe_unused]] const float2 pp_t = pp;  // (SE(2)) p'_xy of this tile; stage_a1 overwrites pp
+        const float2 pp_t = pp;  // (SE(2)) p'_xy of this tile; stage_a1 overwrites pp
         if (T + stride < n_tiles) {
           if (hh == 0) cp_async_wait_all();  // this thread's point of the next tile (phase 5)
           live_n = stage_a1((it + 1) & 1, tD);
@@ -807,12 +770,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     phase(std::integral_constant<int, 9>{});
     phase(std::integral_constant<int, 10>{});
     phase(std::integral_constant<int, 11>{});
-    nx_r += st_r;
-    nx_w += st_w;
-    if (nx_r >= tpw) {
-      nx_r -= tpw;
-      ++nx_w;
-    }
   }
   fence_before();
   __syncthreads();
