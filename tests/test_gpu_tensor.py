@@ -15,7 +15,8 @@ Gates (R17, R28), at the paper's gradient scale (R11: median ||grad_q 
       (R28, EMU-only numbers in DESIGN.md).
 Where the operand type alone exceeds (2) (bf16 at this scale: EMU-only max |df| ~ 8e-2),
 the GPU is held to the EMU's own error + 5e-3 and the shortfall is reported; the bf16
-contract is met by the split GCDF_BF16X3 path (tests/test_gpu_fp16x3.py).
+contract (2e-2 / 5e-2) is met by the fp16 default on every gate; the fp32-accurate split path is
+GCDF_FP16X3 (tests/test_gpu_fp16x3.py).
 """
 import os
 
