@@ -55,6 +55,8 @@ def parse():
                     help="also time the range-partitioned detect (NEXT-1) at this radius; 0 = skip")
     ap.add_argument("--no-kernels", dest="kernels", action="store_false",
                     help="skip the standalone K1 / K3 HBM measurements of the default run")
+    ap.add_argument("--no-workloads", dest="workloads", action="store_false",
+                    help="skip the C2 / C3 / C4 measurements of the default run")
     ap.add_argument("--no-variants", dest="variants", action="store_false",
                     help="skip the softplus / H = 256 variant measurements (NEXT-4) of the default run")
     ap.add_argument("--latency-calls", type=int, default=50,
@@ -560,6 +562,62 @@ def main():
         del vals, grs, outs_k
         torch.cuda.empty_cache()
 
+    # the other configurations of BASELINE.json on the same GPU (default run only): C4 is the
+    # batched-replanning workload (128 trajectories x 64 waypoints, 20k points, 200 + 200 scene
+    # updates per step), C2 / C3 the single-trajectory latency cases.  Per config: device time
+    # per SCO step (scene update + fused detect, L2 flushed before each) and the wall-time
+    # latency of one detect call (q on device -> count on host) replayed as a CUDA graph.
+    workloads = None
+    if world == 1 and a.workloads and a.config == "C5" and prec == "fp16" and not hidden and a.activation == "relu":
+        workloads = {}
+        for wname in ("C2", "C3", "C4"):
+            wc = synth.get_config(wname)
+            wpts, wboxes = synth.make_scene_points(wc)
+            wq = torch.from_numpy(synth.make_waypoints(wc)).to(dev)
+            wn = wc.B * wc.N
+            wma = int(min(wc.pairs + 1024, max(4 * wc.pairs // 100, 1 << 16)))
+            wctx = Context(local, precision=FP16, scene_capacity=wc.M + slack, max_waypoints=wn, max_active=wma)
+            wctx.load_weights(synth.weights_path(wc.H))
+            wctx.update_scene(wpts)
+            wtau = synth.load_tau(wname)
+            wouts = wctx.alloc_detect_outputs(wn, wma)
+            wgen = np.random.default_rng([wc.seed, 11])
+            wk = 5
+            wch = int(max(1, min(200, wc.M // (2 * (wk + 2)))))
+            wadd = [synth.inputs.scene_update_batch(wgen, wboxes, np.zeros((0, 3)), n_add=wch)[0] for _ in range(wk + 2)]
+            wrem = list(wgen.choice(wc.M, size=(wk + 2, wch), replace=False))
+            for i in range(2):
+                wctx.update_scene(wadd[i], wrem[i])
+                wctx.detect_active_set(wq, delta, wtau, outputs=wouts, sync_count=False)
+            torch.cuda.synchronize()
+            wev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(wk)]
+            wpairs = 0
+            for i, (e0, e1) in enumerate(wev):
+                flush.zero_()
+                e0.record()
+                wctx.update_scene(wadd[2 + i], wrem[2 + i])
+                wo = wctx.detect_active_set(wq, delta, wtau, outputs=wouts, sync_count=False)
+                e1.record()
+                wpairs += wctx.scene_info()["n_live"] * wn
+            torch.cuda.synchronize()
+            wms = sum(e0.elapsed_time(e1) for e0, e1 in wev) / wk
+            g = wctx.detect_graph(wq, delta, wtau, capacity=wma)
+            for _ in range(5):
+                g.launch()
+            ts = []
+            for _ in range(20):
+                t0 = time.perf_counter()
+                g.launch()
+                ts.append(time.perf_counter() - t0)
+            g.close()
+            workloads[wname] = {"desc": wc.desc, "ms_per_step": wms, "value": wpairs / wk / (wms / 1e3),
+                                "unit": "queries/s", "active_per_step": int(wo["count"].item()),
+                                "scene_update_per_step": f"{wch} removes + {wch} adds",
+                                "detect_latency_graph_p50_ms": float(np.median(ts) * 1e3)}
+            wctx.close()
+            del wouts
+            torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         cpu = cpu_oracle_rate(cfg, pts, q_np, sample_pts=65536 if cfg.H <= 128 else 16384, single_thread=True,
@@ -579,6 +637,7 @@ def main():
             "partitioned": part,
             "variants": variants,
             "kernels": kernels,
+            "workloads": workloads,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_pairs / e2e_s, "unit": "queries/s", "h2d_bytes_per_step": h2d // e2e_steps,
                     "d2h_bytes_per_step": d2h // e2e_steps, "steps": e2e_steps},
