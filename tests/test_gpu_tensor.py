@@ -321,3 +321,35 @@ def test_c3_dense_scene_full_rows():
         assert int(warg[k]) in set(ids[full[k] <= full[k].min() + 2 * BF16_VAL_ATOL].tolist())
     frac = n / (len(pts) * Q.shape[0])
     print(f"\nC3: {n} active ({frac:.4%})")
+
+
+@pytest.mark.parametrize("n_wp,n_pts", [(1, 100), (1, 128), (1, 300), (2, 200), (3, 129), (4, 257), (5, 700),
+                                        (7, 1000)])
+def test_tile_count_edge_cases(c2, n_wp, n_pts):
+    """Tile counts below / around the three tiles a CTA keeps in flight (K2b): one tile, a
+    ragged last tile, CTAs whose second / third slot has no tile (passed turns), and the
+    last-round tail.  Dense values and gradients vs the EMU oracle (same rounding points),
+    and the fused detect bit-identical to dense query + standalone compaction."""
+    cfg, pts, q, m, exact, emu = c2
+    P = pts[:n_pts]
+    qq = q[:, :n_wp]
+    ctx = _ctx(cfg, "fp16")
+    ctx.update_scene(P)
+    qt = torch.from_numpy(qq)
+    v, g = ctx.query_values_grads(qt)
+    torch.cuda.synchronize()
+    vn, gn = v.cpu().numpy()[:, :n_pts], g.cpu().numpy()[:, :n_pts]
+    em = m.eval(P, qq.reshape(-1, 9), flags=oracle.EMU_FP16)
+    # gate 1 of stats_and_gates (fp16): fp32-noise median, rounding-boundary / kink flips in the tail
+    dv = np.abs(vn - em["f"])
+    assert np.median(dv) <= 1e-6 and dv.max() <= 1e-2, (np.median(dv), dv.max())
+    dg = np.linalg.norm(gn - em["g"], axis=-1) / np.maximum(1.0, np.linalg.norm(em["g"], axis=-1))
+    assert np.percentile(dg, 99) <= 1e-2, np.percentile(dg, 99)
+    assert np.all(np.isinf(v.cpu().numpy()[:, n_pts:]))
+    # threshold at the sample's own median so that every case has actives and inactives
+    tau = float(np.median(em["f"])) - DELTA
+    a = records_np(ctx.compact_dense(v, g, DELTA, tau))
+    b = records_np(ctx.detect_active_set(qt, DELTA, tau))
+    assert len(b["wp"]) > 0
+    for k in ("wp", "pt", "value", "grad"):
+        assert np.array_equal(a[k], b[k]), k
