@@ -1,6 +1,6 @@
 """bench.py -- GCDF value+grad queries/s with active-set detection on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--precision fp16|bf16|fp32|fp16x3]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--precision fp16|bf16|fp32|fp16x3|bf16x3]
     python bench.py --impl reference ...      # the float64 CPU oracle on host cores
 
 One step = one SCO iteration of the hot path (all SURVEY §8(a) rows): an incremental
@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C5")
-    ap.add_argument("--precision", default="auto", choices=["auto", "fp16", "bf16", "fp32", "fp16x3"])
+    ap.add_argument("--precision", default="auto", choices=["auto", "fp16", "bf16", "fp32", "fp16x3", "bf16x3"])
     ap.add_argument("--hidden", type=int, default=None, choices=[128, 256],
                     help="hidden width override for the H = 128 configs (256: NEXT-4 variant, DESIGN.md R27)")
     ap.add_argument("--activation", default="relu", choices=["relu", "softplus"],
@@ -209,7 +209,7 @@ def main():
         sys.exit("bench.py: --same-device (dry run) needs --comm host (one GPU cannot host two NCCL ranks)")
     import torch
     import torch.distributed as dist
-    from paper_2601_18548_b200 import BF16, FP16, FP16X3, FP32, Context
+    from paper_2601_18548_b200 import BF16, BF16X3, FP16, FP16X3, FP32, Context
     from paper_2601_18548_b200.gcdf import load_library
 
     rank = int(os.environ.get("RANK", "0"))
@@ -239,7 +239,7 @@ def main():
     n_wp = cfg.B * cfg.N
     slack = 4096
     max_active = int(min(cfg.pairs // world + 1024, max(4 * cfg.pairs // 100 // world, 1 << 16)))
-    ctx = Context(local, precision={"fp16": FP16, "bf16": BF16, "fp32": FP32, "fp16x3": FP16X3}[prec], scene_capacity=cfg.M + slack,
+    ctx = Context(local, precision={"fp16": FP16, "bf16": BF16, "fp32": FP32, "fp16x3": FP16X3, "bf16x3": BF16X3}[prec], scene_capacity=cfg.M + slack,
                   max_waypoints=n_wp, max_active=max_active, rank=rank, world=world,
                   max_candidates=(cfg.pairs // world + 4096) if a.partition_radius > 0 else 0)
     ctx.load_weights(synth.weights_path(cfg.H, act=act))
@@ -344,10 +344,10 @@ def main():
     # roofline of the dominant kernel (fused MLP): algorithmic flops per launch / live duration
     peaks, peak_src = measured_peaks()
     local_pairs = n_wp * (n_live_total / a.steps) / world
-    if prec in ("bf16", "fp16", "fp16x3"):
+    if prec in ("bf16", "fp16", "fp16x3", "bf16x3"):
         # algorithmic flops: the method's ten H x H GEMMs per pair; fp16x3 (K2c)
         # executes each of them 3 times (the split, R25): reported as a side field
-        n_terms = 3 if prec == "fp16x3" else 1
+        n_terms = 3 if prec in ("fp16x3", "bf16x3") else 1
         flops = FLOPS_PAIR_TENSOR[cfg.H] * local_pairs
         achieved = flops / (mlp_ms / mlp_n / 1e3) / 1e12
         # peak: the measured BURST dense figure (the higher, stricter one) whatever the length of
@@ -478,7 +478,7 @@ def main():
     if world == 1 and a.variants and a.activation == "relu" and not hidden and prec == "fp16":
         variants = {}
         for name, act_v, h_v, prec_v in (("softplus", 2, None, FP16), ("hidden256", 1, 256, FP16),
-                                         ("fp16x3", 1, None, FP16X3)):
+                                         ("fp16x3", 1, None, FP16X3), ("bf16x3", 1, None, BF16X3)):
             cfg_v = dataclasses.replace(cfg, H=h_v) if h_v else cfg
             ctx_v = Context(local, precision=prec_v, scene_capacity=cfg.M + slack, max_waypoints=n_wp,
                             max_active=max_active)
@@ -504,15 +504,17 @@ def main():
             pairs_v = ctx_v.scene_info()["n_live"] * n_wp
             ach = FLOPS_PAIR_TENSOR[cfg_v.H] * pairs_v / (k_ms / k_n / 1e3) / 1e12
             pk = float(peaks.get("bf16_tflops"))
-            variants[name] = {"kernel": "k_mlp_tc_sp" if act_v == 2 else "k_mlp_tc3" if prec_v == FP16X3
+            split = prec_v in (FP16X3, BF16X3)
+            variants[name] = {"kernel": "k_mlp_tc_sp" if act_v == 2 else "k_mlp_tc3" if split
                               else "k_mlp_tc_wide", "hidden": cfg_v.H,
                               "activation": "softplus" if act_v == 2 else "relu", "ms_per_step": ms_v,
-                              "precision": "fp16x3 (fp32-accurate split, R25)" if prec_v == FP16X3 else "fp16",
+                              "precision": ("fp16x3 (fp32-accurate split, R25)" if prec_v == FP16X3 else
+                                            "bf16x3 (3-term split bf16, R29)" if prec_v == BF16X3 else "fp16"),
                               "value": pairs_v / (ms_v / 1e3), "unit": "queries/s", "tau": tau_v,
                               "active_per_step": int(ov["count"].item()),
                               "roofline": {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
                                            "frac": ach / pk, "flops_per_pair": FLOPS_PAIR_TENSOR[cfg_v.H]}}
-            if prec_v == FP16X3:
+            if split:
                 variants[name]["roofline"].update(executed_flops_per_pair=3 * FLOPS_PAIR_TENSOR[cfg_v.H],
                                                   executed_frac=3 * ach / pk)
             ctx_v.close()

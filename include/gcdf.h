@@ -64,9 +64,13 @@ enum gcdf_precision {
   GCDF_FP16 = 2, /* tcgen05 tensor-core path, fp16 operands, fp32 accumulate: same tensor peak as
                     bf16 with 3 more significand bits; meets the north-star tensor-path tolerance
                     (R17, §5); the default */
-  GCDF_FP16X3 = 3 /* fp32-accurate tcgen05 path (NEXT-4): every hidden GEMM on 3-term split fp16
+  GCDF_FP16X3 = 3, /* fp32-accurate tcgen05 path (NEXT-4): every hidden GEMM on 3-term split fp16
                     operands (a_hi w_hi + a_lo w_hi + a_hi w_lo), weights streamed from L2; meets
                     the fp32 tolerance of GCDF_FP32 (R25, §5 "K2c"); needs H = 128 */
+  GCDF_BF16X3 = 4  /* the same 3-term split on bf16 operands (K2c with bf16 UMMAs): every product
+                    to ~2^-16 relative, so the bf16 tensor path meets the north-star tensor
+                    tolerance (2e-2 on f, 5e-2 on the gradient norm) that single-term bf16 misses
+                    at the paper's gradient scale (R28, R29); needs H = 128 */
 };
 
 enum gcdf_tgrad {

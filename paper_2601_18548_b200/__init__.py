@@ -4,8 +4,8 @@ The product is libgcdf.so (C ABI, include/gcdf.h) built from csrc/ for sm_100a; 
 package holds it and a thin ctypes binding (gcdf.py).  Multi-GPU gather helpers live in
 dist.py.  Nothing here computes any step of the hot path on the CPU.
 """
-from .gcdf import (BF16, FP16, FP16X3, FP32, FRAME_SE2, FRAME_TRANSLATE, TGRAD_CHAINRULE, TGRAD_QCHANNEL, Context, GcdfError, load_library,
+from .gcdf import (BF16, BF16X3, FP16, FP16X3, FP32, FRAME_SE2, FRAME_TRANSLATE, TGRAD_CHAINRULE, TGRAD_QCHANNEL, Context, GcdfError, load_library,
                    records_to_dict)
 
-__all__ = ["BF16", "FP16", "FP16X3", "FP32", "FRAME_SE2", "FRAME_TRANSLATE", "TGRAD_CHAINRULE", "TGRAD_QCHANNEL", "Context", "GcdfError", "load_library",
+__all__ = ["BF16", "BF16X3", "FP16", "FP16X3", "FP32", "FRAME_SE2", "FRAME_TRANSLATE", "TGRAD_CHAINRULE", "TGRAD_QCHANNEL", "Context", "GcdfError", "load_library",
            "records_to_dict"]

@@ -204,7 +204,8 @@ uint16_t to_f16_rne(float f);
 WeightsBF16 bf16_view(const gcdf_ctx *c) {
   WeightsF32 f = f32_view(c);
   WeightsBF16 w{};
-  const int64_t wo = c->opt.precision == GCDF_BF16 ? c->L.wbf16 : c->L.wf16;
+  const bool bf = c->opt.precision == GCDF_BF16 || c->opt.precision == GCDF_BF16X3;
+  const int64_t wo = bf ? c->L.wbf16 : c->L.wf16;
   w.w_sw128 = c->ws + wo;
   w.w1t_sw128 = c->ws + wo + 5 * kBfMat;
   w.b1_nosw = c->ws + wo + 5 * kBfMat + kBfW1t;
@@ -219,7 +220,7 @@ WeightsBF16 bf16_view(const gcdf_ctx *c) {
   w.w3_sw128 = c->ws + c->L.wf16x3;
   w.w1t3_sw128 = c->ws + c->L.wf16x3 + 5 * 2 * kBfMat;
   if ((c->H == 128 || c->H == 256) && (int)c->w7host.size() == c->H) {
-    const bool f16 = c->opt.precision != GCDF_BF16;
+    const bool f16 = !bf;
     for (int i = 0; i < c->H; ++i) w.w7half_p[i] = 0.5f * c->w7host[i];
     for (int i = 0; i < c->H / 2; ++i) {
       const float a0 = c->w7host[2 * i], a1 = c->w7host[2 * i + 1];
@@ -389,7 +390,7 @@ int gcdf_create(int cuda_device, const gcdf_options *opt, gcdf_ctx **out) {
       o.max_waypoints > 65535 || o.max_active <= 0 ||
       o.max_active >= (1LL << 31) || o.world < 1 || o.rank < 0 || o.rank >= o.world ||
       (o.precision != GCDF_FP32 && o.precision != GCDF_BF16 && o.precision != GCDF_FP16 &&
-       o.precision != GCDF_FP16X3) ||
+       o.precision != GCDF_FP16X3 && o.precision != GCDF_BF16X3) ||
       (o.tgrad_mode != GCDF_TGRAD_CHAINRULE && o.tgrad_mode != GCDF_TGRAD_QCHANNEL) ||
       (o.frame != GCDF_FRAME_TRANSLATE && o.frame != GCDF_FRAME_SE2) ||
       (o.frame == GCDF_FRAME_SE2 && o.tgrad_mode == GCDF_TGRAD_QCHANNEL))  // R24: theta is not a channel in SE(2)
@@ -650,29 +651,31 @@ int gcdf_load_weights(gcdf_ctx *c, const char *path, void *stream) {
       }
     }
   }
-  // ---- GCDF_FP16X3 (K2c): fp16 hi/lo split of the f64 weights, [W_l hi | W_l lo] per layer ----
+  // ---- GCDF_FP16X3 / GCDF_BF16X3 (K2c): hi/lo split of the f64 weights in the context's
+  // 16-bit type, [W_l hi | W_l lo] per layer ----
   std::vector<uint16_t> x3((size_t)kX3Total / 2, 0);
+  const bool x3f16 = c->opt.precision != GCDF_BF16X3;
   if (H == 128) {
     std::vector<float> mh((size_t)H * H), ml((size_t)H * H);
     float hi, lo;
     for (int li = 0; li < 5; ++li) {
       for (size_t i = 0; i < mh.size(); ++i) {
-        split16(Wd[li + 1][i], true, hi, lo);
+        split16(Wd[li + 1][i], x3f16, hi, lo);
         mh[i] = hi;
         ml[i] = lo;
       }
-      pack_sw128(mh, H, H, x3.data() + (size_t)(2 * li) * kBfMat / 2, true);
-      pack_sw128(ml, H, H, x3.data() + (size_t)(2 * li + 1) * kBfMat / 2, true);
+      pack_sw128(mh, H, H, x3.data() + (size_t)(2 * li) * kBfMat / 2, x3f16);
+      pack_sw128(ml, H, H, x3.data() + (size_t)(2 * li + 1) * kBfMat / 2, x3f16);
     }
     std::vector<float> th((size_t)16 * H, 0.f), tl((size_t)16 * H, 0.f);  // W1^T [n][k]
     for (int n = 0; n < kNin; ++n)
       for (int k = 0; k < H; ++k) {
-        split16(Wd[0][(size_t)k * kNin + n], true, hi, lo);
+        split16(Wd[0][(size_t)k * kNin + n], x3f16, hi, lo);
         th[(size_t)n * H + k] = hi;
         tl[(size_t)n * H + k] = lo;
       }
-    pack_sw128(th, 16, H, x3.data() + (size_t)10 * kBfMat / 2, true);
-    pack_sw128(tl, 16, H, x3.data() + (size_t)(10 * kBfMat + kBfW1t) / 2, true);
+    pack_sw128(th, 16, H, x3.data() + (size_t)10 * kBfMat / 2, x3f16);
+    pack_sw128(tl, 16, H, x3.data() + (size_t)(10 * kBfMat + kBfW1t) / 2, x3f16);
   }
   // ---- H = 256 (K2w) ----
   std::vector<uint16_t> wide;
@@ -846,8 +849,8 @@ static cudaError_t run_mlp(gcdf_ctx *c, const QueryArgs &a, cudaStream_t s) {
   }
   cudaError_t e = c->opt.precision == GCDF_FP32
                       ? launch_mlp_simt(c->H, f32_view(c), a, c->num_sms, s)
-                      : c->opt.precision == GCDF_FP16X3
-                            ? launch_mlp_tc3(bf16_view(c), a, c->num_sms, s)
+                      : c->opt.precision == GCDF_FP16X3 || c->opt.precision == GCDF_BF16X3
+                            ? launch_mlp_tc3(c->opt.precision == GCDF_FP16X3, bf16_view(c), a, c->num_sms, s)
                         : c->H == kWideH ? launch_mlp_tc_wide(bf16_view(c), a, c->num_sms, s)
                         : a.act == 2 ? launch_mlp_tc_sp(bf16_view(c), a, c->num_sms, s)
                             : launch_mlp_tc(c->H, c->opt.precision == GCDF_FP16, bf16_view(c), a, c->num_sms, s);

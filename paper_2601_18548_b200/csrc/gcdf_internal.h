@@ -151,7 +151,7 @@ cudaError_t launch_mlp_tc(int H, bool f16, const WeightsBF16 &w, const QueryArgs
 cudaError_t launch_mlp_tc_wide(const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
 // softplus variant of the tensor-core path (fp16 operands, translation frame; R26)
 cudaError_t launch_mlp_tc_sp(const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
-cudaError_t launch_mlp_tc3(const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
+cudaError_t launch_mlp_tc3(bool f16, const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s);
 bool tc_compiled();
 cudaError_t launch_selftest_umma(int mode, const float *A, const float *B, float *D, cudaStream_t s);
 // standalone A6-A8 over dense values (two passes; writes the ordered output directly)

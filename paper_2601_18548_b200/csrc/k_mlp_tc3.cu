@@ -50,9 +50,10 @@ constexpr int kB1Bytes = 32 * H * 2;
 constexpr int kBextBytes = 16 * H * 2;
 constexpr int kOnesBytes = 16 * H * 2;
 constexpr uint32_t kColAhi = 128, kColAlo = 192;
-constexpr uint32_t kIdescFwd = idesc_f16kind(128, 128, false, true);
-constexpr uint32_t kIdescBwd = idesc_f16kind(128, 128, true, true);
-constexpr uint32_t kIdescFin = idesc_f16kind(128, 16, false, true);
+// F16: the 16-bit operand type of the split (GCDF_FP16X3: fp16; GCDF_BF16X3: bf16)
+template <bool F16> constexpr uint32_t kIdescFwd = idesc_f16kind(128, 128, false, F16);
+template <bool F16> constexpr uint32_t kIdescBwd = idesc_f16kind(128, 128, true, F16);
+template <bool F16> constexpr uint32_t kIdescFin = idesc_f16kind(128, 16, false, F16);
 
 struct __align__(1024) Smem3 {
   uint8_t ring[2][kLayerBytes];    // streamed W_l images [hi SW128 | lo SW128]
@@ -86,20 +87,28 @@ DEVI unsigned ord_f32(float f) {
   unsigned u = __float_as_uint(f);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
+template <bool F16>
 DEVI float round16(float x) {
-  const uint32_t p = pack_f16(x, 0.f);
-  float f;
-  asm("{\n\t.reg .b16 t;\n\tmov.b16 t, %1;\n\tcvt.f32.f16 %0, t;\n\t}" : "=f"(f) : "h"((unsigned short)(p & 0xffffu)));
-  return f;
+  const uint32_t p = pack2<F16>(x, 0.f);
+  if constexpr (F16) {
+    float f;
+    asm("{\n\t.reg .b16 t;\n\tmov.b16 t, %1;\n\tcvt.f32.f16 %0, t;\n\t}" : "=f"(f) : "h"((unsigned short)(p & 0xffffu)));
+    return f;
+  } else {
+    return __uint_as_float(p << 16);
+  }
 }
+template <bool F16>
 DEVI void split3(float x, float *o) {
-  const float hi = round16(x);
+  const float hi = round16<F16>(x);
   o[0] = hi;
   o[1] = x - hi;
   o[2] = hi;
 }
-// x_hi: x truncated to 11 significant bits (exact in fp16 in its normal range)
-DEVI float trunc11(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+// x_hi: x truncated to the type's significand (fp16: 11 significant bits, exact in fp16 in its
+// normal range; bf16: 8, exact in bf16 everywhere), same sign as x
+template <bool F16>
+DEVI float trunc_hi(float x) { return __uint_as_float(__float_as_uint(x) & (F16 ? 0xffffe000u : 0xffff0000u)); }
 DEVI uint32_t add7fff(uint32_t pk, uint32_t one) { return pk * one + 0x7fff7fffu; }
 DEVI uint32_t mask_group_f(uint32_t pk01, uint32_t pk23, int k, uint32_t one) {
   const uint32_t x = prmt(add7fff(pk01, one), add7fff(pk23, one), 0x7531u);
@@ -116,7 +125,7 @@ DEVI int layer_of(int r) {
 }
 DEVI bool starts_run(int t, int p) { return (p >= 2 && p <= 10 && p != 6) || (p == 1 && t == 0); }
 
-template <bool kSE2>
+template <bool F16, bool kSE2>
 __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, const QueryArgs a) {
   extern __shared__ uint8_t smem_raw[];
   Smem3 &S = *reinterpret_cast<Smem3 *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
@@ -137,13 +146,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
     copy16(S.b1, W.b1_nosw, kB1Bytes);
     copy16(S.bext, W.bext_nosw, 5 * kBextBytes);
     for (int i = tid; i < kOnesBytes / 4; i += kThreads)  // element (row, k) at row*16 + (k/8)*2048 + (k%8)*2
-      reinterpret_cast<uint32_t *>(S.ones)[i] = (i % 4 == 0 && i < H * 4) ? pack_f16(1.f, 1.f) : 0u;
+      reinterpret_cast<uint32_t *>(S.ones)[i] = (i % 4 == 0 && i < H * 4) ? pack2<F16>(1.f, 1.f) : 0u;
     for (int i = tid; i < H; i += kThreads) S.w7half[i] = 0.5f * __ldg(W.w7 + i);
     for (int i = tid; i < H / 2; i += kThreads) {
       const float x0 = __ldg(W.w7 + 2 * i), x1 = __ldg(W.w7 + 2 * i + 1);
-      const float h0 = trunc11(x0), h1 = trunc11(x1);
-      S.w7hi[i] = pack_f16(h0, h1);
-      S.w7lo[i] = pack_f16(x0 - h0, x1 - h1);
+      const float h0 = trunc_hi<F16>(x0), h1 = trunc_hi<F16>(x1);
+      S.w7hi[i] = pack2<F16>(h0, h1);
+      S.w7lo[i] = pack2<F16>(x0 - h0, x1 - h1);
     }
     if (tid == 0) S.one = 1u;
   }
@@ -223,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
         if (p == 0) {  // layer 1: K = 32 split operands in A_hi (bias included)
 #pragma unroll
           for (int k = 0; k < 2; ++k)
-            mma_ts_elect(d, ahi + 8u * k, sdesc_nosw(sb1 + k * 2 * 2048, 2048, 128), kIdescFwd, k > 0);
+            mma_ts_elect(d, ahi + 8u * k, sdesc_nosw(sb1 + k * 2 * 2048, 2048, 128), kIdescFwd<F16>, k > 0);
         } else if (p < 11) {
           const int r = run_of(t, p);
           if (producer && starts_run(t, p) && r >= 1 && (r + 1 <= 8 * t + 8 || next_tile)) load_run(r + 1);
@@ -235,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
             return fwd ? sdesc_sw128(wb + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024)
                        : sdesc_sw128(wb + k * 2048, 16384, 1024);
           };
-          const uint32_t id = fwd ? kIdescFwd : kIdescBwd;
+          const uint32_t id = fwd ? kIdescFwd<F16> : kIdescBwd<F16>;
           mbar_wait(&S.ring_full[b][0], par);
 #pragma unroll
           for (int k = 0; k < 8; ++k) mma_ts_elect(d, ahi + 8u * k, bdesc(whi, k), id, k > 0);
@@ -244,18 +253,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
           mbar_wait(&S.ring_full[b][1], par);
 #pragma unroll
           for (int k = 0; k < 8; ++k) mma_ts_elect(d, ahi + 8u * k, bdesc(wlo, k), id, 1u);
-          if (fwd) mma_ss_elect(d, ones_desc, sdesc_nosw(sbx + (uint32_t)(p - 1) * kBextBytes, 2048, 128), kIdescFwd, 1u);
+          if (fwd) mma_ss_elect(d, ones_desc, sdesc_nosw(sbx + (uint32_t)(p - 1) * kBextBytes, 2048, 128), kIdescFwd<F16>, 1u);
         } else {  // g0 = e1 W1 (N = 16)
           const uint32_t hi1 = sw1t, lo1 = sw1t + kW1tBytes;
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            mma_ts_elect(d, ahi + 8u * k, sdesc_sw128(hi1 + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin, k > 0);
+            mma_ts_elect(d, ahi + 8u * k, sdesc_sw128(hi1 + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin<F16>, k > 0);
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            mma_ts_elect(d, alo + 8u * k, sdesc_sw128(hi1 + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin, 1u);
+            mma_ts_elect(d, alo + 8u * k, sdesc_sw128(hi1 + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin<F16>, 1u);
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            mma_ts_elect(d, ahi + 8u * k, sdesc_sw128(lo1 + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin, 1u);
+            mma_ts_elect(d, ahi + 8u * k, sdesc_sw128(lo1 + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin<F16>, 1u);
         }
         if (two) *turn = seq + 1;
         commit_elect(&S.mma_done[ss]);
@@ -331,25 +340,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
         th = 0.f;
         S.pprime[s][par][row] = make_float2(dx, dy);
       }
-      split3(dx, v);
-      split3(dy, v + 3);
-      split3(pt.z, v + 6);
-      split3(th, v + 9);
-      split3(qw[3], v + 12);
-      v[15] = round16(qw[4]);
+      split3<F16>(dx, v);
+      split3<F16>(dy, v + 3);
+      split3<F16>(pt.z, v + 6);
+      split3<F16>(th, v + 9);
+      split3<F16>(qw[3], v + 12);
+      v[15] = round16<F16>(qw[4]);
     } else {
       const float j2 = qw[4];
-      const float j2h = round16(j2);
+      const float j2h = round16<F16>(j2);
       v[0] = j2 - j2h;
       v[1] = j2h;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) split3(qw[5 + i], v + 2 + 3 * i);
+      for (int i = 0; i < 4; ++i) split3<F16>(qw[5 + i], v + 2 + 3 * i);
       v[14] = 1.f;
       v[15] = 1.f;
     }
     uint32_t a1[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) a1[i] = pack_f16(v[2 * i], v[2 * i + 1]);
+    for (int i = 0; i < 8; ++i) a1[i] = pack2<F16>(v[2 * i], v[2 * i + 1]);
     st8(tS + kColAhi + 8u * hh, a1);
     hand_off();
     return lv;
@@ -389,9 +398,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
 #pragma unroll
           for (int j = 0; j < 16; j += 2) {
             const float z0 = __uint_as_float(rr[j]), z1 = __uint_as_float(rr[j + 1]);
-            const float h0 = trunc11(z0), h1 = trunc11(z1);  // same sign as z: ReLU per part
-            ph_[j >> 1] = pack_f16_relu(h0, h1);
-            pl_[j >> 1] = pack_f16_relu(z0 - h0, z1 - h1);
+            const float h0 = trunc_hi<F16>(z0), h1 = trunc_hi<F16>(z1);  // same sign as z: ReLU per part
+            ph_[j >> 1] = pack2_relu<F16>(h0, h1);
+            pl_[j >> 1] = pack2_relu<F16>(z0 - h0, z1 - h1);
           }
 #pragma unroll
           for (int j = 0; j < 8; j += 2) m |= mask_group_f(ph_[j], ph_[j + 1], ((c & 1) * 16 + 2 * j) >> 2, one);
@@ -424,8 +433,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
             const uint2 wl = *reinterpret_cast<const uint2 *>(S.w7lo + (u0 + cb + j) / 2);
             const float z0 = __uint_as_float(rr[j]), z1 = __uint_as_float(rr[j + 1]);
             const float z2 = __uint_as_float(rr[j + 2]), z3 = __uint_as_float(rr[j + 3]);
-            const uint32_t m01 = nz_halves(pack_f16_relu(z0, z1), one);
-            const uint32_t m23 = nz_halves(pack_f16_relu(z2, z3), one);
+            const uint32_t m01 = nz_halves(pack2_relu<F16>(z0, z1), one);
+            const uint32_t m23 = nz_halves(pack2_relu<F16>(z2, z3), one);
             pkh[j >> 1] = wh.x & m01;
             pkh[(j >> 1) + 1] = wh.y & m23;
             pkl[j >> 1] = wl.x & m01;
@@ -469,11 +478,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
             mask_expand(mw[c >> 1], ((c & 1) * 16 + j) >> 2, lo, hi);
             const float g0 = __uint_as_float(rr[j]), g1 = __uint_as_float(rr[j + 1]);
             const float g2 = __uint_as_float(rr[j + 2]), g3 = __uint_as_float(rr[j + 3]);
-            const float h0 = trunc11(g0), h1 = trunc11(g1), h2 = trunc11(g2), h3 = trunc11(g3);
-            pkh[j >> 1] = pack_f16(h0, h1) & lo;
-            pkh[(j >> 1) + 1] = pack_f16(h2, h3) & hi;
-            pkl[j >> 1] = pack_f16(g0 - h0, g1 - h1) & lo;
-            pkl[(j >> 1) + 1] = pack_f16(g2 - h2, g3 - h3) & hi;
+            const float h0 = trunc_hi<F16>(g0), h1 = trunc_hi<F16>(g1), h2 = trunc_hi<F16>(g2), h3 = trunc_hi<F16>(g3);
+            pkh[j >> 1] = pack2<F16>(h0, h1) & lo;
+            pkh[(j >> 1) + 1] = pack2<F16>(h2, h3) & hi;
+            pkl[j >> 1] = pack2<F16>(g0 - h0, g1 - h1) & lo;
+            pkl[(j >> 1) + 1] = pack2<F16>(g2 - h2, g3 - h3) & hi;
           }
           st8(tAh + 8 * c, pkh);
           st8(tAl + 8 * c, pkl);
@@ -587,23 +596,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
   if (warp == 0) tmem_dealloc(tbase, 512);
 }
 
-template <bool kSE2>
+template <bool F16, bool kSE2>
 cudaError_t launch_t(const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s) {
   const int smem = (int)sizeof(Smem3) + 1024;
-  cudaError_t e = cudaFuncSetAttribute(k_mlp_tc3<kSE2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(k_mlp_tc3<F16, kSE2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t n_tiles = a.part.tile_wp ? 2 * (int64_t)num_sms : (int64_t)a.n_wp * a.tiles_per_wp;
   int64_t grid = (n_tiles + 1) / 2;
   if (grid > num_sms) grid = num_sms;
   if (grid < 1) return cudaSuccess;
-  k_mlp_tc3<kSE2><<<(unsigned)grid, kThreads, smem, s>>>(w, a);
+  k_mlp_tc3<F16, kSE2><<<(unsigned)grid, kThreads, smem, s>>>(w, a);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_mlp_tc3(const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s) {
-  return a.frame ? launch_t<true>(w, a, num_sms, s) : launch_t<false>(w, a, num_sms, s);
+cudaError_t launch_mlp_tc3(bool f16, const WeightsBF16 &w, const QueryArgs &a, int num_sms, cudaStream_t s) {
+  if (f16) return a.frame ? launch_t<true, true>(w, a, num_sms, s) : launch_t<true, false>(w, a, num_sms, s);
+  return a.frame ? launch_t<false, true>(w, a, num_sms, s) : launch_t<false, false>(w, a, num_sms, s);
 }
 
 }  // namespace gcdf

@@ -15,7 +15,7 @@ import torch
 _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / "libgcdf.so"  # the in-tree build (python -m paper_2601_18548_b200.build); no override
 
-FP32, BF16, FP16, FP16X3 = 0, 1, 2, 3  # FP16X3: fp32-accurate tensor-core path (3-term split)
+FP32, BF16, FP16, FP16X3, BF16X3 = 0, 1, 2, 3, 4  # FP16X3 / BF16X3: 3-term split tensor-core paths (R25, R29)
 TGRAD_CHAINRULE, TGRAD_QCHANNEL = 0, 1
 FRAME_TRANSLATE, FRAME_SE2 = 0, 1  # gcdf_frame (include/gcdf.h; R24)
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "IO", -3: "BAD_MAGIC", -4: "VERSION", -5: "DIM_MISMATCH",
