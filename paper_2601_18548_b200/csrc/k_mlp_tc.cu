@@ -106,6 +106,7 @@ struct __align__(1024) SmemTC {
   float4 ptn[kSlots][H];       // [slot][row] prefetched point of the slot's next tile
   float qn[kSlots][2][12];     // [slot][tile parity] q row of the slot's tile (cp.async, phases 1-3)
   int wnx[kSlots];             // [slot] (partitioned) step of the slot's next tile, staged at phase 1
+  int rnx[kSlots];             // [slot] (dense map) tile index within its step of the slot's next tile
   int wtile[kSlots][2];        // [slot][tile parity] step (waypoint) of the slot's tile
   uint32_t slotn[kSlots][2][H];  // [slot][tile parity][row] local scene slot of the pair (~0: padding;
                                  // bit 31: a removed point, set when x is staged)
@@ -460,7 +461,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     int wn = 0;
     int64_t sl = 0;
     bool ok = false;
-    if (TT < n_tiles) tile_pair(a, TT, row, wn, sl, ok);
+    if (TT < n_tiles) {
+      if (a.part.tile_wp) {
+        tile_pair(a, TT, row, wn, sl, ok);
+      } else {  // (step, tile of the step) divided out once, at phase 3, by stage_q
+        sl = (int64_t)S.rnx[s] * kTile + row;
+        ok = sl < lb;
+      }
+    }
     S.slotn[s][par][row] = ok ? (uint32_t)sl : ~0u;
     cp_async16(&S.ptn[s][row], ok ? (const void *)(a.scene.pts + sl) : (const void *)a.scene.pts, ok ? 16u : 0u);
     cp_async_commit();
@@ -484,6 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         wn = S.wnx[s];
       } else {
         wn = (int)(TT / a.tiles_per_wp);
+        if (lane == 0) S.rnx[s] = (int)(TT - (int64_t)wn * a.tiles_per_wp);
       }
       if (lane < kNdof) cp_async4(&S.qn[s][par][lane], a.q + (int64_t)wn * kNdof + lane);
       cp_async_commit();
@@ -543,7 +552,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   bool live_n = false;
   if ((int64_t)blockIdx.x * kSlots + s < n_tiles) {
     if (hh == 0) {
-      prefetch_pt((int64_t)blockIdx.x * kSlots + s, 0);
+      int wn;
+      int64_t sl;
+      bool ok;
+      tile_pair(a, (int64_t)blockIdx.x * kSlots + s, row, wn, sl, ok);  // (the first tile: divided here)
+      S.slotn[s][0][row] = ok ? (uint32_t)sl : ~0u;
+      cp_async16(&S.ptn[s][row], ok ? (const void *)(a.scene.pts + sl) : (const void *)a.scene.pts, ok ? 16u : 0u);
+      cp_async_commit();
       cp_async_wait_all();
     }
     live_n = stage_a1(0, region(seq + 1u));  // phase 0's A region
@@ -634,19 +649,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         // f = w7 . h6 + b7 (fp32, no output activation: signed value); both
         // column halves form it from the two partial sums (half 0 writes the records, half 1
         // thresholds)
+        // (no barrier: the other half reads this partial sum two hand-offs later, at phase 7 /
+        // 11, ordered by the mbarrier chain: this warp's arrive -> MMA warp -> commit -> wait)
         S.fpart[s][hh][row] = (fa[0] + fa[1]) + (fa[2] + fa[3]);
-        if (hh == 0 && qd == 0) cp_async_wait_all();  // S.qn of the next tile (stage_q)
-        named_bar_sync(1 + s, kEpiPerSlot);
-        f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
-        if (hh == 1) {
-          const uint32_t sl = S.slotn[s][it & 1][row];
-          live = (sl >> 31) == 0u;
-          if (!a.detect) {
-            const int w = S.wtile[s][it & 1];
-            const int64_t slot = sl & 0x7fffffffu;
-            if (slot < lb) a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
-          }
-        } else {
+        if (hh == 0) {
+          if (qd == 0) cp_async_wait_all();  // S.qn of the next tile (stage_q), read at phase 11
           prefetch_pt(T + stride, (it + 1) & 1);  // the next tile's point, needed at phase 11
         }
       } else if constexpr (p < 11) {
@@ -672,7 +679,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
           if (c < 3) wait_ld();
         }
         hand_off(p);
-        if constexpr (p == 6) {
+        if constexpr (p == 7) {
+          if (hh == 1) {
+            f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
+            const uint32_t sl = S.slotn[s][it & 1][row];
+            live = (sl >> 31) == 0u;
+            if (!a.detect) {
+              const int w = S.wtile[s][it & 1];
+              const int64_t slot = sl & 0x7fffffffu;
+              if (slot < lb) a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
+            }
+          }
           if (hh == 1 && a.detect) {
             // A6/A7 (overlaps the tensor core): threshold and the warp's min key -> the detect warp
             const int64_t slot = S.slotn[s][it & 1][row] & 0x7fffffffu;  // (live implies a real pair)
@@ -712,6 +729,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         }
         hand_off(p);
         if (hh == 0) {
+          f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
           const int w = S.wtile[s][it & 1];
           const int64_t slot = S.slotn[s][it & 1][row] & 0x7fffffffu;
           float gq[kNdof];
