@@ -5,7 +5,7 @@ O=gpurun_out/$1
 mkdir -p $O
 python -m pytest tests -m gpu -q -rf > $O/pytest.log 2>&1
 python bench.py > $O/bench.json 2> $O/bench.err
-SHORT="--steps 2 --warmup 3 --no-variants --latency-calls 0 --partition-radius 0 --no-cpu-baseline --e2e-steps 1"
+SHORT="--steps 2 --warmup 3 --no-variants --no-workloads --latency-calls 0 --partition-radius 0 --no-cpu-baseline --e2e-steps 1"
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file $O/launches.csv python bench.py $SHORT > $O/ncu_launch.log 2>&1
 for k in k_pairgen k_k3_stage k_mlp_tc; do
