@@ -207,10 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
             const int64_t cc = ci + c;
             mbar_wait(&S.full[cc % kNS], (uint32_t)((cc / kNS) & 1));
             const uint32_t base = smem_u32(S.ring[cc % kNS]);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_ts_elect(tbase, ab + 8u * (uint32_t)(4 * c + k), sdesc_sw128(base + k * 32, 16, 1024), kIdescW,
-                           (c | k) > 0);
+            umma4_sw128_elect(tbase, ab + 32u * (uint32_t)c, sdesc_sw128(base, 16, 1024), kIdescW, c > 0);
           }
           if (p < 6) mma_ss_elect(tbase, a_ones, b_bias(p, 0), kIdescW, 1u);
           commit_elect(&S.mma_done[0]);
@@ -220,10 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
           for (int c = 0; c < 4; ++c) {
             const int64_t cc = ci + c;
             const uint32_t base = smem_u32(S.ring[cc % kNS]) + 16384u;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              mma_ts_elect(tbase + 128u, ab + 8u * (uint32_t)(4 * c + k), sdesc_sw128(base + k * 32, 16, 1024),
-                           kIdescW, (c | k) > 0);
+            umma4_sw128_elect(tbase + 128u, ab + 32u * (uint32_t)c, sdesc_sw128(base, 16, 1024), kIdescW, c > 0);
             commit_elect(&S.empty[cc % kNS]);
           }
           if (p < 6) mma_ss_elect(tbase + 128u, a_ones, b_bias(p, 1), kIdescW, 1u);

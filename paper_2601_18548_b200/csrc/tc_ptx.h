@@ -186,6 +186,29 @@ DEVI void mma_ss_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum)
       : "memory");
 }
+// Four UMMAs over one 64-column SWIZZLE_128B K chunk from ONE asm block (a lean issue stream:
+// the per-UMMA operands are adds of immediates): A at a + 8 i (TMEM columns), B descriptor
+// + 2 i (32 B apart inside the 128-B swizzle atom), the first accumulating iff acc != 0.
+DEVI void umma4_sw128_elect(uint32_t d, uint32_t a, uint64_t b0, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred e, p0, pt;\n\t"
+      ".reg .b32 ra;\n\t"
+      ".reg .b64 rb;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p0, %4, 0;\n\t"
+      "setp.eq.b32 pt, %4, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p0;\n\t"
+      "add.u32 ra, %1, 8;\n\tadd.u64 rb, %2, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ra], rb, %3, pt;\n\t"
+      "add.u32 ra, %1, 16;\n\tadd.u64 rb, %2, 4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ra], rb, %3, pt;\n\t"
+      "add.u32 ra, %1, 24;\n\tadd.u64 rb, %2, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ra], rb, %3, pt;\n\t"
+      "}" ::"r"(d),
+      "r"(a), "l"(b0), "r"(idesc), "r"(acc)
+      : "memory");
+}
 DEVI void commit_elect(uint64_t *bar) {
   asm volatile(
       "{\n\t"
