@@ -75,7 +75,7 @@ struct __align__(1024) Smem3 {
   uint64_t mma_done[2];
   uint64_t epi_done[2];
   uint64_t ring_full[2][2];        // [buffer][hi, lo] bulk-copy completion
-  uint32_t turn;
+  uint64_t turnb[2];           // [slot] "your turn" (the other slot's phase is issued)
   unsigned act[2][4];
   unsigned long long kmin[2][4];
   int sbase[2];
@@ -167,7 +167,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
     mbar_init(&S.epi_done[1], kEpiPerSlot);
     for (int b = 0; b < 2; ++b)
       for (int h = 0; h < 2; ++h) mbar_init(&S.ring_full[b][h], 1);
-    S.turn = 0u;
+    mbar_init(&S.turnb[0], 1);
+    mbar_init(&S.turnb[1], 1);
+    mbar_arrive(&S.turnb[0]);  // slot 0 issues the first phase
     fence_barrier_init();
   }
   if (tid < 2 * kNdof) {
@@ -203,7 +205,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
     const int ss = warp - kEpiWarps;
     const uint32_t sw1t = smem_u32(S.w1t), sb1 = smem_u32(S.b1), sbx = smem_u32(S.bext);
     const uint64_t ones_desc = sdesc_nosw(smem_u32(S.ones), 2048, 128);
-    volatile uint32_t *turn = &S.turn;
     const uint32_t d = tbase + (uint32_t)ss * 256u;
     const uint32_t ahi = d + kColAhi, alo = d + kColAlo;
     if (ss == 0 && (int64_t)blockIdx.x * 2 < n_tiles) {  // the first two runs (W2, W3)
@@ -222,12 +223,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
       for (int p = 0; p < kPhases; ++p, seq += 2) {
         mbar_wait(&S.epi_done[ss], ph);
         ph ^= 1u;
-        if (two) {
-          const long long tw = clock64();
-          while (*turn != seq) {
-            if (clock64() - tw > (1ll << 34)) __trap();
-          }
-        }
+        // the turn: an mbarrier (a waiting MMA warp polls try_wait instead of spinning on a
+        // shared counter, which took issue slots from the epilogue warps)
+        if (two) mbar_wait(&S.turnb[ss], (seq >> 1) & 1u);
         fence_after();
         if (p == 0) {  // layer 1: K = 32 split operands in A_hi (bias included)
 #pragma unroll
@@ -245,14 +243,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
                        : sdesc_sw128(wb + k * 2048, 16384, 1024);
           };
           const uint32_t id = fwd ? kIdescFwd<F16> : kIdescBwd<F16>;
+          // (each 8-UMMA group from one asm block: a lean issue stream, see tc_ptx.h)
           mbar_wait(&S.ring_full[b][0], par);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) mma_ts_elect(d, ahi + 8u * k, bdesc(whi, k), id, k > 0);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) mma_ts_elect(d, alo + 8u * k, bdesc(whi, k), id, 1u);
+          if (fwd) {
+            umma8_kmajor_elect(d, ahi, bdesc(whi, 0), id, 0u);
+            umma8_kmajor_elect(d, alo, bdesc(whi, 0), id, 1u);
+          } else {
+            umma8_mnmajor_elect(d, ahi, bdesc(whi, 0), id, 0u);
+            umma8_mnmajor_elect(d, alo, bdesc(whi, 0), id, 1u);
+          }
           mbar_wait(&S.ring_full[b][1], par);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) mma_ts_elect(d, ahi + 8u * k, bdesc(wlo, k), id, 1u);
+          if (fwd) umma8_kmajor_elect(d, ahi, bdesc(wlo, 0), id, 1u);
+          else umma8_mnmajor_elect(d, ahi, bdesc(wlo, 0), id, 1u);
           if (fwd) mma_ss_elect(d, ones_desc, sdesc_nosw(sbx + (uint32_t)(p - 1) * kBextBytes, 2048, 128), kIdescFwd<F16>, 1u);
         } else {  // g0 = e1 W1 (N = 16)
           const uint32_t hi1 = sw1t, lo1 = sw1t + kW1tBytes;
@@ -266,7 +268,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
           for (int k = 0; k < 8; ++k)
             mma_ts_elect(d, ahi + 8u * k, sdesc_sw128(lo1 + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin<F16>, 1u);
         }
-        if (two) *turn = seq + 1;
+        if (two) {
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&S.turnb[ss ^ 1]);
+        }
         commit_elect(&S.mma_done[ss]);
       }
     }

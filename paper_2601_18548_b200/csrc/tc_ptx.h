@@ -209,6 +209,34 @@ DEVI void umma4_sw128_elect(uint32_t d, uint32_t a, uint64_t b0, uint32_t idesc,
       "r"(a), "l"(b0), "r"(idesc), "r"(acc)
       : "memory");
 }
+// Eight UMMAs over K = 128 (8 K steps) from ONE asm block, A at a + 8 k (contiguous TMEM
+// columns), B a SWIZZLE_128B operand: K-major (two 64-column chunks of 16 KB: + (k / 4) 16384
+// + (k % 4) 32 bytes) or MN-major (+ k 2048 bytes); the first accumulating iff acc != 0.
+#define GCDF_UMMA8_STEP(AOFF, DOFF)                  \
+  "add.u32 ra, %1, " #AOFF ";\n\t"                    \
+  "add.u64 rb, %2, " #DOFF ";\n\t"                    \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ra], rb, %3, pt;\n\t"
+#define GCDF_UMMA8_HEAD                                                  \
+  "{\n\t.reg .pred e, p0, pt;\n\t.reg .b32 ra;\n\t.reg .b64 rb;\n\t" \
+  "elect.sync _|e, 0xffffffff;\n\t"                                      \
+  "setp.ne.b32 p0, %4, 0;\n\tsetp.eq.b32 pt, %4, %4;\n\t"               \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p0;\n\t"
+DEVI void umma8_kmajor_elect(uint32_t d, uint32_t a, uint64_t b0, uint32_t idesc, uint32_t acc) {
+  asm volatile(GCDF_UMMA8_HEAD GCDF_UMMA8_STEP(8, 2) GCDF_UMMA8_STEP(16, 4) GCDF_UMMA8_STEP(24, 6)
+                   GCDF_UMMA8_STEP(32, 1024) GCDF_UMMA8_STEP(40, 1026) GCDF_UMMA8_STEP(48, 1028)
+                       GCDF_UMMA8_STEP(56, 1030) "}" ::"r"(d),
+               "r"(a), "l"(b0), "r"(idesc), "r"(acc)
+               : "memory");
+}
+DEVI void umma8_mnmajor_elect(uint32_t d, uint32_t a, uint64_t b0, uint32_t idesc, uint32_t acc) {
+  asm volatile(GCDF_UMMA8_HEAD GCDF_UMMA8_STEP(8, 128) GCDF_UMMA8_STEP(16, 256) GCDF_UMMA8_STEP(24, 384)
+                   GCDF_UMMA8_STEP(32, 512) GCDF_UMMA8_STEP(40, 640) GCDF_UMMA8_STEP(48, 768)
+                       GCDF_UMMA8_STEP(56, 896) "}" ::"r"(d),
+               "r"(a), "l"(b0), "r"(idesc), "r"(acc)
+               : "memory");
+}
+#undef GCDF_UMMA8_STEP
+#undef GCDF_UMMA8_HEAD
 DEVI void commit_elect(uint64_t *bar) {
   asm volatile(
       "{\n\t"
