@@ -138,16 +138,12 @@ DEVI void issue_phase(int p, uint32_t tb, uint32_t sw, uint32_t sw1t, uint32_t s
   } else if (p < 6) {  // layer l = p + 1: D = h_{l-1} W_l^T + ones x bias
     const uint32_t av = tb + kColH + 64u * (uint32_t)(p - 1);
     const uint32_t wb = sw + (uint32_t)(p - 1) * (H * H * 2);
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      mma_ts_elect(d, av + 8u * k, sdesc_sw128(wb + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024), kIdescFwd, k > 0);
+    umma8_kmajor_elect(d, av, sdesc_sw128(wb, 16, 1024), kIdescFwd, 0u);  // (one asm block, tc_ptx.h)
     mma_ts_elect(d, tb + kColOnes, sdesc_nosw(sbx + (uint32_t)(p - 1) * kBextBytes, 2048, 128), kIdescFwd, 1u);
   } else if (p < 11) {  // backward through layer l = 12 - p: D = e_l W_l (B MN-major)
     const uint32_t av = p == 6 ? tb + kColE6 : tb + kColH + 64u * (uint32_t)(11 - p);
     const uint32_t wb = sw + (uint32_t)(10 - p) * (H * H * 2);
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      mma_ts_elect(d, av + 8u * k, sdesc_sw128(wb + k * 2048, 16384, 1024), kIdescBwd, k > 0);
+    umma8_mnmajor_elect(d, av, sdesc_sw128(wb, 16384, 1024), kIdescBwd, 0u);
   } else {  // g0 = e1 W1 (N = 16 rows of W1^T)
 #pragma unroll
     for (int k = 0; k < 8; ++k)
