@@ -17,12 +17,13 @@ NT = max(1, min(os.cpu_count() or 1, 16))
 
 # (precision name, H, activation, frame, value tolerance vs the exact oracle)
 PATHS = [("fp32", 128, 1, 0, 1e-4), ("fp16", 128, 1, 0, 2e-2), ("bf16", 128, 1, 0, 3e-2), ("fp16x3", 128, 1, 0, 1e-4),
-         ("fp16", 128, 1, 1, 2e-2), ("fp16", 128, 2, 0, 2e-2), ("fp16", 256, 1, 0, 2e-2), ("fp32", 256, 2, 0, 1e-4)]
+         ("fp16", 128, 1, 1, 2e-2), ("fp16", 128, 2, 0, 2e-2), ("fp16", 256, 1, 0, 2e-2), ("fp32", 256, 2, 0, 1e-4),
+         ("bf16x3", 128, 1, 0, 1e-3)]
 
 
 def _ctx(prec, H, act, frame):
-    from paper_2601_18548_b200 import BF16, FP16, FP16X3, FP32, Context
-    p = {"fp32": FP32, "fp16": FP16, "bf16": BF16, "fp16x3": FP16X3}[prec]
+    from paper_2601_18548_b200 import BF16, BF16X3, FP16, FP16X3, FP32, Context
+    p = {"fp32": FP32, "fp16": FP16, "bf16": BF16, "fp16x3": FP16X3, "bf16x3": BF16X3}[prec]
     ctx = Context(0, precision=p, scene_capacity=512, max_waypoints=16, max_active=1 << 12, max_candidates=1 << 12,
                   frame=frame)
     ctx.load_weights(synth.weights_path(H, act=act))

@@ -353,3 +353,24 @@ def test_tile_count_edge_cases(c2, n_wp, n_pts):
     assert len(b["wp"]) > 0
     for k in ("wp", "pt", "value", "grad"):
         assert np.array_equal(a[k], b[k]), k
+
+
+def test_staging_overflow_reports_capacity(c2):
+    """More actives than the staging capacity (max_active): the tiles that no longer fit are
+    dropped by the detect warp's allocation, the call reports CAPACITY, and a retry with a
+    context of sufficient capacity returns the full canonical set."""
+    from paper_2601_18548_b200 import Context, GcdfError
+    cfg, pts, q, m, exact, emu = c2
+    qt = torch.from_numpy(q[:, :4])
+    tau = float(np.median(emu["fp16"]["f"])) - DELTA  # ~half of the pairs active
+    small = Context(0, precision=2, scene_capacity=cfg.M + 4096, max_waypoints=64, max_active=1024)
+    small.load_weights(synth.weights_path(cfg.H))
+    small.update_scene(pts)
+    with pytest.raises(GcdfError) as e:
+        small.detect_active_set(qt, DELTA, tau, capacity=1024)
+    assert e.value.name == "CAPACITY"
+    big = _ctx(cfg, "fp16")
+    big.update_scene(pts)
+    full = records_np(big.detect_active_set(qt, DELTA, tau))
+    assert len(full["wp"]) > 1024
+    assert np.all(np.diff(full["wp"].astype(np.int64) * (1 << 32) + full["pt"]) > 0)  # canonical order
