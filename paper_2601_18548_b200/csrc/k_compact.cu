@@ -8,6 +8,7 @@
 // Min keys: key = ord(f) << 32 | pt, ord() order-preserving float -> uint32, so the
 // unsigned minimum is (min f, smallest id on ties) -- one atomicMin per tile.
 #include <algorithm>
+#include <cmath>
 
 #include "gcdf_internal.h"
 #include "k_scan.cuh"
@@ -72,13 +73,30 @@ struct K3Scratch {
 
 constexpr int kK3List = 128;  // per-warp record list (entries per pass)
 
+// The largest float x with fl(x - delta) <= tau (fp32, round to nearest): the active test
+// "f - delta <= tau" of K2b (R12) as one compare per value.  fl(x - delta) is non-decreasing
+// in x, so {x : fl(x - delta) <= tau} = [-inf, x*] exactly (host side, IEEE single arithmetic).
+float k3_threshold(float delta, float tau) {
+  if (std::isnan(delta) || std::isnan(tau)) return -INFINITY;
+  volatile float d = delta, t = tau;  // (no contraction / excess precision: plain fp32 subtracts)
+  auto ok = [&](float x) { volatile float r = x - d; return r <= t; };
+  float x = tau + delta;
+  if (!std::isfinite(x)) return ok(x) ? x : std::nextafter(x, 0.f);
+  while (!ok(x)) x = std::nextafter(x, -INFINITY);
+  for (;;) {
+    const float y = std::nextafter(x, INFINITY);
+    if (!ok(y)) return x;
+    x = y;
+  }
+}
+
 __global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__restrict__ values,
                                                             const float *__restrict__ grads, int64_t stride,
-                                                            int32_t n_wp, int32_t tpw, SceneView scene, float delta,
-                                                            float tau, DetectScratch ds, K3Scratch ks) {
+                                                            int32_t n_wp, int32_t tpw, SceneView scene, float thr,
+                                                            DetectScratch ds, K3Scratch ks) {
   __shared__ int32_t s_wcnt[kK3Warps];
   __shared__ int64_t s_base;
-  __shared__ uint2 s_list[kK3Warps][kK3List];  // (slot in the warp's range, value bits)
+  __shared__ uint2 s_list[kK3Warps][kK3List];  // (tile << 7 | slot in the tile, value bits)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t p = blockIdx.x;
   const int64_t n_tiles = (int64_t)n_wp * tpw;
@@ -87,7 +105,8 @@ __global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__re
   const int w0 = (int)(T0 / tpw);
   const int t0 = (int)(T0 - (int64_t)w0 * tpw);
   const int nt = (int)max((int64_t)0, min((int64_t)kK3TW, n_tiles - T0));  // tiles of this warp
-  // ---- loads: the warp's tiles, all in flight
+  // ---- loads: the warp's tiles, all in flight.  Tile i is (w0 + wi, t0 + i - wi tpw) with wi =
+  // the number of step ends crossed (a warp's 8 tiles cross at most one when tpw >= 8)
   float4 v[kK3TW];
   {
     int w = w0, t = t0;
@@ -97,8 +116,8 @@ __global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__re
       if (++t == tpw) { t = 0; ++w; }
     }
   }
-  // ---- per tile: this lane's 4 active flags (4 bits of `bits`), their count (8-bit fields of
-  // cnt_lo / cnt_hi for the one warp scan below), and the lane's running minimum of the step
+  // ---- per tile: this lane's 4 active flags (nibble i of `bits`), their count (8-bit fields
+  // of cnt_lo / cnt_hi for the one warp scan below), and the lane's running minimum of the step
   uint32_t bits = 0u, cnt_lo = 0u, cnt_hi = 0u;
   const float inf = __int_as_float(0x7f800000);
   float lmin = inf;
@@ -125,8 +144,8 @@ __global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__re
           wk = w;
         }
         const float4 x = v[i];
-        const uint32_t b = (uint32_t)(x.x - delta <= tau) | ((uint32_t)(x.y - delta <= tau) << 1) |
-                           ((uint32_t)(x.z - delta <= tau) << 2) | ((uint32_t)(x.w - delta <= tau) << 3);
+        const uint32_t b = (x.x <= thr ? 1u : 0u) | (x.y <= thr ? 2u : 0u) | (x.z <= thr ? 4u : 0u) |
+                           (x.w <= thr ? 8u : 0u);
         bits |= b << (4 * i);
         const uint32_t c = __popc(b);
         if (i < 4) cnt_lo |= c << (8 * i); else cnt_hi |= c << (8 * (i - 4));
@@ -151,39 +170,38 @@ __global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__re
     }
   }
   const uint32_t tot_lo = __shfl_sync(0xffffffffu, sc_lo, 31), tot_hi = __shfl_sync(0xffffffffu, sc_hi, 31);
-  // tile i: total T_i = field i of tot, this lane's exclusive prefix = field i of (sc - cnt)
-  int tile_pre[kK3TW];  // actives of the warp's tiles before tile i
+  const uint32_t ex_lo = sc_lo - cnt_lo, ex_hi = sc_hi - cnt_hi;
+  // tile i: the warp's actives before tile i (tile_pre) + this lane's exclusive prefix in tile i
+  int rk[kK3TW];
   int wtot = 0;
 #pragma unroll
   for (int i = 0; i < kK3TW; ++i) {
-    tile_pre[i] = wtot;
+    rk[i] = wtot + (int)(((i < 4 ? ex_lo : ex_hi) >> (8 * (i & 3))) & 0xffu);
     wtot += (int)(((i < 4 ? tot_lo : tot_hi) >> (8 * (i & 3))) & 0xffu);
   }
-  const uint32_t ex_lo = sc_lo - cnt_lo, ex_hi = sc_hi - cnt_hi;
   uint2 *list = s_list[warp];
   // the warp's actives in (tile, slot) order into its list: entries [c0, c0 + kK3List) of the
-  // warp's ranks (c0 = 0 here, while the values are in registers; more than kK3List actives
-  // per warp -- rare -- take later passes that re-read the values, which are in L2)
+  // warp's ranks; each lane has at most 4 actives per tile, written by predicated stores (no
+  // per-active loop).  More than kK3List actives per warp (rare) take later passes that re-read
+  // the values (L2-resident).
   auto fill = [&](int c0, const float4 *vv) {
-    if (!bits) return;
 #pragma unroll
     for (int i = 0; i < kK3TW; ++i) {
-      uint32_t b = (bits >> (4 * i)) & 0xfu;
+      const uint32_t b = (bits >> (4 * i)) & 0xfu;
       if (!b) continue;
-      int r = tile_pre[i] + (int)(((i < 4 ? ex_lo : ex_hi) >> (8 * (i & 3))) & 0xffu) - c0;
+      int r = rk[i] - c0;
       const float4 x = vv ? vv[i] : load_tile_values(values, stride, lb, w0 + (t0 + i) / tpw, (t0 + i) % tpw, lane);
-      while (b) {
-        const int k = __ffs(b) - 1;
-        b &= b - 1u;
-        if (r >= 0 && r < kK3List) {
-          const float xk = k == 0 ? x.x : k == 1 ? x.y : k == 2 ? x.z : x.w;
-          list[r] = make_uint2((uint32_t)(i * kTile + 4 * lane + k), __float_as_uint(xk));
+      const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if ((b >> k) & 1u) {
+          if (r >= 0 && r < kK3List) list[r] = make_uint2((uint32_t)(i * kTile + 4 * lane + k), __float_as_uint(xs[k]));
+          ++r;
         }
-        ++r;
       }
     }
   };
-  fill(0, v);
+  if (bits) fill(0, v);
   __syncwarp();
   if (lane == 0) s_wcnt[warp] = wtot;
   __syncthreads();
@@ -204,12 +222,16 @@ __global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__re
   const int64_t base = s_base;
   int64_t pos = 0;  // this warp's first record in the partition
   for (int j = 0; j < warp; ++j) pos += s_wcnt[j];
-  // step starts inside this warp's tiles
-  if (lane == 0) {
-    int t = t0, w = w0;
-    for (int i = 0; i < nt; ++i) {
-      if (t == 0) ks.wstart[w] = (p << 20) | (pos + tile_pre[i]);
-      if (++t == tpw) { t = 0; ++w; }
+  // step starts inside this warp's tiles (lane i: tile i)
+  if (lane < nt) {
+    const int ti = t0 + lane;
+    const int wi = ti / tpw;
+    if (ti - wi * tpw == 0) {
+      int pre = 0;
+#pragma unroll
+      for (int i = 0; i < kK3TW; ++i)
+        if (i < lane) pre += (int)(((i < 4 ? tot_lo : tot_hi) >> (8 * (i & 3))) & 0xffu);
+      ks.wstart[w0 + wi] = (p << 20) | (pos + pre);
     }
   }
   if (base < 0 || wtot == 0) return;
@@ -224,9 +246,9 @@ __global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__re
     const int n = min(kK3List, wtot - c0);
     for (int e = lane; e < n; e += 32) {
       const uint2 it = list[e];
-      const int i = (int)(it.x >> 7);
-      int t = t0 + i, w = w0;
-      while (t >= tpw) { t -= tpw; ++w; }
+      const int ti = t0 + (int)(it.x >> 7);
+      const int wi = ti >= tpw ? ti / tpw : 0;
+      const int w = w0 + wi, t = ti - wi * tpw;
       const int64_t slot = (int64_t)t * kTile + (it.x & 127u);
       const float *g = grads + ((int64_t)w * stride + slot) * kNdof;
       float gg[kNdof];
@@ -496,8 +518,8 @@ cudaError_t launch_compact_dense(const float *values, const float *grads, int64_
   ks.scan_tmp = ks.wstart + n_wp;
   if (n_parts > 0) {
     // (ds.counter[0] = the staging allocation counter and [1] the overflow flag, zeroed by k_detect_init)
-    k_k3_stage<<<(unsigned)n_parts, kK3Warps * 32, 0, s>>>(values, grads, stride, n_wp, tiles_per_wp, scene, delta,
-                                                            tau, ds, ks);
+    k_k3_stage<<<(unsigned)n_parts, kK3Warps * 32, 0, s>>>(values, grads, stride, n_wp, tiles_per_wp, scene,
+                                                            k3_threshold(delta, tau), ds, ks);
     ++*n_launches;
     cudaError_t e = excl_scan(ks.part_cnt, n_parts, ks.part_pre, ks.part_pre + n_parts, ks.scan_tmp, s, n_launches);
     if (e != cudaSuccess) return e;
