@@ -11,8 +11,9 @@ DELTA = synth.inputs.DELTA
 # fp32 path, BASELINE north_star: 1e-4 relative / 1e-5 absolute (allclose form, R17)
 FP32_RTOL, FP32_ATOL = 1e-4, 1e-5
 # gradient of a ReLU net is discontinuous at kinks: a pair may differ only if some
-# hidden pre-activation is within KINK of zero (fp32 rounding of z is ~1e-6)
-KINK_FP32 = 1e-4
+# hidden pre-activation is within KINK of zero.  fp32 rounding of z is ~1e-6 at the R11
+# scale: 1e-5 passes every fp32-tolerance suite, 1e-6 fails four (R17); round 1 used 1e-4
+KINK_FP32 = 1e-5
 BAND_FP32 = 1e-3          # active-set parity band around the threshold (north_star)
 # bf16 tensor-core path (R17)
 BF16_VAL_ATOL = 2e-2      # value vs exact oracle
