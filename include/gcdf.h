@@ -310,6 +310,12 @@ int gcdf_dist_init(gcdf_ctx *ctx, const unsigned char id[128], int32_t rank, int
    Not for production and not capturable into a CUDA graph. */
 typedef int (*gcdf_host_allgather_fn)(const void *send_host, void *recv_host, int64_t bytes_per_rank, void *user);
 int gcdf_dist_init_host(gcdf_ctx *ctx, gcdf_host_allgather_fn fn, void *user);
+/* Broadcast of the waypoint batch q [B][N][9] fp32 (device, in place) from rank 0 to every
+   rank, for drivers that are not SPMD: afterwards every rank's q equals rank
+   0's, so a following detect sees identical waypoints on all ranks.  Enqueued on `stream`
+   (NCCL: one ncclBroadcast; the host test backend synchronizes).  INVALID_ARG (no
+   communicator, null q, B or N <= 0), NCCL, CUDA. */
+int gcdf_broadcast_waypoints(gcdf_ctx *ctx, float *q, int32_t B, int32_t N, void *stream);
 /* Communicator state: *kind 0 = none, 1 = NCCL, 2 = host test backend; *nccl_version (may be
    NULL) = ncclGetVersion of the opened library (0 if none). */
 int gcdf_dist_info(const gcdf_ctx *ctx, int32_t *kind, int32_t *nccl_version);

@@ -32,6 +32,7 @@ struct NcclApi {
   decltype(&ncclCommInitRank) comm_init_rank = nullptr;
   decltype(&ncclCommDestroy) comm_destroy = nullptr;
   decltype(&ncclAllGather) all_gather = nullptr;
+  decltype(&ncclBroadcast) broadcast = nullptr;
   decltype(&ncclGroupStart) group_start = nullptr;
   decltype(&ncclGroupEnd) group_end = nullptr;
   decltype(&ncclGetErrorString) error_string = nullptr;
@@ -57,11 +58,13 @@ const NcclApi *nccl_api(std::string *err) {
   api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(sym("ncclCommInitRank"));
   api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(sym("ncclCommDestroy"));
   api.all_gather = reinterpret_cast<decltype(api.all_gather)>(sym("ncclAllGather"));
+  api.broadcast = reinterpret_cast<decltype(api.broadcast)>(sym("ncclBroadcast"));
   api.group_start = reinterpret_cast<decltype(api.group_start)>(sym("ncclGroupStart"));
   api.group_end = reinterpret_cast<decltype(api.group_end)>(sym("ncclGroupEnd"));
   api.error_string = reinterpret_cast<decltype(api.error_string)>(sym("ncclGetErrorString"));
   api.get_version = reinterpret_cast<decltype(api.get_version)>(sym("ncclGetVersion"));
-  if (!api.get_unique_id || !api.comm_init_rank || !api.comm_destroy || !api.all_gather || !api.group_start ||
+  if (!api.get_unique_id || !api.comm_init_rank || !api.comm_destroy || !api.all_gather || !api.broadcast ||
+      !api.group_start ||
       !api.group_end || !api.error_string) {
     if (err) *err = "libnccl.so.2 lacks an expected symbol";
     return nullptr;
@@ -195,6 +198,36 @@ int comm_allgather(Comm &c, int n, const void *const *send, void *const *recv, c
     return kCommErrCuda;
   }
   return 0;
+}
+
+int comm_broadcast(Comm &c, void *buf, int64_t bytes, cudaStream_t s, std::string *err) {
+  if (bytes <= 0) return 0;
+  if (c.kind == kCommNccl) {
+    const NcclApi *api = nccl_api(err);
+    if (!api) return kCommErrNccl;
+    const ncclResult_t r = api->broadcast(buf, buf, (size_t)bytes, ncclUint8, 0, static_cast<ncclComm_t>(c.nccl), s);
+    return r == ncclSuccess ? 0 : nccl_fail(api, r, "ncclBroadcast", err);
+  }
+  if (c.kind != kCommHost) {
+    if (err) *err = "no communicator";
+    return kCommErrNccl;
+  }
+  // test backend: every rank's bytes are gathered, rank 0's piece is copied back into buf
+  void *tmp = nullptr;
+  if (cudaMallocAsync(&tmp, (size_t)bytes * c.world, s) != cudaSuccess) {
+    if (err) *err = "host backend: broadcast staging";
+    return kCommErrCuda;
+  }
+  const void *send[1] = {buf};
+  void *recv[1] = {tmp};
+  const int64_t b[1] = {bytes};
+  int r = comm_allgather(c, 1, send, recv, b, s, err);
+  if (r == 0 && cudaMemcpyAsync(buf, tmp, (size_t)bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess) {
+    if (err) *err = "host backend: broadcast copy";
+    r = kCommErrCuda;
+  }
+  cudaFreeAsync(tmp, s);
+  return r;
 }
 
 }  // namespace gcdf

@@ -31,5 +31,8 @@ void comm_destroy(Comm &c);
 // recv[i] + r * bytes[i] on every rank; enqueued on s (NCCL) or synchronous (host backend).
 int comm_allgather(Comm &c, int n, const void *const *send, void *const *recv, const int64_t *bytes, cudaStream_t s,
                    std::string *err);
+// rank 0's `bytes` bytes of buf (device) to every rank's buf, in place; enqueued on s (NCCL,
+// ncclBroadcast) or synchronous (host backend: an all-gather of which rank 0's piece is kept)
+int comm_broadcast(Comm &c, void *buf, int64_t bytes, cudaStream_t s, std::string *err);
 
 }  // namespace gcdf

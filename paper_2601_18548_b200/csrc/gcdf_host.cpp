@@ -1310,6 +1310,17 @@ int gcdf_dist_init_host(gcdf_ctx *c, gcdf_host_allgather_fn fn, void *user) {
   return GCDF_OK;
 }
 
+int gcdf_broadcast_waypoints(gcdf_ctx *c, float *q, int32_t B, int32_t N, void *stream) {
+  int rc = precheck(c);
+  if (rc) return rc;
+  if (c->comm.kind == kCommNone) return fail(c, GCDF_ERR_INVALID_ARG, "broadcast_waypoints: no communicator");
+  if (!q || B <= 0 || N <= 0) return fail(c, GCDF_ERR_INVALID_ARG, "broadcast_waypoints: bad arguments");
+  std::string msg;
+  const int r = comm_broadcast(c->comm, q, (int64_t)B * N * kNdof * (int64_t)sizeof(float),
+                               static_cast<cudaStream_t>(stream), &msg);
+  return r ? comm_rc(c, r, msg) : GCDF_OK;
+}
+
 int gcdf_dist_info(const gcdf_ctx *c, int32_t *kind, int32_t *nccl_version) {
   if (!c) return GCDF_ERR_INVALID_ARG;
   if (kind) *kind = c->comm.kind;

@@ -29,7 +29,8 @@ EXPORTED = ["gcdf_default_options", "gcdf_create", "gcdf_destroy", "gcdf_last_er
             "gcdf_detect_active_set_partitioned", "gcdf_detect_active_set_host", "gcdf_sparse_jacobian",
             "gcdf_project_dense", "gcdf_graph_create_detect", "gcdf_graph_launch", "gcdf_graph_destroy", "gcdf_compact_dense", "gcdf_merge_active_sets", "gcdf_launch_count", "gcdf_profile_enable",
             "gcdf_profile_read", "gcdf_profile_read_exchange", "gcdf_selftest_umma", "gcdf_debug_trace",
-            "gcdf_nccl_unique_id", "gcdf_dist_init", "gcdf_dist_init_host", "gcdf_dist_info"]
+            "gcdf_nccl_unique_id", "gcdf_dist_init", "gcdf_dist_init_host", "gcdf_dist_info",
+            "gcdf_broadcast_waypoints"]
 COMM_KINDS = {0: "none", 1: "nccl", 2: "host"}
 # gcdf_host_allgather_fn (include/gcdf.h): the test backend's blocking host all-gather
 HOST_ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
@@ -94,6 +95,7 @@ def load_library(path: str | Path = LIB_PATH):
     lib.gcdf_dist_init.argtypes = [P, C.c_char_p, I32, I32]
     lib.gcdf_dist_init_host.argtypes = [P, HOST_ALLGATHER_FN, P]
     lib.gcdf_dist_info.argtypes = [P, C.POINTER(I32), C.POINTER(I32)]
+    lib.gcdf_broadcast_waypoints.argtypes = [P, P, I32, I32, P]
     lib.gcdf_selftest_umma.argtypes = [C.c_int, C.c_int, P, P, P, P]
     lib.gcdf_debug_trace.argtypes = [P, P]
     _lib = lib
@@ -277,6 +279,15 @@ class Context:
                 return 1
         self._host_cb = HOST_ALLGATHER_FN(_cb)  # kept alive with the context
         self._check(self.lib.gcdf_dist_init_host(self._h, self._host_cb, None))
+
+    def broadcast_waypoints(self, q: torch.Tensor) -> torch.Tensor:
+        """gcdf_broadcast_waypoints: rank 0's waypoints to every rank, in place (q: [B, N, 9]
+        float32 contiguous on this context's device)."""
+        if q.dtype != torch.float32 or not q.is_contiguous() or q.device != self.device or q.dim() != 3:
+            raise ValueError("broadcast_waypoints: q must be a contiguous float32 [B, N, 9] tensor on the context's device")
+        self._check(self.lib.gcdf_broadcast_waypoints(self._h, C.c_void_p(q.data_ptr()), int(q.shape[0]),
+                                                      int(q.shape[1]), _stream(self.device)))
+        return q
 
     def dist_info(self):
         k, v = C.c_int32(), C.c_int32()

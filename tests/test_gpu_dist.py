@@ -74,6 +74,13 @@ def test_nccl_exchange_world1_equals_plain_detect(prec):
     g = ctx.detect_graph(q, DELTA, tau)
     _same(g.launch(), ref.detect_active_set(q, DELTA, tau))
     g.close()
+    # the waypoint broadcast through NCCL (one rank: q unchanged); without a communicator it is refused
+    qb = q.clone()
+    ctx.broadcast_waypoints(qb)
+    assert torch.equal(qb, q)
+    from paper_2601_18548_b200 import GcdfError
+    with pytest.raises(GcdfError):
+        ref.broadcast_waypoints(qb)
 
 
 def test_exchange_capacity_is_reported():
@@ -138,6 +145,10 @@ def _rank_main(rank, world, port, out_q):
             res[name] = {"n": n, "records": o["records"][:n].cpu().numpy(),
                          **{k: o[k].cpu().numpy() for k in ("wp_offsets", "wp_min", "wp_argmin")}}
         res["local_bound"] = ctx.scene_info()["local_bound"]
+        # gcdf_broadcast_waypoints: every rank starts from its own waypoints, ends with rank 0's
+        qb = q + float(rank)
+        ctx.broadcast_waypoints(qb)
+        res["bcast_ok"] = bool(torch.equal(qb, q))
         out_q.put((rank, res))
         dist.barrier()
     finally:
@@ -178,6 +189,7 @@ def test_host_backend_ranks_on_one_gpu_equal_single_gpu(world):
             assert np.array_equal(g["records"], o["records"][:n].cpu().numpy()), (name, r)
             for k in ("wp_offsets", "wp_min", "wp_argmin"):
                 assert np.array_equal(g[k], o[k].cpu().numpy()), (name, r, k)
+    assert all(got[r]["bcast_ok"] for r in range(world))
     # the shards really are shards: each rank holds about 1/world of the slots
     assert all(got[r]["local_bound"] < ref.scene_info()["local_bound"] for r in range(world))
 
