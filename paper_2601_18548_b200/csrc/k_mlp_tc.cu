@@ -695,15 +695,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
             const int64_t slot = S.slotn[s][it & 1][row] & 0x7fffffffu;  // (live implies a real pair)
             const bool act = live && (f - a.delta <= a.tau);
             const unsigned bal = __ballot_sync(0xffffffffu, act);
-            unsigned long long key = ~0ull;
-            if (live)
-              key = ((unsigned long long)ord_f32(f) << 32) |
-                    (unsigned long long)local_to_global(slot, a.scene.rank, a.scene.world);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-              key = other < key ? other : key;
-            }
+            // the warp's min key (ord f << 32 | id) by two 32-bit warp reductions (REDUX): the
+            // min of ord f, then the smallest id among the lanes that hold it
+            const unsigned khi = live ? ord_f32(f) : 0xffffffffu;
+            const unsigned mhi = __reduce_min_sync(0xffffffffu, khi);
+            const unsigned klo = (live && khi == mhi) ? (unsigned)local_to_global(slot, a.scene.rank, a.scene.world)
+                                                      : 0xffffffffu;
+            const unsigned mlo = __reduce_min_sync(0xffffffffu, klo);
+            const unsigned long long key = ((unsigned long long)mhi << 32) | mlo;
             if (lane == 0) {
               S.act[s][qd] = bal;
               S.kmin[s][qd] = key;
