@@ -9,6 +9,7 @@
 // unsigned minimum is (min f, smallest id on ties) -- one atomicMin per tile.
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "gcdf_internal.h"
 #include "k_scan.cuh"
@@ -105,10 +106,17 @@ __global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__re
   const int w0 = (int)(T0 / tpw);
   const int t0 = (int)(T0 - (int64_t)w0 * tpw);
   const int nt = (int)max((int64_t)0, min((int64_t)kK3TW, n_tiles - T0));  // tiles of this warp
+  // Fast path (all but ~1 in tpw / 8 warps): 8 full tiles inside one step -- straight loads
+  // from one base address, no step change inside, no per-tile bounds checks.
+  const bool fast = nt == kK3TW && t0 + kK3TW <= tpw;  // (uniform over the warp)
   // ---- loads: the warp's tiles, all in flight.  Tile i is (w0 + wi, t0 + i - wi tpw) with wi =
   // the number of step ends crossed (a warp's 8 tiles cross at most one when tpw >= 8)
   float4 v[kK3TW];
-  {
+  if (fast) {
+    const float4 *vb = reinterpret_cast<const float4 *>(values + (int64_t)w0 * stride + (int64_t)t0 * kTile) + lane;
+#pragma unroll
+    for (int i = 0; i < kK3TW; ++i) v[i] = __ldcs(vb + (kTile / 4) * i);
+  } else {
     int w = w0, t = t0;
 #pragma unroll
     for (int i = 0; i < kK3TW; ++i) {
@@ -122,25 +130,25 @@ __global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__re
   const float inf = __int_as_float(0x7f800000);
   float lmin = inf;
   uint32_t lslot = 0u;
-  {
+  auto flush = [&](int wk) {  // the step's minimum over the warp: (min value, then smallest slot)
+    float m = lmin;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    uint32_t sl = lmin == m ? lslot : 0xffffffffu;
+    sl = __reduce_min_sync(0xffffffffu, sl);
+    if (lane == 0 && m < inf)
+      atomicMin(ds.wp_key + wk, ((unsigned long long)ord_f32(m) << 32) |
+                                    (unsigned long long)local_to_global(sl, scene.rank, scene.world));
+    lmin = inf;
+  };
+  auto process = [&](auto fc) {
+    constexpr bool F = decltype(fc)::value;
     int w = w0, t = t0, wk = w0;
-    auto flush = [&]() {  // the step's minimum over the warp: (min value, then smallest slot)
-      float m = lmin;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
-      uint32_t sl = lmin == m ? lslot : 0xffffffffu;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sl = min(sl, __shfl_xor_sync(0xffffffffu, sl, o));
-      if (lane == 0 && m < inf)
-        atomicMin(ds.wp_key + wk, ((unsigned long long)ord_f32(m) << 32) |
-                                      (unsigned long long)local_to_global(sl, scene.rank, scene.world));
-      lmin = inf;
-    };
 #pragma unroll
     for (int i = 0; i < kK3TW; ++i) {
-      if (i < nt) {  // (uniform over the warp)
-        if (w != wk) {
-          flush();
+      if (F || i < nt) {  // (uniform over the warp)
+        if (!F && w != wk) {
+          flush(wk);
           wk = w;
         }
         const float4 x = v[i];
@@ -155,10 +163,17 @@ __global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__re
           lslot = (uint32_t)t * kTile + 4u * lane + (x.x == m4 ? 0u : x.y == m4 ? 1u : x.z == m4 ? 2u : 3u);
         }
       }
-      if (++t == tpw) { t = 0; ++w; }
+      if (F) {
+        ++t;
+      } else if (++t == tpw) {
+        t = 0;
+        ++w;
+      }
     }
-    flush();
-  }
+    flush(wk);
+  };
+  if (fast) process(std::true_type{});
+  else process(std::false_type{});
   // ---- one inclusive warp scan of the packed per-tile counts (fields <= 128 fit 8 bits)
   uint32_t sc_lo = cnt_lo, sc_hi = cnt_hi;
 #pragma unroll
