@@ -220,21 +220,16 @@ __global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__re
   __syncwarp();
   if (lane == 0) s_wcnt[warp] = wtot;
   __syncthreads();
+  // the partition's staging allocation: thread 0 issues the atomicAdd here and consumes its
+  // result only after the lanes have issued their first gradient-row loads below, so its
+  // round trip overlaps theirs (the CTA barrier after it was the kernel's top stall)
+  int64_t agg = 0;
+  unsigned long long pb = 0ull;
   if (threadIdx.x == 0) {
-    int64_t agg = 0;
 #pragma unroll
     for (int j = 0; j < kK3Warps; ++j) agg += s_wcnt[j];
-    int64_t base = agg > 0 ? (int64_t)atomicAdd(ds.counter, (unsigned long long)agg) : 0;
-    if (base + agg > ds.max_active) {
-      atomicOr(ds.counter + 1, 1ull);
-      base = -1;
-    }
-    ks.part_base[p] = base;
-    ks.part_cnt[p] = agg;
-    s_base = base;
+    if (agg > 0) pb = atomicAdd(ds.counter, (unsigned long long)agg);
   }
-  __syncthreads();
-  const int64_t base = s_base;
   int64_t pos = 0;  // this warp's first record in the partition
   for (int j = 0; j < warp; ++j) pos += s_wcnt[j];
   // step starts inside this warp's tiles (lane i: tile i)
@@ -249,9 +244,50 @@ __global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__re
       ks.wstart[w0 + wi] = (p << 20) | (pos + pre);
     }
   }
+  // record e of the warp's list: its (step, slot) and gradient row
+  auto rec_at = [&](int e, int &w, int64_t &slot) -> const float * {
+    const uint2 it = list[e];
+    const int ti = t0 + (int)(it.x >> 7);
+    const int wi = ti >= tpw ? ti / tpw : 0;
+    w = w0 + wi;
+    slot = (int64_t)(ti - wi * tpw) * kTile + (it.x & 127u);
+    return grads + ((int64_t)w * stride + slot) * kNdof;
+  };
+  auto put = [&](int64_t dst_i, uint32_t vbits, const float (&gg)[kNdof], int w, int64_t slot) {
+    float4 *dst = reinterpret_cast<float4 *>(ds.staging + dst_i);
+    dst[0] = make_float4(__uint_as_float(vbits), gg[0], gg[1], gg[2]);
+    dst[1] = make_float4(gg[3], gg[4], gg[5], gg[6]);
+    dst[2] = make_float4(gg[7], gg[8], __uint_as_float((unsigned)w),
+                         __uint_as_float((unsigned)local_to_global(slot, scene.rank, scene.world)));
+  };
+  // the lane's first record (list entry `lane`), loads in flight across the barrier
+  const int n0 = min(kK3List, wtot);
+  float g1[kNdof];
+  int w1 = 0;
+  int64_t slot1 = 0;
+  uint32_t v1 = 0u;
+  if (lane < n0) {
+    const float *g = rec_at(lane, w1, slot1);
+    v1 = list[lane].y;
+#pragma unroll
+    for (int q = 0; q < kNdof; ++q) g1[q] = __ldcs(g + q);
+  }
+  if (threadIdx.x == 0) {
+    int64_t base = (int64_t)pb;
+    if (agg > 0 && base + agg > ds.max_active) {
+      atomicOr(ds.counter + 1, 1ull);
+      base = -1;
+    }
+    ks.part_base[p] = base;
+    ks.part_cnt[p] = agg;
+    s_base = base;
+  }
+  __syncthreads();
+  const int64_t base = s_base;
   if (base < 0 || wtot == 0) return;
   // ---- records: one active per lane (the gradient row loads and record stores spread over
   // the lanes)
+  if (lane < n0) put(base + pos + lane, v1, g1, w1, slot1);
   for (int c0 = 0; c0 < wtot; c0 += kK3List) {
     if (c0 > 0) {
       __syncwarp();
@@ -259,21 +295,14 @@ __global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__re
     }
     __syncwarp();
     const int n = min(kK3List, wtot - c0);
-    for (int e = lane; e < n; e += 32) {
-      const uint2 it = list[e];
-      const int ti = t0 + (int)(it.x >> 7);
-      const int wi = ti >= tpw ? ti / tpw : 0;
-      const int w = w0 + wi, t = ti - wi * tpw;
-      const int64_t slot = (int64_t)t * kTile + (it.x & 127u);
-      const float *g = grads + ((int64_t)w * stride + slot) * kNdof;
+    for (int e = c0 == 0 ? lane + 32 : lane; e < n; e += 32) {
+      int w;
+      int64_t slot;
+      const float *g = rec_at(e, w, slot);
       float gg[kNdof];
 #pragma unroll
       for (int q = 0; q < kNdof; ++q) gg[q] = __ldcs(g + q);
-      float4 *dst = reinterpret_cast<float4 *>(ds.staging + base + pos + c0 + e);
-      dst[0] = make_float4(__uint_as_float(it.y), gg[0], gg[1], gg[2]);
-      dst[1] = make_float4(gg[3], gg[4], gg[5], gg[6]);
-      dst[2] = make_float4(gg[7], gg[8], __uint_as_float((unsigned)w),
-                           __uint_as_float((unsigned)local_to_global(slot, scene.rank, scene.world)));
+      put(base + pos + c0 + e, list[e].y, gg, w, slot);
     }
   }
 }
@@ -288,9 +317,17 @@ __global__ void __launch_bounds__(256) k_k3_place(int64_t n_parts, K3Scratch ks,
     if (base < 0) continue;
     const float4 *src = reinterpret_cast<const float4 *>(staging + base);
     float4 *dst = reinterpret_cast<float4 *>(out + dst0);
-    const int64_t nv = 3 * n, lim = 3 * (cap - dst0);
-    for (int64_t e = lane; e < nv; e += 32)
-      if (e < lim) dst[e] = __ldcs(src + e);
+    const int64_t nv = min(3 * n, 3 * (cap - dst0));
+    // four 16-B loads in flight per lane before their stores
+    for (int64_t e0 = lane; e0 < nv; e0 += 128) {
+      float4 x[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (e0 + 32 * k < nv) x[k] = __ldcs(src + e0 + 32 * k);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (e0 + 32 * k < nv) dst[e0 + 32 * k] = x[k];
+    }
   }
 }
 
