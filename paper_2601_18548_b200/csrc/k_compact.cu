@@ -31,21 +31,25 @@ __global__ void k_detect_init(unsigned long long *wp_key, unsigned long long *co
 }
 
 
-// ---- standalone K3 (A6-A8 over dense values): values read ONCE.
-// Stage kernel: a partition = kK3Warps warps x kK3TW consecutive tiles (128 slots, 4 per lane,
-// one 16-B streaming load each) of the flat (step, tile) order.  Each warp ballots its
-// tiles' actives (f - delta <= tau; dead slots hold +INF and never pass) and folds the
-// per-step minimum key (one atomicMin per step run); the CTA takes ONE staging allocation
-// for its actives (atomicAdd), the lanes with actives read their 36-B gradient rows and
-// write their records to the staging area in the partition's (step, slot) order, and the
-// partition's (base, count) -- plus, for a step starting inside it, that step's offset in
-// the partition -- go to the scratch.  No CTA waits on another (no look-back chain).
-// Place kernel: after a scan of the partition counts, every partition's records move from
-// staging to their final position (partitions are contiguous tile ranges, so partition order
-// = (wp, pt) order), and wp_offsets[w] = prefix of the partition holding step w's first tile
-// + that step's offset inside it.  HBM traffic: the values once, the active gradient rows,
-// the records twice (staging write + read) and once in the output.
-constexpr int kK3Warps = 8, kK3TW = 8, kK3Tiles = kK3Warps * kK3TW;
+// ---- standalone K3 (A6-A8 over dense values): values read ONCE, in a pure streaming pass.
+// A unit = kK3TW consecutive tiles of the flat (step, tile) order = one warp (128 slots, 4 per
+// lane, one 16-B streaming load each).
+// Mark kernel: each warp ballots its unit's actives (f - delta <= tau; dead slots hold +INF and
+// never pass), folds the per-step minimum key (one atomicMin per step run), and writes the
+// unit's active bitmap (one 32-bit word per lane: nibble i = tile i's 4 slots of the lane,
+// 128 B per unit) and its active count.  No shared memory, no barrier, no atomic round trip:
+// the warp's life is its loads and ~200 instructions, so the kernel streams the values at the
+// read rate of a plain reduction (tools/probes/read_bw.py).
+// Emit kernel, after a scan of the unit counts: one warp per unit ranks its actives from the
+// bitmap and writes each record (value, gradient row, ids) straight to its final position.
+// HBM traffic: the values once, the bitmaps twice (4 B per 128 values), per active the value
+// and the 36-B gradient row read (random 32-B sectors) and the 48-B record written.
+// (Measured alternatives: round 2's stage kernel allocating per-CTA staging
+// with an atomicAdd and writing records from the streaming warps, plus a place pass: 0.39 ms;
+// a decoupled look-back in the mark kernel: its prefix front lags the loads, 0.51 ms for mark
+// alone; a separate rank kernel writing pair indices + a thread-per-record gather: 0.40 ms.)
+constexpr int kK3TW = 8;           // tiles per unit (warp)
+constexpr int kK3MarkWarps = 4;    // warps per mark CTA
 
 // values of tile tw (0-based within step w) for this lane's 4 slots (+INF outside the scene)
 __device__ __forceinline__ float4 load_tile_values(const float *__restrict__ values, int64_t stride, int64_t lb,
@@ -65,14 +69,11 @@ __device__ __forceinline__ float4 load_tile_values(const float *__restrict__ val
 }
 
 struct K3Scratch {
-  int64_t *part_base;   // [n_parts] staging base of the partition (-1: staging overflow)
-  int64_t *part_cnt;    // [n_parts] actives of the partition
-  int64_t *part_pre;    // [n_parts + 1] exclusive prefix of part_cnt (+ total)
-  int64_t *wstart;      // [n_wp] (partition << 16 | offset of the step's first record in it)
+  int64_t *ucnt;       // [n_units] actives of the unit
+  int64_t *upre;       // [n_units + 1] exclusive prefix of ucnt (+ total)
+  uint32_t *bits;      // [n_units][32] active bitmaps
   int64_t *scan_tmp;
 };
-
-constexpr int kK3List = 128;  // per-warp record list (entries per pass)
 
 // The largest float x with fl(x - delta) <= tau (fp32, round to nearest): the active test
 // "f - delta <= tau" of K2b (R12) as one compare per value.  fl(x - delta) is non-decreasing
@@ -91,26 +92,21 @@ float k3_threshold(float delta, float tau) {
   }
 }
 
-__global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__restrict__ values,
-                                                            const float *__restrict__ grads, int64_t stride,
-                                                            int32_t n_wp, int32_t tpw, SceneView scene, float thr,
-                                                            DetectScratch ds, K3Scratch ks) {
-  __shared__ int32_t s_wcnt[kK3Warps];
-  __shared__ int64_t s_base;
-  __shared__ uint2 s_list[kK3Warps][kK3List];  // (tile << 7 | slot in the tile, value bits)
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t p = blockIdx.x;
+__global__ void __launch_bounds__(kK3MarkWarps * 32, 10) k_k3_mark(const float *__restrict__ values, int64_t stride,
+                                                                   int32_t n_wp, int32_t tpw, SceneView scene,
+                                                                   float thr, DetectScratch ds, K3Scratch ks) {
+  const int lane = threadIdx.x & 31;
+  const int64_t u = (int64_t)blockIdx.x * kK3MarkWarps + (threadIdx.x >> 5);
   const int64_t n_tiles = (int64_t)n_wp * tpw;
-  const int64_t T0 = p * kK3Tiles + (int64_t)warp * kK3TW;  // this warp's first flat tile
+  const int64_t T0 = u * kK3TW;  // this warp's first flat tile
+  if (T0 >= n_tiles) return;
   const int64_t lb = scene.local_bound;
   const int w0 = (int)(T0 / tpw);
   const int t0 = (int)(T0 - (int64_t)w0 * tpw);
-  const int nt = (int)max((int64_t)0, min((int64_t)kK3TW, n_tiles - T0));  // tiles of this warp
+  const int nt = (int)min((int64_t)kK3TW, n_tiles - T0);  // tiles of this warp
   // Fast path (all but ~1 in tpw / 8 warps): 8 full tiles inside one step -- straight loads
   // from one base address, no step change inside, no per-tile bounds checks.
   const bool fast = nt == kK3TW && t0 + kK3TW <= tpw;  // (uniform over the warp)
-  // ---- loads: the warp's tiles, all in flight.  Tile i is (w0 + wi, t0 + i - wi tpw) with wi =
-  // the number of step ends crossed (a warp's 8 tiles cross at most one when tpw >= 8)
   float4 v[kK3TW];
   if (fast) {
     const float4 *vb = reinterpret_cast<const float4 *>(values + (int64_t)w0 * stride + (int64_t)t0 * kTile) + lane;
@@ -124,9 +120,9 @@ __global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__re
       if (++t == tpw) { t = 0; ++w; }
     }
   }
-  // ---- per tile: this lane's 4 active flags (nibble i of `bits`), their count (8-bit fields
-  // of cnt_lo / cnt_hi for the one warp scan below), and the lane's running minimum of the step
-  uint32_t bits = 0u, cnt_lo = 0u, cnt_hi = 0u;
+  // per tile: this lane's 4 active flags (nibble i of `bits`) and the lane's running minimum of
+  // the step
+  uint32_t bits = 0u;
   const float inf = __int_as_float(0x7f800000);
   float lmin = inf;
   uint32_t lslot = 0u;
@@ -155,8 +151,6 @@ __global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__re
         const uint32_t b = (x.x <= thr ? 1u : 0u) | (x.y <= thr ? 2u : 0u) | (x.z <= thr ? 4u : 0u) |
                            (x.w <= thr ? 8u : 0u);
         bits |= b << (4 * i);
-        const uint32_t c = __popc(b);
-        if (i < 4) cnt_lo |= c << (8 * i); else cnt_hi |= c << (8 * (i - 4));
         const float m4 = fminf(fminf(x.x, x.y), fminf(x.z, x.w));
         if (m4 < lmin) {  // (rare after the first tiles of a step)
           lmin = m4;
@@ -174,184 +168,101 @@ __global__ void __launch_bounds__(kK3Warps * 32, 4) k_k3_stage(const float *__re
   };
   if (fast) process(std::true_type{});
   else process(std::false_type{});
-  // ---- one inclusive warp scan of the packed per-tile counts (fields <= 128 fit 8 bits)
-  uint32_t sc_lo = cnt_lo, sc_hi = cnt_hi;
+  ks.bits[u * 32 + lane] = bits;
+  const int wtot = (int)__reduce_add_sync(0xffffffffu, (unsigned)__popc(bits));
+  if (lane == 0) ks.ucnt[u] = wtot;
+}
+
+// Emit kernel (after a scan of the unit counts): one warp per unit -- its count, prefix and
+// bitmap word per lane are loaded together; an active (tile i, lane l, bit q) goes to
+//   upre[u] + (actives of tiles < i) + (actives of tile i in lanes < l) + (bits below q)
+// from one warp scan of the per-tile counts (8-bit fields, even / odd tiles: a tile has <= 128
+// actives, no carries); each lane then loads its actives' values and gradient rows and writes
+// their records in place.  A step starting in the unit gets its wp_offsets entry; the first
+// n_wp + 1 threads of the grid export the per-step min / argmin / keys and the total.
+__global__ void __launch_bounds__(256, 8) k_k3_emit(const float *__restrict__ values, const float *__restrict__ grads,
+                                                 int64_t stride, int32_t n_wp, int32_t tpw, int64_t n_units,
+                                                 SceneView scene, K3Scratch ks, gcdf_active_t *__restrict__ out,
+                                                 int64_t cap, const unsigned long long *__restrict__ keys,
+                                                 float *wp_min, int64_t *wp_argmin, int64_t *wp_key_out,
+                                                 int64_t *wp_offsets, int64_t *count) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gt <= n_wp) {
+    const int w = (int)gt;
+    if (w == n_wp) {
+      const int64_t tot = n_units > 0 ? ks.upre[n_units] : 0;
+      wp_offsets[n_wp] = tot;
+      *count = tot;
+    } else {
+      if (n_units == 0) wp_offsets[w] = 0;
+      const unsigned long long k = keys[w];
+      if (wp_min) wp_min[w] = k == ~0ull ? __int_as_float(0x7f800000) : unord_f32((unsigned)(k >> 32));
+      if (wp_argmin) wp_argmin[w] = k == ~0ull ? -1 : (int64_t)(k & 0xffffffffull);
+      if (wp_key_out) wp_key_out[w] = (int64_t)(k ^ 0x8000000000000000ull);
+    }
+  }
+  const int64_t u = gt >> 5;
+  if (u >= n_units) return;
+  const int64_t cnt = ks.ucnt[u];
+  const int64_t pre = ks.upre[u];
+  const uint32_t x = ks.bits[u * 32 + lane];
+  const int64_t T0 = u * kK3TW;
+  const int w0 = (int)(T0 / tpw);
+  const int t0 = (int)(T0 - (int64_t)w0 * tpw);
+  const int nt = (int)min((int64_t)kK3TW, (int64_t)n_wp * tpw - T0);
+  const bool starts = t0 == 0 || t0 + nt > tpw;  // (a step starts inside the unit: rare)
+  if (cnt == 0 && !starts) return;
+  uint32_t n = x - ((x >> 1) & 0x55555555u);  // popcount of each nibble = each tile
+  n = (n & 0x33333333u) + ((n >> 2) & 0x33333333u);
+  const uint32_t ne = n & 0x0f0f0f0fu, no = (n >> 4) & 0x0f0f0f0fu;  // tiles 0, 2, 4, 6 / 1, 3, 5, 7
+  uint32_t se = ne, so = no;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t a = __shfl_up_sync(0xffffffffu, sc_lo, o), b = __shfl_up_sync(0xffffffffu, sc_hi, o);
+    const uint32_t a = __shfl_up_sync(0xffffffffu, se, o), b = __shfl_up_sync(0xffffffffu, so, o);
     if (lane >= o) {
-      sc_lo += a;
-      sc_hi += b;
+      se += a;
+      so += b;
     }
   }
-  const uint32_t tot_lo = __shfl_sync(0xffffffffu, sc_lo, 31), tot_hi = __shfl_sync(0xffffffffu, sc_hi, 31);
-  const uint32_t ex_lo = sc_lo - cnt_lo, ex_hi = sc_hi - cnt_hi;
-  // tile i: the warp's actives before tile i (tile_pre) + this lane's exclusive prefix in tile i
-  int rk[kK3TW];
-  int wtot = 0;
-#pragma unroll
-  for (int i = 0; i < kK3TW; ++i) {
-    rk[i] = wtot + (int)(((i < 4 ? ex_lo : ex_hi) >> (8 * (i & 3))) & 0xffu);
-    wtot += (int)(((i < 4 ? tot_lo : tot_hi) >> (8 * (i & 3))) & 0xffu);
-  }
-  uint2 *list = s_list[warp];
-  // the warp's actives in (tile, slot) order into its list: entries [c0, c0 + kK3List) of the
-  // warp's ranks; each lane has at most 4 actives per tile, written by predicated stores (no
-  // per-active loop).  More than kK3List actives per warp (rare) take later passes that re-read
-  // the values (L2-resident).
-  auto fill = [&](int c0, const float4 *vv) {
-#pragma unroll
-    for (int i = 0; i < kK3TW; ++i) {
-      const uint32_t b = (bits >> (4 * i)) & 0xfu;
-      if (!b) continue;
-      int r = rk[i] - c0;
-      const float4 x = vv ? vv[i] : load_tile_values(values, stride, lb, w0 + (t0 + i) / tpw, (t0 + i) % tpw, lane);
-      const float xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if ((b >> k) & 1u) {
-          if (r >= 0 && r < kK3List) list[r] = make_uint2((uint32_t)(i * kTile + 4 * lane + k), __float_as_uint(xs[k]));
-          ++r;
-        }
-      }
-    }
-  };
-  if (bits) fill(0, v);
-  __syncwarp();
-  if (lane == 0) s_wcnt[warp] = wtot;
-  __syncthreads();
-  // the partition's staging allocation: thread 0 issues the atomicAdd here and consumes its
-  // result only after the lanes have issued their first gradient-row loads below, so its
-  // round trip overlaps theirs (the CTA barrier after it was the kernel's top stall)
-  int64_t agg = 0;
-  unsigned long long pb = 0ull;
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int j = 0; j < kK3Warps; ++j) agg += s_wcnt[j];
-    if (agg > 0) pb = atomicAdd(ds.counter, (unsigned long long)agg);
-  }
-  int64_t pos = 0;  // this warp's first record in the partition
-  for (int j = 0; j < warp; ++j) pos += s_wcnt[j];
-  // step starts inside this warp's tiles (lane i: tile i)
-  if (lane < nt) {
+  const uint32_t te = __shfl_sync(0xffffffffu, se, 31), to = __shfl_sync(0xffffffffu, so, 31);
+  se -= ne;
+  so -= no;
+  auto tile_tot = [&](int i) { return (int)((((i & 1) ? to : te) >> (8 * (i >> 1))) & 0xffu); };
+  if (starts && lane < nt) {
     const int ti = t0 + lane;
     const int wi = ti / tpw;
     if (ti - wi * tpw == 0) {
-      int pre = 0;
+      int tp = 0;
 #pragma unroll
       for (int i = 0; i < kK3TW; ++i)
-        if (i < lane) pre += (int)(((i < 4 ? tot_lo : tot_hi) >> (8 * (i & 3))) & 0xffu);
-      ks.wstart[w0 + wi] = (p << 20) | (pos + pre);
+        if (i < lane) tp += tile_tot(i);
+      wp_offsets[w0 + wi] = pre + tp;
     }
   }
-  // record e of the warp's list: its (step, slot) and gradient row
-  auto rec_at = [&](int e, int &w, int64_t &slot) -> const float * {
-    const uint2 it = list[e];
-    const int ti = t0 + (int)(it.x >> 7);
-    const int wi = ti >= tpw ? ti / tpw : 0;
-    w = w0 + wi;
-    slot = (int64_t)(ti - wi * tpw) * kTile + (it.x & 127u);
-    return grads + ((int64_t)w * stride + slot) * kNdof;
-  };
-  auto put = [&](int64_t dst_i, uint32_t vbits, const float (&gg)[kNdof], int w, int64_t slot) {
-    float4 *dst = reinterpret_cast<float4 *>(ds.staging + dst_i);
-    dst[0] = make_float4(__uint_as_float(vbits), gg[0], gg[1], gg[2]);
+  int tile_pre = 0, last = 0;
+  uint32_t y = x;
+  while (y) {
+    const int b = __ffs(y) - 1;
+    y &= y - 1u;
+    const int i = b >> 2, q = b & 3;
+    for (; last < i; ++last) tile_pre += tile_tot(last);
+    const int64_t d = pre + tile_pre + (int)((((i & 1) ? so : se) >> (8 * (i >> 1))) & 0xffu) +
+                      __popc((x >> (4 * i)) & ((1u << q) - 1u));
+    if (d >= cap) continue;
+    const int64_t T = T0 + i;
+    const int w = (int)(T / tpw);
+    const int64_t slot = (T - (int64_t)w * tpw) * kTile + 4 * lane + q;
+    const float *g = grads + ((int64_t)w * stride + slot) * kNdof;
+    const float f = __ldcs(values + (int64_t)w * stride + slot);
+    float gg[kNdof];
+#pragma unroll
+    for (int k = 0; k < kNdof; ++k) gg[k] = __ldcs(g + k);
+    float4 *dst = reinterpret_cast<float4 *>(out + d);
+    dst[0] = make_float4(f, gg[0], gg[1], gg[2]);
     dst[1] = make_float4(gg[3], gg[4], gg[5], gg[6]);
     dst[2] = make_float4(gg[7], gg[8], __uint_as_float((unsigned)w),
                          __uint_as_float((unsigned)local_to_global(slot, scene.rank, scene.world)));
-  };
-  // the lane's first record (list entry `lane`), loads in flight across the barrier
-  const int n0 = min(kK3List, wtot);
-  float g1[kNdof];
-  int w1 = 0;
-  int64_t slot1 = 0;
-  uint32_t v1 = 0u;
-  if (lane < n0) {
-    const float *g = rec_at(lane, w1, slot1);
-    v1 = list[lane].y;
-#pragma unroll
-    for (int q = 0; q < kNdof; ++q) g1[q] = __ldcs(g + q);
-  }
-  if (threadIdx.x == 0) {
-    int64_t base = (int64_t)pb;
-    if (agg > 0 && base + agg > ds.max_active) {
-      atomicOr(ds.counter + 1, 1ull);
-      base = -1;
-    }
-    ks.part_base[p] = base;
-    ks.part_cnt[p] = agg;
-    s_base = base;
-  }
-  __syncthreads();
-  const int64_t base = s_base;
-  if (base < 0 || wtot == 0) return;
-  // ---- records: one active per lane (the gradient row loads and record stores spread over
-  // the lanes)
-  if (lane < n0) put(base + pos + lane, v1, g1, w1, slot1);
-  for (int c0 = 0; c0 < wtot; c0 += kK3List) {
-    if (c0 > 0) {
-      __syncwarp();
-      fill(c0, nullptr);
-    }
-    __syncwarp();
-    const int n = min(kK3List, wtot - c0);
-    for (int e = c0 == 0 ? lane + 32 : lane; e < n; e += 32) {
-      int w;
-      int64_t slot;
-      const float *g = rec_at(e, w, slot);
-      float gg[kNdof];
-#pragma unroll
-      for (int q = 0; q < kNdof; ++q) gg[q] = __ldcs(g + q);
-      put(base + pos + c0 + e, list[e].y, gg, w, slot);
-    }
-  }
-}
-
-// one warp per partition: its records from staging to out[part_pre[p] ..]
-__global__ void __launch_bounds__(256) k_k3_place(int64_t n_parts, K3Scratch ks, const gcdf_active_t *__restrict__ staging,
-                                                  gcdf_active_t *__restrict__ out, int64_t cap) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < n_parts;
-       p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t base = ks.part_base[p], n = ks.part_cnt[p], dst0 = ks.part_pre[p];
-    if (base < 0) continue;
-    const float4 *src = reinterpret_cast<const float4 *>(staging + base);
-    float4 *dst = reinterpret_cast<float4 *>(out + dst0);
-    const int64_t nv = min(3 * n, 3 * (cap - dst0));
-    // four 16-B loads in flight per lane before their stores
-    for (int64_t e0 = lane; e0 < nv; e0 += 128) {
-      float4 x[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (e0 + 32 * k < nv) x[k] = __ldcs(src + e0 + 32 * k);
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (e0 + 32 * k < nv) dst[e0 + 32 * k] = x[k];
-    }
-  }
-}
-
-// per-step offsets from the partition prefix (+ the total) and the min / argmin / key export
-__global__ void k_k3_offsets(const unsigned long long *__restrict__ keys, int32_t n_wp, int64_t n_parts, K3Scratch ks,
-                             float *wp_min, int64_t *wp_argmin, int64_t *wp_key_out, int64_t *wp_offsets,
-                             int64_t *count) {
-  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w <= n_wp; w += gridDim.x * blockDim.x) {
-    if (w == n_wp) {
-      const int64_t tot = n_parts > 0 ? ks.part_pre[n_parts] : 0;
-      wp_offsets[n_wp] = tot;
-      *count = tot;
-      continue;
-    }
-    if (n_parts > 0) {
-      const int64_t ws = ks.wstart[w];
-      wp_offsets[w] = ks.part_pre[ws >> 20] + (ws & ((1ll << 20) - 1));
-    } else {
-      wp_offsets[w] = 0;
-    }
-    const unsigned long long k = keys[w];
-    if (wp_min) wp_min[w] = k == ~0ull ? __int_as_float(0x7f800000) : unord_f32((unsigned)(k >> 32));
-    if (wp_argmin) wp_argmin[w] = k == ~0ull ? -1 : (int64_t)(k & 0xffffffffull);
-    if (wp_key_out) wp_key_out[w] = (int64_t)(k ^ 0x8000000000000000ull);
   }
 }
 
@@ -561,37 +472,30 @@ cudaError_t launch_compact_dense(const float *values, const float *grads, int64_
                                  float *wp_min, int64_t *wp_argmin, int64_t *wp_key, int64_t *count,
                                  int64_t *k3_scratch, cudaStream_t s, int *n_launches) {
   const int64_t n_tiles = (int64_t)n_wp * tiles_per_wp;
-  const int64_t n_parts = (n_tiles + kK3Tiles - 1) / kK3Tiles;
+  const int64_t n_units = (n_tiles + kK3TW - 1) / kK3TW;
   K3Scratch ks;
-  ks.part_base = k3_scratch;
-  ks.part_cnt = ks.part_base + n_parts;
-  ks.part_pre = ks.part_cnt + n_parts;
-  ks.wstart = ks.part_pre + n_parts + 1;
-  ks.scan_tmp = ks.wstart + n_wp;
-  if (n_parts > 0) {
-    // (ds.counter[0] = the staging allocation counter and [1] the overflow flag, zeroed by k_detect_init)
-    k_k3_stage<<<(unsigned)n_parts, kK3Warps * 32, 0, s>>>(values, grads, stride, n_wp, tiles_per_wp, scene,
-                                                            k3_threshold(delta, tau), ds, ks);
+  ks.ucnt = k3_scratch;
+  ks.upre = ks.ucnt + n_units;
+  ks.bits = reinterpret_cast<uint32_t *>(ks.upre + n_units + 1);
+  ks.scan_tmp = ks.upre + n_units + 1 + 16 * n_units;
+  if (n_units > 0) {
+    k_k3_mark<<<(unsigned)((n_units + kK3MarkWarps - 1) / kK3MarkWarps), kK3MarkWarps * 32, 0, s>>>(
+        values, stride, n_wp, tiles_per_wp, scene, k3_threshold(delta, tau), ds, ks);
     ++*n_launches;
-    cudaError_t e = excl_scan(ks.part_cnt, n_parts, ks.part_pre, ks.part_pre + n_parts, ks.scan_tmp, s, n_launches);
+    cudaError_t e = excl_scan(ks.ucnt, n_units, ks.upre, ks.upre + n_units, ks.scan_tmp, s, n_launches);
     if (e != cudaSuccess) return e;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t blocks = std::min<int64_t>((n_parts + 7) / 8, (int64_t)sms * 8);
-    k_k3_place<<<(unsigned)blocks, 256, 0, s>>>(n_parts, ks, ds.staging, out, out_capacity);
-    ++*n_launches;
   }
-  k_k3_offsets<<<(n_wp + 256) / 256, 256, 0, s>>>(ds.wp_key, n_wp, n_parts, ks, wp_min, wp_argmin, wp_key, wp_offsets,
-                                                  count);
+  const int64_t eblocks = std::max<int64_t>((n_units * 32 + 255) / 256, (n_wp + 256) / 256);
+  k_k3_emit<<<(unsigned)eblocks, 256, 0, s>>>(values, grads, stride, n_wp, tiles_per_wp, n_units, scene, ks, out,
+                                              out_capacity, ds.wp_key, wp_min, wp_argmin, wp_key, wp_offsets, count);
   ++*n_launches;
   return cudaGetLastError();
 }
 
 // scratch (int64 elements) of the standalone K3 for n_wp steps of tiles_per_wp tiles
 int64_t k3_scratch_elems(int64_t n_wp, int64_t tiles_per_wp) {
-  const int64_t n_parts = (n_wp * tiles_per_wp + kK3Tiles - 1) / kK3Tiles;
-  return 3 * n_parts + 1 + n_wp + (n_parts + 1023) / 1024 + 1;
+  const int64_t n_units = (n_wp * tiles_per_wp + kK3TW - 1) / kK3TW;
+  return 2 * n_units + 1 + 16 * n_units + (n_units + 1023) / 1024 + 1;
 }
 
 

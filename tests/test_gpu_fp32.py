@@ -129,6 +129,41 @@ def test_compaction_exact_vs_own_values(c2):
     assert np.array_equal(fused["wp_min"].cpu().numpy(), vm.min(1))
 
 
+@pytest.mark.parametrize("frac", [0.3, 1.0])
+def test_compaction_dense_activity(c2, frac):
+    """K3 with a large active fraction (hundreds of actives per 8-tile unit, thousands per
+    32-unit emit batch, so the emit kernel's record list fills and drains in pieces): bit-exact
+    against a filter of the same values, offsets included; an output capacity below the count
+    gives CAPACITY with the first `capacity` records still exact."""
+    from paper_2601_18548_b200 import GcdfError
+    cfg, pts, q, m, full = c2
+    ctx = _ctx(cfg)
+    ctx.update_scene(pts)
+    v, g = ctx.query_values_grads(torch.from_numpy(q))
+    torch.cuda.synchronize()
+    vn, gn = v.cpu().numpy(), g.cpu().numpy()
+    W, lb = vn.shape
+    live = np.zeros(lb, bool)
+    live[: len(pts)] = True
+    tau = float(np.quantile(vn[:, : len(pts)], frac)) if frac < 1 else 1e30
+    act = (vn - np.float32(DELTA) <= np.float32(tau)) & live[None, :]
+    w_idx, s_idx = np.nonzero(act)
+    assert len(w_idx) > 0.25 * W * len(pts) * min(frac, 1.0)
+    dense = ctx.compact_dense(v, g, DELTA, tau)
+    a = records_np(dense)
+    assert dense["n"] == len(w_idx)
+    assert np.array_equal(a["wp"], w_idx) and np.array_equal(a["pt"], s_idx)
+    assert np.array_equal(a["value"], vn[w_idx, s_idx]) and np.array_equal(a["grad"], gn[w_idx, s_idx])
+    assert np.array_equal(dense["wp_offsets"].cpu().numpy(), np.searchsorted(w_idx, np.arange(W + 1), side="left"))
+    cap = len(w_idx) // 3 + 7
+    o = ctx.alloc_detect_outputs(W, cap)
+    with pytest.raises(GcdfError):
+        ctx.compact_dense(v, g, DELTA, tau, outputs=o)
+    b = records_np({"records": o["records"], "n": cap, "capacity": cap})
+    assert np.array_equal(b["wp"], w_idx[:cap]) and np.array_equal(b["pt"], s_idx[:cap])
+    assert np.array_equal(b["value"], vn[w_idx[:cap], s_idx[:cap]])
+
+
 def test_pairgen_transform(c1):
     """A2 standalone: p' = fl32(p - q_xy) exactly (one fp32 rounding of the f64 difference)."""
     cfg, pts, q, m, full = c1

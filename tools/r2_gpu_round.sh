@@ -8,7 +8,7 @@ python bench.py > $O/bench.json 2> $O/bench.err
 SHORT="--steps 2 --warmup 3 --no-variants --no-workloads --latency-calls 0 --partition-radius 0 --no-cpu-baseline --e2e-steps 1"
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file $O/launches.csv python bench.py $SHORT > $O/ncu_launch.log 2>&1
-for k in k_pairgen k_k3_stage k_mlp_tc; do
+for k in k_pairgen k_k3_mark k_mlp_tc; do
   ncu --set full --clock-control none --import-source on -k regex:"^${k}\b|${k}<|${k}\(" -c 1 -o $O/ncu_$k \
     python bench.py $SHORT > $O/ncu_$k.log 2>&1
 done
