@@ -70,6 +70,8 @@ constexpr int kDetectWarp = kEpiWarps + kSlots;   // warp 27: per-tile detect bo
 constexpr int kWarps = kDetectWarp + 1;
 constexpr int kThreads = kWarps * 32;             // 896
 constexpr int kEpiArrivals = kEpiPerSlot / 32;    // epi_done count: one arrival per epilogue warp
+constexpr int kRegsIssue = 24, kRegsEpi = 80;     // registers per thread after the split (see k_mlp_tc)
+static_assert(kEpiWarps * kRegsEpi + (kWarps - kEpiWarps) * kRegsIssue <= 65536 / 32, "register split");
 constexpr int kPhases = 12;                       // MMA phases per tile
 constexpr int kMasks = 5;                         // stored ReLU masks: layers 1..5
 constexpr int kWBytes = 5 * H * H * 2;            // 163,840
@@ -408,7 +410,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   const int64_t lb = a.scene.local_bound;
   const int64_t stride = kSlots * (int64_t)gridDim.x;
 
+  // Register split (setmaxnreg, per aligned 4-warp group): the MMA / detect group (warps
+  // 24..27) drops to kRegsIssue, the six epilogue groups rise to kRegsEpi (72 at launch:
+  // 896 threads share the 64K registers).
   if (warp >= kEpiWarps) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsIssue));
     // ============ three MMA warps: warp 24 + s issues slot s's phases, in CTA order ============
     // (the slot is a template argument, so that the issue loop's operands are warp-uniform to
     // the compiler and live in uniform registers)
@@ -421,6 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     __syncthreads();
     return;
   }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));
   const int s = warp >> 3;          // tile slot
   const int hh = (warp >> 2) & 1;   // column half: accumulator columns 32 hh + {0..31, 64..95}
   const int qd = warp & 3;          // TMEM lane quarter of this warp (warp % 4)
@@ -549,7 +556,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
   };
   const uint32_t one = S.one;
   uint32_t ph = 0u;
-  bool live_n = false;
   if ((int64_t)blockIdx.x * kSlots + s < n_tiles) {
     if (hh == 0) {
       int wn;
@@ -561,11 +567,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
       cp_async_commit();
       cp_async_wait_all();
     }
-    live_n = stage_a1(0, region(seq + 1u));  // phase 0's A region
+    stage_a1(0, region(seq + 1u));  // phase 0's A region
     hand_off(-1);
   }
   for (int64_t T = (int64_t)blockIdx.x * kSlots + s; T < n_tiles; T += stride, ++it) {
-    bool live = live_n;  // (half 1: re-read at phase 5 from S.slotn)
     float f = 0.f;
     // one MMA phase of the tile (compile-time phase number: every phase is its own straight
     // code, no run-time dispatch)
@@ -683,30 +688,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
           if (hh == 1) {
             f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
             const uint32_t sl = S.slotn[s][it & 1][row];
-            live = (sl >> 31) == 0u;
+            const bool live = (sl >> 31) == 0u;  // (padding rows: ~0; removed points: bit 31)
+            const int64_t slot = sl & 0x7fffffffu;
             if (!a.detect) {
               const int w = S.wtile[s][it & 1];
-              const int64_t slot = sl & 0x7fffffffu;
               if (slot < lb) a.values[(int64_t)w * lb + slot] = live ? f : __int_as_float(0x7f800000);
-            }
-          }
-          if (hh == 1 && a.detect) {
-            // A6/A7 (overlaps the tensor core): threshold and the warp's min key -> the detect warp
-            const int64_t slot = S.slotn[s][it & 1][row] & 0x7fffffffu;  // (live implies a real pair)
-            const bool act = live && (f - a.delta <= a.tau);
-            const unsigned bal = __ballot_sync(0xffffffffu, act);
-            // the warp's min key (ord f << 32 | id) by two 32-bit warp reductions (REDUX): the
-            // min of ord f, then the smallest id among the lanes that hold it
-            const unsigned khi = live ? ord_f32(f) : 0xffffffffu;
-            const unsigned mhi = __reduce_min_sync(0xffffffffu, khi);
-            const unsigned klo = (live && khi == mhi) ? (unsigned)local_to_global(slot, a.scene.rank, a.scene.world)
-                                                      : 0xffffffffu;
-            const unsigned mlo = __reduce_min_sync(0xffffffffu, klo);
-            const unsigned long long key = ((unsigned long long)mhi << 32) | mlo;
-            if (lane == 0) {
-              S.act[s][qd] = bal;
-              S.kmin[s][qd] = key;
-              mbar_arrive(&S.det_in[s]);
+            } else {
+              // A6/A7 (overlaps the tensor core): threshold and the warp's min key -> the detect warp
+              const bool act = live && (f - a.delta <= a.tau);
+              const unsigned bal = __ballot_sync(0xffffffffu, act);
+              // the warp's min key (ord f << 32 | id) by two 32-bit warp reductions (REDUX): the
+              // min of ord f, then the smallest id among the lanes that hold it
+              const unsigned khi = live ? ord_f32(f) : 0xffffffffu;
+              const unsigned mhi = __reduce_min_sync(0xffffffffu, khi);
+              const unsigned klo = (live && khi == mhi) ? (unsigned)local_to_global(slot, a.scene.rank, a.scene.world)
+                                                        : 0xffffffffu;
+              const unsigned mlo = __reduce_min_sync(0xffffffffu, klo);
+              const unsigned long long key = ((unsigned long long)mhi << 32) | mlo;
+              if (lane == 0) {
+                S.act[s][qd] = bal;
+                S.kmin[s][qd] = key;
+                mbar_arrive(&S.det_in[s]);
+              }
             }
           }
         }
@@ -724,13 +727,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
         const float2 pp_t = pp;  // (SE(2)) p'_xy of this tile; stage_a1 overwrites pp
         if (T + stride < n_tiles) {
           if (hh == 0) cp_async_wait_all();  // this thread's point of the next tile (phase 5)
-          live_n = stage_a1((it + 1) & 1, tD);
+          stage_a1((it + 1) & 1, tD);
         }
         hand_off(p);
         if (hh == 0) {
           f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
           const int w = S.wtile[s][it & 1];
-          const int64_t slot = S.slotn[s][it & 1][row] & 0x7fffffffu;
+          const uint32_t sl = S.slotn[s][it & 1][row];
+          const bool live = (sl >> 31) == 0u;
+          const int64_t slot = sl & 0x7fffffffu;
           float gq[kNdof];
           gq[0] = a.tgrad ? __uint_as_float(r[3]) : -__uint_as_float(r[0]);
           gq[1] = a.tgrad ? __uint_as_float(r[4]) : -__uint_as_float(r[1]);

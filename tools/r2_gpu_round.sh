@@ -1,5 +1,5 @@
 #!/bin/bash
-# one GPU call: tests, bench, launch list, ncu --set full of K1 / K3 / K2b (profiles evidence)
+# one GPU call: tests, bench, launch list, ncu --set full of K1 / K3 / K2b / K2c (profiles evidence)
 set -x
 O=gpurun_out/$1
 mkdir -p $O
@@ -12,4 +12,6 @@ for k in k_pairgen k_k3_mark k_mlp_tc; do
   ncu --set full --clock-control none --import-source on -k regex:"^${k}\b|${k}<|${k}\(" -c 1 -o $O/ncu_$k \
     python bench.py $SHORT > $O/ncu_$k.log 2>&1
 done
+ncu --set full --clock-control none --import-source on -k regex:"k_mlp_tc3" -c 1 -o $O/ncu_k_mlp_tc3 \
+  python bench.py $SHORT --precision fp16x3 > $O/ncu_k_mlp_tc3.log 2>&1
 ls -la $O
