@@ -38,15 +38,16 @@ using namespace tc;
 constexpr int H = 128;
 constexpr int kEpiWarps = 16;                  // warp w: TMEM lane quarter w % 4, unit quarter w / 4
 constexpr int kThreads = (kEpiWarps + 1) * 32; // + one MMA warp
-constexpr int kEpi = kEpiWarps * 32;           // epi_done arrivals per phase
+constexpr int kEpi = kEpiWarps * 32;           // epilogue threads
+constexpr int kEpiHalf = kEpi / 2;             // epi_done[h] arrivals per phase (unit quarters 2h, 2h + 1)
 constexpr int kPhases = 12;
 constexpr int kWBytes = 5 * H * H * 2;
 constexpr int kW1tBytes = 16 * H * 2;
 constexpr int kB1Bytes = 32 * H * 2;
 constexpr int kBextBytes = 16 * H * 2;
 constexpr uint32_t kColH = 128, kColX = 448, kColOnes = 464, kColE6 = 448;
-constexpr uint32_t kIdescFwd = idesc_f16kind(128, 128, false, true);
-constexpr uint32_t kIdescBwd = idesc_f16kind(128, 128, true, true);
+constexpr uint32_t kIdescFwd = idesc_f16kind(128, 64, false, true);  // (output halves: N = 64)
+constexpr uint32_t kIdescBwd = idesc_f16kind(128, 64, true, true);
 constexpr uint32_t kIdescFin = idesc_f16kind(128, 16, false, true);
 
 struct __align__(1024) SmemSP {
@@ -60,8 +61,8 @@ struct __align__(1024) SmemSP {
   float qn[2][12];              // [tile parity] q row of the tile
   int wtile[2];                 // [tile parity] step (waypoint) of the tile
   uint32_t slotn[2][H];         // [tile parity][row] local scene slot (~0: padding)
-  uint64_t mma_done;
-  uint64_t epi_done;
+  uint64_t mma_done[2];  // [output half]
+  uint64_t epi_done[2];
   unsigned act[4];
   unsigned long long kmin[4];
   int sbase;
@@ -128,29 +129,71 @@ DEVI float2 unpack_h2(uint32_t u) {
   return __half22float2(h);
 }
 
-// UMMAs of phase p (one elected lane of the converged MMA warp), committed to bar
-DEVI void issue_phase(int p, uint32_t tb, uint32_t sw, uint32_t sw1t, uint32_t sb1, uint32_t sbx, uint64_t *bar) {
-  const uint32_t d = tb;
-  if (p == 0) {  // layer 1: K = 32 split operands (bias included), A = x
+// UMMAs of phase p by output half (one elected lane of the converged MMA warp): half h writes
+// accumulator columns 64 h .. 64 h + 63 (N = 64, B rows / columns 64 h ..) and is committed to
+// mma_done[h], so the epilogue of half 0 starts while the tensor core runs half 1.  Half 0's
+// first four K steps read only the units half 0's epilogue wrote (A columns of units 0..63):
+// they are issued after epi_done[0]; the rest of the phase after epi_done[1] (wait_half(h)).
+template <typename WaitHalf>
+DEVI void issue_phase(int p, uint32_t tb, uint32_t sw, uint32_t sw1t, uint32_t sb1, uint32_t sbx, uint64_t *done,
+                      WaitHalf &&wait_half) {
+  if (p == 0) {  // layer 1: K = 32 split operands (bias included), A = x (written by half 0)
+    wait_half(0);
 #pragma unroll
-    for (int k = 0; k < 2; ++k)
-      mma_ts_elect(d, tb + kColX + 8u * k, sdesc_nosw(sb1 + k * 2 * 2048, 2048, 128), kIdescFwd, k > 0);
-  } else if (p < 6) {  // layer l = p + 1: D = h_{l-1} W_l^T + ones x bias
-    const uint32_t av = tb + kColH + 64u * (uint32_t)(p - 1);
-    const uint32_t wb = sw + (uint32_t)(p - 1) * (H * H * 2);
-    umma8_kmajor_elect(d, av, sdesc_sw128(wb, 16, 1024), kIdescFwd, 0u);  // (one asm block, tc_ptx.h)
-    mma_ts_elect(d, tb + kColOnes, sdesc_nosw(sbx + (uint32_t)(p - 1) * kBextBytes, 2048, 128), kIdescFwd, 1u);
-  } else if (p < 11) {  // backward through layer l = 12 - p: D = e_l W_l (B MN-major)
-    const uint32_t av = p == 6 ? tb + kColE6 : tb + kColH + 64u * (uint32_t)(11 - p);
-    const uint32_t wb = sw + (uint32_t)(10 - p) * (H * H * 2);
-    umma8_mnmajor_elect(d, av, sdesc_sw128(wb, 16384, 1024), kIdescBwd, 0u);
-  } else {  // g0 = e1 W1 (N = 16 rows of W1^T)
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1) wait_half(1);
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        mma_ts_elect(tb + 64u * h, tb + kColX + 8u * k, sdesc_nosw(sb1 + k * 2 * 2048 + 1024u * h, 2048, 128), kIdescFwd,
+                     k > 0);
+      commit_elect(&done[h]);
+    }
+  } else if (p < 11) {
+    const bool fwd = p < 6;
+    uint32_t av;
+    uint64_t b[2];
+    if (fwd) {  // layer l = p + 1: D = h_{l-1} W_l^T + ones x bias (B K-major: output rows 64 h ..)
+      av = tb + kColH + 64u * (uint32_t)(p - 1);
+      const uint32_t wb = sw + (uint32_t)(p - 1) * (H * H * 2);
+      b[0] = sdesc_sw128(wb, 16, 1024);
+      b[1] = sdesc_sw128(wb + 8192u, 16, 1024);
+    } else {  // backward through layer l = 12 - p: D = e_l W_l (B MN-major: N chunk h)
+      av = p == 6 ? tb + kColE6 : tb + kColH + 64u * (uint32_t)(11 - p);
+      const uint32_t wb = sw + (uint32_t)(10 - p) * (H * H * 2);
+      b[0] = sdesc_sw128(wb, 16384, 1024);
+      b[1] = sdesc_sw128(wb + 16384u, 16384, 1024);
+    }
+    const uint32_t id = fwd ? kIdescFwd : kIdescBwd;
+    const uint32_t kstep = fwd ? 2u : 128u;  // B descriptor step per K step inside a 64-K chunk
+    wait_half(0);
+    // half 0, K steps 0..3 (units 0..63 of A)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) mma_ts_elect(tb, av + 8u * k, b[0] + (uint64_t)(kstep * k), id, k > 0);
+    wait_half(1);
+    // half 0, K steps 4..7 (K-major: the second 64-K chunk at + 16 KB; MN-major: + k 2 KB)
+#pragma unroll
+    for (int k = 4; k < 8; ++k)
+      mma_ts_elect(tb, av + 8u * k, b[0] + (uint64_t)(fwd ? 1024u + 2u * (k - 4) : 128u * k), id, 1u);
+    if (fwd) mma_ts_elect(tb, tb + kColOnes, sdesc_nosw(sbx + (uint32_t)(p - 1) * kBextBytes, 2048, 128), id, 1u);
+    commit_elect(&done[0]);
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      mma_ts_elect(d, tb + kColH + 8u * k, sdesc_sw128(sw1t + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin,
+      mma_ts_elect(tb + 64u, av + 8u * k, b[1] + (uint64_t)(fwd ? (k >> 2) * 1024u + 2u * (k & 3) : 128u * k), id,
                    k > 0);
+    if (fwd)
+      mma_ts_elect(tb + 64u, tb + kColOnes, sdesc_nosw(sbx + (uint32_t)(p - 1) * kBextBytes + 1024u, 2048, 128), id,
+                   1u);
+    commit_elect(&done[1]);
+  } else {  // g0 = e1 W1 (N = 16 rows of W1^T): needs all of e1
+    wait_half(0);
+    wait_half(1);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      mma_ts_elect(tb, tb + kColH + 8u * k, sdesc_sw128(sw1t + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin,
+                   k > 0);
+    commit_elect(&done[0]);
+    commit_elect(&done[1]);
   }
-  commit_elect(bar);
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_sp(const WeightsBF16 W, const QueryArgs a) {
@@ -174,8 +217,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_sp(const WeightsBF16 W, 
     tmem_relinquish();
   }
   if (tid == 32) {
-    mbar_init(&S.mma_done, 1);
-    mbar_init(&S.epi_done, kEpi);
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&S.mma_done[h], 1);
+      mbar_init(&S.epi_done[h], kEpiHalf);
+    }
     fence_barrier_init();
   }
   const int64_t n_tiles = query_tiles(a);
@@ -190,15 +235,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_sp(const WeightsBF16 W, 
   if (warp == kEpiWarps) {
     // ===================== MMA warp ================================================
     const uint32_t sw = smem_u32(S.w), sw1t = smem_u32(S.w1t), sb1 = smem_u32(S.b1), sbx = smem_u32(S.bext);
-    uint32_t ph = 0u;
+    uint32_t ph = 0u;  // bit h: parity of epi_done[h]
+    auto wait_half = [&](int h) {
+      mbar_wait(&S.epi_done[h], (ph >> h) & 1u);
+      ph ^= 1u << h;
+      fence_after();
+    };
     for (int64_t T = blockIdx.x; T < n_tiles; T += stride) {
 #pragma unroll 1
-      for (int p = 0; p < kPhases; ++p) {
-        mbar_wait(&S.epi_done, ph);
-        ph ^= 1u;
-        fence_after();
-        issue_phase(p, tbase, sw, sw1t, sb1, sbx, &S.mma_done);
-      }
+      for (int p = 0; p < kPhases; ++p) issue_phase(p, tbase, sw, sw1t, sb1, sbx, S.mma_done, wait_half);
     }
     __syncwarp();
     fence_before();
@@ -215,10 +260,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_sp(const WeightsBF16 W, 
   const uint32_t tD = tL + (uint32_t)u0;
   auto tH = [&](int l) { return tL + kColH + 64u * (uint32_t)(l - 1) + 16u * (uint32_t)cq; };  // h_l / e_l, l = 1..5
 
+  const int half = cq >> 1;     // output half of this warp's units
   auto hand_off = [&]() {
     wait_st();
     fence_before();
-    mbar_arrive(&S.epi_done);
+    mbar_arrive(&S.epi_done[half]);
   };
   // point of row `row` of tile TT -> S.ptn[row] (cp.async), its slot -> S.slotn[par][row];
   // warp 0 also fetches the tile's q row
@@ -295,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_sp(const WeightsBF16 W, 
     int pend_cnt = 0;
 #pragma unroll 1
     for (int p = 0; p < kPhases; ++p) {
-      mbar_wait(&S.mma_done, ph);
+      mbar_wait(&S.mma_done[half], ph);
       ph ^= 1u;
       fence_after();
       if (p < 5) {
