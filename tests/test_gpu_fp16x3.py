@@ -211,3 +211,36 @@ def test_bf16x3_detect(c2x):
     a = records_np(ctx.compact_dense(v, g, DELTA, tau))
     for k in ("wp", "pt", "value", "grad"):
         assert np.array_equal(a[k], gpu[k]), k
+
+
+@pytest.mark.parametrize("prec", ["fp16x3", "bf16x3"])
+@pytest.mark.parametrize("n_wp,n_pts", [(1, 100), (2, 200), (3, 129), (7, 1000), (11, 5200)])
+def test_x3_tile_count_edge_cases(c2x, prec, n_wp, n_pts):
+    """Tile counts around the three tiles a K2c CTA keeps in flight: one tile (slots 1, 2 pass
+    their turns), rounds with one or two real slots (the round's last real slot streams the
+    next weight run), and (11 x 5200: 451 tiles on 148 CTAs) a second round in which one CTA
+    has a single tile.  Dense values / gradients vs the exact oracle at the path's tolerance,
+    and the fused detect bit-identical to dense query + standalone compaction."""
+    cfg, pts, q, m, full = c2x
+    P = pts[:n_pts]
+    qq = q[:, :n_wp]
+    ctx = _ctx(cfg) if prec == "fp16x3" else _ctx_b(cfg)
+    ctx.update_scene(P)
+    qt = torch.from_numpy(qq)
+    v, g = ctx.query_values_grads(qt)
+    torch.cuda.synchronize()
+    vn, gn = v.cpu().numpy()[:, :n_pts], g.cpu().numpy()[:, :n_pts]
+    ex = m.eval(P, qq.reshape(-1, 9), want_kappa=True, nthreads=NT)
+    if prec == "fp16x3":
+        check_fp32_dense(vn, gn, ex["f"], ex["g"], ex["kappa"], what=f"fp16x3 {n_wp}x{n_pts}")
+    else:
+        assert np.abs(vn - ex["f"]).max() <= 1e-3
+        gd = np.abs(np.linalg.norm(gn, axis=-1) - np.linalg.norm(ex["g"], axis=-1))
+        assert not (gd[ex["kappa"] > 1e-3] > 5e-2).any()
+    assert np.all(np.isinf(v.cpu().numpy()[:, n_pts:]))
+    tau = float(np.median(ex["f"])) - DELTA
+    a = records_np(ctx.compact_dense(v, g, DELTA, tau))
+    b = records_np(ctx.detect_active_set(qt, DELTA, tau))
+    assert len(b["wp"]) > 0
+    for k in ("wp", "pt", "value", "grad"):
+        assert np.array_equal(a[k], b[k]), k
