@@ -264,7 +264,7 @@ def main():
     # Scene-update inputs of every step (A9: 200 removes + 200 adds of a moved box), made
     # before any clock starts: adds are points of a randomly moved clutter box, removals
     # disjoint sets of the initially live ids (valid whatever ids the adds reuse).
-    e2e_steps = a.e2e_steps or max(1, min(a.steps, 5))
+    e2e_steps = a.e2e_steps or max(1, a.steps)  # (as many steps as the device-timed region: the same thermal / power-cap window length)
     n_upd = a.warmup + a.steps + e2e_steps
     gen = np.random.default_rng([cfg.seed, 7])
     n_chg = int(max(1, min(200, cfg.M // (2 * n_upd))))  # 200 (C4 dynamics) unless the scene is tiny
