@@ -27,6 +27,8 @@
 // split hi/lo operands (~fp32), as in K2b.
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "gcdf_internal.h"
 #include "tc_ptx.h"
 
@@ -339,8 +341,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_sp(const WeightsBF16 W, 
     int ridx = -1;
     unsigned long long pend_b = 0ull;
     int pend_cnt = 0;
-#pragma unroll 1
-    for (int p = 0; p < kPhases; ++p) {
+    // one phase of the tile (compile-time phase number, as in K2b: every phase is its own
+    // straight code, no run-time dispatch)
+    auto phase = [&](auto pc) {
+      constexpr int p = decltype(pc)::value;
       mbar_wait(&S.mma_done[half], ph);
       ph ^= 1u;
       fence_after();
@@ -505,7 +509,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_sp(const WeightsBF16 W, 
           }
         }
       }
-    }
+    };
+    phase(std::integral_constant<int, 0>{});
+    phase(std::integral_constant<int, 1>{});
+    phase(std::integral_constant<int, 2>{});
+    phase(std::integral_constant<int, 3>{});
+    phase(std::integral_constant<int, 4>{});
+    phase(std::integral_constant<int, 5>{});
+    phase(std::integral_constant<int, 6>{});
+    phase(std::integral_constant<int, 7>{});
+    phase(std::integral_constant<int, 8>{});
+    phase(std::integral_constant<int, 9>{});
+    phase(std::integral_constant<int, 10>{});
+    phase(std::integral_constant<int, 11>{});
   }
   fence_before();
   __syncthreads();
