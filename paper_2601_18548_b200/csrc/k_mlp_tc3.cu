@@ -525,7 +525,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
   const uint32_t one = S.one;
   uint32_t ph = 0u;
   int it = 0;
-  bool live_n = false;
   if ((int64_t)blockIdx.x * kSlots + s < n_tiles) {
     if (hh == 0) {
       int wn;
@@ -537,11 +536,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
       cp_async_commit();
       cp_async_wait_all();
     }
-    live_n = stage_a1(0, region(seq + 1u));
+    stage_a1(0, region(seq + 1u));
     hand_off();
   }
   for (int64_t T = (int64_t)blockIdx.x * kSlots + s; T < n_tiles; T += stride, ++it) {
-    bool live = live_n;
     float f = 0.f;
     auto phase = [&](auto pc) {
       constexpr int p = decltype(pc)::value;
@@ -655,7 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
           if (hh == 1) {
             f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
             const uint32_t sl = S.slotn[s][it & 1][row];
-            live = (sl >> 31) == 0u;
+            const bool live = (sl >> 31) == 0u;  // (padding rows: ~0; removed points: bit 31)
             if (!a.detect) {
               const int w = S.wtile[s][it & 1];
               const int64_t slot = sl & 0x7fffffffu;
@@ -690,13 +688,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
         const float2 pp_t = pp;
         if (T + stride < n_tiles) {
           if (hh == 0) cp_async_wait_all();
-          live_n = stage_a1((it + 1) & 1, tD);
+          stage_a1((it + 1) & 1, tD);
         }
         hand_off();
         if (hh == 0) {
           f = S.fpart[s][0][row] + S.fpart[s][1][row] + W.b7;
           const int w = S.wtile[s][it & 1];
-          const int64_t slot = S.slotn[s][it & 1][row] & 0x7fffffffu;
+          const uint32_t sl = S.slotn[s][it & 1][row];
+          const bool live = (sl >> 31) == 0u;
+          const int64_t slot = sl & 0x7fffffffu;
           float gq[kNdof];
           gq[0] = a.tgrad ? __uint_as_float(r[3]) : -__uint_as_float(r[0]);
           gq[1] = a.tgrad ? __uint_as_float(r[4]) : -__uint_as_float(r[1]);
