@@ -428,9 +428,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
     return;
   }
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));
-  const int s = warp >> 3;          // tile slot
-  const int hh = (warp >> 2) & 1;   // column half: accumulator columns 32 hh + {0..31, 64..95}
-  const int qd = warp & 3;          // TMEM lane quarter of this warp (warp % 4)
+  // (the warp index through a lane-0 shuffle: warp-uniform to the compiler, so the TMEM
+  // addresses derived from it live in uniform registers -- no R2UR before each TMEM load / store)
+  const int ew = __shfl_sync(0xffffffffu, warp, 0);
+  const int s = ew >> 3;            // tile slot
+  const int hh = (ew >> 2) & 1;     // column half: accumulator columns 32 hh + {0..31, 64..95}
+  const int qd = ew & 3;            // TMEM lane quarter of this warp (warp % 4)
   const int row = qd * 32 + lane;   // pair within the tile = TMEM lane
   const uint32_t tL = tbase + ((uint32_t)(qd * 32) << 16) + 32u * hh;  // region 0, this lane quarter, column half
   uint32_t seq = (uint32_t)s;       // CTA phase index of the slot's next MMA phase
