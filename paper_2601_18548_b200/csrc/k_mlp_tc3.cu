@@ -424,9 +424,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
   }
 
   // ===================== epilogue warps =====================
-  const int s = warp >> 3;
-  const int hh = (warp >> 2) & 1;
-  const int qd = warp & 3;
+  // (the warp index through a lane-0 shuffle: warp-uniform to the compiler, so the TMEM
+  // addresses derived from it live in uniform registers, as in K2b)
+  const int ew = __shfl_sync(0xffffffffu, warp, 0);
+  const int s = ew >> 3;
+  const int hh = (ew >> 2) & 1;
+  const int qd = ew & 3;
   const int row = qd * 32 + lane;
   const uint32_t tL = tbase + ((uint32_t)(qd * 32) << 16) + 32u * hh;
   uint32_t seq = (uint32_t)s;

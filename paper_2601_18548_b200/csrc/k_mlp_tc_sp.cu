@@ -254,8 +254,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_sp(const WeightsBF16 W, 
   }
 
   // ===================== epilogue warps ===============================================
-  const int qd = warp & 3;      // TMEM lane quarter (warp % 4)
-  const int cq = warp >> 2;     // unit quarter: units 32 cq .. 32 cq + 31
+  // (the warp index through a lane-0 shuffle: warp-uniform to the compiler, so the TMEM
+  // addresses derived from it live in uniform registers, as in K2b)
+  const int ew = __shfl_sync(0xffffffffu, warp, 0);
+  const int qd = ew & 3;      // TMEM lane quarter (warp % 4)
+  const int cq = ew >> 2;     // unit quarter: units 32 cq .. 32 cq + 31
   const int row = qd * 32 + lane;
   const int u0 = 32 * cq;
   const uint32_t tL = tbase + ((uint32_t)(qd * 32) << 16);
