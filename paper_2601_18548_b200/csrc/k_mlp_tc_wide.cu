@@ -335,13 +335,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
       fence_after();
       if (p < 5) {
         // ---- forward layer l = p + 1: h = ReLU(z) -> A (fp16), 1-bit masks -> smem ----
-        uint32_t rb[2][16], m = 0u;
-        ld16(tD, rb[0]);
+        uint32_t rb[4][16], m = 0u;
+        // all four chunks' TMEM loads in flight at once, one wait (K2w has the registers)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ld16(tD + 16 * c, rb[c]);
         wait_ld();
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          if (c < 3) ld16(tD + 16 * (c + 1), rb[(c + 1) & 1]);
-          const uint32_t *rr = rb[c & 1];
+          const uint32_t *rr = rb[c];
           uint32_t pk[8];
 #pragma unroll
           for (int j = 0; j < 16; j += 4) {
@@ -354,7 +355,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
             mk[(p * 2 + (c >> 1)) * kEpi] = m;
             m = 0u;
           }
-          if (c < 3) wait_ld();
         }
         hand_off();
       } else if (p == 5) {
@@ -364,14 +364,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
         // quarter): direct constant-bank operands, no shared-memory loads (as in K2b)
         auto layer6 = [&](auto u0c) {
           constexpr int U0 = decltype(u0c)::value;
-          uint32_t rb[2][16];
-          ld16(tD, rb[0]);
+          uint32_t rb[4][16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) ld16(tD + 16 * c, rb[c]);
           wait_ld();
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const int cb = 16 * c;
-            if (c < 3) ld16(tD + cb + 16, rb[(c + 1) & 1]);
-            const uint32_t *rr = rb[c & 1];
+            const uint32_t *rr = rb[c];
             uint32_t pk[8];
 #pragma unroll
             for (int j = 0; j < 16; j += 4) {
@@ -386,7 +386,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
               fa[3] = fmaf(W.w7half_p[u + 3], z3 + fabsf(z3), fa[3]);
             }
             st8(tA(p) + cb / 2, pk);
-            if (c < 3) wait_ld();
           }
         };
         switch (cq) {
@@ -410,13 +409,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
         // ---- backward: g_{l-1} = D; e_{l-1} = g (.) 1[z_{l-1} > 0] -> A ----
         const int mi = 10 - p;
         const uint32_t mw[2] = {mk[(mi * 2) * kEpi], mk[(mi * 2 + 1) * kEpi]};
-        uint32_t rb[2][16];
-        ld16(tD, rb[0]);
+        uint32_t rb[4][16];
+        // all four chunks' TMEM loads in flight at once, one wait (K2w has the registers)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ld16(tD + 16 * c, rb[c]);
         wait_ld();
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          if (c < 3) ld16(tD + 16 * (c + 1), rb[(c + 1) & 1]);
-          const uint32_t *rr = rb[c & 1];
+          const uint32_t *rr = rb[c];
           uint32_t pk[8];
 #pragma unroll
           for (int j = 0; j < 16; j += 4) {
@@ -426,7 +426,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
             pk[(j >> 1) + 1] = pack_f16(__uint_as_float(rr[j + 2]), __uint_as_float(rr[j + 3])) & hi;
           }
           st8(tA(p) + 8 * c, pk);
-          if (c < 3) wait_ld();
         }
         hand_off();
         if (p == 6 && cq == 0 && a.detect) {
