@@ -167,9 +167,6 @@ DEVI uint32_t mask_group_f(uint32_t pk01, uint32_t pk23, int k, uint32_t one) {
   const uint32_t x = prmt(add7fff(pk01, one), add7fff(pk23, one), 0x7531u);
   return (x >> k) & (0x80808080u >> k);
 }
-// 0xffff half-word masks of the nonzero halves of a packed pair of non-negative 16-bit
-// values (bit 15 of v + 0x7fff is set iff v != 0; sign-replicate bytes 1 and 3)
-DEVI uint32_t nz_halves(uint32_t pk, uint32_t one) { return prmt(add7fff(pk, one), 0u, 0xbb99u); }
 
 // UMMAs of MMA phase p: accumulator in the region at TMEM address d, A operand in the region
 // at av (the slot's previous phase's region).  Executed by the whole (converged) MMA warp;
@@ -639,8 +636,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc(const WeightsBF16 W, con
               const int u = U0 + cb + j;
               const float z0 = __uint_as_float(rr[j]), z1 = __uint_as_float(rr[j + 1]);
               const float z2 = __uint_as_float(rr[j + 2]), z3 = __uint_as_float(rr[j + 3]);
-              pk[j >> 1] = W.w7h_p[u / 2] & nz_halves(pack2_relu<F16>(z0, z1), one);
-              pk[(j >> 1) + 1] = W.w7h_p[u / 2 + 1] & nz_halves(pack2_relu<F16>(z2, z3), one);
+              // e6 = w7 (.) 1[z6 >= 0]: halfword masks from the sign bytes of the fp32 z (one PRMT
+              // with sign replication per pair, then w7 & ~sign): the oracle's 1[z > 0] up to
+              // z6 = +0 exactly (a kink, R17)
+              pk[j >> 1] = W.w7h_p[u / 2] & ~prmt(rr[j], rr[j + 1], 0xffbbu);
+              pk[(j >> 1) + 1] = W.w7h_p[u / 2 + 1] & ~prmt(rr[j + 2], rr[j + 3], 0xffbbu);
               // (w7 / 2) (z + |z|) = w7 ReLU(z) exactly (z + |z| = 2 ReLU(z), halving is exact)
               fa[0] = fmaf(W.w7half_p[u], z0 + fabsf(z0), fa[0]);
               fa[1] = fmaf(W.w7half_p[u + 1], z1 + fabsf(z1), fa[1]);
