@@ -138,7 +138,6 @@ DEVI uint32_t mask_group_f(uint32_t pk01, uint32_t pk23, int k, uint32_t one) {
   const uint32_t x = prmt(add7fff(pk01, one), add7fff(pk23, one), 0x7531u);
   return (x >> k) & (0x80808080u >> k);
 }
-DEVI uint32_t nz_halves(uint32_t pk, uint32_t one) { return prmt(add7fff(pk, one), 0u, 0xbb99u); }
 
 // run (streamed-layer use) of phase p of the CTA's tile round t (phases 1..10), and its layer
 DEVI int run_of(int t, int p) { return 8 * t + (p <= 5 ? p - 1 : (p == 6 ? 4 : p - 2)); }
@@ -600,8 +599,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc3(const WeightsBF16 W, co
             const uint2 wl = *reinterpret_cast<const uint2 *>(S.w7lo + (cb + j) / 2);
             const float z0 = __uint_as_float(rr[j]), z1 = __uint_as_float(rr[j + 1]);
             const float z2 = __uint_as_float(rr[j + 2]), z3 = __uint_as_float(rr[j + 3]);
-            const uint32_t m01 = nz_halves(pack2_relu<F16>(z0, z1), one);
-            const uint32_t m23 = nz_halves(pack2_relu<F16>(z2, z3), one);
+            // e6 masks from the sign bytes of the fp32 z6 (as K2b): 1[z >= +0]
+            const uint32_t m01 = ~prmt(rr[j], rr[j + 1], 0xffbbu);
+            const uint32_t m23 = ~prmt(rr[j + 2], rr[j + 3], 0xffbbu);
             pkh[j >> 1] = wh.x & m01;
             pkh[(j >> 1) + 1] = wh.y & m23;
             pkl[j >> 1] = wl.x & m01;

@@ -103,7 +103,6 @@ DEVI uint32_t mask_group_f(uint32_t pk01, uint32_t pk23, int k, uint32_t one) {
   const uint32_t x = prmt(add7fff(pk01, one), add7fff(pk23, one), 0x7531u);
   return (x >> k) & (0x80808080u >> k);
 }
-DEVI uint32_t nz_halves(uint32_t pk, uint32_t one) { return prmt(add7fff(pk, one), 0u, 0xbb99u); }
 
 __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W, const QueryArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -378,8 +377,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_tc_wide(const WeightsBF16 W
               const int u = U0 + cb + j;
               const float z0 = __uint_as_float(rr[j]), z1 = __uint_as_float(rr[j + 1]);
               const float z2 = __uint_as_float(rr[j + 2]), z3 = __uint_as_float(rr[j + 3]);
-              pk[j >> 1] = W.w7h_p[u / 2] & nz_halves(pack_f16_relu(z0, z1), one);
-              pk[(j >> 1) + 1] = W.w7h_p[u / 2 + 1] & nz_halves(pack_f16_relu(z2, z3), one);
+              // e6 masks from the sign bytes of the fp32 z6 (as K2b): 1[z >= +0]
+              pk[j >> 1] = W.w7h_p[u / 2] & ~prmt(rr[j], rr[j + 1], 0xffbbu);
+              pk[(j >> 1) + 1] = W.w7h_p[u / 2 + 1] & ~prmt(rr[j + 2], rr[j + 3], 0xffbbu);
               fa[0] = fmaf(W.w7half_p[u], z0 + fabsf(z0), fa[0]);
               fa[1] = fmaf(W.w7half_p[u + 1], z1 + fabsf(z1), fa[1]);
               fa[2] = fmaf(W.w7half_p[u + 2], z2 + fabsf(z2), fa[2]);
