@@ -49,7 +49,7 @@ __device__ __forceinline__ void gemm_tile(const float *__restrict__ X, const flo
   constexpr int UPT = H / 16;
   const float *xr = X + tp * 8;
   const float *wr = Wp + tu * UPT;
-#pragma unroll 4
+#pragma unroll 16  // (16 k steps in flight: 220M -> 173M SM cycles at C3 vs unroll 4; results identical)
   for (int k = 0; k < H; ++k) {
     const float4 x0 = *reinterpret_cast<const float4 *>(xr + k * LD);
     const float4 x1 = *reinterpret_cast<const float4 *>(xr + k * LD + 4);
