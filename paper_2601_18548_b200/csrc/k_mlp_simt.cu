@@ -73,10 +73,12 @@ __device__ __forceinline__ void store_tile(float *__restrict__ Y, int tp, int tu
   }
 }
 
-// H = 256: one activation buffer updated in place (two would exceed shared memory) plus a
-// separate [128][9] gradient staging area; H <= 128: two buffers in ping-pong
+// H >= 128: one activation buffer updated in place plus a separate [128][9] gradient staging
+// area (H = 256: two buffers would exceed shared memory; H = 128: half the shared memory, so
+// two CTAs of 256 threads share an SM at 128 registers -- 173M -> 147M SM cycles at C3 despite
+// a few spills); H = 32: two buffers in ping-pong
 template <int H>
-constexpr bool in_place() { return H > 128; }
+constexpr bool in_place() { return H >= 128; }
 template <int H>
 constexpr int smem_bytes_simt() {
   return ((in_place<H>() ? 1 : 2) * H * LD + (in_place<H>() ? kTile * kNdof : 0) + 4 * kTile + H + 16 + kTile + 2 * 4 +
@@ -94,7 +96,7 @@ __device__ __forceinline__ float softplus_f32(float z, float &dsig) {
 }
 
 template <int H, int ACT>
-__global__ void __launch_bounds__(256, 1) k_mlp_simt(const WeightsF32 W, const QueryArgs a) {
+__global__ void __launch_bounds__(256, (H == 128 ? 2 : 1)) k_mlp_simt(const WeightsF32 W, const QueryArgs a) {
   constexpr int UPT = H / 16;
   static_assert(ACT == 1 || ACT == 2, "activation");
   constexpr int MW = (8 * UPT + 31) / 32;
