@@ -166,22 +166,21 @@ DEVI void issue_phase(int p, uint32_t tb, uint32_t sw, uint32_t sw1t, uint32_t s
       b[1] = sdesc_sw128(wb + 16384u, 16384, 1024);
     }
     const uint32_t id = fwd ? kIdescFwd : kIdescBwd;
-    const uint32_t kstep = fwd ? 2u : 128u;  // B descriptor step per K step inside a 64-K chunk
+    // (each group of four K steps from one asm block: the lean issue of K2b, tc_ptx.h)
+    auto k4 = [&](uint32_t d, uint32_t a, uint64_t bd, uint32_t acc) {
+      if (fwd) umma4_sw128_elect(d, a, bd, id, acc);
+      else umma4_mn_elect(d, a, bd, id, acc);
+    };
+    // K steps 4..7: K-major B in the second 64-K chunk (+ 16 KB), MN-major B + 4 x 2 KB
+    const uint64_t k47 = fwd ? 1024u : 512u;
     wait_half(0);
-    // half 0, K steps 0..3 (units 0..63 of A)
-#pragma unroll
-    for (int k = 0; k < 4; ++k) mma_ts_elect(tb, av + 8u * k, b[0] + (uint64_t)(kstep * k), id, k > 0);
+    k4(tb, av, b[0], 0u);  // half 0, K steps 0..3 (units 0..63 of A)
     wait_half(1);
-    // half 0, K steps 4..7 (K-major: the second 64-K chunk at + 16 KB; MN-major: + k 2 KB)
-#pragma unroll
-    for (int k = 4; k < 8; ++k)
-      mma_ts_elect(tb, av + 8u * k, b[0] + (uint64_t)(fwd ? 1024u + 2u * (k - 4) : 128u * k), id, 1u);
+    k4(tb, av + 32u, b[0] + k47, 1u);
     if (fwd) mma_ts_elect(tb, tb + kColOnes, sdesc_nosw(sbx + (uint32_t)(p - 1) * kBextBytes, 2048, 128), id, 1u);
     commit_elect(&done[0]);
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      mma_ts_elect(tb + 64u, av + 8u * k, b[1] + (uint64_t)(fwd ? (k >> 2) * 1024u + 2u * (k & 3) : 128u * k), id,
-                   k > 0);
+    k4(tb + 64u, av, b[1], 0u);
+    k4(tb + 64u, av + 32u, b[1] + k47, 1u);
     if (fwd)
       mma_ts_elect(tb + 64u, tb + kColOnes, sdesc_nosw(sbx + (uint32_t)(p - 1) * kBextBytes + 1024u, 2048, 128), id,
                    1u);
@@ -189,10 +188,8 @@ DEVI void issue_phase(int p, uint32_t tb, uint32_t sw, uint32_t sw1t, uint32_t s
   } else {  // g0 = e1 W1 (N = 16 rows of W1^T): needs all of e1
     wait_half(0);
     wait_half(1);
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      mma_ts_elect(tb, tb + kColH + 8u * k, sdesc_sw128(sw1t + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024), kIdescFin,
-                   k > 0);
+    umma4_sw128_elect(tb, tb + kColH, sdesc_sw128(sw1t, 16, 1024), kIdescFin, 0u);
+    umma4_sw128_elect(tb, tb + kColH + 32u, sdesc_sw128(sw1t + 2048, 16, 1024), kIdescFin, 1u);
     commit_elect(&done[0]);
     commit_elect(&done[1]);
   }

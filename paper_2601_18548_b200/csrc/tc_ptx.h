@@ -209,6 +209,28 @@ DEVI void umma4_sw128_elect(uint32_t d, uint32_t a, uint64_t b0, uint32_t idesc,
       "r"(a), "l"(b0), "r"(idesc), "r"(acc)
       : "memory");
 }
+// The same four UMMAs for an MN-major SWIZZLE_128B B operand (B descriptor + 128 = 2048 B per
+// K step)
+DEVI void umma4_mn_elect(uint32_t d, uint32_t a, uint64_t b0, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred e, p0, pt;\n\t"
+      ".reg .b32 ra;\n\t"
+      ".reg .b64 rb;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p0, %4, 0;\n\t"
+      "setp.eq.b32 pt, %4, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p0;\n\t"
+      "add.u32 ra, %1, 8;\n\tadd.u64 rb, %2, 128;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ra], rb, %3, pt;\n\t"
+      "add.u32 ra, %1, 16;\n\tadd.u64 rb, %2, 256;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ra], rb, %3, pt;\n\t"
+      "add.u32 ra, %1, 24;\n\tadd.u64 rb, %2, 384;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ra], rb, %3, pt;\n\t"
+      "}" ::"r"(d),
+      "r"(a), "l"(b0), "r"(idesc), "r"(acc)
+      : "memory");
+}
 // Eight UMMAs over K = 128 (8 K steps) from ONE asm block, A at a + 8 k (contiguous TMEM
 // columns), B a SWIZZLE_128B operand: K-major (two 64-column chunks of 16 KB: + (k / 4) 16384
 // + (k % 4) 32 bytes) or MN-major (+ k 2048 bytes); the first accumulating iff acc != 0.
