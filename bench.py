@@ -472,13 +472,15 @@ def main():
                 lat[name] = {"p50_ms": float(np.percentile(ms, 50)), "p99_ms": float(np.percentile(ms, 99))}
 
     # NEXT-4 variants on the same workload (single GPU, default run only): device time per
-    # detect over the whole scene with the softplus network (K2s) and the H = 256 network
-    # (K2w), each in a context of its own; tensor roofline against the same peak
+    # detect over the whole scene with the softplus network (K2s), the H = 256 network (K2w),
+    # the split paths (K2c) and the fp32 SIMT parity path (K2f), each in a context of its own;
+    # tensor roofline against the same peak (K2f: the FP32-ALU peak)
     variants = None
     if world == 1 and a.variants and a.activation == "relu" and not hidden and prec == "fp16":
         variants = {}
         for name, act_v, h_v, prec_v in (("softplus", 2, None, FP16), ("hidden256", 1, 256, FP16),
-                                         ("fp16x3", 1, None, FP16X3), ("bf16x3", 1, None, BF16X3)):
+                                         ("fp16x3", 1, None, FP16X3), ("bf16x3", 1, None, BF16X3),
+                                         ("fp32", 1, None, FP32)):
             cfg_v = dataclasses.replace(cfg, H=h_v) if h_v else cfg
             ctx_v = Context(local, precision=prec_v, scene_capacity=cfg.M + slack, max_waypoints=n_wp,
                             max_active=max_active)
@@ -502,18 +504,22 @@ def main():
             ctx_v.profile_enable(False)
             ms_v = sum(e0.elapsed_time(e1) for e0, e1 in evs) / len(evs)
             pairs_v = ctx_v.scene_info()["n_live"] * n_wp
-            ach = FLOPS_PAIR_TENSOR[cfg_v.H] * pairs_v / (k_ms / k_n / 1e3) / 1e12
-            pk = float(peaks.get("bf16_tflops"))
+            simt = prec_v == FP32  # (the fp32 SIMT parity path K2f: FP32-ALU roofline)
+            ach = (FLOPS_PAIR_TOTAL if simt else FLOPS_PAIR_TENSOR)[cfg_v.H] * pairs_v / (k_ms / k_n / 1e3) / 1e12
+            pk = (148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12 if simt
+                  else float(peaks.get("bf16_tflops")))
             split = prec_v in (FP16X3, BF16X3)
-            variants[name] = {"kernel": "k_mlp_tc_sp" if act_v == 2 else "k_mlp_tc3" if split
+            variants[name] = {"kernel": "k_mlp_simt" if simt else "k_mlp_tc_sp" if act_v == 2 else "k_mlp_tc3" if split
                               else "k_mlp_tc_wide", "hidden": cfg_v.H,
                               "activation": "softplus" if act_v == 2 else "relu", "ms_per_step": ms_v,
                               "precision": ("fp16x3 (fp32-accurate split, R25)" if prec_v == FP16X3 else
-                                            "bf16x3 (3-term split bf16, R29)" if prec_v == BF16X3 else "fp16"),
+                                            "bf16x3 (3-term split bf16, R29)" if prec_v == BF16X3 else
+                                            "fp32 (SIMT parity path)" if simt else "fp16"),
                               "value": pairs_v / (ms_v / 1e3), "unit": "queries/s", "tau": tau_v,
                               "active_per_step": int(ov["count"].item()),
-                              "roofline": {"bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
-                                           "frac": ach / pk, "flops_per_pair": FLOPS_PAIR_TENSOR[cfg_v.H]}}
+                              "roofline": {"bound": "alu" if simt else "tensor", "achieved": ach, "peak": pk,
+                                           "unit": "TFLOP/s", "frac": ach / pk,
+                                           "flops_per_pair": (FLOPS_PAIR_TOTAL if simt else FLOPS_PAIR_TENSOR)[cfg_v.H]}}
             if split:
                 variants[name]["roofline"].update(executed_flops_per_pair=3 * FLOPS_PAIR_TENSOR[cfg_v.H],
                                                   executed_frac=3 * ach / pk)
