@@ -275,8 +275,9 @@ int gcdf_detect_active_set_host(gcdf_ctx *ctx, const float *q_host, int32_t B, i
    >= local_bound and a multiple of 4 (16-B aligned rows); a value of +INF marks a dead
    slot (the query writes +INF there) and is never active nor the minimum.  Capacity: the
    records are written straight to out_dev in canonical order (no staging area), the first
-   min(count, out_capacity) of them; count_dev always holds the full count, and
-   count_host_or_null gets CAPACITY when count > out_capacity.  The scratch it uses lives in
+   min(count, out_capacity) of them; count_dev always holds the full count; with
+   count_host_or_null given, the call synchronizes and returns CAPACITY when count >
+   out_capacity.  The scratch it uses lives in
    the bound workspace (sized by max_waypoints and the scene capacity). */
 int gcdf_compact_dense(gcdf_ctx *ctx, const float *values_dev, const float *grads_dev, int32_t n_wp,
                        int64_t stride, float delta, float tau, gcdf_active_t *out_dev, int64_t out_capacity,
